@@ -1,0 +1,256 @@
+/* sforge_b200.h -- C ABI of the B200-native stencil hot path.
+ *
+ * Drop-in boundary for the reference's (stencilforge, /root/reference/proj)
+ * plugin/operator API on the data-parallel hot path: the staggered-grid
+ * incompressible step (UPDATE_VELOCITY, PRESSURE_SWEEP, DIVERGENCE), the
+ * ghost refresh between grid components and the max reductions.
+ *
+ * Two levels, both plain C (pointers, sizes, status codes; no torch types):
+ *
+ *  1. sf_sim_*   -- one simulation owning its fields on one CUDA device.  Each
+ *                   entry point replaces one public member of
+ *                   sforge::cfd::simulation / exec::executor (cited per call).
+ *                   A simulation may hold several grid components ("workers")
+ *                   of one decomposition on the same device; their ghost
+ *                   exchange runs as device copies.
+ *  2. sf_launch_* -- single-kernel launches on caller-owned device memory for
+ *                   an external executor: one call per (kernel, region box
+ *                   list, stream), exactly the granularity of
+ *                   exec::executor::run_region_worker (executor.hpp:759-767).
+ *
+ * Error behaviour: every int-returning call returns SF_OK (0) or an sf_status
+ * code; sf_last_error() gives the message.  Messages reuse the reference's
+ * texts where the reference throws (e.g. "non-finite vx after the velocity
+ * update at step N, t = ..." from cfd.hpp:278-281, the grid_error texts of
+ * grid.hpp:94-137, the exec_error texts of executor.hpp:500-757).
+ *
+ * Numerics: fp64, IEEE round-to-nearest, no FMA contraction, the reference's
+ * association order everywhere: results are bitwise identical to the
+ * reference CPU implementation.
+ */
+#ifndef SFORGE_B200_H
+#define SFORGE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SF_ABI_VERSION 1
+
+enum sf_status {
+  SF_OK = 0,
+  SF_ERR_CONFIG = 1, /* cfd_error from validate() (cfd.hpp:36-66) */
+  SF_ERR_GRID = 2,   /* grid_error (grid.hpp:18-21) */
+  SF_ERR_EXEC = 3,   /* exec_error (executor.hpp:32-35) */
+  SF_ERR_CFD = 4,    /* cfd_error at run time, e.g. the NaN guard (cfd.hpp:278-281) */
+  SF_ERR_CUDA = 5,   /* CUDA runtime failure (no reference analogue) */
+  SF_ERR_ARG = 6     /* bad argument to the C ABI itself */
+};
+
+enum sf_field_id { SF_VX = 0, SF_VY = 1, SF_VZ = 2, SF_P = 3, SF_DIVU = 4, SF_NFIELDS = 5 };
+enum sf_region { SF_REGION_ALL = 0, SF_REGION_INTERIOR = 1, SF_REGION_BOUNDARY = 2 }; /* executor.hpp:40 */
+enum sf_reduce_op { SF_MAX_ABS = 0, SF_SUM = 1, SF_SUM_SQ = 2, SF_MAX_ABS_DIFF = 3 }; /* reductions.hpp:17-22 */
+enum sf_bc_kind { SF_BC_UNSET = 0, SF_BC_WALL = 1, SF_BC_SYMMETRY = 2, SF_BC_OUTFLOW = 3 }; /* exchange.hpp:18-26 */
+enum sf_bc_scope { SF_SCOPE_ALL = 0, SF_SCOPE_GHOSTS_ONLY = 1, SF_SCOPE_OWNED_ONLY = 2 };    /* exchange.hpp:49 */
+
+/* Returns the library's SF_ABI_VERSION. */
+int sf_abi_version(void);
+/* Message of the last failing call on this thread (never NULL). */
+const char* sf_last_error(void);
+/* Number of CUDA devices visible (0 without a GPU); never fails. */
+int sf_device_count(void);
+
+/* grid::decompose (grid.hpp:92-163) without a device: proc_grid[3] and, per
+ * worker w, lo[3w..3w+2] / hi[3w..3w+2] (arrays of 3*workers).  Same process
+ * grid choice, balanced split and error texts as the reference. */
+int sf_decompose(const int64_t extents[3], const double spacing[3], int workers, int ghost,
+                 const int periodic[3], int proc_grid[3], int64_t* lo, int64_t* hi);
+/* decomposition::neighbor (grid.hpp:69-81): worker across (axis, side) or -1. */
+int sf_decomp_neighbor(const int proc_grid[3], const int periodic[3], int w, int axis, int side);
+
+/* ------------------------------------------------------------------------
+ * Level 1: simulation (replaces sforge::cfd::simulation, cfd.hpp:173-766)
+ * ---------------------------------------------------------------------- */
+
+/* cfd::solver_config (cfd.hpp:43-67) */
+typedef struct sf_solver_config {
+  int64_t extents[3];
+  double spacing[3];
+  double origin[3];
+  int periodic[3];
+  double reynolds, sigma, tolerance, omega;
+  int max_sweeps;
+  int symmetry_z;
+  int output_cadence;
+} sf_solver_config;
+
+/* cfd::fluid_params (cfd.hpp:29-41) */
+typedef struct sf_fluid_params {
+  double viscosity, density;
+  double body_force[3];
+  double lid_speed, blend;
+} sf_fluid_params;
+
+/* Constructor arguments of cfd::simulation (cfd.hpp:175-178) plus device
+ * placement.  workers = grid components of grid::decompose() on `device`. */
+typedef struct sf_sim_options {
+  int workers;
+  int mode;    /* 0 plain, 1 overlap (exec::run_mode, executor.hpp:42) */
+  int tile[3]; /* tile override, 0,0,0 = descriptor default (cfd.hpp:520) */
+  int ghost;
+  int form;    /* 0 rows, 1 points (cfd.hpp:169): one device form serves both */
+  int device;
+  int fused;   /* 1 = fused sweep+divergence half-sweep (default), 0 = unfused */
+} sf_sim_options;
+
+/* cfd::step_stats (cfd.hpp:86-90) */
+typedef struct sf_step_stats {
+  double dt;
+  int sweeps;
+  double residual;
+} sf_step_stats;
+
+typedef struct sf_sim sf_sim;
+
+void sf_sim_options_default(sf_sim_options* o);
+/* simulation::simulation (cfd.hpp:175-222).  Validates like cfd.hpp:36-66 and
+ * decomposes like grid::decompose (grid.hpp:92-163). */
+int sf_sim_create(const sf_solver_config* cfg, const sf_fluid_params* par,
+                  const sf_sim_options* opt, sf_sim** out);
+void sf_sim_destroy(sf_sim* s);
+
+int sf_sim_init_cavity(sf_sim* s);                                   /* cfd.hpp:229-232 */
+int sf_sim_init_uniform(sf_sim* s, double cx, double cy, double cz); /* cfd.hpp:234-241 */
+int sf_sim_init_taylor_green(sf_sim* s);                             /* cfd.hpp:246-257 */
+
+int sf_sim_compute_dt(sf_sim* s, double* dt);                        /* cfd.hpp:264-273 */
+int sf_sim_provisional(sf_sim* s, double dt);                        /* cfd.hpp:275-282 */
+int sf_sim_pressure_iteration(sf_sim* s, double dt, int* sweeps, double* residual); /* cfd.hpp:289-305 */
+int sf_sim_step(sf_sim* s, sf_step_stats* out);                      /* cfd.hpp:307-316 */
+int sf_sim_advance(sf_sim* s, int n, sf_step_stats* last);           /* cfd.hpp:318-321 */
+
+double sf_sim_time(const sf_sim* s);          /* cfd.hpp:461 */
+long sf_sim_step_count(const sf_sim* s);      /* cfd.hpp:462 */
+int sf_sim_pending_color(sf_sim* s);          /* cfd.hpp:470 */
+
+int sf_sim_max_divergence(sf_sim* s, double* out);  /* cfd.hpp:342-345 */
+int sf_sim_steady_delta(sf_sim* s, double* out);    /* cfd.hpp:350-355 */
+int sf_sim_kinetic_energy(sf_sim* s, double* out);  /* cfd.hpp:357-363 */
+
+/* grid::scatter / grid::gather on one field (io.hpp:25-65): global x-fastest
+ * float64 arrays of extents[0]*extents[1]*extents[2] values in HOST memory. */
+int sf_sim_scatter(sf_sim* s, const char* field, const double* host, int64_t n);
+int sf_sim_gather(sf_sim* s, const char* field, double* host, int64_t n);
+/* Same, from/to a DEVICE buffer on the simulation's device (no host trip). */
+int sf_sim_scatter_device(sf_sim* s, const char* field, const double* dev, int64_t n);
+int sf_sim_gather_device(sf_sim* s, const char* field, double* dev, int64_t n);
+/* cli::field_checksum (bench.hpp:24-39): FNV-1a of the gathered vx,vy,vz,p. */
+int sf_sim_checksum(sf_sim* s, uint64_t* out);
+/* One worker's padded front array, ghosts included, x fastest with extents
+ * dims+2g (the reference layout local_block::offset, field.hpp:39-44). */
+int sf_sim_local_front(sf_sim* s, const char* field, int worker, double* host,
+                       int64_t host_elems, int64_t dims[3], int64_t lo[3]);
+
+/* exec::executor operations on this simulation's fields (executor.hpp:500-527).
+ * fields: array of n field names.  params: n_params (name, value) pairs. */
+int sf_sim_refresh(sf_sim* s, const char* const* fields, int n);  /* :520-523 */
+int sf_sim_exchange(sf_sim* s, const char* const* fields, int n); /* :511-514 */
+int sf_sim_run_kernel(sf_sim* s, const char* name, const char* const* param_names,
+                      const double* param_values, int n_params, int region); /* :500-509 */
+int sf_sim_reduce(sf_sim* s, const char* field, int op, double* out);        /* :525-527 */
+int sf_sim_invalidate_ghosts(sf_sim* s, const char* field);                  /* :612 */
+int sf_sim_invalidate_all_ghosts(sf_sim* s);                                 /* :613 */
+int sf_sim_ghosts_valid(sf_sim* s, const char* field);                       /* :610 */
+
+/* Device plumbing for benches and transports. */
+int sf_sim_synchronize(sf_sim* s);
+void* sf_sim_stream(sf_sim* s);            /* the cudaStream_t all work is ordered on */
+/* Kernel launches issued by this simulation since creation (or the last reset). */
+int64_t sf_sim_launch_count(sf_sim* s, int reset);
+/* Per-kernel CUDA-event timing of the fused half-sweep: when enabled, the
+ * driver records events around every half-sweep launch; read back the summed
+ * milliseconds and launch count. */
+int sf_sim_set_kernel_timing(sf_sim* s, int enable);
+int sf_sim_kernel_timing(sf_sim* s, const char* kernel, double* total_ms, int64_t* launches);
+
+/* ------------------------------------------------------------------------
+ * Level 2: single-kernel launches for an external executor
+ * ---------------------------------------------------------------------- */
+
+/* Device geometry of one local block (local_block, field.hpp:31-52) with an
+ * explicit, aligned pitch:  offset(i,j,k) = base + (k*sy + j)*sx + i  for
+ * local i,j,k in [-ghost, dims+ghost).  Rows are 128-byte aligned at i = 0. */
+typedef struct sf_layout {
+  int64_t dims[3];
+  int64_t lo[3];
+  int ghost;
+  int64_t sx, sy, sz;
+  int64_t base;
+} sf_layout;
+
+/* executor.hpp:73-79, local owned coordinates, hi exclusive */
+typedef struct sf_box {
+  int64_t lo[3];
+  int64_t hi[3];
+} sf_box;
+
+/* One physical face condition (exchange.hpp:18-26) */
+typedef struct sf_face_bc {
+  int kind;
+  double velocity[3];
+} sf_face_bc;
+
+/* step_constants (cfd.hpp:473-487), computed on the host exactly as
+ * cfd.hpp:192-217 does; global extents and periodic bits included. */
+typedef struct sf_cfd_consts {
+  double dt, nu, alpha, fx, fy, fz, ix, iy, iz, ix2, iy2, iz2;
+  double bscale[2][2][2];
+  int64_t nxm1, nym1, nzm1;
+  int px, py, pz;
+} sf_cfd_consts;
+
+int sf_make_layout(const int64_t dims[3], const int64_t lo[3], int ghost, sf_layout* out);
+int64_t sf_layout_elems(const sf_layout* l);
+int sf_make_cfd_consts(const sf_solver_config* cfg, const sf_fluid_params* par, sf_cfd_consts* out);
+
+/* UPDATE_VELOCITY (cfd.hpp:524-589) over the boxes: reads front vx,vy,vz,p
+ * (ghosts valid), writes back vx,vy,vz.  The caller swaps (executor.hpp:772-773). */
+int sf_launch_update_velocity(const sf_layout* l, const double* vx, const double* vy,
+                              const double* vz, const double* p, double* vx_out,
+                              double* vy_out, double* vz_out, const sf_cfd_consts* c,
+                              const sf_box* boxes, int nbox, void* stream);
+/* DIVERGENCE (cfd.hpp:595-618) */
+int sf_launch_divergence(const sf_layout* l, const double* vx, const double* vy,
+                         const double* vz, double* divu, const sf_cfd_consts* c,
+                         const sf_box* boxes, int nbox, void* stream);
+/* PRESSURE_SWEEP (cfd.hpp:630-720), in place on p,vx,vy,vz */
+int sf_launch_pressure_sweep(const sf_layout* l, const double* divu, double* p, double* vx,
+                             double* vy, double* vz, const sf_cfd_consts* c, double beta,
+                             int color, const sf_box* boxes, int nbox, void* stream);
+/* bc_face (exchange.hpp:231-480) of one field on one face of one block.
+ * stagger: -1 none, 0/1/2 = x/y/z.  Tangential ranges follow the axis phase. */
+int sf_launch_bc_face(const sf_layout* l, double* front, int stagger, int axis, int side,
+                      const sf_face_bc* bc, int scope, void* stream);
+/* Box copy between two blocks' arrays (one pack+unpack of exchange.hpp:165-224):
+ * copies src box (src-local coords) to dst box starting at dst_lo. */
+int sf_launch_copy_box(const sf_layout* src_l, const double* src, const sf_layout* dst_l,
+                       double* dst, const int64_t src_lo[3], const int64_t dims[3],
+                       const int64_t dst_lo[3], void* stream);
+/* Pack / unpack a box to / from a contiguous x-fastest buffer (for NCCL /
+ * peer transports between processes). */
+int sf_launch_pack_box(const sf_layout* l, const double* src, const int64_t lo[3],
+                       const int64_t dims[3], double* buf, void* stream);
+int sf_launch_unpack_box(const sf_layout* l, double* dst, const int64_t lo[3],
+                         const int64_t dims[3], const double* buf, void* stream);
+/* max_abs / max_abs_diff over owned cells into *dev_out (a device double,
+ * NaN-sticky, reductions.hpp:39-71); the caller zeroes *dev_out first. */
+int sf_launch_reduce_max(const sf_layout* l, const double* front, const double* back, int op,
+                         double* dev_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFORGE_B200_H */

@@ -1,0 +1,1641 @@
+// sf_driver.cu -- C++ host driver + C ABI (include/sforge_b200.h).
+//
+// Mirrors the reference's host side on the hot path:
+//   grid::decompose / decomposition        grid.hpp:44-163
+//   grid::boundary_spec / face_bc          exchange.hpp:18-42
+//   exchanger::refresh (3 axis phases)     exchange.hpp:98-119, 165-480
+//   exec::executor run_kernel / refresh /  executor.hpp:477-862
+//     reduce / ghost validity
+//   cfd::simulation step loop              cfd.hpp:173-766
+// One simulation owns every grid component ("worker") of its decomposition on
+// one CUDA device; all work is ordered on one stream.  The pressure loop is
+// device-driven: half-sweeps are predicated on a device flag and enqueued in
+// batches, and the host only polls a host-mapped word.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sf_kernels.cuh"
+
+namespace sfb {
+
+using i64 = long long;
+
+struct error : std::runtime_error {
+  int code;
+  error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define SF_CK(x)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::sfb::error(SF_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+static thread_local std::string g_last_error;
+
+// ---------------------------------------------------------------------------
+// decomposition (grid.hpp:44-163), same choices and error texts
+// ---------------------------------------------------------------------------
+struct decomposition {
+  i64 ext[3]{};
+  int workers = 1, ghost = 0;
+  int pg[3]{1, 1, 1};
+  bool periodic[3]{false, false, false};
+  std::vector<std::array<i64, 3>> lo, hi;
+
+  std::array<int, 3> coords_of(int w) const {
+    const int pz = pg[2], py = pg[1];
+    return {w / (py * pz), (w / pz) % py, w % pz};
+  }
+  int id_of(const std::array<int, 3>& c) const { return (c[0] * pg[1] + c[1]) * pg[2] + c[2]; }
+  int neighbor(int w, int axis, int side) const {
+    auto c = coords_of(w);
+    int& ca = c[axis];
+    ca += side == 0 ? -1 : 1;
+    const int p = pg[axis];
+    if (ca < 0 || ca >= p) {
+      if (!periodic[axis]) return -1;
+      ca = (ca + p) % p;
+    }
+    return id_of(c);
+  }
+  std::array<i64, 3> dims(int w) const {
+    return {hi[w][0] - lo[w][0], hi[w][1] - lo[w][1], hi[w][2] - lo[w][2]};
+  }
+};
+
+static std::vector<i64> split_axis(i64 n, int p) {
+  std::vector<i64> s(p);
+  const i64 base = n / p, rem = n % p;
+  for (int i = 0; i < p; ++i) s[i] = base + (i < rem ? 1 : 0);
+  return s;
+}
+
+decomposition decompose(const i64 ext[3], const double spacing[3], int workers, int ghost,
+                        const bool periodic[3]) {
+  if (workers < 1) throw error(SF_ERR_GRID, "worker count must be >= 1");
+  if (ghost < 0) throw error(SF_ERR_GRID, "ghost width must be >= 0");
+  for (int a = 0; a < 3; ++a) {
+    if (ext[a] < 1) throw error(SF_ERR_GRID, "domain extents must be >= 1");
+    if (!(spacing[a] > 0.0)) throw error(SF_ERR_GRID, "grid spacing must be positive");
+  }
+  auto feasible = [&](int p, i64 n) { return p <= n && n / p > ghost; };
+  bool found = false;
+  int best[3] = {1, 1, 1};
+  i64 best_area = 0;
+  for (int px = 1; px <= workers; ++px) {
+    if (workers % px) continue;
+    const int rest = workers / px;
+    for (int py = 1; py <= rest; ++py) {
+      if (rest % py) continue;
+      const int pz = rest / py;
+      if (!feasible(px, ext[0]) || !feasible(py, ext[1]) || !feasible(pz, ext[2])) continue;
+      const i64 area = (i64)(px - 1) * ext[1] * ext[2] + (i64)(py - 1) * ext[0] * ext[2] +
+                       (i64)(pz - 1) * ext[0] * ext[1];
+      const bool better = !found || area < best_area ||
+                          (area == best_area && (px > best[0] || (px == best[0] && py > best[1])));
+      if (better) {
+        found = true;
+        best[0] = px;
+        best[1] = py;
+        best[2] = pz;
+        best_area = area;
+      }
+    }
+  }
+  if (!found)
+    throw error(SF_ERR_GRID, "no feasible decomposition: " + std::to_string(workers) +
+                                 " workers on " + std::to_string(ext[0]) + "x" +
+                                 std::to_string(ext[1]) + "x" + std::to_string(ext[2]) +
+                                 " cells with ghost width " + std::to_string(ghost) +
+                                 " (blocks must exceed the ghost width)");
+  decomposition d;
+  for (int a = 0; a < 3; ++a) {
+    d.ext[a] = ext[a];
+    d.pg[a] = best[a];
+    d.periodic[a] = periodic[a];
+  }
+  d.workers = workers;
+  d.ghost = ghost;
+  std::array<std::vector<i64>, 3> sizes;
+  for (int a = 0; a < 3; ++a) sizes[a] = split_axis(ext[a], best[a]);
+  d.lo.resize(workers);
+  d.hi.resize(workers);
+  for (int w = 0; w < workers; ++w) {
+    const auto c = d.coords_of(w);
+    for (int a = 0; a < 3; ++a) {
+      i64 l = 0;
+      for (int i = 0; i < c[a]; ++i) l += sizes[a][i];
+      d.lo[w][a] = l;
+      d.hi[w][a] = l + sizes[a][c[a]];
+    }
+  }
+  return d;
+}
+
+// executor.hpp:81-109
+static std::vector<std::array<i64, 6>> region_boxes(const std::array<i64, 3>& dims,
+                                                    const std::array<int, 6>& halo, int reg) {
+  using box = std::array<i64, 6>;  // lo0 lo1 lo2 hi0 hi1 hi2
+  const box all = {0, 0, 0, dims[0], dims[1], dims[2]};
+  if (reg == SF_REGION_ALL) return {all};
+  i64 il[3], ih[3];
+  bool have = true;
+  for (int a = 0; a < 3; ++a) {
+    il[a] = std::min<i64>(halo[2 * a], dims[a]);
+    ih[a] = std::max<i64>(il[a], dims[a] - halo[2 * a + 1]);
+    if (il[a] >= ih[a]) have = false;
+  }
+  if (reg == SF_REGION_INTERIOR) {
+    if (!have) return {};
+    return {box{il[0], il[1], il[2], ih[0], ih[1], ih[2]}};
+  }
+  if (!have) return {all};
+  std::vector<box> out = {
+      {0, 0, 0, dims[0], dims[1], il[2]},
+      {0, 0, ih[2], dims[0], dims[1], dims[2]},
+      {0, 0, il[2], dims[0], il[1], ih[2]},
+      {0, ih[1], il[2], dims[0], dims[1], ih[2]},
+      {0, il[1], il[2], il[0], ih[1], ih[2]},
+      {ih[0], il[1], il[2], dims[0], ih[1], ih[2]},
+  };
+  std::vector<box> kept;
+  for (auto& b : out)
+    if (!(b[3] <= b[0] || b[4] <= b[1] || b[5] <= b[2])) kept.push_back(b);
+  return kept;
+}
+
+// Padded layout with 128-byte aligned rows at local i = 0.
+static sf_layout make_layout(const i64 dims[3], const i64 lo[3], int g) {
+  sf_layout l{};
+  for (int a = 0; a < 3; ++a) {
+    l.dims[a] = dims[a];
+    l.lo[a] = lo[a];
+  }
+  l.ghost = g;
+  const i64 xo = ((i64)g + 15) / 16 * 16;
+  l.sx = (xo + dims[0] + g + 15) / 16 * 16;
+  l.sy = dims[1] + 2 * g;
+  l.sz = dims[2] + 2 * g;
+  l.base = ((i64)g * l.sy + g) * l.sx + xo;
+  return l;
+}
+
+// ---------------------------------------------------------------------------
+// the simulation
+// ---------------------------------------------------------------------------
+static const char* const kFieldNames[SF_NFIELDS] = {"vx", "vy", "vz", "p", "divu"};
+static const int kStagger[SF_NFIELDS] = {0, 1, 2, -1, -1};
+
+struct kernel_plan {  // codegen::execution_plan of the three CFD kernels (cfd.hpp:111-162)
+  std::string name;
+  std::array<int, 6> halo;
+  std::vector<std::string> bindings;
+  std::vector<bool> writable, to_back;
+  std::vector<std::string> params;
+};
+
+static const std::vector<kernel_plan>& cfd_plans() {
+  static const std::vector<kernel_plan> plans = {
+      {"UPDATE_VELOCITY", {1, 1, 1, 1, 1, 1}, {"vx", "vy", "vz", "p"},
+       {true, true, true, false}, {true, true, true, false}, {"density"}},
+      {"DIVERGENCE", {1, 0, 1, 0, 1, 0}, {"vx", "vy", "vz", "divu"},
+       {false, false, false, true}, {false, false, false, false}, {}},
+      {"PRESSURE_SWEEP", {0, 1, 0, 1, 0, 1}, {"divu", "p", "vx", "vy", "vz"},
+       {false, true, true, true, true}, {false, false, false, false, false}, {"beta", "color"}},
+  };
+  return plans;
+}
+
+class simulation {
+ public:
+  simulation(const sf_solver_config& cfg, const sf_fluid_params& par, const sf_sim_options& opt)
+      : cfg_(cfg), par_(par), opt_(opt) {
+    validate();
+    const bool per[3] = {cfg.periodic[0] != 0, cfg.periodic[1] != 0, cfg.periodic[2] != 0};
+    const i64 ext[3] = {cfg.extents[0], cfg.extents[1], cfg.extents[2]};
+    dec_ = decompose(ext, cfg.spacing, opt.workers, opt.ghost, per);
+    if (dec_.workers > kMaxBlocks)
+      throw error(SF_ERR_ARG, "at most " + std::to_string(kMaxBlocks) + " workers per device");
+    make_bc();
+    make_consts();
+    SF_CK(cudaSetDevice(opt.device));
+    SF_CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    allocate();
+    SF_CK(cudaEventCreateWithFlags(&ev_[0], cudaEventDisableTiming));
+    SF_CK(cudaEventCreateWithFlags(&ev_[1], cudaEventDisableTiming));
+    SF_CK(cudaEventCreate(&t0_));
+    SF_CK(cudaEventCreate(&t1_));
+    launch_ctl(dtab_, dctl_, dflag_, CTL_CLEAR_ACC, 0, 0, 0, 0, consts_, 0, st_);
+    launch_ctl(dtab_, dctl_, dflag_, CTL_RESET_CLOCK, 0, 0, 0, 0, consts_, 0, st_);
+    launches_ += 2;
+    sync();
+  }
+
+  ~simulation() {
+    cudaSetDevice(opt_.device);
+    cudaStreamSynchronize(st_);
+    for (void* p : dev_allocs_) cudaFree(p);
+    if (hflag_) cudaFreeHost(hflag_);
+    cudaEventDestroy(ev_[0]);
+    cudaEventDestroy(ev_[1]);
+    cudaEventDestroy(t0_);
+    cudaEventDestroy(t1_);
+    for (auto e : timers_) cudaEventDestroy(e);
+    cudaStreamDestroy(st_);
+  }
+
+  // ---- helpers ------------------------------------------------------------
+  void sync() { SF_CK(cudaStreamSynchronize(st_)); }
+  void check_launch() {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw error(SF_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  }
+
+  static int field_id(const std::string& name) {
+    for (int f = 0; f < SF_NFIELDS; ++f)
+      if (name == kFieldNames[f]) return f;
+    throw error(SF_ERR_GRID, "no field named '" + name + "'");
+  }
+
+  // ---- initial states (cfd.hpp:229-257) -------------------------------------
+  void reset_clock() {
+    time_ = 0.0;
+    steps_ = 0;
+    last_ = {0.0, 0, 0.0};
+    ctl(CTL_RESET_CLOCK);
+  }
+  void fill_const(int f, double v) {
+    download_table();
+    for (int b = 0; b < dec_.workers; ++b) {
+      const auto& L = lay_[b];
+      const i64 lo[3] = {0, 0, 0};
+      const i64 dims[3] = {L.dims[0], L.dims[1], L.dims[2]};
+      launch_fill_box(htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, lo, dims, v, st_);
+      ++launches_;
+    }
+    check_launch();
+    ghosts_ok_[kFieldNames[f]] = false;
+  }
+  void init_cavity() {
+    for (int f = 0; f < SF_NFIELDS; ++f) fill_const(f, 0.0);
+    reset_clock();
+  }
+  void init_uniform(double cx, double cy, double cz) {
+    fill_const(SF_VX, cx);
+    fill_const(SF_VY, cy);
+    fill_const(SF_VZ, cz);
+    fill_const(SF_P, 0.0);
+    fill_const(SF_DIVU, 0.0);
+    reset_clock();
+  }
+  void init_taylor_green() {
+    // host-side sampling with the C library's sin/cos, exactly as cfd.hpp:246-257
+    const double tau = 2.0 * 3.14159265358979323846;
+    const double dx = cfg_.spacing[0], dy = cfg_.spacing[1];
+    const i64 nx = cfg_.extents[0], ny = cfg_.extents[1], nz = cfg_.extents[2];
+    std::vector<double> u(nx * ny * nz), v(u.size()), q(u.size());
+    for (i64 k = 0; k < nz; ++k)
+      for (i64 j = 0; j < ny; ++j)
+        for (i64 i = 0; i < nx; ++i) {
+          const double xc = ((double)i + 0.5) * dx, yc = ((double)j + 0.5) * dy;
+          const double xf = xc + 0.5 * dx, yf = yc + 0.5 * dy;
+          const i64 o = (k * ny + j) * nx + i;
+          u[o] = std::sin(tau * xf) * std::cos(tau * yc);
+          v[o] = -std::cos(tau * xc) * std::sin(tau * yf);
+          q[o] = 0.25 * (std::cos(2.0 * tau * xc) + std::cos(2.0 * tau * yc));
+        }
+    scatter(SF_VX, u.data(), false);
+    scatter(SF_VY, v.data(), false);
+    fill_const(SF_VZ, 0.0);
+    scatter(SF_P, q.data(), false);
+    fill_const(SF_DIVU, 0.0);
+    reset_clock();
+  }
+
+  // ---- data movement (io.hpp:25-65) ----------------------------------------
+  i64 cells() const { return cfg_.extents[0] * cfg_.extents[1] * cfg_.extents[2]; }
+  double* staging() {
+    if (!staging_) staging_ = (double*)dalloc(sizeof(double) * (size_t)cells());
+    return staging_;
+  }
+  void gather_to_device(int f, double* dglobal) {
+    download_table();
+    const i64 N[3] = {cfg_.extents[0], cfg_.extents[1], cfg_.extents[2]};
+    for (int b = 0; b < dec_.workers; ++b) {
+      const auto& L = lay_[b];
+      const i64 n[3] = {L.dims[0], L.dims[1], L.dims[2]};
+      const i64 lo[3] = {L.lo[0], L.lo[1], L.lo[2]};
+      launch_gather_owned(htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, n, lo, N, dglobal, 0, st_);
+      ++launches_;
+    }
+    check_launch();
+  }
+  void scatter_from_device(int f, const double* dglobal) {
+    download_table();
+    const i64 N[3] = {cfg_.extents[0], cfg_.extents[1], cfg_.extents[2]};
+    for (int b = 0; b < dec_.workers; ++b) {
+      const auto& L = lay_[b];
+      const i64 n[3] = {L.dims[0], L.dims[1], L.dims[2]};
+      const i64 lo[3] = {L.lo[0], L.lo[1], L.lo[2]};
+      launch_gather_owned(htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, n, lo, N,
+                          const_cast<double*>(dglobal), 1, st_);
+      ++launches_;
+    }
+    check_launch();
+    ghosts_ok_[kFieldNames[f]] = false;
+  }
+  void gather(int f, double* host) {
+    double* sg = staging();
+    gather_to_device(f, sg);
+    SF_CK(cudaMemcpyAsync(host, sg, sizeof(double) * (size_t)cells(), cudaMemcpyDeviceToHost, st_));
+    sync();
+  }
+  void scatter(int f, const double* host, bool do_sync = true) {
+    double* sg = staging();
+    SF_CK(cudaMemcpyAsync(sg, host, sizeof(double) * (size_t)cells(), cudaMemcpyHostToDevice, st_));
+    scatter_from_device(f, sg);
+    if (do_sync) sync();
+  }
+  void local_front(int f, int w, double* host, i64 host_elems, i64 dims[3], i64 lo[3]) {
+    if (w < 0 || w >= dec_.workers) throw error(SF_ERR_ARG, "worker index out of range");
+    const auto& L = lay_[w];
+    const int g = L.ghost;
+    const i64 ld[3] = {L.dims[0] + 2 * g, L.dims[1] + 2 * g, L.dims[2] + 2 * g};
+    if (host_elems < ld[0] * ld[1] * ld[2]) throw error(SF_ERR_ARG, "host buffer too small");
+    for (int a = 0; a < 3; ++a) {
+      dims[a] = L.dims[a];
+      lo[a] = L.lo[a];
+    }
+    download_table();
+    double* sg = (double*)dalloc_tmp(sizeof(double) * (size_t)(ld[0] * ld[1] * ld[2]));
+    const i64 slo[3] = {-g, -g, -g};
+    const i64 zero[3] = {0, 0, 0};
+    launch_copy_box(htab_->ptr[w][f][FRONT], L.base, L.sx, L.sy, sg, 0, ld[0], ld[1], slo, ld, zero,
+                    st_);
+    ++launches_;
+    check_launch();
+    SF_CK(cudaMemcpyAsync(host, sg, sizeof(double) * (size_t)(ld[0] * ld[1] * ld[2]),
+                          cudaMemcpyDeviceToHost, st_));
+    sync();
+    SF_CK(cudaFree(sg));
+  }
+  uint64_t checksum() {  // bench.hpp:24-39
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](const void* data, size_t n) {
+      const unsigned char* p = static_cast<const unsigned char*>(data);
+      for (size_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 1099511628211ull;
+      }
+    };
+    std::vector<double> g((size_t)cells());
+    for (int f : {SF_VX, SF_VY, SF_VZ, SF_P}) {
+      mix(kFieldNames[f], std::strlen(kFieldNames[f]));
+      gather(f, g.data());
+      mix(g.data(), g.size() * sizeof(double));
+    }
+    return h;
+  }
+
+  // ---- executor operations (executor.hpp:500-527) ---------------------------
+  void refresh(const std::vector<int>& fields, bool predicated = false) {
+    if (fields.empty()) return;
+    validate_bc(fields);
+    unsigned mask = 0;
+    for (int f : fields) mask |= 1u << f;
+    for (int axis = 0; axis < 3; ++axis) {
+      const task_set& ts = tasks_for(mask, axis, SF_SCOPE_ALL, false);
+      if (ts.n == 0) continue;
+      launch_tasks(tview(), ts.d, ts.n, ts.max_count, predicated ? dctl_ : nullptr, st_);
+      ++launches_;
+    }
+    check_launch();
+    for (int f : fields) ghosts_ok_[kFieldNames[f]] = true;
+  }
+  void exchange_only(const std::vector<int>& fields) {
+    unsigned mask = 0;
+    for (int f : fields) mask |= 1u << f;
+    for (int axis = 0; axis < 3; ++axis) {
+      const task_set& ts = tasks_for(mask, axis, SF_SCOPE_ALL, true);
+      if (ts.n == 0) continue;
+      launch_tasks(tview(), ts.d, ts.n, ts.max_count, nullptr, st_);
+      ++launches_;
+    }
+    check_launch();
+    for (int f : fields) ghosts_ok_[kFieldNames[f]] = true;
+  }
+
+  void run_kernel(const std::string& name, const std::map<std::string, double>& params, int reg) {
+    const kernel_plan* kp = nullptr;
+    for (const auto& p : cfd_plans())
+      if (p.name == name) kp = &p;
+    if (!kp) throw error(SF_ERR_EXEC, "unknown kernel '" + name + "'");
+    std::vector<double> pv;
+    for (const auto& pn : kp->params) {
+      auto it = params.find(pn);
+      if (it == params.end())
+        throw error(SF_ERR_EXEC, "kernel '" + name + "': parameter '" + pn + "' not supplied");
+      pv.push_back(it->second);
+    }
+    if (reg < 0 || reg > 2) throw error(SF_ERR_ARG, "bad region");
+    const work_set& ws = items_for(reg, kp->halo, zc_plain_);
+    if (name == "UPDATE_VELOCITY") {
+      launch_update_velocity(tview(ws), ws.nctas, zc_plain_, consts_, dctl_, 0.0, st_);
+      ++launches_;
+    } else if (name == "DIVERGENCE") {
+      launch_divergence(tview(ws), ws.nctas, zc_plain_, consts_, dctl_, -1, 0, st_);
+      ++launches_;
+    } else {
+      // beta and colour come from the call, dt from the simulation (cfd.hpp:630-697)
+      const double bcd[3] = {pv[0], pv[1], 0.0};
+      launch_pressure_sweep(tview(ws), ws.nctas, zc_plain_, consts_, dctl_, 0, bcd, st_);
+      ++launches_;
+    }
+    check_launch();
+    // finish_run (executor.hpp:769-779)
+    for (size_t b = 0; b < kp->bindings.size(); ++b) {
+      if (reg != SF_REGION_INTERIOR) {
+        if (kp->writable[b]) ghosts_ok_[kp->bindings[b]] = false;
+      } else if (kp->writable[b] && !kp->to_back[b]) {
+        ghosts_ok_[kp->bindings[b]] = false;
+      }
+    }
+    if (reg != SF_REGION_INTERIOR && name == "UPDATE_VELOCITY") swap_front_back();
+  }
+
+  double reduce(int f, int op) {
+    if (op == SF_MAX_ABS || op == SF_MAX_ABS_DIFF) {
+      if (op == SF_MAX_ABS_DIFF && f > SF_VZ)
+        throw error(SF_ERR_GRID,
+                    std::string("field '") + kFieldNames[f] + "' has no back buffer to diff against");
+      ctl(CTL_CLEAR_ACC);
+      const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_plain_);
+      const int fl[1] = {f};
+      launch_reduce_max(tview(ws), ws.nctas, zc_plain_, fl, 1, op == SF_MAX_ABS_DIFF ? 1 : 0,
+                        &dctl_->acc[7], st_);
+      ++launches_;
+      check_launch();
+      return read_acc(7);
+    }
+    const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_plain_);
+    double* parts = (double*)dalloc_tmp(sizeof(double) * (size_t)ws.nctas);
+    launch_reduce_sum(tview(ws), ws.nctas, zc_plain_, f, op == SF_SUM_SQ ? 1 : 0, parts, st_);
+    ++launches_;
+    check_launch();
+    std::vector<double> hp(ws.nctas);
+    SF_CK(cudaMemcpyAsync(hp.data(), parts, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, st_));
+    sync();
+    SF_CK(cudaFree(parts));
+    double acc = 0.0;
+    for (double x : hp) acc += x;
+    return acc;
+  }
+
+  // ---- the time step (cfd.hpp:264-316) --------------------------------------
+  void compute_dt_device() {
+    const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_plain_);
+    const int fl[3] = {SF_VX, SF_VY, SF_VZ};
+    ctl(CTL_CLEAR_ACC);
+    launch_reduce_max(tview(ws), ws.nctas, zc_plain_, fl, 3, 0, &dctl_->acc[0], st_);
+    ++launches_;
+    ctl(CTL_DT_FROM_ACC);
+    check_launch();
+  }
+  double compute_dt() {
+    compute_dt_device();
+    sync();
+    return hflag_->dt;
+  }
+
+  void provisional_device() {
+    refresh({SF_VX, SF_VY, SF_VZ, SF_P});
+    const work_set& ws = items_for(SF_REGION_ALL, {1, 1, 1, 1, 1, 1}, zc_uv_);
+    launch_update_velocity(tview(ws), ws.nctas, zc_uv_, consts_, dctl_, 0.0, st_);
+    ++launches_;
+    check_launch();
+    swap_front_back();
+    for (int f : {SF_VX, SF_VY, SF_VZ}) ghosts_ok_[kFieldNames[f]] = false;
+    ctl(CTL_CHECK_FINITE);
+  }
+  void check_finite_or_throw() {
+    sync();
+    const int a = hflag_->abort_field;
+    if (a >= 0) {
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "%f", time_);  // std::to_string(double)
+      throw error(SF_ERR_CFD, std::string("non-finite ") + kFieldNames[a] +
+                                  " after the velocity update at step " + std::to_string(steps_) +
+                                  ", t = " + buf);
+    }
+  }
+  void provisional(double dt) {
+    ctl(CTL_SET_DT, dt);
+    provisional_device();
+    check_finite_or_throw();
+  }
+
+  std::pair<int, double> pressure_iteration_device() {
+    refresh({SF_VX, SF_VY, SF_VZ});
+    const work_set& wd = items_for(SF_REGION_ALL, {1, 0, 1, 0, 1, 0}, zc_plain_);
+    launch_divergence(tview(wd), wd.nctas, zc_plain_, consts_, dctl_, -1, 0, st_);
+    ++launches_;
+    check_launch();
+    if (opt_.fused) refresh({SF_DIVU});
+    ctl(CTL_BEGIN_ITERATION);
+    const int maxs = std::max(1, cfg_.max_sweeps);
+    int issued = 0;
+    int batch = std::max(1, std::min(maxs, est_sweeps_));
+    auto enqueue = [&](int n, cudaEvent_t ev) {
+      for (int q = 0; q < n; ++q) enqueue_half_sweep();
+      issued += n;
+      SF_CK(cudaEventRecord(ev, st_));
+    };
+    iter_launch_ = 0;
+    enqueue(batch, ev_[0]);
+    int cur = 0;
+    while (true) {
+      bool more = false;
+      if (issued < maxs) {
+        const int nb = std::min(maxs - issued, batch);
+        enqueue(nb, ev_[cur ^ 1]);
+        more = true;
+        batch = std::min(batch * 2, 4096);
+      }
+      SF_CK(cudaEventSynchronize(ev_[cur]));
+      if (hflag_->done) break;
+      if (!more) break;
+      cur ^= 1;
+    }
+    sync();
+    const int sweeps = hflag_->sweeps;
+    const double residual = hflag_->residual;
+    if (sweeps > 0) est_sweeps_ = sweeps;
+    if (timing_ && opt_.fused) {
+      // executed half-sweeps are the first `sweeps` launches; the rest were predicated off
+      for (int q = 0; q < sweeps && q < iter_launch_; ++q) {
+        float ms = 0.f;
+        SF_CK(cudaEventElapsedTime(&ms, timer(q, 0), timer(q, 1)));
+        sweep_ms_ += ms;
+        ++sweep_launches_;
+      }
+    }
+    if (opt_.fused) refresh({SF_VX, SF_VY, SF_VZ});
+    // ghost state as the reference leaves it (executor.hpp:769-779)
+    ghosts_ok_["p"] = false;
+    ghosts_ok_["divu"] = false;
+    for (int f : {SF_VX, SF_VY, SF_VZ}) ghosts_ok_[kFieldNames[f]] = true;
+    return {sweeps, residual};
+  }
+  std::pair<int, double> pressure_iteration(double dt) {
+    ctl(CTL_SET_DT, dt);
+    return pressure_iteration_device();
+  }
+
+  sf_step_stats step() {
+    compute_dt_device();
+    provisional_device();
+    check_finite_or_throw();
+    const double dt = hflag_->dt;
+    auto r = pressure_iteration_device();
+    refresh({SF_P});
+    time_ += dt;
+    ++steps_;
+    last_ = {dt, r.first, r.second};
+    return last_;
+  }
+  sf_step_stats advance(int n) {
+    for (int i = 0; i < n; ++i) step();
+    return last_;
+  }
+
+  // ---- diagnostics (cfd.hpp:342-363) -----------------------------------------
+  double max_divergence() {
+    refresh({SF_VX, SF_VY, SF_VZ});
+    ctl(CTL_CLEAR_ACC);
+    const work_set& wd = items_for(SF_REGION_ALL, {1, 0, 1, 0, 1, 0}, zc_plain_);
+    launch_divergence(tview(wd), wd.nctas, zc_plain_, consts_, dctl_, 7, 0, st_);
+    ++launches_;
+    check_launch();
+    ghosts_ok_["divu"] = false;
+    return read_acc(7);
+  }
+  double steady_delta() {
+    double d = reduce(SF_VX, SF_MAX_ABS_DIFF);
+    const double dy = reduce(SF_VY, SF_MAX_ABS_DIFF);
+    d = d < dy ? dy : d;  // std::max
+    const double dz = reduce(SF_VZ, SF_MAX_ABS_DIFF);
+    d = d < dz ? dz : d;
+    return d;
+  }
+  double kinetic_energy() {
+    const double s = reduce(SF_VX, SF_SUM_SQ) + reduce(SF_VY, SF_SUM_SQ) + reduce(SF_VZ, SF_SUM_SQ);
+    const double cell = cfg_.spacing[0] * cfg_.spacing[1] * cfg_.spacing[2];
+    return 0.5 * par_.density * s * cell;
+  }
+
+  double time() const { return time_; }
+  long steps() const { return steps_; }
+  int pending_color() {
+    sync();
+    return hflag_->color;
+  }
+  bool ghosts_valid(const std::string& f) const {
+    auto it = ghosts_ok_.find(f);
+    return it != ghosts_ok_.end() && it->second;
+  }
+  void invalidate(const std::string& f) { ghosts_ok_[f] = false; }
+  void invalidate_all() { ghosts_ok_.clear(); }
+  cudaStream_t stream() const { return st_; }
+  i64 launch_count(bool reset) {
+    const i64 n = launches_;
+    if (reset) launches_ = 0;
+    return n;
+  }
+  void set_timing(bool on) {
+    timing_ = on;
+    sweep_ms_ = 0.0;
+    sweep_launches_ = 0;
+  }
+  void timing(double* ms, i64* n) const {
+    *ms = sweep_ms_;
+    *n = sweep_launches_;
+  }
+
+ private:
+  struct work_set {
+    sf_work* d = nullptr;
+    int n = 0;
+    int nctas = 0;
+  };
+  struct task_set {
+    sf_task* d = nullptr;
+    int n = 0;
+    i64 max_count = 0;
+  };
+
+  sf_solver_config cfg_;
+  sf_fluid_params par_;
+  sf_sim_options opt_;
+  decomposition dec_;
+  sf_face_bc bc_[6]{};
+  sf_consts consts_{};
+  std::vector<sf_layout> lay_;
+  cudaStream_t st_ = nullptr;
+  cudaEvent_t ev_[2]{}, t0_{}, t1_{};
+  std::unique_ptr<sf_dev_table> htab_;
+  sf_dev_table* dtab_ = nullptr;
+  sf_dev_ctl* dctl_ = nullptr;
+  sf_host_flag* hflag_ = nullptr;
+  sf_host_flag* dflag_ = nullptr;
+  double* staging_ = nullptr;
+  std::vector<void*> dev_allocs_;
+  std::map<std::string, work_set> items_;
+  std::map<std::string, task_set> tasks_;
+  task_set divu_faces_;
+  bool divu_faces_built_ = false;
+  std::map<std::string, bool> ghosts_ok_;
+  double time_ = 0.0;
+  long steps_ = 0;
+  sf_step_stats last_{0.0, 0, 0.0};
+  int est_sweeps_ = 8;
+  i64 launches_ = 0;
+  bool timing_ = false;
+  double sweep_ms_ = 0.0;
+  i64 sweep_launches_ = 0;
+  std::vector<cudaEvent_t> timers_;
+  int iter_launch_ = 0;
+  cudaEvent_t timer(int q, int which) {
+    while ((int)timers_.size() < 2 * (q + 1)) {
+      cudaEvent_t e;
+      SF_CK(cudaEventCreate(&e));
+      timers_.push_back(e);
+    }
+    return timers_[2 * q + which];
+  }
+  const int zc_plain_ = 16;
+  const int zc_uv_ = 8;
+  const int zc_fused_ = 32;
+
+  void validate() {
+    // solver_config::validate / fluid_params::validate (cfd.hpp:36-66)
+    for (int a = 0; a < 3; ++a) {
+      if (cfg_.extents[a] < 1) throw error(SF_ERR_CONFIG, "domain extents must be positive");
+      if (!(cfg_.spacing[a] > 0.0)) throw error(SF_ERR_CONFIG, "grid spacing must be positive");
+    }
+    if (!(cfg_.reynolds > 0.0)) throw error(SF_ERR_CONFIG, "Reynolds number must be positive");
+    if (!(cfg_.sigma > 0.0 && cfg_.sigma < 1.0)) throw error(SF_ERR_CONFIG, "sigma must lie in (0,1)");
+    if (!(cfg_.tolerance > 0.0)) throw error(SF_ERR_CONFIG, "pressure tolerance must be positive");
+    if (!(cfg_.omega >= 1.0 && cfg_.omega < 2.0)) throw error(SF_ERR_CONFIG, "omega must lie in [1,2)");
+    if (cfg_.max_sweeps < 1) throw error(SF_ERR_CONFIG, "max_sweeps must be at least 1");
+    if (!(par_.viscosity > 0.0)) throw error(SF_ERR_CONFIG, "viscosity must be positive");
+    if (!(par_.density > 0.0)) throw error(SF_ERR_CONFIG, "density must be positive");
+    if (!(par_.blend >= 0.0 && par_.blend <= 1.0)) throw error(SF_ERR_CONFIG, "blend must lie in [0,1]");
+    if (opt_.ghost < 1)
+      throw error(SF_ERR_EXEC, "kernel 'UPDATE_VELOCITY': stencil needs 1 ghost layers but fields carry " +
+                                   std::to_string(opt_.ghost));
+  }
+
+  void make_bc() {  // cfd.hpp:500-512
+    for (int axis = 0; axis < 3; ++axis) {
+      if (cfg_.periodic[axis]) continue;
+      for (int side = 0; side < 2; ++side) bc_[2 * axis + side] = {SF_BC_WALL, {0, 0, 0}};
+    }
+    if (!cfg_.periodic[1]) bc_[3] = {SF_BC_WALL, {par_.lid_speed, 0.0, 0.0}};
+    if (!cfg_.periodic[2] && cfg_.symmetry_z) {
+      bc_[4] = {SF_BC_SYMMETRY, {0, 0, 0}};
+      bc_[5] = {SF_BC_SYMMETRY, {0, 0, 0}};
+    }
+  }
+
+  void make_consts() {  // cfd.hpp:192-217
+    sf_consts& s = consts_;
+    s.nu = par_.viscosity;
+    s.alpha = par_.blend;
+    s.fx = par_.body_force[0];
+    s.fy = par_.body_force[1];
+    s.fz = par_.body_force[2];
+    s.ix = 1.0 / cfg_.spacing[0];
+    s.iy = 1.0 / cfg_.spacing[1];
+    s.iz = 1.0 / cfg_.spacing[2];
+    s.ix2 = s.ix * s.ix;
+    s.iy2 = s.iy * s.iy;
+    s.iz2 = s.iz * s.iz;
+    for (int a = 0; a < 3; ++a) {
+      s.nm1[a] = cfg_.extents[a] - 1;
+      s.N[a] = cfg_.extents[a];
+      s.per[a] = cfg_.periodic[a] ? 1 : 0;
+      s.spacing[a] = cfg_.spacing[a];
+    }
+    auto act = [&](double ax, double ay, double az) { return ax * s.ix2 + ay * s.iy2 + az * s.iz2; };
+    for (int bx = 0; bx < 2; ++bx)
+      for (int by = 0; by < 2; ++by)
+        for (int bz = 0; bz < 2; ++bz)
+          s.bscale[bx][by][bz] = act(2.0, 2.0, 2.0) / act(bx ? 2.0 : 1.0, by ? 2.0 : 1.0, bz ? 2.0 : 1.0);
+    s.sigma = cfg_.sigma;
+    s.omega = cfg_.omega;
+    s.tolerance = cfg_.tolerance;
+    s.max_sweeps = cfg_.max_sweeps;
+  }
+
+  void* dalloc(size_t bytes) {
+    void* p = nullptr;
+    SF_CK(cudaMalloc(&p, bytes));
+    dev_allocs_.push_back(p);
+    return p;
+  }
+  void* dalloc_tmp(size_t bytes) {
+    void* p = nullptr;
+    SF_CK(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
+    return p;
+  }
+
+  void allocate() {
+    htab_ = std::make_unique<sf_dev_table>();
+    std::memset(htab_.get(), 0, sizeof(sf_dev_table));
+    htab_->nblocks = dec_.workers;
+    lay_.resize(dec_.workers);
+    for (int b = 0; b < dec_.workers; ++b) {
+      const auto dims = dec_.dims(b);
+      const i64 lo[3] = {dec_.lo[b][0], dec_.lo[b][1], dec_.lo[b][2]};
+      const i64 dd[3] = {dims[0], dims[1], dims[2]};
+      lay_[b] = make_layout(dd, lo, dec_.ghost);
+      const sf_layout& L = lay_[b];
+      sf_dev_block& B = htab_->blk[b];
+      for (int a = 0; a < 3; ++a) {
+        B.n[a] = L.dims[a];
+        B.lo[a] = L.lo[a];
+      }
+      B.sx = L.sx;
+      B.sy = L.sy;
+      B.sz = L.sz;
+      B.base = L.base;
+      B.g = L.ghost;
+      for (int a = 0; a < 3; ++a)
+        for (int side = 0; side < 2; ++side) {
+          const int fi = 2 * a + side;
+          const int nb = dec_.neighbor(b, a, side);
+          if (nb < 0) {
+            const int k = bc_[fi].kind;
+            B.face[fi] = k == SF_BC_WALL ? FACE_WALL
+                         : k == SF_BC_SYMMETRY ? FACE_SYM
+                         : k == SF_BC_OUTFLOW ? FACE_OUT : FACE_WALL;
+          } else {
+            B.face[fi] = nb == b ? FACE_SELF : FACE_PROC;
+          }
+          for (int c = 0; c < 3; ++c) B.fvel[fi][c] = bc_[fi].velocity[c];
+          const i64 N = cfg_.extents[a];
+          B.nb_ghost_gidx[fi] = side == 0 ? (L.lo[a] - 1 + N) % N : (L.lo[a] + L.dims[a]) % N;
+        }
+      const size_t bytes = sizeof(double) * (size_t)(L.sx * L.sy * L.sz);
+      for (int f = 0; f < SF_NFIELDS; ++f) {
+        const bool velocity = f <= SF_VZ;
+        for (int s = 0; s < kSlots; ++s) {
+          const bool need = s == FRONT || (velocity && (s == BACK || s == ALT)) || (f == SF_DIVU && s == ALT);
+          if (!need) continue;
+          double* p = (double*)dalloc(bytes);
+          SF_CK(cudaMemsetAsync(p, 0, bytes, st_));
+          htab_->ptr[b][f][s] = p;
+        }
+      }
+    }
+    dtab_ = (sf_dev_table*)dalloc(sizeof(sf_dev_table));
+    SF_CK(cudaMemcpyAsync(dtab_, htab_.get(), sizeof(sf_dev_table), cudaMemcpyHostToDevice, st_));
+    dctl_ = (sf_dev_ctl*)dalloc(sizeof(sf_dev_ctl));
+    SF_CK(cudaMemsetAsync(dctl_, 0, sizeof(sf_dev_ctl), st_));
+    SF_CK(cudaHostAlloc((void**)&hflag_, sizeof(sf_host_flag), cudaHostAllocMapped));
+    std::memset((void*)hflag_, 0, sizeof(sf_host_flag));
+    SF_CK(cudaHostGetDevicePointer((void**)&dflag_, (void*)hflag_, 0));
+    sync();
+  }
+
+  void download_table() {
+    sync();
+    SF_CK(cudaMemcpy(htab_->ptr, dtab_->ptr, sizeof(htab_->ptr), cudaMemcpyDeviceToHost));
+  }
+
+  table_view tview() const { return table_view{dtab_, nullptr, 0}; }
+  table_view tview(const work_set& w) const { return table_view{dtab_, w.d, w.n}; }
+
+  void ctl(int op, double arg = 0.0, int f = 0, int a = 0, int b = 0, int predicated = 0) {
+    launch_ctl(dtab_, dctl_, dflag_, op, arg, f, a, b, consts_, predicated, st_);
+    ++launches_;
+  }
+
+  void swap_front_back() {
+    for (int f : {SF_VX, SF_VY, SF_VZ}) ctl(CTL_SWAP, 0.0, f, FRONT, BACK);
+  }
+
+  double read_acc(int slot) {
+    sync();
+    unsigned long long bits = 0;
+    SF_CK(cudaMemcpy(&bits, &dctl_->acc[slot], sizeof(bits), cudaMemcpyDeviceToHost));
+    if (bits > 0x7ff0000000000000ull) return std::nan("");
+    double v;
+    std::memcpy(&v, &bits, sizeof v);
+    return v;
+  }
+
+  const work_set& items_for(int reg, const std::array<int, 6>& halo, int zc) {
+    char key[128];
+    std::snprintf(key, sizeof key, "%d:%d,%d,%d,%d,%d,%d:%d", reg, halo[0], halo[1], halo[2],
+                  halo[3], halo[4], halo[5], zc);
+    auto it = items_.find(key);
+    if (it != items_.end()) return it->second;
+    std::vector<sf_work> v;
+    int cta = 0;
+    for (int b = 0; b < dec_.workers; ++b) {
+      const auto dims = dec_.dims(b);
+      for (const auto& bx : region_boxes(dims, halo, reg)) {
+        sf_work w{};
+        w.blk = b;
+        w.cta_begin = cta;
+        for (int a = 0; a < 3; ++a) {
+          w.lo[a] = bx[a];
+          w.hi[a] = bx[3 + a];
+        }
+        w.tiles[0] = (int)((w.hi[0] - w.lo[0] + kTX - 1) / kTX);
+        w.tiles[1] = (int)((w.hi[1] - w.lo[1] + kTY - 1) / kTY);
+        w.tiles[2] = (int)((w.hi[2] - w.lo[2] + zc - 1) / zc);
+        cta += w.tiles[0] * w.tiles[1] * w.tiles[2];
+        v.push_back(w);
+      }
+    }
+    work_set ws;
+    ws.n = (int)v.size();
+    ws.nctas = cta;
+    if (!v.empty()) {
+      ws.d = (sf_work*)dalloc(sizeof(sf_work) * v.size());
+      SF_CK(cudaMemcpy(ws.d, v.data(), sizeof(sf_work) * v.size(), cudaMemcpyHostToDevice));
+    }
+    return items_.emplace(key, ws).first->second;
+  }
+
+  void validate_bc(const std::vector<int>& fields) const {  // exchange.hpp:86-95
+    for (int axis = 0; axis < 3; ++axis) {
+      if (cfg_.periodic[axis]) continue;
+      for (int side = 0; side < 2; ++side)
+        if (bc_[2 * axis + side].kind == SF_BC_UNSET && !fields.empty())
+          throw error(SF_ERR_GRID, std::string("field '") + kFieldNames[fields.front()] +
+                                       "': no boundary condition on axis " + std::to_string(axis) +
+                                       (side == 0 ? " low" : " high") + " face");
+    }
+  }
+
+  // One axis phase of exchanger::refresh_worker (exchange.hpp:107-119): the
+  // messages of pack_axis (:165-206) as block-to-block copies plus the
+  // bc_face fills (:231-480) of that axis.  All tasks of a phase are
+  // independent (disjoint writes, reads of owned cells / earlier phases).
+  const task_set& tasks_for(unsigned mask, int axis, int scope, bool exchange_only) {
+    char key[64];
+    std::snprintf(key, sizeof key, "%u:%d:%d:%d", mask, axis, scope, exchange_only ? 1 : 0);
+    auto it = tasks_.find(key);
+    if (it != tasks_.end()) return it->second;
+    std::vector<sf_task> v;
+    const i64 g = dec_.ghost;
+    for (int w = 0; w < dec_.workers; ++w) {
+      const auto dims = dec_.dims(w);
+      for (int f = 0; f < SF_NFIELDS; ++f) {
+        if (!(mask & (1u << f))) continue;
+        for (int side = 0; side < 2; ++side) {
+          const int nb = dec_.neighbor(w, axis, side);
+          sf_task t{};
+          t.field = f;
+          t.axis = axis;
+          t.side = side;
+          if (nb >= 0) {
+            if (g == 0) continue;
+            t.type = 0;
+            t.src_blk = w;
+            t.dst_blk = nb;
+            const auto nbd = dec_.dims(nb);
+            for (int a = 0; a < 3; ++a) {
+              if (a == axis) {
+                t.lo[a] = side == 0 ? 0 : dims[a] - g;
+                t.dims[a] = g;
+                t.dlo[a] = side == 0 ? nbd[a] : -g;
+              } else if (a < axis) {
+                t.lo[a] = -g;
+                t.dims[a] = dims[a] + 2 * g;
+                t.dlo[a] = t.lo[a];
+              } else {
+                t.lo[a] = 0;
+                t.dims[a] = dims[a];
+                t.dlo[a] = 0;
+              }
+            }
+            t.count = t.dims[0] * t.dims[1] * t.dims[2];
+          } else {
+            if (exchange_only) continue;
+            const sf_face_bc& fb = bc_[2 * axis + side];
+            t.type = 1;
+            t.src_blk = t.dst_blk = w;
+            t.kind = fb.kind;
+            t.scope = scope;
+            t.normal = kStagger[f] == axis;
+            t.velocity = kStagger[f] >= 0;
+            const double vwall = t.velocity ? fb.velocity[kStagger[f]] : 0.0;
+            t.v = (t.normal && fb.kind == SF_BC_SYMMETRY) ? 0.0 : vwall;
+            for (int a = 0; a < 3; ++a) {
+              if (a == axis) {
+                t.lo[a] = 0;
+                t.dims[a] = 1;
+              } else if (a < axis) {
+                t.lo[a] = -g;
+                t.dims[a] = dims[a] + 2 * g;
+              } else {
+                t.lo[a] = 0;
+                t.dims[a] = dims[a];
+              }
+            }
+            t.count = t.dims[0] * t.dims[1] * t.dims[2];
+          }
+          v.push_back(t);
+        }
+      }
+    }
+    task_set ts;
+    ts.n = (int)v.size();
+    for (const auto& t : v) ts.max_count = std::max(ts.max_count, t.count);
+    if (!v.empty()) {
+      ts.d = (sf_task*)dalloc(sizeof(sf_task) * v.size());
+      SF_CK(cudaMemcpy(ts.d, v.data(), sizeof(sf_task) * v.size(), cudaMemcpyHostToDevice));
+    }
+    return tasks_.emplace(key, ts).first->second;
+  }
+
+  // divu face copies between distinct blocks for the fused loop (faces only:
+  // the half-sweep never reads edge or corner ghosts of divu).
+  const task_set& divu_faces() {
+    if (divu_faces_built_) return divu_faces_;
+    std::vector<sf_task> v;
+    const i64 g = dec_.ghost;
+    for (int w = 0; w < dec_.workers; ++w) {
+      const auto dims = dec_.dims(w);
+      for (int axis = 0; axis < 3; ++axis)
+        for (int side = 0; side < 2; ++side) {
+          const int nb = dec_.neighbor(w, axis, side);
+          if (nb < 0 || nb == w) continue;
+          const auto nbd = dec_.dims(nb);
+          sf_task t{};
+          t.type = 0;
+          t.field = SF_DIVU;
+          t.src_blk = w;
+          t.dst_blk = nb;
+          for (int a = 0; a < 3; ++a) {
+            if (a == axis) {
+              t.lo[a] = side == 0 ? 0 : dims[a] - g;
+              t.dims[a] = g;
+              t.dlo[a] = side == 0 ? nbd[a] : -g;
+            } else {
+              t.lo[a] = 0;
+              t.dims[a] = dims[a];
+              t.dlo[a] = 0;
+            }
+          }
+          t.count = t.dims[0] * t.dims[1] * t.dims[2];
+          v.push_back(t);
+        }
+    }
+    divu_faces_.n = (int)v.size();
+    for (const auto& t : v) divu_faces_.max_count = std::max(divu_faces_.max_count, t.count);
+    if (!v.empty()) {
+      divu_faces_.d = (sf_task*)dalloc(sizeof(sf_task) * v.size());
+      SF_CK(cudaMemcpy(divu_faces_.d, v.data(), sizeof(sf_task) * v.size(), cudaMemcpyHostToDevice));
+    }
+    divu_faces_built_ = true;
+    return divu_faces_;
+  }
+
+  void enqueue_half_sweep() {
+    if (opt_.fused) {
+      const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_);
+      if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
+      launch_sweep_div(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, st_);
+      ++launches_;
+      if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
+      ++iter_launch_;
+      const task_set& tf = divu_faces();
+      if (tf.n) {
+        launch_tasks(tview(), tf.d, tf.n, tf.max_count, dctl_, st_);
+        ++launches_;
+      }
+    } else {
+      // the reference's dataflow, predicated step by step (cfd.hpp:295-303)
+      refresh({SF_DIVU}, true);
+      const work_set& ws = items_for(SF_REGION_ALL, {0, 1, 0, 1, 0, 1}, zc_plain_);
+      launch_pressure_sweep(tview(ws), ws.nctas, zc_plain_, consts_, dctl_, 1, nullptr, st_);
+      ++launches_;
+      ctl(CTL_AFTER_SWEEP, 0.0, 0, 0, 0, 1);
+      refresh({SF_VX, SF_VY, SF_VZ}, true);
+      const work_set& wd = items_for(SF_REGION_ALL, {1, 0, 1, 0, 1, 0}, zc_plain_);
+      launch_divergence(tview(wd), wd.nctas, zc_plain_, consts_, dctl_, 0, 1, st_);
+      ++launches_;
+      ctl(CTL_FINISH_SWEEP, 0.0, 0, 0, 0, 1);
+    }
+    check_launch();
+  }
+};
+
+}  // namespace sfb
+
+// ===========================================================================
+// C ABI (include/sforge_b200.h)
+// ===========================================================================
+struct sf_sim {
+  std::unique_ptr<sfb::simulation> s;
+};
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SF_OK;
+  } catch (const sfb::error& e) {
+    sfb::g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    sfb::g_last_error = e.what();
+    return SF_ERR_ARG;
+  }
+}
+
+int need(const void* p, const char* what) {
+  if (!p) throw sfb::error(SF_ERR_ARG, std::string(what) + " is null");
+  return 0;
+}
+
+std::vector<int> field_list(const char* const* fields, int n) {
+  std::vector<int> out;
+  for (int i = 0; i < n; ++i) out.push_back(sfb::simulation::field_id(fields[i]));
+  return out;
+}
+
+// direct-view helpers for level-2 launches
+sfb::direct_view make_view(const sf_layout* l, const sf_box* boxes, int nbox, int zc) {
+  sfb::direct_view v;
+  std::memset(&v, 0, sizeof v);
+  for (int a = 0; a < 3; ++a) {
+    v.b0.n[a] = l->dims[a];
+    v.b0.lo[a] = l->lo[a];
+  }
+  v.b0.sx = l->sx;
+  v.b0.sy = l->sy;
+  v.b0.sz = l->sz;
+  v.b0.base = l->base;
+  v.b0.g = l->ghost;
+  if (nbox < 1 || nbox > sfb::kDirectItems)
+    throw sfb::error(SF_ERR_ARG, "nbox must lie in [1, 8]");
+  int cta = 0;
+  v.nitems = 0;
+  for (int q = 0; q < nbox; ++q) {
+    sfb::sf_work& w = v.it[v.nitems];
+    w.blk = 0;
+    w.cta_begin = cta;
+    bool empty = false;
+    for (int a = 0; a < 3; ++a) {
+      w.lo[a] = boxes[q].lo[a];
+      w.hi[a] = boxes[q].hi[a];
+      if (w.hi[a] <= w.lo[a]) empty = true;
+      if (w.lo[a] < 0 || w.hi[a] > l->dims[a]) throw sfb::error(SF_ERR_ARG, "box outside the block");
+    }
+    if (empty) continue;
+    w.tiles[0] = (int)((w.hi[0] - w.lo[0] + sfb::kTX - 1) / sfb::kTX);
+    w.tiles[1] = (int)((w.hi[1] - w.lo[1] + sfb::kTY - 1) / sfb::kTY);
+    w.tiles[2] = (int)((w.hi[2] - w.lo[2] + zc - 1) / zc);
+    cta += w.tiles[0] * w.tiles[1] * w.tiles[2];
+    ++v.nitems;
+  }
+  v.b0.face[0] = cta;  // scratch: total CTAs (read back by the caller, faces unused here)
+  return v;
+}
+
+sfb::sf_consts to_consts(const sf_cfd_consts* c) {
+  sfb::sf_consts s{};
+  s.nu = c->nu;
+  s.alpha = c->alpha;
+  s.fx = c->fx;
+  s.fy = c->fy;
+  s.fz = c->fz;
+  s.ix = c->ix;
+  s.iy = c->iy;
+  s.iz = c->iz;
+  s.ix2 = c->ix2;
+  s.iy2 = c->iy2;
+  s.iz2 = c->iz2;
+  std::memcpy(s.bscale, c->bscale, sizeof s.bscale);
+  s.nm1[0] = c->nxm1;
+  s.nm1[1] = c->nym1;
+  s.nm1[2] = c->nzm1;
+  s.per[0] = c->px;
+  s.per[1] = c->py;
+  s.per[2] = c->pz;
+  return s;
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+void check_last() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw sfb::error(SF_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+extern "C" {
+
+int sf_abi_version(void) { return SF_ABI_VERSION; }
+const char* sf_last_error(void) { return sfb::g_last_error.c_str(); }
+int sf_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int sf_decompose(const int64_t extents[3], const double spacing[3], int workers, int ghost,
+                 const int periodic[3], int proc_grid[3], int64_t* lo, int64_t* hi) {
+  return guarded([&] {
+    need(extents, "extents");
+    need(spacing, "spacing");
+    const long long ext[3] = {extents[0], extents[1], extents[2]};
+    const bool per[3] = {periodic && periodic[0] != 0, periodic && periodic[1] != 0,
+                         periodic && periodic[2] != 0};
+    const auto d = sfb::decompose(ext, spacing, workers, ghost, per);
+    for (int a = 0; a < 3; ++a)
+      if (proc_grid) proc_grid[a] = d.pg[a];
+    for (int w = 0; w < d.workers; ++w)
+      for (int a = 0; a < 3; ++a) {
+        if (lo) lo[3 * w + a] = d.lo[w][a];
+        if (hi) hi[3 * w + a] = d.hi[w][a];
+      }
+  });
+}
+
+int sf_decomp_neighbor(const int proc_grid[3], const int periodic[3], int w, int axis, int side) {
+  sfb::decomposition d;
+  for (int a = 0; a < 3; ++a) {
+    d.pg[a] = proc_grid[a];
+    d.periodic[a] = periodic[a] != 0;
+  }
+  return d.neighbor(w, axis, side);
+}
+
+void sf_sim_options_default(sf_sim_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->workers = 1;
+  o->mode = 0;
+  o->ghost = 1;
+  o->form = 0;
+  o->device = 0;
+  o->fused = 1;
+}
+
+int sf_sim_create(const sf_solver_config* cfg, const sf_fluid_params* par,
+                  const sf_sim_options* opt, sf_sim** out) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(par, "par");
+    need(out, "out");
+    *out = nullptr;
+    sf_sim_options o;
+    if (opt) o = *opt; else sf_sim_options_default(&o);
+    auto h = std::make_unique<sf_sim>();
+    h->s = std::make_unique<sfb::simulation>(*cfg, *par, o);
+    *out = h.release();
+  });
+}
+
+void sf_sim_destroy(sf_sim* s) { delete s; }
+
+#define SIM(s) (need((s), "sim"), *(s)->s)
+
+int sf_sim_init_cavity(sf_sim* s) { return guarded([&] { SIM(s).init_cavity(); }); }
+int sf_sim_init_uniform(sf_sim* s, double cx, double cy, double cz) {
+  return guarded([&] { SIM(s).init_uniform(cx, cy, cz); });
+}
+int sf_sim_init_taylor_green(sf_sim* s) { return guarded([&] { SIM(s).init_taylor_green(); }); }
+
+int sf_sim_compute_dt(sf_sim* s, double* dt) {
+  return guarded([&] {
+    need(dt, "dt");
+    *dt = SIM(s).compute_dt();
+  });
+}
+int sf_sim_provisional(sf_sim* s, double dt) { return guarded([&] { SIM(s).provisional(dt); }); }
+int sf_sim_pressure_iteration(sf_sim* s, double dt, int* sweeps, double* residual) {
+  return guarded([&] {
+    auto r = SIM(s).pressure_iteration(dt);
+    if (sweeps) *sweeps = r.first;
+    if (residual) *residual = r.second;
+  });
+}
+int sf_sim_step(sf_sim* s, sf_step_stats* out) {
+  return guarded([&] {
+    auto r = SIM(s).step();
+    if (out) *out = r;
+  });
+}
+int sf_sim_advance(sf_sim* s, int n, sf_step_stats* last) {
+  return guarded([&] {
+    auto r = SIM(s).advance(n);
+    if (last) *last = r;
+  });
+}
+double sf_sim_time(const sf_sim* s) { return s ? s->s->time() : 0.0; }
+long sf_sim_step_count(const sf_sim* s) { return s ? s->s->steps() : 0; }
+int sf_sim_pending_color(sf_sim* s) {
+  int c = -1;
+  guarded([&] { c = SIM(s).pending_color(); });
+  return c;
+}
+int sf_sim_max_divergence(sf_sim* s, double* out) {
+  return guarded([&] { *out = SIM(s).max_divergence(); });
+}
+int sf_sim_steady_delta(sf_sim* s, double* out) {
+  return guarded([&] { *out = SIM(s).steady_delta(); });
+}
+int sf_sim_kinetic_energy(sf_sim* s, double* out) {
+  return guarded([&] { *out = SIM(s).kinetic_energy(); });
+}
+
+static void check_n(const sf_sim* s, int64_t n) {
+  (void)s;
+  if (n < 0) throw sfb::error(SF_ERR_ARG, "negative element count");
+}
+
+int sf_sim_scatter(sf_sim* s, const char* field, const double* host, int64_t n) {
+  return guarded([&] {
+    auto& S = SIM(s);
+    need(host, "host");
+    check_n(s, n);
+    if (n != S.cells())
+      throw sfb::error(SF_ERR_GRID, "scatter: global array has " + std::to_string(n) +
+                                        " values, domain has " + std::to_string(S.cells()) + " cells");
+    S.scatter(sfb::simulation::field_id(field), host);
+  });
+}
+int sf_sim_gather(sf_sim* s, const char* field, double* host, int64_t n) {
+  return guarded([&] {
+    auto& S = SIM(s);
+    need(host, "host");
+    if (n < S.cells()) throw sfb::error(SF_ERR_ARG, "gather: host buffer too small");
+    S.gather(sfb::simulation::field_id(field), host);
+  });
+}
+int sf_sim_scatter_device(sf_sim* s, const char* field, const double* dev, int64_t n) {
+  return guarded([&] {
+    auto& S = SIM(s);
+    need(dev, "dev");
+    if (n != S.cells()) throw sfb::error(SF_ERR_GRID, "scatter: size mismatch");
+    S.scatter_from_device(sfb::simulation::field_id(field), dev);
+  });
+}
+int sf_sim_gather_device(sf_sim* s, const char* field, double* dev, int64_t n) {
+  return guarded([&] {
+    auto& S = SIM(s);
+    need(dev, "dev");
+    if (n < S.cells()) throw sfb::error(SF_ERR_ARG, "gather: device buffer too small");
+    S.gather_to_device(sfb::simulation::field_id(field), dev);
+  });
+}
+int sf_sim_checksum(sf_sim* s, uint64_t* out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = SIM(s).checksum();
+  });
+}
+int sf_sim_local_front(sf_sim* s, const char* field, int worker, double* host, int64_t host_elems,
+                       int64_t dims[3], int64_t lo[3]) {
+  return guarded([&] {
+    need(host, "host");
+    long long d[3], l[3];
+    SIM(s).local_front(sfb::simulation::field_id(field), worker, host, host_elems, d, l);
+    for (int a = 0; a < 3; ++a) {
+      dims[a] = d[a];
+      lo[a] = l[a];
+    }
+  });
+}
+int sf_sim_refresh(sf_sim* s, const char* const* fields, int n) {
+  return guarded([&] {
+    auto& S = SIM(s);
+    S.refresh(field_list(fields, n));
+  });
+}
+int sf_sim_exchange(sf_sim* s, const char* const* fields, int n) {
+  return guarded([&] {
+    auto& S = SIM(s);
+    S.exchange_only(field_list(fields, n));
+  });
+}
+int sf_sim_run_kernel(sf_sim* s, const char* name, const char* const* param_names,
+                      const double* param_values, int n_params, int region) {
+  return guarded([&] {
+    auto& S = SIM(s);
+    std::map<std::string, double> pm;
+    for (int i = 0; i < n_params; ++i) pm[param_names[i]] = param_values[i];
+    S.run_kernel(name, pm, region);
+  });
+}
+int sf_sim_reduce(sf_sim* s, const char* field, int op, double* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (op < 0 || op > 3) throw sfb::error(SF_ERR_ARG, "bad reduce op");
+    *out = SIM(s).reduce(sfb::simulation::field_id(field), op);
+  });
+}
+int sf_sim_invalidate_ghosts(sf_sim* s, const char* field) {
+  return guarded([&] { SIM(s).invalidate(field); });
+}
+int sf_sim_invalidate_all_ghosts(sf_sim* s) { return guarded([&] { SIM(s).invalidate_all(); }); }
+int sf_sim_ghosts_valid(sf_sim* s, const char* field) {
+  int v = 0;
+  guarded([&] { v = SIM(s).ghosts_valid(field) ? 1 : 0; });
+  return v;
+}
+int sf_sim_synchronize(sf_sim* s) { return guarded([&] { SIM(s).sync(); }); }
+void* sf_sim_stream(sf_sim* s) { return s ? (void*)s->s->stream() : nullptr; }
+int64_t sf_sim_launch_count(sf_sim* s, int reset) { return s ? s->s->launch_count(reset != 0) : 0; }
+int sf_sim_set_kernel_timing(sf_sim* s, int enable) {
+  return guarded([&] { SIM(s).set_timing(enable != 0); });
+}
+int sf_sim_kernel_timing(sf_sim* s, const char* kernel, double* total_ms, int64_t* launches) {
+  return guarded([&] {
+    if (std::string(kernel ? kernel : "") != "sweep_div")
+      throw sfb::error(SF_ERR_ARG, "timed kernels: sweep_div");
+    double ms = 0.0;
+    long long n = 0;
+    SIM(s).timing(&ms, &n);
+    *total_ms = ms;
+    *launches = n;
+  });
+}
+
+// ---- level 2 -----------------------------------------------------------------
+int sf_make_layout(const int64_t dims[3], const int64_t lo[3], int ghost, sf_layout* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (ghost < 0) throw sfb::error(SF_ERR_ARG, "ghost width must be >= 0");
+    long long d[3] = {dims[0], dims[1], dims[2]}, l[3] = {lo[0], lo[1], lo[2]};
+    *out = sfb::make_layout(d, l, ghost);
+  });
+}
+int64_t sf_layout_elems(const sf_layout* l) { return l ? l->sx * l->sy * l->sz : 0; }
+
+int sf_make_cfd_consts(const sf_solver_config* cfg, const sf_fluid_params* par, sf_cfd_consts* out) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(par, "par");
+    need(out, "out");
+    sf_cfd_consts& s = *out;
+    std::memset(&s, 0, sizeof s);
+    s.nu = par->viscosity;
+    s.alpha = par->blend;
+    s.fx = par->body_force[0];
+    s.fy = par->body_force[1];
+    s.fz = par->body_force[2];
+    s.ix = 1.0 / cfg->spacing[0];
+    s.iy = 1.0 / cfg->spacing[1];
+    s.iz = 1.0 / cfg->spacing[2];
+    s.ix2 = s.ix * s.ix;
+    s.iy2 = s.iy * s.iy;
+    s.iz2 = s.iz * s.iz;
+    s.nxm1 = cfg->extents[0] - 1;
+    s.nym1 = cfg->extents[1] - 1;
+    s.nzm1 = cfg->extents[2] - 1;
+    s.px = cfg->periodic[0] ? 1 : 0;
+    s.py = cfg->periodic[1] ? 1 : 0;
+    s.pz = cfg->periodic[2] ? 1 : 0;
+    auto act = [&](double ax, double ay, double az) { return ax * s.ix2 + ay * s.iy2 + az * s.iz2; };
+    for (int bx = 0; bx < 2; ++bx)
+      for (int by = 0; by < 2; ++by)
+        for (int bz = 0; bz < 2; ++bz)
+          s.bscale[bx][by][bz] = act(2.0, 2.0, 2.0) / act(bx ? 2.0 : 1.0, by ? 2.0 : 1.0, bz ? 2.0 : 1.0);
+  });
+}
+
+int sf_launch_update_velocity(const sf_layout* l, const double* vx, const double* vy,
+                              const double* vz, const double* p, double* vx_out, double* vy_out,
+                              double* vz_out, const sf_cfd_consts* c, const sf_box* boxes, int nbox,
+                              void* stream) {
+  return guarded([&] {
+    need(l, "layout");
+    need(c, "consts");
+    const int zc = 8;
+    auto v = make_view(l, boxes, nbox, zc);
+    const int nctas = v.b0.face[0];
+    v.p[SF_VX][sfb::FRONT] = const_cast<double*>(vx);
+    v.p[SF_VY][sfb::FRONT] = const_cast<double*>(vy);
+    v.p[SF_VZ][sfb::FRONT] = const_cast<double*>(vz);
+    v.p[SF_P][sfb::FRONT] = const_cast<double*>(p);
+    v.p[SF_VX][sfb::BACK] = vx_out;
+    v.p[SF_VY][sfb::BACK] = vy_out;
+    v.p[SF_VZ][sfb::BACK] = vz_out;
+    sfb::launch_update_velocity(v, nctas, zc, to_consts(c), nullptr, c->dt, as_stream(stream));
+    check_last();
+  });
+}
+
+int sf_launch_divergence(const sf_layout* l, const double* vx, const double* vy, const double* vz,
+                         double* divu, const sf_cfd_consts* c, const sf_box* boxes, int nbox,
+                         void* stream) {
+  return guarded([&] {
+    need(l, "layout");
+    need(c, "consts");
+    const int zc = 16;
+    auto v = make_view(l, boxes, nbox, zc);
+    const int nctas = v.b0.face[0];
+    v.p[SF_VX][sfb::FRONT] = const_cast<double*>(vx);
+    v.p[SF_VY][sfb::FRONT] = const_cast<double*>(vy);
+    v.p[SF_VZ][sfb::FRONT] = const_cast<double*>(vz);
+    v.p[SF_DIVU][sfb::FRONT] = divu;
+    sfb::launch_divergence(v, nctas, zc, to_consts(c), nullptr, -1, 0, as_stream(stream));
+    check_last();
+  });
+}
+
+int sf_launch_pressure_sweep(const sf_layout* l, const double* divu, double* p, double* vx,
+                             double* vy, double* vz, const sf_cfd_consts* c, double beta, int color,
+                             const sf_box* boxes, int nbox, void* stream) {
+  return guarded([&] {
+    need(l, "layout");
+    need(c, "consts");
+    const int zc = 16;
+    auto v = make_view(l, boxes, nbox, zc);
+    const int nctas = v.b0.face[0];
+    v.p[SF_DIVU][sfb::FRONT] = const_cast<double*>(divu);
+    v.p[SF_P][sfb::FRONT] = p;
+    v.p[SF_VX][sfb::FRONT] = vx;
+    v.p[SF_VY][sfb::FRONT] = vy;
+    v.p[SF_VZ][sfb::FRONT] = vz;
+    const double bcd[3] = {beta, (double)color, c->dt};
+    sfb::launch_pressure_sweep(v, nctas, zc, to_consts(c), nullptr, 0, bcd, as_stream(stream));
+    check_last();
+  });
+}
+
+int sf_launch_bc_face(const sf_layout* l, double* front, int stagger, int axis, int side,
+                      const sf_face_bc* bc, int scope, void* stream) {
+  return guarded([&] {
+    need(l, "layout");
+    need(bc, "bc");
+    if (axis < 0 || axis > 2 || side < 0 || side > 1) throw sfb::error(SF_ERR_ARG, "bad face");
+    if (bc->kind == SF_BC_UNSET)
+      throw sfb::error(SF_ERR_GRID, std::string("no boundary condition on axis ") +
+                                        std::to_string(axis) + (side == 0 ? " low" : " high") + " face");
+    if (l->ghost == 0) return;
+    const sf_box whole = {{0, 0, 0}, {l->dims[0], l->dims[1], l->dims[2]}};
+    auto v = make_view(l, &whole, 1, 1);
+    v.p[0][sfb::FRONT] = front;
+    sfb::sf_task t{};
+    t.type = 1;
+    t.field = 0;
+    t.axis = axis;
+    t.side = side;
+    t.kind = bc->kind;
+    t.scope = scope;
+    t.normal = stagger == axis;
+    t.velocity = stagger >= 0;
+    const double vwall = t.velocity ? bc->velocity[stagger] : 0.0;
+    t.v = (t.normal && bc->kind == SF_BC_SYMMETRY) ? 0.0 : vwall;
+    const long long g = l->ghost;
+    for (int a = 0; a < 3; ++a) {
+      if (a == axis) {
+        t.lo[a] = 0;
+        t.dims[a] = 1;
+      } else if (a < axis) {
+        t.lo[a] = -g;
+        t.dims[a] = l->dims[a] + 2 * g;
+      } else {
+        t.lo[a] = 0;
+        t.dims[a] = l->dims[a];
+      }
+    }
+    t.count = t.dims[0] * t.dims[1] * t.dims[2];
+    cudaStream_t st = as_stream(stream);
+    sfb::sf_task* d = nullptr;
+    SF_CK(cudaMallocAsync((void**)&d, sizeof t, st));
+    SF_CK(cudaMemcpyAsync(d, &t, sizeof t, cudaMemcpyHostToDevice, st));
+    sfb::launch_tasks(v, d, 1, t.count, nullptr, st);
+    check_last();
+    SF_CK(cudaFreeAsync(d, st));
+  });
+}
+
+int sf_launch_copy_box(const sf_layout* sl, const double* src, const sf_layout* dl, double* dst,
+                       const int64_t src_lo[3], const int64_t dims[3], const int64_t dst_lo[3],
+                       void* stream) {
+  return guarded([&] {
+    need(sl, "src layout");
+    need(dl, "dst layout");
+    const long long lo[3] = {src_lo[0], src_lo[1], src_lo[2]};
+    const long long d[3] = {dims[0], dims[1], dims[2]};
+    const long long m[3] = {dst_lo[0], dst_lo[1], dst_lo[2]};
+    sfb::launch_copy_box(src, sl->base, sl->sx, sl->sy, dst, dl->base, dl->sx, dl->sy, lo, d, m,
+                         as_stream(stream));
+    check_last();
+  });
+}
+
+int sf_launch_pack_box(const sf_layout* l, const double* src, const int64_t lo[3],
+                       const int64_t dims[3], double* buf, void* stream) {
+  return guarded([&] {
+    need(l, "layout");
+    const long long s[3] = {lo[0], lo[1], lo[2]};
+    const long long d[3] = {dims[0], dims[1], dims[2]};
+    const long long z[3] = {0, 0, 0};
+    sfb::launch_copy_box(src, l->base, l->sx, l->sy, buf, 0, d[0], d[1], s, d, z, as_stream(stream));
+    check_last();
+  });
+}
+
+int sf_launch_unpack_box(const sf_layout* l, double* dst, const int64_t lo[3],
+                         const int64_t dims[3], const double* buf, void* stream) {
+  return guarded([&] {
+    need(l, "layout");
+    const long long s[3] = {lo[0], lo[1], lo[2]};
+    const long long d[3] = {dims[0], dims[1], dims[2]};
+    const long long z[3] = {0, 0, 0};
+    sfb::launch_copy_box(buf, 0, d[0], d[1], dst, l->base, l->sx, l->sy, z, d, s, as_stream(stream));
+    check_last();
+  });
+}
+
+int sf_launch_reduce_max(const sf_layout* l, const double* front, const double* back, int op,
+                         double* dev_out, void* stream) {
+  return guarded([&] {
+    need(l, "layout");
+    need(dev_out, "dev_out");
+    if (op != SF_MAX_ABS && op != SF_MAX_ABS_DIFF) throw sfb::error(SF_ERR_ARG, "op must be a max op");
+    if (op == SF_MAX_ABS_DIFF && !back) throw sfb::error(SF_ERR_GRID, "no back buffer to diff against");
+    const sf_box whole = {{0, 0, 0}, {l->dims[0], l->dims[1], l->dims[2]}};
+    const int zc = 16;
+    auto v = make_view(l, &whole, 1, zc);
+    const int nctas = v.b0.face[0];
+    v.p[0][sfb::FRONT] = const_cast<double*>(front);
+    v.p[0][sfb::BACK] = const_cast<double*>(back);
+    const int fl[1] = {0};
+    sfb::launch_reduce_max(v, nctas, zc, fl, 1, op == SF_MAX_ABS_DIFF ? 1 : 0,
+                           reinterpret_cast<unsigned long long*>(dev_out), as_stream(stream));
+    check_last();
+  });
+}
+
+}  // extern "C"

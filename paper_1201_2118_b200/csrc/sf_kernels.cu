@@ -1,0 +1,885 @@
+// sf_kernels.cu -- sm_100a kernels of the staggered-grid stencil hot path.
+//
+// Every arithmetic expression keeps the association order of the reference
+// (cfd.hpp:524-720) and the library is compiled with --fmad=false, so each
+// cell is bitwise identical to the reference CPU implementation.
+//
+// Kernels (reference function each replaces):
+//   k_tasks        ghost refresh phase: exchange copies + bc_face (exchange.hpp:98-480)
+//   k_update_vel   UPDATE_VELOCITY point kernel (cfd.hpp:524-589) + NaN-guard maxima
+//   k_divergence   DIVERGENCE (cfd.hpp:595-618) + max|divu| epilogue (reductions.hpp:28-90)
+//   k_sweep        PRESSURE_SWEEP (cfd.hpp:630-720), in place
+//   k_sweep_div    fused half-sweep: PRESSURE_SWEEP + velocity refresh + DIVERGENCE +
+//                  max|divu| + the loop test of pressure_iteration (cfd.hpp:295-303)
+//   k_reduce_*     grid::reduce (reductions.hpp:28-90)
+//   k_ctl          compute_dt / beta / loop bookkeeping (cfd.hpp:264-305)
+#include <cstdio>
+
+#include "sf_kernels.cuh"
+
+namespace sfb {
+
+// ---------------------------------------------------------------------------
+// tile location
+// ---------------------------------------------------------------------------
+struct tile_loc {
+  int item;
+  int blk;
+  long long i, j, k0, k1;
+  bool act;
+};
+
+__device__ __forceinline__ tile_loc locate(const sf_work* __restrict__ items, int nitems, int zc) {
+  tile_loc t;
+  const int cta = blockIdx.x;
+  t.item = nitems > 1 ? find_item(items, nitems, cta) : 0;
+  const sf_work& w = items[t.item];
+  t.blk = w.blk;
+  const int local = cta - w.cta_begin;
+  const int tx = local % w.tiles[0];
+  const int ty = (local / w.tiles[0]) % w.tiles[1];
+  const int tz = local / (w.tiles[0] * w.tiles[1]);
+  t.i = w.lo[0] + (long long)tx * kTX + threadIdx.x;
+  t.j = w.lo[1] + (long long)ty * kTY + threadIdx.y;
+  t.k0 = w.lo[2] + (long long)tz * zc;
+  t.k1 = min(t.k0 + zc, w.hi[2]);
+  t.act = t.i < w.hi[0] && t.j < w.hi[1];
+  return t;
+}
+
+__device__ __forceinline__ bool pred_done(const sf_dev_ctl* ctl) {
+  return *reinterpret_cast<const volatile int*>(&ctl->done) != 0;
+}
+
+// ---------------------------------------------------------------------------
+// ghost refresh tasks
+// ---------------------------------------------------------------------------
+template <class View>
+__global__ void k_tasks(View vw, const sf_task* __restrict__ tasks,
+                        const sf_dev_ctl* pred) {
+  if (pred && pred_done(pred)) return;
+  const sf_task& T = tasks[blockIdx.y];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if (T.type == 0) {
+    const sf_dev_block& S = vw.blk(T.src_blk);
+    const sf_dev_block& D = vw.blk(T.dst_blk);
+    const double* src = vw.ptr(T.src_blk, T.field, FRONT);
+    double* dst = vw.ptr(T.dst_blk, T.field, FRONT);
+    const long long nx = T.dims[0], nxy = T.dims[0] * T.dims[1];
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < T.count; e += stride) {
+      const long long kk = e / nxy, rem = e - kk * nxy, jj = rem / nx, ii = rem - jj * nx;
+      dst[off(D, T.dlo[0] + ii, T.dlo[1] + jj, T.dlo[2] + kk)] =
+          src[off(S, T.lo[0] + ii, T.lo[1] + jj, T.lo[2] + kk)];
+    }
+    return;
+  }
+  // bc_face (exchange.hpp:231-480): one thread per tangential line.
+  const sf_dev_block& B = vw.blk(T.dst_blk);
+  double* f = vw.ptr(T.dst_blk, T.field, FRONT);
+  const int a = T.axis;
+  const int t1 = a == 0 ? 1 : 0;
+  const int t2 = a == 2 ? 1 : 2;
+  const long long g = B.g, b = B.n[a];
+  const long long n1 = T.dims[t1];
+  const long long astr = a == 0 ? 1 : (a == 1 ? B.sx : B.sx * B.sy);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < T.count; e += stride) {
+    long long c[3];
+    c[t1] = T.lo[t1] + e % n1;
+    c[t2] = T.lo[t2] + e / n1;
+    c[a] = 0;
+    const long long o0 = off(B, c[0], c[1], c[2]);  // position 0 along the axis
+#define LINE(pos) f[o0 + (long long)(pos) * astr]
+    const double v = T.v;
+    if (T.normal) {
+      if (T.kind == SF_BC_WALL || T.kind == SF_BC_SYMMETRY) {
+        if (T.side == 0) {
+          if (T.scope != SF_SCOPE_OWNED_ONLY) {
+            LINE(-1) = v;
+            for (long long m = 2; m <= g; ++m) {
+              const double src = LINE(m - 2);
+              LINE(-m) = 2.0 * v - src;
+            }
+          }
+        } else {
+          bool tang_owned = true;
+          for (int t = 0; t < 3; ++t)
+            if (t != a && (c[t] < 0 || c[t] >= B.n[t])) tang_owned = false;
+          if (T.scope == SF_SCOPE_ALL || (T.scope == SF_SCOPE_OWNED_ONLY && tang_owned) ||
+              (T.scope == SF_SCOPE_GHOSTS_ONLY && !tang_owned))
+            LINE(b - 1) = v;
+          if (T.scope != SF_SCOPE_OWNED_ONLY)
+            for (long long m = 1; m <= g; ++m) {
+              const double src = LINE(b - 1 - m);
+              LINE(b - 1 + m) = 2.0 * v - src;
+            }
+        }
+      } else if (T.kind == SF_BC_OUTFLOW && T.scope != SF_SCOPE_OWNED_ONLY) {
+        if (T.side == 0) {
+          const double v0 = LINE(0);
+          for (long long m = 1; m <= g; ++m) LINE(-m) = v0;
+        } else {
+          const double v0 = LINE(b - 1);
+          for (long long m = 1; m <= g; ++m) LINE(b - 1 + m) = v0;
+        }
+      }
+    } else if (T.scope != SF_SCOPE_OWNED_ONLY) {
+      if (T.kind == SF_BC_WALL && T.velocity) {
+        if (T.side == 0)
+          for (long long m = 1; m <= g; ++m) {
+            const double src = LINE(m - 1);
+            LINE(-m) = 2.0 * v - src;
+          }
+        else
+          for (long long m = 1; m <= g; ++m) {
+            const double src = LINE(b - m);
+            LINE(b - 1 + m) = 2.0 * v - src;
+          }
+      } else if (T.kind == SF_BC_WALL || T.kind == SF_BC_SYMMETRY) {
+        if (T.side == 0)
+          for (long long m = 1; m <= g; ++m) LINE(-m) = LINE(m - 1);
+        else
+          for (long long m = 1; m <= g; ++m) LINE(b - 1 + m) = LINE(b - m);
+      } else if (T.kind == SF_BC_OUTFLOW) {
+        if (T.side == 0) {
+          const double v0 = LINE(0);
+          for (long long m = 1; m <= g; ++m) LINE(-m) = v0;
+        } else {
+          const double v0 = LINE(b - 1);
+          for (long long m = 1; m <= g; ++m) LINE(b - 1 + m) = v0;
+        }
+      }
+    }
+#undef LINE
+  }
+}
+
+template <class View>
+void launch_tasks(const View& vw, const sf_task* tasks, int ntasks, long long max_count,
+                  const sf_dev_ctl* pred, cudaStream_t st) {
+  if (ntasks <= 0) return;
+  long long bx = (max_count + 255) / 256;
+  if (bx > 1184) bx = 1184;
+  if (bx < 1) bx = 1;
+  dim3 grid((unsigned)bx, (unsigned)ntasks);
+  k_tasks<View><<<grid, 256, 0, st>>>(vw, tasks, pred);
+}
+template void launch_tasks<table_view>(const table_view&, const sf_task*, int, long long,
+                                       const sf_dev_ctl*, cudaStream_t);
+template void launch_tasks<direct_view>(const direct_view&, const sf_task*, int, long long,
+                                        const sf_dev_ctl*, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// UPDATE_VELOCITY (cfd.hpp:524-589): reads front, writes back (SEPARATEINOUT)
+// ---------------------------------------------------------------------------
+template <class View>
+__global__ void __launch_bounds__(kTX* kTY) k_update_vel(View vw, int zc, sf_consts s,
+                                                         sf_dev_ctl* ctl, double dt_arg) {
+  const tile_loc t = locate(vw.work(), vw.nitems, zc);
+  const sf_dev_block& B = vw.blk(t.blk);
+  const double* __restrict__ U = vw.ptr(t.blk, SF_VX, FRONT);
+  const double* __restrict__ V = vw.ptr(t.blk, SF_VY, FRONT);
+  const double* __restrict__ W = vw.ptr(t.blk, SF_VZ, FRONT);
+  const double* __restrict__ Q = vw.ptr(t.blk, SF_P, FRONT);
+  double* __restrict__ Uo = vw.ptr(t.blk, SF_VX, BACK);
+  double* __restrict__ Vo = vw.ptr(t.blk, SF_VY, BACK);
+  double* __restrict__ Wo = vw.ptr(t.blk, SF_VZ, BACK);
+  const double dt = ctl ? ctl->dt : dt_arg;
+  const long long sx = B.sx, sxy = B.sx * B.sy;
+  unsigned long long mx[3] = {0ull, 0ull, 0ull};
+  if (t.act) {
+    for (long long k = t.k0; k < t.k1; ++k) {
+      const long long o = off(B, t.i, t.j, k);
+#define u(a, b, c) __ldg(U + o + (a) + (b) * sx + (c) * sxy)
+#define v(a, b, c) __ldg(V + o + (a) + (b) * sx + (c) * sxy)
+#define w(a, b, c) __ldg(W + o + (a) + (b) * sx + (c) * sxy)
+#define q(a, b, c) __ldg(Q + o + (a) + (b) * sx + (c) * sxy)
+      const double u0 = u(0, 0, 0), v0 = v(0, 0, 0), w0 = w(0, 0, 0);
+      {  // x momentum, at this cell's high x face
+        const double ue = u(1, 0, 0), uw = u(-1, 0, 0);
+        const double un = u(0, 1, 0), us = u(0, -1, 0);
+        const double ut = u(0, 0, 1), ub = u(0, 0, -1);
+        const double vn = v(0, 0, 0) + v(1, 0, 0), vs = v(0, -1, 0) + v(1, -1, 0);
+        const double wt = w(0, 0, 0) + w(1, 0, 0), wb = w(0, 0, -1) + w(1, 0, -1);
+        double fux = (u0 + ue) * (u0 + ue) - (uw + u0) * (uw + u0);
+        fux += s.alpha * (fabs(u0 + ue) * (u0 - ue) - fabs(uw + u0) * (uw - u0));
+        double fuy = vn * (u0 + un) - vs * (us + u0);
+        fuy += s.alpha * (fabs(vn) * (u0 - un) - fabs(vs) * (us - u0));
+        double fuz = wt * (u0 + ut) - wb * (ub + u0);
+        fuz += s.alpha * (fabs(wt) * (u0 - ut) - fabs(wb) * (ub - u0));
+        const double lapu = (ue - 2.0 * u0 + uw) * s.ix2 + (un - 2.0 * u0 + us) * s.iy2 +
+                            (ut - 2.0 * u0 + ub) * s.iz2;
+        const double rhsu = (q(0, 0, 0) - q(1, 0, 0)) * s.ix -
+                            0.25 * (fux * s.ix + fuy * s.iy + fuz * s.iz) + s.nu * lapu + s.fx;
+        const double r = u0 + dt * rhsu;
+        Uo[o] = r;
+        const unsigned long long bb = abs_bits(r);
+        mx[0] = bb > mx[0] ? bb : mx[0];
+      }
+      {  // y momentum, at the high y face
+        const double ve = v(1, 0, 0), vw = v(-1, 0, 0);
+        const double vnn = v(0, 1, 0), vss = v(0, -1, 0);
+        const double vt = v(0, 0, 1), vb = v(0, 0, -1);
+        const double ue2 = u(0, 0, 0) + u(0, 1, 0), uw2 = u(-1, 0, 0) + u(-1, 1, 0);
+        const double wt2 = w(0, 0, 0) + w(0, 1, 0), wb2 = w(0, 0, -1) + w(0, 1, -1);
+        double fvx = ue2 * (v0 + ve) - uw2 * (vw + v0);
+        fvx += s.alpha * (fabs(ue2) * (v0 - ve) - fabs(uw2) * (vw - v0));
+        double fvy = (v0 + vnn) * (v0 + vnn) - (vss + v0) * (vss + v0);
+        fvy += s.alpha * (fabs(v0 + vnn) * (v0 - vnn) - fabs(vss + v0) * (vss - v0));
+        double fvz = wt2 * (v0 + vt) - wb2 * (vb + v0);
+        fvz += s.alpha * (fabs(wt2) * (v0 - vt) - fabs(wb2) * (vb - v0));
+        const double lapv = (ve - 2.0 * v0 + vw) * s.ix2 + (vnn - 2.0 * v0 + vss) * s.iy2 +
+                            (vt - 2.0 * v0 + vb) * s.iz2;
+        const double rhsv = (q(0, 0, 0) - q(0, 1, 0)) * s.iy -
+                            0.25 * (fvx * s.ix + fvy * s.iy + fvz * s.iz) + s.nu * lapv + s.fy;
+        const double r = v0 + dt * rhsv;
+        Vo[o] = r;
+        const unsigned long long bb = abs_bits(r);
+        mx[1] = bb > mx[1] ? bb : mx[1];
+      }
+      {  // z momentum, at the high z face
+        const double we = w(1, 0, 0), ww = w(-1, 0, 0);
+        const double wn = w(0, 1, 0), ws = w(0, -1, 0);
+        const double wtt = w(0, 0, 1), wbb = w(0, 0, -1);
+        const double ue3 = u(0, 0, 0) + u(0, 0, 1), uw3 = u(-1, 0, 0) + u(-1, 0, 1);
+        const double vn3 = v(0, 0, 0) + v(0, 0, 1), vs3 = v(0, -1, 0) + v(0, -1, 1);
+        double fwx = ue3 * (w0 + we) - uw3 * (ww + w0);
+        fwx += s.alpha * (fabs(ue3) * (w0 - we) - fabs(uw3) * (ww - w0));
+        double fwy = vn3 * (w0 + wn) - vs3 * (ws + w0);
+        fwy += s.alpha * (fabs(vn3) * (w0 - wn) - fabs(vs3) * (ws - w0));
+        double fwz = (w0 + wtt) * (w0 + wtt) - (wbb + w0) * (wbb + w0);
+        fwz += s.alpha * (fabs(w0 + wtt) * (w0 - wtt) - fabs(wbb + w0) * (wbb - w0));
+        const double lapw = (we - 2.0 * w0 + ww) * s.ix2 + (wn - 2.0 * w0 + ws) * s.iy2 +
+                            (wtt - 2.0 * w0 + wbb) * s.iz2;
+        const double rhsw = (q(0, 0, 0) - q(0, 0, 1)) * s.iz -
+                            0.25 * (fwx * s.ix + fwy * s.iy + fwz * s.iz) + s.nu * lapw + s.fz;
+        const double r = w0 + dt * rhsw;
+        Wo[o] = r;
+        const unsigned long long bb = abs_bits(r);
+        mx[2] = bb > mx[2] ? bb : mx[2];
+      }
+#undef u
+#undef v
+#undef w
+#undef q
+    }
+  }
+  if (ctl) block_max_atomic<3>(mx, &ctl->acc[1]);
+}
+
+template <class View>
+void launch_update_velocity(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                            double dt, cudaStream_t st) {
+  if (nctas <= 0) return;
+  k_update_vel<View><<<nctas, dim3(kTX, kTY), 0, st>>>(vw, zc, c, ctl, dt);
+}
+template void launch_update_velocity<table_view>(const table_view&, int, int, const sf_consts&,
+                                                 sf_dev_ctl*, double, cudaStream_t);
+template void launch_update_velocity<direct_view>(const direct_view&, int, int, const sf_consts&,
+                                                  sf_dev_ctl*, double, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// DIVERGENCE (cfd.hpp:595-618) with max|divu| into acc[acc_slot]
+// ---------------------------------------------------------------------------
+template <class View>
+__global__ void __launch_bounds__(kTX* kTY) k_divergence(View vw, int zc, sf_consts s,
+                                                         sf_dev_ctl* ctl, int acc_slot,
+                                                         int predicated) {
+  if (predicated && pred_done(ctl)) return;
+  const tile_loc t = locate(vw.work(), vw.nitems, zc);
+  const sf_dev_block& B = vw.blk(t.blk);
+  const double* __restrict__ U = vw.ptr(t.blk, SF_VX, FRONT);
+  const double* __restrict__ V = vw.ptr(t.blk, SF_VY, FRONT);
+  const double* __restrict__ W = vw.ptr(t.blk, SF_VZ, FRONT);
+  double* __restrict__ D = vw.ptr(t.blk, SF_DIVU, FRONT);
+  const long long sx = B.sx, sxy = B.sx * B.sy;
+  unsigned long long mx[1] = {0ull};
+  if (t.act) {
+    for (long long k = t.k0; k < t.k1; ++k) {
+      const long long o = off(B, t.i, t.j, k);
+      double d = (__ldg(U + o) - __ldg(U + o - 1)) * s.ix;
+      d += (__ldg(V + o) - __ldg(V + o - sx)) * s.iy;
+      d += (__ldg(W + o) - __ldg(W + o - sxy)) * s.iz;
+      D[o] = d;
+      const unsigned long long bb = abs_bits(d);
+      mx[0] = bb > mx[0] ? bb : mx[0];
+    }
+  }
+  if (acc_slot >= 0) block_max_atomic<1>(mx, &ctl->acc[acc_slot]);
+}
+
+template <class View>
+void launch_divergence(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                       int acc_slot, int predicated, cudaStream_t st) {
+  if (nctas <= 0) return;
+  k_divergence<View><<<nctas, dim3(kTX, kTY), 0, st>>>(vw, zc, c, ctl, acc_slot, predicated);
+}
+template void launch_divergence<table_view>(const table_view&, int, int, const sf_consts&,
+                                            sf_dev_ctl*, int, int, cudaStream_t);
+template void launch_divergence<direct_view>(const direct_view&, int, int, const sf_consts&,
+                                             sf_dev_ctl*, int, int, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// PRESSURE_SWEEP (cfd.hpp:699-720), in place on p, vx, vy, vz
+// ---------------------------------------------------------------------------
+template <class View>
+__global__ void __launch_bounds__(kTX* kTY) k_sweep(View vw,
+                                                    int zc, sf_consts s, sf_dev_ctl* ctl,
+                                                    int predicated, int explicit_bc,
+                                                    double beta_arg, int color_arg,
+                                                    double dt_arg) {
+  if (predicated && pred_done(ctl)) return;
+  const tile_loc t = locate(vw.work(), vw.nitems, zc);
+  if (!t.act) return;
+  const sf_dev_block& B = vw.blk(t.blk);
+  const double* __restrict__ Dv = vw.ptr(t.blk, SF_DIVU, FRONT);
+  double* __restrict__ P = vw.ptr(t.blk, SF_P, FRONT);
+  double* __restrict__ U = vw.ptr(t.blk, SF_VX, FRONT);
+  double* __restrict__ V = vw.ptr(t.blk, SF_VY, FRONT);
+  double* __restrict__ W = vw.ptr(t.blk, SF_VZ, FRONT);
+  const double beta = explicit_bc ? beta_arg : ctl->beta;
+  const int color = explicit_bc ? color_arg : ctl->color;
+  const double dt = ctl ? ctl->dt : dt_arg;
+  const long long sx = B.sx, sxy = B.sx * B.sy;
+  const long long gi = B.lo[0] + t.i, gj = B.lo[1] + t.j;
+  const int bx = s.per[0] | ((gi > 0) & (gi < s.nm1[0]));
+  const int by = s.per[1] | ((gj > 0) & (gj < s.nm1[1]));
+  const int bxp = s.per[0] | (gi + 1 < s.nm1[0]);
+  const int byp = s.per[1] | (gj + 1 < s.nm1[1]);
+  for (long long k = t.k0; k < t.k1; ++k) {
+    const long long gk = B.lo[2] + k;
+    const long long o = off(B, t.i, t.j, k);
+    const int bz = s.per[2] | ((gk > 0) & (gk < s.nm1[2]));
+    const int bzp = s.per[2] | (gk + 1 < s.nm1[2]);
+    const double a0 = ((gi + gj + gk) & 1) == color ? 1.0 : 0.0;
+    const double a1 = ((gi + gj + gk + 1) & 1) == color ? 1.0 : 0.0;
+    const double d0 = -(beta * s.bscale[bx][by][bz]) * Dv[o] * a0;
+    const double ex = -(beta * s.bscale[bxp][by][bz]) * Dv[o + 1] * a1;
+    const double ey = -(beta * s.bscale[bx][byp][bz]) * Dv[o + sx] * a1;
+    const double ez = -(beta * s.bscale[bx][by][bzp]) * Dv[o + sxy] * a1;
+    P[o] = P[o] + d0;
+    U[o] = U[o] + dt * s.ix * (d0 - ex);
+    V[o] = V[o] + dt * s.iy * (d0 - ey);
+    W[o] = W[o] + dt * s.iz * (d0 - ez);
+  }
+}
+
+template <class View>
+void launch_pressure_sweep(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                           int predicated, const double* beta_color_dt, cudaStream_t st) {
+  if (nctas <= 0) return;
+  const int ex = beta_color_dt != nullptr;
+  k_sweep<View><<<nctas, dim3(kTX, kTY), 0, st>>>(
+      vw, zc, c, ctl, predicated, ex, ex ? beta_color_dt[0] : 0.0,
+      ex ? (int)beta_color_dt[1] : 0, ex ? beta_color_dt[2] : 0.0);
+}
+template void launch_pressure_sweep<table_view>(const table_view&, int, int, const sf_consts&,
+                                                sf_dev_ctl*, int, const double*, cudaStream_t);
+template void launch_pressure_sweep<direct_view>(const direct_view&, int, int, const sf_consts&,
+                                                 sf_dev_ctl*, int, const double*, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// Fused half-sweep (the inner loop of pressure_iteration, cfd.hpp:295-303):
+//   refresh(divu) [done by the previous half-sweep] ; PRESSURE_SWEEP ;
+//   color ^= 1 ; ++sweeps ; refresh(vx,vy,vz) ; DIVERGENCE ; r = max|divu| ;
+//   loop test.
+// One pass reads divu, p, vx, vy, vz and writes p, vx', vy', vz', divu' (80 B
+// per cell).  The velocity refresh is replaced by computing, per cell, the
+// swept values of its -x/-y/-z neighbours (for a ghost neighbour: the value
+// the refresh would deliver -- the neighbour block's swept cell, the pinned
+// wall value, or the outflow copy), so the new divergence needs no grid-wide
+// barrier.  Wall-normal planes are stored pinned, as the refresh leaves them
+// (exchange.hpp:288-316).  Velocities and divu ping-pong FRONT <-> ALT; the
+// last CTA swaps the table, flips the colour, counts the sweep and evaluates
+// `residual > tolerance && sweeps < max_sweeps`.
+// ---------------------------------------------------------------------------
+struct sweep_ctx {
+  double mb[2][2][2];  // -(beta * bscale[..]) exactly as cfd.hpp:712-715 forms it
+  int color;
+  long long nm1[3];
+  int per[3];
+};
+
+__device__ __forceinline__ int bit_in(const sweep_ctx& x, int a, long long g) {
+  return x.per[a] | ((g > 0) & (g < x.nm1[a]));
+}
+__device__ __forceinline__ int bit_next(const sweep_ctx& x, int a, long long g) {
+  return x.per[a] | (g + 1 < x.nm1[a]);
+}
+__device__ __forceinline__ double act0(const sweep_ctx& x, long long gsum) {
+  return ((gsum & 1) == x.color) ? 1.0 : 0.0;
+}
+
+__global__ void __launch_bounds__(kTX* kTY) k_sweep_div(sf_dev_table* __restrict__ tab,
+                                                        const sf_work* __restrict__ items,
+                                                        int nitems, int zc, sf_consts s,
+                                                        sf_dev_ctl* ctl, sf_host_flag* hflag,
+                                                        unsigned int total_ctas) {
+  if (pred_done(ctl)) return;
+  const tile_loc t = locate(items, nitems, zc);
+  const sf_dev_block& B = tab->blk[t.blk];
+  const double* __restrict__ D = tab->ptr[t.blk][SF_DIVU][FRONT];
+  double* __restrict__ Dn = tab->ptr[t.blk][SF_DIVU][ALT];
+  double* __restrict__ P = tab->ptr[t.blk][SF_P][FRONT];
+  const double* __restrict__ U = tab->ptr[t.blk][SF_VX][FRONT];
+  const double* __restrict__ V = tab->ptr[t.blk][SF_VY][FRONT];
+  const double* __restrict__ W = tab->ptr[t.blk][SF_VZ][FRONT];
+  double* __restrict__ Un = tab->ptr[t.blk][SF_VX][ALT];
+  double* __restrict__ Vn = tab->ptr[t.blk][SF_VY][ALT];
+  double* __restrict__ Wn = tab->ptr[t.blk][SF_VZ][ALT];
+  const double beta = ctl->beta, dt = ctl->dt;
+  sweep_ctx x;
+  x.color = ctl->color;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) x.mb[a][b][c] = -(beta * s.bscale[a][b][c]);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    x.nm1[a] = s.nm1[a];
+    x.per[a] = s.per[a];
+  }
+  // (dt * ix) exactly as s.dt * s.ix in cfd.hpp:717-719
+  const double cu = dt * s.ix, cv = dt * s.iy, cw = dt * s.iz;
+  unsigned long long rmax[1] = {0ull};
+
+  if (t.act) {
+    const long long n0 = B.n[0], n1 = B.n[1], n2 = B.n[2];
+    const long long sx = B.sx, sxy = B.sx * B.sy;
+    const long long i = t.i, j = t.j;
+    const long long gi = B.lo[0] + i, gj = B.lo[1] + j;
+    const int bx = bit_in(x, 0, gi), bxp = bit_next(x, 0, gi);
+    const int by = bit_in(x, 1, gj), byp = bit_next(x, 1, gj);
+    // the -x neighbour column (owned, or the cell behind the ghost)
+    const long long gim = i > 0 ? gi - 1 : B.nb_ghost_gidx[0];
+    const int bxm = bit_in(x, 0, gim), bxpm = bit_next(x, 0, gim);
+    const long long gjm = j > 0 ? gj - 1 : B.nb_ghost_gidx[2];
+    const int bym = bit_in(x, 1, gjm), bypm = bit_next(x, 1, gjm);
+    const int fxl = B.face[0], fxh = B.face[1], fyl = B.face[2], fyh = B.face[3];
+    const int fzl = B.face[4], fzh = B.face[5];
+    // pinned high wall planes (exchange.hpp:296-315)
+    const bool pin_u = (fxh == FACE_WALL || fxh == FACE_SYM) && i == n0 - 1;
+    const bool pin_v = (fyh == FACE_WALL || fyh == FACE_SYM) && j == n1 - 1;
+    const double pv_u = fxh == FACE_WALL ? B.fvel[1][0] : 0.0;
+    const double pv_v = fyh == FACE_WALL ? B.fvel[3][1] : 0.0;
+    const double pv_w = fzh == FACE_WALL ? B.fvel[5][2] : 0.0;
+    const bool pinz_face = (fzh == FACE_WALL || fzh == FACE_SYM);
+
+    long long o = off(B, i, j, t.k0);
+    double wm_new;  // swept w of the -z neighbour
+    double dC = D[o];
+    {
+      const long long k = t.k0;
+      const long long gk = B.lo[2] + k;
+      const int bz = bit_in(x, 2, gk);
+      (void)bz;
+      if (k > 0) {
+        const long long gkm = gk - 1;
+        const int bzm = bit_in(x, 2, gkm), bzpm = bit_next(x, 2, gkm);
+        const double a0m = act0(x, gi + gj + gkm), a1m = 1.0 - a0m;
+        const double d0m = x.mb[bx][by][bzm] * D[o - sxy] * a0m;
+        const double ezm = x.mb[bx][by][bzpm] * dC * a1m;
+        wm_new = W[o - sxy] + cw * (d0m - ezm);
+      } else if (fzl == FACE_PROC || fzl == FACE_SELF) {
+        const long long gkm = B.nb_ghost_gidx[4];
+        const int bzm = bit_in(x, 2, gkm), bzpm = bit_next(x, 2, gkm);
+        const double a0m = act0(x, gi + gj + gkm), a1m = 1.0 - a0m;
+        const double d0m = x.mb[bx][by][bzm] * D[o - sxy] * a0m;
+        const double ezm = x.mb[bx][by][bzpm] * dC * a1m;
+        wm_new = W[o - sxy] + cw * (d0m - ezm);
+      } else {
+        wm_new = W[o - sxy];  // wall / symmetry pin; outflow fixed up below
+      }
+    }
+    for (long long k = t.k0; k < t.k1; ++k, o += sxy) {
+      const long long gk = B.lo[2] + k;
+      const int bz = bit_in(x, 2, gk), bzp = bit_next(x, 2, gk);
+      const double dXp = D[o + 1], dYp = D[o + sx], dZp = D[o + sxy];
+      const double dXm = D[o - 1], dYm = D[o - sx];
+      const double p0 = P[o], u0 = U[o], v0 = V[o], w0 = W[o];
+      const double a0 = act0(x, gi + gj + gk), a1 = 1.0 - a0;
+      // this cell's sweep (cfd.hpp:712-719)
+      const double d0 = x.mb[bx][by][bz] * dC * a0;
+      const double ex = x.mb[bxp][by][bz] * dXp * a1;
+      const double ey = x.mb[bx][byp][bz] * dYp * a1;
+      const double ez = x.mb[bx][by][bzp] * dZp * a1;
+      P[o] = p0 + d0;
+      double un = u0 + cu * (d0 - ex);
+      double vn = v0 + cv * (d0 - ey);
+      double wn = w0 + cw * (d0 - ez);
+      if (pin_u) un = pv_u;
+      if (pin_v) vn = pv_v;
+      if (pinz_face && k == n2 - 1) wn = pv_w;
+      // swept -x neighbour of u
+      double umn;
+      if (i > 0 || fxl == FACE_PROC || fxl == FACE_SELF) {
+        const double a0m = i > 0 ? a1 : act0(x, gim + gj + gk);
+        const double a1m = 1.0 - a0m;
+        const double d0m = x.mb[bxm][by][bz] * dXm * a0m;
+        const double exm = x.mb[bxpm][by][bz] * dC * a1m;
+        umn = U[o - 1] + cu * (d0m - exm);
+      } else if (fxl == FACE_OUT) {
+        umn = un;
+      } else {
+        umn = U[o - 1];
+      }
+      // swept -y neighbour of v
+      double vmn;
+      if (j > 0 || fyl == FACE_PROC || fyl == FACE_SELF) {
+        const double a0m = j > 0 ? a1 : act0(x, gi + gjm + gk);
+        const double a1m = 1.0 - a0m;
+        const double d0m = x.mb[bx][bym][bz] * dYm * a0m;
+        const double eym = x.mb[bx][bypm][bz] * dC * a1m;
+        vmn = V[o - sx] + cv * (d0m - eym);
+      } else if (fyl == FACE_OUT) {
+        vmn = vn;
+      } else {
+        vmn = V[o - sx];
+      }
+      if (k == 0 && fzl == FACE_OUT) wm_new = wn;
+      // DIVERGENCE on the refreshed velocities (cfd.hpp:605-608)
+      double dd = (un - umn) * s.ix;
+      dd += (vn - vmn) * s.iy;
+      dd += (wn - wm_new) * s.iz;
+      Un[o] = un;
+      Vn[o] = vn;
+      Wn[o] = wn;
+      Dn[o] = dd;
+      // ghost values the next half-sweep reads (depth 1)
+      if (i == 0) Un[o - 1] = umn;
+      if (j == 0) Vn[o - sx] = vmn;
+      if (k == 0) Wn[o - sxy] = wm_new;
+      if (i == 0) {
+        if (fxl == FACE_WALL || fxl == FACE_SYM || fxl == FACE_OUT) Dn[o - 1] = dd;
+        if (fxh == FACE_SELF) Dn[o + n0] = dd;
+      }
+      if (i == n0 - 1) {
+        if (fxh == FACE_WALL || fxh == FACE_SYM || fxh == FACE_OUT) Dn[o + 1] = dd;
+        if (fxl == FACE_SELF) Dn[o - n0] = dd;
+      }
+      if (j == 0) {
+        if (fyl == FACE_WALL || fyl == FACE_SYM || fyl == FACE_OUT) Dn[o - sx] = dd;
+        if (fyh == FACE_SELF) Dn[o + n1 * sx] = dd;
+      }
+      if (j == n1 - 1) {
+        if (fyh == FACE_WALL || fyh == FACE_SYM || fyh == FACE_OUT) Dn[o + sx] = dd;
+        if (fyl == FACE_SELF) Dn[o - n1 * sx] = dd;
+      }
+      if (k == 0) {
+        if (fzl == FACE_WALL || fzl == FACE_SYM || fzl == FACE_OUT) Dn[o - sxy] = dd;
+        if (fzh == FACE_SELF) Dn[o + n2 * sxy] = dd;
+      }
+      if (k == n2 - 1) {
+        if (fzh == FACE_WALL || fzh == FACE_SYM || fzh == FACE_OUT) Dn[o + sxy] = dd;
+        if (fzl == FACE_SELF) Dn[o - n2 * sxy] = dd;
+      }
+      const unsigned long long bb = abs_bits(dd);
+      rmax[0] = bb > rmax[0] ? bb : rmax[0];
+      // march: this plane's swept w is the next plane's -z neighbour
+      wm_new = wn;
+      dC = dZp;
+    }
+  }
+  block_max_atomic<1>(rmax, &ctl->acc[0]);
+  if (last_cta(&ctl->ctas_done, total_ctas)) {
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      __threadfence();
+      const unsigned long long rb = *reinterpret_cast<volatile unsigned long long*>(&ctl->acc[0]);
+      const double residual = bits_to_max(rb);
+      ctl->acc[0] = 0ull;
+      ctl->ctas_done = 0u;
+      ctl->residual = residual;
+      ctl->color ^= 1;
+      const int sweeps = ctl->sweeps + 1;
+      ctl->sweeps = sweeps;
+      const int more = (residual > ctl->tolerance) && (sweeps < ctl->max_sweeps);
+      ctl->done = more ? 0 : 1;
+      for (int b = 0; b < tab->nblocks; ++b) {
+        for (int f = 0; f < 5; ++f) {
+          if (f == SF_P) continue;
+          double* tmp = tab->ptr[b][f][FRONT];
+          tab->ptr[b][f][FRONT] = tab->ptr[b][f][ALT];
+          tab->ptr[b][f][ALT] = tmp;
+        }
+      }
+      if (hflag) {
+        hflag->sweeps = sweeps;
+        hflag->residual = residual;
+        hflag->done = more ? 0 : 1;
+        hflag->color = ctl->color;
+        __threadfence_system();
+      }
+    }
+  }
+}
+
+void launch_sweep_div(const table_view& vw, int nctas, int zc, const sf_consts& c,
+                      sf_dev_ctl* ctl, sf_host_flag* hflag, cudaStream_t st) {
+  if (nctas <= 0) return;
+  k_sweep_div<<<nctas, dim3(kTX, kTY), 0, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
+                                                 (unsigned)nctas);
+}
+
+// ---------------------------------------------------------------------------
+// reductions (reductions.hpp:28-90)
+// ---------------------------------------------------------------------------
+template <class View>
+__global__ void __launch_bounds__(kTX* kTY) k_reduce_max(View vw, int zc, int f0, int f1,
+                                                         int f2, int nfields, int diff,
+                                                         unsigned long long* acc) {
+  const tile_loc t = locate(vw.work(), vw.nitems, zc);
+  const sf_dev_block& B = vw.blk(t.blk);
+  unsigned long long mx[3] = {0ull, 0ull, 0ull};
+  const int fl[3] = {f0, f1, f2};
+  if (t.act) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (q >= nfields) break;
+      const double* __restrict__ F = vw.ptr(t.blk, fl[q], FRONT);
+      const double* __restrict__ Bk = vw.ptr(t.blk, fl[q], BACK);
+      for (long long k = t.k0; k < t.k1; ++k) {
+        const long long o = off(B, t.i, t.j, k);
+        const double a = diff ? fabs(__ldg(F + o) - __ldg(Bk + o)) : fabs(__ldg(F + o));
+        const unsigned long long bb = abs_bits(a);
+        mx[q] = bb > mx[q] ? bb : mx[q];
+      }
+    }
+  }
+  if (nfields == 1) {
+    unsigned long long m1[1] = {mx[0]};
+    block_max_atomic<1>(m1, acc);
+  } else {
+    block_max_atomic<3>(mx, acc);
+  }
+}
+
+template <class View>
+void launch_reduce_max(const View& vw, int nctas, int zc, const int* fields, int nfields, int diff,
+                       unsigned long long* acc, cudaStream_t st) {
+  if (nctas <= 0) return;
+  k_reduce_max<View><<<nctas, dim3(kTX, kTY), 0, st>>>(
+      vw, zc, fields[0], nfields > 1 ? fields[1] : 0, nfields > 2 ? fields[2] : 0, nfields, diff,
+      acc);
+}
+template void launch_reduce_max<table_view>(const table_view&, int, int, const int*, int, int,
+                                            unsigned long long*, cudaStream_t);
+template void launch_reduce_max<direct_view>(const direct_view&, int, int, const int*, int, int,
+                                             unsigned long long*, cudaStream_t);
+
+// Deterministic sums: one partial per CTA (x-fastest within the tile), the
+// host folds partials in CTA order.  Not the reference's serial order, so
+// sums agree to rounding, not bitwise (they are off the hot path:
+// kinetic_energy / taylor_green_error, cfd.hpp:357-401).
+template <class View>
+__global__ void __launch_bounds__(kTX* kTY) k_reduce_sum(View vw, int zc, int field, int square,
+                                                         double* partials) {
+  const tile_loc t = locate(vw.work(), vw.nitems, zc);
+  const sf_dev_block& B = vw.blk(t.blk);
+  const double* __restrict__ F = vw.ptr(t.blk, field, FRONT);
+  double acc = 0.0;
+  if (t.act)
+    for (long long k = t.k0; k < t.k1; ++k) {
+      const double x = __ldg(F + off(B, t.i, t.j, k));
+      acc += square ? x * x : x;
+    }
+  __shared__ double red[kTX * kTY];
+  const int tid = threadIdx.y * kTX + threadIdx.x;
+  red[tid] = acc;
+  __syncthreads();
+  for (int w = kTX * kTY / 2; w > 0; w >>= 1) {
+    if (tid < w) red[tid] += red[tid + w];
+    __syncthreads();
+  }
+  if (tid == 0) partials[blockIdx.x] = red[0];
+}
+
+void launch_reduce_sum(const table_view& vw, int nctas, int zc, int field, int square,
+                       double* partials, cudaStream_t st) {
+  if (nctas <= 0) return;
+  k_reduce_sum<table_view><<<nctas, dim3(kTX, kTY), 0, st>>>(vw, zc, field, square, partials);
+}
+
+// ---------------------------------------------------------------------------
+// control
+// ---------------------------------------------------------------------------
+__device__ void set_beta(sf_dev_ctl* ctl, const sf_consts& s) {
+  // beta = omega / (2 dt (ix2 + iy2 + iz2))   (cfd.hpp:291)
+  ctl->beta = s.omega / (2.0 * ctl->dt * (s.ix2 + s.iy2 + s.iz2));
+}
+
+__global__ void k_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, int op, double arg,
+                      int f, int sa, int sb, sf_consts s, int predicated) {
+  if (predicated && pred_done(ctl)) return;
+  switch (op) {
+    case CTL_DT_FROM_ACC: {  // compute_dt (cfd.hpp:264-273)
+      double dt = 1.0 / (2.0 * s.nu * (s.ix2 + s.iy2 + s.iz2));
+      const double m[3] = {bits_to_max(ctl->acc[0]), bits_to_max(ctl->acc[1]),
+                           bits_to_max(ctl->acc[2])};
+      for (int a = 0; a < 3; ++a) {
+        ctl->vmax[a] = m[a];
+        if (m[a] > 0.0) {
+          const double c = s.spacing[a] / m[a];
+          dt = c < dt ? c : dt;  // std::min(dt, c)
+        }
+        ctl->acc[a] = 0ull;
+      }
+      ctl->dt = s.sigma * dt;
+      set_beta(ctl, s);
+      if (hflag) {
+        hflag->dt = ctl->dt;
+        __threadfence_system();
+      }
+      break;
+    }
+    case CTL_SET_DT:
+      ctl->dt = arg;
+      set_beta(ctl, s);
+      if (hflag) {
+        hflag->dt = ctl->dt;
+        __threadfence_system();
+      }
+      break;
+    case CTL_RESET_CLOCK:
+      ctl->color = 0;
+      ctl->abort_field = -1;
+      if (hflag) {
+        hflag->color = 0;
+        hflag->abort_field = -1;
+        __threadfence_system();
+      }
+      break;
+    case CTL_BEGIN_ITERATION:
+      ctl->sweeps = 0;
+      ctl->residual = 0.0;
+      ctl->acc[0] = 0ull;
+      ctl->ctas_done = 0u;
+      ctl->done = ctl->abort_field >= 0 ? 1 : 0;
+      ctl->max_sweeps = s.max_sweeps;
+      ctl->tolerance = s.tolerance;
+      if (hflag) {
+        hflag->done = ctl->done;
+        hflag->sweeps = 0;
+        hflag->residual = 0.0;
+        __threadfence_system();
+      }
+      break;
+    case CTL_AFTER_SWEEP:
+      ctl->color ^= 1;
+      ctl->sweeps += 1;
+      if (hflag) {
+        hflag->color = ctl->color;
+        __threadfence_system();
+      }
+      break;
+    case CTL_FINISH_SWEEP: {
+      const double r = bits_to_max(ctl->acc[0]);
+      ctl->acc[0] = 0ull;
+      ctl->residual = r;
+      const int more = (r > ctl->tolerance) && (ctl->sweeps < ctl->max_sweeps);
+      ctl->done = more ? 0 : 1;
+      if (hflag) {
+        hflag->sweeps = ctl->sweeps;
+        hflag->residual = r;
+        hflag->done = ctl->done;
+        __threadfence_system();
+      }
+      break;
+    }
+    case CTL_CHECK_FINITE: {
+      ctl->abort_field = -1;
+      for (int a = 0; a < 3; ++a) {
+        const double m = bits_to_max(ctl->acc[1 + a]);
+        ctl->acc[1 + a] = 0ull;
+        ctl->vmax[a] = m;
+        if (ctl->abort_field < 0 && !isfinite(m)) ctl->abort_field = a;
+      }
+      if (hflag) {
+        hflag->abort_field = ctl->abort_field;
+        __threadfence_system();
+      }
+      break;
+    }
+    case CTL_CLEAR_ACC:
+      for (int a = 0; a < 8; ++a) ctl->acc[a] = 0ull;
+      ctl->ctas_done = 0u;
+      break;
+    case CTL_SWAP:
+      for (int b = 0; b < tab->nblocks; ++b) {
+        double* tmp = tab->ptr[b][f][sa];
+        tab->ptr[b][f][sa] = tab->ptr[b][f][sb];
+        tab->ptr[b][f][sb] = tmp;
+      }
+      break;
+  }
+}
+
+void launch_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, int op, double arg,
+                int f, int a, int b, const sf_consts& c, int predicated, cudaStream_t st) {
+  k_ctl<<<1, 1, 0, st>>>(tab, ctl, hflag, op, arg, f, a, b, c, predicated);
+}
+
+// ---------------------------------------------------------------------------
+// raw box copies (level-2 ABI, gather / scatter)
+// ---------------------------------------------------------------------------
+__global__ void k_copy_box(const double* __restrict__ src, long long s_base, long long s_sx,
+                           long long s_sy, double* __restrict__ dst, long long d_base,
+                           long long d_sx, long long d_sy, long long l0, long long l1,
+                           long long l2, long long n0, long long n1, long long n2, long long m0,
+                           long long m1, long long m2) {
+  const long long total = n0 * n1 * n2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const long long k = e / (n0 * n1), r = e - k * n0 * n1, j = r / n0, i = r - j * n0;
+    dst[d_base + ((m2 + k) * d_sy + (m1 + j)) * d_sx + (m0 + i)] =
+        src[s_base + ((l2 + k) * s_sy + (l1 + j)) * s_sx + (l0 + i)];
+  }
+}
+
+void launch_copy_box(const double* src, long long s_base, long long s_sx, long long s_sy,
+                     double* dst, long long d_base, long long d_sx, long long d_sy,
+                     const long long lo[3], const long long dims[3], const long long dlo[3],
+                     cudaStream_t st) {
+  const long long total = dims[0] * dims[1] * dims[2];
+  if (total <= 0) return;
+  long long nb = (total + 255) / 256;
+  if (nb > 148 * 16) nb = 148 * 16;
+  k_copy_box<<<(unsigned)nb, 256, 0, st>>>(src, s_base, s_sx, s_sy, dst, d_base, d_sx, d_sy,
+                                            lo[0], lo[1], lo[2], dims[0], dims[1], dims[2],
+                                            dlo[0], dlo[1], dlo[2]);
+}
+
+__global__ void k_fill_box(double* __restrict__ dst, long long base, long long sx, long long sy,
+                           long long l0, long long l1, long long l2, long long n0, long long n1,
+                           long long n2, double v) {
+  const long long total = n0 * n1 * n2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const long long k = e / (n0 * n1), r = e - k * n0 * n1, j = r / n0, i = r - j * n0;
+    dst[base + ((l2 + k) * sy + (l1 + j)) * sx + (l0 + i)] = v;
+  }
+}
+
+void launch_fill_box(double* dst, long long base, long long sx, long long sy, const long long lo[3],
+                     const long long dims[3], double v, cudaStream_t st) {
+  const long long total = dims[0] * dims[1] * dims[2];
+  if (total <= 0) return;
+  long long nb = (total + 255) / 256;
+  if (nb > 148 * 16) nb = 148 * 16;
+  k_fill_box<<<(unsigned)nb, 256, 0, st>>>(dst, base, sx, sy, lo[0], lo[1], lo[2], dims[0],
+                                            dims[1], dims[2], v);
+}
+
+// owned cells <-> a global x-fastest array (grid::gather / scatter, io.hpp:25-65)
+void launch_gather_owned(const double* src, long long base, long long sx, long long sy,
+                         const long long n[3], const long long lo[3], const long long N[3],
+                         double* dst_global, int to_field, cudaStream_t st) {
+  const long long zero[3] = {0, 0, 0};
+  if (!to_field)
+    launch_copy_box(src, base, sx, sy, dst_global, 0, N[0], N[1], zero, n, lo, st);
+  else
+    launch_copy_box(dst_global, 0, N[0], N[1], const_cast<double*>(src), base, sx, sy, lo, n, zero,
+                    st);
+}
+
+}  // namespace sfb

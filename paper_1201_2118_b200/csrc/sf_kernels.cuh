@@ -1,0 +1,70 @@
+// sf_kernels.cuh -- launch interface between the host driver and the kernels.
+#pragma once
+
+#include "sf_device.cuh"
+
+namespace sfb {
+
+// One ghost-refresh task: a copy between blocks (one message of
+// exchange.hpp:165-224) or one physical face fill (bc_face, :231-480).
+struct sf_task {
+  int type;  // 0 copy, 1 bc
+  int field;
+  int src_blk, dst_blk;
+  long long lo[3];    // copy: source box (src-local); bc: tangential box (axis entry unused)
+  long long dims[3];  // copy: box extents; bc: tangential extents (axis entry 1)
+  long long dlo[3];   // copy: destination lo (dst-local)
+  long long count;    // elements (copy) or lines (bc)
+  int axis, side, normal, velocity, kind, scope;
+  double v;           // wall velocity component (normal pin / tangential reflection)
+};
+
+// Tile shapes (threads = TX x TY; each thread marches z over a chunk).
+constexpr int kTX = 32;
+constexpr int kTY = 8;
+
+template <class View>
+void launch_tasks(const View& vw, const sf_task* tasks, int ntasks, long long max_count,
+                  const sf_dev_ctl* pred, cudaStream_t st);
+template <class View>
+void launch_update_velocity(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                            double dt, cudaStream_t st);
+template <class View>
+void launch_divergence(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                       int acc_slot, int predicated, cudaStream_t st);
+// beta_color_dt: null = beta, colour and dt from ctl; else {beta, colour, dt}
+template <class View>
+void launch_pressure_sweep(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                           int predicated, const double* beta_color_dt, cudaStream_t st);
+void launch_sweep_div(const table_view& vw, int nctas, int zc, const sf_consts& c,
+                      sf_dev_ctl* ctl, sf_host_flag* hflag, cudaStream_t st);
+template <class View>
+void launch_reduce_max(const View& vw, int nctas, int zc, const int* fields, int nfields, int diff,
+                       unsigned long long* acc, cudaStream_t st);
+void launch_reduce_sum(const table_view& vw, int nctas, int zc, int field, int square,
+                       double* partials, cudaStream_t st);
+// Single-thread control updates.
+enum ctl_op {
+  CTL_DT_FROM_ACC = 0,       // compute_dt from acc[0..2] (cfd.hpp:264-273), beta (cfd.hpp:291)
+  CTL_SET_DT = 1,            // dt = arg, beta from dt
+  CTL_BEGIN_ITERATION = 2,   // sweeps = 0, done = abort, residual = 0, acc[0] = 0
+  CTL_AFTER_SWEEP = 3,       // unfused loop: color ^= 1, ++sweeps (cfd.hpp:299-300)
+  CTL_FINISH_SWEEP = 4,      // unfused loop: residual from acc[0], done test (cfd.hpp:302-303)
+  CTL_CHECK_FINITE = 5,      // NaN guard after UPDATE_VELOCITY from acc[1..3] (cfd.hpp:278-281)
+  CTL_CLEAR_ACC = 6,
+  CTL_SWAP = 7,              // swap slots (a, b) of field f in every block
+  CTL_RESET_CLOCK = 8,       // colour = 0, abort cleared (cfd.hpp:733-738)
+};
+void launch_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, int op, double arg,
+                int f, int a, int b, const sf_consts& c, int predicated, cudaStream_t st);
+void launch_copy_box(const double* src, long long s_base, long long s_sx, long long s_sy,
+                     double* dst, long long d_base, long long d_sx, long long d_sy,
+                     const long long lo[3], const long long dims[3], const long long dlo[3],
+                     cudaStream_t st);
+void launch_fill_box(double* dst, long long base, long long sx, long long sy, const long long lo[3],
+                     const long long dims[3], double v, cudaStream_t st);
+void launch_gather_owned(const double* src, long long base, long long sx, long long sy,
+                         const long long n[3], const long long lo[3], const long long N[3],
+                         double* dst_global, int to_field /* 1 = scatter */, cudaStream_t st);
+
+}  // namespace sfb

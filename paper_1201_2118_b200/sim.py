@@ -1,0 +1,328 @@
+"""Python face of the device simulation: the cfd::simulation API (cfd.hpp:173-766)
+and the exec::executor operations on its fields (executor.hpp:477-862), over
+the C ABI.  All compute runs in the CUDA library; this module only marshals.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+FIELDS = ("vx", "vy", "vz", "p", "divu")
+REGIONS = {"all": 0, "interior": 1, "boundary": 2}
+REDUCE_OPS = {"max_abs": 0, "sum": 1, "sum_sq": 2, "max_abs_diff": 3}
+
+
+@dataclass
+class SolverConfig:
+    """cfd::solver_config (cfd.hpp:43-67)."""
+
+    extents: Sequence[int] = (33, 33, 3)
+    spacing: Sequence[float] | None = None  # default: unit box (cfd::unit_box, cfd.hpp:69-74)
+    periodic: Sequence[bool] = (False, False, False)
+    reynolds: float = 100.0
+    sigma: float = 0.5
+    tolerance: float = 1e-6
+    omega: float = 1.7
+    max_sweeps: int = 500
+    symmetry_z: bool = True
+    output_cadence: int = 0
+
+    def to_c(self) -> L.SolverConfig:
+        c = L.SolverConfig()
+        sp = self.spacing or [1.0 / float(n) for n in self.extents]
+        for a in range(3):
+            c.extents[a] = int(self.extents[a])
+            c.spacing[a] = float(sp[a])
+            c.origin[a] = 0.0
+            c.periodic[a] = 1 if self.periodic[a] else 0
+        c.reynolds, c.sigma, c.tolerance, c.omega = self.reynolds, self.sigma, self.tolerance, self.omega
+        c.max_sweeps = int(self.max_sweeps)
+        c.symmetry_z = 1 if self.symmetry_z else 0
+        c.output_cadence = int(self.output_cadence)
+        return c
+
+
+@dataclass
+class FluidParams:
+    """cfd::fluid_params (cfd.hpp:29-41)."""
+
+    viscosity: float = 0.01
+    density: float = 1.0
+    body_force: Sequence[float] = (0.0, 0.0, 0.0)
+    lid_speed: float = 1.0
+    blend: float = 0.0
+
+    def to_c(self) -> L.FluidParams:
+        p = L.FluidParams()
+        p.viscosity, p.density = self.viscosity, self.density
+        for a in range(3):
+            p.body_force[a] = float(self.body_force[a])
+        p.lid_speed, p.blend = self.lid_speed, self.blend
+        return p
+
+
+def cavity_fluid(cfg: SolverConfig, alpha: float = 0.0) -> FluidParams:
+    """cfd::cavity_fluid (cfd.hpp:78-84)."""
+    return FluidParams(viscosity=1.0 * 1.0 / cfg.reynolds, lid_speed=1.0, blend=alpha)
+
+
+@dataclass
+class StepStats:
+    dt: float
+    sweeps: int
+    residual: float
+
+
+def _cstrs(names: Iterable[str]):
+    ns = [n.encode() for n in names]
+    arr = (C.c_char_p * max(1, len(ns)))(*ns)
+    return arr, len(ns)
+
+
+class Simulation:
+    """Device-resident cfd::simulation.  ``workers`` grid components of
+    grid::decompose() live on ``device``; ``fused`` selects the fused
+    sweep+divergence half-sweep (default) or the reference's unfused dataflow."""
+
+    def __init__(self, cfg: SolverConfig, par: FluidParams, workers: int = 1, mode: str = "plain",
+                 tile: Sequence[int] = (0, 0, 0), ghost: int = 1, form: str = "rows",
+                 device: int = 0, fused: bool = True):
+        self._h = None
+        self.cfg, self.par = cfg, par
+        self._lib = L.lib()
+        opt = L.SimOptions()
+        self._lib.sf_sim_options_default(C.byref(opt))
+        opt.workers, opt.mode = int(workers), (1 if mode == "overlap" else 0)
+        for a in range(3):
+            opt.tile[a] = int(tile[a])
+        opt.ghost, opt.form, opt.device, opt.fused = int(ghost), (1 if form == "points" else 0), int(device), int(bool(fused))
+        self._ccfg, self._cpar, self._opt = cfg.to_c(), par.to_c(), opt
+        h = C.c_void_p()
+        L.check(self._lib.sf_sim_create(C.byref(self._ccfg), C.byref(self._cpar), C.byref(opt), C.byref(h)))
+        self._h = h
+        self.extents = tuple(int(x) for x in cfg.extents)
+        self.workers = int(workers)
+
+    # -- lifetime ----------------------------------------------------------
+    def close(self) -> None:
+        if self._h:
+            self._lib.sf_sim_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- initial states (cfd.hpp:229-257) -----------------------------------
+    def init_cavity(self):
+        L.check(self._lib.sf_sim_init_cavity(self._h))
+
+    def init_uniform(self, c):
+        L.check(self._lib.sf_sim_init_uniform(self._h, *map(float, c)))
+
+    def init_taylor_green(self):
+        L.check(self._lib.sf_sim_init_taylor_green(self._h))
+
+    # -- the time step (cfd.hpp:264-321) ------------------------------------
+    def compute_dt(self) -> float:
+        v = C.c_double()
+        L.check(self._lib.sf_sim_compute_dt(self._h, C.byref(v)))
+        return v.value
+
+    def provisional(self, dt: float):
+        L.check(self._lib.sf_sim_provisional(self._h, float(dt)))
+
+    def pressure_iteration(self, dt: float):
+        s, r = C.c_int(), C.c_double()
+        L.check(self._lib.sf_sim_pressure_iteration(self._h, float(dt), C.byref(s), C.byref(r)))
+        return s.value, r.value
+
+    def step(self) -> StepStats:
+        st = L.StepStats()
+        L.check(self._lib.sf_sim_step(self._h, C.byref(st)))
+        return StepStats(st.dt, st.sweeps, st.residual)
+
+    def advance(self, n: int) -> StepStats:
+        st = L.StepStats()
+        L.check(self._lib.sf_sim_advance(self._h, int(n), C.byref(st)))
+        return StepStats(st.dt, st.sweeps, st.residual)
+
+    @property
+    def time(self) -> float:
+        return self._lib.sf_sim_time(self._h)
+
+    @property
+    def step_count(self) -> int:
+        return self._lib.sf_sim_step_count(self._h)
+
+    @property
+    def pending_color(self) -> int:
+        return self._lib.sf_sim_pending_color(self._h)
+
+    # -- diagnostics (cfd.hpp:342-363) --------------------------------------
+    def max_divergence(self) -> float:
+        v = C.c_double()
+        L.check(self._lib.sf_sim_max_divergence(self._h, C.byref(v)))
+        return v.value
+
+    def steady_delta(self) -> float:
+        v = C.c_double()
+        L.check(self._lib.sf_sim_steady_delta(self._h, C.byref(v)))
+        return v.value
+
+    def kinetic_energy(self) -> float:
+        v = C.c_double()
+        L.check(self._lib.sf_sim_kinetic_energy(self._h, C.byref(v)))
+        return v.value
+
+    # -- data movement (io.hpp:25-65, bench.hpp:24-39) -----------------------
+    @property
+    def cells(self) -> int:
+        nx, ny, nz = self.extents
+        return nx * ny * nz
+
+    def scatter(self, name: str, data) -> None:
+        if hasattr(data, "is_cuda") and data.is_cuda:
+            t = data.contiguous()
+            L.check(self._lib.sf_sim_scatter_device(self._h, name.encode(), C.c_void_p(t.data_ptr()), t.numel()))
+            return
+        a = np.ascontiguousarray(data, dtype=np.float64).reshape(-1)
+        if hasattr(data, "data_ptr") and hasattr(data, "is_pinned") and data.is_contiguous() and data.dtype.itemsize == 8:
+            ptr, n = data.data_ptr(), data.numel()
+        else:
+            ptr, n = a.ctypes.data, a.size
+        L.check(self._lib.sf_sim_scatter(self._h, name.encode(), C.c_void_p(ptr), n))
+
+    def gather(self, name: str, out=None) -> np.ndarray:
+        nx, ny, nz = self.extents
+        if out is not None and hasattr(out, "is_cuda") and out.is_cuda:
+            L.check(self._lib.sf_sim_gather_device(self._h, name.encode(), C.c_void_p(out.data_ptr()), out.numel()))
+            return out
+        if out is not None and hasattr(out, "data_ptr"):
+            L.check(self._lib.sf_sim_gather(self._h, name.encode(), C.c_void_p(out.data_ptr()), out.numel()))
+            return out
+        a = np.empty((nz, ny, nx), dtype=np.float64)
+        L.check(self._lib.sf_sim_gather(self._h, name.encode(), C.c_void_p(a.ctypes.data), a.size))
+        return a
+
+    def checksum(self) -> str:
+        v = C.c_uint64()
+        L.check(self._lib.sf_sim_checksum(self._h, C.byref(v)))
+        return "%016x" % v.value
+
+    def local_front(self, name: str, worker: int = 0) -> np.ndarray:
+        g = int(self._opt.ghost)
+        nx, ny, nz = self.extents
+        buf = np.empty((nx + 2 * g) * (ny + 2 * g) * (nz + 2 * g), dtype=np.float64)
+        dims = (C.c_int64 * 3)()
+        lo = (C.c_int64 * 3)()
+        L.check(self._lib.sf_sim_local_front(self._h, name.encode(), int(worker), C.c_void_p(buf.ctypes.data),
+                                             buf.size, dims, lo))
+        d = [dims[0] + 2 * g, dims[1] + 2 * g, dims[2] + 2 * g]
+        return buf[: d[0] * d[1] * d[2]].reshape(d[2], d[1], d[0]).copy()
+
+    # -- executor operations (executor.hpp:500-527) -------------------------
+    def refresh(self, names: Sequence[str]):
+        arr, n = _cstrs(names)
+        L.check(self._lib.sf_sim_refresh(self._h, arr, n))
+
+    def exchange(self, names: Sequence[str]):
+        arr, n = _cstrs(names)
+        L.check(self._lib.sf_sim_exchange(self._h, arr, n))
+
+    def run_kernel(self, name: str, params: dict | None = None, region: str = "all"):
+        params = params or {}
+        arr, n = _cstrs(params.keys())
+        vals = (C.c_double * max(1, n))(*[float(v) for v in params.values()])
+        L.check(self._lib.sf_sim_run_kernel(self._h, name.encode(), arr, vals, n, REGIONS[region]))
+
+    def reduce(self, name: str, op: str = "max_abs") -> float:
+        v = C.c_double()
+        L.check(self._lib.sf_sim_reduce(self._h, name.encode(), REDUCE_OPS[op], C.byref(v)))
+        return v.value
+
+    def invalidate_ghosts(self, name: str):
+        L.check(self._lib.sf_sim_invalidate_ghosts(self._h, name.encode()))
+
+    def invalidate_all_ghosts(self):
+        L.check(self._lib.sf_sim_invalidate_all_ghosts(self._h))
+
+    def ghosts_valid(self, name: str) -> bool:
+        return bool(self._lib.sf_sim_ghosts_valid(self._h, name.encode()))
+
+    # -- device plumbing -----------------------------------------------------
+    def synchronize(self):
+        L.check(self._lib.sf_sim_synchronize(self._h))
+
+    @property
+    def stream(self) -> int:
+        return self._lib.sf_sim_stream(self._h) or 0
+
+    def launch_count(self, reset: bool = False) -> int:
+        return int(self._lib.sf_sim_launch_count(self._h, 1 if reset else 0))
+
+    def set_kernel_timing(self, on: bool):
+        L.check(self._lib.sf_sim_set_kernel_timing(self._h, 1 if on else 0))
+
+    def kernel_timing(self, kernel: str = "sweep_div"):
+        ms, n = C.c_double(), C.c_int64()
+        L.check(self._lib.sf_sim_kernel_timing(self._h, kernel.encode(), C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+
+@dataclass
+class Decomposition:
+    """grid::decomposition (grid.hpp:52-86) as computed by the library."""
+
+    extents: tuple
+    workers: int
+    ghost: int
+    proc_grid: tuple
+    periodic: tuple
+    lo: list = field(default_factory=list)
+    hi: list = field(default_factory=list)
+
+    def coords_of(self, w: int):
+        pz, py = self.proc_grid[2], self.proc_grid[1]
+        return (w // (py * pz), (w // pz) % py, w % pz)
+
+    def neighbor(self, w: int, axis: int, side: int) -> int:
+        pg = (C.c_int * 3)(*self.proc_grid)
+        per = (C.c_int * 3)(*[1 if p else 0 for p in self.periodic])
+        return L.lib().sf_decomp_neighbor(pg, per, int(w), int(axis), int(side))
+
+    def face_physical(self, w: int, axis: int, side: int) -> bool:
+        return self.neighbor(w, axis, side) < 0
+
+    def size(self, w: int):
+        return tuple(self.hi[w][a] - self.lo[w][a] for a in range(3))
+
+
+def decompose(extents, workers: int, ghost: int, periodic=(False, False, False), spacing=None) -> Decomposition:
+    """grid::decompose (grid.hpp:92-163) -- host logic, no GPU needed."""
+    lib = L.lib()
+    ext = (C.c_int64 * 3)(*[int(x) for x in extents])
+    sp = (C.c_double * 3)(*(spacing or [1.0 / float(n) if n else 1.0 for n in extents]))
+    per = (C.c_int * 3)(*[1 if p else 0 for p in periodic])
+    pg = (C.c_int * 3)()
+    n = max(1, int(workers))
+    lo = (C.c_int64 * (3 * n))()
+    hi = (C.c_int64 * (3 * n))()
+    L.check(lib.sf_decompose(ext, sp, int(workers), int(ghost), per, pg, lo, hi))
+    return Decomposition(tuple(int(x) for x in extents), int(workers), int(ghost), tuple(pg),
+                         tuple(bool(p) for p in periodic),
+                         [tuple(lo[3 * w + a] for a in range(3)) for w in range(workers)],
+                         [tuple(hi[3 * w + a] for a in range(3)) for w in range(workers)])

@@ -1,0 +1,51 @@
+"""Regenerates tests/golden/golden.json from the reference compiled in place
+(oracle/_ref/libsfref.so, built by oracle/Makefile from /root/reference).
+
+Run here (the container that has /root/reference):  python tests/golden/make_golden.py
+The GPU box never runs this; the JSON travels with the repo.
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle.oracle import Oracle, cavity_case  # noqa: E402
+
+
+def cavity_run(n, steps_list, **kw):
+    o = Oracle(cavity_case(n, **kw), "ref")
+    o.init_cavity()
+    out = {"checksums": {}, "stats": []}
+    done = 0
+    for s in steps_list:
+        dts, sw, res = o.advance(s - done)
+        out["stats"] += [[float(a), int(b), float(c)] for a, b, c in zip(dts, sw, res)]
+        done = s
+        out["checksums"][str(s)] = o.checksum()
+    out["time"] = o.time
+    out["color"] = o.pending_color
+    return out
+
+
+def main():
+    t0 = time.time()
+    g = {"source": "oracle/_ref/libsfref.so (reference stencilforge compiled in place)"}
+    # 64^3 cavity, re=100, symmetry_z=false, defaults
+    g["cavity64"] = cavity_run(64, [1, 10], symmetry_z=False)
+    g["cavity64"]["checksums"]["100"] = "6782272b270ef89a"  # SURVEY.md Appendix A (391.9 s run)
+    # runs/bench128.cfg: 128^3, omega 1.9525, tolerance 1e-30, max_sweeps 200, 2 steps
+    g["bench128"] = cavity_run(128, [2], symmetry_z=False, omega=1.9525, tolerance=1e-30, max_sweeps=200)
+    # quasi-2D cavity (symmetry_z default) and ghost width 2
+    g["quasi2d_33"] = cavity_run((33, 33, 3), [20], sigma=0.8)
+    g["cavity24_g2"] = cavity_run(24, [3], symmetry_z=False, ghost=2)
+    g["cavity24_g3_w1"] = cavity_run(24, [2], symmetry_z=False, ghost=3)
+    g["elapsed_s"] = time.time() - t0
+    with open(os.path.join(os.path.dirname(__file__), "golden.json"), "w") as f:
+        json.dump(g, f, indent=1)
+    print(json.dumps({k: v.get("checksums") if isinstance(v, dict) else v for k, v in g.items()}, indent=1))
+
+
+if __name__ == "__main__":
+    main()

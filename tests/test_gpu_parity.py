@@ -1,0 +1,315 @@
+"""GPU parity: the CUDA library (through the C ABI) against the CPU oracles --
+the reference compiled in place (oracle/_ref/libsfref.so, travels with the
+repo as a built artifact) and the committed golden fixtures.  fp64 results
+must be BITWISE equal (integer/byte-exact bar; SURVEY.md section 7 hard part 1)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1201_2118_b200 as sfb
+from oracle.oracle import Case, Oracle, cavity_case
+
+pytestmark = pytest.mark.gpu
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+FIELDS5 = ("vx", "vy", "vz", "p", "divu")
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+def same(a, b):
+    return np.array_equal(bits(a), bits(b))
+
+
+def dev_cavity(n, workers=1, fused=True, ghost=1, **kw):
+    ext = (n, n, n) if isinstance(n, int) else tuple(n)
+    re = kw.pop("reynolds", 100.0)
+    cfg = sfb.SolverConfig(extents=ext, reynolds=re, **kw)
+    return sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=workers, ghost=ghost, fused=fused)
+
+
+def dev_from_case(c: Case, fused=True):
+    cfg = sfb.SolverConfig(extents=tuple(c.extents), spacing=c.spacing, periodic=tuple(c.periodic),
+                           reynolds=c.reynolds, sigma=c.sigma, tolerance=c.tolerance, omega=c.omega,
+                           max_sweeps=c.max_sweeps, symmetry_z=c.symmetry_z)
+    par = sfb.FluidParams(viscosity=c.viscosity, density=c.density, body_force=tuple(c.body_force),
+                          lid_speed=c.lid_speed, blend=c.blend)
+    return sfb.Simulation(cfg, par, workers=c.workers, ghost=c.ghost, fused=fused)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_cavity64_first_step_matches_golden(fused):
+    s = dev_cavity(64, symmetry_z=False, fused=fused)
+    s.init_cavity()
+    st = s.step()
+    assert [st.dt, st.sweeps, st.residual] == GOLDEN["cavity64"]["stats"][0]
+    assert s.checksum() == "1b07d1f577d4bad0"
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_cavity64_ten_steps_match_golden_per_step(fused):
+    s = dev_cavity(64, symmetry_z=False, fused=fused)
+    s.init_cavity()
+    stats = []
+    for _ in range(10):
+        st = s.step()
+        stats.append([st.dt, st.sweeps, st.residual])
+    assert stats == GOLDEN["cavity64"]["stats"]
+    assert s.checksum() == "32b900f8b9e72ed2"
+    assert s.step_count == 10
+
+
+def test_cavity64_hundred_steps_match_the_391_second_oracle_run():
+    s = dev_cavity(64, symmetry_z=False)
+    s.init_cavity()
+    s.advance(100)
+    assert s.checksum() == "6782272b270ef89a"
+    assert s.time == 0.20345052083333356
+
+
+def test_bench128_config_matches_golden():
+    s = dev_cavity(128, symmetry_z=False, omega=1.9525, tolerance=1e-30, max_sweeps=200)
+    s.init_cavity()
+    s.advance(2)
+    assert s.checksum() == GOLDEN["bench128"]["checksums"]["2"] == "a4dba62f6c310dd8"
+
+
+def test_quasi2d_and_ghost_widths_match_golden():
+    s = dev_cavity((33, 33, 3), sigma=0.8)
+    s.init_cavity()
+    s.advance(20)
+    assert s.checksum() == GOLDEN["quasi2d_33"]["checksums"]["20"]
+    s = dev_cavity(24, symmetry_z=False, ghost=2)
+    s.init_cavity()
+    s.advance(3)
+    assert s.checksum() == GOLDEN["cavity24_g2"]["checksums"]["3"]
+    s = dev_cavity(24, symmetry_z=False, ghost=3)
+    s.init_cavity()
+    s.advance(2)
+    assert s.checksum() == GOLDEN["cavity24_g3_w1"]["checksums"]["2"]
+
+
+@pytest.mark.parametrize("workers", [2, 4, 8])
+@pytest.mark.parametrize("fused", [True, False])
+def test_grid_components_on_one_device_give_identical_steps(ref_available, workers, fused):
+    o = Oracle(cavity_case((16, 16, 8)), "ref")
+    o.init_cavity()
+    o.advance(5)
+    s = dev_cavity((16, 16, 8), workers=workers, fused=fused)
+    s.init_cavity()
+    s.advance(5)
+    assert s.checksum() == o.checksum()
+
+
+def _random_case_pair(case, seed, fused=True):
+    rng = np.random.default_rng(seed)
+    fields = {f: rng.uniform(-1.0, 1.0, size=tuple(case.extents)[::-1]) for f in ("vx", "vy", "vz")}
+    o = Oracle(case, "ref")
+    d = dev_from_case(case, fused=fused)
+    for f, a in fields.items():
+        o.scatter(f, a)
+        d.scatter(f, a)
+    o.invalidate_all_ghosts()
+    d.invalidate_all_ghosts()
+    return o, d
+
+
+@pytest.mark.parametrize("workers", [1, 2, 4])
+@pytest.mark.parametrize("fused", [True, False])
+def test_projection_matches_reference_bitwise(ref_available, workers, fused):
+    # tests/test_cfd.cpp:231-273
+    c = Case(extents=(16, 16, 16), periodic=(True, True, True), tolerance=1e-8, max_sweeps=20000,
+             viscosity=0.01, lid_speed=0.0, workers=workers)
+    o, d = _random_case_pair(c, 12, fused)
+    so, ro = o.pressure_iteration(0.005)
+    sd, rd = d.pressure_iteration(0.005)
+    assert (sd, rd) == (so, ro)
+    assert ro <= 1e-8
+    for f in ("vx", "vy", "vz", "p", "divu"):
+        assert same(d.gather(f), o.gather(f)), f
+
+
+@pytest.mark.parametrize("periodic", [False, True])
+@pytest.mark.parametrize("workers", [1, 2, 3])
+@pytest.mark.parametrize("fused", [True, False])
+def test_odd_extents_capped_sweeps_match_reference(ref_available, periodic, workers, fused):
+    # tests/test_cfd.cpp:275-325: 17x13x5, two steps, 40 capped sweeps
+    c = Case(extents=(17, 13, 5), periodic=(periodic,) * 3, tolerance=1e-12, max_sweeps=40,
+             viscosity=0.05, lid_speed=0.0 if periodic else 1.0, workers=workers)
+    o, d = _random_case_pair(c, 13, fused)
+    so = o.advance(2)
+    dd = [d.step() for _ in range(2)]
+    assert [[x.dt, x.sweeps, x.residual] for x in dd] == [[float(a), int(b), float(r)] for a, b, r in zip(*so)]
+    for f in FIELDS5:
+        assert same(d.gather(f), o.gather(f)), f
+    assert d.pending_color == o.pending_color
+
+
+@pytest.mark.parametrize("workers", [1, 2, 4, 8])
+@pytest.mark.parametrize("ghost", [1, 2])
+@pytest.mark.parametrize("per", [(False, False, False), (True, False, True), (True, True, True)])
+def test_refresh_fills_every_ghost_like_the_reference(ref_available, workers, ghost, per):
+    c = Case(extents=(12, 10, 9), periodic=per, symmetry_z=not per[2], lid_speed=0.7, ghost=ghost,
+             workers=workers)
+    try:
+        o = Oracle(c, "ref")
+    except Exception:
+        pytest.skip("infeasible decomposition")
+    d = dev_from_case(c)
+    rng = np.random.default_rng(7)
+    for f in FIELDS5:
+        a = rng.standard_normal((9, 10, 12))
+        o.scatter(f, a)
+        d.scatter(f, a)
+    o.refresh(list(FIELDS5))
+    d.refresh(list(FIELDS5))
+    for w in range(workers):
+        for f in FIELDS5:
+            assert same(d.local_front(f, w), o.local_front(f, w)), (f, w)
+
+
+@pytest.mark.parametrize("region", ["all", "interior", "boundary"])
+def test_single_kernels_match_the_reference(ref_available, region):
+    c = Case(extents=(19, 11, 7), symmetry_z=False, lid_speed=1.0, blend=0.3, viscosity=0.02)
+    o, d = _random_case_pair(c, 5)
+    rng = np.random.default_rng(9)
+    q = rng.standard_normal((7, 11, 19))
+    o.scatter("p", q)
+    d.scatter("p", q)
+    # sets the simulation's dt the kernels use (cfd.hpp:276)
+    o.refresh(["vx", "vy", "vz", "p"])
+    d.refresh(["vx", "vy", "vz", "p"])
+    o.run_kernel("DIVERGENCE", {}, region)
+    d.run_kernel("DIVERGENCE", {}, region)
+    assert same(d.gather("divu"), o.gather("divu"))
+    o.refresh(["divu"])
+    d.refresh(["divu"])
+    o.run_kernel("PRESSURE_SWEEP", {"beta": 0.37, "color": 1}, region)
+    d.run_kernel("PRESSURE_SWEEP", {"beta": 0.37, "color": 1}, region)
+    for f in ("p", "vx", "vy", "vz"):
+        assert same(d.gather(f), o.gather(f)), f
+
+
+def test_update_velocity_matches_the_reference_with_upwind_blend(ref_available):
+    c = Case(extents=(19, 11, 7), symmetry_z=False, lid_speed=1.0, blend=0.3, viscosity=0.02,
+             body_force=(0.1, -0.2, 0.3))
+    o, d = _random_case_pair(c, 6)
+    q = np.random.default_rng(3).standard_normal((7, 11, 19))
+    o.scatter("p", q)
+    d.scatter("p", q)
+    o.provisional(0.0123)
+    d.provisional(0.0123)
+    for f in ("vx", "vy", "vz"):
+        assert same(d.gather(f), o.gather(f)), f
+    assert same(np.array([d.steady_delta()]), np.array([o.steady_delta()]))
+
+
+def test_reductions_match_the_reference(ref_available):
+    c = Case(extents=(21, 9, 6), workers=1)
+    o, d = _random_case_pair(c, 8)
+    for f in ("vx", "vy", "vz"):
+        assert d.reduce(f, "max_abs") == o.reduce(f, "max_abs")
+        assert d.reduce(f, "sum") == pytest.approx(o.reduce(f, "sum"), rel=1e-12, abs=1e-12)
+        assert d.reduce(f, "sum_sq") == pytest.approx(o.reduce(f, "sum_sq"), rel=1e-12)
+    assert d.compute_dt() == o.compute_dt()
+    nan = np.zeros((6, 9, 21))
+    nan[3, 4, 5] = np.nan
+    d.scatter("p", nan)
+    assert np.isnan(d.reduce("p", "max_abs"))
+
+
+def test_nan_guard_throws_like_the_reference():
+    # tests/test_cfd.cpp:474-480
+    cfg = sfb.SolverConfig(extents=(8, 8, 8), periodic=(True, True, True))
+    s = sfb.Simulation(cfg, sfb.FluidParams(viscosity=0.01, lid_speed=0.0))
+    s.init_uniform((1e308, 0.0, 0.0))
+    with pytest.raises(sfb.CfdError, match="non-finite vx after the velocity update at step 0, t = 0.000000"):
+        s.provisional(1.0)
+
+
+def test_body_force_alone_accelerates_linearly():
+    # tests/test_cfd.cpp:133-145
+    cfg = sfb.SolverConfig(extents=(6, 6, 6), periodic=(True, True, True))
+    s = sfb.Simulation(cfg, sfb.FluidParams(viscosity=0.01, lid_speed=0.0, body_force=(1.0, 0.0, 0.0)))
+    s.init_uniform((0.0, 0.0, 0.0))
+    dt = 0.015625
+    s.provisional(dt)
+    assert np.all(s.gather("vx") == dt)
+    assert np.all(s.gather("vy") == 0.0)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_one_sweep_cancels_an_impulse(fused):
+    # tests/test_cfd.cpp:147-177
+    cfg = sfb.SolverConfig(extents=(8, 8, 8), periodic=(True, True, True), omega=1.0, tolerance=1e-30, max_sweeps=1)
+    s = sfb.Simulation(cfg, sfb.FluidParams(viscosity=0.01, lid_speed=0.0), fused=fused)
+    s.init_uniform((0.0, 0.0, 0.0))
+    vx = np.zeros((8, 8, 8))
+    vx[2, 4, 4] = 1.0
+    s.scatter("vx", vx)
+    sweeps, residual = s.pressure_iteration(0.01)
+    assert sweeps == 1 and residual > 0.0
+    beta = 1.0 / (2.0 * 0.01 * 192.0)
+    div, p = s.gather("divu"), s.gather("p")
+    assert abs(div[2, 4, 4]) < 1e-12
+    assert p[2, 4, 4] == -beta * 8.0
+    assert p[2, 4, 3] == 0.0 and p[2, 4, 5] == 0.0
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_one_sweep_cancels_a_corner_impulse(fused):
+    # tests/test_cfd.cpp:179-212
+    cfg = sfb.SolverConfig(extents=(8, 8, 8), omega=1.0, tolerance=1e-30, max_sweeps=1)
+    s = sfb.Simulation(cfg, sfb.FluidParams(viscosity=0.01, lid_speed=0.0), fused=fused)
+    s.init_cavity()
+    vx = np.zeros((8, 8, 8))
+    vx[0, 0, 0] = 1.0
+    s.scatter("vx", vx)
+    sweeps, residual = s.pressure_iteration(0.01)
+    assert sweeps == 1 and residual > 0.0
+    beta = 1.0 / (2.0 * 0.01 * 192.0)
+    div, p = s.gather("divu"), s.gather("p")
+    assert abs(div[0, 0, 0]) < 1e-12
+    assert p[0, 0, 0] == -(beta * 2.0) * 8.0
+    assert p[0, 0, 1] == 0.0 and p[0, 1, 0] == 0.0
+
+
+def test_uniform_periodic_flow_is_a_bitwise_fixed_point():
+    # tests/test_cfd.cpp:111-131
+    cfg = sfb.SolverConfig(extents=(8, 8, 8), periodic=(True, True, True))
+    s = sfb.Simulation(cfg, sfb.FluidParams(viscosity=0.01, lid_speed=0.0), workers=2)
+    s.init_uniform((0.3, -0.2, 0.1))
+    before = {f: s.gather(f) for f in ("vx", "vy", "vz", "p")}
+    for _ in range(5):
+        st = s.step()
+        assert st.sweeps == 1 and st.residual == 0.0
+    for f, a in before.items():
+        assert same(s.gather(f), a)
+
+
+def test_taylor_green_start_and_diagnostics_match_reference(ref_available):
+    c = Case(extents=(16, 16, 2), periodic=(True, True, True), tolerance=1e-8, viscosity=0.01, lid_speed=0.0, workers=2)
+    o = Oracle(c, "ref")
+    o.init_taylor_green()
+    d = dev_from_case(c)
+    d.init_taylor_green()
+    for f in ("vx", "vy", "vz", "p"):
+        assert same(d.gather(f), o.gather(f))
+    assert d.max_divergence() == o.max_divergence()
+    assert d.pressure_iteration(0.001) == o.pressure_iteration(0.001)
+    assert d.kinetic_energy() == pytest.approx(o.kinetic_energy(), rel=1e-13)
+
+
+def test_errors_keep_the_reference_texts():
+    s = dev_cavity(8)
+    with pytest.raises(sfb.ExecError, match="unknown kernel 'NOPE'"):
+        s.run_kernel("NOPE")
+    with pytest.raises(sfb.ExecError, match="kernel 'PRESSURE_SWEEP': parameter 'beta' not supplied"):
+        s.run_kernel("PRESSURE_SWEEP", {"color": 0})
+    with pytest.raises(sfb.GridError, match="no field named 'q'"):
+        s.gather("q")
+    with pytest.raises(sfb.ConfigError, match="sigma must lie in"):
+        sfb.Simulation(sfb.SolverConfig(extents=(8, 8, 8), sigma=1.0), sfb.FluidParams())

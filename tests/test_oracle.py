@@ -1,0 +1,91 @@
+"""Pins the CPU oracles (test infrastructure) before anything is checked
+against them: the plain-C restatement (oracle/sf_oracle.c) against the golden
+checksums of SURVEY.md Appendix A and bitwise against the reference compiled
+in place (oracle/_ref/libsfref.so)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Case, Oracle, available, cavity_case
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+
+
+def test_port_reproduces_the_64_cube_golden_checksum_after_one_step():
+    o = Oracle(cavity_case(64, symmetry_z=False), "port")
+    o.init_cavity()
+    dt, sweeps, res = o.step()
+    assert o.checksum() == GOLDEN["cavity64"]["checksums"]["1"] == "1b07d1f577d4bad0"
+    assert dt == 0.0020345052083333335
+    assert sweeps == 500
+    assert [dt, sweeps, res] == GOLDEN["cavity64"]["stats"][0]
+
+
+def test_port_reproduces_the_golden_after_ten_steps():
+    o = Oracle(cavity_case(64, symmetry_z=False), "port")
+    o.init_cavity()
+    dts, sw, res = o.advance(10)
+    assert o.checksum() == "32b900f8b9e72ed2"
+    assert [[float(a), int(b), float(c)] for a, b, c in zip(dts, sw, res)] == GOLDEN["cavity64"]["stats"]
+
+
+def test_port_reproduces_the_quasi2d_and_ghost_width_goldens():
+    o = Oracle(cavity_case((33, 33, 3), sigma=0.8), "port")
+    o.init_cavity()
+    o.advance(20)
+    assert o.checksum() == GOLDEN["quasi2d_33"]["checksums"]["20"]
+    o = Oracle(cavity_case(24, symmetry_z=False, ghost=2), "port")
+    o.init_cavity()
+    o.advance(3)
+    assert o.checksum() == GOLDEN["cavity24_g2"]["checksums"]["3"]
+
+
+def _random_fields(shape, seed):
+    rng = np.random.default_rng(seed)
+    return [rng.uniform(-1.0, 1.0, size=shape[::-1]) for _ in range(3)]
+
+
+@pytest.mark.parametrize("periodic", [False, True])
+@pytest.mark.parametrize("ghost", [1, 2])
+def test_port_matches_the_reference_bitwise_on_random_fields(ref_available, periodic, ghost):
+    # the shape of tests/test_cfd.cpp:275-325: odd extents, capped sweeps
+    ext = (17, 13, 5)
+    vx, vy, vz = _random_fields(ext, 13)
+    outs = []
+    for kind in ("ref", "port"):
+        c = Case(extents=ext, periodic=(periodic,) * 3, tolerance=1e-12, max_sweeps=40,
+                 viscosity=0.05, lid_speed=0.0 if periodic else 1.0, ghost=ghost)
+        o = Oracle(c, kind)
+        o.scatter("vx", vx)
+        o.scatter("vy", vy)
+        o.scatter("vz", vz)
+        o.invalidate_all_ghosts()
+        stats = o.advance(2)
+        outs.append(([o.gather(f) for f in ("vx", "vy", "vz", "p", "divu")], [list(s) for s in stats]))
+    (a, sa), (b, sb) = outs
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
+    assert sa == sb
+
+
+def test_port_matches_reference_ghosts_after_a_refresh(ref_available):
+    ext = (9, 7, 6)
+    for kind_bc in (dict(symmetry_z=True), dict(symmetry_z=False), dict(periodic=(True, False, True))):
+        arrs = {}
+        for kind in ("ref", "port"):
+            o = Oracle(Case(extents=ext, lid_speed=0.7, ghost=2, **kind_bc), kind)
+            for i, f in enumerate(("vx", "vy", "vz", "p", "divu")):
+                o.scatter(f, np.random.default_rng(i).standard_normal(ext[::-1]))
+            o.refresh(["vx", "vy", "vz", "p", "divu"])
+            arrs[kind] = [o.local_front(f) for f in ("vx", "vy", "vz", "p", "divu")]
+        for x, y in zip(arrs["ref"], arrs["port"]):
+            assert np.array_equal(x, y)
+
+
+def test_reference_golden_fixture_is_reproducible(ref_available):
+    o = Oracle(cavity_case(24, symmetry_z=False, ghost=3), "ref")
+    o.init_cavity()
+    o.advance(2)
+    assert o.checksum() == GOLDEN["cavity24_g3_w1"]["checksums"]["2"]
