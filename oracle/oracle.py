@@ -155,6 +155,8 @@ def _load(kind: str) -> C.CDLL:
         "invalidate_all_ghosts": ([vp], None),
         "diag": ([vp, dp, dp, dp], i),
         "time_phases": ([vp, dp, dp, ip], i),
+        "time_half_sweeps": ([vp, i, d, dp], i),
+        "time_provisional": ([vp, dp, dp], i),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, pre + name, None)
@@ -318,6 +320,16 @@ class Oracle:
         v = C.c_double()
         self._ck(self._f("diag")(self._h, None, None, C.byref(v)))
         return v.value
+
+    def time_half_sweeps(self, k: int, beta: float) -> float:
+        t = C.c_double()
+        self._ck(self._f("time_half_sweeps")(self._h, int(k), float(beta), C.byref(t)))
+        return t.value
+
+    def time_provisional(self):
+        t, dt = C.c_double(), C.c_double()
+        self._ck(self._f("time_provisional")(self._h, C.byref(t), C.byref(dt)))
+        return t.value, dt.value
 
     def time_phases(self):
         tp, ti, s = C.c_double(), C.c_double(), C.c_int()

@@ -253,4 +253,39 @@ int sfref_time_phases(void* h, double* t_prov, double* t_iter, int* sweeps) {
   } catch (const std::exception& e) { return fail(e); }
 }
 
+// One half-sweep of pressure_iteration's loop body (cfd.hpp:295-303) through
+// the reference's own executor API, k times: refresh(divu), PRESSURE_SWEEP,
+// refresh(vx,vy,vz), DIVERGENCE, reduce(divu, max_abs).  Wall seconds.
+int sfref_time_half_sweeps(void* h, int k, double beta, double* seconds) {
+  try {
+    auto& e = S(h).engine();
+    auto t0 = std::chrono::steady_clock::now();
+    int color = 0;
+    for (int q = 0; q < k; ++q) {
+      e.refresh({"divu"});
+      e.run_kernel("PRESSURE_SWEEP", {{"beta", beta}, {"color", static_cast<double>(color)}});
+      color ^= 1;
+      e.refresh({"vx", "vy", "vz"});
+      e.run_kernel("DIVERGENCE", {});
+      (void)e.reduce("divu", grid::reduce_op::max_abs);
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// compute_dt + provisional (cfd.hpp:264-282) through the reference, wall seconds.
+int sfref_time_provisional(void* h, double* seconds, double* dt_out) {
+  try {
+    auto t0 = std::chrono::steady_clock::now();
+    const double dt = S(h).compute_dt();
+    S(h).provisional(dt);
+    auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    *dt_out = dt;
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
 }  // extern "C"
