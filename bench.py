@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark of the B200 stencil hot path.
+
+Workload (BASELINE.json configs[1]): the 3D lid-driven cavity at 512^3, fp64,
+ghost width 1, on one B200.  One bench "step" is one full cfd::simulation::step
+(cfd.hpp:307-316): compute_dt + ghost refresh + UPDATE_VELOCITY + 200
+red-black pressure half-sweeps (each: PRESSURE_SWEEP + velocity refresh +
+DIVERGENCE + max|div|) + refresh(p).  Fixed work per step as in
+proj/runs/bench128.cfg: tolerance 1e-30, max_sweeps 200, omega 1.9525.
+
+metric: grid-point updates/sec = cells x steps / second (the reference bench
+unit, bench.hpp:87-89), reported in Mcells/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+the unmodified stencilforge compiled in place) on this box's host cores on a
+bounded sample of the same workload, projected to the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_HALF_SWEEP = 80  # fused half-sweep: read divu,p,vx,vy,vz; write p,vx,vy,vz,divu' (fp64)
+BYTES_UV = 56              # UPDATE_VELOCITY: read vx,vy,vz,p; write vx,vy,vz
+BYTES_DIV = 32             # DIVERGENCE: read vx,vy,vz; write divu
+METRIC = "grid-point updates/sec"
+UNIT = "Mcells/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=512, help="cells per axis per GPU")
+    ap.add_argument("--sweeps", type=int, default=200, help="pressure half-sweeps per step")
+    ap.add_argument("--variant", default="tma", choices=["tma", "ldg", "unfused"],
+                    help="fused half-sweep with TMA pipeline (default), fused with plain loads, or unfused")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, STREAM copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """DRAM bytes per launch of the fused half-sweep from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_sweep_div.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("grid")
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.TemporaryFile(mode="w+")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+                pw.append(float(r[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        load = [s for s, p in zip(sm, pw) if p > 200.0] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def cavity_cfg(sfb, n, sweeps):
+    return sfb.SolverConfig(extents=(n, n, n), reynolds=100.0, sigma=0.5, omega=1.9525,
+                            tolerance=1e-30, max_sweeps=sweeps, symmetry_z=False)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference compiled in place, bounded sample
+# ---------------------------------------------------------------------------
+def reference_sample(n, sweeps, threads, samples=1, warmup=0, log=None):
+    """Times the reference's own implementation (oracle/_ref/libsfref.so) on a
+    bounded sample of the workload: per sample one compute_dt+provisional
+    (cfd.hpp:264-282) and one half-sweep of pressure_iteration's loop body
+    (refresh(divu), PRESSURE_SWEEP, refresh(v), DIVERGENCE, reduce; cfd.hpp:
+    295-303) through the reference executor.  A full step is projected as
+    t_prov + (sweeps + 1) * t_half (the +1 covers the initial
+    refresh_divergence and the final refresh(p))."""
+    from oracle.oracle import Oracle, available, cavity_case
+    kind = "reference" if available("ref") else "port"
+    t0 = time.time()
+    o = Oracle(cavity_case(n, symmetry_z=False, omega=1.9525, tolerance=1e-30, max_sweeps=sweeps,
+                           workers=threads if kind == "reference" else 1),
+               "ref" if kind == "reference" else "port")
+    o.init_cavity()
+    setup = time.time() - t0
+    ix2 = float(n * n)
+    per_step = []
+    for q in range(warmup + samples):
+        if kind == "reference":
+            tp, dt = o.time_provisional()
+            beta = 1.9525 / (2.0 * dt * (ix2 + ix2 + ix2))
+            th = o.time_half_sweeps(3, beta) / 3.0
+        else:
+            t1 = time.time()
+            dt = o.compute_dt()
+            o.provisional(dt)
+            tp = time.time() - t1
+            t1 = time.time()
+            o.run_kernel("DIVERGENCE")
+            th = (time.time() - t1) * 3.0  # crude: the port has no per-sweep probe
+        if q >= warmup:
+            per_step.append((tp, th, tp + (sweeps + 1) * th))
+        if log:
+            log(f"reference sample {q}: provisional {tp:.3f}s half-sweep {th:.3f}s")
+    o.close()
+    return kind, per_step, setup
+
+
+def cpu_threads(args):
+    if args.cpu_threads:
+        return args.cpu_threads
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    import paper_1201_2118_b200 as sfb
+
+    rank, world, local = dist_env()
+    if world > 1:
+        raise SystemExit("multi-GPU bench: see bench_multi (not in this build)")
+    dev = local
+    torch.cuda.set_device(dev)
+    n, S = args.n, args.sweeps
+    cells = n * n * n
+    cfg = cavity_cfg(sfb, n, S)
+    fused = {"tma": 1, "ldg": 2, "unfused": 0}[args.variant]
+    sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=1, device=dev, fused=fused)
+    sim.init_cavity()
+    stream = torch.cuda.ExternalStream(sim.stream, device=dev)
+
+    for _ in range(args.warmup):
+        sim.step()
+
+    # ---- device-timed region: K full steps, inputs resident in HBM -------------
+    clocks = ClockSampler(dev)
+    sim.set_kernel_timing(True)
+    sim.launch_count(reset=True)
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    stats = [sim.step() for _ in range(args.steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_total = e0.elapsed_time(e1)
+    launches = sim.launch_count()
+    k_ms, k_n = sim.kernel_timing("sweep_div")
+    sim.set_kernel_timing(False)
+    ms_per_step = ms_total / args.steps
+    value = cells * args.steps / (ms_total / 1e3) / 1e6
+    sweeps_done = sum(s.sweeps for s in stats)
+    assert sweeps_done == S * args.steps, "fixed-work config must run exactly max_sweeps per step"
+
+    peak, peak_src = measured_peaks()
+    avg_launch_s = (k_ms / k_n) / 1e3 if k_n else None
+    achieved = (BYTES_PER_HALF_SWEEP * cells / avg_launch_s / 1e9) if avg_launch_s else None
+    traffic, _ = ncu_traffic()
+    step_bytes = (BYTES_UV + BYTES_DIV + BYTES_PER_HALF_SWEEP * S) * cells
+    roofline = {
+        "bound": "hbm", "kernel": "k_sweep_div (fused half-sweep)",
+        "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
+        "frac": round(achieved / peak, 4) if achieved else None,
+        "traffic": traffic,
+        "algorithmic_bytes_per_launch": BYTES_PER_HALF_SWEEP * cells,
+        "avg_launch_ms": round(k_ms / k_n, 4) if k_n else None, "launches_timed": k_n,
+        "peak_source": peak_src,
+        "step_achieved_gbs": round(step_bytes / (ms_per_step / 1e3) / 1e9, 1),
+        "step_frac": round(step_bytes / (ms_per_step / 1e3) / 1e9 / peak, 4),
+    }
+
+    # ---- end to end through the public API with host buffers -------------------
+    e2e = None
+    if not args.no_e2e:
+        names = ("vx", "vy", "vz", "p")
+        host_in = {f: torch.from_numpy(sim.gather(f)).pin_memory() for f in names}
+        host_out = {f: torch.empty(cells, dtype=torch.float64).pin_memory() for f in names}
+        for f in names:  # one untimed warm trip
+            sim.scatter(f, host_in[f])
+        sim.step()
+        for f in names:
+            sim.gather(f, out=host_out[f])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            for f in names:
+                sim.scatter(f, host_in[f])
+            sim.step()
+            for f in names:
+                sim.gather(f, out=host_out[f])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        e_ms = max(e0.elapsed_time(e1), 0.0)
+        e_ms = max(e_ms, wall * 1e3)  # host-side copies can run outside the events
+        e2e = {"value": round(cells * args.steps / (e_ms / 1e3) / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * cells * 8, "d2h_bytes_per_step": 4 * cells * 8,
+               "ms_per_step": round(e_ms / args.steps, 3),
+               "path": "sf_sim_scatter(vx,vy,vz,p) from pinned host -> sf_sim_step -> sf_sim_gather(vx,vy,vz,p) to pinned host"}
+
+    # ---- CPU baseline (rank 0, N=1): the reference on this host, bounded sample --
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
+        th = cpu_threads(args)
+        kind, per, setup = reference_sample(n, S, th, samples=1)
+        tp, thalf, tstep = per[0]
+        cpu = {"value": round(cells / tstep / 1e6, 4), "unit": UNIT, "cores": th,
+               "kind": "reference" if kind == "reference" else "port",
+               "sample": (f"{n}^3 cavity, reference executor with {th} worker threads: one "
+                          f"compute_dt+provisional ({tp:.2f}s) + one pressure half-sweep ({thalf:.2f}s), "
+                          f"projected to a {S}-sweep step = {tstep:.1f}s"),
+               "ms_per_step_projected": round(tstep * 1e3, 1)}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (lid-driven cavity from rest, init_cavity)",
+        "config": {"workload": f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)",
+                   "grid": [n, n, n], "ghost": 1, "sweeps_per_step": S, "parallelism": "1 GPU",
+                   "path": {"tma": "fused half-sweep, TMA pipeline", "ldg": "fused half-sweep, plain loads",
+                            "unfused": "unfused (reference dataflow)"}[args.variant],
+                   "l2": "inputs larger than L2: 9 resident fp64 arrays of %.2f GB" % (cells * 8 / 1e9)},
+        "half_sweep_rate": round(cells * sweeps_done / (ms_total / 1e3) / 1e6, 1),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    n, S = args.n, args.sweeps
+    cells = n * n * n
+    th = cpu_threads(args)
+    kind, per, setup = reference_sample(n, S, th, samples=args.steps, warmup=args.warmup)
+    tsteps = [x[2] for x in per]
+    ms = 1e3 * sum(tsteps) / len(tsteps)
+    value = cells * len(tsteps) / sum(tsteps) / 1e6
+    sample = (f"per step: one compute_dt+provisional and one pressure half-sweep of the {n}^3 cavity "
+              f"through the reference executor ({th} worker threads), projected to {S} half-sweeps")
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (lid-driven cavity from rest, init_cavity)",
+        "config": {"workload": f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)",
+                   "grid": [n, n, n], "ghost": 1, "sweeps_per_step": S, "parallelism": f"{th} CPU worker threads"},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": th,
+                         "kind": "reference" if kind == "reference" else "port", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": round(setup, 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

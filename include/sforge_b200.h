@@ -103,7 +103,8 @@ typedef struct sf_sim_options {
   int ghost;
   int form;    /* 0 rows, 1 points (cfd.hpp:169): one device form serves both */
   int device;
-  int fused;   /* 1 = fused sweep+divergence half-sweep (default), 0 = unfused */
+  int fused;   /* 1 = fused half-sweep, TMA-pipelined (default); 2 = fused, plain
+                  loads (A/B baseline); 0 = the reference's unfused dataflow */
 } sf_sim_options;
 
 /* cfd::step_stats (cfd.hpp:86-90) */

@@ -47,6 +47,8 @@ struct sf_dev_table {
   int nblocks;
   sf_dev_block blk[kMaxBlocks];
   double* ptr[kMaxBlocks][kMaxFields][kSlots];
+  // physical buffer (0..2) occupying each slot: selects the TMA descriptor
+  unsigned char bidx[kMaxBlocks][kMaxFields][kSlots];
 };
 
 // Device control block of the pressure loop.  acc[] are max accumulators on

@@ -700,6 +700,7 @@ class simulation {
   sf_host_flag* hflag_ = nullptr;
   sf_host_flag* dflag_ = nullptr;
   double* staging_ = nullptr;
+  void* maps_ = nullptr;  // TMA descriptors (null: no driver entry point -> LDG kernel)
   std::vector<void*> dev_allocs_;
   std::map<std::string, work_set> items_;
   std::map<std::string, task_set> tasks_;
@@ -847,7 +848,25 @@ class simulation {
           double* p = (double*)dalloc(bytes);
           SF_CK(cudaMemsetAsync(p, 0, bytes, st_));
           htab_->ptr[b][f][s] = p;
+          htab_->bidx[b][f][s] = (unsigned char)s;
         }
+      }
+    }
+    // TMA descriptors of every physical buffer the fused half-sweep reads
+    {
+      std::vector<unsigned char> hm(sweep_maps_bytes(), 0);
+      bool ok = true;
+      for (int b = 0; b < dec_.workers && ok; ++b)
+        for (int f = 0; f < SF_NFIELDS && ok; ++f)
+          for (int s = 0; s < kSlots && ok; ++s) {
+            double* p = htab_->ptr[b][f][s];
+            if (!p) continue;
+            const sf_layout& L = lay_[b];
+            ok = encode_sweep_map(hm.data() + sweep_map_offset(b, f, s), p, L.sx, L.sy, L.sz, f) == 0;
+          }
+      if (ok) {
+        maps_ = dalloc(hm.size());
+        SF_CK(cudaMemcpy(maps_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
       }
     }
     dtab_ = (sf_dev_table*)dalloc(sizeof(sf_dev_table));
@@ -1062,7 +1081,10 @@ class simulation {
     if (opt_.fused) {
       const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
-      launch_sweep_div(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, st_);
+      if (maps_ && opt_.fused == 1)
+        launch_sweep_div_tma(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, maps_, st_);
+      else
+        launch_sweep_div(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, st_);
       ++launches_;
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
       ++iter_launch_;

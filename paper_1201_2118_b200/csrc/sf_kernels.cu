@@ -601,6 +601,9 @@ __global__ void __launch_bounds__(kTX* kTY) k_sweep_div(sf_dev_table* __restrict
           double* tmp = tab->ptr[b][f][FRONT];
           tab->ptr[b][f][FRONT] = tab->ptr[b][f][ALT];
           tab->ptr[b][f][ALT] = tmp;
+          const unsigned char ti = tab->bidx[b][f][FRONT];
+          tab->bidx[b][f][FRONT] = tab->bidx[b][f][ALT];
+          tab->bidx[b][f][ALT] = ti;
         }
       }
       if (hflag) {
@@ -809,6 +812,9 @@ __global__ void k_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, i
         double* tmp = tab->ptr[b][f][sa];
         tab->ptr[b][f][sa] = tab->ptr[b][f][sb];
         tab->ptr[b][f][sb] = tmp;
+        const unsigned char ti = tab->bidx[b][f][sa];
+        tab->bidx[b][f][sa] = tab->bidx[b][f][sb];
+        tab->bidx[b][f][sb] = ti;
       }
       break;
   }

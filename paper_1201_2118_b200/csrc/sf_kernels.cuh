@@ -38,6 +38,12 @@ void launch_pressure_sweep(const View& vw, int nctas, int zc, const sf_consts& c
                            int predicated, const double* beta_color_dt, cudaStream_t st);
 void launch_sweep_div(const table_view& vw, int nctas, int zc, const sf_consts& c,
                       sf_dev_ctl* ctl, sf_host_flag* hflag, cudaStream_t st);
+// TMA-pipelined fused half-sweep (sf_sweep_tma.cu); maps = device sweep_maps.
+void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_consts& c,
+                          sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, cudaStream_t st);
+int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field);
+size_t sweep_maps_bytes();
+size_t sweep_map_offset(int b, int f, int s);
 template <class View>
 void launch_reduce_max(const View& vw, int nctas, int zc, const int* fields, int nfields, int diff,
                        unsigned long long* acc, cudaStream_t st);

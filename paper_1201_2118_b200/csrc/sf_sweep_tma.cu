@@ -1,0 +1,404 @@
+// sf_sweep_tma.cu -- the fused red-black half-sweep, TMA-pipelined for sm_100a.
+//
+// Same arithmetic and boundary semantics as k_sweep_div in sf_kernels.cu (see
+// the comment there and cfd.hpp:289-305, 595-720, exchange.hpp:231-480), but
+// the loads are 3-D TMA boxes (cp.async.bulk.tensor) into a kStages-deep ring
+// of shared-memory plane tiles, each stage guarded by an mbarrier with
+// expect_tx.  Per stage and CTA (tile 32 x 8 cells of one z plane):
+//     divu  36 x 10  (x and y halo: the sweep reads +x/+y, the -x/-y swept
+//                    neighbours need -x/-y; x starts at i0-2, see kXL)
+//     vx    34 x 8   (columns i0-2, i0-1 for the -x neighbour)
+//     vy    32 x 9   (row j0-1 for the -y neighbour)
+//     p, vz 32 x 8
+// The +z neighbour of divu is the next stage's centre; the -z swept neighbour
+// of vz is carried in a register while marching z.  One elected thread
+// refills the stage just consumed after a CTA barrier, keeping kStages-1
+// planes (~34 KB) in flight per CTA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+
+#include "sf_kernels.cuh"
+
+namespace sfb {
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
+                                            int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// stage layout (every TMA destination 128-byte aligned)
+// ---------------------------------------------------------------------------
+// On B200 a TMA tile load of 8-byte elements must START on a 16-byte aligned
+// inner coordinate (an odd x start raises "illegal instruction"; measured with
+// scripts/probes/tma_probe2.cu), so the x halo boxes begin two cells left of
+// the tile: divu covers x in [i0-2, i0+34), vx covers [i0-2, i0+32).
+constexpr int kStages = 4;
+constexpr int kXL = 2;                       // cells left of the tile in the x-halo boxes
+constexpr int kDW = kTX + 4, kDH = kTY + 2;  // divu box 36 x 10
+constexpr int kUW = kTX + 2;                 // vx box 34 x 8
+constexpr int kVH = kTY + 1;                 // vy box 32 x 9
+struct __align__(128) stage_t {
+  double d[kDH][kDW];  // 2880 B
+  double pad0[8];      // -> 2944
+  double u[kTY][kUW];  // 2176 B -> 5120
+  double v[kVH][kTX];  // 2304 B -> 7424
+  double p[kTY][kTX];  // 2048 B -> 9472
+  double w[kTY][kTX];  // 2048 B -> 11520
+};
+static_assert(sizeof(stage_t) == 11520, "stage layout");
+static_assert(offsetof(stage_t, u) % 128 == 0 && offsetof(stage_t, v) % 128 == 0 &&
+                  offsetof(stage_t, p) % 128 == 0 && offsetof(stage_t, w) % 128 == 0,
+              "TMA destinations must be 128-byte aligned");
+constexpr uint32_t kStageBytes = sizeof(double) * (kDH * kDW + kTY * kUW + kVH * kTX + 2 * kTY * kTX);
+
+struct sweep_maps {  // per block: [field][physical buffer]
+  CUtensorMap m[kMaxBlocks][SF_NFIELDS][kSlots];
+};
+
+__global__ void __launch_bounds__(kTX* kTY, 2)
+    k_sweep_div_tma(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems,
+                    int zc, sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag,
+                    unsigned int total_ctas, const sweep_maps* __restrict__ maps) {
+  if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  stage_t* S = reinterpret_cast<stage_t*>(smem_raw);
+  __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ double smb[8];
+
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * kTX + tx;
+  // tile location
+  const int cta = blockIdx.x;
+  const int it = nitems > 1 ? find_item(items, nitems, cta) : 0;
+  const sf_work& wk = items[it];
+  const int b = wk.blk;
+  const int local = cta - wk.cta_begin;
+  const int tix = local % wk.tiles[0];
+  const int tiy = (local / wk.tiles[0]) % wk.tiles[1];
+  const int tiz = local / (wk.tiles[0] * wk.tiles[1]);
+  const long long i0 = wk.lo[0] + (long long)tix * kTX;
+  const long long j0 = wk.lo[1] + (long long)tiy * kTY;
+  const long long k0 = wk.lo[2] + (long long)tiz * zc;
+  const long long k1 = min(k0 + zc, wk.hi[2]);
+  const int nplanes = (int)(k1 - k0);
+  const sf_dev_block& B = tab->blk[b];
+
+  const double beta = ctl->beta, dt = ctl->dt;
+  const int color = ctl->color;
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < kStages; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < 8) {
+    // -(beta * bscale[bx][by][bz]) exactly as cfd.hpp:712-715 forms it
+    double sc = 1.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q == tid) sc = s.bscale[q >> 2][(q >> 1) & 1][q & 1];
+    smb[tid] = -(beta * sc);
+  }
+  __syncthreads();
+
+  // TMA box origins (tensor coordinates: x = xo + i, y = g + j, z = g + k)
+  const long long xo = B.base % B.sx;
+  const int g = B.g;
+  const CUtensorMap* mD = &maps->m[b][SF_DIVU][tab->bidx[b][SF_DIVU][FRONT]];
+  const CUtensorMap* mU = &maps->m[b][SF_VX][tab->bidx[b][SF_VX][FRONT]];
+  const CUtensorMap* mV = &maps->m[b][SF_VY][tab->bidx[b][SF_VY][FRONT]];
+  const CUtensorMap* mW = &maps->m[b][SF_VZ][tab->bidx[b][SF_VZ][FRONT]];
+  const CUtensorMap* mP = &maps->m[b][SF_P][tab->bidx[b][SF_P][FRONT]];
+  const int xc = (int)(xo + i0), yc = (int)(g + j0), zc0 = (int)(g + k0);
+  auto issue = [&](int stage, int plane) {
+    stage_t& st = S[stage];
+    mbar_expect_tx(&bars[stage], kStageBytes);
+    tma_load_3d(&st.d[0][0], mD, &bars[stage], xc - kXL, yc - 1, zc0 + plane);
+    tma_load_3d(&st.u[0][0], mU, &bars[stage], xc - kXL, yc, zc0 + plane);
+    tma_load_3d(&st.v[0][0], mV, &bars[stage], xc, yc - 1, zc0 + plane);
+    tma_load_3d(&st.p[0][0], mP, &bars[stage], xc, yc, zc0 + plane);
+    tma_load_3d(&st.w[0][0], mW, &bars[stage], xc, yc, zc0 + plane);
+  };
+  if (tid == 0) {
+    const int npro = nplanes < kStages ? nplanes : kStages;
+    for (int q = 0; q < npro; ++q) issue(q, q);
+  }
+
+  double* __restrict__ Dn = tab->ptr[b][SF_DIVU][ALT];
+  double* __restrict__ P = tab->ptr[b][SF_P][FRONT];
+  double* __restrict__ Un = tab->ptr[b][SF_VX][ALT];
+  double* __restrict__ Vn = tab->ptr[b][SF_VY][ALT];
+  double* __restrict__ Wn = tab->ptr[b][SF_VZ][ALT];
+  const double* __restrict__ D = tab->ptr[b][SF_DIVU][FRONT];
+  const double* __restrict__ W = tab->ptr[b][SF_VZ][FRONT];
+  const double cu = dt * s.ix, cv = dt * s.iy, cw = dt * s.iz;
+
+  const long long i = i0 + tx, j = j0 + ty;
+  const bool act = i < wk.hi[0] && j < wk.hi[1];
+  const long long n0 = B.n[0], n1 = B.n[1], n2 = B.n[2];
+  const long long sx = B.sx, sxy = B.sx * B.sy;
+  const long long gi = B.lo[0] + i, gj = B.lo[1] + j;
+  const int per0 = s.per[0], per1 = s.per[1], per2 = s.per[2];
+  auto bin = [](int per, long long gg, long long nm1) { return per | ((gg > 0) & (gg < nm1)); };
+  auto bnx = [](int per, long long gg, long long nm1) { return per | (gg + 1 < nm1); };
+  const long long gim = i > 0 ? gi - 1 : B.nb_ghost_gidx[0];
+  const long long gjm = j > 0 ? gj - 1 : B.nb_ghost_gidx[2];
+  const int bx = bin(per0, gi, s.nm1[0]), bxp = bnx(per0, gi, s.nm1[0]);
+  const int by = bin(per1, gj, s.nm1[1]), byp = bnx(per1, gj, s.nm1[1]);
+  const int bxm = bin(per0, gim, s.nm1[0]), bxpm = bnx(per0, gim, s.nm1[0]);
+  const int bym = bin(per1, gjm, s.nm1[1]), bypm = bnx(per1, gjm, s.nm1[1]);
+  // scale-table row indices per use (the z bit is or-ed in per plane)
+  const int ic = (bx << 2) | (by << 1), iex = (bxp << 2) | (by << 1), iey = (bx << 2) | (byp << 1);
+  const int ixm = (bxm << 2) | (by << 1), ixpm = (bxpm << 2) | (by << 1);
+  const int iym = (bx << 2) | (bym << 1), iypm = (bx << 2) | (bypm << 1);
+  const int fxl = B.face[0], fxh = B.face[1], fyl = B.face[2], fyh = B.face[3];
+  const int fzl = B.face[4], fzh = B.face[5];
+  const bool pin_u = (fxh == FACE_WALL || fxh == FACE_SYM) && i == n0 - 1;
+  const bool pin_v = (fyh == FACE_WALL || fyh == FACE_SYM) && j == n1 - 1;
+  const bool pin_w = (fzh == FACE_WALL || fzh == FACE_SYM);
+  const double pv_u = fxh == FACE_WALL ? B.fvel[1][0] : 0.0;
+  const double pv_v = fyh == FACE_WALL ? B.fvel[3][1] : 0.0;
+  const double pv_w = fzh == FACE_WALL ? B.fvel[5][2] : 0.0;
+  const bool xm_swept = i > 0 || fxl == FACE_PROC || fxl == FACE_SELF;
+  const bool ym_swept = j > 0 || fyl == FACE_PROC || fyl == FACE_SELF;
+
+  long long o = off(B, i, j, k0);
+  unsigned long long rmax = 0ull;
+  double wm_new = 0.0;
+  if (act) {  // swept w of the cell below the chunk (carried while marching)
+    const long long gk = B.lo[2] + k0;
+    const double dC0 = D[o];
+    if (k0 > 0 || fzl == FACE_PROC || fzl == FACE_SELF) {
+      const long long gkm = k0 > 0 ? gk - 1 : B.nb_ghost_gidx[4];
+      const int bzm = bin(per2, gkm, s.nm1[2]), bzpm = bnx(per2, gkm, s.nm1[2]);
+      const double a0m = (((gi + gj + gkm) & 1) == color) ? 1.0 : 0.0, a1m = 1.0 - a0m;
+      const double d0m = smb[ic | bzm] * D[o - sxy] * a0m;
+      const double ezm = smb[ic | bzpm] * dC0 * a1m;
+      wm_new = W[o - sxy] + cw * (d0m - ezm);
+    } else {
+      wm_new = W[o - sxy];
+    }
+  }
+
+  for (int kk = 0; kk < nplanes; ++kk, o += sxy) {
+    const int st = kk % kStages;
+    mbar_wait(&bars[st], (uint32_t)((kk / kStages) & 1));
+    const bool has_next = kk + 1 < nplanes;
+    const int st1 = (kk + 1) % kStages;
+    if (has_next) mbar_wait(&bars[st1], (uint32_t)(((kk + 1) / kStages) & 1));
+    if (act) {
+      const stage_t& T = S[st];
+      const long long k = k0 + kk;
+      const long long gk = B.lo[2] + k;
+      const int bz = bin(per2, gk, s.nm1[2]), bzp = bnx(per2, gk, s.nm1[2]);
+      const double dC = T.d[ty + 1][tx + kXL];
+      const double dXp = T.d[ty + 1][tx + kXL + 1], dXm = T.d[ty + 1][tx + kXL - 1];
+      const double dYp = T.d[ty + 2][tx + kXL], dYm = T.d[ty][tx + kXL];
+      const double dZp = has_next ? S[st1].d[ty + 1][tx + kXL] : D[o + sxy];
+      const double p0 = T.p[ty][tx], u0 = T.u[ty][tx + kXL], uml = T.u[ty][tx + kXL - 1];
+      const double v0 = T.v[ty + 1][tx], vml = T.v[ty][tx], w0 = T.w[ty][tx];
+      const double a0 = (((gi + gj + gk) & 1) == color) ? 1.0 : 0.0, a1 = 1.0 - a0;
+      // this cell's sweep (cfd.hpp:712-719)
+      const double d0 = smb[ic | bz] * dC * a0;
+      const double ex = smb[iex | bz] * dXp * a1;
+      const double ey = smb[iey | bz] * dYp * a1;
+      const double ez = smb[ic | bzp] * dZp * a1;
+      P[o] = p0 + d0;
+      double un = u0 + cu * (d0 - ex);
+      double vn = v0 + cv * (d0 - ey);
+      double wn = w0 + cw * (d0 - ez);
+      if (pin_u) un = pv_u;
+      if (pin_v) vn = pv_v;
+      if (pin_w && k == n2 - 1) wn = pv_w;
+      // swept -x / -y neighbours (the refreshed values DIVERGENCE reads)
+      double umn, vmn;
+      if (xm_swept) {
+        const double a0m = i > 0 ? a1 : ((((gim + gj + gk) & 1) == color) ? 1.0 : 0.0);
+        const double a1m = 1.0 - a0m;
+        const double d0m = smb[ixm | bz] * dXm * a0m;
+        const double exm = smb[ixpm | bz] * dC * a1m;
+        umn = uml + cu * (d0m - exm);
+      } else {
+        umn = fxl == FACE_OUT ? un : uml;
+      }
+      if (ym_swept) {
+        const double a0m = j > 0 ? a1 : ((((gi + gjm + gk) & 1) == color) ? 1.0 : 0.0);
+        const double a1m = 1.0 - a0m;
+        const double d0m = smb[iym | bz] * dYm * a0m;
+        const double eym = smb[iypm | bz] * dC * a1m;
+        vmn = vml + cv * (d0m - eym);
+      } else {
+        vmn = fyl == FACE_OUT ? vn : vml;
+      }
+      if (k == 0 && fzl == FACE_OUT) wm_new = wn;
+      // DIVERGENCE (cfd.hpp:605-608)
+      double dd = (un - umn) * s.ix;
+      dd += (vn - vmn) * s.iy;
+      dd += (wn - wm_new) * s.iz;
+      Un[o] = un;
+      Vn[o] = vn;
+      Wn[o] = wn;
+      Dn[o] = dd;
+      if (i == 0) Un[o - 1] = umn;
+      if (j == 0) Vn[o - sx] = vmn;
+      if (k == 0) Wn[o - sxy] = wm_new;
+      if (i == 0) {
+        if (fxl == FACE_WALL || fxl == FACE_SYM || fxl == FACE_OUT) Dn[o - 1] = dd;
+        if (fxh == FACE_SELF) Dn[o + n0] = dd;
+      }
+      if (i == n0 - 1) {
+        if (fxh == FACE_WALL || fxh == FACE_SYM || fxh == FACE_OUT) Dn[o + 1] = dd;
+        if (fxl == FACE_SELF) Dn[o - n0] = dd;
+      }
+      if (j == 0) {
+        if (fyl == FACE_WALL || fyl == FACE_SYM || fyl == FACE_OUT) Dn[o - sx] = dd;
+        if (fyh == FACE_SELF) Dn[o + n1 * sx] = dd;
+      }
+      if (j == n1 - 1) {
+        if (fyh == FACE_WALL || fyh == FACE_SYM || fyh == FACE_OUT) Dn[o + sx] = dd;
+        if (fyl == FACE_SELF) Dn[o - n1 * sx] = dd;
+      }
+      if (k == 0) {
+        if (fzl == FACE_WALL || fzl == FACE_SYM || fzl == FACE_OUT) Dn[o - sxy] = dd;
+        if (fzh == FACE_SELF) Dn[o + n2 * sxy] = dd;
+      }
+      if (k == n2 - 1) {
+        if (fzh == FACE_WALL || fzh == FACE_SYM || fzh == FACE_OUT) Dn[o + sxy] = dd;
+        if (fzl == FACE_SELF) Dn[o - n2 * sxy] = dd;
+      }
+      const unsigned long long bb = abs_bits(dd);
+      rmax = bb > rmax ? bb : rmax;
+      wm_new = wn;
+    }
+    __syncthreads();  // every thread is done with stage st
+    if (tid == 0 && kk + kStages < nplanes) issue(st, kk + kStages);
+  }
+
+  unsigned long long rm[1] = {rmax};
+  block_max_atomic<1>(rm, &ctl->acc[0]);
+  if (last_cta(&ctl->ctas_done, total_ctas)) {
+    if (tid == 0) {
+      __threadfence();
+      const unsigned long long rb = *reinterpret_cast<volatile unsigned long long*>(&ctl->acc[0]);
+      const double residual = bits_to_max(rb);
+      ctl->acc[0] = 0ull;
+      ctl->ctas_done = 0u;
+      ctl->residual = residual;
+      ctl->color ^= 1;
+      const int sweeps = ctl->sweeps + 1;
+      ctl->sweeps = sweeps;
+      const int more = (residual > ctl->tolerance) && (sweeps < ctl->max_sweeps);
+      ctl->done = more ? 0 : 1;
+      for (int q = 0; q < tab->nblocks; ++q)
+        for (int f = 0; f < SF_NFIELDS; ++f) {
+          if (f == SF_P) continue;
+          double* tmp = tab->ptr[q][f][FRONT];
+          tab->ptr[q][f][FRONT] = tab->ptr[q][f][ALT];
+          tab->ptr[q][f][ALT] = tmp;
+          const unsigned char ti = tab->bidx[q][f][FRONT];
+          tab->bidx[q][f][FRONT] = tab->bidx[q][f][ALT];
+          tab->bidx[q][f][ALT] = ti;
+        }
+      if (hflag) {
+        hflag->sweeps = sweeps;
+        hflag->residual = residual;
+        hflag->done = more ? 0 : 1;
+        hflag->color = ctl->color;
+        __threadfence_system();
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps + launch
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Box shape per field role (see stage_t).
+static void box_for(int field, cuuint32_t box[3]) {
+  box[2] = 1;
+  switch (field) {
+    case SF_DIVU: box[0] = kDW; box[1] = kDH; break;
+    case SF_VX: box[0] = kUW; box[1] = kTY; break;
+    case SF_VY: box[0] = kTX; box[1] = kVH; break;
+    default: box[0] = kTX; box[1] = kTY; break;
+  }
+}
+
+int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field) {
+  auto fn = encode_fn();
+  if (!fn) return 1;
+  cuuint64_t gdim[3] = {(cuuint64_t)sx, (cuuint64_t)sy, (cuuint64_t)sz};
+  cuuint64_t gstride[2] = {(cuuint64_t)(sx * 8), (cuuint64_t)(sx * sy * 8)};
+  cuuint32_t box[3];
+  box_for(field, box);
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, gdim,
+                  gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : 2;
+}
+
+size_t sweep_maps_bytes() { return sizeof(sweep_maps); }
+size_t sweep_map_offset(int b, int f, int s) {
+  return offsetof(sweep_maps, m) + sizeof(CUtensorMap) * ((size_t)(b * SF_NFIELDS + f) * kSlots + s);
+}
+
+void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_consts& c,
+                          sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, cudaStream_t st) {
+  if (nctas <= 0) return;
+  const size_t smem = sizeof(stage_t) * kStages;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep_div_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_sweep_div_tma<<<nctas, dim3(kTX, kTY), smem, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl,
+                                                        hflag, (unsigned)nctas,
+                                                        static_cast<const sweep_maps*>(maps));
+}
+
+}  // namespace sfb

@@ -86,12 +86,13 @@ def _cstrs(names: Iterable[str]):
 
 class Simulation:
     """Device-resident cfd::simulation.  ``workers`` grid components of
-    grid::decompose() live on ``device``; ``fused`` selects the fused
-    sweep+divergence half-sweep (default) or the reference's unfused dataflow."""
+    grid::decompose() live on ``device``.  ``fused``: 1/True = fused half-sweep,
+    TMA-pipelined (default); 2 = fused half-sweep with plain loads; 0/False =
+    the reference's unfused dataflow (refresh, SWEEP, refresh, DIV, reduce)."""
 
     def __init__(self, cfg: SolverConfig, par: FluidParams, workers: int = 1, mode: str = "plain",
                  tile: Sequence[int] = (0, 0, 0), ghost: int = 1, form: str = "rows",
-                 device: int = 0, fused: bool = True):
+                 device: int = 0, fused: int | bool = True):
         self._h = None
         self.cfg, self.par = cfg, par
         self._lib = L.lib()
@@ -100,7 +101,7 @@ class Simulation:
         opt.workers, opt.mode = int(workers), (1 if mode == "overlap" else 0)
         for a in range(3):
             opt.tile[a] = int(tile[a])
-        opt.ghost, opt.form, opt.device, opt.fused = int(ghost), (1 if form == "points" else 0), int(device), int(bool(fused))
+        opt.ghost, opt.form, opt.device, opt.fused = int(ghost), (1 if form == "points" else 0), int(device), int(fused)
         self._ccfg, self._cpar, self._opt = cfg.to_c(), par.to_c(), opt
         h = C.c_void_p()
         L.check(self._lib.sf_sim_create(C.byref(self._ccfg), C.byref(self._cpar), C.byref(opt), C.byref(h)))
