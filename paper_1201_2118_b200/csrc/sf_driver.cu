@@ -17,6 +17,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -727,7 +728,7 @@ class simulation {
   }
   const int zc_plain_ = 16;
   const int zc_uv_ = 8;
-  const int zc_fused_ = 32;
+  const int zc_fused_ = getenv("SF_ZC") ? atoi(getenv("SF_ZC")) : 64;
 
   void validate() {
     // solver_config::validate / fluid_params::validate (cfd.hpp:36-66)

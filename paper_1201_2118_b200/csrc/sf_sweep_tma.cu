@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "sf_kernels.cuh"
 
@@ -87,18 +88,25 @@ struct sweep_maps {  // per block: [field][physical buffer]
   CUtensorMap m[kMaxBlocks][SF_NFIELDS][kSlots];
 };
 
-__global__ void __launch_bounds__(kTX* kTY, 2)
+// STAGES: ring depth.  MINB: CTAs per SM the register budget targets.  WS:
+// warp-specialised -- a ninth warp produces (TMA) and consumer warps release
+// stages through "empty" mbarriers instead of a per-plane CTA barrier.
+template <int STAGES, int MINB, bool WS>
+__global__ void __launch_bounds__(kTX* kTY + (WS ? 32 : 0), MINB)
     k_sweep_div_tma(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems,
                     int zc, sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag,
                     unsigned int total_ctas, const sweep_maps* __restrict__ maps) {
+  constexpr int kStages = STAGES;
   if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   stage_t* S = reinterpret_cast<stage_t*>(smem_raw);
   __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ __align__(8) uint64_t empty_bars[kStages];
   __shared__ double smb[8];
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * kTX + tx;
+  const bool producer_warp = WS && ty == kTY;
   // tile location
   const int cta = blockIdx.x;
   const int it = nitems > 1 ? find_item(items, nitems, cta) : 0;
@@ -119,7 +127,10 @@ __global__ void __launch_bounds__(kTX* kTY, 2)
   const int color = ctl->color;
   if (tid == 0) {
 #pragma unroll
-    for (int q = 0; q < kStages; ++q) mbar_init(&bars[q], 1);
+    for (int q = 0; q < kStages; ++q) {
+      mbar_init(&bars[q], 1);
+      if (WS) mbar_init(&empty_bars[q], kTY);  // one arrive per consumer warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < 8) {
@@ -150,9 +161,17 @@ __global__ void __launch_bounds__(kTX* kTY, 2)
     tma_load_3d(&st.p[0][0], mP, &bars[stage], xc, yc, zc0 + plane);
     tma_load_3d(&st.w[0][0], mW, &bars[stage], xc, yc, zc0 + plane);
   };
-  if (tid == 0) {
+  if (!WS && tid == 0) {
     const int npro = nplanes < kStages ? nplanes : kStages;
     for (int q = 0; q < npro; ++q) issue(q, q);
+  }
+  if (WS && producer_warp) {
+    if (tx == 0)
+      for (int kk = 0; kk < nplanes; ++kk) {
+        const int st = kk % kStages;
+        if (kk >= kStages) mbar_wait(&empty_bars[st], (uint32_t)(((kk / kStages) - 1) & 1));
+        issue(st, kk);
+      }
   }
 
   double* __restrict__ Dn = tab->ptr[b][SF_DIVU][ALT];
@@ -165,7 +184,7 @@ __global__ void __launch_bounds__(kTX* kTY, 2)
   const double cu = dt * s.ix, cv = dt * s.iy, cw = dt * s.iz;
 
   const long long i = i0 + tx, j = j0 + ty;
-  const bool act = i < wk.hi[0] && j < wk.hi[1];
+  const bool act = !producer_warp && i < wk.hi[0] && j < wk.hi[1];
   const long long n0 = B.n[0], n1 = B.n[1], n2 = B.n[2];
   const long long sx = B.sx, sxy = B.sx * B.sy;
   const long long gi = B.lo[0] + i, gj = B.lo[1] + j;
@@ -192,6 +211,18 @@ __global__ void __launch_bounds__(kTX* kTY, 2)
   const double pv_w = fzh == FACE_WALL ? B.fvel[5][2] : 0.0;
   const bool xm_swept = i > 0 || fxl == FACE_PROC || fxl == FACE_SELF;
   const bool ym_swept = j > 0 || fyl == FACE_PROC || fyl == FACE_SELF;
+  // Interior column: every x/y scale bit of the cell and of its -x/-y
+  // neighbours is 1 (so each -(beta*bscale) is -(beta*1.0)), the -x/-y
+  // neighbours are owned cells of opposite parity, and no pin or ghost write
+  // applies.  The z part is checked per plane.  The fast path evaluates the
+  // identical IEEE operations in the identical order, so it is bitwise the
+  // general path restricted to such cells.
+  const bool col_fast = i >= 1 && i <= n0 - 2 && j >= 1 && j <= n1 - 2 && bx && bxp && bxm &&
+                        bxpm && by && byp && bym && bypm;
+  const double mbI = smb[7];  // -(beta * bscale[1][1][1])
+  const int zlo_fast = (int)max(1ll, (per2 ? 0ll : 1ll) - B.lo[2]);  // local k range of the fast path
+  const int zhi_fast = (int)min(n2 - 2, (per2 ? n2 - 2 : s.nm1[2] - 2 - B.lo[2]));
+  const int par_col = (int)((gi + gj) & 1);
 
   long long o = off(B, i, j, k0);
   unsigned long long rmax = 0ull;
@@ -211,13 +242,45 @@ __global__ void __launch_bounds__(kTX* kTY, 2)
     }
   }
 
-  for (int kk = 0; kk < nplanes; ++kk, o += sxy) {
+  for (int kk = 0; kk < nplanes && !producer_warp; ++kk, o += sxy) {
     const int st = kk % kStages;
     mbar_wait(&bars[st], (uint32_t)((kk / kStages) & 1));
     const bool has_next = kk + 1 < nplanes;
     const int st1 = (kk + 1) % kStages;
     if (has_next) mbar_wait(&bars[st1], (uint32_t)(((kk + 1) / kStages) & 1));
-    if (act) {
+    const int kl = (int)(k0 + kk);
+    if (act && col_fast && kl >= zlo_fast && kl <= zhi_fast) {
+      const stage_t& T = S[st];
+      const double dC = T.d[ty + 1][tx + kXL];
+      const double dXp = T.d[ty + 1][tx + kXL + 1], dXm = T.d[ty + 1][tx + kXL - 1];
+      const double dYp = T.d[ty + 2][tx + kXL], dYm = T.d[ty][tx + kXL];
+      const double dZp = has_next ? S[st1].d[ty + 1][tx + kXL] : D[o + sxy];
+      const double p0 = T.p[ty][tx], u0 = T.u[ty][tx + kXL], uml = T.u[ty][tx + kXL - 1];
+      const double v0 = T.v[ty + 1][tx], vml = T.v[ty][tx], w0 = T.w[ty][tx];
+      const int par = par_col ^ ((int)(B.lo[2] + kl) & 1);
+      const double a0 = (par == color) ? 1.0 : 0.0, a1 = 1.0 - a0;
+      const double d0 = mbI * dC * a0;
+      const double ex = mbI * dXp * a1;
+      const double ey = mbI * dYp * a1;
+      const double ez = mbI * dZp * a1;
+      P[o] = p0 + d0;
+      const double un = u0 + cu * (d0 - ex);
+      const double vn = v0 + cv * (d0 - ey);
+      const double wn = w0 + cw * (d0 - ez);
+      // -x / -y neighbours: parity a1, their +x/+y term is mbI*dC*a0 == d0
+      const double umn = uml + cu * (mbI * dXm * a1 - d0);
+      const double vmn = vml + cv * (mbI * dYm * a1 - d0);
+      double dd = (un - umn) * s.ix;
+      dd += (vn - vmn) * s.iy;
+      dd += (wn - wm_new) * s.iz;
+      Un[o] = un;
+      Vn[o] = vn;
+      Wn[o] = wn;
+      Dn[o] = dd;
+      const unsigned long long bb = abs_bits(dd);
+      rmax = bb > rmax ? bb : rmax;
+      wm_new = wn;
+    } else if (act) {
       const stage_t& T = S[st];
       const long long k = k0 + kk;
       const long long gk = B.lo[2] + k;
@@ -301,8 +364,13 @@ __global__ void __launch_bounds__(kTX* kTY, 2)
       rmax = bb > rmax ? bb : rmax;
       wm_new = wn;
     }
-    __syncthreads();  // every thread is done with stage st
-    if (tid == 0 && kk + kStages < nplanes) issue(st, kk + kStages);
+    if (WS) {
+      __syncwarp();
+      if (tx == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty_bars[st])) : "memory");
+    } else {
+      __syncthreads();  // every thread is done with stage st
+      if (tid == 0 && kk + kStages < nplanes) issue(st, kk + kStages);
+    }
   }
 
   unsigned long long rm[1] = {rmax};
@@ -387,18 +455,42 @@ size_t sweep_map_offset(int b, int f, int s) {
   return offsetof(sweep_maps, m) + sizeof(CUtensorMap) * ((size_t)(b * SF_NFIELDS + f) * kSlots + s);
 }
 
+template <int STAGES, int MINB, bool WS>
+static void launch_variant(const table_view& vw, int nctas, int zc, const sf_consts& c,
+                           sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, cudaStream_t st) {
+  const size_t smem = sizeof(stage_t) * STAGES;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep_div_tma<STAGES, MINB, WS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  k_sweep_div_tma<STAGES, MINB, WS><<<nctas, dim3(kTX, kTY + (WS ? 1 : 0)), smem, st>>>(
+      vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas,
+      static_cast<const sweep_maps*>(maps));
+}
+
+// SF_SWEEP_VARIANT selects the pipeline shape for A/B runs (default 0).
+static int sweep_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SF_SWEEP_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_consts& c,
                           sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, cudaStream_t st) {
   if (nctas <= 0) return;
-  const size_t smem = sizeof(stage_t) * kStages;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sweep_div_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  switch (sweep_variant()) {
+    case 1: launch_variant<3, 3, false>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
+    case 2: launch_variant<4, 2, true>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
+    case 3: launch_variant<3, 3, true>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
+    case 4: launch_variant<6, 2, true>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
+    case 5: launch_variant<2, 4, false>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
+    default: launch_variant<4, 2, false>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
   }
-  k_sweep_div_tma<<<nctas, dim3(kTX, kTY), smem, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl,
-                                                        hflag, (unsigned)nctas,
-                                                        static_cast<const sweep_maps*>(maps));
 }
 
 }  // namespace sfb
