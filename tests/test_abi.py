@@ -157,3 +157,18 @@ def test_no_gpu_here_fails_loudly_not_silently():
     with pytest.raises(sfb.SfError) as e:
         sfb.Simulation(sfb.SolverConfig(extents=(8, 8, 8)), sfb.FluidParams())
     assert e.value.kind == "cuda"
+
+
+def test_cpp_header_compiles_against_the_library(tmp_path):
+    """The C++ face (include/sforge_b200.hpp) builds and links against the
+    in-tree library; without a GPU it reports the CUDA failure as an exception."""
+    import subprocess
+    exe = tmp_path / "cavity_cpp"
+    lib_dir = os.path.dirname(_lib.LIB_PATH)
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-I" + os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "cavity_cpp.cpp"), "-L" + lib_dir, "-lsfb200",
+                        "-Wl,-rpath," + lib_dir, "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    if sfb.lib().sf_device_count() == 0:
+        out = subprocess.run([str(exe), "8", "1"], capture_output=True, text=True)
+        assert out.returncode == 1 and "error:" in out.stdout

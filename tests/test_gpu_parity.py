@@ -314,3 +314,18 @@ def test_errors_keep_the_reference_texts():
         s.gather("q")
     with pytest.raises(sfb.ConfigError, match="sigma must lie in"):
         sfb.Simulation(sfb.SolverConfig(extents=(8, 8, 8), sigma=1.0), sfb.FluidParams())
+
+
+def test_cpp_drop_in_reproduces_the_golden_checksum(tmp_path):
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.join(root, "paper_1201_2118_b200", "_lib")
+    exe = tmp_path / "cavity_cpp"
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-I" + os.path.join(root, "include"),
+                        os.path.join(root, "tests", "cpp", "cavity_cpp.cpp"), "-L" + lib_dir, "-lsfb200",
+                        "-Wl,-rpath," + lib_dir, "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe), "64", "1", "2"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "checksum=1b07d1f577d4bad0" in out.stdout
+    assert "exec_error: kernel 'PRESSURE_SWEEP': parameter 'beta' not supplied" in out.stdout
