@@ -193,23 +193,60 @@ def cpu_threads(args):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def weak_extents(n, world):
+    """Global grid with an n^3 block per rank: double x, y, z in turn per factor
+    of two (2: 2n x n x n, 4: 2n x 2n x n, 8: (2n)^3), the weak-scaling configs
+    of BASELINE.json configs[2]; grid::decompose then picks exactly that grid."""
+    p, w, a = [1, 1, 1], world, 0
+    while w % 2 == 0:
+        p[a % 3] *= 2
+        w //= 2
+        a += 1
+    p[0] *= w
+    return tuple(n * q for q in p)
+
+
 def run_ours(args):
     import torch
 
     import paper_1201_2118_b200 as sfb
 
     rank, world, local = dist_env()
-    if world > 1:
-        raise SystemExit("multi-GPU bench: see bench_multi (not in this build)")
     dev = local
     torch.cuda.set_device(dev)
     n, S = args.n, args.sweeps
-    cells = n * n * n
-    cfg = cavity_cfg(sfb, n, S)
     fused = {"tma": 1, "ldg": 2, "unfused": 0}[args.variant]
-    sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=1, device=dev, fused=fused)
+    dist = None
+    if world > 1:  # one rank per GPU over NCCL, weak scaling: n^3 per rank
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        uid = [sfb.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ext = weak_extents(n, world)
+        d = sfb.decompose(ext, world, 1)
+        assert all(d.size(w) == (n, n, n) for w in range(world)), d
+        cfg = cavity_cfg(sfb, n, S)
+        cfg.extents = ext
+        sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), device=dev, fused=fused, rank=rank, world=world,
+                             nccl_id=uid[0])
+    else:
+        cfg = cavity_cfg(sfb, n, S)
+        sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=1, device=dev, fused=fused)
+    cells = n * n * n          # per rank
+    total_cells = cells * world
     sim.init_cavity()
     stream = torch.cuda.ExternalStream(sim.stream, device=dev)
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
 
     for _ in range(args.warmup):
         sim.step()
@@ -218,6 +255,7 @@ def run_ours(args):
     clocks = ClockSampler(dev)
     sim.set_kernel_timing(True)
     sim.launch_count(reset=True)
+    barrier()
     torch.cuda.synchronize()
     clocks.start()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -226,13 +264,15 @@ def run_ours(args):
     stats = [sim.step() for _ in range(args.steps)]
     e1.record(stream)
     torch.cuda.synchronize()
+    barrier()
     clk = clocks.stop()
-    ms_total = e0.elapsed_time(e1)
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
     launches = sim.launch_count()
     k_ms, k_n = sim.kernel_timing("sweep_div")
+    k_ms = max_over_ranks(k_ms)
     sim.set_kernel_timing(False)
     ms_per_step = ms_total / args.steps
-    value = cells * args.steps / (ms_total / 1e3) / 1e6
+    value = total_cells * args.steps / (ms_total / 1e3) / 1e6
     sweeps_done = sum(s.sweeps for s in stats)
     assert sweeps_done == S * args.steps, "fixed-work config must run exactly max_sweeps per step"
 
@@ -256,32 +296,35 @@ def run_ours(args):
     # ---- end to end through the public API with host buffers -------------------
     e2e = None
     if not args.no_e2e:
+        # each rank moves its own block (sf_sim_scatter_block / gather_block);
+        # at N=1 the block is the whole grid
         names = ("vx", "vy", "vz", "p")
-        host_in = {f: torch.from_numpy(sim.gather(f)).pin_memory() for f in names}
+        host_in = {f: torch.from_numpy(sim.gather_block(f)).reshape(-1).pin_memory() for f in names}
         host_out = {f: torch.empty(cells, dtype=torch.float64).pin_memory() for f in names}
         for f in names:  # one untimed warm trip
-            sim.scatter(f, host_in[f])
+            sim.scatter_block(f, host_in[f])
         sim.step()
         for f in names:
-            sim.gather(f, out=host_out[f])
+            sim.gather_block(f, out=host_out[f])
+        barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e0.record(stream)
         for _ in range(args.steps):
             for f in names:
-                sim.scatter(f, host_in[f])
+                sim.scatter_block(f, host_in[f])
             sim.step()
             for f in names:
-                sim.gather(f, out=host_out[f])
+                sim.gather_block(f, out=host_out[f])
         e1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         e_ms = max(e0.elapsed_time(e1), 0.0)
-        e_ms = max(e_ms, wall * 1e3)  # host-side copies can run outside the events
-        e2e = {"value": round(cells * args.steps / (e_ms / 1e3) / 1e6, 3), "unit": UNIT,
-               "h2d_bytes_per_step": 4 * cells * 8, "d2h_bytes_per_step": 4 * cells * 8,
+        e_ms = max_over_ranks(max(e_ms, wall * 1e3))  # host-side copies can run outside the events
+        e2e = {"value": round(total_cells * args.steps / (e_ms / 1e3) / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * total_cells * 8, "d2h_bytes_per_step": 4 * total_cells * 8,
                "ms_per_step": round(e_ms / args.steps, 3),
-               "path": "sf_sim_scatter(vx,vy,vz,p) from pinned host -> sf_sim_step -> sf_sim_gather(vx,vy,vz,p) to pinned host"}
+               "path": "sf_sim_scatter_block(vx,vy,vz,p) from pinned host -> sf_sim_step -> sf_sim_gather_block(vx,vy,vz,p) to pinned host, per rank"}
 
     # ---- CPU baseline (rank 0, N=1): the reference on this host, bounded sample --
     cpu = None
@@ -301,19 +344,27 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (lid-driven cavity from rest, init_cavity)",
-        "config": {"workload": f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)",
-                   "grid": [n, n, n], "ghost": 1, "sweeps_per_step": S, "parallelism": "1 GPU",
+        "config": {"workload": (f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)"
+                                if world == 1 else
+                                f"3D lid-driven cavity, {n}^3 per GPU weak scaling, global {list(cfg.extents)} block-decomposed over {world} B200 with NCCL ghost exchange (BASELINE.json configs[2]), {S} half-sweeps per step"),
+                   "grid": list(cfg.extents), "ghost": 1, "sweeps_per_step": S,
+                   "parallelism": "1 GPU" if world == 1 else f"{world} ranks, block decomposition (grid::decompose), NCCL halo + allreduce",
                    "path": {"tma": "fused half-sweep, TMA pipeline", "ldg": "fused half-sweep, plain loads",
                             "unfused": "unfused (reference dataflow)"}[args.variant],
                    "l2": "inputs larger than L2: 9 resident fp64 arrays of %.2f GB" % (cells * 8 / 1e9)},
-        "half_sweep_rate": round(cells * sweeps_done / (ms_total / 1e3) / 1e6, 1),
+        "half_sweep_rate": round(total_cells * sweeps_done / (ms_total / 1e3) / 1e6, 1),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk,
     }
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        sim.close()
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------

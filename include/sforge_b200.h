@@ -166,6 +166,33 @@ int sf_sim_invalidate_ghosts(sf_sim* s, const char* field);                  /* 
 int sf_sim_invalidate_all_ghosts(sf_sim* s);                                 /* :613 */
 int sf_sim_ghosts_valid(sf_sim* s, const char* field);                       /* :610 */
 
+/* ---- one process per GPU ---------------------------
+ * Rank r of `world` owns grid component r of grid::decompose(dom, world, g,
+ * periodic); ghost faces between ranks move over NCCL (send/recv per peer and
+ * refresh phase), the per-sweep residual, dt maxima and NaN guard over
+ * ncclAllReduce(max).  Rank 0 creates the NCCL unique id (128 bytes), the
+ * caller broadcasts it (e.g. torch.distributed) and every rank calls
+ * sf_sim_create_distributed collectively.  opt->workers must be 1. */
+int sf_nccl_unique_id(void* out128);
+int sf_sim_create_distributed(const sf_solver_config* cfg, const sf_fluid_params* par,
+                              const sf_sim_options* opt, int rank, int world, const void* nccl_id,
+                              sf_sim** out);
+int sf_sim_rank(const sf_sim* s);
+int sf_sim_world(const sf_sim* s);
+/* Owned cells of one grid component (global worker id) as a dense x-fastest
+ * host array of dims[0]*dims[1]*dims[2] values: the per-rank slice of
+ * grid::gather / grid::scatter (io.hpp:25-65). */
+int sf_sim_gather_block(sf_sim* s, const char* field, int worker, double* host, int64_t n);
+int sf_sim_scatter_block(sf_sim* s, const char* field, int worker, const double* host, int64_t n);
+/* The exchange plan of one refresh phase (axis 0..2, slabs widened as in
+ * exchange.hpp:165-206) or of the fused loop's face exchange (axis = -1) for
+ * rank `rank` of a `world`-rank decomposition -- host logic, no device.  Rows
+ * of 15 int64: kind (0 send, 1 recv, 2 local copy), peer, field, axis, side,
+ * lo[3], dims[3], dlo[3], count; sends and receives per peer in posting order
+ * (sender: sides 0,1; receiver: sides 1,0). */
+int sf_exchange_plan(const int64_t extents[3], int world, int ghost, const int periodic[3], int rank,
+                     unsigned field_mask, int axis, int max_msgs, int64_t* out, int* n_out);
+
 /* Device plumbing for benches and transports. */
 int sf_sim_synchronize(sf_sim* s);
 void* sf_sim_stream(sf_sim* s);            /* the cudaStream_t all work is ordered on */

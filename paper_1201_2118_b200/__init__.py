@@ -15,9 +15,10 @@ from .sim import (  # noqa: F401
     StepStats,
     cavity_fluid,
     decompose,
+    nccl_unique_id,
 )
 
 __all__ = [
     "Simulation", "SolverConfig", "FluidParams", "StepStats", "cavity_fluid", "decompose",
-    "Decomposition", "FIELDS", "SfError", "ConfigError", "GridError", "ExecError", "CfdError", "lib",
+    "Decomposition", "nccl_unique_id", "FIELDS", "SfError", "ConfigError", "GridError", "ExecError", "CfdError", "lib",
 ]

@@ -159,6 +159,14 @@ SIGNATURES = [
     ("sf_sim_invalidate_ghosts", [_vp, _cp], _i),
     ("sf_sim_invalidate_all_ghosts", [_vp], _i),
     ("sf_sim_ghosts_valid", [_vp, _cp], _i),
+    ("sf_nccl_unique_id", [_vp], _i),
+    ("sf_sim_create_distributed", [C.POINTER(SolverConfig), C.POINTER(FluidParams), C.POINTER(SimOptions),
+                                   _i, _i, _vp, C.POINTER(_vp)], _i),
+    ("sf_sim_rank", [_vp], _i),
+    ("sf_sim_world", [_vp], _i),
+    ("sf_sim_gather_block", [_vp, _cp, _i, _vp, _i64], _i),
+    ("sf_sim_scatter_block", [_vp, _cp, _i, _vp, _i64], _i),
+    ("sf_exchange_plan", [_i64p, _i, _i, _ip, _i, C.c_uint, _i, _i, _i64p, _ip], _i),
     ("sf_sim_synchronize", [_vp], _i),
     ("sf_sim_stream", [_vp], _vp),
     ("sf_sim_launch_count", [_vp, _i], _i64),

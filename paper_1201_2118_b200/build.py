@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libsfb200.so")
 SOURCES = ["sf_kernels.cu", "sf_sweep_tma.cu", "sf_driver.cu"]
-HEADERS = ["sf_device.cuh", "sf_kernels.cuh"]
+HEADERS = ["sf_device.cuh", "sf_kernels.cuh", "sf_plan.hpp"]
 
 NVCC_FLAGS = [
     "-std=c++17",
@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed for %s:\n%s" % (s, r.stdout + r.stderr))
         objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs]
+    cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc link failed:\n%s" % (r.stdout + r.stderr))

@@ -25,7 +25,10 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+
 #include "sf_kernels.cuh"
+#include "sf_plan.hpp"
 
 namespace sfb {
 
@@ -44,6 +47,65 @@ struct error : std::runtime_error {
   } while (0)
 
 static thread_local std::string g_last_error;
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded at run time (the libnccl.so.2 torch already mapped into the
+// process when there is one).  Types restated from nccl.h (stable ABI).
+// ---------------------------------------------------------------------------
+struct nccl_uid {
+  char internal[128];
+};
+typedef struct ncclComm* nccl_comm_t;
+enum { kNcclUint64 = 5, kNcclFloat64 = 8, kNcclMax = 2 };
+struct nccl_api {
+  int (*GetUniqueId)(nccl_uid*) = nullptr;
+  int (*CommInitRank)(nccl_comm_t*, int, nccl_uid, int) = nullptr;
+  int (*CommDestroy)(nccl_comm_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  int (*Send)(const void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+
+static nccl_api* nccl() {
+  static nccl_api api;
+  static bool tried = false;
+  if (tried) return api.Send ? &api : nullptr;
+  tried = true;
+  void* h = nullptr;
+  if (const char* e = getenv("SF_NCCL_LIB")) h = dlopen(e, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return nullptr;
+  auto sym = [&](const char* n) { return dlsym(h, n); };
+  api.GetUniqueId = (int (*)(nccl_uid*))sym("ncclGetUniqueId");
+  api.CommInitRank = (int (*)(nccl_comm_t*, int, nccl_uid, int))sym("ncclCommInitRank");
+  api.CommDestroy = (int (*)(nccl_comm_t))sym("ncclCommDestroy");
+  api.GroupStart = (int (*)())sym("ncclGroupStart");
+  api.GroupEnd = (int (*)())sym("ncclGroupEnd");
+  api.Send = (int (*)(const void*, size_t, int, int, nccl_comm_t, cudaStream_t))sym("ncclSend");
+  api.Recv = (int (*)(void*, size_t, int, int, nccl_comm_t, cudaStream_t))sym("ncclRecv");
+  api.AllReduce = (int (*)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t))sym("ncclAllReduce");
+  api.AllGather = (int (*)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t))sym("ncclAllGather");
+  api.GetErrorString = (const char* (*)(int))sym("ncclGetErrorString");
+  if (!api.GetUniqueId || !api.CommInitRank || !api.Send || !api.Recv || !api.AllReduce ||
+      !api.AllGather || !api.GroupStart || !api.GroupEnd) {
+    api.Send = nullptr;
+    return nullptr;
+  }
+  return &api;
+}
+
+#define SF_NC(x)                                                                              \
+  do {                                                                                        \
+    const int r_ = (x);                                                                       \
+    if (r_ != 0)                                                                              \
+      throw ::sfb::error(SF_ERR_CUDA, std::string("NCCL: ") + #x + ": " +                     \
+                                          (::sfb::nccl()->GetErrorString ? ::sfb::nccl()->GetErrorString(r_) : "?")); \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // decomposition (grid.hpp:44-163), same choices and error texts
@@ -221,18 +283,45 @@ static const std::vector<kernel_plan>& cfd_plans() {
 
 class simulation {
  public:
-  simulation(const sf_solver_config& cfg, const sf_fluid_params& par, const sf_sim_options& opt)
-      : cfg_(cfg), par_(par), opt_(opt) {
+  // world > 1: one process per GPU; this rank owns grid component `rank` of
+  // grid::decompose(dom, world, ghost, periodic) and talks to the others over
+  // NCCL (communicator from `uid`, created collectively here).
+  simulation(const sf_solver_config& cfg, const sf_fluid_params& par, const sf_sim_options& opt,
+             int rank = 0, int world = 1, const void* uid = nullptr)
+      : cfg_(cfg), par_(par), opt_(opt), rank_(rank), world_(world) {
     validate();
     const bool per[3] = {cfg.periodic[0] != 0, cfg.periodic[1] != 0, cfg.periodic[2] != 0};
     const i64 ext[3] = {cfg.extents[0], cfg.extents[1], cfg.extents[2]};
-    dec_ = decompose(ext, cfg.spacing, opt.workers, opt.ghost, per);
-    if (dec_.workers > kMaxBlocks)
+    dist_ = uid != nullptr;
+    if (dist_) {
+      if (opt.workers != 1)
+        throw error(SF_ERR_ARG, "distributed mode owns one grid component per rank (workers must be 1)");
+      if (rank_ < 0 || rank_ >= world_) throw error(SF_ERR_ARG, "rank out of range");
+      dec_ = decompose(ext, cfg.spacing, world_, opt.ghost, per);
+      gid_ = {rank_};
+      owner_.resize(world_);
+      for (int w = 0; w < world_; ++w) owner_[w] = w;
+    } else {
+      dec_ = decompose(ext, cfg.spacing, opt.workers, opt.ghost, per);
+      for (int w = 0; w < dec_.workers; ++w) gid_.push_back(w);
+      owner_.assign(dec_.workers, 0);
+    }
+    nloc_ = (int)gid_.size();
+    lid_.assign(dec_.workers, -1);
+    for (int b = 0; b < nloc_; ++b) lid_[gid_[b]] = b;
+    if (nloc_ > kMaxBlocks)
       throw error(SF_ERR_ARG, "at most " + std::to_string(kMaxBlocks) + " workers per device");
     make_bc();
     make_consts();
     SF_CK(cudaSetDevice(opt.device));
     SF_CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    if (dist_) {
+      if (!nccl()) throw error(SF_ERR_CUDA, "NCCL library not found (set SF_NCCL_LIB)");
+      if (!uid) throw error(SF_ERR_ARG, "distributed mode needs the NCCL unique id of rank 0");
+      nccl_uid id;
+      std::memcpy(&id, uid, sizeof id);
+      SF_NC(nccl()->CommInitRank(&comm_, world_, id, rank_));
+    }
     allocate();
     SF_CK(cudaEventCreateWithFlags(&ev_[0], cudaEventDisableTiming));
     SF_CK(cudaEventCreateWithFlags(&ev_[1], cudaEventDisableTiming));
@@ -254,6 +343,7 @@ class simulation {
     cudaEventDestroy(t0_);
     cudaEventDestroy(t1_);
     for (auto e : timers_) cudaEventDestroy(e);
+    if (comm_ && nccl() && nccl()->CommDestroy) nccl()->CommDestroy(comm_);
     cudaStreamDestroy(st_);
   }
 
@@ -279,7 +369,7 @@ class simulation {
   }
   void fill_const(int f, double v) {
     download_table();
-    for (int b = 0; b < dec_.workers; ++b) {
+    for (int b = 0; b < nloc_; ++b) {
       const auto& L = lay_[b];
       const i64 lo[3] = {0, 0, 0};
       const i64 dims[3] = {L.dims[0], L.dims[1], L.dims[2]};
@@ -334,7 +424,7 @@ class simulation {
   void gather_to_device(int f, double* dglobal) {
     download_table();
     const i64 N[3] = {cfg_.extents[0], cfg_.extents[1], cfg_.extents[2]};
-    for (int b = 0; b < dec_.workers; ++b) {
+    for (int b = 0; b < nloc_; ++b) {
       const auto& L = lay_[b];
       const i64 n[3] = {L.dims[0], L.dims[1], L.dims[2]};
       const i64 lo[3] = {L.lo[0], L.lo[1], L.lo[2]};
@@ -346,7 +436,7 @@ class simulation {
   void scatter_from_device(int f, const double* dglobal) {
     download_table();
     const i64 N[3] = {cfg_.extents[0], cfg_.extents[1], cfg_.extents[2]};
-    for (int b = 0; b < dec_.workers; ++b) {
+    for (int b = 0; b < nloc_; ++b) {
       const auto& L = lay_[b];
       const i64 n[3] = {L.dims[0], L.dims[1], L.dims[2]};
       const i64 lo[3] = {L.lo[0], L.lo[1], L.lo[2]};
@@ -357,7 +447,69 @@ class simulation {
     check_launch();
     ghosts_ok_[kFieldNames[f]] = false;
   }
+  // grid::gather across ranks: every rank packs its owned block, one
+  // all-gather, every rank places all blocks (bitwise, no arithmetic)
+  void gather_global(int f, double* host) {
+    download_table();
+    i64 maxc = 0;
+    for (int w = 0; w < dec_.workers; ++w) {
+      const auto d = dec_.dims(w);
+      maxc = std::max(maxc, d[0] * d[1] * d[2]);
+    }
+    double* snd = (double*)dalloc_tmp(sizeof(double) * (size_t)maxc);
+    double* all = (double*)dalloc_tmp(sizeof(double) * (size_t)(maxc * world_));
+    const auto& L = lay_[0];
+    const i64 n[3] = {L.dims[0], L.dims[1], L.dims[2]};
+    const i64 z[3] = {0, 0, 0};
+    launch_copy_box(htab_->ptr[0][f][FRONT], L.base, L.sx, L.sy, snd, 0, n[0], n[1], z, n, z, st_);
+    ++launches_;
+    SF_NC(nccl()->AllGather(snd, all, (size_t)maxc, kNcclFloat64, comm_, st_));
+    std::vector<double> h((size_t)(maxc * world_));
+    SF_CK(cudaMemcpyAsync(h.data(), all, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st_));
+    sync();
+    SF_CK(cudaFree(snd));
+    SF_CK(cudaFree(all));
+    const i64 N0 = cfg_.extents[0], N1 = cfg_.extents[1];
+    for (int w = 0; w < dec_.workers; ++w) {
+      const auto d = dec_.dims(w);
+      const double* src = h.data() + (size_t)(maxc * w);
+      for (i64 k = 0; k < d[2]; ++k)
+        for (i64 j = 0; j < d[1]; ++j)
+          std::memcpy(host + ((dec_.lo[w][2] + k) * N1 + dec_.lo[w][1] + j) * N0 + dec_.lo[w][0],
+                      src + (k * d[1] + j) * d[0], sizeof(double) * (size_t)d[0]);
+    }
+  }
+  // owned block of local component w (global worker id) <-> dense x-fastest host array
+  void block_io(int f, int w, double* host, i64 n, bool to_device) {
+    if (w < 0 || w >= dec_.workers || lid_[w] < 0)
+      throw error(SF_ERR_ARG, "worker " + std::to_string(w) + " is not owned by this process");
+    const int b = lid_[w];
+    const auto& L = lay_[b];
+    const i64 d[3] = {L.dims[0], L.dims[1], L.dims[2]};
+    if (n < d[0] * d[1] * d[2]) throw error(SF_ERR_ARG, "block buffer too small");
+    download_table();
+    double* sg = staging();
+    const i64 z[3] = {0, 0, 0};
+    if (to_device) {
+      SF_CK(cudaMemcpyAsync(sg, host, sizeof(double) * (size_t)(d[0] * d[1] * d[2]), cudaMemcpyHostToDevice, st_));
+      launch_copy_box(sg, 0, d[0], d[1], htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, z, d, z, st_);
+      ghosts_ok_[kFieldNames[f]] = false;
+    } else {
+      launch_copy_box(htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, sg, 0, d[0], d[1], z, d, z, st_);
+      SF_CK(cudaMemcpyAsync(host, sg, sizeof(double) * (size_t)(d[0] * d[1] * d[2]), cudaMemcpyDeviceToHost, st_));
+    }
+    ++launches_;
+    check_launch();
+    sync();
+  }
+  int rank() const { return rank_; }
+  int world() const { return world_; }
+
   void gather(int f, double* host) {
+    if (dist_) {
+      gather_global(f, host);
+      return;
+    }
     double* sg = staging();
     gather_to_device(f, sg);
     SF_CK(cudaMemcpyAsync(host, sg, sizeof(double) * (size_t)cells(), cudaMemcpyDeviceToHost, st_));
@@ -370,7 +522,9 @@ class simulation {
     if (do_sync) sync();
   }
   void local_front(int f, int w, double* host, i64 host_elems, i64 dims[3], i64 lo[3]) {
-    if (w < 0 || w >= dec_.workers) throw error(SF_ERR_ARG, "worker index out of range");
+    if (w < 0 || w >= dec_.workers || lid_[w] < 0)
+      throw error(SF_ERR_ARG, "worker " + std::to_string(w) + " is not owned by this process");
+    w = lid_[w];
     const auto& L = lay_[w];
     const int g = L.ghost;
     const i64 ld[3] = {L.dims[0] + 2 * g, L.dims[1] + 2 * g, L.dims[2] + 2 * g};
@@ -416,24 +570,14 @@ class simulation {
     validate_bc(fields);
     unsigned mask = 0;
     for (int f : fields) mask |= 1u << f;
-    for (int axis = 0; axis < 3; ++axis) {
-      const task_set& ts = tasks_for(mask, axis, SF_SCOPE_ALL, false);
-      if (ts.n == 0) continue;
-      launch_tasks(tview(), ts.d, ts.n, ts.max_count, predicated ? dctl_ : nullptr, st_);
-      ++launches_;
-    }
+    for (int axis = 0; axis < 3; ++axis) run_phase(phase_for(mask, axis, SF_SCOPE_ALL, false), predicated);
     check_launch();
     for (int f : fields) ghosts_ok_[kFieldNames[f]] = true;
   }
   void exchange_only(const std::vector<int>& fields) {
     unsigned mask = 0;
     for (int f : fields) mask |= 1u << f;
-    for (int axis = 0; axis < 3; ++axis) {
-      const task_set& ts = tasks_for(mask, axis, SF_SCOPE_ALL, true);
-      if (ts.n == 0) continue;
-      launch_tasks(tview(), ts.d, ts.n, ts.max_count, nullptr, st_);
-      ++launches_;
-    }
+    for (int axis = 0; axis < 3; ++axis) run_phase(phase_for(mask, axis, SF_SCOPE_ALL, true), false);
     check_launch();
     for (int f : fields) ghosts_ok_[kFieldNames[f]] = true;
   }
@@ -488,6 +632,7 @@ class simulation {
                         &dctl_->acc[7], st_);
       ++launches_;
       check_launch();
+      allreduce_max(&dctl_->acc[7], 1);
       return read_acc(7);
     }
     const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_plain_);
@@ -501,6 +646,17 @@ class simulation {
     SF_CK(cudaFree(parts));
     double acc = 0.0;
     for (double x : hp) acc += x;
+    if (dist_) {  // partials combined in rank order, as reductions.hpp:75-88 does
+      double* d = (double*)dalloc_tmp(sizeof(double) * (size_t)(world_ + 1));
+      SF_CK(cudaMemcpyAsync(d, &acc, sizeof(double), cudaMemcpyHostToDevice, st_));
+      SF_NC(nccl()->AllGather(d, d + 1, 1, kNcclFloat64, comm_, st_));
+      std::vector<double> all(world_);
+      SF_CK(cudaMemcpyAsync(all.data(), d + 1, sizeof(double) * world_, cudaMemcpyDeviceToHost, st_));
+      sync();
+      SF_CK(cudaFree(d));
+      acc = all[0];
+      for (int r = 1; r < world_; ++r) acc += all[r];
+    }
     return acc;
   }
 
@@ -511,6 +667,7 @@ class simulation {
     ctl(CTL_CLEAR_ACC);
     launch_reduce_max(tview(ws), ws.nctas, zc_plain_, fl, 3, 0, &dctl_->acc[0], st_);
     ++launches_;
+    allreduce_max(&dctl_->acc[0], 3);
     ctl(CTL_DT_FROM_ACC);
     check_launch();
   }
@@ -528,6 +685,7 @@ class simulation {
     check_launch();
     swap_front_back();
     for (int f : {SF_VX, SF_VY, SF_VZ}) ghosts_ok_[kFieldNames[f]] = false;
+    allreduce_max(&dctl_->acc[1], 3);
     ctl(CTL_CHECK_FINITE);
   }
   void check_finite_or_throw() {
@@ -629,6 +787,7 @@ class simulation {
     launch_divergence(tview(wd), wd.nctas, zc_plain_, consts_, dctl_, 7, 0, st_);
     ++launches_;
     check_launch();
+    allreduce_max(&dctl_->acc[7], 1);
     ghosts_ok_["divu"] = false;
     return read_acc(7);
   }
@@ -689,7 +848,14 @@ class simulation {
   sf_solver_config cfg_;
   sf_fluid_params par_;
   sf_sim_options opt_;
+  int rank_ = 0, world_ = 1;
+  bool dist_ = false;  // NCCL transport (one grid component per rank)
   decomposition dec_;
+  int nloc_ = 0;
+  std::vector<int> gid_;    // local block -> global worker id
+  std::vector<int> lid_;    // global worker id -> local block, or -1
+  std::vector<int> owner_;  // global worker id -> rank
+  nccl_comm_t comm_ = nullptr;
   sf_face_bc bc_[6]{};
   sf_consts consts_{};
   std::vector<sf_layout> lay_;
@@ -806,11 +972,12 @@ class simulation {
   void allocate() {
     htab_ = std::make_unique<sf_dev_table>();
     std::memset(htab_.get(), 0, sizeof(sf_dev_table));
-    htab_->nblocks = dec_.workers;
-    lay_.resize(dec_.workers);
-    for (int b = 0; b < dec_.workers; ++b) {
-      const auto dims = dec_.dims(b);
-      const i64 lo[3] = {dec_.lo[b][0], dec_.lo[b][1], dec_.lo[b][2]};
+    htab_->nblocks = nloc_;
+    lay_.resize(nloc_);
+    for (int b = 0; b < nloc_; ++b) {
+      const int gw = gid_[b];
+      const auto dims = dec_.dims(gw);
+      const i64 lo[3] = {dec_.lo[gw][0], dec_.lo[gw][1], dec_.lo[gw][2]};
       const i64 dd[3] = {dims[0], dims[1], dims[2]};
       lay_[b] = make_layout(dd, lo, dec_.ghost);
       const sf_layout& L = lay_[b];
@@ -827,14 +994,14 @@ class simulation {
       for (int a = 0; a < 3; ++a)
         for (int side = 0; side < 2; ++side) {
           const int fi = 2 * a + side;
-          const int nb = dec_.neighbor(b, a, side);
+          const int nb = dec_.neighbor(gw, a, side);
           if (nb < 0) {
             const int k = bc_[fi].kind;
             B.face[fi] = k == SF_BC_WALL ? FACE_WALL
                          : k == SF_BC_SYMMETRY ? FACE_SYM
                          : k == SF_BC_OUTFLOW ? FACE_OUT : FACE_WALL;
           } else {
-            B.face[fi] = nb == b ? FACE_SELF : FACE_PROC;
+            B.face[fi] = nb == gw ? FACE_SELF : FACE_PROC;
           }
           for (int c = 0; c < 3; ++c) B.fvel[fi][c] = bc_[fi].velocity[c];
           const i64 N = cfg_.extents[a];
@@ -857,7 +1024,7 @@ class simulation {
     {
       std::vector<unsigned char> hm(sweep_maps_bytes(), 0);
       bool ok = true;
-      for (int b = 0; b < dec_.workers && ok; ++b)
+      for (int b = 0; b < nloc_ && ok; ++b)
         for (int f = 0; f < SF_NFIELDS && ok; ++f)
           for (int s = 0; s < kSlots && ok; ++s) {
             double* p = htab_->ptr[b][f][s];
@@ -915,8 +1082,8 @@ class simulation {
     if (it != items_.end()) return it->second;
     std::vector<sf_work> v;
     int cta = 0;
-    for (int b = 0; b < dec_.workers; ++b) {
-      const auto dims = dec_.dims(b);
+    for (int b = 0; b < nloc_; ++b) {
+      const auto dims = dec_.dims(gid_[b]);
       for (const auto& bx : region_boxes(dims, halo, reg)) {
         sf_work w{};
         w.blk = b;
@@ -953,78 +1120,25 @@ class simulation {
     }
   }
 
-  // One axis phase of exchanger::refresh_worker (exchange.hpp:107-119): the
-  // messages of pack_axis (:165-206) as block-to-block copies plus the
-  // bc_face fills (:231-480) of that axis.  All tasks of a phase are
-  // independent (disjoint writes, reads of owned cells / earlier phases).
-  const task_set& tasks_for(unsigned mask, int axis, int scope, bool exchange_only) {
-    char key[64];
-    std::snprintf(key, sizeof key, "%u:%d:%d:%d", mask, axis, scope, exchange_only ? 1 : 0);
-    auto it = tasks_.find(key);
-    if (it != tasks_.end()) return it->second;
-    std::vector<sf_task> v;
-    const i64 g = dec_.ghost;
-    for (int w = 0; w < dec_.workers; ++w) {
-      const auto dims = dec_.dims(w);
-      for (int f = 0; f < SF_NFIELDS; ++f) {
-        if (!(mask & (1u << f))) continue;
-        for (int side = 0; side < 2; ++side) {
-          const int nb = dec_.neighbor(w, axis, side);
-          sf_task t{};
-          t.field = f;
-          t.axis = axis;
-          t.side = side;
-          if (nb >= 0) {
-            if (g == 0) continue;
-            t.type = 0;
-            t.src_blk = w;
-            t.dst_blk = nb;
-            const auto nbd = dec_.dims(nb);
-            for (int a = 0; a < 3; ++a) {
-              if (a == axis) {
-                t.lo[a] = side == 0 ? 0 : dims[a] - g;
-                t.dims[a] = g;
-                t.dlo[a] = side == 0 ? nbd[a] : -g;
-              } else if (a < axis) {
-                t.lo[a] = -g;
-                t.dims[a] = dims[a] + 2 * g;
-                t.dlo[a] = t.lo[a];
-              } else {
-                t.lo[a] = 0;
-                t.dims[a] = dims[a];
-                t.dlo[a] = 0;
-              }
-            }
-            t.count = t.dims[0] * t.dims[1] * t.dims[2];
-          } else {
-            if (exchange_only) continue;
-            const sf_face_bc& fb = bc_[2 * axis + side];
-            t.type = 1;
-            t.src_blk = t.dst_blk = w;
-            t.kind = fb.kind;
-            t.scope = scope;
-            t.normal = kStagger[f] == axis;
-            t.velocity = kStagger[f] >= 0;
-            const double vwall = t.velocity ? fb.velocity[kStagger[f]] : 0.0;
-            t.v = (t.normal && fb.kind == SF_BC_SYMMETRY) ? 0.0 : vwall;
-            for (int a = 0; a < 3; ++a) {
-              if (a == axis) {
-                t.lo[a] = 0;
-                t.dims[a] = 1;
-              } else if (a < axis) {
-                t.lo[a] = -g;
-                t.dims[a] = dims[a] + 2 * g;
-              } else {
-                t.lo[a] = 0;
-                t.dims[a] = dims[a];
-              }
-            }
-            t.count = t.dims[0] * t.dims[1] * t.dims[2];
-          }
-          v.push_back(t);
-        }
-      }
-    }
+  // One phase of exchanger::refresh_worker (exchange.hpp:107-119) on device:
+  // launch 1 = copies between local blocks + bc_face fills + packs of the
+  // messages to other ranks; then one NCCL group of per-peer send/recv; then
+  // launch 2 = unpacks.  All work of launch 1 is independent (disjoint writes;
+  // reads of owned cells and of ghosts filled by earlier phases).
+  struct phase {
+    task_set first;   // copies + bcs + packs
+    task_set unpack;
+    struct msg {
+      int peer;
+      long long off, count;
+    };
+    std::vector<msg> sends, recvs;
+    double* sbuf = nullptr;
+    double* rbuf = nullptr;
+  };
+  std::map<std::string, phase> phases_;
+
+  task_set upload_tasks(const std::vector<sf_task>& v) {
     task_set ts;
     ts.n = (int)v.size();
     for (const auto& t : v) ts.max_count = std::max(ts.max_count, t.count);
@@ -1032,68 +1146,133 @@ class simulation {
       ts.d = (sf_task*)dalloc(sizeof(sf_task) * v.size());
       SF_CK(cudaMemcpy(ts.d, v.data(), sizeof(sf_task) * v.size(), cudaMemcpyHostToDevice));
     }
-    return tasks_.emplace(key, ts).first->second;
+    return ts;
   }
 
-  // divu face copies between distinct blocks for the fused loop (faces only:
-  // the half-sweep never reads edge or corner ghosts of divu).
-  const task_set& divu_faces() {
-    if (divu_faces_built_) return divu_faces_;
-    std::vector<sf_task> v;
-    const i64 g = dec_.ghost;
-    for (int w = 0; w < dec_.workers; ++w) {
-      const auto dims = dec_.dims(w);
-      for (int axis = 0; axis < 3; ++axis)
-        for (int side = 0; side < 2; ++side) {
-          const int nb = dec_.neighbor(w, axis, side);
-          if (nb < 0 || nb == w) continue;
-          const auto nbd = dec_.dims(nb);
-          sf_task t{};
-          t.type = 0;
-          t.field = SF_DIVU;
-          t.src_blk = w;
-          t.dst_blk = nb;
-          for (int a = 0; a < 3; ++a) {
-            if (a == axis) {
-              t.lo[a] = side == 0 ? 0 : dims[a] - g;
-              t.dims[a] = g;
-              t.dlo[a] = side == 0 ? nbd[a] : -g;
-            } else {
-              t.lo[a] = 0;
-              t.dims[a] = dims[a];
-              t.dlo[a] = 0;
-            }
-          }
-          t.count = t.dims[0] * t.dims[1] * t.dims[2];
-          v.push_back(t);
-        }
+  static sf_task task_of(const plan_box& p, int type) {
+    sf_task t{};
+    t.type = type;
+    t.field = p.field;
+    t.axis = p.axis;
+    t.side = p.side;
+    t.src_blk = p.blk;
+    t.dst_blk = type == 0 ? p.dst_blk : p.blk;
+    for (int a = 0; a < 3; ++a) {
+      t.lo[a] = p.lo[a];
+      t.dims[a] = p.dims[a];
+      t.dlo[a] = p.dlo[a];
     }
-    divu_faces_.n = (int)v.size();
-    for (const auto& t : v) divu_faces_.max_count = std::max(divu_faces_.max_count, t.count);
-    if (!v.empty()) {
-      divu_faces_.d = (sf_task*)dalloc(sizeof(sf_task) * v.size());
-      SF_CK(cudaMemcpy(divu_faces_.d, v.data(), sizeof(sf_task) * v.size(), cudaMemcpyHostToDevice));
+    t.count = p.count;
+    return t;
+  }
+
+  // axis >= 0: refresh/exchange phase of that axis (slabs widened over earlier
+  // axes).  axis < 0: the fused loop's divu faces, all axes, owned tangential
+  // ranges, no physical fills (the half-sweep writes those itself).
+  const phase& phase_for(unsigned mask, int axis, int scope, bool exchange_only) {
+    char key[64];
+    std::snprintf(key, sizeof key, "%u:%d:%d:%d", mask, axis, scope, exchange_only ? 1 : 0);
+    auto it = phases_.find(key);
+    if (it != phases_.end()) return it->second;
+    const bool faces = axis < 0;
+    const std::vector<int> axes = faces ? std::vector<int>{0, 1, 2} : std::vector<int>{axis};
+    const phase_plan P = build_phase_plan(dec_, gid_, lid_, owner_, mask, axes, !faces, exchange_only, faces);
+    phase ph;
+    std::vector<sf_task> first, unpack;
+    for (const auto& c : P.copies) first.push_back(task_of(c, 0));
+    for (const auto& b : P.bcs) {
+      sf_task t = task_of(b, 1);
+      const sf_face_bc& fb = bc_[2 * b.axis + b.side];
+      t.kind = fb.kind;
+      t.scope = scope;
+      t.normal = kStagger[b.field] == b.axis;
+      t.velocity = kStagger[b.field] >= 0;
+      const double vwall = t.velocity ? fb.velocity[kStagger[b.field]] : 0.0;
+      t.v = (t.normal && fb.kind == SF_BC_SYMMETRY) ? 0.0 : vwall;
+      first.push_back(t);
     }
-    divu_faces_built_ = true;
-    return divu_faces_;
+    long long soff = 0, roff = 0;
+    for (const auto& kv : P.sends) {
+      long long n = 0;
+      for (const auto& b : kv.second) n += b.count;
+      ph.sends.push_back({kv.first, soff, n});
+      soff += n;
+    }
+    for (const auto& kv : P.recvs) {
+      long long n = 0;
+      for (const auto& b : kv.second) n += b.count;
+      ph.recvs.push_back({kv.first, roff, n});
+      roff += n;
+    }
+    if (soff) ph.sbuf = (double*)dalloc(sizeof(double) * soff);
+    if (roff) ph.rbuf = (double*)dalloc(sizeof(double) * roff);
+    soff = roff = 0;
+    for (const auto& kv : P.sends)
+      for (const auto& b : kv.second) {
+        sf_task t = task_of(b, 2);
+        t.buf = ph.sbuf + soff;
+        soff += b.count;
+        first.push_back(t);
+      }
+    for (const auto& kv : P.recvs)
+      for (const auto& b : kv.second) {
+        sf_task t = task_of(b, 3);
+        t.buf = ph.rbuf + roff;
+        roff += b.count;
+        unpack.push_back(t);
+      }
+    ph.first = upload_tasks(first);
+    ph.unpack = upload_tasks(unpack);
+    return phases_.emplace(key, ph).first->second;
+  }
+
+  void run_phase(const phase& ph, bool predicated) {
+    const sf_dev_ctl* pred = predicated ? dctl_ : nullptr;
+    if (ph.first.n) {
+      launch_tasks(tview(), ph.first.d, ph.first.n, ph.first.max_count, pred, st_);
+      ++launches_;
+    }
+    if (!ph.sends.empty() || !ph.recvs.empty()) {
+      SF_NC(nccl()->GroupStart());
+      for (const auto& m : ph.sends)
+        SF_NC(nccl()->Send(ph.sbuf + m.off, (size_t)m.count, kNcclFloat64, m.peer, comm_, st_));
+      for (const auto& m : ph.recvs)
+        SF_NC(nccl()->Recv(ph.rbuf + m.off, (size_t)m.count, kNcclFloat64, m.peer, comm_, st_));
+      SF_NC(nccl()->GroupEnd());
+    }
+    if (ph.unpack.n) {
+      launch_tasks(tview(), ph.unpack.d, ph.unpack.n, ph.unpack.max_count, pred, st_);
+      ++launches_;
+    }
+  }
+
+  // max over ranks of n accumulators (IEEE bit patterns of |x|): order-free,
+  // NaN-sticky, so bitwise the reference's worker-order combine
+  // (reductions.hpp:75-88)
+  void allreduce_max(unsigned long long* dev, int n) {
+    if (!dist_) return;
+    SF_NC(nccl()->AllReduce(dev, dev, (size_t)n, kNcclUint64, kNcclMax, comm_, st_));
   }
 
   void enqueue_half_sweep() {
     if (opt_.fused) {
       const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
+      // single process: the kernel's last CTA finalises the sweep; across
+      // ranks the residual first needs the max over ranks
+      const int fin = dist_ ? 0 : 1;
       if (maps_ && opt_.fused == 1)
-        launch_sweep_div_tma(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, maps_, st_);
+        launch_sweep_div_tma(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, maps_, fin, st_);
       else
-        launch_sweep_div(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, st_);
+        launch_sweep_div(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, fin, st_);
       ++launches_;
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
       ++iter_launch_;
-      const task_set& tf = divu_faces();
-      if (tf.n) {
-        launch_tasks(tview(), tf.d, tf.n, tf.max_count, dctl_, st_);
-        ++launches_;
+      if (!fin) {
+        allreduce_max(&dctl_->acc[0], 1);
+        ctl(CTL_FINISH_FUSED, 0.0, 0, 0, 0, 1);
       }
+      run_phase(phase_for(1u << SF_DIVU, -1, SF_SCOPE_ALL, true), true);
     } else {
       // the reference's dataflow, predicated step by step (cfd.hpp:295-303)
       refresh({SF_DIVU}, true);
@@ -1105,6 +1284,7 @@ class simulation {
       const work_set& wd = items_for(SF_REGION_ALL, {1, 0, 1, 0, 1, 0}, zc_plain_);
       launch_divergence(tview(wd), wd.nctas, zc_plain_, consts_, dctl_, 0, 1, st_);
       ++launches_;
+      allreduce_max(&dctl_->acc[0], 1);
       ctl(CTL_FINISH_SWEEP, 0.0, 0, 0, 0, 1);
     }
     check_launch();
@@ -1258,6 +1438,92 @@ int sf_decomp_neighbor(const int proc_grid[3], const int periodic[3], int w, int
   }
   return d.neighbor(w, axis, side);
 }
+
+int sf_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    need(out128, "out");
+    if (!sfb::nccl()) throw sfb::error(SF_ERR_CUDA, "NCCL library not found (set SF_NCCL_LIB)");
+    sfb::nccl_uid id;
+    SF_NC(sfb::nccl()->GetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof id);
+  });
+}
+
+int sf_exchange_plan(const int64_t extents[3], int world, int ghost, const int periodic[3], int rank,
+                     unsigned field_mask, int axis, int max_msgs, int64_t* out, int* n_out) {
+  return guarded([&] {
+    need(extents, "extents");
+    need(n_out, "n_out");
+    const long long ext[3] = {extents[0], extents[1], extents[2]};
+    const double sp[3] = {1.0, 1.0, 1.0};
+    const bool per[3] = {periodic && periodic[0] != 0, periodic && periodic[1] != 0,
+                         periodic && periodic[2] != 0};
+    const auto d = sfb::decompose(ext, sp, world, ghost, per);
+    if (rank < 0 || rank >= world) throw sfb::error(SF_ERR_ARG, "rank out of range");
+    std::vector<int> gid = {rank}, lid(world, -1), owner(world);
+    lid[rank] = 0;
+    for (int w = 0; w < world; ++w) owner[w] = w;
+    const bool faces = axis < 0;
+    const std::vector<int> axes = faces ? std::vector<int>{0, 1, 2} : std::vector<int>{axis};
+    const auto P = sfb::build_phase_plan(d, gid, lid, owner, field_mask, axes, !faces, true, faces);
+    // rows: kind (0 send, 1 recv, 2 local copy), peer, field, axis, side, lo[3], dims[3], dlo[3]
+    int n = 0;
+    auto emit = [&](int kind, int peer, const sfb::plan_box& b) {
+      if (out && n < max_msgs) {
+        int64_t* r = out + 15 * n;
+        r[0] = kind;
+        r[1] = peer;
+        r[2] = b.field;
+        r[3] = b.axis;
+        r[4] = b.side;
+        for (int a = 0; a < 3; ++a) {
+          r[5 + a] = b.lo[a];
+          r[8 + a] = b.dims[a];
+          r[11 + a] = b.dlo[a];
+        }
+        r[14] = b.count;
+      }
+      ++n;
+    };
+    for (const auto& kv : P.sends)
+      for (const auto& b : kv.second) emit(0, kv.first, b);
+    for (const auto& kv : P.recvs)
+      for (const auto& b : kv.second) emit(1, kv.first, b);
+    for (const auto& b : P.copies) emit(2, rank, b);
+    *n_out = n;
+  });
+}
+
+int sf_sim_create_distributed(const sf_solver_config* cfg, const sf_fluid_params* par,
+                              const sf_sim_options* opt, int rank, int world, const void* nccl_id,
+                              sf_sim** out) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(par, "par");
+    need(out, "out");
+    *out = nullptr;
+    sf_sim_options o;
+    if (opt) o = *opt; else sf_sim_options_default(&o);
+    auto h = std::make_unique<sf_sim>();
+    h->s = std::make_unique<sfb::simulation>(*cfg, *par, o, rank, world, nccl_id);
+    *out = h.release();
+  });
+}
+
+int sf_sim_rank(const sf_sim* s) { return s ? s->s->rank() : -1; }
+int sf_sim_gather_block(sf_sim* s, const char* field, int worker, double* host, int64_t n) {
+  return guarded([&] {
+    need(s, "sim");
+    s->s->block_io(sfb::simulation::field_id(field), worker, host, n, false);
+  });
+}
+int sf_sim_scatter_block(sf_sim* s, const char* field, int worker, const double* host, int64_t n) {
+  return guarded([&] {
+    need(s, "sim");
+    s->s->block_io(sfb::simulation::field_id(field), worker, const_cast<double*>(host), n, true);
+  });
+}
+int sf_sim_world(const sf_sim* s) { return s ? s->s->world() : 0; }
 
 void sf_sim_options_default(sf_sim_options* o) {
   if (!o) return;

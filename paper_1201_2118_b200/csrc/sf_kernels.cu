@@ -60,6 +60,20 @@ __global__ void k_tasks(View vw, const sf_task* __restrict__ tasks,
   if (pred && pred_done(pred)) return;
   const sf_task& T = tasks[blockIdx.y];
   const long long stride = (long long)gridDim.x * blockDim.x;
+  if (T.type == 2 || T.type == 3) {  // message pack / unpack (exchange.hpp:165-224)
+    const sf_dev_block& Bk = vw.blk(T.dst_blk);
+    double* f = vw.ptr(T.dst_blk, T.field, FRONT);
+    const long long nx = T.dims[0], nxy = T.dims[0] * T.dims[1];
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < T.count; e += stride) {
+      const long long kk = e / nxy, rem = e - kk * nxy, jj = rem / nx, ii = rem - jj * nx;
+      const long long o = off(Bk, T.lo[0] + ii, T.lo[1] + jj, T.lo[2] + kk);
+      if (T.type == 2)
+        T.buf[e] = f[o];
+      else
+        f[o] = T.buf[e];
+    }
+    return;
+  }
   if (T.type == 0) {
     const sf_dev_block& S = vw.blk(T.src_blk);
     const sf_dev_block& D = vw.blk(T.dst_blk);
@@ -413,7 +427,7 @@ __global__ void __launch_bounds__(kTX* kTY) k_sweep_div(sf_dev_table* __restrict
                                                         const sf_work* __restrict__ items,
                                                         int nitems, int zc, sf_consts s,
                                                         sf_dev_ctl* ctl, sf_host_flag* hflag,
-                                                        unsigned int total_ctas) {
+                                                        unsigned int total_ctas, int finalize) {
   if (pred_done(ctl)) return;
   const tile_loc t = locate(items, nitems, zc);
   const sf_dev_block& B = tab->blk[t.blk];
@@ -582,6 +596,7 @@ __global__ void __launch_bounds__(kTX* kTY) k_sweep_div(sf_dev_table* __restrict
     }
   }
   block_max_atomic<1>(rmax, &ctl->acc[0]);
+  if (!finalize) return;  // across ranks: allreduce, then CTL_FINISH_FUSED
   if (last_cta(&ctl->ctas_done, total_ctas)) {
     if (threadIdx.x == 0 && threadIdx.y == 0) {
       __threadfence();
@@ -618,10 +633,10 @@ __global__ void __launch_bounds__(kTX* kTY) k_sweep_div(sf_dev_table* __restrict
 }
 
 void launch_sweep_div(const table_view& vw, int nctas, int zc, const sf_consts& c,
-                      sf_dev_ctl* ctl, sf_host_flag* hflag, cudaStream_t st) {
+                      sf_dev_ctl* ctl, sf_host_flag* hflag, int fin, cudaStream_t st) {
   if (nctas <= 0) return;
   k_sweep_div<<<nctas, dim3(kTX, kTY), 0, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
-                                                 (unsigned)nctas);
+                                                 (unsigned)nctas, fin);
 }
 
 // ---------------------------------------------------------------------------
@@ -799,6 +814,33 @@ __global__ void k_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, i
       }
       if (hflag) {
         hflag->abort_field = ctl->abort_field;
+        __threadfence_system();
+      }
+      break;
+    }
+    case CTL_FINISH_FUSED: {  // the fused kernel's finalize, after the residual allreduce
+      const double r = bits_to_max(ctl->acc[0]);
+      ctl->acc[0] = 0ull;
+      ctl->residual = r;
+      ctl->color ^= 1;
+      ctl->sweeps += 1;
+      const int more = (r > ctl->tolerance) && (ctl->sweeps < ctl->max_sweeps);
+      ctl->done = more ? 0 : 1;
+      for (int b = 0; b < tab->nblocks; ++b)
+        for (int q = 0; q < 5; ++q) {
+          if (q == SF_P) continue;
+          double* tmp = tab->ptr[b][q][FRONT];
+          tab->ptr[b][q][FRONT] = tab->ptr[b][q][ALT];
+          tab->ptr[b][q][ALT] = tmp;
+          const unsigned char ti = tab->bidx[b][q][FRONT];
+          tab->bidx[b][q][FRONT] = tab->bidx[b][q][ALT];
+          tab->bidx[b][q][ALT] = ti;
+        }
+      if (hflag) {
+        hflag->sweeps = ctl->sweeps;
+        hflag->residual = r;
+        hflag->done = ctl->done;
+        hflag->color = ctl->color;
         __threadfence_system();
       }
       break;

@@ -8,7 +8,7 @@ namespace sfb {
 // One ghost-refresh task: a copy between blocks (one message of
 // exchange.hpp:165-224) or one physical face fill (bc_face, :231-480).
 struct sf_task {
-  int type;  // 0 copy, 1 bc
+  int type;  // 0 copy, 1 bc, 2 pack (box -> buf), 3 unpack (buf -> box)
   int field;
   int src_blk, dst_blk;
   long long lo[3];    // copy: source box (src-local); bc: tangential box (axis entry unused)
@@ -17,6 +17,7 @@ struct sf_task {
   long long count;    // elements (copy) or lines (bc)
   int axis, side, normal, velocity, kind, scope;
   double v;           // wall velocity component (normal pin / tangential reflection)
+  double* buf;        // pack / unpack: contiguous x-fastest message buffer
 };
 
 // Tile shapes (threads = TX x TY; each thread marches z over a chunk).
@@ -36,11 +37,14 @@ void launch_divergence(const View& vw, int nctas, int zc, const sf_consts& c, sf
 template <class View>
 void launch_pressure_sweep(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                            int predicated, const double* beta_color_dt, cudaStream_t st);
+// fin = 1: the last CTA finalises the sweep; 0: the caller allreduces acc[0]
+// across ranks and runs CTL_FINISH_FUSED
 void launch_sweep_div(const table_view& vw, int nctas, int zc, const sf_consts& c,
-                      sf_dev_ctl* ctl, sf_host_flag* hflag, cudaStream_t st);
+                      sf_dev_ctl* ctl, sf_host_flag* hflag, int fin, cudaStream_t st);
 // TMA-pipelined fused half-sweep (sf_sweep_tma.cu); maps = device sweep_maps.
 void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_consts& c,
-                          sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, cudaStream_t st);
+                          sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,
+                          cudaStream_t st);
 int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field);
 size_t sweep_maps_bytes();
 size_t sweep_map_offset(int b, int f, int s);
@@ -60,6 +64,7 @@ enum ctl_op {
   CTL_CLEAR_ACC = 6,
   CTL_SWAP = 7,              // swap slots (a, b) of field f in every block
   CTL_RESET_CLOCK = 8,       // colour = 0, abort cleared (cfd.hpp:733-738)
+  CTL_FINISH_FUSED = 9,      // fused half-sweep finalise after a cross-rank residual allreduce
 };
 void launch_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, int op, double arg,
                 int f, int a, int b, const sf_consts& c, int predicated, cudaStream_t st);

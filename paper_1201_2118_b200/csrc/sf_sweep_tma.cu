@@ -95,7 +95,7 @@ template <int STAGES, int MINB, bool WS>
 __global__ void __launch_bounds__(kTX* kTY + (WS ? 32 : 0), MINB)
     k_sweep_div_tma(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems,
                     int zc, sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag,
-                    unsigned int total_ctas, const sweep_maps* __restrict__ maps) {
+                    unsigned int total_ctas, const sweep_maps* __restrict__ maps, int finalize) {
   constexpr int kStages = STAGES;
   if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -375,6 +375,7 @@ __global__ void __launch_bounds__(kTX* kTY + (WS ? 32 : 0), MINB)
 
   unsigned long long rm[1] = {rmax};
   block_max_atomic<1>(rm, &ctl->acc[0]);
+  if (!finalize) return;  // across ranks: allreduce, then CTL_FINISH_FUSED
   if (last_cta(&ctl->ctas_done, total_ctas)) {
     if (tid == 0) {
       __threadfence();
@@ -457,7 +458,8 @@ size_t sweep_map_offset(int b, int f, int s) {
 
 template <int STAGES, int MINB, bool WS>
 static void launch_variant(const table_view& vw, int nctas, int zc, const sf_consts& c,
-                           sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, cudaStream_t st) {
+                           sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,
+                           cudaStream_t st) {
   const size_t smem = sizeof(stage_t) * STAGES;
   static bool attr = false;
   if (!attr) {
@@ -467,7 +469,7 @@ static void launch_variant(const table_view& vw, int nctas, int zc, const sf_con
   }
   k_sweep_div_tma<STAGES, MINB, WS><<<nctas, dim3(kTX, kTY + (WS ? 1 : 0)), smem, st>>>(
       vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas,
-      static_cast<const sweep_maps*>(maps));
+      static_cast<const sweep_maps*>(maps), fin);
 }
 
 // SF_SWEEP_VARIANT selects the pipeline shape for A/B runs (default 0).
@@ -481,15 +483,16 @@ static int sweep_variant() {
 }
 
 void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_consts& c,
-                          sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, cudaStream_t st) {
+                          sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,
+                          cudaStream_t st) {
   if (nctas <= 0) return;
   switch (sweep_variant()) {
-    case 1: launch_variant<3, 3, false>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
-    case 2: launch_variant<4, 2, true>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
-    case 3: launch_variant<3, 3, true>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
-    case 4: launch_variant<6, 2, true>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
-    case 5: launch_variant<2, 4, false>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
-    default: launch_variant<4, 2, false>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
+    case 1: launch_variant<3, 3, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
+    case 2: launch_variant<4, 2, true>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
+    case 3: launch_variant<3, 3, true>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
+    case 4: launch_variant<6, 2, true>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
+    case 5: launch_variant<2, 4, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
+    default: launch_variant<4, 2, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
   }
 }
 

@@ -92,7 +92,11 @@ class Simulation:
 
     def __init__(self, cfg: SolverConfig, par: FluidParams, workers: int = 1, mode: str = "plain",
                  tile: Sequence[int] = (0, 0, 0), ghost: int = 1, form: str = "rows",
-                 device: int = 0, fused: int | bool = True):
+                 device: int = 0, fused: int | bool = True, rank: int | None = None,
+                 world: int | None = None, nccl_id: bytes | None = None):
+        """With ``nccl_id`` (from :func:`nccl_unique_id` on rank 0, broadcast to all
+        ranks) the simulation is the rank-``rank`` component of a ``world``-rank
+        decomposition and exchanges ghosts over NCCL."""
         self._h = None
         self.cfg, self.par = cfg, par
         self._lib = L.lib()
@@ -104,8 +108,15 @@ class Simulation:
         opt.ghost, opt.form, opt.device, opt.fused = int(ghost), (1 if form == "points" else 0), int(device), int(fused)
         self._ccfg, self._cpar, self._opt = cfg.to_c(), par.to_c(), opt
         h = C.c_void_p()
-        L.check(self._lib.sf_sim_create(C.byref(self._ccfg), C.byref(self._cpar), C.byref(opt), C.byref(h)))
+        if nccl_id is not None:
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+            L.check(self._lib.sf_sim_create_distributed(C.byref(self._ccfg), C.byref(self._cpar), C.byref(opt),
+                                                        int(rank or 0), int(world or 1), idbuf, C.byref(h)))
+        else:
+            L.check(self._lib.sf_sim_create(C.byref(self._ccfg), C.byref(self._cpar), C.byref(opt), C.byref(h)))
         self._h = h
+        self.rank = int(rank or 0)
+        self.world = int(world or 1)
         self.extents = tuple(int(x) for x in cfg.extents)
         self.workers = int(workers)
 
@@ -219,6 +230,30 @@ class Simulation:
         L.check(self._lib.sf_sim_gather(self._h, name.encode(), C.c_void_p(a.ctypes.data), a.size))
         return a
 
+    def block_shape(self, worker: int | None = None):
+        d = decompose(self.extents, self.world if self.world > 1 else self.workers, int(self._opt.ghost),
+                      tuple(bool(x) for x in self.cfg.periodic))
+        return d.size(self.rank if worker is None else worker)
+
+    def gather_block(self, name: str, worker: int | None = None, out=None):
+        w = self.rank if worker is None else worker
+        if out is None:
+            nx, ny, nz = self.block_shape(w)
+            out = np.empty((nz, ny, nx), dtype=np.float64)
+        ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        n = out.numel() if hasattr(out, "numel") else out.size
+        L.check(self._lib.sf_sim_gather_block(self._h, name.encode(), int(w), C.c_void_p(ptr), n))
+        return out
+
+    def scatter_block(self, name: str, data, worker: int | None = None):
+        w = self.rank if worker is None else worker
+        if hasattr(data, "data_ptr"):
+            ptr, n = data.data_ptr(), data.numel()
+        else:
+            data = np.ascontiguousarray(data, dtype=np.float64)
+            ptr, n = data.ctypes.data, data.size
+        L.check(self._lib.sf_sim_scatter_block(self._h, name.encode(), int(w), C.c_void_p(ptr), n))
+
     def checksum(self) -> str:
         v = C.c_uint64()
         L.check(self._lib.sf_sim_checksum(self._h, C.byref(v)))
@@ -282,6 +317,13 @@ class Simulation:
         ms, n = C.c_double(), C.c_int64()
         L.check(self._lib.sf_sim_kernel_timing(self._h, kernel.encode(), C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0 calls it, then broadcasts)."""
+    buf = C.create_string_buffer(128)
+    L.check(L.lib().sf_nccl_unique_id(buf))
+    return buf.raw
 
 
 @dataclass

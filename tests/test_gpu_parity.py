@@ -329,3 +329,24 @@ def test_cpp_drop_in_reproduces_the_golden_checksum(tmp_path):
     assert out.returncode == 0, out.stdout + out.stderr
     assert "checksum=1b07d1f577d4bad0" in out.stdout
     assert "exec_error: kernel 'PRESSURE_SWEEP': parameter 'beta' not supplied" in out.stdout
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+def test_distributed_mode_on_one_rank_runs_the_nccl_path(fused):
+    # world = 1 exercises the NCCL communicator, the residual/dt/NaN allreduces,
+    # the cross-rank finalize of the fused half-sweep and the all-gather of
+    # grid::gather without co-scheduling ranks on one GPU
+    uid = sfb.nccl_unique_id()
+    cfg = sfb.SolverConfig(extents=(64, 64, 64), reynolds=100.0, symmetry_z=False)
+    s = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), rank=0, world=1, nccl_id=uid, fused=fused)
+    s.init_cavity()
+    stats = [s.step() for _ in range(2)]
+    assert [[x.dt, x.sweeps, x.residual] for x in stats] == GOLDEN["cavity64"]["stats"][:2]
+    o = Oracle(cavity_case(64, symmetry_z=False), "port")
+    o.init_cavity()
+    o.advance(2)
+    assert s.checksum() == o.checksum()
+    blk = s.gather_block("vx")
+    assert same(blk, s.gather("vx"))
+    s.scatter_block("p", np.zeros_like(blk))
+    assert np.all(s.gather("p") == 0.0)
