@@ -193,6 +193,61 @@ int sf_sim_scatter_block(sf_sim* s, const char* field, int worker, const double*
 int sf_exchange_plan(const int64_t extents[3], int world, int ghost, const int periodic[3], int rank,
                      unsigned field_mask, int axis, int max_msgs, int64_t* out, int* n_out);
 
+/* ---- descriptor-declared kernels (the plugin path, executor.hpp:484-498) -----
+ * codegen::execution_plan (codegen.hpp:41-57): tile, halo (-x,+x,-y,+y,-z,+z),
+ * bindings (field, intent, cached) in declaration order, parameter names.
+ * intent: 0 IN, 1 OUT, 2 INOUT, 3 SEPARATEINOUT (descriptor.hpp:216). */
+typedef struct sf_binding {
+  const char* field;
+  int intent;
+  int cached;
+} sf_binding;
+typedef struct sf_plan {
+  const char* kernel;
+  int tile[3];
+  int halo[6];
+  const sf_binding* bindings;
+  int n_bindings;
+  const char* const* params;
+  int n_params;
+} sf_plan;
+/* field_store::create (field.hpp:108-112); stagger -1 none, 0/1/2 = x/y/z. */
+int sf_sim_create_field(sf_sim* s, const char* name, int stagger);
+/* executor::register_kernel with the point function given as the CUDA C++
+ * BODY of `void f(const point_ctx& c)` against the reference's accessors
+ * (c.field(s)(di,dj,dk), .load(), .store(v), c.param(s), c.i/c.j/c.k;
+ * executor.hpp:130-184).  The body is JIT-compiled for sm_100a (NVRTC,
+ * --fmad=false) into a tile kernel whose CTA is the plan's TILE.  Same checks
+ * and error texts as register_common (executor.hpp:650-692); a compile error
+ * returns SF_ERR_EXEC with the compiler log.  Run with sf_sim_run_kernel. */
+int sf_sim_register_kernel(sf_sim* s, const sf_plan* plan, const char* const* sig_fields, int n_sig_fields,
+                           const char* const* sig_params, int n_sig_params, const char* point_body);
+
+/* executor::boundary() (executor.hpp:482): one physical face condition
+ * (kind sf_bc_kind, velocity used by walls); faces indexed (axis, side). */
+int sf_sim_set_face_bc(sf_sim* s, int axis, int side, int kind, const double velocity[3]);
+/* executor::physical_bc (executor.hpp:516-518) */
+int sf_sim_physical_bc(sf_sim* s, const char* const* fields, int n);
+
+/* exec::schedule_step (executor.hpp:422-466): kind 0 run, 1 exchange,
+ * 2 physical_bc, 3 refresh, 4 reduce. */
+typedef struct sf_schedule_step {
+  int kind;
+  const char* kernel;
+  int region;
+  const char* const* fields;
+  int n_fields;
+  const char* source;
+  int op;
+  const char* target;
+} sf_schedule_step;
+/* executor::run_schedule (executor.hpp:533-553) incl. the dry run's
+ * ghost-validity check and its error texts; reduce steps store results. */
+int sf_sim_run_schedule(sf_sim* s, const sf_schedule_step* steps, int n_steps, const char* const* param_names,
+                        const double* param_values, int n_params, int passes, int mode);
+/* executor::results() (executor.hpp:615) */
+int sf_sim_result(sf_sim* s, const char* name, double* value);
+
 /* Device plumbing for benches and transports. */
 int sf_sim_synchronize(sf_sim* s);
 void* sf_sim_stream(sf_sim* s);            /* the cudaStream_t all work is ordered on */

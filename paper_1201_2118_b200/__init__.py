@@ -9,7 +9,9 @@ from ._lib import CfdError, ConfigError, ExecError, GridError, SfError, lib  # n
 from .sim import (  # noqa: F401
     FIELDS,
     Decomposition,
+    ExecutionPlan,
     FluidParams,
+    ScheduleStep,
     Simulation,
     SolverConfig,
     StepStats,
@@ -20,5 +22,5 @@ from .sim import (  # noqa: F401
 
 __all__ = [
     "Simulation", "SolverConfig", "FluidParams", "StepStats", "cavity_fluid", "decompose",
-    "Decomposition", "nccl_unique_id", "FIELDS", "SfError", "ConfigError", "GridError", "ExecError", "CfdError", "lib",
+    "Decomposition", "ExecutionPlan", "ScheduleStep", "nccl_unique_id", "FIELDS", "SfError", "ConfigError", "GridError", "ExecError", "CfdError", "lib",
 ]

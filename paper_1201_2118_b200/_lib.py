@@ -107,6 +107,35 @@ class FaceBC(C.Structure):
     _fields_ = [("kind", C.c_int), ("velocity", C.c_double * 3)]
 
 
+class Binding(C.Structure):
+    _fields_ = [("field", C.c_char_p), ("intent", C.c_int), ("cached", C.c_int)]
+
+
+class Plan(C.Structure):
+    _fields_ = [
+        ("kernel", C.c_char_p),
+        ("tile", C.c_int * 3),
+        ("halo", C.c_int * 6),
+        ("bindings", C.POINTER(Binding)),
+        ("n_bindings", C.c_int),
+        ("params", C.POINTER(C.c_char_p)),
+        ("n_params", C.c_int),
+    ]
+
+
+class ScheduleStep(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int),
+        ("kernel", C.c_char_p),
+        ("region", C.c_int),
+        ("fields", C.POINTER(C.c_char_p)),
+        ("n_fields", C.c_int),
+        ("source", C.c_char_p),
+        ("op", C.c_int),
+        ("target", C.c_char_p),
+    ]
+
+
 class CfdConsts(C.Structure):
     _fields_ = [
         ("dt", C.c_double), ("nu", C.c_double), ("alpha", C.c_double),
@@ -156,6 +185,12 @@ SIGNATURES = [
     ("sf_sim_exchange", [_vp, _cpp, _i], _i),
     ("sf_sim_run_kernel", [_vp, _cp, _cpp, _dp, _i, _i], _i),
     ("sf_sim_reduce", [_vp, _cp, _i, _dp], _i),
+    ("sf_sim_create_field", [_vp, _cp, _i], _i),
+    ("sf_sim_register_kernel", [_vp, C.POINTER(Plan), _cpp, _i, _cpp, _i, _cp], _i),
+    ("sf_sim_set_face_bc", [_vp, _i, _i, _i, _dp], _i),
+    ("sf_sim_physical_bc", [_vp, _cpp, _i], _i),
+    ("sf_sim_run_schedule", [_vp, C.POINTER(ScheduleStep), _i, _cpp, _dp, _i, _i, _i], _i),
+    ("sf_sim_result", [_vp, _cp, _dp], _i),
     ("sf_sim_invalidate_ghosts", [_vp, _cp], _i),
     ("sf_sim_invalidate_all_ghosts", [_vp], _i),
     ("sf_sim_ghosts_valid", [_vp, _cp], _i),

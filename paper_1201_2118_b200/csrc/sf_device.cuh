@@ -19,7 +19,7 @@
 namespace sfb {
 
 constexpr int kMaxBlocks = 64;   // grid components per device
-constexpr int kMaxFields = 8;    // vx, vy, vz, p, divu (+ room for user fields)
+constexpr int kMaxFields = 16;   // vx, vy, vz, p, divu + user fields
 constexpr int kSlots = 3;        // front, back, alt
 
 enum slot { FRONT = 0, BACK = 1, ALT = 2 };

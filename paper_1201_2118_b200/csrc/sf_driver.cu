@@ -29,6 +29,7 @@
 
 #include "sf_kernels.cuh"
 #include "sf_plan.hpp"
+#include "sf_jit.hpp"
 
 namespace sfb {
 
@@ -258,8 +259,6 @@ static sf_layout make_layout(const i64 dims[3], const i64 lo[3], int g) {
 // ---------------------------------------------------------------------------
 // the simulation
 // ---------------------------------------------------------------------------
-static const char* const kFieldNames[SF_NFIELDS] = {"vx", "vy", "vz", "p", "divu"};
-static const int kStagger[SF_NFIELDS] = {0, 1, 2, -1, -1};
 
 struct kernel_plan {  // codegen::execution_plan of the three CFD kernels (cfd.hpp:111-162)
   std::string name;
@@ -283,6 +282,17 @@ static const std::vector<kernel_plan>& cfd_plans() {
 
 class simulation {
  public:
+  struct user_kernel {
+    std::string name;
+    std::array<int, 3> tile{};
+    std::array<int, 6> halo{};
+    std::vector<int> fid, intent;
+    std::vector<std::string> params;
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t k = nullptr;
+    int tx = 32, ty = 8, zc = 16;
+    bool debug = false;
+  };
   // world > 1: one process per GPU; this rank owns grid component `rank` of
   // grid::decompose(dom, world, ghost, periodic) and talks to the others over
   // NCCL (communicator from `uid`, created collectively here).
@@ -336,6 +346,8 @@ class simulation {
   ~simulation() {
     cudaSetDevice(opt_.device);
     cudaStreamSynchronize(st_);
+    for (auto& kv : ukernels_)
+      if (kv.second.lib) cudaLibraryUnload(kv.second.lib);
     for (void* p : dev_allocs_) cudaFree(p);
     if (hflag_) cudaFreeHost(hflag_);
     cudaEventDestroy(ev_[0]);
@@ -354,11 +366,42 @@ class simulation {
     if (e != cudaSuccess) throw error(SF_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   }
 
-  static int field_id(const std::string& name) {
-    for (int f = 0; f < SF_NFIELDS; ++f)
-      if (name == kFieldNames[f]) return f;
+  int field_id(const std::string& name) const {
+    for (int f = 0; f < (int)fname_.size(); ++f)
+      if (name == fname_[f]) return f;
     throw error(SF_ERR_GRID, "no field named '" + name + "'");
   }
+  int nfields() const { return (int)fname_.size(); }
+  const std::string& field_name(int f) const { return fname_[f]; }
+
+  // field_store::create (field.hpp:108-112): a zero-filled front buffer on
+  // every local component; stagger -1 none, 0/1/2 = x/y/z (field.hpp:23)
+  int create_field(const std::string& name, int stagger) {
+    for (const auto& n : fname_)
+      if (n == name) throw error(SF_ERR_GRID, "field '" + name + "' already exists");
+    if ((int)fname_.size() >= kMaxFields)
+      throw error(SF_ERR_ARG, "at most " + std::to_string(kMaxFields) + " fields");
+    if (stagger < -1 || stagger > 2) throw error(SF_ERR_ARG, "stagger must be -1, 0, 1 or 2");
+    download_table();
+    const int f = (int)fname_.size();
+    fname_.push_back(name);
+    fstag_.push_back(stagger);
+    for (int b = 0; b < nloc_; ++b) alloc_slot(b, f, FRONT);
+    upload_table();
+    return f;
+  }
+  // distributed_field::ensure_back (field.hpp:80-87)
+  void ensure_back(int f) {
+    download_table();
+    bool any = false;
+    for (int b = 0; b < nloc_; ++b)
+      if (!htab_->ptr[b][f][BACK]) {
+        alloc_slot(b, f, BACK);
+        any = true;
+      }
+    if (any) upload_table();
+  }
+  bool has_back(int f) const { return htab_->ptr[0][f][BACK] != nullptr; }
 
   // ---- initial states (cfd.hpp:229-257) -------------------------------------
   void reset_clock() {
@@ -377,7 +420,7 @@ class simulation {
       ++launches_;
     }
     check_launch();
-    ghosts_ok_[kFieldNames[f]] = false;
+    ghosts_ok_[fname_[f]] = false;
   }
   void init_cavity() {
     for (int f = 0; f < SF_NFIELDS; ++f) fill_const(f, 0.0);
@@ -445,7 +488,7 @@ class simulation {
       ++launches_;
     }
     check_launch();
-    ghosts_ok_[kFieldNames[f]] = false;
+    ghosts_ok_[fname_[f]] = false;
   }
   // grid::gather across ranks: every rank packs its owned block, one
   // all-gather, every rank places all blocks (bitwise, no arithmetic)
@@ -493,7 +536,7 @@ class simulation {
     if (to_device) {
       SF_CK(cudaMemcpyAsync(sg, host, sizeof(double) * (size_t)(d[0] * d[1] * d[2]), cudaMemcpyHostToDevice, st_));
       launch_copy_box(sg, 0, d[0], d[1], htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, z, d, z, st_);
-      ghosts_ok_[kFieldNames[f]] = false;
+      ghosts_ok_[fname_[f]] = false;
     } else {
       launch_copy_box(htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, sg, 0, d[0], d[1], z, d, z, st_);
       SF_CK(cudaMemcpyAsync(host, sg, sizeof(double) * (size_t)(d[0] * d[1] * d[2]), cudaMemcpyDeviceToHost, st_));
@@ -557,7 +600,7 @@ class simulation {
     };
     std::vector<double> g((size_t)cells());
     for (int f : {SF_VX, SF_VY, SF_VZ, SF_P}) {
-      mix(kFieldNames[f], std::strlen(kFieldNames[f]));
+      mix(fname_[f].data(), fname_[f].size());
       gather(f, g.data());
       mix(g.data(), g.size() * sizeof(double));
     }
@@ -572,17 +615,22 @@ class simulation {
     for (int f : fields) mask |= 1u << f;
     for (int axis = 0; axis < 3; ++axis) run_phase(phase_for(mask, axis, SF_SCOPE_ALL, false), predicated);
     check_launch();
-    for (int f : fields) ghosts_ok_[kFieldNames[f]] = true;
+    for (int f : fields) ghosts_ok_[fname_[f]] = true;
   }
   void exchange_only(const std::vector<int>& fields) {
     unsigned mask = 0;
     for (int f : fields) mask |= 1u << f;
     for (int axis = 0; axis < 3; ++axis) run_phase(phase_for(mask, axis, SF_SCOPE_ALL, true), false);
     check_launch();
-    for (int f : fields) ghosts_ok_[kFieldNames[f]] = true;
+    for (int f : fields) ghosts_ok_[fname_[f]] = true;
   }
 
   void run_kernel(const std::string& name, const std::map<std::string, double>& params, int reg) {
+    if (is_user_kernel(name)) {
+      run_user_kernel(name, params, reg);
+      check_launch();
+      return;
+    }
     const kernel_plan* kp = nullptr;
     for (const auto& p : cfd_plans())
       if (p.name == name) kp = &p;
@@ -620,11 +668,348 @@ class simulation {
     if (reg != SF_REGION_INTERIOR && name == "UPDATE_VELOCITY") swap_front_back();
   }
 
+  // ---- descriptor-declared kernels (executor.hpp:484-498, 650-692) ---------
+  void register_kernel(const std::string& name, const std::array<int, 3>& tile,
+                       const std::array<int, 6>& halo, const std::vector<std::string>& bfields,
+                       const std::vector<int>& intents, const std::vector<std::string>& params,
+                       const std::vector<std::string>& sig_fields,
+                       const std::vector<std::string>& sig_params, const std::string& body) {
+    const std::string head = "kernel '" + name + "': ";
+    for (const auto& p : cfd_plans())
+      if (p.name == name) throw error(SF_ERR_EXEC, "kernel '" + name + "' is already registered");
+    if (ukernels_.count(name)) throw error(SF_ERR_EXEC, "kernel '" + name + "' is already registered");
+    if (bfields.empty()) throw error(SF_ERR_EXEC, "kernel '" + name + "' has no field bindings");
+    for (int a = 0; a < 3; ++a)
+      if (tile[a] < 1) throw error(SF_ERR_EXEC, head + "tile extents must be positive");
+    // check_signature (executor.hpp:715-737)
+    for (size_t i = 0; i < std::max(bfields.size(), sig_fields.size()); ++i) {
+      if (i >= sig_fields.size()) throw error(SF_ERR_EXEC, head + "function is missing binding '" + bfields[i] + "'");
+      if (i >= bfields.size())
+        throw error(SF_ERR_EXEC, head + "function declares unknown binding '" + sig_fields[i] + "'");
+      if (bfields[i] != sig_fields[i])
+        throw error(SF_ERR_EXEC, head + "slot " + std::to_string(i) + " binds '" + bfields[i] +
+                                     "' but the function declares '" + sig_fields[i] + "'");
+    }
+    for (size_t i = 0; i < std::max(params.size(), sig_params.size()); ++i) {
+      if (i >= sig_params.size()) throw error(SF_ERR_EXEC, head + "function is missing parameter '" + params[i] + "'");
+      if (i >= params.size())
+        throw error(SF_ERR_EXEC, head + "function declares unknown parameter '" + sig_params[i] + "'");
+      if (params[i] != sig_params[i])
+        throw error(SF_ERR_EXEC, head + "parameter slot " + std::to_string(i) + " is '" + params[i] +
+                                     "' but the function declares '" + sig_params[i] + "'");
+    }
+    int mh = 0;
+    for (int h : halo) mh = std::max(mh, h);
+    if (mh > dec_.ghost)
+      throw error(SF_ERR_EXEC, head + "stencil needs " + std::to_string(mh) + " ghost layers but fields carry " +
+                                   std::to_string(dec_.ghost));
+    user_kernel uk;
+    uk.name = name;
+    uk.tile = tile;
+    uk.halo = halo;
+    uk.params = params;
+    for (size_t i = 0; i < bfields.size(); ++i) {
+      int f = -1;
+      for (int q = 0; q < (int)fname_.size(); ++q)
+        if (fname_[q] == bfields[i]) f = q;
+      if (f < 0) throw error(SF_ERR_EXEC, "kernel '" + name + "' binds unknown field '" + bfields[i] + "'");
+      if (intents[i] < 0 || intents[i] > 3) throw error(SF_ERR_ARG, "bad intent");
+      uk.fid.push_back(f);
+      uk.intent.push_back(intents[i]);
+    }
+    for (size_t i = 0; i < uk.fid.size(); ++i)
+      if (uk.intent[i] == 3) ensure_back(uk.fid[i]);
+    // CTA tile = the descriptor's TILE (x, y threads), z chunk = TILE z
+    uk.tx = std::min(tile[0], 1024);
+    uk.ty = std::max(1, std::min(tile[1], 1024 / uk.tx));
+    uk.zc = tile[2];
+    compile_user(uk, body);
+    ukernels_.emplace(name, uk);
+  }
+
+  void compile_user(user_kernel& uk, const std::string& body) {
+    nvrtc_api* rt = nvrtc();
+    if (!rt) throw error(SF_ERR_CUDA, "NVRTC not found (set SF_NVRTC_LIB)");
+    std::string src;
+    src += "#define SF_NB " + std::to_string(uk.fid.size()) + "\n";
+    src += "#define SF_NP " + std::to_string(uk.params.size()) + "\n";
+    src += "#define SF_TX " + std::to_string(uk.tx) + "\n#define SF_TY " + std::to_string(uk.ty) + "\n";
+    src += "#define SF_MAXF " + std::to_string(kMaxFields) + "\n#define SF_SLOTS " + std::to_string(kSlots) + "\n";
+    std::string fids, wsl;
+    for (size_t i = 0; i < uk.fid.size(); ++i) {
+      fids += (i ? "," : "") + std::to_string(uk.fid[i]);
+      wsl += (i ? "," : "") + std::string(uk.intent[i] == 3 ? "1" : "0");
+    }
+    std::string rdb, wrb, cen;
+    for (size_t i = 0; i < uk.fid.size(); ++i) {
+      const int in = uk.intent[i];
+      rdb += (i ? "," : "") + std::string(in != 1 ? "1" : "0");
+      wrb += (i ? "," : "") + std::string(in != 0 ? "1" : "0");
+      cen += (i ? "," : "") + std::string(in == 2 ? "1" : "0");
+    }
+    src += "__device__ constexpr int SF_FID[] = {" + fids + "};\n";
+    src += "__device__ constexpr int SF_WSLOT[] = {" + wsl + "};\n";
+    src += "__device__ constexpr int SF_READABLE[] = {" + rdb + "};\n";
+    src += "__device__ constexpr int SF_WRITABLE[] = {" + wrb + "};\n";
+    src += "__device__ constexpr int SF_CENTER_ONLY[] = {" + cen + "};\n";
+    src += "__device__ constexpr int SF_HALO[] = {";
+    for (int a = 0; a < 6; ++a) src += (a ? "," : "") + std::to_string(uk.halo[a]);
+    src += "};\n#define SF_DEBUG " + std::string(debug_bounds() ? "1" : "0") + "\n";
+    uk.debug = debug_bounds();
+    std::string tmpl = jit_template();
+    const size_t at = tmpl.find("SF_BODY");
+    tmpl.replace(at, 7, "#line 1 \"" + uk.name + "\"\n" + body + "\n");
+    src += tmpl;
+    void* prog = nullptr;
+    if (rt->create(&prog, src.c_str(), (uk.name + ".cu").c_str(), 0, nullptr, nullptr) != 0)
+      throw error(SF_ERR_CUDA, "nvrtcCreateProgram failed");
+    const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-std=c++17", "-lineinfo",
+                          "-default-device"};
+    const int rc = rt->compile(prog, 5, opts);
+    std::string log;
+    size_t ls = 0;
+    if (rt->log_size && rt->log_size(prog, &ls) == 0 && ls > 1) {
+      log.resize(ls);
+      rt->log(prog, &log[0]);
+    }
+    if (rc != 0) {
+      rt->destroy(&prog);
+      throw error(SF_ERR_EXEC, "kernel '" + uk.name + "': device compilation failed:\n" + log);
+    }
+    size_t cs = 0;
+    rt->cubin_size(prog, &cs);
+    std::string cubin(cs, '\0');
+    rt->cubin(prog, &cubin[0]);
+    rt->destroy(&prog);
+    SF_CK(cudaLibraryLoadData(&uk.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    SF_CK(cudaLibraryGetKernel(&uk.k, uk.lib, "sf_user_kernel"));
+    if (uk.debug) {  // point the module's error word at a device buffer
+      if (!dbg_word_) {
+        dbg_word_ = (int*)dalloc(8 * sizeof(int));
+        SF_CK(cudaMemset(dbg_word_, 0, 8 * sizeof(int)));
+      }
+      void* sym = nullptr;
+      size_t bytes = 0;
+      SF_CK(cudaLibraryGetGlobal(&sym, &bytes, uk.lib, "sf_err_word"));
+      SF_CK(cudaMemcpy(sym, &dbg_word_, sizeof(int*), cudaMemcpyHostToDevice));
+    }
+  }
+
+  bool is_user_kernel(const std::string& name) const { return ukernels_.count(name) > 0; }
+
+  // executor::boundary() (executor.hpp:482): replace one face condition
+  void set_face_bc(int axis, int side, int kind, const double vel[3]) {
+    if (axis < 0 || axis > 2 || side < 0 || side > 1 || kind < 0 || kind > 3)
+      throw error(SF_ERR_ARG, "bad face condition");
+    bc_[2 * axis + side] = {kind, {vel ? vel[0] : 0.0, vel ? vel[1] : 0.0, vel ? vel[2] : 0.0}};
+    // refresh the block face kinds the fused kernels read and drop cached phases
+    download_table();
+    for (int b = 0; b < nloc_; ++b) {
+      const int fi = 2 * axis + side;
+      if (dec_.neighbor(gid_[b], axis, side) < 0) {
+        htab_->blk[b].face[fi] = kind == SF_BC_WALL ? FACE_WALL : kind == SF_BC_SYMMETRY ? FACE_SYM
+                                 : kind == SF_BC_OUTFLOW ? FACE_OUT : FACE_WALL;
+        for (int c = 0; c < 3; ++c) htab_->blk[b].fvel[fi][c] = bc_[fi].velocity[c];
+      }
+    }
+    SF_CK(cudaMemcpy(dtab_->blk, htab_->blk, sizeof(htab_->blk), cudaMemcpyHostToDevice));
+    phases_.clear();
+  }
+
+  // executor::physical_bc (executor.hpp:516-518): bc fills only, x then y then z
+  void physical_bc(const std::vector<int>& fields) {
+    if (fields.empty()) return;
+    validate_bc(fields);
+    unsigned mask = 0;
+    for (int f : fields) mask |= 1u << f;
+    for (int axis = 0; axis < 3; ++axis) run_phase(phase_for(mask, axis, SF_SCOPE_ALL, false, true), false);
+    check_launch();
+  }
+
+  // ---- schedules (executor.hpp:420-470, 533-601) ---------------------------
+  struct sched_step {
+    int kind;  // 0 run, 1 exchange, 2 physical_bc, 3 refresh, 4 reduce (schedule_step::kind)
+    std::string kernel;
+    int reg = 0;
+    std::vector<std::string> fields;
+    std::string source, target;
+    int op = 0;
+  };
+  std::map<std::string, double> results_;
+
+  void kernel_io(const std::string& name, std::vector<std::string>& reads, std::vector<std::string>& writes,
+                 int& max_halo) {
+    reads.clear();
+    writes.clear();
+    max_halo = 0;
+    if (is_user_kernel(name)) {
+      const auto& k = ukernels_.at(name);
+      for (int h : k.halo) max_halo = std::max(max_halo, h);
+      for (size_t b = 0; b < k.fid.size(); ++b) {
+        if (k.intent[b] != 1) reads.push_back(fname_[k.fid[b]]);
+        if (k.intent[b] != 0) writes.push_back(fname_[k.fid[b]]);
+      }
+      return;
+    }
+    for (const auto& p : cfd_plans())
+      if (p.name == name) {
+        for (int h : p.halo) max_halo = std::max(max_halo, h);
+        for (size_t b = 0; b < p.bindings.size(); ++b) {
+          const bool w = p.writable[b];
+          // every CFD binding is readable except DIVERGENCE's OUT divu (cfd.hpp:139-142)
+          if (!(p.name == "DIVERGENCE" && p.bindings[b] == "divu")) reads.push_back(p.bindings[b]);
+          if (w) writes.push_back(p.bindings[b]);
+        }
+        return;
+      }
+    throw error(SF_ERR_EXEC, "unknown kernel '" + name + "'");
+  }
+
+  void dry_run(const std::vector<sched_step>& s, int steps) {  // executor.hpp:559-601
+    auto ok = ghosts_ok_;
+    const int passes = std::min(steps, 4);
+    for (int pass = 0; pass < passes; ++pass) {
+      const auto before = ok;
+      for (size_t i = 0; i < s.size(); ++i) {
+        const auto& st = s[i];
+        const std::string where = "schedule step " + std::to_string(i + 1);
+        auto require = [&](const std::string& f) {
+          bool found = false;
+          for (const auto& n : fname_) found = found || n == f;
+          if (!found) throw error(SF_ERR_EXEC, where + ": unknown field '" + f + "'");
+        };
+        switch (st.kind) {
+          case 1:
+          case 3:
+            for (const auto& f : st.fields) {
+              require(f);
+              ok[f] = true;
+            }
+            break;
+          case 2:
+            for (const auto& f : st.fields) require(f);
+            break;
+          case 4:
+            require(st.source);
+            break;
+          case 0: {
+            std::vector<std::string> rd, wr;
+            int mh = 0;
+            try {
+              kernel_io(st.kernel, rd, wr, mh);
+            } catch (const error&) {
+              throw error(SF_ERR_EXEC, where + ": unknown kernel '" + st.kernel + "'");
+            }
+            if (mh > 0 && st.reg != SF_REGION_INTERIOR)
+              for (const auto& f : rd) {
+                auto it = ok.find(f);
+                if (it == ok.end() || !it->second)
+                  throw error(SF_ERR_EXEC, where + ": kernel '" + st.kernel + "' reads ghosts of '" + f +
+                                               "' that were never exchanged");
+              }
+            for (const auto& f : wr) ok[f] = false;
+            break;
+          }
+        }
+      }
+      if (ok == before) break;
+    }
+  }
+
+  void run_schedule(const std::vector<sched_step>& s, const std::map<std::string, double>& params, int steps) {
+    dry_run(s, steps);
+    for (int pass = 0; pass < steps; ++pass)
+      for (const auto& st : s) {
+        std::vector<int> fl;
+        for (const auto& f : st.fields) fl.push_back(field_id(f));
+        switch (st.kind) {
+          case 0: run_kernel(st.kernel, params, st.reg); break;
+          case 1: exchange_only(fl); break;
+          case 2: physical_bc(fl); break;
+          case 3: refresh(fl); break;
+          case 4: results_[st.target] = reduce(field_id(st.source), st.op); break;
+        }
+      }
+  }
+  bool result(const std::string& name, double* v) const {
+    auto it = results_.find(name);
+    if (it == results_.end()) return false;
+    *v = it->second;
+    return true;
+  }
+
+  void run_user_kernel(const std::string& name, const std::map<std::string, double>& params, int reg) {
+    user_kernel& uk = ukernels_.at(name);
+    struct { double v[32]; } prm{};
+    if (uk.params.size() > 32) throw error(SF_ERR_ARG, "at most 32 parameters");
+    for (size_t i = 0; i < uk.params.size(); ++i) {
+      auto it = params.find(uk.params[i]);
+      if (it == params.end())
+        throw error(SF_ERR_EXEC, "kernel '" + name + "': parameter '" + uk.params[i] + "' not supplied");
+      prm.v[i] = it->second;
+    }
+    if (reg < 0 || reg > 2) throw error(SF_ERR_ARG, "bad region");
+    if (debug_bounds()) check_ghosts(uk, reg);
+    const work_set& ws = items_for(reg, uk.halo, uk.zc, uk.tx, uk.ty);
+    if (ws.nctas > 0) {
+      double* const* ptrs = &dtab_->ptr[0][0][0];
+      const void* geo = geo_;
+      const sf_work* items = ws.d;
+      int nitems = ws.n, zc = uk.zc;
+      void* args[] = {(void*)&ptrs, (void*)&geo, (void*)&items, (void*)&nitems, (void*)&zc, (void*)&prm};
+      SF_CK(cudaLaunchKernel((const void*)uk.k, dim3(ws.nctas), dim3(uk.tx, uk.ty), args, 0, st_));
+      ++launches_;
+      if (uk.debug) {
+        int w[5] = {0, 0, 0, 0, 0};
+        sync();
+        SF_CK(cudaMemcpy(w, dbg_word_, sizeof w, cudaMemcpyDeviceToHost));
+        if (w[0]) {
+          SF_CK(cudaMemset(dbg_word_, 0, 8 * sizeof(int)));
+          const std::string f = fname_[uk.fid[w[1]]];
+          const std::string k = "kernel '" + name + "': ";
+          switch (w[0]) {  // executor.hpp:153-172
+            case 1: throw error(SF_ERR_EXEC, k + "read of write-only binding '" + f + "'");
+            case 2: throw error(SF_ERR_EXEC, k + "non-center read of in-place binding '" + f + "'");
+            case 3:
+              throw error(SF_ERR_EXEC, k + "read offset (" + std::to_string(w[2]) + "," + std::to_string(w[3]) + "," +
+                                           std::to_string(w[4]) + ") outside the declared stencil of '" + f + "'");
+            default: throw error(SF_ERR_EXEC, k + "store to read-only binding '" + f + "'");
+          }
+        }
+      }
+    }
+    // finish_run (executor.hpp:769-779)
+    for (size_t b = 0; b < uk.fid.size(); ++b) {
+      const bool writable = uk.intent[b] != 0;
+      const bool to_back = uk.intent[b] == 3;
+      if (reg != SF_REGION_INTERIOR) {
+        if (to_back) ctl(CTL_SWAP, 0.0, uk.fid[b], FRONT, BACK);
+        if (writable) ghosts_ok_[fname_[uk.fid[b]]] = false;
+      } else if (writable && !to_back) {
+        ghosts_ok_[fname_[uk.fid[b]]] = false;
+      }
+    }
+  }
+
+  static bool debug_bounds() {  // executor.hpp:645-648
+    const char* e = getenv("SF_DEBUG_BOUNDS");
+    return e && *e && std::string(e) != "0";
+  }
+  void check_ghosts(const user_kernel& k, int reg) const {  // executor.hpp:751-757
+    int mh = 0;
+    for (int h : k.halo) mh = std::max(mh, h);
+    if (mh == 0 || reg == SF_REGION_INTERIOR) return;
+    for (size_t b = 0; b < k.fid.size(); ++b)
+      if (k.intent[b] != 1 && !ghosts_valid(fname_[k.fid[b]]))
+        throw error(SF_ERR_EXEC, "kernel '" + k.name + "' reads ghosts of '" + fname_[k.fid[b]] +
+                                     "' that were never exchanged");
+  }
+
   double reduce(int f, int op) {
     if (op == SF_MAX_ABS || op == SF_MAX_ABS_DIFF) {
-      if (op == SF_MAX_ABS_DIFF && f > SF_VZ)
+      if (op == SF_MAX_ABS_DIFF && !has_back(f))
         throw error(SF_ERR_GRID,
-                    std::string("field '") + kFieldNames[f] + "' has no back buffer to diff against");
+                    std::string("field '") + fname_[f] + "' has no back buffer to diff against");
       ctl(CTL_CLEAR_ACC);
       const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_plain_);
       const int fl[1] = {f};
@@ -684,7 +1069,7 @@ class simulation {
     ++launches_;
     check_launch();
     swap_front_back();
-    for (int f : {SF_VX, SF_VY, SF_VZ}) ghosts_ok_[kFieldNames[f]] = false;
+    for (int f : {SF_VX, SF_VY, SF_VZ}) ghosts_ok_[fname_[f]] = false;
     allreduce_max(&dctl_->acc[1], 3);
     ctl(CTL_CHECK_FINITE);
   }
@@ -694,7 +1079,7 @@ class simulation {
     if (a >= 0) {
       char buf[64];
       std::snprintf(buf, sizeof buf, "%f", time_);  // std::to_string(double)
-      throw error(SF_ERR_CFD, std::string("non-finite ") + kFieldNames[a] +
+      throw error(SF_ERR_CFD, std::string("non-finite ") + fname_[a] +
                                   " after the velocity update at step " + std::to_string(steps_) +
                                   ", t = " + buf);
     }
@@ -754,7 +1139,7 @@ class simulation {
     // ghost state as the reference leaves it (executor.hpp:769-779)
     ghosts_ok_["p"] = false;
     ghosts_ok_["divu"] = false;
-    for (int f : {SF_VX, SF_VY, SF_VZ}) ghosts_ok_[kFieldNames[f]] = true;
+    for (int f : {SF_VX, SF_VY, SF_VZ}) ghosts_ok_[fname_[f]] = true;
     return {sweeps, residual};
   }
   std::pair<int, double> pressure_iteration(double dt) {
@@ -848,6 +1233,11 @@ class simulation {
   sf_solver_config cfg_;
   sf_fluid_params par_;
   sf_sim_options opt_;
+  std::map<std::string, user_kernel> ukernels_;
+  int* dbg_word_ = nullptr;  // debug policing: {code, slot, di, dj, dk}
+  void* geo_ = nullptr;  // per local block: n[3], lo[3], sx, sy, base (sf_jit.hpp sf_geo)
+  std::vector<std::string> fname_ = {"vx", "vy", "vz", "p", "divu"};
+  std::vector<int> fstag_ = {0, 1, 2, -1, -1};  // stagger per field (field.hpp:23)
   int rank_ = 0, world_ = 1;
   bool dist_ = false;  // NCCL transport (one grid component per rank)
   decomposition dec_;
@@ -1007,16 +1397,11 @@ class simulation {
           const i64 N = cfg_.extents[a];
           B.nb_ghost_gidx[fi] = side == 0 ? (L.lo[a] - 1 + N) % N : (L.lo[a] + L.dims[a]) % N;
         }
-      const size_t bytes = sizeof(double) * (size_t)(L.sx * L.sy * L.sz);
       for (int f = 0; f < SF_NFIELDS; ++f) {
         const bool velocity = f <= SF_VZ;
         for (int s = 0; s < kSlots; ++s) {
           const bool need = s == FRONT || (velocity && (s == BACK || s == ALT)) || (f == SF_DIVU && s == ALT);
-          if (!need) continue;
-          double* p = (double*)dalloc(bytes);
-          SF_CK(cudaMemsetAsync(p, 0, bytes, st_));
-          htab_->ptr[b][f][s] = p;
-          htab_->bidx[b][f][s] = (unsigned char)s;
+          if (need) alloc_slot(b, f, s);
         }
       }
     }
@@ -1037,6 +1422,19 @@ class simulation {
         SF_CK(cudaMemcpy(maps_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
       }
     }
+    {
+      std::vector<long long> geo;
+      for (int b = 0; b < nloc_; ++b) {
+        const sf_layout& L = lay_[b];
+        for (int a = 0; a < 3; ++a) geo.push_back(L.dims[a]);
+        for (int a = 0; a < 3; ++a) geo.push_back(L.lo[a]);
+        geo.push_back(L.sx);
+        geo.push_back(L.sy);
+        geo.push_back(L.base);
+      }
+      geo_ = dalloc(sizeof(long long) * geo.size());
+      SF_CK(cudaMemcpy(geo_, geo.data(), sizeof(long long) * geo.size(), cudaMemcpyHostToDevice));
+    }
     dtab_ = (sf_dev_table*)dalloc(sizeof(sf_dev_table));
     SF_CK(cudaMemcpyAsync(dtab_, htab_.get(), sizeof(sf_dev_table), cudaMemcpyHostToDevice, st_));
     dctl_ = (sf_dev_ctl*)dalloc(sizeof(sf_dev_ctl));
@@ -1050,6 +1448,19 @@ class simulation {
   void download_table() {
     sync();
     SF_CK(cudaMemcpy(htab_->ptr, dtab_->ptr, sizeof(htab_->ptr), cudaMemcpyDeviceToHost));
+    SF_CK(cudaMemcpy(htab_->bidx, dtab_->bidx, sizeof(htab_->bidx), cudaMemcpyDeviceToHost));
+  }
+  void upload_table() {
+    SF_CK(cudaMemcpy(dtab_->ptr, htab_->ptr, sizeof(htab_->ptr), cudaMemcpyHostToDevice));
+    SF_CK(cudaMemcpy(dtab_->bidx, htab_->bidx, sizeof(htab_->bidx), cudaMemcpyHostToDevice));
+  }
+  void alloc_slot(int b, int f, int s) {
+    const sf_layout& L = lay_[b];
+    const size_t bytes = sizeof(double) * (size_t)(L.sx * L.sy * L.sz);
+    double* p = (double*)dalloc(bytes);
+    SF_CK(cudaMemsetAsync(p, 0, bytes, st_));
+    htab_->ptr[b][f][s] = p;
+    htab_->bidx[b][f][s] = (unsigned char)s;
   }
 
   table_view tview() const { return table_view{dtab_, nullptr, 0}; }
@@ -1074,10 +1485,11 @@ class simulation {
     return v;
   }
 
-  const work_set& items_for(int reg, const std::array<int, 6>& halo, int zc) {
-    char key[128];
-    std::snprintf(key, sizeof key, "%d:%d,%d,%d,%d,%d,%d:%d", reg, halo[0], halo[1], halo[2],
-                  halo[3], halo[4], halo[5], zc);
+  const work_set& items_for(int reg, const std::array<int, 6>& halo, int zc, int tx = kTX,
+                            int ty = kTY) {
+    char key[160];
+    std::snprintf(key, sizeof key, "%d:%d,%d,%d,%d,%d,%d:%d:%d:%d", reg, halo[0], halo[1], halo[2],
+                  halo[3], halo[4], halo[5], zc, tx, ty);
     auto it = items_.find(key);
     if (it != items_.end()) return it->second;
     std::vector<sf_work> v;
@@ -1092,8 +1504,8 @@ class simulation {
           w.lo[a] = bx[a];
           w.hi[a] = bx[3 + a];
         }
-        w.tiles[0] = (int)((w.hi[0] - w.lo[0] + kTX - 1) / kTX);
-        w.tiles[1] = (int)((w.hi[1] - w.lo[1] + kTY - 1) / kTY);
+        w.tiles[0] = (int)((w.hi[0] - w.lo[0] + tx - 1) / tx);
+        w.tiles[1] = (int)((w.hi[1] - w.lo[1] + ty - 1) / ty);
         w.tiles[2] = (int)((w.hi[2] - w.lo[2] + zc - 1) / zc);
         cta += w.tiles[0] * w.tiles[1] * w.tiles[2];
         v.push_back(w);
@@ -1114,7 +1526,7 @@ class simulation {
       if (cfg_.periodic[axis]) continue;
       for (int side = 0; side < 2; ++side)
         if (bc_[2 * axis + side].kind == SF_BC_UNSET && !fields.empty())
-          throw error(SF_ERR_GRID, std::string("field '") + kFieldNames[fields.front()] +
+          throw error(SF_ERR_GRID, std::string("field '") + fname_[fields.front()] +
                                        "': no boundary condition on axis " + std::to_string(axis) +
                                        (side == 0 ? " low" : " high") + " face");
     }
@@ -1169,14 +1581,19 @@ class simulation {
   // axis >= 0: refresh/exchange phase of that axis (slabs widened over earlier
   // axes).  axis < 0: the fused loop's divu faces, all axes, owned tangential
   // ranges, no physical fills (the half-sweep writes those itself).
-  const phase& phase_for(unsigned mask, int axis, int scope, bool exchange_only) {
+  const phase& phase_for(unsigned mask, int axis, int scope, bool exchange_only, bool bc_only = false) {
     char key[64];
-    std::snprintf(key, sizeof key, "%u:%d:%d:%d", mask, axis, scope, exchange_only ? 1 : 0);
+    std::snprintf(key, sizeof key, "%u:%d:%d:%d:%d", mask, axis, scope, exchange_only ? 1 : 0, bc_only ? 1 : 0);
     auto it = phases_.find(key);
     if (it != phases_.end()) return it->second;
     const bool faces = axis < 0;
     const std::vector<int> axes = faces ? std::vector<int>{0, 1, 2} : std::vector<int>{axis};
-    const phase_plan P = build_phase_plan(dec_, gid_, lid_, owner_, mask, axes, !faces, exchange_only, faces);
+    phase_plan P = build_phase_plan(dec_, gid_, lid_, owner_, mask, axes, !faces, exchange_only, faces);
+    if (bc_only) {  // executor::physical_bc: no exchange at all
+      P.copies.clear();
+      P.sends.clear();
+      P.recvs.clear();
+    }
     phase ph;
     std::vector<sf_task> first, unpack;
     for (const auto& c : P.copies) first.push_back(task_of(c, 0));
@@ -1185,9 +1602,9 @@ class simulation {
       const sf_face_bc& fb = bc_[2 * b.axis + b.side];
       t.kind = fb.kind;
       t.scope = scope;
-      t.normal = kStagger[b.field] == b.axis;
-      t.velocity = kStagger[b.field] >= 0;
-      const double vwall = t.velocity ? fb.velocity[kStagger[b.field]] : 0.0;
+      t.normal = fstag_[b.field] == b.axis;
+      t.velocity = fstag_[b.field] >= 0;
+      const double vwall = t.velocity ? fb.velocity[fstag_[b.field]] : 0.0;
       t.v = (t.normal && fb.kind == SF_BC_SYMMETRY) ? 0.0 : vwall;
       first.push_back(t);
     }
@@ -1256,7 +1673,9 @@ class simulation {
 
   void enqueue_half_sweep() {
     if (opt_.fused) {
-      const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_);
+      int ftx = kTX, fty = kTY;
+      if (maps_ && opt_.fused == 1) sweep_tile_shape(&ftx, &fty);
+      const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, ftx, fty);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
       // single process: the kernel's last CTA finalises the sweep; across
       // ranks the residual first needs the max over ranks
@@ -1321,9 +1740,9 @@ int need(const void* p, const char* what) {
   return 0;
 }
 
-std::vector<int> field_list(const char* const* fields, int n) {
+std::vector<int> field_list(const sfb::simulation& S, const char* const* fields, int n) {
   std::vector<int> out;
-  for (int i = 0; i < n; ++i) out.push_back(sfb::simulation::field_id(fields[i]));
+  for (int i = 0; i < n; ++i) out.push_back(S.field_id(fields[i]));
   return out;
 }
 
@@ -1514,13 +1933,13 @@ int sf_sim_rank(const sf_sim* s) { return s ? s->s->rank() : -1; }
 int sf_sim_gather_block(sf_sim* s, const char* field, int worker, double* host, int64_t n) {
   return guarded([&] {
     need(s, "sim");
-    s->s->block_io(sfb::simulation::field_id(field), worker, host, n, false);
+    s->s->block_io(s->s->field_id(field), worker, host, n, false);
   });
 }
 int sf_sim_scatter_block(sf_sim* s, const char* field, int worker, const double* host, int64_t n) {
   return guarded([&] {
     need(s, "sim");
-    s->s->block_io(sfb::simulation::field_id(field), worker, const_cast<double*>(host), n, true);
+    s->s->block_io(s->s->field_id(field), worker, const_cast<double*>(host), n, true);
   });
 }
 int sf_sim_world(const sf_sim* s) { return s ? s->s->world() : 0; }
@@ -1617,7 +2036,7 @@ int sf_sim_scatter(sf_sim* s, const char* field, const double* host, int64_t n) 
     if (n != S.cells())
       throw sfb::error(SF_ERR_GRID, "scatter: global array has " + std::to_string(n) +
                                         " values, domain has " + std::to_string(S.cells()) + " cells");
-    S.scatter(sfb::simulation::field_id(field), host);
+    S.scatter(S.field_id(field), host);
   });
 }
 int sf_sim_gather(sf_sim* s, const char* field, double* host, int64_t n) {
@@ -1625,7 +2044,7 @@ int sf_sim_gather(sf_sim* s, const char* field, double* host, int64_t n) {
     auto& S = SIM(s);
     need(host, "host");
     if (n < S.cells()) throw sfb::error(SF_ERR_ARG, "gather: host buffer too small");
-    S.gather(sfb::simulation::field_id(field), host);
+    S.gather(S.field_id(field), host);
   });
 }
 int sf_sim_scatter_device(sf_sim* s, const char* field, const double* dev, int64_t n) {
@@ -1633,7 +2052,7 @@ int sf_sim_scatter_device(sf_sim* s, const char* field, const double* dev, int64
     auto& S = SIM(s);
     need(dev, "dev");
     if (n != S.cells()) throw sfb::error(SF_ERR_GRID, "scatter: size mismatch");
-    S.scatter_from_device(sfb::simulation::field_id(field), dev);
+    S.scatter_from_device(S.field_id(field), dev);
   });
 }
 int sf_sim_gather_device(sf_sim* s, const char* field, double* dev, int64_t n) {
@@ -1641,7 +2060,7 @@ int sf_sim_gather_device(sf_sim* s, const char* field, double* dev, int64_t n) {
     auto& S = SIM(s);
     need(dev, "dev");
     if (n < S.cells()) throw sfb::error(SF_ERR_ARG, "gather: device buffer too small");
-    S.gather_to_device(sfb::simulation::field_id(field), dev);
+    S.gather_to_device(S.field_id(field), dev);
   });
 }
 int sf_sim_checksum(sf_sim* s, uint64_t* out) {
@@ -1655,7 +2074,7 @@ int sf_sim_local_front(sf_sim* s, const char* field, int worker, double* host, i
   return guarded([&] {
     need(host, "host");
     long long d[3], l[3];
-    SIM(s).local_front(sfb::simulation::field_id(field), worker, host, host_elems, d, l);
+    SIM(s).local_front(SIM(s).field_id(field), worker, host, host_elems, d, l);
     for (int a = 0; a < 3; ++a) {
       dims[a] = d[a];
       lo[a] = l[a];
@@ -1665,13 +2084,13 @@ int sf_sim_local_front(sf_sim* s, const char* field, int worker, double* host, i
 int sf_sim_refresh(sf_sim* s, const char* const* fields, int n) {
   return guarded([&] {
     auto& S = SIM(s);
-    S.refresh(field_list(fields, n));
+    S.refresh(field_list(S, fields, n));
   });
 }
 int sf_sim_exchange(sf_sim* s, const char* const* fields, int n) {
   return guarded([&] {
     auto& S = SIM(s);
-    S.exchange_only(field_list(fields, n));
+    S.exchange_only(field_list(S, fields, n));
   });
 }
 int sf_sim_run_kernel(sf_sim* s, const char* name, const char* const* param_names,
@@ -1687,9 +2106,79 @@ int sf_sim_reduce(sf_sim* s, const char* field, int op, double* out) {
   return guarded([&] {
     need(out, "out");
     if (op < 0 || op > 3) throw sfb::error(SF_ERR_ARG, "bad reduce op");
-    *out = SIM(s).reduce(sfb::simulation::field_id(field), op);
+    *out = SIM(s).reduce(SIM(s).field_id(field), op);
   });
 }
+int sf_sim_create_field(sf_sim* s, const char* name, int stagger) {
+  return guarded([&] {
+    need(name, "name");
+    SIM(s).create_field(name, stagger);
+  });
+}
+
+int sf_sim_register_kernel(sf_sim* s, const sf_plan* plan, const char* const* sig_fields, int n_sig_fields,
+                           const char* const* sig_params, int n_sig_params, const char* point_body) {
+  return guarded([&] {
+    need(plan, "plan");
+    need(plan->kernel, "plan->kernel");
+    need(point_body, "point_body");
+    std::array<int, 3> tile{plan->tile[0], plan->tile[1], plan->tile[2]};
+    std::array<int, 6> halo{};
+    for (int a = 0; a < 6; ++a) halo[a] = plan->halo[a];
+    std::vector<std::string> bf, pr, sf, sp;
+    std::vector<int> in;
+    for (int i = 0; i < plan->n_bindings; ++i) {
+      bf.push_back(plan->bindings[i].field);
+      in.push_back(plan->bindings[i].intent);
+    }
+    for (int i = 0; i < plan->n_params; ++i) pr.push_back(plan->params[i]);
+    for (int i = 0; i < n_sig_fields; ++i) sf.push_back(sig_fields[i]);
+    for (int i = 0; i < n_sig_params; ++i) sp.push_back(sig_params[i]);
+    SIM(s).register_kernel(plan->kernel, tile, halo, bf, in, pr, sf, sp, point_body);
+  });
+}
+
+int sf_sim_set_face_bc(sf_sim* s, int axis, int side, int kind, const double velocity[3]) {
+  return guarded([&] { SIM(s).set_face_bc(axis, side, kind, velocity); });
+}
+
+int sf_sim_physical_bc(sf_sim* s, const char* const* fields, int n) {
+  return guarded([&] {
+    auto& S = SIM(s);
+    S.physical_bc(field_list(S, fields, n));
+  });
+}
+
+int sf_sim_run_schedule(sf_sim* s, const sf_schedule_step* steps, int n_steps, const char* const* param_names,
+                        const double* param_values, int n_params, int passes, int mode) {
+  return guarded([&] {
+    (void)mode;  // overlap and plain give identical results (executor.hpp:812-861); one stream here
+    auto& S = SIM(s);
+    std::vector<sfb::simulation::sched_step> v;
+    for (int i = 0; i < n_steps; ++i) {
+      sfb::simulation::sched_step st;
+      st.kind = steps[i].kind;
+      if (steps[i].kernel) st.kernel = steps[i].kernel;
+      st.reg = steps[i].region;
+      for (int q = 0; q < steps[i].n_fields; ++q) st.fields.push_back(steps[i].fields[q]);
+      if (steps[i].source) st.source = steps[i].source;
+      if (steps[i].target) st.target = steps[i].target;
+      st.op = steps[i].op;
+      v.push_back(st);
+    }
+    std::map<std::string, double> pm;
+    for (int i = 0; i < n_params; ++i) pm[param_names[i]] = param_values[i];
+    S.run_schedule(v, pm, passes);
+  });
+}
+
+int sf_sim_result(sf_sim* s, const char* name, double* value) {
+  return guarded([&] {
+    need(value, "value");
+    if (!SIM(s).result(name, value)) throw sfb::error(SF_ERR_EXEC, std::string("no result named '") + name + "'");
+  });
+}
+
 int sf_sim_invalidate_ghosts(sf_sim* s, const char* field) {
   return guarded([&] { SIM(s).invalidate(field); });
 }

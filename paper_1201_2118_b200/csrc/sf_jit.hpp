@@ -1,0 +1,167 @@
+// sf_jit.hpp -- descriptor-declared stencil kernels, generated and compiled on
+// the fly for sm_100a (the B200 form of CaCUDA's "kernel descriptor ->
+// generated CUDA tile template"; reference API
+// exec::executor::register_kernel, executor.hpp:484-488, 650-692).
+//
+// The user supplies the BODY of a point function written against the
+// reference's point_ctx / cell_view API (executor.hpp:130-184):
+//     c.field(s)(di, dj, dk)   read at an offset inside the declared halo
+//     c.field(s).load()        read the centre
+//     c.field(s).store(v)      write the centre (OUT, INOUT, SEPARATEINOUT)
+//     c.param(s)               parameter value in plan order
+//     c.i, c.j, c.k            global cell index
+// The body is pasted into a tile template (one 2-D column tile per CTA from
+// the plan's TILE, marching z, reads through the read-only path) and compiled
+// with NVRTC.  SEPARATEINOUT bindings read the front buffer and write the
+// back buffer; the executor swaps after the run (executor.hpp:769-779).
+#pragma once
+
+#include <dlfcn.h>
+
+#include <string>
+
+namespace sfb {
+
+struct nvrtc_api {
+  typedef int (*create_t)(void**, const char*, const char*, int, const char* const*, const char* const*);
+  typedef int (*compile_t)(void*, int, const char* const*);
+  typedef int (*size_t_fn)(void*, size_t*);
+  typedef int (*get_t)(void*, char*);
+  typedef int (*destroy_t)(void**);
+  typedef const char* (*err_t)(int);
+  create_t create = nullptr;
+  compile_t compile = nullptr;
+  size_t_fn log_size = nullptr;
+  get_t log = nullptr;
+  size_t_fn cubin_size = nullptr;
+  get_t cubin = nullptr;
+  destroy_t destroy = nullptr;
+  err_t err = nullptr;
+};
+
+inline nvrtc_api* nvrtc() {
+  static nvrtc_api api;
+  static bool tried = false;
+  if (tried) return api.create ? &api : nullptr;
+  tried = true;
+  const char* names[] = {getenv("SF_NVRTC_LIB"), "libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12",
+                         "libnvrtc.so"};
+  void* h = nullptr;
+  for (const char* n : names)
+    if (n && (h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!h) return nullptr;
+  api.create = (nvrtc_api::create_t)dlsym(h, "nvrtcCreateProgram");
+  api.compile = (nvrtc_api::compile_t)dlsym(h, "nvrtcCompileProgram");
+  api.log_size = (nvrtc_api::size_t_fn)dlsym(h, "nvrtcGetProgramLogSize");
+  api.log = (nvrtc_api::get_t)dlsym(h, "nvrtcGetProgramLog");
+  api.cubin_size = (nvrtc_api::size_t_fn)dlsym(h, "nvrtcGetCUBINSize");
+  api.cubin = (nvrtc_api::get_t)dlsym(h, "nvrtcGetCUBIN");
+  api.destroy = (nvrtc_api::destroy_t)dlsym(h, "nvrtcDestroyProgram");
+  api.err = (nvrtc_api::err_t)dlsym(h, "nvrtcGetErrorString");
+  if (!api.create || !api.compile || !api.cubin || !api.cubin_size) api.create = nullptr;
+  return api.create ? &api : nullptr;
+}
+
+// The tile template.  SF_NB bindings, SF_NP parameters, SF_TX x SF_TY threads,
+// SF_MAXF fields / SF_SLOTS slots per block in the device pointer table.
+inline const char* jit_template() {
+  return R"JIT(
+struct sf_work { int blk; int cta_begin; int tiles[3]; long long lo[3], hi[3]; };
+struct sf_params { double v[SF_NP > 0 ? SF_NP : 1]; };
+struct sf_geo { long long n[3], lo[3], sx, sy, base; };
+
+// Debug policing (SF_DEBUG_BOUNDS, executor.hpp:153-172): the first
+// violation is recorded as {code, slot, di, dj, dk} and the access skipped;
+// the host raises exec_error with the reference's text after the launch.
+__device__ int* sf_err_word;
+__device__ __forceinline__ void sf_violation(int code, int slot, int di, int dj, int dk) {
+  if (atomicCAS(sf_err_word, 0, code) == 0) {
+    sf_err_word[1] = slot;
+    sf_err_word[2] = di;
+    sf_err_word[3] = dj;
+    sf_err_word[4] = dk;
+  }
+}
+
+struct cell_view {
+  const double* rd;
+  double* wr;
+  long long o, sx, sxy;
+  int slot;
+  __device__ __forceinline__ double operator()(int di, int dj, int dk) const {
+#if SF_DEBUG
+    if (!SF_READABLE[slot]) { sf_violation(1, slot, di, dj, dk); return 0.0; }
+    if (SF_CENTER_ONLY[slot] && (di != 0 || dj != 0 || dk != 0)) { sf_violation(2, slot, di, dj, dk); return 0.0; }
+    if (di < -SF_HALO[0] || di > SF_HALO[1] || dj < -SF_HALO[2] || dj > SF_HALO[3] || dk < -SF_HALO[4] ||
+        dk > SF_HALO[5]) { sf_violation(3, slot, di, dj, dk); return 0.0; }
+#endif
+    return rd[o + di + dj * sx + dk * sxy];
+  }
+  __device__ __forceinline__ double load() const { return (*this)(0, 0, 0); }
+  __device__ __forceinline__ void store(double v) const {
+#if SF_DEBUG
+    if (!SF_WRITABLE[slot]) { sf_violation(4, slot, 0, 0, 0); return; }
+#endif
+    wr[o] = v;
+  }
+};
+
+struct point_ctx {
+  cell_view f_[SF_NB];
+  const double* p_;
+  long long i, j, k;
+  __device__ __forceinline__ const cell_view& field(int s) const { return f_[s]; }
+  __device__ __forceinline__ double param(int s) const { return p_[s]; }
+};
+
+__device__ __forceinline__ void sf_user_point(const point_ctx& c) {
+SF_BODY
+}
+
+extern "C" __global__ void __launch_bounds__(SF_TX * SF_TY)
+sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
+               const sf_work* __restrict__ items, int nitems, int zc, sf_params prm) {
+  const int cta = blockIdx.x;
+  int lo_i = 0, hi_i = nitems - 1;
+  while (lo_i < hi_i) {
+    const int mid = (lo_i + hi_i + 1) >> 1;
+    if (items[mid].cta_begin <= cta) lo_i = mid; else hi_i = mid - 1;
+  }
+  const sf_work& w = items[lo_i];
+  const int local = cta - w.cta_begin;
+  const int tx = local % w.tiles[0];
+  const int ty = (local / w.tiles[0]) % w.tiles[1];
+  const int tz = local / (w.tiles[0] * w.tiles[1]);
+  const long long i = w.lo[0] + (long long)tx * SF_TX + threadIdx.x;
+  const long long j = w.lo[1] + (long long)ty * SF_TY + threadIdx.y;
+  if (i >= w.hi[0] || j >= w.hi[1]) return;
+  const long long k0 = w.lo[2] + (long long)tz * zc;
+  const long long k1 = k0 + zc < w.hi[2] ? k0 + zc : w.hi[2];
+  const sf_geo& G = geo[w.blk];
+  const long long sx = G.sx, sxy = G.sx * G.sy;
+  __shared__ double sp[SF_NP > 0 ? SF_NP : 1];
+  point_ctx c;
+  c.p_ = prm.v;
+  (void)sp;
+#pragma unroll
+  for (int s = 0; s < SF_NB; ++s) {
+    c.f_[s].rd = ptrs[(w.blk * SF_MAXF + SF_FID[s]) * SF_SLOTS + 0];
+    c.f_[s].wr = ptrs[(w.blk * SF_MAXF + SF_FID[s]) * SF_SLOTS + SF_WSLOT[s]];
+    c.f_[s].sx = sx;
+    c.f_[s].sxy = sxy;
+    c.f_[s].slot = s;
+  }
+  c.i = G.lo[0] + i;
+  c.j = G.lo[1] + j;
+  for (long long k = k0; k < k1; ++k) {
+    const long long o = G.base + (k * G.sy + j) * sx + i;
+#pragma unroll
+    for (int s = 0; s < SF_NB; ++s) c.f_[s].o = o;
+    c.k = G.lo[2] + k;
+    sf_user_point(c);
+  }
+}
+)JIT";
+}
+
+}  // namespace sfb

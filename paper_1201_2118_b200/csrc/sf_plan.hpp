@@ -47,7 +47,7 @@ phase_plan build_phase_plan(const Dec& dec, const std::vector<int>& gid, const s
   for (int b = 0; b < (int)gid.size(); ++b) {
     const int gw = gid[b];
     const auto dims = dec.dims(gw);
-    for (int f = 0; f < 8; ++f) {
+    for (int f = 0; f < 32; ++f) {
       if (!(mask & (1u << f))) continue;
       for (int a : axes) {
         auto send_box = [&](int side) {

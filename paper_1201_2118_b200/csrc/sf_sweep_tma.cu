@@ -65,24 +65,24 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 // inner coordinate (an odd x start raises "illegal instruction"; measured with
 // scripts/probes/tma_probe2.cu), so the x halo boxes begin two cells left of
 // the tile: divu covers x in [i0-2, i0+34), vx covers [i0-2, i0+32).
-constexpr int kStages = 4;
-constexpr int kXL = 2;                       // cells left of the tile in the x-halo boxes
-constexpr int kDW = kTX + 4, kDH = kTY + 2;  // divu box 36 x 10
-constexpr int kUW = kTX + 2;                 // vx box 34 x 8
-constexpr int kVH = kTY + 1;                 // vy box 32 x 9
-struct __align__(128) stage_t {
-  double d[kDH][kDW];  // 2880 B
-  double pad0[8];      // -> 2944
-  double u[kTY][kUW];  // 2176 B -> 5120
-  double v[kVH][kTX];  // 2304 B -> 7424
-  double p[kTY][kTX];  // 2048 B -> 9472
-  double w[kTY][kTX];  // 2048 B -> 11520
+constexpr int kXL = 2;  // cells left of the tile in the x-halo boxes
+
+// Shared-memory stage of one z plane for a TX x TY tile (every TMA
+// destination 128-byte aligned):
+//   divu (TX+4) x (TY+2), vx (TX+2) x TY, vy TX x (TY+1), p and vz TX x TY
+template <int TX, int TY>
+struct tile {
+  static constexpr int DW = TX + 4, DH = TY + 2, UW = TX + 2, VH = TY + 1;
+  static constexpr int r128(int b) { return (b + 127) / 128 * 128; }
+  static constexpr int OFF_D = 0;
+  static constexpr int OFF_U = r128(8 * DH * DW);
+  static constexpr int OFF_V = OFF_U + r128(8 * TY * UW);
+  static constexpr int OFF_P = OFF_V + r128(8 * VH * TX);
+  static constexpr int OFF_W = OFF_P + r128(8 * TY * TX);
+  static constexpr int BYTES = OFF_W + r128(8 * TY * TX);
+  static constexpr uint32_t TXB = 8u * (DH * DW + TY * UW + VH * TX + 2 * TY * TX);
+  static_assert((UW * 8) % 16 == 0 && (DW * 8) % 16 == 0, "TMA rows must be 16-byte multiples");
 };
-static_assert(sizeof(stage_t) == 11520, "stage layout");
-static_assert(offsetof(stage_t, u) % 128 == 0 && offsetof(stage_t, v) % 128 == 0 &&
-                  offsetof(stage_t, p) % 128 == 0 && offsetof(stage_t, w) % 128 == 0,
-              "TMA destinations must be 128-byte aligned");
-constexpr uint32_t kStageBytes = sizeof(double) * (kDH * kDW + kTY * kUW + kVH * kTX + 2 * kTY * kTX);
 
 struct sweep_maps {  // per block: [field][physical buffer]
   CUtensorMap m[kMaxBlocks][SF_NFIELDS][kSlots];
@@ -91,22 +91,23 @@ struct sweep_maps {  // per block: [field][physical buffer]
 // STAGES: ring depth.  MINB: CTAs per SM the register budget targets.  WS:
 // warp-specialised -- a ninth warp produces (TMA) and consumer warps release
 // stages through "empty" mbarriers instead of a per-plane CTA barrier.
-template <int STAGES, int MINB, bool WS>
-__global__ void __launch_bounds__(kTX* kTY + (WS ? 32 : 0), MINB)
+template <int STAGES, int MINB, bool WS, int TX, int TY>
+__global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
     k_sweep_div_tma(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems,
                     int zc, sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag,
                     unsigned int total_ctas, const sweep_maps* __restrict__ maps, int finalize) {
   constexpr int kStages = STAGES;
+  using TL = tile<TX, TY>;
   if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  stage_t* S = reinterpret_cast<stage_t*>(smem_raw);
+  auto sptr = [&](int st, int off) { return reinterpret_cast<double*>(smem_raw + st * TL::BYTES + off); };
   __shared__ __align__(8) uint64_t bars[kStages];
   __shared__ __align__(8) uint64_t empty_bars[kStages];
   __shared__ double smb[8];
 
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int tid = ty * kTX + tx;
-  const bool producer_warp = WS && ty == kTY;
+  const int tid = ty * TX + tx;
+  const bool producer_warp = WS && ty == TY;
   // tile location
   const int cta = blockIdx.x;
   const int it = nitems > 1 ? find_item(items, nitems, cta) : 0;
@@ -116,8 +117,8 @@ __global__ void __launch_bounds__(kTX* kTY + (WS ? 32 : 0), MINB)
   const int tix = local % wk.tiles[0];
   const int tiy = (local / wk.tiles[0]) % wk.tiles[1];
   const int tiz = local / (wk.tiles[0] * wk.tiles[1]);
-  const long long i0 = wk.lo[0] + (long long)tix * kTX;
-  const long long j0 = wk.lo[1] + (long long)tiy * kTY;
+  const long long i0 = wk.lo[0] + (long long)tix * TX;
+  const long long j0 = wk.lo[1] + (long long)tiy * TY;
   const long long k0 = wk.lo[2] + (long long)tiz * zc;
   const long long k1 = min(k0 + zc, wk.hi[2]);
   const int nplanes = (int)(k1 - k0);
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(kTX* kTY + (WS ? 32 : 0), MINB)
 #pragma unroll
     for (int q = 0; q < kStages; ++q) {
       mbar_init(&bars[q], 1);
-      if (WS) mbar_init(&empty_bars[q], kTY);  // one arrive per consumer warp
+      if (WS) mbar_init(&empty_bars[q], TY);  // one arrive per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -153,13 +154,12 @@ __global__ void __launch_bounds__(kTX* kTY + (WS ? 32 : 0), MINB)
   const CUtensorMap* mP = &maps->m[b][SF_P][tab->bidx[b][SF_P][FRONT]];
   const int xc = (int)(xo + i0), yc = (int)(g + j0), zc0 = (int)(g + k0);
   auto issue = [&](int stage, int plane) {
-    stage_t& st = S[stage];
-    mbar_expect_tx(&bars[stage], kStageBytes);
-    tma_load_3d(&st.d[0][0], mD, &bars[stage], xc - kXL, yc - 1, zc0 + plane);
-    tma_load_3d(&st.u[0][0], mU, &bars[stage], xc - kXL, yc, zc0 + plane);
-    tma_load_3d(&st.v[0][0], mV, &bars[stage], xc, yc - 1, zc0 + plane);
-    tma_load_3d(&st.p[0][0], mP, &bars[stage], xc, yc, zc0 + plane);
-    tma_load_3d(&st.w[0][0], mW, &bars[stage], xc, yc, zc0 + plane);
+    mbar_expect_tx(&bars[stage], TL::TXB);
+    tma_load_3d(sptr(stage, TL::OFF_D), mD, &bars[stage], xc - kXL, yc - 1, zc0 + plane);
+    tma_load_3d(sptr(stage, TL::OFF_U), mU, &bars[stage], xc - kXL, yc, zc0 + plane);
+    tma_load_3d(sptr(stage, TL::OFF_V), mV, &bars[stage], xc, yc - 1, zc0 + plane);
+    tma_load_3d(sptr(stage, TL::OFF_P), mP, &bars[stage], xc, yc, zc0 + plane);
+    tma_load_3d(sptr(stage, TL::OFF_W), mW, &bars[stage], xc, yc, zc0 + plane);
   };
   if (!WS && tid == 0) {
     const int npro = nplanes < kStages ? nplanes : kStages;
@@ -250,13 +250,17 @@ __global__ void __launch_bounds__(kTX* kTY + (WS ? 32 : 0), MINB)
     if (has_next) mbar_wait(&bars[st1], (uint32_t)(((kk + 1) / kStages) & 1));
     const int kl = (int)(k0 + kk);
     if (act && col_fast && kl >= zlo_fast && kl <= zhi_fast) {
-      const stage_t& T = S[st];
-      const double dC = T.d[ty + 1][tx + kXL];
-      const double dXp = T.d[ty + 1][tx + kXL + 1], dXm = T.d[ty + 1][tx + kXL - 1];
-      const double dYp = T.d[ty + 2][tx + kXL], dYm = T.d[ty][tx + kXL];
-      const double dZp = has_next ? S[st1].d[ty + 1][tx + kXL] : D[o + sxy];
-      const double p0 = T.p[ty][tx], u0 = T.u[ty][tx + kXL], uml = T.u[ty][tx + kXL - 1];
-      const double v0 = T.v[ty + 1][tx], vml = T.v[ty][tx], w0 = T.w[ty][tx];
+      const double* Td = sptr(st, TL::OFF_D);
+      const double* Tu = sptr(st, TL::OFF_U);
+      const double* Tv = sptr(st, TL::OFF_V);
+      const double* Tp = sptr(st, TL::OFF_P);
+      const double* Tw = sptr(st, TL::OFF_W);
+      const double dC = Td[(ty + 1) * TL::DW + (tx + kXL)];
+      const double dXp = Td[(ty + 1) * TL::DW + (tx + kXL + 1)], dXm = Td[(ty + 1) * TL::DW + (tx + kXL - 1)];
+      const double dYp = Td[(ty + 2) * TL::DW + (tx + kXL)], dYm = Td[(ty) * TL::DW + (tx + kXL)];
+      const double dZp = has_next ? sptr(st1, TL::OFF_D)[(ty + 1) * TL::DW + (tx + kXL)] : D[o + sxy];
+      const double p0 = Tp[(ty) * TX + (tx)], u0 = Tu[(ty) * TL::UW + (tx + kXL)], uml = Tu[(ty) * TL::UW + (tx + kXL - 1)];
+      const double v0 = Tv[(ty + 1) * TX + (tx)], vml = Tv[(ty) * TX + (tx)], w0 = Tw[(ty) * TX + (tx)];
       const int par = par_col ^ ((int)(B.lo[2] + kl) & 1);
       const double a0 = (par == color) ? 1.0 : 0.0, a1 = 1.0 - a0;
       const double d0 = mbI * dC * a0;
@@ -281,16 +285,20 @@ __global__ void __launch_bounds__(kTX* kTY + (WS ? 32 : 0), MINB)
       rmax = bb > rmax ? bb : rmax;
       wm_new = wn;
     } else if (act) {
-      const stage_t& T = S[st];
+      const double* Td = sptr(st, TL::OFF_D);
+      const double* Tu = sptr(st, TL::OFF_U);
+      const double* Tv = sptr(st, TL::OFF_V);
+      const double* Tp = sptr(st, TL::OFF_P);
+      const double* Tw = sptr(st, TL::OFF_W);
       const long long k = k0 + kk;
       const long long gk = B.lo[2] + k;
       const int bz = bin(per2, gk, s.nm1[2]), bzp = bnx(per2, gk, s.nm1[2]);
-      const double dC = T.d[ty + 1][tx + kXL];
-      const double dXp = T.d[ty + 1][tx + kXL + 1], dXm = T.d[ty + 1][tx + kXL - 1];
-      const double dYp = T.d[ty + 2][tx + kXL], dYm = T.d[ty][tx + kXL];
-      const double dZp = has_next ? S[st1].d[ty + 1][tx + kXL] : D[o + sxy];
-      const double p0 = T.p[ty][tx], u0 = T.u[ty][tx + kXL], uml = T.u[ty][tx + kXL - 1];
-      const double v0 = T.v[ty + 1][tx], vml = T.v[ty][tx], w0 = T.w[ty][tx];
+      const double dC = Td[(ty + 1) * TL::DW + (tx + kXL)];
+      const double dXp = Td[(ty + 1) * TL::DW + (tx + kXL + 1)], dXm = Td[(ty + 1) * TL::DW + (tx + kXL - 1)];
+      const double dYp = Td[(ty + 2) * TL::DW + (tx + kXL)], dYm = Td[(ty) * TL::DW + (tx + kXL)];
+      const double dZp = has_next ? sptr(st1, TL::OFF_D)[(ty + 1) * TL::DW + (tx + kXL)] : D[o + sxy];
+      const double p0 = Tp[(ty) * TX + (tx)], u0 = Tu[(ty) * TL::UW + (tx + kXL)], uml = Tu[(ty) * TL::UW + (tx + kXL - 1)];
+      const double v0 = Tv[(ty + 1) * TX + (tx)], vml = Tv[(ty) * TX + (tx)], w0 = Tw[(ty) * TX + (tx)];
       const double a0 = (((gi + gj + gk) & 1) == color) ? 1.0 : 0.0, a1 = 1.0 - a0;
       // this cell's sweep (cfd.hpp:712-719)
       const double d0 = smb[ic | bz] * dC * a0;
@@ -426,14 +434,26 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// Box shape per field role (see stage_t).
+static int sweep_variant();
+// tile shape of the selected pipeline variant
+void sweep_tile_shape(int* tx, int* ty) {
+  switch (sweep_variant()) {
+    case 9: case 11: *tx = 64; *ty = 4; break;
+    case 10: *tx = 128; *ty = 2; break;
+    default: *tx = 32; *ty = 8; break;
+  }
+}
+
+// Box shape per field role (see tile<>).
 static void box_for(int field, cuuint32_t box[3]) {
+  int tx, ty;
+  sweep_tile_shape(&tx, &ty);
   box[2] = 1;
   switch (field) {
-    case SF_DIVU: box[0] = kDW; box[1] = kDH; break;
-    case SF_VX: box[0] = kUW; box[1] = kTY; break;
-    case SF_VY: box[0] = kTX; box[1] = kVH; break;
-    default: box[0] = kTX; box[1] = kTY; break;
+    case SF_DIVU: box[0] = tx + 4; box[1] = ty + 2; break;
+    case SF_VX: box[0] = tx + 2; box[1] = ty; break;
+    case SF_VY: box[0] = tx; box[1] = ty + 1; break;
+    default: box[0] = tx; box[1] = ty; break;
   }
 }
 
@@ -456,18 +476,18 @@ size_t sweep_map_offset(int b, int f, int s) {
   return offsetof(sweep_maps, m) + sizeof(CUtensorMap) * ((size_t)(b * SF_NFIELDS + f) * kSlots + s);
 }
 
-template <int STAGES, int MINB, bool WS>
+template <int STAGES, int MINB, bool WS, int TX = 32, int TY = 8>
 static void launch_variant(const table_view& vw, int nctas, int zc, const sf_consts& c,
                            sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,
                            cudaStream_t st) {
-  const size_t smem = sizeof(stage_t) * STAGES;
+  const size_t smem = (size_t)tile<TX, TY>::BYTES * STAGES;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sweep_div_tma<STAGES, MINB, WS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(k_sweep_div_tma<STAGES, MINB, WS, TX, TY>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_sweep_div_tma<STAGES, MINB, WS><<<nctas, dim3(kTX, kTY + (WS ? 1 : 0)), smem, st>>>(
+  k_sweep_div_tma<STAGES, MINB, WS, TX, TY><<<nctas, dim3(TX, TY + (WS ? 1 : 0)), smem, st>>>(
       vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas,
       static_cast<const sweep_maps*>(maps), fin);
 }
@@ -492,6 +512,12 @@ void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_cons
     case 3: launch_variant<3, 3, true>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
     case 4: launch_variant<6, 2, true>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
     case 5: launch_variant<2, 4, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
+    case 6: launch_variant<6, 2, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
+    case 7: launch_variant<8, 2, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
+    case 8: launch_variant<6, 1, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
+    case 9: launch_variant<4, 2, false, 64, 4>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
+    case 10: launch_variant<4, 2, false, 128, 2>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
+    case 11: launch_variant<3, 2, false, 64, 4>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
     default: launch_variant<4, 2, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
   }
 }

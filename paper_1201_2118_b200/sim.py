@@ -71,6 +71,60 @@ def cavity_fluid(cfg: SolverConfig, alpha: float = 0.0) -> FluidParams:
     return FluidParams(viscosity=1.0 * 1.0 / cfg.reynolds, lid_speed=1.0, blend=alpha)
 
 
+INTENTS = {"IN": 0, "OUT": 1, "INOUT": 2, "SEPARATEINOUT": 3}
+STAGGER = {"none": -1, "x": 0, "y": 1, "z": 2}
+
+
+@dataclass
+class ExecutionPlan:
+    """codegen::execution_plan (codegen.hpp:41-57): kernel name, TILE, per-face
+    halo (-x,+x,-y,+y,-z,+z), bindings [(field, intent, cached)] in declaration
+    order, parameter names."""
+
+    kernel: str
+    tile: Sequence[int] = (16, 16, 16)
+    halo: Sequence[int] = (0, 0, 0, 0, 0, 0)
+    bindings: Sequence[tuple] = ()
+    parameters: Sequence[str] = ()
+
+
+BC_KINDS = {"unset": 0, "wall": 1, "symmetry": 2, "outflow": 3}
+STEP_KINDS = {"run": 0, "exchange": 1, "physical_bc": 2, "refresh": 3, "reduce": 4}
+
+
+@dataclass
+class ScheduleStep:
+    """exec::schedule_step (executor.hpp:422-466)."""
+
+    kind: str
+    kernel: str = ""
+    region: str = "all"
+    fields: Sequence[str] = ()
+    source: str = ""
+    op: str = "max_abs"
+    target: str = ""
+
+    @staticmethod
+    def run(kernel, region="all"):
+        return ScheduleStep("run", kernel=kernel, region=region)
+
+    @staticmethod
+    def exchange(fields):
+        return ScheduleStep("exchange", fields=tuple(fields))
+
+    @staticmethod
+    def physical_bc(fields):
+        return ScheduleStep("physical_bc", fields=tuple(fields))
+
+    @staticmethod
+    def refresh(fields):
+        return ScheduleStep("refresh", fields=tuple(fields))
+
+    @staticmethod
+    def reduce(source, op, target):
+        return ScheduleStep("reduce", source=source, op=op, target=target)
+
+
 @dataclass
 class StepStats:
     dt: float
@@ -288,6 +342,86 @@ class Simulation:
     def reduce(self, name: str, op: str = "max_abs") -> float:
         v = C.c_double()
         L.check(self._lib.sf_sim_reduce(self._h, name.encode(), REDUCE_OPS[op], C.byref(v)))
+        return v.value
+
+    def create_field(self, name: str, stagger: str | int = "none"):
+        """field_store::create (field.hpp:108-112)."""
+        st = STAGGER[stagger] if isinstance(stagger, str) else int(stagger)
+        L.check(self._lib.sf_sim_create_field(self._h, name.encode(), st))
+
+    def register_kernel(self, plan: ExecutionPlan, signature: tuple, body: str):
+        """executor::register_kernel (executor.hpp:484-488, 650-692).  ``signature``
+        = (fields, params) as kernel_signature; ``body`` is the CUDA C++ body of
+        the point function over point_ctx ``c`` (c.field(s)(di,dj,dk), .load(),
+        .store(v), c.param(s), c.i/c.j/c.k), JIT-compiled for sm_100a."""
+        binds = (L.Binding * max(1, len(plan.bindings)))()
+        keep = []
+        for i, b in enumerate(plan.bindings):
+            name, intent = b[0], b[1]
+            cached = b[2] if len(b) > 2 else False
+            keep.append(name.encode())
+            binds[i].field = keep[-1]
+            binds[i].intent = INTENTS[intent] if isinstance(intent, str) else int(intent)
+            binds[i].cached = 1 if cached else 0
+        params, npar = _cstrs(plan.parameters)
+        cp = L.Plan()
+        cp.kernel = plan.kernel.encode()
+        for a in range(3):
+            cp.tile[a] = int(plan.tile[a])
+        for a in range(6):
+            cp.halo[a] = int(plan.halo[a])
+        cp.bindings = binds
+        cp.n_bindings = len(plan.bindings)
+        cp.params = params
+        cp.n_params = npar
+        sf, nsf = _cstrs(signature[0])
+        sp, nsp = _cstrs(signature[1] if len(signature) > 1 else ())
+        L.check(self._lib.sf_sim_register_kernel(self._h, C.byref(cp), sf, nsf, sp, nsp, body.encode()))
+
+    def set_face_bc(self, axis: int, side: int, kind: str, velocity=(0.0, 0.0, 0.0)):
+        """executor::boundary() at (axis, side) (exchange.hpp:18-42)."""
+        v = (C.c_double * 3)(*map(float, velocity))
+        L.check(self._lib.sf_sim_set_face_bc(self._h, int(axis), int(side), BC_KINDS[kind], v))
+
+    def set_boundary_uniform(self, kind: str, velocity=(0.0, 0.0, 0.0)):
+        """boundary_spec::uniform (exchange.hpp:37-41)."""
+        for a in range(3):
+            for sd in range(2):
+                self.set_face_bc(a, sd, kind, velocity)
+
+    def physical_bc(self, names: Sequence[str]):
+        arr, n = _cstrs(names)
+        L.check(self._lib.sf_sim_physical_bc(self._h, arr, n))
+
+    def run_schedule(self, steps: Sequence[ScheduleStep], params: dict | None = None, passes: int = 1,
+                     mode: str = "plain", results: dict | None = None):
+        """executor::run_schedule (executor.hpp:533-553) with its dry run."""
+        cs = (L.ScheduleStep * max(1, len(steps)))()
+        keep = []
+        for i, st in enumerate(steps):
+            fl, nf = _cstrs(st.fields)
+            keep.append(fl)
+            cs[i].kind = STEP_KINDS[st.kind]
+            cs[i].kernel = st.kernel.encode()
+            cs[i].region = REGIONS[st.region]
+            cs[i].fields = fl
+            cs[i].n_fields = nf
+            cs[i].source = st.source.encode()
+            cs[i].op = REDUCE_OPS[st.op]
+            cs[i].target = st.target.encode()
+        params = params or {}
+        pn, npn = _cstrs(params.keys())
+        pv = (C.c_double * max(1, npn))(*[float(v) for v in params.values()])
+        L.check(self._lib.sf_sim_run_schedule(self._h, cs, len(steps), pn, pv, npn, int(passes),
+                                              1 if mode == "overlap" else 0))
+        if results is not None:
+            for st in steps:
+                if st.kind == "reduce":
+                    results[st.target] = self.result(st.target)
+
+    def result(self, name: str) -> float:
+        v = C.c_double()
+        L.check(self._lib.sf_sim_result(self._h, name.encode(), C.byref(v)))
         return v.value
 
     def invalidate_ghosts(self, name: str):
