@@ -51,6 +51,11 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--workload", default="cavity", choices=["cavity", "stencil"],
+                    help="cavity = configs[1] (headline); stencil = configs[4], a descriptor-declared "
+                         "high-order Laplacian (radius 2 or 3) JIT-compiled from its point function")
+    ap.add_argument("--radius", type=int, default=2)
+    ap.add_argument("--tile", default="32,8,16", help="descriptor TILE for --workload stencil")
     return ap.parse_args()
 
 
@@ -399,8 +404,100 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+LAP_BODIES = {
+    2: """
+  const auto& f = c.field(0);
+  const double c0 = -2.5, c1 = 4.0 / 3.0, c2 = -1.0 / 12.0;
+  double sx = c1 * (f(-1, 0, 0) + f(1, 0, 0)) + c2 * (f(-2, 0, 0) + f(2, 0, 0));
+  double sy = c1 * (f(0, -1, 0) + f(0, 1, 0)) + c2 * (f(0, -2, 0) + f(0, 2, 0));
+  double sz = c1 * (f(0, 0, -1) + f(0, 0, 1)) + c2 * (f(0, 0, -2) + f(0, 0, 2));
+  c.field(1).store((3.0 * c0) * f.load() + ((sx + sy) + sz));
+""",
+    3: """
+  const auto& f = c.field(0);
+  const double c0 = -49.0 / 18.0, c1 = 1.5, c2 = -0.15, c3 = 1.0 / 90.0;
+  double s[3];
+  for (int a = 0; a < 3; ++a) {
+    const int x = a == 0, y = a == 1, z = a == 2;
+    s[a] = c1 * (f(-x, -y, -z) + f(x, y, z)) + c2 * (f(-2 * x, -2 * y, -2 * z) + f(2 * x, 2 * y, 2 * z))
+         + c3 * (f(-3 * x, -3 * y, -3 * z) + f(3 * x, 3 * y, 3 * z));
+  }
+  c.field(1).store((3.0 * c0) * f.load() + ((s[0] + s[1]) + s[2]));
+""",
+}
+
+
+def run_stencil(args):
+    """configs[4]: a ghost-width-2/3 stencil declared as an execution plan +
+    point-function body (the reference's user-kernel path, executor.hpp:484),
+    JIT-compiled for sm_100a.  One step = exchange(u) + run_kernel over the grid.
+    Algorithmic bytes: read u, write lu = 16 B/cell (fp64)."""
+    import numpy as np
+    import torch
+
+    import paper_1201_2118_b200 as sfb
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    n = args.n if args.n != 512 else 768
+    r = args.radius
+    tile = tuple(int(x) for x in args.tile.split(","))
+    cfg = sfb.SolverConfig(extents=(n, n, n), periodic=(True, True, True))
+    sim = sfb.Simulation(cfg, sfb.FluidParams(), workers=1, ghost=r, device=local)
+    sim.create_field("u")
+    sim.create_field("lu")
+    sim.scatter("u", np.random.default_rng(1).uniform(-1, 1, size=(n, n, n)))
+    name = f"LAP{2 * r}"
+    sim.register_kernel(sfb.ExecutionPlan(name, tile, (r,) * 6, [("u", "IN", True), ("lu", "OUT")]),
+                        (["u", "lu"], []), LAP_BODIES[r])
+    stream = torch.cuda.ExternalStream(sim.stream, device=local)
+    for _ in range(args.warmup):
+        sim.exchange(["u"])
+        sim.run_kernel(name)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    sim.launch_count(reset=True)
+    e0.record(stream)
+    kms = 0.0
+    for _ in range(args.steps):
+        sim.exchange(["u"])
+        k0.record(stream)
+        sim.run_kernel(name)
+        k1.record(stream)
+        k1.synchronize()
+        kms += k0.elapsed_time(k1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    cells = n ** 3
+    peak, src = measured_peaks()
+    ach = 16.0 * cells / (kms / args.steps / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(cells * args.steps / (ms / 1e3) / 1e6, 2), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (uniform random field)",
+        "config": {"workload": f"configs[4]: radius-{r} Laplacian ({6 * r + 1}-point, order {2 * r}) at {n}^3 fp64, "
+                               f"ghost width {r}, descriptor TILE {tile}, periodic, exchange + run_kernel per step",
+                   "grid": [n, n, n], "ghost": r, "tile": list(tile)},
+        "roofline": {"bound": "hbm", "kernel": f"sf_user_kernel ({name}, NVRTC)", "achieved": round(ach, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
+                     "algorithmic_bytes_per_launch": 16 * cells, "avg_launch_ms": round(kms / args.steps, 4),
+                     "peak_source": src},
+        "gpu_launches": sim.launch_count(), "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse_args()
+    if args.workload == "stencil":
+        run_stencil(args)
+        return
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

@@ -292,6 +292,13 @@ class simulation {
     cudaKernel_t k = nullptr;
     int tx = 32, ty = 8, zc = 16;
     bool debug = false;
+    // TMA-staged template (CACHED readable bindings)
+    bool tma = false;
+    std::vector<int> cslot;  // binding index of each cached binding
+    int xl = 0, bw = 0, bh = 0, ring = 0;
+    size_t smem = 0;
+    void* maps = nullptr;
+    long long maps_gen = -1;
   };
   // world > 1: one process per GPU; this rank owns grid component `rank` of
   // grid::decompose(dom, world, ghost, periodic) and talks to the others over
@@ -671,7 +678,8 @@ class simulation {
   // ---- descriptor-declared kernels (executor.hpp:484-498, 650-692) ---------
   void register_kernel(const std::string& name, const std::array<int, 3>& tile,
                        const std::array<int, 6>& halo, const std::vector<std::string>& bfields,
-                       const std::vector<int>& intents, const std::vector<std::string>& params,
+                       const std::vector<int>& intents, const std::vector<int>& cached,
+                       const std::vector<std::string>& params,
                        const std::vector<std::string>& sig_fields,
                        const std::vector<std::string>& sig_params, const std::string& body) {
     const std::string head = "kernel '" + name + "': ";
@@ -723,6 +731,29 @@ class simulation {
     uk.tx = std::min(tile[0], 1024);
     uk.ty = std::max(1, std::min(tile[1], 1024 / uk.tx));
     uk.zc = tile[2];
+    // CACHED readable bindings -> TMA plane ring (needs an even TX for the
+    // 16-byte aligned box start, boxes <= 256 per dimension, fitting smem)
+    std::vector<int> cs;
+    for (size_t i = 0; i < bfields.size(); ++i)
+      if (i < cached.size() && cached[i] && uk.intent[i] != 1) cs.push_back((int)i);
+    if (!cs.empty() && uk.tx % 2 == 0 && !getenv("SF_JIT_NO_TMA")) {
+      const int xl = (halo[0] + 1) / 2 * 2;
+      const int bw = (xl + uk.tx + halo[1] + 1) / 2 * 2;
+      const int bh = halo[2] + uk.ty + halo[3];
+      const int ring = halo[4] + halo[5] + 1 + 2;
+      const size_t smem = (size_t)cs.size() * ring * ((bw * bh + 15) / 16 * 16) * 8;
+      bool fits = true;  // a box larger than the padded array is pointless (and rejected)
+      for (const auto& L : lay_) fits = fits && bw <= L.sx && bh <= L.sy;
+      if (bw <= 256 && bh <= 256 && smem <= 200 * 1024 && fits) {
+        uk.tma = true;
+        uk.cslot = cs;
+        uk.xl = xl;
+        uk.bw = bw;
+        uk.bh = bh;
+        uk.ring = ring;
+        uk.smem = smem;
+      }
+    }
     compile_user(uk, body);
     ukernels_.emplace(name, uk);
   }
@@ -756,7 +787,24 @@ class simulation {
     for (int a = 0; a < 6; ++a) src += (a ? "," : "") + std::to_string(uk.halo[a]);
     src += "};\n#define SF_DEBUG " + std::string(debug_bounds() ? "1" : "0") + "\n";
     uk.debug = debug_bounds();
-    std::string tmpl = jit_template();
+    if (uk.tma) {
+      std::string csl;
+      for (size_t i = 0; i < uk.cslot.size(); ++i) csl += (i ? "," : "") + std::to_string(uk.cslot[i]);
+      std::string cached_flags, cidx;
+      for (size_t b = 0; b < uk.fid.size(); ++b) {
+        int ci = -1;
+        for (size_t q = 0; q < uk.cslot.size(); ++q)
+          if (uk.cslot[q] == (int)b) ci = (int)q;
+        cached_flags += (b ? "," : "") + std::string(ci >= 0 ? "1" : "0");
+        cidx += (b ? "," : "") + std::to_string(ci >= 0 ? ci : 0);
+      }
+      src += "__device__ constexpr int SF_CACHED[] = {" + cached_flags + "};\n";
+      src += "__device__ constexpr int SF_CIDX[] = {" + cidx + "};\n";
+      src += "#define SF_NC " + std::to_string(uk.cslot.size()) + "\n__device__ constexpr int SF_CSLOT[] = {" + csl +
+             "};\n#define SF_XL " + std::to_string(uk.xl) + "\n#define SF_BW " + std::to_string(uk.bw) +
+             "\n#define SF_BH " + std::to_string(uk.bh) + "\n#define SF_R " + std::to_string(uk.ring) + "\n";
+    }
+    std::string tmpl = uk.tma ? jit_template_tma() : jit_template();
     const size_t at = tmpl.find("SF_BODY");
     tmpl.replace(at, 7, "#line 1 \"" + uk.name + "\"\n" + body + "\n");
     src += tmpl;
@@ -783,6 +831,8 @@ class simulation {
     rt->destroy(&prog);
     SF_CK(cudaLibraryLoadData(&uk.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     SF_CK(cudaLibraryGetKernel(&uk.k, uk.lib, "sf_user_kernel"));
+    if (uk.tma)
+      SF_CK(cudaFuncSetAttribute((const void*)uk.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)uk.smem));
     if (uk.debug) {  // point the module's error word at a device buffer
       if (!dbg_word_) {
         dbg_word_ = (int*)dalloc(8 * sizeof(int));
@@ -956,8 +1006,17 @@ class simulation {
       const void* geo = geo_;
       const sf_work* items = ws.d;
       int nitems = ws.n, zc = uk.zc;
-      void* args[] = {(void*)&ptrs, (void*)&geo, (void*)&items, (void*)&nitems, (void*)&zc, (void*)&prm};
-      SF_CK(cudaLaunchKernel((const void*)uk.k, dim3(ws.nctas), dim3(uk.tx, uk.ty), args, 0, st_));
+      if (uk.tma) {
+        if (uk.maps_gen != alloc_gen_) build_user_maps(uk);
+        const unsigned char* bidx = &dtab_->bidx[0][0][0];
+        const void* maps = uk.maps;
+        void* args[] = {(void*)&ptrs, (void*)&geo, (void*)&items, (void*)&nitems, (void*)&zc,
+                        (void*)&prm,  (void*)&bidx, (void*)&maps};
+        SF_CK(cudaLaunchKernel((const void*)uk.k, dim3(ws.nctas), dim3(uk.tx, uk.ty), args, uk.smem, st_));
+      } else {
+        void* args[] = {(void*)&ptrs, (void*)&geo, (void*)&items, (void*)&nitems, (void*)&zc, (void*)&prm};
+        SF_CK(cudaLaunchKernel((const void*)uk.k, dim3(ws.nctas), dim3(uk.tx, uk.ty), args, 0, st_));
+      }
       ++launches_;
       if (uk.debug) {
         int w[5] = {0, 0, 0, 0, 0};
@@ -989,6 +1048,31 @@ class simulation {
         ghosts_ok_[fname_[uk.fid[b]]] = false;
       }
     }
+  }
+
+  // tensor maps [block][cached binding][physical buffer] for the TMA template
+  void build_user_maps(user_kernel& uk) {
+    download_table();
+    const size_t n = (size_t)nloc_ * uk.cslot.size() * kSlots;
+    std::vector<unsigned char> hm(n * 128, 0);
+    for (int b = 0; b < nloc_; ++b)
+      for (size_t c = 0; c < uk.cslot.size(); ++c) {
+        const int f = uk.fid[uk.cslot[c]];
+        for (int sl = 0; sl < kSlots; ++sl) {
+          // the buffer whose physical index is sl (slots permute on swaps)
+          double* p = nullptr;
+          for (int q = 0; q < kSlots; ++q)
+            if (htab_->ptr[b][f][q] && htab_->bidx[b][f][q] == sl) p = htab_->ptr[b][f][q];
+          if (!p) continue;
+          const sf_layout& L = lay_[b];
+          if (encode_box_map(hm.data() + 128 * ((b * uk.cslot.size() + c) * kSlots + sl), p, L.sx, L.sy, L.sz,
+                             uk.bw, uk.bh))
+            throw error(SF_ERR_CUDA, "cuTensorMapEncodeTiled failed for kernel '" + uk.name + "'");
+        }
+      }
+    if (!uk.maps) uk.maps = dalloc(std::max<size_t>(hm.size(), 128) + 64 * n);
+    SF_CK(cudaMemcpy(uk.maps, hm.data(), hm.size(), cudaMemcpyHostToDevice));
+    uk.maps_gen = alloc_gen_;
   }
 
   static bool debug_bounds() {  // executor.hpp:645-648
@@ -1234,6 +1318,7 @@ class simulation {
   sf_fluid_params par_;
   sf_sim_options opt_;
   std::map<std::string, user_kernel> ukernels_;
+  long long alloc_gen_ = 0;  // bumps on every buffer allocation (TMA maps go stale)
   int* dbg_word_ = nullptr;  // debug policing: {code, slot, di, dj, dk}
   void* geo_ = nullptr;  // per local block: n[3], lo[3], sx, sy, base (sf_jit.hpp sf_geo)
   std::vector<std::string> fname_ = {"vx", "vy", "vz", "p", "divu"};
@@ -1461,6 +1546,7 @@ class simulation {
     SF_CK(cudaMemsetAsync(p, 0, bytes, st_));
     htab_->ptr[b][f][s] = p;
     htab_->bidx[b][f][s] = (unsigned char)s;
+    ++alloc_gen_;
   }
 
   table_view tview() const { return table_view{dtab_, nullptr, 0}; }
@@ -2126,15 +2212,16 @@ int sf_sim_register_kernel(sf_sim* s, const sf_plan* plan, const char* const* si
     std::array<int, 6> halo{};
     for (int a = 0; a < 6; ++a) halo[a] = plan->halo[a];
     std::vector<std::string> bf, pr, sf, sp;
-    std::vector<int> in;
+    std::vector<int> in, ca;
     for (int i = 0; i < plan->n_bindings; ++i) {
       bf.push_back(plan->bindings[i].field);
       in.push_back(plan->bindings[i].intent);
+      ca.push_back(plan->bindings[i].cached);
     }
     for (int i = 0; i < plan->n_params; ++i) pr.push_back(plan->params[i]);
     for (int i = 0; i < n_sig_fields; ++i) sf.push_back(sig_fields[i]);
     for (int i = 0; i < n_sig_params; ++i) sp.push_back(sig_params[i]);
-    SIM(s).register_kernel(plan->kernel, tile, halo, bf, in, pr, sf, sp, point_body);
+    SIM(s).register_kernel(plan->kernel, tile, halo, bf, in, ca, pr, sf, sp, point_body);
   });
 }
 

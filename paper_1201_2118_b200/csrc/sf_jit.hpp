@@ -164,4 +164,167 @@ sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
 )JIT";
 }
 
+// The TMA-staged variant for plans with CACHED readable bindings (the CaCUDA
+// template: "shared arrays with appropriate stencil sizes ... streamed in while
+// calculations proceed").  Each cached binding gets a ring
+// of SF_R z planes in shared memory, one (SF_BW x SF_BH) halo box per plane,
+// filled by cp.async.bulk.tensor and guarded by one mbarrier per ring slot;
+// the CTA marches its z chunk and refills the slot of the plane that left the
+// stencil window.  Uncached bindings read global memory directly.
+inline const char* jit_template_tma() {
+  return R"JIT(
+struct sf_work { int blk; int cta_begin; int tiles[3]; long long lo[3], hi[3]; };
+struct sf_params { double v[SF_NP > 0 ? SF_NP : 1]; };
+struct sf_geo { long long n[3], lo[3], sx, sy, base; };
+struct __align__(64) sf_tmap { unsigned long long opaque[16]; };
+
+__device__ int* sf_err_word;
+__device__ __forceinline__ void sf_violation(int code, int slot, int di, int dj, int dk) {
+  if (atomicCAS(sf_err_word, 0, code) == 0) {
+    sf_err_word[1] = slot; sf_err_word[2] = di; sf_err_word[3] = dj; sf_err_word[4] = dk;
+  }
+}
+__device__ __forceinline__ unsigned sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+constexpr int SF_PLANE = (SF_BW * SF_BH + 15) / 16 * 16;  // 128-byte aligned ring planes
+
+constexpr int SF_ZW = SF_HALO[4] + SF_HALO[5] + 1;  // z window of the stencil
+
+struct cell_view {
+  const double* rd;
+  double* wr;
+  long long o, sx, sxy;
+  int slot;
+  const double* rb;  // cached: ring base + this cell's in-plane offset
+  int zoff[SF_ZW];   // cached: ring-plane offset for dk = t - halo_lo_z (updated per plane)
+  __device__ __forceinline__ double operator()(int di, int dj, int dk) const {
+#if SF_DEBUG
+    if (!SF_READABLE[slot]) { sf_violation(1, slot, di, dj, dk); return 0.0; }
+    if (SF_CENTER_ONLY[slot] && (di != 0 || dj != 0 || dk != 0)) { sf_violation(2, slot, di, dj, dk); return 0.0; }
+    if (di < -SF_HALO[0] || di > SF_HALO[1] || dj < -SF_HALO[2] || dj > SF_HALO[3] || dk < -SF_HALO[4] ||
+        dk > SF_HALO[5]) { sf_violation(3, slot, di, dj, dk); return 0.0; }
+#endif
+    if (SF_CACHED[slot]) return rb[zoff[dk + SF_HALO[4]] + dj * SF_BW + di];
+    return rd[o + di + dj * sx + dk * sxy];
+  }
+  __device__ __forceinline__ double load() const { return (*this)(0, 0, 0); }
+  __device__ __forceinline__ void store(double v) const {
+#if SF_DEBUG
+    if (!SF_WRITABLE[slot]) { sf_violation(4, slot, 0, 0, 0); return; }
+#endif
+    wr[o] = v;
+  }
+};
+
+struct point_ctx {
+  cell_view f_[SF_NB];
+  const double* p_;
+  long long i, j, k;
+  __device__ __forceinline__ const cell_view& field(int s) const { return f_[s]; }
+  __device__ __forceinline__ double param(int s) const { return p_[s]; }
+};
+
+__device__ __forceinline__ void sf_user_point(const point_ctx& c) {
+SF_BODY
+}
+
+extern "C" __global__ void __launch_bounds__(SF_TX * SF_TY)
+sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
+               const sf_work* __restrict__ items, int nitems, int zc, sf_params prm,
+               const unsigned char* __restrict__ bidx, const sf_tmap* __restrict__ maps) {
+  extern __shared__ __align__(128) double sring[];
+  __shared__ __align__(8) unsigned long long bars[SF_R];
+  const int cta = blockIdx.x;
+  int lo_i = 0, hi_i = nitems - 1;
+  while (lo_i < hi_i) {
+    const int mid = (lo_i + hi_i + 1) >> 1;
+    if (items[mid].cta_begin <= cta) lo_i = mid; else hi_i = mid - 1;
+  }
+  const sf_work& w = items[lo_i];
+  const int local = cta - w.cta_begin;
+  const int tix = local % w.tiles[0];
+  const int tiy = (local / w.tiles[0]) % w.tiles[1];
+  const int tiz = local / (w.tiles[0] * w.tiles[1]);
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * SF_TX + tx;
+  const long long i0 = w.lo[0] + (long long)tix * SF_TX, j0 = w.lo[1] + (long long)tiy * SF_TY;
+  const long long i = i0 + tx, j = j0 + ty;
+  const long long k0 = w.lo[2] + (long long)tiz * zc;
+  const long long k1 = k0 + zc < w.hi[2] ? k0 + zc : w.hi[2];
+  const int nplanes = (int)(k1 - k0);
+  const int nload = nplanes + SF_HALO[4] + SF_HALO[5];  // planes k0-hzl .. k1-1+hzh
+  const sf_geo& G = geo[w.blk];
+  const long long sx = G.sx, sxy = G.sx * G.sy;
+  const int g = (int)(G.base / sxy);  // ghost width: base = (g*sy + g)*sx + xo
+  const int xo = (int)(G.base % G.sx);
+  const int xcs = xo + (int)i0 - SF_XL, ycs = g + (int)j0 - SF_HALO[2], zcs = g + (int)k0 - SF_HALO[4];
+
+  if (tid == 0) {
+    for (int q = 0; q < SF_R; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bars[q])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int q) {  // load plane q (z = k0 - hzl + q) of every cached binding
+    const int slot = q % SF_R;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bars[slot])),
+                 "r"((unsigned)(SF_NC * SF_BW * SF_BH * 8)) : "memory");
+    for (int c = 0; c < SF_NC; ++c) {
+      const int b = SF_CSLOT[c];
+      const int phys = bidx[(w.blk * SF_MAXF + SF_FID[b]) * SF_SLOTS + 0];
+      const sf_tmap* m = &maps[((w.blk * SF_NC) + c) * SF_SLOTS + phys];
+      double* dst = sring + (c * SF_R + slot) * SF_PLANE;
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(sa(dst)), "l"((unsigned long long)m),
+          "r"(sa(&bars[slot])), "r"(xcs), "r"(ycs), "r"(zcs + q) : "memory");
+    }
+  };
+  auto wait = [&](int q) {
+    const unsigned par = (unsigned)((q / SF_R) & 1);
+    asm volatile("{\n .reg .pred P1;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                 " @!P1 bra W_%=;\n}" ::"r"(sa(&bars[q % SF_R])), "r"(par) : "memory");
+  };
+  if (tid == 0)
+    for (int q = 0; q < SF_R && q < nload; ++q) issue(q);
+
+  const bool act = i < w.hi[0] && j < w.hi[1];
+  point_ctx c;
+  c.p_ = prm.v;
+#pragma unroll
+  for (int s = 0; s < SF_NB; ++s) {
+    c.f_[s].rd = ptrs[(w.blk * SF_MAXF + SF_FID[s]) * SF_SLOTS + 0];
+    c.f_[s].wr = ptrs[(w.blk * SF_MAXF + SF_FID[s]) * SF_SLOTS + SF_WSLOT[s]];
+    c.f_[s].sx = sx;
+    c.f_[s].sxy = sxy;
+    c.f_[s].slot = s;
+    c.f_[s].rb = sring + SF_CIDX[s] * SF_R * SF_PLANE + (ty + SF_HALO[2]) * SF_BW + tx + SF_XL;
+  }
+  c.i = G.lo[0] + i;
+  c.j = G.lo[1] + j;
+  for (int q = 0; q < SF_HALO[4] + SF_HALO[5] && q < nload; ++q) wait(q);
+  for (int kk = 0; kk < nplanes; ++kk) {
+    const int qn = kk + SF_HALO[4] + SF_HALO[5];  // newest plane of this window
+    if (qn < nload) wait(qn);
+    const long long k = k0 + kk;
+    if (act) {
+      const long long o = G.base + (k * G.sy + j) * sx + i;
+      int zo[SF_ZW];
+#pragma unroll
+      for (int t = 0; t < SF_ZW; ++t) zo[t] = ((kk + t) % SF_R) * SF_PLANE;
+#pragma unroll
+      for (int s = 0; s < SF_NB; ++s) {
+        c.f_[s].o = o;
+#pragma unroll
+        for (int t = 0; t < SF_ZW; ++t) c.f_[s].zoff[t] = zo[t];
+      }
+      c.k = G.lo[2] + k;
+      sf_user_point(c);
+    }
+    __syncthreads();  // plane kk (ring q = kk) left every window
+    if (tid == 0 && kk + SF_R < nload) issue(kk + SF_R);
+  }
+}
+)JIT";
+}
+
 }  // namespace sfb

@@ -47,6 +47,7 @@ void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_cons
                           cudaStream_t st);
 int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field);
 size_t sweep_maps_bytes();
+int encode_box_map(void* map_out, double* base, long long sx, long long sy, long long sz, int bw, int bh);
 void sweep_tile_shape(int* tx, int* ty);  // tile of the selected TMA pipeline variant
 size_t sweep_map_offset(int b, int f, int s);
 template <class View>
