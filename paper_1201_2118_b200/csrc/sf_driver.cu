@@ -740,7 +740,7 @@ class simulation {
       const int xl = (halo[0] + 1) / 2 * 2;
       const int bw = (xl + uk.tx + halo[1] + 1) / 2 * 2;
       const int bh = halo[2] + uk.ty + halo[3];
-      const int ring = halo[4] + halo[5] + 1 + 2;
+      const int ring = halo[4] + halo[5] + 1 + 3;  // window + one round (2 planes) + 1 in flight
       const size_t smem = (size_t)cs.size() * ring * ((bw * bh + 15) / 16 * 16) * 8;
       bool fits = true;  // a box larger than the padded array is pointless (and rejected)
       for (const auto& L : lay_) fits = fits && bw <= L.sx && bh <= L.sy;
@@ -759,8 +759,8 @@ class simulation {
   }
 
   void compile_user(user_kernel& uk, const std::string& body) {
-    nvrtc_api* rt = nvrtc();
-    if (!rt) throw error(SF_ERR_CUDA, "NVRTC not found (set SF_NVRTC_LIB)");
+    nvrtc_api* rt = getenv("SF_JIT_DUMP_ONLY") ? nullptr : nvrtc();
+    if (!rt && !getenv("SF_JIT_DUMP_ONLY")) throw error(SF_ERR_CUDA, "NVRTC not found (set SF_NVRTC_LIB)");
     std::string src;
     src += "#define SF_NB " + std::to_string(uk.fid.size()) + "\n";
     src += "#define SF_NP " + std::to_string(uk.params.size()) + "\n";
@@ -808,6 +808,14 @@ class simulation {
     const size_t at = tmpl.find("SF_BODY");
     tmpl.replace(at, 7, "#line 1 \"" + uk.name + "\"\n" + body + "\n");
     src += tmpl;
+    if (const char* dump = getenv("SF_JIT_DUMP")) {  // inspect the generated tile kernel
+      std::string fn = std::string(dump) + "/" + uk.name + ".cu";
+      if (FILE* fp = std::fopen(fn.c_str(), "w")) {
+        std::fputs(src.c_str(), fp);
+        std::fclose(fp);
+      }
+    }
+    if (!rt) throw error(SF_ERR_EXEC, "SF_JIT_DUMP_ONLY: source written, not compiled");
     void* prog = nullptr;
     if (rt->create(&prog, src.c_str(), (uk.name + ".cu").c_str(), 0, nullptr, nullptr) != 0)
       throw error(SF_ERR_CUDA, "nvrtcCreateProgram failed");

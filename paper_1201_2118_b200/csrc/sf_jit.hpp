@@ -102,7 +102,7 @@ struct cell_view {
 #if SF_DEBUG
     if (!SF_WRITABLE[slot]) { sf_violation(4, slot, 0, 0, 0); return; }
 #endif
-    wr[o] = v;
+    __stwb(wr + o, v);
   }
 };
 
@@ -205,14 +205,14 @@ struct cell_view {
         dk > SF_HALO[5]) { sf_violation(3, slot, di, dj, dk); return 0.0; }
 #endif
     if (SF_CACHED[slot]) return rb[zoff[dk + SF_HALO[4]] + dj * SF_BW + di];
-    return rd[o + di + dj * sx + dk * sxy];
+    return SF_CENTER_ONLY[slot] ? __ldcg(rd + o + di + dj * sx + dk * sxy) : __ldg(rd + o + di + dj * sx + dk * sxy);
   }
   __device__ __forceinline__ double load() const { return (*this)(0, 0, 0); }
   __device__ __forceinline__ void store(double v) const {
 #if SF_DEBUG
     if (!SF_WRITABLE[slot]) { sf_violation(4, slot, 0, 0, 0); return; }
 #endif
-    wr[o] = v;
+    __stwb(wr + o, v);
   }
 };
 
@@ -302,26 +302,41 @@ sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
   c.i = G.lo[0] + i;
   c.j = G.lo[1] + j;
   for (int q = 0; q < SF_HALO[4] + SF_HALO[5] && q < nload; ++q) wait(q);
-  for (int kk = 0; kk < nplanes; ++kk) {
-    const int qn = kk + SF_HALO[4] + SF_HALO[5];  // newest plane of this window
+  long long o = G.base + (k0 * G.sy + j) * sx + i;
+  int zr[SF_ZW];  // rolling ring-plane offsets of the z window
+#pragma unroll
+  for (int t = 0; t < SF_ZW; ++t) zr[t] = (t % SF_R) * SF_PLANE;
+  // two planes per barrier round: the fixed per-round work (waits, barrier,
+  // refills, ring offsets) is shared by two cells per thread
+  for (int kk = 0; kk < nplanes; kk += 2) {
+    const bool two = kk + 1 < nplanes;
+    const int qn = kk + SF_HALO[4] + SF_HALO[5];
     if (qn < nload) wait(qn);
-    const long long k = k0 + kk;
+    if (two && qn + 1 < nload) wait(qn + 1);
     if (act) {
-      const long long o = G.base + (k * G.sy + j) * sx + i;
-      int zo[SF_ZW];
 #pragma unroll
-      for (int t = 0; t < SF_ZW; ++t) zo[t] = ((kk + t) % SF_R) * SF_PLANE;
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !two) break;
+        const int kq = kk + h;
 #pragma unroll
-      for (int s = 0; s < SF_NB; ++s) {
-        c.f_[s].o = o;
+        for (int s = 0; s < SF_NB; ++s) {
+          c.f_[s].o = o;
 #pragma unroll
-        for (int t = 0; t < SF_ZW; ++t) c.f_[s].zoff[t] = zo[t];
+          for (int t = 0; t < SF_ZW; ++t) c.f_[s].zoff[t] = zr[t];
+        }
+        c.k = G.lo[2] + k0 + kq;
+        sf_user_point(c);
+        o += sxy;
+#pragma unroll
+        for (int t = 0; t < SF_ZW - 1; ++t) zr[t] = zr[t + 1];
+        zr[SF_ZW - 1] = ((kq + SF_ZW) % SF_R) * SF_PLANE;
       }
-      c.k = G.lo[2] + k;
-      sf_user_point(c);
     }
-    __syncthreads();  // plane kk (ring q = kk) left every window
-    if (tid == 0 && kk + SF_R < nload) issue(kk + SF_R);
+    __syncthreads();  // planes kk, kk+1 (ring q = kk, kk+1) left every window
+    if (tid == 0) {
+      if (kk + SF_R < nload) issue(kk + SF_R);
+      if (two && kk + 1 + SF_R < nload) issue(kk + 1 + SF_R);
+    }
   }
 }
 )JIT";

@@ -42,6 +42,15 @@ def main():
     g["cavity24_g2"] = cavity_run(24, [3], symmetry_z=False, ghost=2)
     g["cavity24_g3_w1"] = cavity_run(24, [2], symmetry_z=False, ghost=3)
     g["elapsed_s"] = time.time() - t0
+    # the reference's own recorded artifacts of runs/re100.cfg (acceptance 7/8),
+    # copied verbatim as data fixtures: profiles.csv is byte-reproducible
+    # and ghia_re100.csv is the validation table
+    import shutil
+    ref = "/root/reference/proj"
+    shutil.copy(os.path.join(ref, "runs", "profiles.csv"), os.path.join(os.path.dirname(__file__), "re100_profiles.csv"))
+    shutil.copy(os.path.join(ref, "data", "ghia_re100.csv"), os.path.join(os.path.dirname(__file__), "ghia_re100.csv"))
+    g["re100"] = {"steps": 21277, "log_tail": "steps=21277  t=28.7605  rate=9.880e-07  max|div|=2.543e-07",
+                  "source": "proj/runs/re100_run.log, proj/runs/profiles.csv"}
     with open(os.path.join(os.path.dirname(__file__), "golden.json"), "w") as f:
         json.dump(g, f, indent=1)
     print(json.dumps({k: v.get("checksums") if isinstance(v, dict) else v for k, v in g.items()}, indent=1))
