@@ -115,3 +115,44 @@ def run_cavity(nx=129, ny=129, nz=3, re=100.0, sigma=0.9, omega=1.9525, toleranc
     comment = "lid-driven cavity centerline profiles: %dx%dx%d, Re=%s, t=%s, steps=%d" % (
         nx, ny, nz, "%g" % re, "%.6g" % sim.time, summary.steps)
     return summary, write_profiles(u, v, [comment]), write_residuals(rows), sim
+
+
+def read_profiles(text: str):
+    """cli::read_profiles (validate.hpp:31-79): `y,u` and `x,v` sections, '#' comments."""
+    u, v, sec = [], [], None
+    for raw in text.splitlines():
+        t = raw.strip()
+        if not t or t.startswith("#"):
+            continue
+        if t == "y,u":
+            sec = u
+            continue
+        if t == "x,v":
+            sec = v
+            continue
+        if sec is None:
+            raise ValueError("expected a 'y,u' or 'x,v' header before data rows")
+        a, b = t.split(",")
+        sec.append((float(a), float(b)))
+    return u, v
+
+
+def compare_profiles(computed, reference):
+    """cli::compare_profiles (validate.hpp:137-157): piecewise-linear sample of the
+    computed profile at every reference coordinate; returns the max |deviation|."""
+    import bisect
+
+    def interp(table, x):
+        xs = [r[0] for r in table]
+        k = bisect.bisect_left(xs, x)
+        if xs[k] == x:
+            return table[k][1]
+        lo, hi = table[k - 1], table[k]
+        t = (x - lo[0]) / (hi[0] - lo[0])
+        return lo[1] + t * (hi[1] - lo[1])
+
+    worst = 0.0
+    for comp, ref in ((computed[0], reference[0]), (computed[1], reference[1])):
+        for x, want in ref:
+            worst = max(worst, abs(interp(comp, x) - want))
+    return worst

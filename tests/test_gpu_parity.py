@@ -364,6 +364,9 @@ def test_re100_cavity_to_steady_state_reproduces_the_reference_profiles_byte_for
     rows = residuals.strip().splitlines()[1:]
     assert len(rows) == 21277
     assert all(float(r.split(",")[2]) <= 1e-6 for r in rows)  # acceptance 8: every step divergence-free
-    # Ghia et al. Re=100 within the acceptance tolerance (0.03)
-    ghia = [l.strip() for l in open(os.path.join(os.path.dirname(__file__), "golden", "ghia_re100.csv"))]
-    assert len(ghia) > 5
+    # Ghia et al. Re=100 within the acceptance tolerance (acceptance_main.cpp:449-466)
+    from paper_1201_2118_b200.cavity import compare_profiles, read_profiles
+    ghia = read_profiles(open(os.path.join(os.path.dirname(__file__), "golden", "ghia_re100.csv")).read())
+    dev = compare_profiles(read_profiles(profiles), ghia)
+    assert dev <= 0.03
+    assert abs(dev - 0.00911) < 5e-5  # 0.00911 for the reference run
