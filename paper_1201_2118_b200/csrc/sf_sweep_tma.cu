@@ -49,6 +49,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// with an L2 cache-policy operand (createpolicy), for read-once streams
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
+                                                 int y, int z, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
                                             int y, int z) {
   asm volatile(
@@ -95,7 +109,8 @@ template <int STAGES, int MINB, bool WS, int TX, int TY>
 __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
     k_sweep_div_tma(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems,
                     int zc, sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag,
-                    unsigned int total_ctas, const sweep_maps* __restrict__ maps, int finalize) {
+                    unsigned int total_ctas, const sweep_maps* __restrict__ maps, int finalize,
+                    int hints) {
   constexpr int kStages = STAGES;
   using TL = tile<TX, TY>;
   if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
@@ -153,13 +168,21 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
   const CUtensorMap* mW = &maps->m[b][SF_VZ][tab->bidx[b][SF_VZ][FRONT]];
   const CUtensorMap* mP = &maps->m[b][SF_P][tab->bidx[b][SF_P][FRONT]];
   const int xc = (int)(xo + i0), yc = (int)(g + j0), zc0 = (int)(g + k0);
+  const uint64_t pol = (hints & 2) ? policy_evict_first() : 0ull;
   auto issue = [&](int stage, int plane) {
     mbar_expect_tx(&bars[stage], TL::TXB);
     tma_load_3d(sptr(stage, TL::OFF_D), mD, &bars[stage], xc - kXL, yc - 1, zc0 + plane);
-    tma_load_3d(sptr(stage, TL::OFF_U), mU, &bars[stage], xc - kXL, yc, zc0 + plane);
-    tma_load_3d(sptr(stage, TL::OFF_V), mV, &bars[stage], xc, yc - 1, zc0 + plane);
-    tma_load_3d(sptr(stage, TL::OFF_P), mP, &bars[stage], xc, yc, zc0 + plane);
-    tma_load_3d(sptr(stage, TL::OFF_W), mW, &bars[stage], xc, yc, zc0 + plane);
+    if (hints & 2) {  // p and vz are read by this CTA only: evict first
+      tma_load_3d(sptr(stage, TL::OFF_U), mU, &bars[stage], xc - kXL, yc, zc0 + plane);
+      tma_load_3d(sptr(stage, TL::OFF_V), mV, &bars[stage], xc, yc - 1, zc0 + plane);
+      tma_load_3d_hint(sptr(stage, TL::OFF_P), mP, &bars[stage], xc, yc, zc0 + plane, pol);
+      tma_load_3d_hint(sptr(stage, TL::OFF_W), mW, &bars[stage], xc, yc, zc0 + plane, pol);
+    } else {
+      tma_load_3d(sptr(stage, TL::OFF_U), mU, &bars[stage], xc - kXL, yc, zc0 + plane);
+      tma_load_3d(sptr(stage, TL::OFF_V), mV, &bars[stage], xc, yc - 1, zc0 + plane);
+      tma_load_3d(sptr(stage, TL::OFF_P), mP, &bars[stage], xc, yc, zc0 + plane);
+      tma_load_3d(sptr(stage, TL::OFF_W), mW, &bars[stage], xc, yc, zc0 + plane);
+    }
   };
   if (!WS && tid == 0) {
     const int npro = nplanes < kStages ? nplanes : kStages;
@@ -267,7 +290,7 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
       const double ex = mbI * dXp * a1;
       const double ey = mbI * dYp * a1;
       const double ez = mbI * dZp * a1;
-      P[o] = p0 + d0;
+      const double pn = p0 + d0;
       const double un = u0 + cu * (d0 - ex);
       const double vn = v0 + cv * (d0 - ey);
       const double wn = w0 + cw * (d0 - ez);
@@ -277,10 +300,19 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
       double dd = (un - umn) * s.ix;
       dd += (vn - vmn) * s.iy;
       dd += (wn - wm_new) * s.iz;
-      Un[o] = un;
-      Vn[o] = vn;
-      Wn[o] = wn;
-      Dn[o] = dd;
+      if (hints & 1) {  // streaming stores (evict-first): nothing here is re-read this sweep
+        __stcs(P + o, pn);
+        __stcs(Un + o, un);
+        __stcs(Vn + o, vn);
+        __stcs(Wn + o, wn);
+        __stcs(Dn + o, dd);
+      } else {
+        P[o] = pn;
+        Un[o] = un;
+        Vn[o] = vn;
+        Wn[o] = wn;
+        Dn[o] = dd;
+      }
       const unsigned long long bb = abs_bits(dd);
       rmax = bb > rmax ? bb : rmax;
       wm_new = wn;
@@ -435,6 +467,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 static int sweep_variant();
+static int sweep_hints();
 // tile shape of the selected pipeline variant
 void sweep_tile_shape(int* tx, int* ty) {
   switch (sweep_variant()) {
@@ -467,7 +500,9 @@ int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, lo
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, gdim,
                   gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  getenv("SF_L2_PROMO") ? (CUtensorMapL2promotion)atoi(getenv("SF_L2_PROMO"))
+                                        : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : 2;
 }
 
@@ -503,7 +538,17 @@ static void launch_variant(const table_view& vw, int nctas, int zc, const sf_con
   }
   k_sweep_div_tma<STAGES, MINB, WS, TX, TY><<<nctas, dim3(TX, TY + (WS ? 1 : 0)), smem, st>>>(
       vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas,
-      static_cast<const sweep_maps*>(maps), fin);
+      static_cast<const sweep_maps*>(maps), fin, sweep_hints());
+}
+
+// SF_SWEEP_HINTS: bit 0 streaming stores, bit 1 evict-first TMA loads of p / vz
+static int sweep_hints() {
+  static int h = -1;
+  if (h < 0) {
+    const char* e = getenv("SF_SWEEP_HINTS");
+    h = e ? atoi(e) : 0;
+  }
+  return h;
 }
 
 // SF_SWEEP_VARIANT selects the pipeline shape for A/B runs (default 0).
