@@ -46,8 +46,10 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=512, help="cells per axis per GPU")
     ap.add_argument("--sweeps", type=int, default=200, help="pressure half-sweeps per step")
-    ap.add_argument("--variant", default="tma", choices=["tma", "ldg", "unfused"],
-                    help="fused half-sweep with TMA pipeline (default), fused with plain loads, or unfused")
+    ap.add_argument("--variant", default="tma", choices=["tma", "tma1", "ldg", "unfused"],
+                    help="tma: TMA pipeline with the temporal pass (two half-sweeps per launch) where it "
+                         "applies (default); tma1: one TMA half-sweep per launch; ldg: fused with plain "
+                         "loads; unfused: the reference's dataflow")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
@@ -69,9 +71,9 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """DRAM bytes per launch of the fused half-sweep from the committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_sweep_div.json")
+def ncu_traffic(kernel="sweep_div"):
+    """DRAM bytes per launch of the dominant kernel from its committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", f"ncu_{kernel}.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -220,7 +222,7 @@ def run_ours(args):
     dev = local
     torch.cuda.set_device(dev)
     n, S = args.n, args.sweeps
-    fused = {"tma": 1, "ldg": 2, "unfused": 0}[args.variant]
+    fused = {"tma": 1, "tma1": 3, "ldg": 2, "unfused": 0}[args.variant]
     dist = None
     if world > 1:  # one rank per GPU over NCCL, weak scaling: n^3 per rank
         import torch.distributed as dist
@@ -273,7 +275,10 @@ def run_ours(args):
     clk = clocks.stop()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     launches = sim.launch_count()
-    k_ms, k_n = sim.kernel_timing("sweep_div")
+    # the dominant kernel: the temporal pass where it ran, else the half-sweep;
+    # both move 80 algorithmic bytes per cell per launch (read S0, write S2)
+    kname = "sweep2" if sim.kernel_timing("sweep2")[1] > 0 else "sweep_div"
+    k_ms, k_n = sim.kernel_timing(kname)
     k_ms = max_over_ranks(k_ms)
     sim.set_kernel_timing(False)
     ms_per_step = ms_total / args.steps
@@ -284,10 +289,12 @@ def run_ours(args):
     peak, peak_src = measured_peaks()
     avg_launch_s = (k_ms / k_n) / 1e3 if k_n else None
     achieved = (BYTES_PER_HALF_SWEEP * cells / avg_launch_s / 1e9) if avg_launch_s else None
-    traffic, _ = ncu_traffic()
-    step_bytes = (BYTES_UV + BYTES_DIV + BYTES_PER_HALF_SWEEP * S) * cells
+    traffic, _ = ncu_traffic(kname)
+    step_bytes = (BYTES_UV + BYTES_DIV + BYTES_PER_HALF_SWEEP * S // (2 if kname == "sweep2" else 1)) * cells
     roofline = {
-        "bound": "hbm", "kernel": "k_sweep_div (fused half-sweep)",
+        "bound": "hbm",
+        "kernel": ("k_sweep2 (temporal pass: two fused half-sweeps per launch)" if kname == "sweep2"
+                   else "k_sweep_div (fused half-sweep)"),
         "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4) if achieved else None,
         "traffic": traffic,
@@ -354,7 +361,9 @@ def run_ours(args):
                                 f"3D lid-driven cavity, {n}^3 per GPU weak scaling, global {list(cfg.extents)} block-decomposed over {world} B200 with NCCL ghost exchange (BASELINE.json configs[2]), {S} half-sweeps per step"),
                    "grid": list(cfg.extents), "ghost": 1, "sweeps_per_step": S,
                    "parallelism": "1 GPU" if world == 1 else f"{world} ranks, block decomposition (grid::decompose), NCCL halo + allreduce",
-                   "path": {"tma": "fused half-sweep, TMA pipeline", "ldg": "fused half-sweep, plain loads",
+                   "path": {"tma": "TMA pipeline, temporal pass (two half-sweeps per launch)" if kname == "sweep2"
+                            else "fused half-sweep, TMA pipeline",
+                            "tma1": "fused half-sweep, TMA pipeline", "ldg": "fused half-sweep, plain loads",
                             "unfused": "unfused (reference dataflow)"}[args.variant],
                    "l2": "inputs larger than L2: 9 resident fp64 arrays of %.2f GB" % (cells * 8 / 1e9)},
         "half_sweep_rate": round(total_cells * sweeps_done / (ms_total / 1e3) / 1e6, 1),

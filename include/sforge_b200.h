@@ -103,8 +103,11 @@ typedef struct sf_sim_options {
   int ghost;
   int form;    /* 0 rows, 1 points (cfd.hpp:169): one device form serves both */
   int device;
-  int fused;   /* 1 = fused half-sweep, TMA-pipelined (default); 2 = fused, plain
-                  loads (A/B baseline); 0 = the reference's unfused dataflow */
+  int fused;   /* 1 = fused half-sweep, TMA-pipelined (default), with the
+                  temporal pass (two half-sweeps per launch) where it applies:
+                  one grid component per device, wall / symmetry faces;
+                  3 = TMA half-sweep only; 2 = fused, plain loads (A/B
+                  baseline); 0 = the reference's unfused dataflow */
 } sf_sim_options;
 
 /* cfd::step_stats (cfd.hpp:86-90) */
@@ -253,9 +256,10 @@ int sf_sim_synchronize(sf_sim* s);
 void* sf_sim_stream(sf_sim* s);            /* the cudaStream_t all work is ordered on */
 /* Kernel launches issued by this simulation since creation (or the last reset). */
 int64_t sf_sim_launch_count(sf_sim* s, int reset);
-/* Per-kernel CUDA-event timing of the fused half-sweep: when enabled, the
- * driver records events around every half-sweep launch; read back the summed
- * milliseconds and launch count. */
+/* Per-kernel CUDA-event timing of the pressure loop: when enabled, the driver
+ * records events around every executed launch of the fused half-sweep
+ * (kernel "sweep_div") or of the temporal pass (kernel "sweep2", two
+ * half-sweeps per launch); read back the summed milliseconds and launches. */
 int sf_sim_set_kernel_timing(sf_sim* s, int enable);
 int sf_sim_kernel_timing(sf_sim* s, const char* kernel, double* total_ms, int64_t* launches);
 

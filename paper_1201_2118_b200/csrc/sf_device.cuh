@@ -62,7 +62,7 @@ struct sf_dev_ctl {
   int max_sweeps;
   int color;         // red-black colour carried across sweeps and steps (cfd.hpp:299)
   int abort_field;   // -1, or first non-finite velocity after UPDATE_VELOCITY
-  int pad0;
+  int redo;          // temporal pass stopped after its first sweep: redo it single
   double dt, beta, tolerance, residual;
   double vmax[3];
 };

@@ -1193,9 +1193,11 @@ class simulation {
     const int maxs = std::max(1, cfg_.max_sweeps);
     int issued = 0;
     int batch = std::max(1, std::min(maxs, est_sweeps_));
+    const bool two = temporal();
     auto enqueue = [&](int n, cudaEvent_t ev) {
-      for (int q = 0; q < n; ++q) enqueue_half_sweep();
-      issued += n;
+      int c = 0;
+      while (c < n) c += enqueue_sweep_unit();
+      issued += c;
       SF_CK(cudaEventRecord(ev, st_));
     };
     iter_launch_ = 0;
@@ -1219,12 +1221,14 @@ class simulation {
     const double residual = hflag_->residual;
     if (sweeps > 0) est_sweeps_ = sweeps;
     if (timing_ && opt_.fused) {
-      // executed half-sweeps are the first `sweeps` launches; the rest were predicated off
-      for (int q = 0; q < sweeps && q < iter_launch_; ++q) {
+      // the first units ran (a temporal pass covers two half-sweeps, the last
+      // one possibly only its first); the rest were predicated off
+      const int ran = two ? (sweeps + 1) / 2 : sweeps;
+      for (int q = 0; q < ran && q < iter_launch_; ++q) {
         float ms = 0.f;
         SF_CK(cudaEventElapsedTime(&ms, timer(q, 0), timer(q, 1)));
-        sweep_ms_ += ms;
-        ++sweep_launches_;
+        (two ? pass_ms_ : sweep_ms_) += ms;
+        ++(two ? pass_launches_ : sweep_launches_);
       }
     }
     if (opt_.fused) refresh({SF_VX, SF_VY, SF_VZ});
@@ -1302,12 +1306,13 @@ class simulation {
   }
   void set_timing(bool on) {
     timing_ = on;
-    sweep_ms_ = 0.0;
-    sweep_launches_ = 0;
+    sweep_ms_ = pass_ms_ = 0.0;
+    sweep_launches_ = pass_launches_ = 0;
   }
-  void timing(double* ms, i64* n) const {
-    *ms = sweep_ms_;
-    *n = sweep_launches_;
+  // which = 0: single half-sweep kernel; 1: temporal pass (two half-sweeps)
+  void timing(int which, double* ms, i64* n) const {
+    *ms = which ? pass_ms_ : sweep_ms_;
+    *n = which ? pass_launches_ : sweep_launches_;
   }
 
  private:
@@ -1351,6 +1356,8 @@ class simulation {
   sf_host_flag* dflag_ = nullptr;
   double* staging_ = nullptr;
   void* maps_ = nullptr;  // TMA descriptors (null: no driver entry point -> LDG kernel)
+  void* maps2_ = nullptr;  // temporal-pass descriptors (null: pass unavailable)
+  const bool temporal_env_ = getenv("SF_NO_TEMPORAL") == nullptr;
   std::vector<void*> dev_allocs_;
   std::map<std::string, work_set> items_;
   std::map<std::string, task_set> tasks_;
@@ -1363,8 +1370,8 @@ class simulation {
   int est_sweeps_ = 8;
   i64 launches_ = 0;
   bool timing_ = false;
-  double sweep_ms_ = 0.0;
-  i64 sweep_launches_ = 0;
+  double sweep_ms_ = 0.0, pass_ms_ = 0.0;
+  i64 sweep_launches_ = 0, pass_launches_ = 0;
   std::vector<cudaEvent_t> timers_;
   int iter_launch_ = 0;
   cudaEvent_t timer(int q, int which) {
@@ -1493,7 +1500,9 @@ class simulation {
       for (int f = 0; f < SF_NFIELDS; ++f) {
         const bool velocity = f <= SF_VZ;
         for (int s = 0; s < kSlots; ++s) {
-          const bool need = s == FRONT || (velocity && (s == BACK || s == ALT)) || (f == SF_DIVU && s == ALT);
+          // p gets an ALT buffer where the temporal pass can run (sf_sweep2.cu)
+          const bool need = s == FRONT || (velocity && (s == BACK || s == ALT)) ||
+                            (f == SF_DIVU && s == ALT) || (f == SF_P && s == ALT && nloc_ == 1 && !dist_);
           if (need) alloc_slot(b, f, s);
         }
       }
@@ -1513,6 +1522,25 @@ class simulation {
       if (ok) {
         maps_ = dalloc(hm.size());
         SF_CK(cudaMemcpy(maps_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
+      }
+    }
+    // descriptors of the temporal pass (halo'd boxes, block 0 only)
+    if (maps_ && nloc_ == 1 && !dist_) {
+      std::vector<unsigned char> hm(sweep2_maps_bytes(), 0);
+      bool ok = true;
+      for (int f : {SF_VX, SF_VY, SF_VZ, SF_P, SF_DIVU})
+        for (int s = 0; s < kSlots && ok; ++s) {
+          double* p = htab_->ptr[0][f][s];
+          if (!p) continue;
+          const sf_layout& L = lay_[0];
+          int bw, bh;
+          sweep2_box(f, &bw, &bh);
+          ok = bw <= L.sx && bh <= L.sy &&
+               encode_box_map(hm.data() + sweep2_map_offset(f, s), p, L.sx, L.sy, L.sz, bw, bh) == 0;
+        }
+      if (ok) {
+        maps2_ = dalloc(hm.size());
+        SF_CK(cudaMemcpy(maps2_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
       }
     }
     {
@@ -1765,16 +1793,49 @@ class simulation {
     SF_NC(nccl()->AllReduce(dev, dev, (size_t)n, kNcclUint64, kNcclMax, comm_, st_));
   }
 
+  // The temporal pass (two half-sweeps per launch, sf_sweep2.cu) applies to one
+  // grid component per device with wall / symmetry faces only, fused = 1.
+  bool temporal() const {
+    if (!maps2_ || !temporal_env_ || opt_.fused != 1 || nloc_ != 1 || dist_) return false;
+    for (int fi = 0; fi < 6; ++fi) {
+      const int k = htab_->blk[0].face[fi];
+      if (k != FACE_WALL && k != FACE_SYM) return false;
+    }
+    return true;
+  }
+  bool tma_sweep() const { return maps_ && (opt_.fused == 1 || opt_.fused == 3); }
+
+  // Enqueues one unit of the pressure loop; returns the half-sweeps it covers.
+  int enqueue_sweep_unit() {
+    if (!temporal()) {
+      enqueue_half_sweep();
+      return 1;
+    }
+    const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, kTX, kTY);
+    if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
+    launch_sweep2(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, maps2_, st_);
+    if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
+    ++iter_launch_;
+    // predicated redo of the first sweep when the pass stopped after it
+    int ftx, fty;
+    sweep_tile_shape(&ftx, &fty);
+    const work_set& wr = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, ftx, fty);
+    launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, dflag_, maps_, 2, st_);
+    launches_ += 2;
+    check_launch();
+    return 2;
+  }
+
   void enqueue_half_sweep() {
     if (opt_.fused) {
       int ftx = kTX, fty = kTY;
-      if (maps_ && opt_.fused == 1) sweep_tile_shape(&ftx, &fty);
+      if (tma_sweep()) sweep_tile_shape(&ftx, &fty);
       const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, ftx, fty);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
       // single process: the kernel's last CTA finalises the sweep; across
       // ranks the residual first needs the max over ranks
       const int fin = dist_ ? 0 : 1;
-      if (maps_ && opt_.fused == 1)
+      if (tma_sweep())
         launch_sweep_div_tma(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, maps_, fin, st_);
       else
         launch_sweep_div(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, fin, st_);
@@ -2291,11 +2352,12 @@ int sf_sim_set_kernel_timing(sf_sim* s, int enable) {
 }
 int sf_sim_kernel_timing(sf_sim* s, const char* kernel, double* total_ms, int64_t* launches) {
   return guarded([&] {
-    if (std::string(kernel ? kernel : "") != "sweep_div")
-      throw sfb::error(SF_ERR_ARG, "timed kernels: sweep_div");
+    const std::string k = kernel ? kernel : "";
+    if (k != "sweep_div" && k != "sweep2")
+      throw sfb::error(SF_ERR_ARG, "timed kernels: sweep_div, sweep2");
     double ms = 0.0;
     long long n = 0;
-    SIM(s).timing(&ms, &n);
+    SIM(s).timing(k == "sweep2" ? 1 : 0, &ms, &n);
     *total_ms = ms;
     *launches = n;
   });

@@ -771,7 +771,9 @@ __global__ void k_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, i
       ctl->sweeps = 0;
       ctl->residual = 0.0;
       ctl->acc[0] = 0ull;
+      ctl->acc[1] = 0ull;
       ctl->ctas_done = 0u;
+      ctl->redo = 0;
       ctl->done = ctl->abort_field >= 0 ? 1 : 0;
       ctl->max_sweeps = s.max_sweeps;
       ctl->tolerance = s.tolerance;

@@ -38,13 +38,21 @@ template <class View>
 void launch_pressure_sweep(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                            int predicated, const double* beta_color_dt, cudaStream_t st);
 // fin = 1: the last CTA finalises the sweep; 0: the caller allreduces acc[0]
-// across ranks and runs CTL_FINISH_FUSED
+// across ranks and runs CTL_FINISH_FUSED; 2 (TMA kernel only): the predicated
+// redo of a temporal pass's first sweep (see launch_sweep2)
 void launch_sweep_div(const table_view& vw, int nctas, int zc, const sf_consts& c,
                       sf_dev_ctl* ctl, sf_host_flag* hflag, int fin, cudaStream_t st);
 // TMA-pipelined fused half-sweep (sf_sweep_tma.cu); maps = device sweep_maps.
 void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_consts& c,
                           sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,
                           cudaStream_t st);
+// Temporal pass: two half-sweeps per launch (sf_sweep2.cu); single block with
+// wall / symmetry faces only.  maps = device table of sweep2 descriptors.
+void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                   sf_host_flag* hflag, const void* maps, cudaStream_t st);
+size_t sweep2_maps_bytes();
+size_t sweep2_map_offset(int f, int s);
+void sweep2_box(int field, int* bw, int* bh);
 int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field);
 size_t sweep_maps_bytes();
 int encode_box_map(void* map_out, double* base, long long sx, long long sy, long long sz, int bw, int bh);

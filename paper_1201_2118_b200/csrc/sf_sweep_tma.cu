@@ -113,7 +113,13 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
                     int hints) {
   constexpr int kStages = STAGES;
   using TL = tile<TX, TY>;
-  if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
+  // finalize 2: redo of a temporal pass's first sweep (sf_sweep2.cu), runs
+  // only when that pass flagged it
+  if (finalize == 2) {
+    if (!*reinterpret_cast<const volatile int*>(&ctl->redo)) return;
+  } else if (*reinterpret_cast<const volatile int*>(&ctl->done)) {
+    return;
+  }
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto sptr = [&](int st, int off) { return reinterpret_cast<double*>(smem_raw + st * TL::BYTES + off); };
   __shared__ __align__(8) uint64_t bars[kStages];
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
   const sf_dev_block& B = tab->blk[b];
 
   const double beta = ctl->beta, dt = ctl->dt;
-  const int color = ctl->color;
+  const int color = finalize == 2 ? (ctl->color ^ 1) : ctl->color;
   if (tid == 0) {
 #pragma unroll
     for (int q = 0; q < kStages; ++q) {
@@ -413,6 +419,23 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
     }
   }
 
+  if (finalize == 2) {  // counters and residual were set by the temporal pass
+    if (last_cta(&ctl->ctas_done, total_ctas) && tid == 0) {
+      __threadfence();
+      ctl->ctas_done = 0u;
+      ctl->redo = 0;
+      for (int f = 0; f < 5; ++f) {
+        if (f == SF_P) continue;
+        double* tmp = tab->ptr[b][f][FRONT];
+        tab->ptr[b][f][FRONT] = tab->ptr[b][f][ALT];
+        tab->ptr[b][f][ALT] = tmp;
+        const unsigned char ti = tab->bidx[b][f][FRONT];
+        tab->bidx[b][f][FRONT] = tab->bidx[b][f][ALT];
+        tab->bidx[b][f][ALT] = ti;
+      }
+    }
+    return;
+  }
   unsigned long long rm[1] = {rmax};
   block_max_atomic<1>(rm, &ctl->acc[0]);
   if (!finalize) return;  // across ranks: allreduce, then CTL_FINISH_FUSED

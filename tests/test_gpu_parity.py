@@ -40,7 +40,7 @@ def dev_from_case(c: Case, fused=True):
     return sfb.Simulation(cfg, par, workers=c.workers, ghost=c.ghost, fused=fused)
 
 
-@pytest.mark.parametrize("fused", [1, 2, 0])
+@pytest.mark.parametrize("fused", [1, 3, 2, 0])
 def test_cavity64_first_step_matches_golden(fused):
     s = dev_cavity(64, symmetry_z=False, fused=fused)
     s.init_cavity()
@@ -49,7 +49,7 @@ def test_cavity64_first_step_matches_golden(fused):
     assert s.checksum() == "1b07d1f577d4bad0"
 
 
-@pytest.mark.parametrize("fused", [1, 2, 0])
+@pytest.mark.parametrize("fused", [1, 3, 2, 0])
 def test_cavity64_ten_steps_match_golden_per_step(fused):
     s = dev_cavity(64, symmetry_z=False, fused=fused)
     s.init_cavity()
@@ -70,7 +70,7 @@ def test_cavity64_hundred_steps_match_the_391_second_oracle_run():
     assert s.time == 0.20345052083333356
 
 
-@pytest.mark.parametrize("fused", [1, 2])
+@pytest.mark.parametrize("fused", [1, 3, 2])
 def test_bench128_config_matches_golden(fused):
     s = dev_cavity(128, symmetry_z=False, omega=1.9525, tolerance=1e-30, max_sweeps=200, fused=fused)
     s.init_cavity()
@@ -94,7 +94,7 @@ def test_quasi2d_and_ghost_widths_match_golden():
 
 
 @pytest.mark.parametrize("workers", [2, 4, 8])
-@pytest.mark.parametrize("fused", [1, 2, 0])
+@pytest.mark.parametrize("fused", [1, 3, 2, 0])
 def test_grid_components_on_one_device_give_identical_steps(ref_available, workers, fused):
     o = Oracle(cavity_case((16, 16, 8)), "ref")
     o.init_cavity()
@@ -119,7 +119,7 @@ def _random_case_pair(case, seed, fused=True):
 
 
 @pytest.mark.parametrize("workers", [1, 2, 4])
-@pytest.mark.parametrize("fused", [1, 2, 0])
+@pytest.mark.parametrize("fused", [1, 3, 2, 0])
 def test_projection_matches_reference_bitwise(ref_available, workers, fused):
     # tests/test_cfd.cpp:231-273
     c = Case(extents=(16, 16, 16), periodic=(True, True, True), tolerance=1e-8, max_sweeps=20000,
@@ -135,7 +135,7 @@ def test_projection_matches_reference_bitwise(ref_available, workers, fused):
 
 @pytest.mark.parametrize("periodic", [False, True])
 @pytest.mark.parametrize("workers", [1, 2, 3])
-@pytest.mark.parametrize("fused", [1, 2, 0])
+@pytest.mark.parametrize("fused", [1, 3, 2, 0])
 def test_odd_extents_capped_sweeps_match_reference(ref_available, periodic, workers, fused):
     # tests/test_cfd.cpp:275-325: 17x13x5, two steps, 40 capped sweeps
     c = Case(extents=(17, 13, 5), periodic=(periodic,) * 3, tolerance=1e-12, max_sweeps=40,
@@ -370,3 +370,47 @@ def test_re100_cavity_to_steady_state_reproduces_the_reference_profiles_byte_for
     dev = compare_profiles(read_profiles(profiles), ghia)
     assert dev <= 0.03
     assert abs(dev - 0.00911) < 5e-5  # 0.00911 for the reference run
+
+
+def _temporal_pair(ext, steps, **kw):
+    """The same cavity run with the temporal pass (fused=1) and with one
+    half-sweep per launch (fused=3); returns both sims and per-step stats."""
+    out = []
+    for fused in (1, 3):
+        s = dev_cavity(ext, fused=fused, **kw)
+        s.init_cavity()
+        s.set_kernel_timing(True)
+        st = [s.step() for _ in range(steps)]
+        out.append((s, [[x.dt, x.sweeps, x.residual] for x in st]))
+    return out
+
+
+@pytest.mark.parametrize("max_sweeps", [1, 2, 7, 40])
+def test_temporal_pass_matches_single_sweeps_at_every_stop_parity(max_sweeps):
+    # fixed work: the pass stops after its first sweep whenever max_sweeps is odd
+    (s1, st1), (s3, st3) = _temporal_pair((40, 24, 20), 3, tolerance=1e-30, max_sweeps=max_sweeps,
+                                          symmetry_z=False)
+    assert st1 == st3 and all(r[1] == max_sweeps for r in st1)
+    assert s1.kernel_timing("sweep2")[1] == 3 * ((max_sweeps + 1) // 2)
+    assert s3.kernel_timing("sweep2")[1] == 0 and s3.kernel_timing("sweep_div")[1] == 3 * max_sweeps
+    for f in FIELDS5:
+        assert same(s1.gather(f), s3.gather(f)), f
+    assert s1.checksum() == s3.checksum()
+    assert s1.pending_color == s3.pending_color
+
+
+def test_temporal_pass_tolerance_stops_match_the_oracle(ref_available):
+    # tolerance-driven stops at both parities, tiles cut by the domain edge in x and y
+    c = cavity_case((45, 19, 23), symmetry_z=True, tolerance=1e-3, max_sweeps=500)  # sweeps 441 140 198 175 167 160
+    o = Oracle(c, "ref")
+    o.init_cavity()
+    so = o.advance(6)
+    d = dev_from_case(c, fused=1)
+    d.init_cavity()
+    d.set_kernel_timing(True)
+    dd = [d.step() for _ in range(6)]
+    want = [[float(a), int(b), float(r)] for a, b, r in zip(*so)]
+    assert [[x.dt, x.sweeps, x.residual] for x in dd] == want
+    assert len({w[1] % 2 for w in want}) == 2, "want stops after both sweeps of a pass"
+    assert d.kernel_timing("sweep2")[1] > 0
+    assert d.checksum() == o.checksum()
