@@ -55,6 +55,12 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void prefetch3(const CUtensorMap* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
 __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
@@ -76,10 +82,9 @@ constexpr int IN_W = IN_V + r128(8 * IW * IFH);
 constexpr int IN_P = IN_W + r128(8 * IW * IFH);
 constexpr int IN_BYTES = IN_P + r128(8 * IW * IFH);
 constexpr uint32_t IN_TX = 8u * (IW * IDH + 4 * IW * IFH);
-constexpr int S1_PLANE = 5 * EN;  // doubles per S1 plane (u1 v1 w1 p1 d1)
 enum { U1 = 0, V1 = 1, W1 = 2, P1 = 3, D1 = 4 };
 
-constexpr int smem_bytes(int nin) { return nin * IN_BYTES + 2 * S1_PLANE * 8; }
+constexpr int smem_bytes(int nin) { return nin * IN_BYTES + (3 * 4 + 2) * EN * 8; }
 
 struct maps2_t {  // [field][physical buffer]
   CUtensorMap m[SF_NFIELDS][kSlots];
@@ -94,13 +99,13 @@ void sweep2_box(int field, int* bw, int* bh) {
   *bh = field == SF_DIVU ? IDH : IFH;
 }
 
-// S0 plane q (z = k0 - 2 + q) lives in input stage q % NIN; S1 plane m
-// (z = k0 - 2 + m) in ring slot m & 1.
+// S0 plane q (z = k0 - 2 + q) lives in input stage q % NIN; S1 plane m is
+// z = k0 - 2 + m.
 template <int NIN, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
     k_sweep2(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc,
              sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag, unsigned int total_ctas,
-             const maps2_t* __restrict__ maps) {
+             const maps2_t* __restrict__ maps, int pf) {
   static_assert(NIN >= 4, "the prologue keeps four S0 planes in flight");
   if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
   extern __shared__ __align__(128) unsigned char sm[];
@@ -162,115 +167,165 @@ __global__ void __launch_bounds__(NT, MINB)
     tma3(st + IN_V, mV, bar, xs, ys, zs + q);
     tma3(st + IN_W, mW, bar, xs, ys, zs + q);
     tma3(st + IN_P, mP, bar, xs, ys, zs + q);
+    // L2 prefetch pf planes further: more bytes in flight than the stages hold
+    if (pf > 0 && q + pf < nin) {
+      const int zp = zs + q + pf;
+      prefetch3(mD, xs, ys, zp);
+      prefetch3(mU, xs, ys, zp);
+      prefetch3(mV, xs, ys, zp);
+      prefetch3(mW, xs, ys, zp);
+      prefetch3(mP, xs, ys, zp);
+    }
   };
+  const uint32_t bar0 = smem32(&bars[0]);
   auto wait_in = [&](int q) {
-    if (q < nin) bar_wait(&bars[q % NIN], (uint32_t)((q / NIN) & 1));
+    if (q < nin) {
+      const uint32_t a = bar0 + 8u * (uint32_t)(q % NIN), par = (uint32_t)((q / NIN) & 1);
+      asm volatile(
+          "{\n .reg .pred P1;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+          " @!P1 bra W_%=;\n}\n" ::"r"(a),
+          "r"(par)
+          : "memory");
+    }
   };
   if (tid == 0)
     for (int q = 0; q < NIN; ++q) issue(q);
 
-  double* s1 = reinterpret_cast<double*>(sm + NIN * IN_BYTES);
-  auto S1 = [&](int m, int f) { return s1 + (m & 1) * S1_PLANE + f * EN; };
+  // S1 rings: fields (u1 v1 w1 p1) of plane m in slot m % 3, divu1 in m & 1.
+  // Three field slots let s1_fields(m+1) overwrite plane m-2 without waiting
+  // for the previous sweep B.
+  // All shared-memory accesses below index one array with 32-bit offsets.
+  double* const S = reinterpret_cast<double*>(sm);
+  constexpr int FRING = NIN * IN_BYTES / 8, DRING = FRING + 3 * 4 * EN;
 
-  // ---- per-thread widened cells (x/y parts of the scale bits, parity, pins) ----
-  int e_ia[NE], e_q[NE], e_rc[NE], e_rx[NE], e_ry[NE], e_par[NE], e_qd[NE];
-  bool e_in[NE], e_px[NE], e_py[NE];
+  // ---- per-thread widened cells ---------------------------------------------
+  // Thread t owns widened cells e = t + 1 and, for t < 128 (warps 0-3),
+  // e = t + 257. The corner e = 0 (x = i0-2, y = j0-2) is never read.
+  // e_ia: index into the S0 boxes; e_qd: DIVERGENCE source cell (wall
+  // mirror applied); bt: scale-table rows rc | rx << 3 | ry << 6 (x/y bits),
+  // parity << 9, owned << 10, x pin << 11, y pin << 12, div source << 13
+  const bool has2 = tid < EN - 1 - NT;
+  int e_e[NE], e_ia[NE], e_qd[NE], e_bt[NE];
 #pragma unroll
   for (int r = 0; r < NE; ++r) {
-    const int e = tid + r * NT;
-    e_q[r] = e < EN ? e : -1;
+    const int e = r == 0 || has2 ? tid + 1 + r * NT : EN - 1;
     const int ex = e % EW, ey = e / EW;
     const int x = i0 - 2 + ex, y = j0 - 2 + ey;
-    e_ia[r] = ey * IW + ex;  // the S0 boxes share the widened tile's origin
-    e_in[r] = e < EN && x >= 0 && x < n0 && y >= 0 && y < n1;
     const long long gi = B.lo[0] + x, gj = B.lo[1] + y;
     const int bx = bin(s.per[0], gi, nm0), bxp = bnx(s.per[0], gi, nm0);
     const int by = bin(s.per[1], gj, nm1), byp = bnx(s.per[1], gj, nm1);
-    e_rc[r] = (bx << 2) | (by << 1);
-    e_rx[r] = (bxp << 2) | (by << 1);
-    e_ry[r] = (bx << 2) | (byp << 1);
-    e_par[r] = (int)((gi + gj) & 1);
-    e_px[r] = x == n0 - 1;
-    e_py[r] = y == n1 - 1;
     // DIVERGENCE source cell: x >= i0-1, y >= j0-1; the +x / +y ghost (x = n0,
     // y = n1) takes the wall mirror of the last owned cell (exchange.hpp:438-449),
     // evaluated with that cell's operands
     int dx = ex, dy = ey;
     if (x >= n0) dx -= x - (n0 - 1);
     if (y >= n1) dy -= y - (n1 - 1);
-    e_qd[r] = (e < EN && ex >= 1 && ey >= 1) ? dy * EW + dx : -1;
+    e_e[r] = e;
+    e_ia[r] = ey * IW + ex;
+    e_qd[r] = dy * EW + dx;
+    e_bt[r] = ((bx << 2) | (by << 1)) | (((bxp << 2) | (by << 1)) << 3) | (((bx << 2) | (byp << 1)) << 6) |
+              ((int)((gi + gj) & 1) << 9) | ((x >= 0 && x < n0 && y >= 0 && y < n1) << 10) |
+              ((x == n0 - 1) << 11) | ((y == n1 - 1) << 12) | ((ex >= 1 && ey >= 1) << 13);
   }
+  // Interior tile: every widened cell has all x/y scale bits 1 (so each
+  // -(beta*bscale) is -(beta*1.0) = smb[7]), is owned and unpinned, and needs
+  // no divu mirror; planes with z in [zf_lo, zf_hi] add the same for z. The
+  // fast paths evaluate the identical IEEE operations in the identical order,
+  // so they are bitwise the general paths restricted to such cells.
+  const bool fast_xy = B.lo[0] + i0 - 2 >= 1 && B.lo[0] + i0 + TX <= nm0 - 2 && B.lo[1] + j0 - 2 >= 1 &&
+                       B.lo[1] + j0 + TY <= nm1 - 2 && i0 + TX <= n0 - 2 && j0 + TY <= n1 - 2 &&
+                       !s.per[0] && !s.per[1];
+  const int zf_lo = s.per[2] ? 1 << 30 : (int)max(1ll, 1ll - B.lo[2]);
+  const int zf_hi = (int)min((long long)n2 - 3, nm2 - 2 - B.lo[2]);
+  const double mbI = smb[7];
 
-  // S1 fields of plane m from S0 planes m and m+1: sweep A's cell update
-  // (cfd.hpp:699-719) with the wall pins. Cells outside the domain carry S0;
-  // their wall-normal values are the constant pins.
-  auto s1_fields = [&](int m) {
-    const int z = k0 - 2 + m;
-    const unsigned char* st = stage(m);
-    const double* Di = reinterpret_cast<const double*>(st + IN_D);
-    const double* Ui = reinterpret_cast<const double*>(st + IN_U);
-    const double* Vi = reinterpret_cast<const double*>(st + IN_V);
-    const double* Wi = reinterpret_cast<const double*>(st + IN_W);
-    const double* Pi = reinterpret_cast<const double*>(st + IN_P);
-    const double* Dz = reinterpret_cast<const double*>(stage(m + 1) + IN_D);
-    double* u1 = S1(m, U1);
-    double* v1 = S1(m, V1);
-    double* w1 = S1(m, W1);
-    double* p1 = S1(m, P1);
-    const bool zin = z >= 0 && z < n2;
+  // S1 fields of plane z from its S0 stage and divu0 of plane z+1: sweep A's
+  // cell update (cfd.hpp:699-719) with the wall pins. Cells outside the
+  // domain carry S0; their wall-normal values are the constant pins.
+  // st / stn: S0 stages of planes z and z+1 (offsets in doubles); fo: field slot
+  auto s1_fields = [&](int z, int st, int stn, int fo) {
+    const int Di = st + IN_D / 8, Ui = st + IN_U / 8, Vi = st + IN_V / 8, Wi = st + IN_W / 8,
+              Pi = st + IN_P / 8, Dz = stn + IN_D / 8;
+    const int u1 = fo + U1 * EN, v1 = fo + V1 * EN, w1 = fo + W1 * EN, p1 = fo + P1 * EN;
     const long long gk = B.lo[2] + z;
-    const int bz = bin(s.per[2], gk, nm2), bzp = bnx(s.per[2], gk, nm2);
     const int zpar = (int)(gk & 1);
+    if (fast_xy && z >= zf_lo && z <= zf_hi) {
+#pragma unroll
+      for (int r = 0; r < NE; ++r) {
+        if (r > 0 && !has2) break;
+        const int ia = e_ia[r], e = e_e[r];
+        // all loads first: the stores below may alias them as far as the compiler knows
+        const double dc = S[Di + ia], dx = S[Di + ia + 1], dy = S[Di + ia + IW], dz = S[Dz + ia];
+        const double uu = S[Ui + ia], vv = S[Vi + ia], ww = S[Wi + ia], pp = S[Pi + ia];
+        const double a0 = ((((e_bt[r] >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
+        const double d0 = mbI * dc * a0;
+        const double exv = mbI * dx * a1;
+        const double eyv = mbI * dy * a1;
+        const double ezv = mbI * dz * a1;
+        S[p1 + e] = pp + d0;
+        S[u1 + e] = uu + cu * (d0 - exv);
+        S[v1 + e] = vv + cv * (d0 - eyv);
+        S[w1 + e] = ww + cw * (d0 - ezv);
+      }
+      return;
+    }
+    const bool zin = z >= 0 && z < n2;
+    const int bz = bin(s.per[2], gk, nm2), bzp = bnx(s.per[2], gk, nm2);
     const bool pz = z == n2 - 1;
 #pragma unroll
     for (int r = 0; r < NE; ++r) {
-      const int e = e_q[r];
-      if (e < 0) continue;
-      const int ia = e_ia[r];
-      if (!(zin && e_in[r])) {
-        u1[e] = Ui[ia];
-        v1[e] = Vi[ia];
-        w1[e] = Wi[ia];
-        p1[e] = Pi[ia];
+      if (r > 0 && !has2) break;
+      const int e = e_e[r], ia = e_ia[r], bt = e_bt[r];
+      if (!(zin && ((bt >> 10) & 1))) {
+        S[u1 + e] = S[Ui + ia];
+        S[v1 + e] = S[Vi + ia];
+        S[w1 + e] = S[Wi + ia];
+        S[p1 + e] = S[Pi + ia];
         continue;
       }
-      const double a0 = ((e_par[r] ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
-      const double d0 = smb[e_rc[r] | bz] * Di[ia] * a0;
-      const double exv = smb[e_rx[r] | bz] * Di[ia + 1] * a1;
-      const double eyv = smb[e_ry[r] | bz] * Di[ia + IW] * a1;
-      const double ezv = smb[e_rc[r] | bzp] * Dz[ia] * a1;
-      p1[e] = Pi[ia] + d0;
-      u1[e] = e_px[r] ? pin_u : Ui[ia] + cu * (d0 - exv);
-      v1[e] = e_py[r] ? pin_v : Vi[ia] + cv * (d0 - eyv);
-      w1[e] = pz ? pin_w : Wi[ia] + cw * (d0 - ezv);
+      const int rc = bt & 7, rx = (bt >> 3) & 7, ry = (bt >> 6) & 7;
+      const double a0 = ((((bt >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
+      const double d0 = smb[rc | bz] * S[Di + ia] * a0;
+      const double exv = smb[rx | bz] * S[Di + ia + 1] * a1;
+      const double eyv = smb[ry | bz] * S[Di + ia + IW] * a1;
+      const double ezv = smb[rc | bzp] * S[Dz + ia] * a1;
+      S[p1 + e] = S[Pi + ia] + d0;
+      S[u1 + e] = ((bt >> 11) & 1) ? pin_u : S[Ui + ia] + cu * (d0 - exv);
+      S[v1 + e] = ((bt >> 12) & 1) ? pin_v : S[Vi + ia] + cv * (d0 - eyv);
+      S[w1 + e] = pz ? pin_w : S[Wi + ia] + cw * (d0 - ezv);
     }
   };
-  // DIVERGENCE of S1 on plane m (cfd.hpp:605-608); the top ghost plane
-  // mirrors plane n2-1 (plane m-1).
-  auto s1_div = [&](int m) {
-    const int z = k0 - 2 + m;
-    double* d1 = S1(m, D1);
+  // DIVERGENCE of S1 on plane z (cfd.hpp:605-608); the top ghost plane
+  // mirrors plane n2-1 (dm).
+  // fo / fom: field slots of planes z and z-1; d1 / dm: divu1 slots of z and z-1
+  auto s1_div = [&](int z, int fo, int fom, int d1, int dm) {
     if (z >= n2) {
-      const double* dm = S1(m - 1, D1);
 #pragma unroll
-      for (int r = 0; r < NE; ++r)
-        if (e_q[r] >= 0) d1[e_q[r]] = dm[e_q[r]];
+      for (int r = 0; r < NE; ++r) {
+        if (r > 0 && !has2) break;
+        S[d1 + e_e[r]] = S[dm + e_e[r]];
+      }
       return;
     }
-    const double* u1 = S1(m, U1);
-    const double* v1 = S1(m, V1);
-    const double* w1 = S1(m, W1);
-    const double* w1m = S1(m - 1, W1);
+    const int u1 = fo + U1 * EN, v1 = fo + V1 * EN, w1 = fo + W1 * EN, w1m = fom + W1 * EN;
 #pragma unroll
     for (int r = 0; r < NE; ++r) {
+      if (r > 0 && !has2) break;
+      // non-source cells (x = i0-2 or y = j0-2) compute on in-bounds operands
+      // and skip the store: no divergent branch
       const int q = e_qd[r];
-      if (q < 0) continue;
-      double dd = (u1[q] - u1[q - 1]) * s.ix;
-      dd += (v1[q] - v1[q - EW]) * s.iy;
-      dd += (w1[q] - w1m[q]) * s.iz;
-      d1[e_q[r]] = dd;
+      const double du = S[u1 + q] - S[u1 + q - 1];
+      const double dv = S[v1 + q] - S[v1 + q - EW];
+      const double dw = S[w1 + q] - S[w1m + q];
+      double dd = du * s.ix;
+      dd += dv * s.iy;
+      dd += dw * s.iz;
+      if ((e_bt[r] >> 13) & 1) S[d1 + e_e[r]] = dd;
     }
   };
+  auto F = [&](int slot) { return FRING + slot * 4 * EN; };  // field slot offset
+  auto Dr = [&](int slot) { return DRING + slot * EN; };     // divu1 slot offset
+  auto so = [&](int q) { return (q % NIN) * (IN_BYTES / 8); };  // S0 stage offset
 
   // ---- this thread's tile cell ----------------------------------------------
   const int i = i0 + tx, j = j0 + ty;
@@ -286,23 +341,22 @@ __global__ void __launch_bounds__(NT, MINB)
   const int par_col = (int)((gi + gj) & 1);
   const int q0 = (ty + 2) * EW + (tx + 2);
 
-  // prologue: S1 planes 0..2 (z = k0-2 .. k0), divu1 of planes 1 and 2
+  // prologue: S1 planes m = 0..2 (z = k0-2 .. k0), divu1 of planes 1 and 2
   wait_in(0);
   wait_in(1);
   wait_in(2);
-  s1_fields(0);
-  s1_fields(1);
+  s1_fields(k0 - 2, so(0), so(1), F(0));
+  s1_fields(k0 - 1, so(1), so(2), F(1));
   __syncthreads();
   if (tid == 0) issue(NIN);  // S0 plane 0 is consumed
-  s1_div(1);
-  __syncthreads();
-  // w1 and divu1 of the plane below the chunk, for sweep B's swept -z neighbour
-  const double w1_below = S1(1, W1)[q0], d1_below = S1(1, D1)[q0];
+  s1_div(k0 - 1, F(1), F(0), Dr(1), Dr(0));
   wait_in(3);
-  s1_fields(2);
+  s1_fields(k0, so(2), so(3), F(2));
   __syncthreads();
   if (tid == 0) issue(NIN + 1);  // S0 plane 1 is consumed
-  s1_div(2);
+  // w1 and divu1 of the plane below the chunk, for sweep B's swept -z neighbour
+  const double w1_below = S[F(1) + W1 * EN + q0], d1_below = S[Dr(1) + q0];
+  s1_div(k0, F(2), F(1), Dr(0), Dr(1));
   __syncthreads();
 
   double* __restrict__ Dn = tab->ptr[0][SF_DIVU][ALT];
@@ -318,7 +372,7 @@ __global__ void __launch_bounds__(NT, MINB)
       const int bzm = bin(s.per[2], gkm, nm2), bzpm = bnx(s.per[2], gkm, nm2);
       const double a0m = (((gi + gj + gkm) & 1) == colB) ? 1.0 : 0.0, a1m = 1.0 - a0m;
       const double d0m = smb[ic | bzm] * d1_below * a0m;
-      const double ezm = smb[ic | bzpm] * S1(2, D1)[q0] * a1m;
+      const double ezm = smb[ic | bzpm] * S[Dr(0) + q0] * a1m;
       wm2 = w1_below + cw * (d0m - ezm);
     } else {
       wm2 = w1_below;  // pinned ghost plane
@@ -326,25 +380,59 @@ __global__ void __launch_bounds__(NT, MINB)
   }
   long long o = B.base + ((long long)k0 * B.sy + j) * sx + i;
 
+  // ring slots of planes m-1, m, m+1 (fields, mod 3) and m (divu1, mod 2)
+  int fm = 2, fn = 0, fp = 1, dc = 0;
   for (int kk = 0; kk < nplanes; ++kk, o += sxy) {
     const int z = k0 + kk;
     const int m = kk + 2;
-    // S1 of plane z+1 (S0 planes m+1, m+2). Its ring slot held plane m-1,
-    // which no thread reads once the barrier below is passed.
+    // S1 of plane z+1 from S0 planes m+1, m+2 into field slot fn (held plane
+    // m-2, which the previous iteration's barriers retired)
     wait_in(m + 2);
-    __syncthreads();
-    s1_fields(m + 1);
+    s1_fields(z + 1, so(m + 1), so(m + 2), F(fn));
     __syncthreads();
     if (tid == 0) issue(m + NIN);  // S0 plane m is consumed
-    s1_div(m + 1);
+    // divu1 of plane z+1 into divu slot dc^1 (held plane m-1, read by the
+    // previous sweep B before the barrier above)
+    s1_div(z + 1, F(fn), F(fm), Dr(dc ^ 1), Dr(dc));
     __syncthreads();
-    if (act) {
-      const double* u1 = S1(m, U1);
-      const double* v1 = S1(m, V1);
-      const double* w1 = S1(m, W1);
-      const double* p1 = S1(m, P1);
-      const double* d1 = S1(m, D1);
-      const double dZp = S1(m + 1, D1)[q0];
+    const double* u1 = S + F(fm) + U1 * EN;
+    const double* v1 = S + F(fm) + V1 * EN;
+    const double* w1 = S + F(fm) + W1 * EN;
+    const double* p1 = S + F(fm) + P1 * EN;
+    const double* d1 = S + Dr(dc);
+    const double* d1p = S + Dr(dc ^ 1);
+    if (fast_xy && z >= zf_lo && z <= zf_hi) {
+      // interior plane (see fast_xy): bitwise the general path below
+      const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
+      const double dXm = d1[q0 - 1], dYm = d1[q0 - EW], dZp = d1p[q0];
+      const double p0 = p1[q0], u0 = u1[q0], uml = u1[q0 - 1], v0 = v1[q0], vml = v1[q0 - EW], w0 = w1[q0];
+      const int par = par_col ^ (int)((B.lo[2] + z) & 1);
+      const double a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
+      const double d0 = mbI * dC * a0;
+      const double exv = mbI * dXp * a1;
+      const double eyv = mbI * dYp * a1;
+      const double ezv = mbI * dZp * a1;
+      const double pn = p0 + d0;
+      const double un = u0 + cu * (d0 - exv);
+      const double vn = v0 + cv * (d0 - eyv);
+      const double wn = w0 + cw * (d0 - ezv);
+      // -x / -y neighbours: parity a1, their +x / +y term is mbI*dC*a0 == d0
+      const double umn = uml + cu * (mbI * dXm * a1 - d0);
+      const double vmn = vml + cv * (mbI * dYm * a1 - d0);
+      double dd = (un - umn) * s.ix;
+      dd += (vn - vmn) * s.iy;
+      dd += (wn - wm2) * s.iz;
+      Pn[o] = pn;
+      Un[o] = un;
+      Vn[o] = vn;
+      Wn[o] = wn;
+      Dn[o] = dd;
+      const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
+      r1 = b1 > r1 ? b1 : r1;
+      r2 = b2 > r2 ? b2 : r2;
+      wm2 = wn;
+    } else if (act) {
+      const double dZp = d1p[q0];
       const long long gk = B.lo[2] + z;
       const int bz = bin(s.per[2], gk, nm2), bzp = bnx(s.per[2], gk, nm2);
       const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
@@ -409,6 +497,10 @@ __global__ void __launch_bounds__(NT, MINB)
       r2 = b2 > r2 ? b2 : r2;
       wm2 = wn;
     }
+    fm = fn;
+    fn = fp;
+    fp = fp == 2 ? 0 : fp + 1;
+    dc ^= 1;
   }
 
   unsigned long long rr[2] = {r1, r2};
@@ -454,6 +546,16 @@ __global__ void __launch_bounds__(NT, MINB)
   }
 }
 
+// SF_S2_PF: L2 prefetch distance in planes (default 0 = off: measured no gain)
+static int sweep2_prefetch() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SF_S2_PF");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <int NIN, int MINB>
 static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                     sf_host_flag* hflag, const void* maps, cudaStream_t st) {
@@ -464,7 +566,8 @@ static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c,
     attr = true;
   }
   k_sweep2<NIN, MINB><<<nctas, dim3(TX, TY), smem_bytes(NIN), st>>>(
-      vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas, static_cast<const maps2_t*>(maps));
+      vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas, static_cast<const maps2_t*>(maps),
+      sweep2_prefetch());
 }
 
 // SF_SWEEP2_VARIANT: 0 = 4 S0 stages, 2 CTAs/SM (default); 1 = 6 stages, 1 CTA/SM
