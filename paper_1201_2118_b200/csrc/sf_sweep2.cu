@@ -84,7 +84,7 @@ constexpr int IN_BYTES = IN_P + r128(8 * IW * IFH);
 constexpr uint32_t IN_TX = 8u * (IW * IDH + 4 * IW * IFH);
 enum { U1 = 0, V1 = 1, W1 = 2, P1 = 3, D1 = 4 };
 
-constexpr int smem_bytes(int nin) { return nin * IN_BYTES + (3 * 4 + 2) * EN * 8; }
+constexpr int smem_bytes(int nin) { return nin * IN_BYTES + (4 * 4 + 3) * EN * 8; }
 
 struct maps2_t {  // [field][physical buffer]
   CUtensorMap m[SF_NFIELDS][kSlots];
@@ -99,14 +99,21 @@ void sweep2_box(int field, int* bw, int* bh) {
   *bh = field == SF_DIVU ? IDH : IFH;
 }
 
-// S0 plane q (z = k0 - 2 + q) lives in input stage q % NIN; S1 plane m is
-// z = k0 - 2 + m.
+// Schedule (S0 plane q and S1 plane m both mean z = k0 - 2 + q / m). One CTA
+// barrier per plane; iteration u runs
+//     phase u:  s1_fields(m = u+2)  and  s1_div(m = u+1)     (independent)
+//     barrier
+//     sweep B on plane m = u (u >= 2), overlapping phase u+1 of other warps
+// Warps 0-3 take the second round of s1_fields, warps 4-7 that of s1_div, so
+// every warp does three cell updates per phase. Rings: S0 planes in q % NIN
+// (NIN >= 3), S1 fields (u1 v1 w1 p1) in m % 4, divu1 in m % 3 -- the slot a
+// phase overwrites was last read before the previous barrier.
 template <int NIN, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
     k_sweep2(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc,
              sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag, unsigned int total_ctas,
              const maps2_t* __restrict__ maps, int pf) {
-  static_assert(NIN >= 4, "the prologue keeps four S0 planes in flight");
+  static_assert(NIN >= 3, "three S0 planes are read or in flight per phase");
   if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t bars[NIN];
@@ -156,10 +163,9 @@ __global__ void __launch_bounds__(NT, MINB)
   const CUtensorMap* mW = &maps->m[SF_VZ][tab->bidx[0][SF_VZ][FRONT]];
   const CUtensorMap* mP = &maps->m[SF_P][tab->bidx[0][SF_P][FRONT]];
   const int nin = nplanes + 4;  // S0 planes k0-2 .. k1+1
-  auto stage = [&](int q) { return sm + (q % NIN) * IN_BYTES; };
   auto issue = [&](int q) {
     if (q >= nin) return;
-    unsigned char* st = stage(q);
+    unsigned char* st = sm + (q % NIN) * IN_BYTES;
     uint64_t* bar = &bars[q % NIN];
     bar_expect(bar, IN_TX);
     tma3(st + IN_D, mD, bar, xs, ys, zs + q);
@@ -191,41 +197,49 @@ __global__ void __launch_bounds__(NT, MINB)
   if (tid == 0)
     for (int q = 0; q < NIN; ++q) issue(q);
 
-  // S1 rings: fields (u1 v1 w1 p1) of plane m in slot m % 3, divu1 in m & 1.
-  // Three field slots let s1_fields(m+1) overwrite plane m-2 without waiting
-  // for the previous sweep B.
   // All shared-memory accesses below index one array with 32-bit offsets.
   double* const S = reinterpret_cast<double*>(sm);
-  constexpr int FRING = NIN * IN_BYTES / 8, DRING = FRING + 3 * 4 * EN;
+  constexpr int FRING = NIN * IN_BYTES / 8, DRING = FRING + 4 * 4 * EN;
+  auto so = [&](int q) { return (q % NIN) * (IN_BYTES / 8); };  // S0 stage offset
 
   // ---- per-thread widened cells ---------------------------------------------
-  // Thread t owns widened cells e = t + 1 and, for t < 128 (warps 0-3),
-  // e = t + 257. The corner e = 0 (x = i0-2, y = j0-2) is never read.
-  // e_ia: index into the S0 boxes; e_qd: DIVERGENCE source cell (wall
-  // mirror applied); bt: scale-table rows rc | rx << 3 | ry << 6 (x/y bits),
-  // parity << 9, owned << 10, x pin << 11, y pin << 12, div source << 13
-  const bool has2 = tid < EN - 1 - NT;
-  int e_e[NE], e_ia[NE], e_qd[NE], e_bt[NE];
+  // s1_fields: thread t owns e = t + 1 and, for t < 128 (warps 0-3),
+  // e = t + 257. s1_div: e = 384 - t and, for t >= 128 (warps 4-7),
+  // e = 256 - t. The corner e = 0 (x = i0-2, y = j0-2) is never read.
+  // f_ia: index into the S0 boxes; f_bt: scale-table rows rc | rx << 3 |
+  // ry << 6 (x/y bits), parity << 9, owned << 10, x pin << 11, y pin << 12.
+  // d_q: DIVERGENCE operand cell (wall mirror applied), d_ok: bit r set when
+  // div cell r is a source (x >= i0-1, y >= j0-1).
+  const bool has2f = tid < EN - 1 - NT, has2d = tid >= EN - 1 - NT;
+  int f_e[NE], f_ia[NE], f_bt[NE], d_e[NE], d_q[NE], d_ok = 0;
 #pragma unroll
   for (int r = 0; r < NE; ++r) {
-    const int e = r == 0 || has2 ? tid + 1 + r * NT : EN - 1;
-    const int ex = e % EW, ey = e / EW;
-    const int x = i0 - 2 + ex, y = j0 - 2 + ey;
-    const long long gi = B.lo[0] + x, gj = B.lo[1] + y;
-    const int bx = bin(s.per[0], gi, nm0), bxp = bnx(s.per[0], gi, nm0);
-    const int by = bin(s.per[1], gj, nm1), byp = bnx(s.per[1], gj, nm1);
-    // DIVERGENCE source cell: x >= i0-1, y >= j0-1; the +x / +y ghost (x = n0,
-    // y = n1) takes the wall mirror of the last owned cell (exchange.hpp:438-449),
-    // evaluated with that cell's operands
-    int dx = ex, dy = ey;
-    if (x >= n0) dx -= x - (n0 - 1);
-    if (y >= n1) dy -= y - (n1 - 1);
-    e_e[r] = e;
-    e_ia[r] = ey * IW + ex;
-    e_qd[r] = dy * EW + dx;
-    e_bt[r] = ((bx << 2) | (by << 1)) | (((bxp << 2) | (by << 1)) << 3) | (((bx << 2) | (byp << 1)) << 6) |
-              ((int)((gi + gj) & 1) << 9) | ((x >= 0 && x < n0 && y >= 0 && y < n1) << 10) |
-              ((x == n0 - 1) << 11) | ((y == n1 - 1) << 12) | ((ex >= 1 && ey >= 1) << 13);
+    {
+      const int e = r == 0 ? tid + 1 : (has2f ? tid + 1 + NT : EN - 1);
+      const int ex = e % EW, ey = e / EW;
+      const int x = i0 - 2 + ex, y = j0 - 2 + ey;
+      const long long gi = B.lo[0] + x, gj = B.lo[1] + y;
+      const int bx = bin(s.per[0], gi, nm0), bxp = bnx(s.per[0], gi, nm0);
+      const int by = bin(s.per[1], gj, nm1), byp = bnx(s.per[1], gj, nm1);
+      f_e[r] = e;
+      f_ia[r] = ey * IW + ex;
+      f_bt[r] = ((bx << 2) | (by << 1)) | (((bxp << 2) | (by << 1)) << 3) | (((bx << 2) | (byp << 1)) << 6) |
+                ((int)((gi + gj) & 1) << 9) | ((x >= 0 && x < n0 && y >= 0 && y < n1) << 10) |
+                ((x == n0 - 1) << 11) | ((y == n1 - 1) << 12);
+    }
+    {
+      const int e = r == 0 ? EN - 1 - tid : (has2d ? EN - 1 - NT - tid + 128 : EN - 1);
+      const int ex = e % EW, ey = e / EW;
+      const int x = i0 - 2 + ex, y = j0 - 2 + ey;
+      // the +x / +y ghost (x = n0, y = n1) takes the wall mirror of the last
+      // owned cell (exchange.hpp:438-449), evaluated with that cell's operands
+      int dx = ex, dy = ey;
+      if (x >= n0) dx -= x - (n0 - 1);
+      if (y >= n1) dy -= y - (n1 - 1);
+      d_e[r] = e;
+      d_q[r] = dy * EW + dx;
+      if (ex >= 1 && ey >= 1 && (r == 0 || has2d)) d_ok |= 1 << r;
+    }
   }
   // Interior tile: every widened cell has all x/y scale bits 1 (so each
   // -(beta*bscale) is -(beta*1.0) = smb[7]), is owned and unpinned, and needs
@@ -239,10 +253,10 @@ __global__ void __launch_bounds__(NT, MINB)
   const int zf_hi = (int)min((long long)n2 - 3, nm2 - 2 - B.lo[2]);
   const double mbI = smb[7];
 
-  // S1 fields of plane z from its S0 stage and divu0 of plane z+1: sweep A's
-  // cell update (cfd.hpp:699-719) with the wall pins. Cells outside the
-  // domain carry S0; their wall-normal values are the constant pins.
-  // st / stn: S0 stages of planes z and z+1 (offsets in doubles); fo: field slot
+  // S1 fields of plane z from its S0 stage (st) and divu0 of plane z+1 (stn):
+  // sweep A's cell update (cfd.hpp:699-719) with the wall pins, into field
+  // slot fo. Cells outside the domain carry S0; their wall-normal values are
+  // the constant pins.
   auto s1_fields = [&](int z, int st, int stn, int fo) {
     const int Di = st + IN_D / 8, Ui = st + IN_U / 8, Vi = st + IN_V / 8, Wi = st + IN_W / 8,
               Pi = st + IN_P / 8, Dz = stn + IN_D / 8;
@@ -252,12 +266,12 @@ __global__ void __launch_bounds__(NT, MINB)
     if (fast_xy && z >= zf_lo && z <= zf_hi) {
 #pragma unroll
       for (int r = 0; r < NE; ++r) {
-        if (r > 0 && !has2) break;
-        const int ia = e_ia[r], e = e_e[r];
+        if (r > 0 && !has2f) break;
+        const int ia = f_ia[r], e = f_e[r];
         // all loads first: the stores below may alias them as far as the compiler knows
         const double dc = S[Di + ia], dx = S[Di + ia + 1], dy = S[Di + ia + IW], dz = S[Dz + ia];
         const double uu = S[Ui + ia], vv = S[Vi + ia], ww = S[Wi + ia], pp = S[Pi + ia];
-        const double a0 = ((((e_bt[r] >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
+        const double a0 = ((((f_bt[r] >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
         const double d0 = mbI * dc * a0;
         const double exv = mbI * dx * a1;
         const double eyv = mbI * dy * a1;
@@ -274,8 +288,8 @@ __global__ void __launch_bounds__(NT, MINB)
     const bool pz = z == n2 - 1;
 #pragma unroll
     for (int r = 0; r < NE; ++r) {
-      if (r > 0 && !has2) break;
-      const int e = e_e[r], ia = e_ia[r], bt = e_bt[r];
+      if (r > 0 && !has2f) break;
+      const int e = f_e[r], ia = f_ia[r], bt = f_bt[r];
       if (!(zin && ((bt >> 10) & 1))) {
         S[u1 + e] = S[Ui + ia];
         S[v1 + e] = S[Vi + ia];
@@ -295,37 +309,34 @@ __global__ void __launch_bounds__(NT, MINB)
       S[w1 + e] = pz ? pin_w : S[Wi + ia] + cw * (d0 - ezv);
     }
   };
-  // DIVERGENCE of S1 on plane z (cfd.hpp:605-608); the top ghost plane
-  // mirrors plane n2-1 (dm).
-  // fo / fom: field slots of planes z and z-1; d1 / dm: divu1 slots of z and z-1
+  // DIVERGENCE of S1 on plane z (cfd.hpp:605-608) from field slots fo (z) and
+  // fom (z-1) into divu1 slot d1; the top ghost plane mirrors plane n2-1 (dm).
   auto s1_div = [&](int z, int fo, int fom, int d1, int dm) {
     if (z >= n2) {
 #pragma unroll
       for (int r = 0; r < NE; ++r) {
-        if (r > 0 && !has2) break;
-        S[d1 + e_e[r]] = S[dm + e_e[r]];
+        if (r > 0 && !has2d) break;
+        S[d1 + d_e[r]] = S[dm + d_e[r]];
       }
       return;
     }
     const int u1 = fo + U1 * EN, v1 = fo + V1 * EN, w1 = fo + W1 * EN, w1m = fom + W1 * EN;
 #pragma unroll
     for (int r = 0; r < NE; ++r) {
-      if (r > 0 && !has2) break;
-      // non-source cells (x = i0-2 or y = j0-2) compute on in-bounds operands
-      // and skip the store: no divergent branch
-      const int q = e_qd[r];
+      if (r > 0 && !has2d) break;
+      // non-source cells compute on in-bounds operands and skip the store
+      const int q = d_q[r];
       const double du = S[u1 + q] - S[u1 + q - 1];
       const double dv = S[v1 + q] - S[v1 + q - EW];
       const double dw = S[w1 + q] - S[w1m + q];
       double dd = du * s.ix;
       dd += dv * s.iy;
       dd += dw * s.iz;
-      if ((e_bt[r] >> 13) & 1) S[d1 + e_e[r]] = dd;
+      if ((d_ok >> r) & 1) S[d1 + d_e[r]] = dd;
     }
   };
   auto F = [&](int slot) { return FRING + slot * 4 * EN; };  // field slot offset
   auto Dr = [&](int slot) { return DRING + slot * EN; };     // divu1 slot offset
-  auto so = [&](int q) { return (q % NIN) * (IN_BYTES / 8); };  // S0 stage offset
 
   // ---- this thread's tile cell ----------------------------------------------
   const int i = i0 + tx, j = j0 + ty;
@@ -341,24 +352,6 @@ __global__ void __launch_bounds__(NT, MINB)
   const int par_col = (int)((gi + gj) & 1);
   const int q0 = (ty + 2) * EW + (tx + 2);
 
-  // prologue: S1 planes m = 0..2 (z = k0-2 .. k0), divu1 of planes 1 and 2
-  wait_in(0);
-  wait_in(1);
-  wait_in(2);
-  s1_fields(k0 - 2, so(0), so(1), F(0));
-  s1_fields(k0 - 1, so(1), so(2), F(1));
-  __syncthreads();
-  if (tid == 0) issue(NIN);  // S0 plane 0 is consumed
-  s1_div(k0 - 1, F(1), F(0), Dr(1), Dr(0));
-  wait_in(3);
-  s1_fields(k0, so(2), so(3), F(2));
-  __syncthreads();
-  if (tid == 0) issue(NIN + 1);  // S0 plane 1 is consumed
-  // w1 and divu1 of the plane below the chunk, for sweep B's swept -z neighbour
-  const double w1_below = S[F(1) + W1 * EN + q0], d1_below = S[Dr(1) + q0];
-  s1_div(k0, F(2), F(1), Dr(0), Dr(1));
-  __syncthreads();
-
   double* __restrict__ Dn = tab->ptr[0][SF_DIVU][ALT];
   double* __restrict__ Pn = tab->ptr[0][SF_P][ALT];
   double* __restrict__ Un = tab->ptr[0][SF_VX][ALT];
@@ -366,141 +359,151 @@ __global__ void __launch_bounds__(NT, MINB)
   double* __restrict__ Wn = tab->ptr[0][SF_VZ][ALT];
   unsigned long long r1 = 0ull, r2 = 0ull;
   double wm2 = 0.0;  // swept w2 of the -z neighbour (marching register)
-  if (act) {
-    if (k0 > 0) {
-      const long long gkm = B.lo[2] + k0 - 1;
-      const int bzm = bin(s.per[2], gkm, nm2), bzpm = bnx(s.per[2], gkm, nm2);
-      const double a0m = (((gi + gj + gkm) & 1) == colB) ? 1.0 : 0.0, a1m = 1.0 - a0m;
-      const double d0m = smb[ic | bzm] * d1_below * a0m;
-      const double ezm = smb[ic | bzpm] * S[Dr(0) + q0] * a1m;
-      wm2 = w1_below + cw * (d0m - ezm);
-    } else {
-      wm2 = w1_below;  // pinned ghost plane
-    }
-  }
   long long o = B.base + ((long long)k0 * B.sy + j) * sx + i;
 
-  // ring slots of planes m-1, m, m+1 (fields, mod 3) and m (divu1, mod 2)
-  int fm = 2, fn = 0, fp = 1, dc = 0;
-  for (int kk = 0; kk < nplanes; ++kk, o += sxy) {
-    const int z = k0 + kk;
-    const int m = kk + 2;
-    // S1 of plane z+1 from S0 planes m+1, m+2 into field slot fn (held plane
-    // m-2, which the previous iteration's barriers retired)
-    wait_in(m + 2);
-    s1_fields(z + 1, so(m + 1), so(m + 2), F(fn));
+  // pre-phase: S1 fields of planes 0 and 1 (S0 planes 0..2)
+  wait_in(0);
+  wait_in(1);
+  wait_in(2);
+  s1_fields(k0 - 2, so(0), so(1), F(0));
+  s1_fields(k0 - 1, so(1), so(2), F(1));
+  __syncthreads();
+  if (tid == 0) {  // S0 planes 0 and 1 are consumed
+    issue(NIN);
+    issue(NIN + 1);
+  }
+
+  // S1 plane m: fields in slot m & 3, divu1 in slot m % 3 (dsu = u % 3)
+  int dsu = 0;
+  for (int u = 0; u <= nplanes + 1; ++u) {
+    const int dsu1 = dsu == 2 ? 0 : dsu + 1;
+    wait_in(u + 3);
+    if (u <= nplanes) s1_fields(k0 + u, so(u + 2), so(u + 3), F((u + 2) & 3));
+    s1_div(k0 + u - 1, F((u + 1) & 3), F(u & 3), Dr(dsu1), Dr(dsu));
     __syncthreads();
-    if (tid == 0) issue(m + NIN);  // S0 plane m is consumed
-    // divu1 of plane z+1 into divu slot dc^1 (held plane m-1, read by the
-    // previous sweep B before the barrier above)
-    s1_div(z + 1, F(fn), F(fm), Dr(dc ^ 1), Dr(dc));
-    __syncthreads();
-    const double* u1 = S + F(fm) + U1 * EN;
-    const double* v1 = S + F(fm) + V1 * EN;
-    const double* w1 = S + F(fm) + W1 * EN;
-    const double* p1 = S + F(fm) + P1 * EN;
-    const double* d1 = S + Dr(dc);
-    const double* d1p = S + Dr(dc ^ 1);
-    if (fast_xy && z >= zf_lo && z <= zf_hi) {
-      // interior plane (see fast_xy): bitwise the general path below
-      const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
-      const double dXm = d1[q0 - 1], dYm = d1[q0 - EW], dZp = d1p[q0];
-      const double p0 = p1[q0], u0 = u1[q0], uml = u1[q0 - 1], v0 = v1[q0], vml = v1[q0 - EW], w0 = w1[q0];
-      const int par = par_col ^ (int)((B.lo[2] + z) & 1);
-      const double a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
-      const double d0 = mbI * dC * a0;
-      const double exv = mbI * dXp * a1;
-      const double eyv = mbI * dYp * a1;
-      const double ezv = mbI * dZp * a1;
-      const double pn = p0 + d0;
-      const double un = u0 + cu * (d0 - exv);
-      const double vn = v0 + cv * (d0 - eyv);
-      const double wn = w0 + cw * (d0 - ezv);
-      // -x / -y neighbours: parity a1, their +x / +y term is mbI*dC*a0 == d0
-      const double umn = uml + cu * (mbI * dXm * a1 - d0);
-      const double vmn = vml + cv * (mbI * dYm * a1 - d0);
-      double dd = (un - umn) * s.ix;
-      dd += (vn - vmn) * s.iy;
-      dd += (wn - wm2) * s.iz;
-      Pn[o] = pn;
-      Un[o] = un;
-      Vn[o] = vn;
-      Wn[o] = wn;
-      Dn[o] = dd;
-      const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
-      r1 = b1 > r1 ? b1 : r1;
-      r2 = b2 > r2 ? b2 : r2;
-      wm2 = wn;
-    } else if (act) {
-      const double dZp = d1p[q0];
-      const long long gk = B.lo[2] + z;
-      const int bz = bin(s.per[2], gk, nm2), bzp = bnx(s.per[2], gk, nm2);
-      const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
-      const double dXm = d1[q0 - 1], dYm = d1[q0 - EW];
-      const int par = par_col ^ (int)(gk & 1);
-      const double a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
-      const double d0 = smb[ic | bz] * dC * a0;
-      const double exv = smb[iex | bz] * dXp * a1;
-      const double eyv = smb[iey | bz] * dYp * a1;
-      const double ezv = smb[ic | bzp] * dZp * a1;
-      const double pn = p1[q0] + d0;
-      double un = u1[q0] + cu * (d0 - exv);
-      double vn = v1[q0] + cv * (d0 - eyv);
-      double wn = w1[q0] + cw * (d0 - ezv);
-      if (i == n0 - 1) un = pin_u;
-      if (j == n1 - 1) vn = pin_v;
-      if (z == n2 - 1) wn = pin_w;
-      // swept -x / -y neighbours; at the low wall the pinned ghost (in S1)
-      double umn, vmn;
-      if (i > 0) {
-        const double a0m = a1, a1m = 1.0 - a0m;
-        const double d0m = smb[ixm | bz] * dXm * a0m;
-        const double exm = smb[ixpm | bz] * dC * a1m;
-        umn = u1[q0 - 1] + cu * (d0m - exm);
+    if (tid == 0) issue(u + 2 + NIN);  // S0 plane u+2 is consumed
+    if (u == 1 && act) {
+      // swept w2 of the plane below the chunk: sweep B's -z neighbour at k0
+      const double w1_below = S[F(1) + W1 * EN + q0];
+      if (k0 > 0) {
+        const long long gkm = B.lo[2] + k0 - 1;
+        const int bzm = bin(s.per[2], gkm, nm2), bzpm = bnx(s.per[2], gkm, nm2);
+        const double a0m = (((gi + gj + gkm) & 1) == colB) ? 1.0 : 0.0, a1m = 1.0 - a0m;
+        const double d0m = smb[ic | bzm] * S[Dr(1) + q0] * a0m;
+        const double ezm = smb[ic | bzpm] * S[Dr(2) + q0] * a1m;
+        wm2 = w1_below + cw * (d0m - ezm);
       } else {
-        umn = u1[q0 - 1];
+        wm2 = w1_below;  // pinned ghost plane
       }
-      if (j > 0) {
-        const double a0m = a1, a1m = 1.0 - a0m;
-        const double d0m = smb[iym | bz] * dYm * a0m;
-        const double eym = smb[iypm | bz] * dC * a1m;
-        vmn = v1[q0 - EW] + cv * (d0m - eym);
-      } else {
-        vmn = v1[q0 - EW];
-      }
-      double dd = (un - umn) * s.ix;
-      dd += (vn - vmn) * s.iy;
-      dd += (wn - wm2) * s.iz;
-      Pn[o] = pn;
-      Un[o] = un;
-      Vn[o] = vn;
-      Wn[o] = wn;
-      Dn[o] = dd;
-      // ghosts the next pass reads: pinned low-face velocities, mirrored divu
-      if (i == 0) {
-        Un[o - 1] = umn;
-        Dn[o - 1] = dd;
-      }
-      if (j == 0) {
-        Vn[o - sx] = vmn;
-        Dn[o - sx] = dd;
-      }
-      if (z == 0) {
-        Wn[o - sxy] = wm2;
-        Dn[o - sxy] = dd;
-      }
-      if (i == n0 - 1) Dn[o + 1] = dd;
-      if (j == n1 - 1) Dn[o + sx] = dd;
-      if (z == n2 - 1) Dn[o + sxy] = dd;
-      const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
-      r1 = b1 > r1 ? b1 : r1;
-      r2 = b2 > r2 ? b2 : r2;
-      wm2 = wn;
     }
-    fm = fn;
-    fn = fp;
-    fp = fp == 2 ? 0 : fp + 1;
-    dc ^= 1;
+    if (u >= 2) {
+      // sweep B on plane m = u, z = k0 + u - 2
+      const int z = k0 + u - 2;
+      const double* u1 = S + F(u & 3) + U1 * EN;
+      const double* v1 = S + F(u & 3) + V1 * EN;
+      const double* w1 = S + F(u & 3) + W1 * EN;
+      const double* p1 = S + F(u & 3) + P1 * EN;
+      const double* d1 = S + Dr(dsu);
+      const double* d1p = S + Dr(dsu1);
+      if (fast_xy && z >= zf_lo && z <= zf_hi) {
+        // interior plane (see fast_xy): bitwise the general path below
+        const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
+        const double dXm = d1[q0 - 1], dYm = d1[q0 - EW], dZp = d1p[q0];
+        const double p0 = p1[q0], u0 = u1[q0], uml = u1[q0 - 1], v0 = v1[q0], vml = v1[q0 - EW], w0 = w1[q0];
+        const int par = par_col ^ (int)((B.lo[2] + z) & 1);
+        const double a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
+        const double d0 = mbI * dC * a0;
+        const double exv = mbI * dXp * a1;
+        const double eyv = mbI * dYp * a1;
+        const double ezv = mbI * dZp * a1;
+        const double pn = p0 + d0;
+        const double un = u0 + cu * (d0 - exv);
+        const double vn = v0 + cv * (d0 - eyv);
+        const double wn = w0 + cw * (d0 - ezv);
+        // -x / -y neighbours: parity a1, their +x / +y term is mbI*dC*a0 == d0
+        const double umn = uml + cu * (mbI * dXm * a1 - d0);
+        const double vmn = vml + cv * (mbI * dYm * a1 - d0);
+        double dd = (un - umn) * s.ix;
+        dd += (vn - vmn) * s.iy;
+        dd += (wn - wm2) * s.iz;
+        Pn[o] = pn;
+        Un[o] = un;
+        Vn[o] = vn;
+        Wn[o] = wn;
+        Dn[o] = dd;
+        const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
+        r1 = b1 > r1 ? b1 : r1;
+        r2 = b2 > r2 ? b2 : r2;
+        wm2 = wn;
+      } else if (act) {
+        const double dZp = d1p[q0];
+        const long long gk = B.lo[2] + z;
+        const int bz = bin(s.per[2], gk, nm2), bzp = bnx(s.per[2], gk, nm2);
+        const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
+        const double dXm = d1[q0 - 1], dYm = d1[q0 - EW];
+        const int par = par_col ^ (int)(gk & 1);
+        const double a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
+        const double d0 = smb[ic | bz] * dC * a0;
+        const double exv = smb[iex | bz] * dXp * a1;
+        const double eyv = smb[iey | bz] * dYp * a1;
+        const double ezv = smb[ic | bzp] * dZp * a1;
+        const double pn = p1[q0] + d0;
+        double un = u1[q0] + cu * (d0 - exv);
+        double vn = v1[q0] + cv * (d0 - eyv);
+        double wn = w1[q0] + cw * (d0 - ezv);
+        if (i == n0 - 1) un = pin_u;
+        if (j == n1 - 1) vn = pin_v;
+        if (z == n2 - 1) wn = pin_w;
+        // swept -x / -y neighbours; at the low wall the pinned ghost (in S1)
+        double umn, vmn;
+        if (i > 0) {
+          const double a0m = a1, a1m = 1.0 - a0m;
+          const double d0m = smb[ixm | bz] * dXm * a0m;
+          const double exm = smb[ixpm | bz] * dC * a1m;
+          umn = u1[q0 - 1] + cu * (d0m - exm);
+        } else {
+          umn = u1[q0 - 1];
+        }
+        if (j > 0) {
+          const double a0m = a1, a1m = 1.0 - a0m;
+          const double d0m = smb[iym | bz] * dYm * a0m;
+          const double eym = smb[iypm | bz] * dC * a1m;
+          vmn = v1[q0 - EW] + cv * (d0m - eym);
+        } else {
+          vmn = v1[q0 - EW];
+        }
+        double dd = (un - umn) * s.ix;
+        dd += (vn - vmn) * s.iy;
+        dd += (wn - wm2) * s.iz;
+        Pn[o] = pn;
+        Un[o] = un;
+        Vn[o] = vn;
+        Wn[o] = wn;
+        Dn[o] = dd;
+        // ghosts the next pass reads: pinned low-face velocities, mirrored divu
+        if (i == 0) {
+          Un[o - 1] = umn;
+          Dn[o - 1] = dd;
+        }
+        if (j == 0) {
+          Vn[o - sx] = vmn;
+          Dn[o - sx] = dd;
+        }
+        if (z == 0) {
+          Wn[o - sxy] = wm2;
+          Dn[o - sxy] = dd;
+        }
+        if (i == n0 - 1) Dn[o + 1] = dd;
+        if (j == n1 - 1) Dn[o + sx] = dd;
+        if (z == n2 - 1) Dn[o + sxy] = dd;
+        const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
+        r1 = b1 > r1 ? b1 : r1;
+        r2 = b2 > r2 ? b2 : r2;
+        wm2 = wn;
+      }
+      o += sxy;
+    }
+    dsu = dsu1;
   }
 
   unsigned long long rr[2] = {r1, r2};
@@ -570,7 +573,7 @@ static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c,
       sweep2_prefetch());
 }
 
-// SF_SWEEP2_VARIANT: 0 = 4 S0 stages, 2 CTAs/SM (default); 1 = 6 stages, 1 CTA/SM
+// SF_SWEEP2_VARIANT: 0 = 3 S0 stages, 2 CTAs/SM (default); 1 = 6 stages, 1 CTA/SM
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                    sf_host_flag* hflag, const void* maps, cudaStream_t st) {
   if (nctas <= 0) return;
@@ -581,7 +584,7 @@ void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, 
   }
   switch (v) {
     case 1: launch2<6, 1>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
-    default: launch2<4, 2>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
+    default: launch2<3, 2>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
   }
 }
 
