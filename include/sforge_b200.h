@@ -187,6 +187,13 @@ int sf_sim_world(const sf_sim* s);
  * grid::gather / grid::scatter (io.hpp:25-65). */
 int sf_sim_gather_block(sf_sim* s, const char* field, int worker, double* host, int64_t n);
 int sf_sim_scatter_block(sf_sim* s, const char* field, int worker, const double* host, int64_t n);
+/* Asynchronous forms: the transfer is queued on the library's upload or
+ * download stream and the call returns at once. `host` must be page-locked
+ * and left untouched until sf_sim_synchronize. Device-side ordering against
+ * compute and against other transfers of the same field is kept by the
+ * library, so an upload of one field overlaps the download of another. */
+int sf_sim_gather_block_async(sf_sim* s, const char* field, int worker, double* host, int64_t n);
+int sf_sim_scatter_block_async(sf_sim* s, const char* field, int worker, const double* host, int64_t n);
 /* The exchange plan of one refresh phase (axis 0..2, slabs widened as in
  * exchange.hpp:165-206) or of the fused loop's face exchange (axis = -1) for
  * rank `rank` of a `world`-rank decomposition -- host logic, no device.  Rows
@@ -252,7 +259,7 @@ int sf_sim_run_schedule(sf_sim* s, const sf_schedule_step* steps, int n_steps, c
 int sf_sim_result(sf_sim* s, const char* name, double* value);
 
 /* Device plumbing for benches and transports. */
-int sf_sim_synchronize(sf_sim* s);
+int sf_sim_synchronize(sf_sim* s);        /* waits for compute and host transfers */
 void* sf_sim_stream(sf_sim* s);            /* the cudaStream_t all work is ordered on */
 /* Kernel launches issued by this simulation since creation (or the last reset). */
 int64_t sf_sim_launch_count(sf_sim* s, int reset);

@@ -201,6 +201,8 @@ SIGNATURES = [
     ("sf_sim_world", [_vp], _i),
     ("sf_sim_gather_block", [_vp, _cp, _i, _vp, _i64], _i),
     ("sf_sim_scatter_block", [_vp, _cp, _i, _vp, _i64], _i),
+    ("sf_sim_gather_block_async", [_vp, _cp, _i, _vp, _i64], _i),
+    ("sf_sim_scatter_block_async", [_vp, _cp, _i, _vp, _i64], _i),
     ("sf_exchange_plan", [_i64p, _i, _i, _ip, _i, C.c_uint, _i, _i, _i64p, _ip], _i),
     ("sf_sim_synchronize", [_vp], _i),
     ("sf_sim_stream", [_vp], _vp),
@@ -226,6 +228,24 @@ SIGNATURES = [
 _lib = None
 
 
+def _pin_nccl() -> None:
+    """Point the library's run-time NCCL load (SF_NCCL_LIB) at the libnccl.so.2
+    torch links against (the nvidia-nccl wheel), so a later `import torch` finds
+    the same library instead of clashing with an older system copy."""
+    if os.environ.get("SF_NCCL_LIB"):
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for d in (spec.submodule_search_locations or []) if spec else []:
+            cand = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["SF_NCCL_LIB"] = cand
+                return
+    except Exception:
+        pass
+
+
 def lib() -> C.CDLL:
     """Load the library (building it first if sources are newer)."""
     global _lib
@@ -238,6 +258,7 @@ def lib() -> C.CDLL:
             if not os.path.exists(LIB_PATH):
                 raise RuntimeError(
                     f"CUDA library {LIB_PATH} is missing and could not be built: {e}") from e
+    _pin_nccl()
     L = C.CDLL(LIB_PATH)
     for name, args, res in SIGNATURES:
         fn = getattr(L, name)

@@ -362,12 +362,23 @@ class simulation {
     cudaEventDestroy(t0_);
     cudaEventDestroy(t1_);
     for (auto e : timers_) cudaEventDestroy(e);
+    if (io_[0]) {
+      for (int k = 0; k < 2; ++k) {
+        cudaStreamSynchronize(io_[k]);
+        cudaStreamDestroy(io_[k]);
+      }
+      for (auto e : io_ev_) cudaEventDestroy(e);
+      for (auto e : io_up_) cudaEventDestroy(e);
+    }
     if (comm_ && nccl() && nccl()->CommDestroy) nccl()->CommDestroy(comm_);
     cudaStreamDestroy(st_);
   }
 
   // ---- helpers ------------------------------------------------------------
-  void sync() { SF_CK(cudaStreamSynchronize(st_)); }
+  void sync() {
+    flush_io();
+    SF_CK(cudaStreamSynchronize(st_));
+  }
   void check_launch() {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw error(SF_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
@@ -529,28 +540,61 @@ class simulation {
                       src + (k * d[1] + j) * d[0], sizeof(double) * (size_t)d[0]);
     }
   }
-  // owned block of local component w (global worker id) <-> dense x-fastest host array
-  void block_io(int f, int w, double* host, i64 n, bool to_device) {
+  // Owned block of local component w (global worker id) <-> dense x-fastest
+  // host array: one 3-D copy-engine transfer straight between the host array
+  // and the padded device block (row pitch sx, slice pitch sx*sy), on a
+  // dedicated stream per direction. Ordering, all on the device:
+  //  - a gather waits for the compute stream (the table download syncs it);
+  //  - a scatter of field f waits for the last gather of f;
+  //  - later compute waits for both.
+  // Async mode returns at once: host memory must be pinned and stay untouched
+  // until sf_sim_synchronize. Uploads then overlap downloads of other fields
+  // (PCIe is full duplex).
+  void block_io(int f, int w, double* host, i64 n, bool to_device, bool async = false) {
     if (w < 0 || w >= dec_.workers || lid_[w] < 0)
       throw error(SF_ERR_ARG, "worker " + std::to_string(w) + " is not owned by this process");
     const int b = lid_[w];
     const auto& L = lay_[b];
     const i64 d[3] = {L.dims[0], L.dims[1], L.dims[2]};
     if (n < d[0] * d[1] * d[2]) throw error(SF_ERR_ARG, "block buffer too small");
-    download_table();
-    double* sg = staging();
-    const i64 z[3] = {0, 0, 0};
+    download_table(false);
+    if (!io_[0]) {
+      for (int k = 0; k < 2; ++k) SF_CK(cudaStreamCreateWithFlags(&io_[k], cudaStreamNonBlocking));
+      for (int k = 0; k < kMaxFields; ++k) {
+        SF_CK(cudaEventCreateWithFlags(&io_ev_[k], cudaEventDisableTiming));
+        SF_CK(cudaEventCreateWithFlags(&io_up_[k], cudaEventDisableTiming));
+      }
+    }
+    cudaMemcpy3DParms prm = {};
+    double* dev = htab_->ptr[b][f][FRONT] + L.base;
+    cudaPitchedPtr dp = make_cudaPitchedPtr(dev, (size_t)L.sx * sizeof(double), (size_t)d[0] * sizeof(double),
+                                            (size_t)L.sy);
+    cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)d[0] * sizeof(double), (size_t)d[0] * sizeof(double),
+                                            (size_t)d[1]);
+    prm.extent = make_cudaExtent((size_t)d[0] * sizeof(double), (size_t)d[1], (size_t)d[2]);
     if (to_device) {
-      SF_CK(cudaMemcpyAsync(sg, host, sizeof(double) * (size_t)(d[0] * d[1] * d[2]), cudaMemcpyHostToDevice, st_));
-      launch_copy_box(sg, 0, d[0], d[1], htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, z, d, z, st_);
+      prm.srcPtr = hp;
+      prm.dstPtr = dp;
+      prm.kind = cudaMemcpyHostToDevice;
+      SF_CK(cudaStreamWaitEvent(io_[0], io_ev_[f], 0));  // the last download of f
+      SF_CK(cudaMemcpy3DAsync(&prm, io_[0]));
+      SF_CK(cudaEventRecord(io_up_[f], io_[0]));
+      io_pending_.push_back(io_up_[f]);
       ghosts_ok_[fname_[f]] = false;
     } else {
-      launch_copy_box(htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, sg, 0, d[0], d[1], z, d, z, st_);
-      SF_CK(cudaMemcpyAsync(host, sg, sizeof(double) * (size_t)(d[0] * d[1] * d[2]), cudaMemcpyDeviceToHost, st_));
+      prm.srcPtr = dp;
+      prm.dstPtr = hp;
+      prm.kind = cudaMemcpyDeviceToHost;
+      SF_CK(cudaStreamWaitEvent(io_[1], io_up_[f], 0));  // after the last upload of f
+      SF_CK(cudaMemcpy3DAsync(&prm, io_[1]));
+      SF_CK(cudaEventRecord(io_ev_[f], io_[1]));
+      io_pending_.push_back(io_ev_[f]);  // compute may not overwrite f before it is read
     }
-    ++launches_;
-    check_launch();
-    sync();
+    if (!async) SF_CK(cudaStreamSynchronize(io_[to_device ? 0 : 1]));
+  }
+  void io_sync() {
+    for (int k = 0; k < 2; ++k)
+      if (io_[k]) SF_CK(cudaStreamSynchronize(io_[k]));
   }
   int rank() const { return rank_; }
   int world() const { return world_; }
@@ -1010,6 +1054,7 @@ class simulation {
     if (debug_bounds()) check_ghosts(uk, reg);
     const work_set& ws = items_for(reg, uk.halo, uk.zc, uk.tx, uk.ty);
     if (ws.nctas > 0) {
+      flush_io();
       double* const* ptrs = &dtab_->ptr[0][0][0];
       const void* geo = geo_;
       const sf_work* items = ws.d;
@@ -1356,6 +1401,14 @@ class simulation {
   sf_host_flag* dflag_ = nullptr;
   double* staging_ = nullptr;
   void* maps_ = nullptr;  // TMA descriptors (null: no driver entry point -> LDG kernel)
+  cudaStream_t io_[2]{};    // host transfers: 0 uploads, 1 downloads
+  cudaEvent_t io_ev_[kMaxFields]{};  // last download of each field
+  cudaEvent_t io_up_[kMaxFields]{};  // last upload of each field
+  mutable std::vector<cudaEvent_t> io_pending_;  // not yet ordered before compute
+  // compute enqueues so far / at the last table download: block_io skips the
+  // download (a copy that would queue behind large transfers) when equal
+  mutable unsigned long long compute_epoch_ = 1;
+  unsigned long long table_epoch_ = 0;
   void* maps2_ = nullptr;  // temporal-pass descriptors (null: pass unavailable)
   const bool temporal_env_ = getenv("SF_NO_TEMPORAL") == nullptr;
   std::vector<void*> dev_allocs_;
@@ -1566,10 +1619,17 @@ class simulation {
     sync();
   }
 
-  void download_table() {
-    sync();
+  // flush = false: wait for enqueued compute only, without first ordering the
+  // compute stream after pending host transfers (block_io)
+  void download_table(bool flush = true) {
+    if (!flush && table_epoch_ == compute_epoch_) return;  // nothing enqueued since the last download
+    if (flush)
+      sync();
+    else
+      SF_CK(cudaStreamSynchronize(st_));
     SF_CK(cudaMemcpy(htab_->ptr, dtab_->ptr, sizeof(htab_->ptr), cudaMemcpyDeviceToHost));
     SF_CK(cudaMemcpy(htab_->bidx, dtab_->bidx, sizeof(htab_->bidx), cudaMemcpyDeviceToHost));
+    table_epoch_ = compute_epoch_;
   }
   void upload_table() {
     SF_CK(cudaMemcpy(dtab_->ptr, htab_->ptr, sizeof(htab_->ptr), cudaMemcpyHostToDevice));
@@ -1585,10 +1645,24 @@ class simulation {
     ++alloc_gen_;
   }
 
-  table_view tview() const { return table_view{dtab_, nullptr, 0}; }
-  table_view tview(const work_set& w) const { return table_view{dtab_, w.d, w.n}; }
+  table_view tview() const {
+    flush_io();
+    return table_view{dtab_, nullptr, 0};
+  }
+  table_view tview(const work_set& w) const {
+    flush_io();
+    return table_view{dtab_, w.d, w.n};
+  }
+  // Compute enqueued from here on waits for the pending host transfers
+  // (uploads it must read, downloads of fields it may overwrite).
+  void flush_io() const {
+    ++compute_epoch_;  // called before every compute enqueue: the table may change
+    for (cudaEvent_t e : io_pending_) SF_CK(cudaStreamWaitEvent(st_, e, 0));
+    io_pending_.clear();
+  }
 
   void ctl(int op, double arg = 0.0, int f = 0, int a = 0, int b = 0, int predicated = 0) {
+    flush_io();
     launch_ctl(dtab_, dctl_, dflag_, op, arg, f, a, b, consts_, predicated, st_);
     ++launches_;
   }
@@ -2097,6 +2171,18 @@ int sf_sim_scatter_block(sf_sim* s, const char* field, int worker, const double*
     s->s->block_io(s->s->field_id(field), worker, const_cast<double*>(host), n, true);
   });
 }
+int sf_sim_gather_block_async(sf_sim* s, const char* field, int worker, double* host, int64_t n) {
+  return guarded([&] {
+    need(s, "sim");
+    s->s->block_io(s->s->field_id(field), worker, host, n, false, true);
+  });
+}
+int sf_sim_scatter_block_async(sf_sim* s, const char* field, int worker, const double* host, int64_t n) {
+  return guarded([&] {
+    need(s, "sim");
+    s->s->block_io(s->s->field_id(field), worker, const_cast<double*>(host), n, true, true);
+  });
+}
 int sf_sim_world(const sf_sim* s) { return s ? s->s->world() : 0; }
 
 void sf_sim_options_default(sf_sim_options* o) {
@@ -2344,7 +2430,12 @@ int sf_sim_ghosts_valid(sf_sim* s, const char* field) {
   guarded([&] { v = SIM(s).ghosts_valid(field) ? 1 : 0; });
   return v;
 }
-int sf_sim_synchronize(sf_sim* s) { return guarded([&] { SIM(s).sync(); }); }
+int sf_sim_synchronize(sf_sim* s) {
+  return guarded([&] {
+    SIM(s).sync();
+    SIM(s).io_sync();
+  });
+}
 void* sf_sim_stream(sf_sim* s) { return s ? (void*)s->s->stream() : nullptr; }
 int64_t sf_sim_launch_count(sf_sim* s, int reset) { return s ? s->s->launch_count(reset != 0) : 0; }
 int sf_sim_set_kernel_timing(sf_sim* s, int enable) {

@@ -289,24 +289,35 @@ class Simulation:
                       tuple(bool(x) for x in self.cfg.periodic))
         return d.size(self.rank if worker is None else worker)
 
-    def gather_block(self, name: str, worker: int | None = None, out=None):
+    def gather_block(self, name: str, worker: int | None = None, out=None, wait: bool = True):
+        """Owned block -> dense host array. ``wait=False`` queues the download
+        (``out`` must be pinned, e.g. a pinned torch tensor) and returns; call
+        ``synchronize()`` before reading it."""
         w = self.rank if worker is None else worker
         if out is None:
+            if not wait:
+                raise ValueError("an asynchronous gather needs a pinned `out` buffer")
             nx, ny, nz = self.block_shape(w)
             out = np.empty((nz, ny, nx), dtype=np.float64)
         ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
         n = out.numel() if hasattr(out, "numel") else out.size
-        L.check(self._lib.sf_sim_gather_block(self._h, name.encode(), int(w), C.c_void_p(ptr), n))
+        fn = self._lib.sf_sim_gather_block if wait else self._lib.sf_sim_gather_block_async
+        L.check(fn(self._h, name.encode(), int(w), C.c_void_p(ptr), n))
         return out
 
-    def scatter_block(self, name: str, data, worker: int | None = None):
+    def scatter_block(self, name: str, data, worker: int | None = None, wait: bool = True):
+        """Dense host array -> owned block. ``wait=False`` queues the upload
+        (``data`` must be pinned and unchanged until ``synchronize()``)."""
         w = self.rank if worker is None else worker
         if hasattr(data, "data_ptr"):
             ptr, n = data.data_ptr(), data.numel()
         else:
+            if not wait:
+                raise ValueError("an asynchronous scatter needs a pinned tensor")
             data = np.ascontiguousarray(data, dtype=np.float64)
             ptr, n = data.ctypes.data, data.size
-        L.check(self._lib.sf_sim_scatter_block(self._h, name.encode(), int(w), C.c_void_p(ptr), n))
+        fn = self._lib.sf_sim_scatter_block if wait else self._lib.sf_sim_scatter_block_async
+        L.check(fn(self._h, name.encode(), int(w), C.c_void_p(ptr), n))
 
     def checksum(self) -> str:
         v = C.c_uint64()

@@ -442,3 +442,36 @@ def test_temporal_pass_with_moving_walls_and_symmetry_faces_matches_the_other_pa
         if fused == 1:
             assert s.kernel_timing("sweep2")[1] > 0
     assert out[1] == out[3] == out[0]
+
+
+def test_async_block_transfers_keep_device_order():
+    # sf_sim_gather_block_async / sf_sim_scatter_block_async: an upload queued
+    # right after a download of the same field may not overtake it, and a step
+    # after async uploads sees them (bitwise the synchronous path)
+    import torch
+    names = ("vx", "vy", "vz", "p")
+    s = dev_cavity((40, 24, 20), symmetry_z=False)
+    s.init_cavity()
+    s.step()
+    want = {f: s.gather_block(f) for f in names}
+    n = want["vx"].size
+    pinned = {f: torch.empty(n, dtype=torch.float64).pin_memory() for f in names}
+    zeros = torch.zeros(n, dtype=torch.float64).pin_memory()
+    for f in names:
+        s.gather_block(f, out=pinned[f], wait=False)
+    s.scatter_block("vx", zeros, wait=False)
+    s.synchronize()
+    for f in names:
+        assert same(pinned[f].numpy().reshape(want[f].shape), want[f]), f
+    assert np.all(s.gather_block("vx") == 0.0)
+    # async uploads feeding a step == synchronous uploads feeding a step
+    t = dev_cavity((40, 24, 20), symmetry_z=False)
+    t.init_cavity()
+    for f in names:
+        s.scatter_block(f, torch.from_numpy(want[f].reshape(-1)).pin_memory(), wait=False)
+        t.scatter_block(f, want[f])
+    st_s, st_t = s.step(), t.step()
+    s.synchronize()
+    assert [st_s.dt, st_s.sweeps, st_s.residual] == [st_t.dt, st_t.sweeps, st_t.residual]
+    for f in FIELDS5:
+        assert same(s.gather(f), t.gather(f)), f
