@@ -362,6 +362,7 @@ class simulation {
     cudaEventDestroy(t0_);
     cudaEventDestroy(t1_);
     for (auto e : timers_) cudaEventDestroy(e);
+    drop_loop_graph();
     if (io_[0]) {
       for (int k = 0; k < 2; ++k) {
         cudaStreamSynchronize(io_[k]);
@@ -916,6 +917,7 @@ class simulation {
     }
     SF_CK(cudaMemcpy(dtab_->blk, htab_->blk, sizeof(htab_->blk), cudaMemcpyHostToDevice));
     phases_.clear();
+    drop_loop_graph();
   }
 
   // executor::physical_bc (executor.hpp:516-518): bc fills only, x then y then z
@@ -1227,6 +1229,48 @@ class simulation {
     check_finite_or_throw();
   }
 
+  // Also re-arms one batched call, which builds any work sets and exchange
+  // phases the capture will need (they allocate, which a capture may not).
+  void drop_loop_graph() {
+    if (loop_exec_) cudaGraphExecDestroy(loop_exec_);
+    loop_exec_ = nullptr;
+    loop_mode_ = -1;
+    pressure_calls_ = 0;
+  }
+  // The whole pressure loop without the host: a conditional WHILE node runs
+  // the body (kUnits units of the device-predicated loop) until the last
+  // unit's finalize sets ctl->done. The body is captured from the same
+  // enqueue code as the batched path, so both issue identical kernels.
+  void build_loop_graph(int mode) {
+    constexpr int kUnits = 2;
+    drop_loop_graph();
+    flush_io();  // no pending transfer events may be waited on inside the capture
+    cudaGraph_t g = nullptr;
+    SF_CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    SF_CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    SF_CK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    SF_CK(cudaStreamBeginCaptureToGraph(st_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    const i64 l0 = launches_;
+    for (int q = 0; q < kUnits; ++q) enqueue_sweep_unit();
+    launch_loop_cond(h, dctl_, st_);
+    cudaGraph_t cap = nullptr;
+    SF_CK(cudaStreamEndCapture(st_, &cap));
+    SF_CK(cudaGraphInstantiate(&loop_exec_, g, 0));
+    SF_CK(cudaGraphDestroy(g));
+    loop_units_launches_ = launches_ - l0;
+    launches_ = l0;
+    loop_mode_ = mode;
+  }
+  i64 loop_units_launches_ = 0;
+
   std::pair<int, double> pressure_iteration_device() {
     refresh({SF_VX, SF_VY, SF_VZ});
     const work_set& wd = items_for(SF_REGION_ALL, {1, 0, 1, 0, 1, 0}, zc_plain_);
@@ -1236,6 +1280,19 @@ class simulation {
     if (opt_.fused) refresh({SF_DIVU});
     ctl(CTL_BEGIN_ITERATION);
     const int maxs = std::max(1, cfg_.max_sweeps);
+    const bool graph = graph_env_ && !dist_ && !timing_ && pressure_calls_++ > 0;
+    if (graph) {
+      const int mode = opt_.fused | (temporal() ? 16 : 0);
+      if (!loop_exec_ || loop_mode_ != mode) build_loop_graph(mode);
+      SF_CK(cudaGraphLaunch(loop_exec_, st_));
+      sync();
+      const int sweeps = hflag_->sweeps;
+      // launches the graph ran: bodies of kUnits units, one per 2*kUnits (or kUnits) sweeps
+      const int per_body = temporal() ? 4 : 2;
+      launches_ += (i64)((sweeps + per_body - 1) / per_body) * (loop_units_launches_ + 1);
+      if (sweeps > 0) est_sweeps_ = sweeps;
+      return finish_pressure_iteration();
+    }
     int issued = 0;
     int batch = std::max(1, std::min(maxs, est_sweeps_));
     const bool two = temporal();
@@ -1276,6 +1333,12 @@ class simulation {
         ++(two ? pass_launches_ : sweep_launches_);
       }
     }
+    (void)residual;
+    return finish_pressure_iteration();
+  }
+  std::pair<int, double> finish_pressure_iteration() {
+    const int sweeps = hflag_->sweeps;
+    const double residual = hflag_->residual;
     if (opt_.fused) refresh({SF_VX, SF_VY, SF_VZ});
     // ghost state as the reference leaves it (executor.hpp:769-779)
     ghosts_ok_["p"] = false;
@@ -1421,6 +1484,12 @@ class simulation {
   long steps_ = 0;
   sf_step_stats last_{0.0, 0, 0.0};
   int est_sweeps_ = 8;
+  // pressure loop as one CUDA graph: a while node whose body is kUnits sweep
+  // units and the condition kernel (single process, no per-launch timing)
+  cudaGraphExec_t loop_exec_ = nullptr;
+  int loop_mode_ = -1;  // fused mode | temporal << 4 the graph was built for
+  long pressure_calls_ = 0;
+  const bool graph_env_ = getenv("SF_NO_GRAPH") == nullptr;
   i64 launches_ = 0;
   bool timing_ = false;
   double sweep_ms_ = 0.0, pass_ms_ = 0.0;

@@ -864,6 +864,15 @@ __global__ void k_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, i
   }
 }
 
+// Condition of the pressure loop's CUDA-graph while node: run another body
+// iteration while the device predicate says the loop goes on.
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const sf_dev_ctl* ctl) {
+  cudaGraphSetConditional(h, *reinterpret_cast<const volatile int*>(&ctl->done) ? 0u : 1u);
+}
+void launch_loop_cond(cudaGraphConditionalHandle h, const sf_dev_ctl* ctl, cudaStream_t st) {
+  k_loop_cond<<<1, 1, 0, st>>>(h, ctl);
+}
+
 void launch_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, int op, double arg,
                 int f, int a, int b, const sf_consts& c, int predicated, cudaStream_t st) {
   k_ctl<<<1, 1, 0, st>>>(tab, ctl, hflag, op, arg, f, a, b, c, predicated);

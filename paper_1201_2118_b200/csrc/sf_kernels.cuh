@@ -76,6 +76,8 @@ enum ctl_op {
   CTL_RESET_CLOCK = 8,       // colour = 0, abort cleared (cfd.hpp:733-738)
   CTL_FINISH_FUSED = 9,      // fused half-sweep finalise after a cross-rank residual allreduce
 };
+// sets the pressure-loop graph's while condition to !ctl->done
+void launch_loop_cond(cudaGraphConditionalHandle h, const sf_dev_ctl* ctl, cudaStream_t st);
 void launch_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, int op, double arg,
                 int f, int a, int b, const sf_consts& c, int predicated, cudaStream_t st);
 void launch_copy_box(const double* src, long long s_base, long long s_sx, long long s_sy,
