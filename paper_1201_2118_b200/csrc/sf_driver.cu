@@ -1259,8 +1259,10 @@ class simulation {
     cudaGraph_t body = np.conditional.phGraph_out[0];
     SF_CK(cudaStreamBeginCaptureToGraph(st_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     const i64 l0 = launches_;
+    capturing_ = true;
     for (int q = 0; q < kUnits; ++q) enqueue_sweep_unit();
     launch_loop_cond(h, dctl_, st_);
+    capturing_ = false;
     cudaGraph_t cap = nullptr;
     SF_CK(cudaStreamEndCapture(st_, &cap));
     SF_CK(cudaGraphInstantiate(&loop_exec_, g, 0));
@@ -1270,6 +1272,10 @@ class simulation {
     loop_mode_ = mode;
   }
   i64 loop_units_launches_ = 0;
+  // Inside the captured loop no kernel writes the host-mapped flag (a
+  // system-scope fence per sweep); CTL_PUBLISH writes it once afterwards.
+  bool capturing_ = false;
+  sf_host_flag* loop_flag() const { return capturing_ ? nullptr : dflag_; }
 
   std::pair<int, double> pressure_iteration_device() {
     refresh({SF_VX, SF_VY, SF_VZ});
@@ -1285,6 +1291,7 @@ class simulation {
       const int mode = opt_.fused | (temporal() ? 16 : 0);
       if (!loop_exec_ || loop_mode_ != mode) build_loop_graph(mode);
       SF_CK(cudaGraphLaunch(loop_exec_, st_));
+      ctl(CTL_PUBLISH);
       sync();
       const int sweeps = hflag_->sweeps;
       // launches the graph ran: bodies of kUnits units, one per 2*kUnits (or kUnits) sweeps
@@ -1351,12 +1358,15 @@ class simulation {
     return pressure_iteration_device();
   }
 
+  // The NaN guard after UPDATE_VELOCITY (cfd.hpp:278-281) is read once the
+  // pressure loop has synchronised: the loop is predicated off on the device
+  // after a non-finite velocity, so no host round trip sits between the two.
   sf_step_stats step() {
     compute_dt_device();
     provisional_device();
+    auto r = pressure_iteration_device();
     check_finite_or_throw();
     const double dt = hflag_->dt;
-    auto r = pressure_iteration_device();
     refresh({SF_P});
     time_ += dt;
     ++steps_;
@@ -1380,12 +1390,25 @@ class simulation {
     ghosts_ok_["divu"] = false;
     return read_acc(7);
   }
+  // cfd.hpp:347-355: max over vx, vy, vz of max|front - back|. One launch
+  // reduces all three into acc[4..6] (exact bit-pattern maxima), combined on
+  // the host in the reference's order.
   double steady_delta() {
-    double d = reduce(SF_VX, SF_MAX_ABS_DIFF);
-    const double dy = reduce(SF_VY, SF_MAX_ABS_DIFF);
-    d = d < dy ? dy : d;  // std::max
-    const double dz = reduce(SF_VZ, SF_MAX_ABS_DIFF);
-    d = d < dz ? dz : d;
+    for (int f : {SF_VX, SF_VY, SF_VZ})
+      if (!has_back(f))
+        throw error(SF_ERR_GRID, std::string("field '") + fname_[f] + "' has no back buffer to diff against");
+    ctl(CTL_CLEAR_ACC);
+    const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_plain_);
+    const int fl[3] = {SF_VX, SF_VY, SF_VZ};
+    launch_reduce_max(tview(ws), ws.nctas, zc_plain_, fl, 3, 1, &dctl_->acc[4], st_);
+    ++launches_;
+    check_launch();
+    allreduce_max(&dctl_->acc[4], 3);
+    double m[3];
+    read_accs(4, 3, m);
+    double d = m[0];
+    d = d < m[1] ? m[1] : d;  // std::max
+    d = d < m[2] ? m[2] : d;
     return d;
   }
   double kinetic_energy() {
@@ -1732,7 +1755,7 @@ class simulation {
 
   void ctl(int op, double arg = 0.0, int f = 0, int a = 0, int b = 0, int predicated = 0) {
     flush_io();
-    launch_ctl(dtab_, dctl_, dflag_, op, arg, f, a, b, consts_, predicated, st_);
+    launch_ctl(dtab_, dctl_, loop_flag(), op, arg, f, a, b, consts_, predicated, st_);
     ++launches_;
   }
 
@@ -1740,6 +1763,18 @@ class simulation {
     for (int f : {SF_VX, SF_VY, SF_VZ}) ctl(CTL_SWAP, 0.0, f, FRONT, BACK);
   }
 
+  void read_accs(int slot, int n, double* out) {
+    sync();
+    unsigned long long bits[8];
+    SF_CK(cudaMemcpy(bits, &dctl_->acc[slot], sizeof(bits[0]) * (size_t)n, cudaMemcpyDeviceToHost));
+    for (int q = 0; q < n; ++q) {
+      if (bits[q] > 0x7ff0000000000000ull) {
+        out[q] = std::nan("");
+      } else {
+        std::memcpy(&out[q], &bits[q], sizeof(double));
+      }
+    }
+  }
   double read_acc(int slot) {
     sync();
     unsigned long long bits = 0;
@@ -1956,14 +1991,14 @@ class simulation {
     }
     const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, kTX, kTY);
     if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
-    launch_sweep2(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, maps2_, st_);
+    launch_sweep2(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps2_, st_);
     if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
     ++iter_launch_;
     // predicated redo of the first sweep when the pass stopped after it
     int ftx, fty;
     sweep_tile_shape(&ftx, &fty);
     const work_set& wr = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, ftx, fty);
-    launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, dflag_, maps_, 2, st_);
+    launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, 2, st_);
     launches_ += 2;
     check_launch();
     return 2;
@@ -1979,9 +2014,9 @@ class simulation {
       // ranks the residual first needs the max over ranks
       const int fin = dist_ ? 0 : 1;
       if (tma_sweep())
-        launch_sweep_div_tma(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, maps_, fin, st_);
+        launch_sweep_div_tma(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, fin, st_);
       else
-        launch_sweep_div(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, dflag_, fin, st_);
+        launch_sweep_div(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, loop_flag(), fin, st_);
       ++launches_;
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
       ++iter_launch_;

@@ -847,6 +847,15 @@ __global__ void k_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, i
       }
       break;
     }
+    case CTL_PUBLISH:
+      if (hflag) {
+        hflag->sweeps = ctl->sweeps;
+        hflag->residual = ctl->residual;
+        hflag->done = ctl->done;
+        hflag->color = ctl->color;
+        __threadfence_system();
+      }
+      break;
     case CTL_CLEAR_ACC:
       for (int a = 0; a < 8; ++a) ctl->acc[a] = 0ull;
       ctl->ctas_done = 0u;

@@ -75,6 +75,7 @@ enum ctl_op {
   CTL_SWAP = 7,              // swap slots (a, b) of field f in every block
   CTL_RESET_CLOCK = 8,       // colour = 0, abort cleared (cfd.hpp:733-738)
   CTL_FINISH_FUSED = 9,      // fused half-sweep finalise after a cross-rank residual allreduce
+  CTL_PUBLISH = 10,          // loop state -> host-mapped flag (after the graph-captured loop)
 };
 // sets the pressure-loop graph's while condition to !ctl->done
 void launch_loop_cond(cudaGraphConditionalHandle h, const sf_dev_ctl* ctl, cudaStream_t st);
