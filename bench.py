@@ -288,9 +288,14 @@ def run_ours(args):
 
     peak, peak_src = measured_peaks()
     avg_launch_s = (k_ms / k_n) / 1e3 if k_n else None
-    achieved = (BYTES_PER_HALF_SWEEP * cells / avg_launch_s / 1e9) if avg_launch_s else None
+    # 80 algorithmic bytes per cell per half-sweep; a temporal
+    # pass processes two half-sweeps per launch (its DRAM traffic is half of
+    # that: the first sweep's state never leaves the SM, see dram_* below)
+    units = 2 if kname == "sweep2" else 1
+    algo_launch = BYTES_PER_HALF_SWEEP * units * cells
+    achieved = (algo_launch / avg_launch_s / 1e9) if avg_launch_s else None
     traffic, _ = ncu_traffic(kname)
-    step_bytes = (BYTES_UV + BYTES_DIV + BYTES_PER_HALF_SWEEP * S // (2 if kname == "sweep2" else 1)) * cells
+    step_bytes = (BYTES_UV + BYTES_DIV + BYTES_PER_HALF_SWEEP * S) * cells
     roofline = {
         "bound": "hbm",
         "kernel": ("k_sweep2 (temporal pass: two fused half-sweeps per launch)" if kname == "sweep2"
@@ -298,9 +303,13 @@ def run_ours(args):
         "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4) if achieved else None,
         "traffic": traffic,
-        "algorithmic_bytes_per_launch": BYTES_PER_HALF_SWEEP * cells,
+        "half_sweeps_per_launch": units,
+        "algorithmic_bytes_per_launch": algo_launch,
         "avg_launch_ms": round(k_ms / k_n, 4) if k_n else None, "launches_timed": k_n,
         "peak_source": peak_src,
+        # bytes the kernel actually moves (ncu DRAM traffic per launch) over the same time
+        "dram_gbs": round(traffic / avg_launch_s / 1e9, 1) if (traffic and avg_launch_s) else None,
+        "dram_frac": round(traffic / avg_launch_s / 1e9 / peak, 4) if (traffic and avg_launch_s) else None,
         "step_achieved_gbs": round(step_bytes / (ms_per_step / 1e3) / 1e9, 1),
         "step_frac": round(step_bytes / (ms_per_step / 1e3) / 1e9 / peak, 4),
     }
