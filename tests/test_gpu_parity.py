@@ -475,3 +475,32 @@ def test_async_block_transfers_keep_device_order():
     assert [st_s.dt, st_s.sweeps, st_s.residual] == [st_t.dt, st_t.sweeps, st_t.residual]
     for f in FIELDS5:
         assert same(s.gather(f), t.gather(f)), f
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_temporal_pass_random_configurations_match_single_sweeps(seed):
+    # random extents (partial tiles in x, y and z chunks), face kinds, wall
+    # velocities, sweep caps and tolerances: temporal pass == single sweeps
+    rng = np.random.default_rng(100 + seed)
+    ext = (int(rng.integers(20, 90)), int(rng.integers(12, 45)), int(rng.integers(3, 80)))
+    kinds = ["wall", "symmetry"]
+    faces = [(a, sd, kinds[int(rng.integers(0, 2))], tuple(rng.uniform(-0.3, 0.3, 3))) for a in range(3) for sd in range(2)]
+    tol = float(rng.choice([1e-30, 1e-3, 1e-4]))
+    maxs = int(rng.integers(1, 30))
+    omega = float(rng.uniform(1.0, 1.95))
+    vel = {f: rng.uniform(-0.5, 0.5, size=ext[::-1]) for f in ("vx", "vy", "vz")}
+    out = {}
+    for fused in (1, 3):
+        cfg = sfb.SolverConfig(extents=ext, tolerance=tol, max_sweeps=maxs, symmetry_z=False, omega=omega)
+        s = sfb.Simulation(cfg, sfb.FluidParams(viscosity=0.02, lid_speed=0.0), fused=fused)
+        s.init_cavity()
+        for a, sd, k, v in faces:
+            s.set_face_bc(a, sd, k, v)
+        for f, arr in vel.items():
+            s.scatter(f, arr)
+        s.set_kernel_timing(True)
+        st = [s.step() for _ in range(3)]
+        out[fused] = ([[x.dt, x.sweeps, x.residual] for x in st], s.checksum(), s.pending_color)
+        if fused == 1:
+            assert s.kernel_timing("sweep2")[1] > 0, ext
+    assert out[1] == out[3], (ext, tol, maxs)
