@@ -230,13 +230,16 @@ def run_ours(args):
         uid = [sfb.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ext = weak_extents(n, world)
-        d = sfb.decompose(ext, world, 1)
+        # the temporal pass reads 2-deep halos across processor faces
+        ghost = 2 if fused == 1 else 1
+        d = sfb.decompose(ext, world, ghost)
         assert all(d.size(w) == (n, n, n) for w in range(world)), d
         cfg = cavity_cfg(sfb, n, S)
         cfg.extents = ext
         sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), device=dev, fused=fused, rank=rank, world=world,
-                             nccl_id=uid[0])
+                             nccl_id=uid[0], ghost=ghost)
     else:
+        ghost = 1
         cfg = cavity_cfg(sfb, n, S)
         sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=1, device=dev, fused=fused)
     cells = n * n * n          # per rank
@@ -373,7 +376,7 @@ def run_ours(args):
         "config": {"workload": (f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)"
                                 if world == 1 else
                                 f"3D lid-driven cavity, {n}^3 per GPU weak scaling, global {list(cfg.extents)} block-decomposed over {world} B200 with NCCL ghost exchange (BASELINE.json configs[2]), {S} half-sweeps per step"),
-                   "grid": list(cfg.extents), "ghost": 1, "sweeps_per_step": S,
+                   "grid": list(cfg.extents), "ghost": ghost, "sweeps_per_step": S,
                    "parallelism": "1 GPU" if world == 1 else f"{world} ranks, block decomposition (grid::decompose), NCCL halo + allreduce",
                    "path": {"tma": "TMA pipeline, temporal pass (two half-sweeps per launch)" if kname == "sweep2"
                             else "fused half-sweep, TMA pipeline",

@@ -1645,9 +1645,9 @@ class simulation {
       for (int f = 0; f < SF_NFIELDS; ++f) {
         const bool velocity = f <= SF_VZ;
         for (int s = 0; s < kSlots; ++s) {
-          // p gets an ALT buffer where the temporal pass can run (sf_sweep2.cu)
+          // p gets an ALT buffer for the temporal pass (sf_sweep2.cu)
           const bool need = s == FRONT || (velocity && (s == BACK || s == ALT)) ||
-                            (f == SF_DIVU && s == ALT) || (f == SF_P && s == ALT && nloc_ == 1 && !dist_);
+                            (f == SF_DIVU && s == ALT) || (f == SF_P && s == ALT);
           if (need) alloc_slot(b, f, s);
         }
       }
@@ -1669,20 +1669,21 @@ class simulation {
         SF_CK(cudaMemcpy(maps_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
       }
     }
-    // descriptors of the temporal pass (halo'd boxes, block 0 only)
-    if (maps_ && nloc_ == 1 && !dist_) {
+    // descriptors of the temporal pass (halo'd boxes)
+    if (maps_) {
       std::vector<unsigned char> hm(sweep2_maps_bytes(), 0);
       bool ok = true;
-      for (int f : {SF_VX, SF_VY, SF_VZ, SF_P, SF_DIVU})
-        for (int s = 0; s < kSlots && ok; ++s) {
-          double* p = htab_->ptr[0][f][s];
-          if (!p) continue;
-          const sf_layout& L = lay_[0];
-          int bw, bh;
-          sweep2_box(f, &bw, &bh);
-          ok = bw <= L.sx && bh <= L.sy &&
-               encode_box_map(hm.data() + sweep2_map_offset(f, s), p, L.sx, L.sy, L.sz, bw, bh) == 0;
-        }
+      for (int b = 0; b < nloc_ && ok; ++b)
+        for (int f : {SF_VX, SF_VY, SF_VZ, SF_P, SF_DIVU})
+          for (int s = 0; s < kSlots && ok; ++s) {
+            double* p = htab_->ptr[b][f][s];
+            if (!p) continue;
+            const sf_layout& L = lay_[b];
+            int bw, bh;
+            sweep2_box(f, &bw, &bh);
+            ok = bw <= L.sx && bh <= L.sy &&
+                 encode_box_map(hm.data() + sweep2_map_offset(b, f, s), p, L.sx, L.sy, L.sz, bw, bh) == 0;
+          }
       if (ok) {
         maps2_ = dalloc(hm.size());
         SF_CK(cudaMemcpy(maps2_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
@@ -1971,15 +1972,39 @@ class simulation {
     SF_NC(nccl()->AllReduce(dev, dev, (size_t)n, kNcclUint64, kNcclMax, comm_, st_));
   }
 
-  // The temporal pass (two half-sweeps per launch, sf_sweep2.cu) applies to one
-  // grid component per device with wall / symmetry faces only, fused = 1.
+  // The temporal pass (two half-sweeps per launch, sf_sweep2.cu) applies with
+  // fused = 1 when every face of every local grid component is a wall, a
+  // symmetry plane or a processor face, and the ghost shell is 2 deep where
+  // there are processor faces (the pass reads 2-deep halos of the old state).
   bool temporal() const {
-    if (!maps2_ || !temporal_env_ || opt_.fused != 1 || nloc_ != 1 || dist_) return false;
-    for (int fi = 0; fi < 6; ++fi) {
-      const int k = htab_->blk[0].face[fi];
-      if (k != FACE_WALL && k != FACE_SYM) return false;
-    }
-    return true;
+    if (!maps2_ || !temporal_env_ || opt_.fused != 1) return false;
+    bool proc = false;
+    for (int b = 0; b < nloc_; ++b)
+      for (int fi = 0; fi < 6; ++fi) {
+        const int k = htab_->blk[b].face[fi];
+        if (k == FACE_PROC)
+          proc = true;
+        else if (k != FACE_WALL && k != FACE_SYM)
+          return false;
+      }
+    return !proc || opt_.ghost >= 2;
+  }
+  bool has_proc_faces() const {
+    for (int b = 0; b < nloc_; ++b)
+      for (int fi = 0; fi < 6; ++fi)
+        if (htab_->blk[b].face[fi] == FACE_PROC) return true;
+    return false;
+  }
+  // wall-normal velocities pinned on the domain's faces (exchange.hpp:288-316)
+  sweep2_pins wall_pins() const {
+    sweep2_pins p{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (bc_[1].kind == SF_BC_WALL) p.u = bc_[1].velocity[0];
+    if (bc_[3].kind == SF_BC_WALL) p.v = bc_[3].velocity[1];
+    if (bc_[5].kind == SF_BC_WALL) p.w = bc_[5].velocity[2];
+    if (bc_[0].kind == SF_BC_WALL) p.ul = bc_[0].velocity[0];
+    if (bc_[2].kind == SF_BC_WALL) p.vl = bc_[2].velocity[1];
+    if (bc_[4].kind == SF_BC_WALL) p.wl = bc_[4].velocity[2];
+    return p;
   }
   bool tma_sweep() const { return maps_ && (opt_.fused == 1 || opt_.fused == 3); }
 
@@ -1991,9 +2016,20 @@ class simulation {
     }
     const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, kTX, kTY);
     if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
-    launch_sweep2(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps2_, st_);
+    const int fin = dist_ ? 0 : 1;
+    launch_sweep2(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_);
     if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
     ++iter_launch_;
+    if (!fin) {
+      allreduce_max(&dctl_->acc[0], 2);
+      ctl(CTL_FINISH_PASS, 0.0, 0, 0, 0, 1);
+    }
+    // processor faces: the next pass reads 2-deep halos of the new state
+    // (vx, vy, vz, divu; p is read on owned cells only)
+    if (has_proc_faces()) {
+      const unsigned mask = (1u << SF_VX) | (1u << SF_VY) | (1u << SF_VZ) | (1u << SF_DIVU);
+      for (int axis = 0; axis < 3; ++axis) run_phase(phase_for(mask, axis, SF_SCOPE_ALL, true), true);
+    }
     // predicated redo of the first sweep when the pass stopped after it
     int ftx, fty;
     sweep_tile_shape(&ftx, &fty);

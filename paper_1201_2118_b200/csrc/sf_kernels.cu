@@ -847,6 +847,40 @@ __global__ void k_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, i
       }
       break;
     }
+    case CTL_FINISH_PASS: {  // the temporal pass's in-kernel finalize (sf_sweep2.cu), across ranks
+      const double r1 = bits_to_max(ctl->acc[0]), r2 = bits_to_max(ctl->acc[1]);
+      ctl->acc[0] = 0ull;
+      ctl->acc[1] = 0ull;
+      const int sw = ctl->sweeps;
+      if (!((r1 > ctl->tolerance) && (sw + 1 < ctl->max_sweeps))) {
+        ctl->sweeps = sw + 1;
+        ctl->residual = r1;
+        ctl->color ^= 1;
+        ctl->done = 1;
+        ctl->redo = 1;
+      } else {
+        ctl->sweeps = sw + 2;
+        ctl->residual = r2;
+        ctl->done = ((r2 > ctl->tolerance) && (sw + 2 < ctl->max_sweeps)) ? 0 : 1;
+        for (int b = 0; b < tab->nblocks; ++b)
+          for (int q = 0; q < 5; ++q) {
+            double* tmp = tab->ptr[b][q][FRONT];
+            tab->ptr[b][q][FRONT] = tab->ptr[b][q][ALT];
+            tab->ptr[b][q][ALT] = tmp;
+            const unsigned char ti = tab->bidx[b][q][FRONT];
+            tab->bidx[b][q][FRONT] = tab->bidx[b][q][ALT];
+            tab->bidx[b][q][ALT] = ti;
+          }
+      }
+      if (hflag) {
+        hflag->sweeps = ctl->sweeps;
+        hflag->residual = ctl->residual;
+        hflag->done = ctl->done;
+        hflag->color = ctl->color;
+        __threadfence_system();
+      }
+      break;
+    }
     case CTL_PUBLISH:
       if (hflag) {
         hflag->sweeps = ctl->sweeps;

@@ -46,12 +46,19 @@ void launch_sweep_div(const table_view& vw, int nctas, int zc, const sf_consts& 
 void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_consts& c,
                           sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,
                           cudaStream_t st);
-// Temporal pass: two half-sweeps per launch (sf_sweep2.cu); single block with
-// wall / symmetry faces only.  maps = device table of sweep2 descriptors.
+// Temporal pass: two half-sweeps per launch (sf_sweep2.cu). Blocks whose
+// faces are walls, symmetry planes or processor faces (ghost width >= 2 when
+// there are processor faces); maps = device table of sweep2 descriptors.
+// fin = 1: the last CTA finalises; 0: the caller allreduces acc[0..1] across
+// ranks and runs CTL_FINISH_PASS. pins: wall-normal velocities of the
+// domain's high walls (u, v, w) and low walls (ul, vl, wl); 0 for symmetry.
+struct sweep2_pins {
+  double u, v, w, ul, vl, wl;
+};
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                   sf_host_flag* hflag, const void* maps, cudaStream_t st);
+                   sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st);
 size_t sweep2_maps_bytes();
-size_t sweep2_map_offset(int f, int s);
+size_t sweep2_map_offset(int b, int f, int s);
 void sweep2_box(int field, int* bw, int* bh);
 int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field);
 size_t sweep_maps_bytes();
@@ -76,6 +83,7 @@ enum ctl_op {
   CTL_RESET_CLOCK = 8,       // colour = 0, abort cleared (cfd.hpp:733-738)
   CTL_FINISH_FUSED = 9,      // fused half-sweep finalise after a cross-rank residual allreduce
   CTL_PUBLISH = 10,          // loop state -> host-mapped flag (after the graph-captured loop)
+  CTL_FINISH_PASS = 11,      // temporal pass finalise after the cross-rank allreduce of acc[0..1]
 };
 // sets the pressure-loop graph's while condition to !ctl->done
 void launch_loop_cond(cudaGraphConditionalHandle h, const sf_dev_ctl* ctl, cudaStream_t st);

@@ -86,14 +86,16 @@ enum { U1 = 0, V1 = 1, W1 = 2, P1 = 3, D1 = 4 };
 
 constexpr int smem_bytes(int nin) { return nin * IN_BYTES + (4 * 4 + 3) * EN * 8; }
 
-struct maps2_t {  // [field][physical buffer]
-  CUtensorMap m[SF_NFIELDS][kSlots];
+struct maps2_t {  // [block][field][physical buffer]
+  CUtensorMap m[kMaxBlocks][SF_NFIELDS][kSlots];
 };
 
 }  // namespace
 
 size_t sweep2_maps_bytes() { return sizeof(maps2_t); }
-size_t sweep2_map_offset(int f, int s) { return sizeof(CUtensorMap) * ((size_t)f * kSlots + s); }
+size_t sweep2_map_offset(int b, int f, int s) {
+  return sizeof(CUtensorMap) * (((size_t)b * SF_NFIELDS + f) * kSlots + s);
+}
 void sweep2_box(int field, int* bw, int* bh) {
   *bw = IW;
   *bh = field == SF_DIVU ? IDH : IFH;
@@ -112,7 +114,7 @@ template <int NIN, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
     k_sweep2(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc,
              sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag, unsigned int total_ctas,
-             const maps2_t* __restrict__ maps, int pf) {
+             const maps2_t* __restrict__ maps, int pf, int finalize, sweep2_pins pins) {
   static_assert(NIN >= 3, "three S0 planes are read or in flight per phase");
   if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
   extern __shared__ __align__(128) unsigned char sm[];
@@ -128,15 +130,19 @@ __global__ void __launch_bounds__(NT, MINB)
   const int k0 = (int)wk.lo[2] + tiz * zc;
   const int k1 = (int)min((long long)k0 + zc, wk.hi[2]);
   const int nplanes = k1 - k0;
-  const sf_dev_block& B = tab->blk[0];
+  const int b = wk.blk;
+  const sf_dev_block& B = tab->blk[b];
   const int n0 = (int)B.n[0], n1 = (int)B.n[1], n2 = (int)B.n[2];
+  // global extents and this block's origin: cells across a processor face
+  // (another block's, valid in the ghost shell, g >= 2) are computed like
+  // owned ones; cells outside the domain are physical ghosts
+  const int N0 = (int)s.N[0], N1 = (int)s.N[1], N2 = (int)s.N[2];
+  const int lo0 = (int)B.lo[0], lo1 = (int)B.lo[1], lo2 = (int)B.lo[2];
   const long long sx = B.sx, sxy = B.sx * B.sy;
   const double beta = ctl->beta, dt = ctl->dt;
   const int colA = ctl->color, colB = colA ^ 1;
   const double cu = dt * s.ix, cv = dt * s.iy, cw = dt * s.iz;
-  const double pin_u = B.face[1] == FACE_WALL ? B.fvel[1][0] : 0.0;
-  const double pin_v = B.face[3] == FACE_WALL ? B.fvel[3][1] : 0.0;
-  const double pin_w = B.face[5] == FACE_WALL ? B.fvel[5][2] : 0.0;
+  const double pin_u = pins.u, pin_v = pins.v, pin_w = pins.w;  // global high-wall normals
   const long long nm0 = s.nm1[0], nm1 = s.nm1[1], nm2 = s.nm1[2];
   auto bin = [](int per, long long gg, long long nm) { return per | ((gg > 0) & (gg < nm)); };
   auto bnx = [](int per, long long gg, long long nm) { return per | (gg + 1 < nm); };
@@ -157,11 +163,11 @@ __global__ void __launch_bounds__(NT, MINB)
   // ---- S0 input ring ---------------------------------------------------------
   const int xo = (int)(B.base % B.sx), g = B.g;
   const int xs = xo + i0 - 2, ys = g + j0 - 2, zs = g + k0 - 2;
-  const CUtensorMap* mD = &maps->m[SF_DIVU][tab->bidx[0][SF_DIVU][FRONT]];
-  const CUtensorMap* mU = &maps->m[SF_VX][tab->bidx[0][SF_VX][FRONT]];
-  const CUtensorMap* mV = &maps->m[SF_VY][tab->bidx[0][SF_VY][FRONT]];
-  const CUtensorMap* mW = &maps->m[SF_VZ][tab->bidx[0][SF_VZ][FRONT]];
-  const CUtensorMap* mP = &maps->m[SF_P][tab->bidx[0][SF_P][FRONT]];
+  const CUtensorMap* mD = &maps->m[b][SF_DIVU][tab->bidx[b][SF_DIVU][FRONT]];
+  const CUtensorMap* mU = &maps->m[b][SF_VX][tab->bidx[b][SF_VX][FRONT]];
+  const CUtensorMap* mV = &maps->m[b][SF_VY][tab->bidx[b][SF_VY][FRONT]];
+  const CUtensorMap* mW = &maps->m[b][SF_VZ][tab->bidx[b][SF_VZ][FRONT]];
+  const CUtensorMap* mP = &maps->m[b][SF_P][tab->bidx[b][SF_P][FRONT]];
   const int nin = nplanes + 4;  // S0 planes k0-2 .. k1+1
   auto issue = [&](int q) {
     if (q >= nin) return;
@@ -224,8 +230,8 @@ __global__ void __launch_bounds__(NT, MINB)
       f_e[r] = e;
       f_ia[r] = ey * IW + ex;
       f_bt[r] = ((bx << 2) | (by << 1)) | (((bxp << 2) | (by << 1)) << 3) | (((bx << 2) | (byp << 1)) << 6) |
-                ((int)((gi + gj) & 1) << 9) | ((x >= 0 && x < n0 && y >= 0 && y < n1) << 10) |
-                ((x == n0 - 1) << 11) | ((y == n1 - 1) << 12);
+                ((int)((gi + gj) & 1) << 9) | ((gi >= 0 && gi < N0 && gj >= 0 && gj < N1) << 10) |
+                ((gi == N0 - 1) << 11) | ((gj == N1 - 1) << 12) | ((gi == -1) << 13) | ((gj == -1) << 14);
     }
     {
       const int e = r == 0 ? EN - 1 - tid : (has2d ? EN - 1 - NT - tid + 128 : EN - 1);
@@ -234,8 +240,8 @@ __global__ void __launch_bounds__(NT, MINB)
       // the +x / +y ghost (x = n0, y = n1) takes the wall mirror of the last
       // owned cell (exchange.hpp:438-449), evaluated with that cell's operands
       int dx = ex, dy = ey;
-      if (x >= n0) dx -= x - (n0 - 1);
-      if (y >= n1) dy -= y - (n1 - 1);
+      if (lo0 + x >= N0) dx -= lo0 + x - (N0 - 1);
+      if (lo1 + y >= N1) dy -= lo1 + y - (N1 - 1);
       d_e[r] = e;
       d_q[r] = dy * EW + dx;
       if (ex >= 1 && ey >= 1 && (r == 0 || has2d)) d_ok |= 1 << r;
@@ -246,11 +252,13 @@ __global__ void __launch_bounds__(NT, MINB)
   // no divu mirror; planes with z in [zf_lo, zf_hi] add the same for z. The
   // fast paths evaluate the identical IEEE operations in the identical order,
   // so they are bitwise the general paths restricted to such cells.
+  // (the tile must also lie wholly inside the block: the fast path has no
+  // per-thread guard)
   const bool fast_xy = B.lo[0] + i0 - 2 >= 1 && B.lo[0] + i0 + TX <= nm0 - 2 && B.lo[1] + j0 - 2 >= 1 &&
-                       B.lo[1] + j0 + TY <= nm1 - 2 && i0 + TX <= n0 - 2 && j0 + TY <= n1 - 2 &&
-                       !s.per[0] && !s.per[1];
+                       B.lo[1] + j0 + TY <= nm1 - 2 && !s.per[0] && !s.per[1] && i0 + TX <= (int)wk.hi[0] &&
+                       j0 + TY <= (int)wk.hi[1];
   const int zf_lo = s.per[2] ? 1 << 30 : (int)max(1ll, 1ll - B.lo[2]);
-  const int zf_hi = (int)min((long long)n2 - 3, nm2 - 2 - B.lo[2]);
+  const int zf_hi = (int)(nm2 - 2 - B.lo[2]);
   const double mbI = smb[7];
 
   // S1 fields of plane z from its S0 stage (st) and divu0 of plane z+1 (stn):
@@ -283,17 +291,20 @@ __global__ void __launch_bounds__(NT, MINB)
       }
       return;
     }
-    const bool zin = z >= 0 && z < n2;
+    const bool zin = lo2 + z >= 0 && lo2 + z < N2;
     const int bz = bin(s.per[2], gk, nm2), bzp = bnx(s.per[2], gk, nm2);
-    const bool pz = z == n2 - 1;
+    const bool pz = lo2 + z == N2 - 1, zlow = lo2 + z == -1;
 #pragma unroll
     for (int r = 0; r < NE; ++r) {
       if (r > 0 && !has2f) break;
       const int e = f_e[r], ia = f_ia[r], bt = f_bt[r];
       if (!(zin && ((bt >> 10) & 1))) {
-        S[u1 + e] = S[Ui + ia];
-        S[v1 + e] = S[Vi + ia];
-        S[w1 + e] = S[Wi + ia];
+        // outside the domain: the low-wall normals are the pins (a ghost
+        // corner next to a processor face may hold an older copy); the rest
+        // is carried over and never read
+        S[u1 + e] = ((bt >> 13) & 1) ? pins.ul : S[Ui + ia];
+        S[v1 + e] = ((bt >> 14) & 1) ? pins.vl : S[Vi + ia];
+        S[w1 + e] = zlow ? pins.wl : S[Wi + ia];
         S[p1 + e] = S[Pi + ia];
         continue;
       }
@@ -310,9 +321,10 @@ __global__ void __launch_bounds__(NT, MINB)
     }
   };
   // DIVERGENCE of S1 on plane z (cfd.hpp:605-608) from field slots fo (z) and
-  // fom (z-1) into divu1 slot d1; the top ghost plane mirrors plane n2-1 (dm).
+  // fom (z-1) into divu1 slot d1; the ghost plane above a top wall mirrors
+  // plane N2-1 (dm).
   auto s1_div = [&](int z, int fo, int fom, int d1, int dm) {
-    if (z >= n2) {
+    if (lo2 + z >= N2) {
 #pragma unroll
       for (int r = 0; r < NE; ++r) {
         if (r > 0 && !has2d) break;
@@ -352,11 +364,11 @@ __global__ void __launch_bounds__(NT, MINB)
   const int par_col = (int)((gi + gj) & 1);
   const int q0 = (ty + 2) * EW + (tx + 2);
 
-  double* __restrict__ Dn = tab->ptr[0][SF_DIVU][ALT];
-  double* __restrict__ Pn = tab->ptr[0][SF_P][ALT];
-  double* __restrict__ Un = tab->ptr[0][SF_VX][ALT];
-  double* __restrict__ Vn = tab->ptr[0][SF_VY][ALT];
-  double* __restrict__ Wn = tab->ptr[0][SF_VZ][ALT];
+  double* __restrict__ Dn = tab->ptr[b][SF_DIVU][ALT];
+  double* __restrict__ Pn = tab->ptr[b][SF_P][ALT];
+  double* __restrict__ Un = tab->ptr[b][SF_VX][ALT];
+  double* __restrict__ Vn = tab->ptr[b][SF_VY][ALT];
+  double* __restrict__ Wn = tab->ptr[b][SF_VZ][ALT];
   unsigned long long r1 = 0ull, r2 = 0ull;
   double wm2 = 0.0;  // swept w2 of the -z neighbour (marching register)
   long long o = B.base + ((long long)k0 * B.sy + j) * sx + i;
@@ -385,7 +397,7 @@ __global__ void __launch_bounds__(NT, MINB)
     if (u == 1 && act) {
       // swept w2 of the plane below the chunk: sweep B's -z neighbour at k0
       const double w1_below = S[F(1) + W1 * EN + q0];
-      if (k0 > 0) {
+      if (lo2 + k0 > 0) {
         const long long gkm = B.lo[2] + k0 - 1;
         const int bzm = bin(s.per[2], gkm, nm2), bzpm = bnx(s.per[2], gkm, nm2);
         const double a0m = (((gi + gj + gkm) & 1) == colB) ? 1.0 : 0.0, a1m = 1.0 - a0m;
@@ -451,12 +463,12 @@ __global__ void __launch_bounds__(NT, MINB)
         double un = u1[q0] + cu * (d0 - exv);
         double vn = v1[q0] + cv * (d0 - eyv);
         double wn = w1[q0] + cw * (d0 - ezv);
-        if (i == n0 - 1) un = pin_u;
-        if (j == n1 - 1) vn = pin_v;
-        if (z == n2 - 1) wn = pin_w;
+        if (gi == N0 - 1) un = pin_u;
+        if (gj == N1 - 1) vn = pin_v;
+        if (gk == N2 - 1) wn = pin_w;
         // swept -x / -y neighbours; at the low wall the pinned ghost (in S1)
         double umn, vmn;
-        if (i > 0) {
+        if (gi > 0) {
           const double a0m = a1, a1m = 1.0 - a0m;
           const double d0m = smb[ixm | bz] * dXm * a0m;
           const double exm = smb[ixpm | bz] * dC * a1m;
@@ -464,7 +476,7 @@ __global__ void __launch_bounds__(NT, MINB)
         } else {
           umn = u1[q0 - 1];
         }
-        if (j > 0) {
+        if (gj > 0) {
           const double a0m = a1, a1m = 1.0 - a0m;
           const double d0m = smb[iym | bz] * dYm * a0m;
           const double eym = smb[iypm | bz] * dC * a1m;
@@ -481,21 +493,21 @@ __global__ void __launch_bounds__(NT, MINB)
         Wn[o] = wn;
         Dn[o] = dd;
         // ghosts the next pass reads: pinned low-face velocities, mirrored divu
-        if (i == 0) {
+        if (gi == 0) {
           Un[o - 1] = umn;
           Dn[o - 1] = dd;
         }
-        if (j == 0) {
+        if (gj == 0) {
           Vn[o - sx] = vmn;
           Dn[o - sx] = dd;
         }
-        if (z == 0) {
+        if (gk == 0) {
           Wn[o - sxy] = wm2;
           Dn[o - sxy] = dd;
         }
-        if (i == n0 - 1) Dn[o + 1] = dd;
-        if (j == n1 - 1) Dn[o + sx] = dd;
-        if (z == n2 - 1) Dn[o + sxy] = dd;
+        if (gi == N0 - 1) Dn[o + 1] = dd;
+        if (gj == N1 - 1) Dn[o + sx] = dd;
+        if (gk == N2 - 1) Dn[o + sxy] = dd;
         const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
         r1 = b1 > r1 ? b1 : r1;
         r2 = b2 > r2 ? b2 : r2;
@@ -508,6 +520,7 @@ __global__ void __launch_bounds__(NT, MINB)
 
   unsigned long long rr[2] = {r1, r2};
   block_max_atomic<2>(rr, &ctl->acc[0]);
+  if (!finalize) return;  // across ranks: allreduce acc[0..1], then CTL_FINISH_PASS
   if (last_cta(&ctl->ctas_done, total_ctas)) {
     if (tid == 0) {
       __threadfence();
@@ -529,14 +542,15 @@ __global__ void __launch_bounds__(NT, MINB)
         ctl->residual = res2;
         const int more = (res2 > ctl->tolerance) && (sw + 2 < ctl->max_sweeps);
         ctl->done = more ? 0 : 1;
-        for (int f = 0; f < 5; ++f) {
-          double* tmp = tab->ptr[0][f][FRONT];
-          tab->ptr[0][f][FRONT] = tab->ptr[0][f][ALT];
-          tab->ptr[0][f][ALT] = tmp;
-          const unsigned char ti = tab->bidx[0][f][FRONT];
-          tab->bidx[0][f][FRONT] = tab->bidx[0][f][ALT];
-          tab->bidx[0][f][ALT] = ti;
-        }
+        for (int q = 0; q < tab->nblocks; ++q)
+          for (int f = 0; f < 5; ++f) {
+            double* tmp = tab->ptr[q][f][FRONT];
+            tab->ptr[q][f][FRONT] = tab->ptr[q][f][ALT];
+            tab->ptr[q][f][ALT] = tmp;
+            const unsigned char ti = tab->bidx[q][f][FRONT];
+            tab->bidx[q][f][FRONT] = tab->bidx[q][f][ALT];
+            tab->bidx[q][f][ALT] = ti;
+          }
       }
       if (hflag) {
         hflag->sweeps = ctl->sweeps;
@@ -561,7 +575,7 @@ static int sweep2_prefetch() {
 
 template <int NIN, int MINB>
 static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                    sf_host_flag* hflag, const void* maps, cudaStream_t st) {
+                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sweep2<NIN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -570,12 +584,12 @@ static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c,
   }
   k_sweep2<NIN, MINB><<<nctas, dim3(TX, TY), smem_bytes(NIN), st>>>(
       vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas, static_cast<const maps2_t*>(maps),
-      sweep2_prefetch());
+      sweep2_prefetch(), fin, pins);
 }
 
 // SF_SWEEP2_VARIANT: 0 = 3 S0 stages, 2 CTAs/SM (default); 1 = 6 stages, 1 CTA/SM
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                   sf_host_flag* hflag, const void* maps, cudaStream_t st) {
+                   sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st) {
   if (nctas <= 0) return;
   static int v = -1;
   if (v < 0) {
@@ -583,8 +597,8 @@ void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, 
     v = e ? atoi(e) : 0;
   }
   switch (v) {
-    case 1: launch2<6, 1>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
-    default: launch2<3, 2>(vw, nctas, zc, c, ctl, hflag, maps, st); break;
+    case 1: launch2<6, 1>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st); break;
+    default: launch2<3, 2>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st); break;
   }
 }
 

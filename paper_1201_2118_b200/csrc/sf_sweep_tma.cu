@@ -424,15 +424,16 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
       __threadfence();
       ctl->ctas_done = 0u;
       ctl->redo = 0;
-      for (int f = 0; f < 5; ++f) {
-        if (f == SF_P) continue;
-        double* tmp = tab->ptr[b][f][FRONT];
-        tab->ptr[b][f][FRONT] = tab->ptr[b][f][ALT];
-        tab->ptr[b][f][ALT] = tmp;
-        const unsigned char ti = tab->bidx[b][f][FRONT];
-        tab->bidx[b][f][FRONT] = tab->bidx[b][f][ALT];
-        tab->bidx[b][f][ALT] = ti;
-      }
+      for (int q = 0; q < tab->nblocks; ++q)
+        for (int f = 0; f < 5; ++f) {
+          if (f == SF_P) continue;
+          double* tmp = tab->ptr[q][f][FRONT];
+          tab->ptr[q][f][FRONT] = tab->ptr[q][f][ALT];
+          tab->ptr[q][f][ALT] = tmp;
+          const unsigned char ti = tab->bidx[q][f][FRONT];
+          tab->bidx[q][f][FRONT] = tab->bidx[q][f][ALT];
+          tab->bidx[q][f][ALT] = ti;
+        }
     }
     return;
   }

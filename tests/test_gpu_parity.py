@@ -504,3 +504,50 @@ def test_temporal_pass_random_configurations_match_single_sweeps(seed):
         if fused == 1:
             assert s.kernel_timing("sweep2")[1] > 0, ext
     assert out[1] == out[3], (ext, tol, maxs)
+
+
+@pytest.mark.parametrize("workers", [2, 4, 8])
+def test_temporal_pass_across_grid_components_matches_the_reference(ref_available, workers):
+    # processor faces between grid components on one device, ghost width 2:
+    # the pass recomputes the neighbours' first-sweep state from their 2-deep
+    # halo and exchanges vx, vy, vz, divu after every pass
+    c = cavity_case((48, 40, 36), symmetry_z=False, tolerance=1e-4, max_sweeps=61, ghost=2, workers=workers)
+    o = Oracle(c, "ref")
+    o.init_cavity()
+    so = o.advance(3)
+    d = dev_from_case(c, fused=1)
+    d.init_cavity()
+    d.set_kernel_timing(True)
+    dd = [d.step() for _ in range(3)]
+    assert [[x.dt, x.sweeps, x.residual] for x in dd] == [[float(a), int(b), float(r)] for a, b, r in zip(*so)]
+    assert d.kernel_timing("sweep2")[1] > 0
+    assert d.checksum() == o.checksum()
+    for f in FIELDS5:
+        assert same(d.gather(f), o.gather(f)), f
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_temporal_pass_random_decompositions_match_single_sweeps(seed):
+    rng = np.random.default_rng(200 + seed)
+    ext = (int(rng.integers(40, 90)), int(rng.integers(24, 60)), int(rng.integers(6, 70)))
+    workers = int(rng.choice([2, 3, 4, 6]))
+    kinds = ["wall", "symmetry"]
+    faces = [(a, sd, kinds[int(rng.integers(0, 2))], tuple(rng.uniform(-0.3, 0.3, 3))) for a in range(3) for sd in range(2)]
+    tol, maxs, omega = float(rng.choice([1e-30, 1e-3])), int(rng.integers(1, 25)), float(rng.uniform(1.0, 1.95))
+    vel = {f: rng.uniform(-0.5, 0.5, size=ext[::-1]) for f in ("vx", "vy", "vz")}
+    out = {}
+    for fused in (1, 3):
+        cfg = sfb.SolverConfig(extents=ext, tolerance=tol, max_sweeps=maxs, symmetry_z=False, omega=omega)
+        s = sfb.Simulation(cfg, sfb.FluidParams(viscosity=0.02, lid_speed=0.0), workers=workers, ghost=2,
+                           fused=fused)
+        s.init_cavity()
+        for a, sd, k, v in faces:
+            s.set_face_bc(a, sd, k, v)
+        for f, arr in vel.items():
+            s.scatter(f, arr)
+        s.set_kernel_timing(True)
+        st = [s.step() for _ in range(3)]
+        out[fused] = ([[x.dt, x.sweeps, x.residual] for x in st], s.checksum(), s.pending_color)
+        if fused == 1:
+            assert s.kernel_timing("sweep2")[1] > 0, (ext, workers)
+    assert out[1] == out[3], (ext, workers, tol, maxs)
