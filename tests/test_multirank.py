@@ -169,6 +169,8 @@ CASES = [
     ((11, 8, 7), 1, (False, False, False), False),
     ((12, 10, 9), 1, (True, True, True), True),
     ((11, 8, 7), 1, (False, False, False), True),
+    # the temporal pass's per-pass exchange: 2 deep, no periodic axis
+    ((14, 12, 10), 2, (False, False, False), False),
 ]
 
 
@@ -181,9 +183,9 @@ def test_two_ranks_exchange_every_ghost_like_the_global_oracle():
 
 def test_four_ranks_with_shared_periodic_faces():
     # (2,2,1) process grid: both x faces of a rank face the same peer when periodic
-    out = run_world(4, CASES[:2] + CASES[3:4])
+    out = run_world(4, CASES[:2] + CASES[3:4] + CASES[5:6])
     for rank, res in out.items():
-        assert res[:-1] == [0, 0, 0], (rank, res)
+        assert res[:-1] == [0, 0, 0, 0], (rank, res)
 
 
 def test_plan_counts_match_between_peers():
