@@ -551,3 +551,22 @@ def test_temporal_pass_random_decompositions_match_single_sweeps(seed):
         if fused == 1:
             assert s.kernel_timing("sweep2")[1] > 0, (ext, workers)
     assert out[1] == out[3], (ext, workers, tol, maxs)
+
+
+@pytest.mark.parametrize("maxs", [7, 8])
+def test_temporal_pass_cross_rank_finalize_on_one_rank(maxs):
+    # world = 1 NCCL mode: the pass leaves both residuals for the allreduce and
+    # CTL_FINISH_PASS decides continue / stop / redo (odd caps stop after the
+    # first sweep of a pass)
+    uid = sfb.nccl_unique_id()
+    cfg = sfb.SolverConfig(extents=(48, 40, 36), tolerance=1e-30, max_sweeps=maxs, symmetry_z=False)
+    d = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), rank=0, world=1, nccl_id=uid, fused=1, ghost=2)
+    s = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), fused=3)
+    for x in (d, s):
+        x.init_cavity()
+    d.set_kernel_timing(True)
+    a = [d.step() for _ in range(3)]
+    b = [s.step() for _ in range(3)]
+    assert [[x.dt, x.sweeps, x.residual] for x in a] == [[x.dt, x.sweeps, x.residual] for x in b]
+    assert d.kernel_timing("sweep2")[1] > 0
+    assert d.checksum() == s.checksum() and d.pending_color == s.pending_color
