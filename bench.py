@@ -57,7 +57,7 @@ def parse_args():
                     help="cavity = configs[1] (headline); stencil = configs[4], a descriptor-declared "
                          "high-order Laplacian (radius 2 or 3) JIT-compiled from its point function")
     ap.add_argument("--radius", type=int, default=2)
-    ap.add_argument("--tile", default="32,8,16", help="descriptor TILE for --workload stencil")
+    ap.add_argument("--tile", default="32,8,64", help="descriptor TILE for --workload stencil")
     return ap.parse_args()
 
 

@@ -197,6 +197,7 @@ struct cell_view {
   int slot;
   const double* rb;  // cached: ring base + this cell's in-plane offset
   int zoff[SF_ZW];   // cached: ring-plane offset for dk = t - halo_lo_z (updated per plane)
+  double zq[SF_ZW];  // cached: this column's values for dk = t - halo_lo_z (register queue)
   __device__ __forceinline__ double operator()(int di, int dj, int dk) const {
 #if SF_DEBUG
     if (!SF_READABLE[slot]) { sf_violation(1, slot, di, dj, dk); return 0.0; }
@@ -204,6 +205,9 @@ struct cell_view {
     if (di < -SF_HALO[0] || di > SF_HALO[1] || dj < -SF_HALO[2] || dj > SF_HALO[3] || dk < -SF_HALO[4] ||
         dk > SF_HALO[5]) { sf_violation(3, slot, di, dj, dk); return 0.0; }
 #endif
+    // the column itself comes from the register queue: one shared-memory load
+    // per plane instead of one per z offset (offsets fold to constants)
+    if (SF_CACHED[slot] && di == 0 && dj == 0) return zq[dk + SF_HALO[4]];
     if (SF_CACHED[slot]) return rb[zoff[dk + SF_HALO[4]] + dj * SF_BW + di];
     return SF_CENTER_ONLY[slot] ? __ldcg(rd + o + di + dj * sx + dk * sxy) : __ldg(rd + o + di + dj * sx + dk * sxy);
   }
@@ -323,6 +327,16 @@ sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
           c.f_[s].o = o;
 #pragma unroll
           for (int t = 0; t < SF_ZW; ++t) c.f_[s].zoff[t] = zr[t];
+          if (SF_CACHED[s]) {  // column queue: shift in the plane that entered the window
+            if (kq == 0) {
+#pragma unroll
+              for (int t = 0; t < SF_ZW; ++t) c.f_[s].zq[t] = c.f_[s].rb[zr[t]];
+            } else {
+#pragma unroll
+              for (int t = 0; t < SF_ZW - 1; ++t) c.f_[s].zq[t] = c.f_[s].zq[t + 1];
+              c.f_[s].zq[SF_ZW - 1] = c.f_[s].rb[zr[SF_ZW - 1]];
+            }
+          }
         }
         c.k = G.lo[2] + k0 + kq;
         sf_user_point(c);
