@@ -2014,7 +2014,7 @@ class simulation {
       enqueue_half_sweep();
       return 1;
     }
-    const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, kTX, kTY);
+    const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, kTX, sweep2_tile_y());
     if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
     const int fin = dist_ ? 0 : 1;
     launch_sweep2(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_);

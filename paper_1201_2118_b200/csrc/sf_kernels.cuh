@@ -60,6 +60,7 @@ void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, 
 size_t sweep2_maps_bytes();
 size_t sweep2_map_offset(int b, int f, int s);
 void sweep2_box(int field, int* bw, int* bh);
+int sweep2_tile_y();  // tile height of the selected temporal-pass variant (tile width 32)
 int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field);
 size_t sweep_maps_bytes();
 int encode_box_map(void* map_out, double* base, long long sx, long long sy, long long sz, int bw, int bh);

@@ -69,22 +69,30 @@ __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, uint64_t
       : "memory");
 }
 
-constexpr int TX = 32, TY = 8, NT = TX * TY;
-constexpr int EW = TX + 3, EH = TY + 3, EN = EW * EH;  // widened S1 tile (385 cells)
-constexpr int NE = (EN + NT - 1) / NT;                  // widened cells per thread
-constexpr int IW = TX + 4;                              // S0 box width (x from i0-2)
-constexpr int IDH = TY + 4, IFH = TY + 3;               // divu / other S0 box heights
 constexpr int r128(int b) { return (b + 127) / 128 * 128; }
-constexpr int IN_D = 0;
-constexpr int IN_U = r128(8 * IW * IDH);
-constexpr int IN_V = IN_U + r128(8 * IW * IFH);
-constexpr int IN_W = IN_V + r128(8 * IW * IFH);
-constexpr int IN_P = IN_W + r128(8 * IW * IFH);
-constexpr int IN_BYTES = IN_P + r128(8 * IW * IFH);
-constexpr uint32_t IN_TX = 8u * (IW * IDH + 4 * IW * IFH);
-enum { U1 = 0, V1 = 1, W1 = 2, P1 = 3, D1 = 4 };
 
-constexpr int smem_bytes(int nin) { return nin * IN_BYTES + (4 * 4 + 3) * EN * 8; }
+// Tile geometry: TX x TY cells per CTA (one thread each), the S1 tile widened
+// to EW x EH, and the S0 stage layout (every TMA destination 128-byte aligned).
+template <int TYV>
+struct geom {
+  static constexpr int TX = 32, TY = TYV, NT = TX * TY;
+  static constexpr int EW = TX + 3, EH = TY + 3, EN = EW * EH;  // widened S1 tile
+  static constexpr int NE = (EN + NT - 1) / NT;                  // widened cells per thread
+  static constexpr int R2 = EN - 1 - NT;                         // second-round cells
+  static constexpr int IW = TX + 4;                              // S0 box width (x from i0-2)
+  static constexpr int IDH = TY + 4, IFH = TY + 3;               // divu / other S0 box heights
+  static constexpr int IN_D = 0;
+  static constexpr int IN_U = r128(8 * IW * IDH);
+  static constexpr int IN_V = IN_U + r128(8 * IW * IFH);
+  static constexpr int IN_W = IN_V + r128(8 * IW * IFH);
+  static constexpr int IN_P = IN_W + r128(8 * IW * IFH);
+  static constexpr int IN_BYTES = IN_P + r128(8 * IW * IFH);
+  static constexpr uint32_t IN_TX = 8u * (IW * IDH + 4 * IW * IFH);
+  static constexpr int smem_bytes(int nin) { return nin * IN_BYTES + (4 * 4 + 3) * EN * 8; }
+  static_assert(NE == 2 && R2 > 0 && R2 <= NT, "two rounds of widened cells per thread");
+};
+
+enum { U1 = 0, V1 = 1, W1 = 2, P1 = 3, D1 = 4 };
 
 struct maps2_t {  // [block][field][physical buffer]
   CUtensorMap m[kMaxBlocks][SF_NFIELDS][kSlots];
@@ -96,9 +104,13 @@ size_t sweep2_maps_bytes() { return sizeof(maps2_t); }
 size_t sweep2_map_offset(int b, int f, int s) {
   return sizeof(CUtensorMap) * (((size_t)b * SF_NFIELDS + f) * kSlots + s);
 }
+static int sweep2_variant();
+// tile height of the selected variant (SF_SWEEP2_VARIANT 2: 32 x 16)
+int sweep2_tile_y() { return sweep2_variant() == 2 ? 16 : 8; }
 void sweep2_box(int field, int* bw, int* bh) {
-  *bw = IW;
-  *bh = field == SF_DIVU ? IDH : IFH;
+  const int ty = sweep2_tile_y();
+  *bw = 32 + 4;
+  *bh = field == SF_DIVU ? ty + 4 : ty + 3;
 }
 
 // Schedule (S0 plane q and S1 plane m both mean z = k0 - 2 + q / m). One CTA
@@ -106,16 +118,22 @@ void sweep2_box(int field, int* bw, int* bh) {
 //     phase u:  s1_fields(m = u+2)  and  s1_div(m = u+1)     (independent)
 //     barrier
 //     sweep B on plane m = u (u >= 2), overlapping phase u+1 of other warps
-// Warps 0-3 take the second round of s1_fields, warps 4-7 that of s1_div, so
+// The first threads take the second round of s1_fields, the last ones that of
+// s1_div (R2 cells each), so the phases are balanced across warps; with 32x8
 // every warp does three cell updates per phase. Rings: S0 planes in q % NIN
 // (NIN >= 3), S1 fields (u1 v1 w1 p1) in m % 4, divu1 in m % 3 -- the slot a
 // phase overwrites was last read before the previous barrier.
-template <int NIN, int MINB>
-__global__ void __launch_bounds__(NT, MINB)
+template <int TYV, int NIN, int MINB>
+__global__ void __launch_bounds__(32 * TYV, MINB)
     k_sweep2(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc,
              sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag, unsigned int total_ctas,
              const maps2_t* __restrict__ maps, int pf, int finalize, sweep2_pins pins) {
   static_assert(NIN >= 3, "three S0 planes are read or in flight per phase");
+  using G = geom<TYV>;
+  constexpr int TX = G::TX, TY = G::TY, NT = G::NT, EW = G::EW, EN = G::EN, NE = G::NE, R2 = G::R2;
+  constexpr int IW = G::IW, IN_D = G::IN_D, IN_U = G::IN_U, IN_V = G::IN_V, IN_W = G::IN_W, IN_P = G::IN_P;
+  constexpr int IN_BYTES = G::IN_BYTES;
+  constexpr uint32_t IN_TX = G::IN_TX;
   if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t bars[NIN];
@@ -209,14 +227,14 @@ __global__ void __launch_bounds__(NT, MINB)
   auto so = [&](int q) { return (q % NIN) * (IN_BYTES / 8); };  // S0 stage offset
 
   // ---- per-thread widened cells ---------------------------------------------
-  // s1_fields: thread t owns e = t + 1 and, for t < 128 (warps 0-3),
-  // e = t + 257. s1_div: e = 384 - t and, for t >= 128 (warps 4-7),
-  // e = 256 - t. The corner e = 0 (x = i0-2, y = j0-2) is never read.
+  // s1_fields: thread t owns e = t + 1 and, for t < R2, e = t + 1 + NT.
+  // s1_div: e = EN - 1 - t and, for t >= NT - R2, e = NT - t. (32x8: R2 = 128,
+  // warps 0-3 / 4-7.) The corner e = 0 (x = i0-2, y = j0-2) is never read.
   // f_ia: index into the S0 boxes; f_bt: scale-table rows rc | rx << 3 |
   // ry << 6 (x/y bits), parity << 9, owned << 10, x pin << 11, y pin << 12.
   // d_q: DIVERGENCE operand cell (wall mirror applied), d_ok: bit r set when
   // div cell r is a source (x >= i0-1, y >= j0-1).
-  const bool has2f = tid < EN - 1 - NT, has2d = tid >= EN - 1 - NT;
+  const bool has2f = tid < R2, has2d = tid >= NT - R2;
   int f_e[NE], f_ia[NE], f_bt[NE], d_e[NE], d_q[NE], d_ok = 0;
 #pragma unroll
   for (int r = 0; r < NE; ++r) {
@@ -234,7 +252,7 @@ __global__ void __launch_bounds__(NT, MINB)
                 ((gi == N0 - 1) << 11) | ((gj == N1 - 1) << 12) | ((gi == -1) << 13) | ((gj == -1) << 14);
     }
     {
-      const int e = r == 0 ? EN - 1 - tid : (has2d ? EN - 1 - NT - tid + 128 : EN - 1);
+      const int e = r == 0 ? EN - 1 - tid : (has2d ? NT - tid : EN - 1);
       const int ex = e % EW, ey = e / EW;
       const int x = i0 - 2 + ex, y = j0 - 2 + ey;
       // the +x / +y ghost (x = n0, y = n1) takes the wall mirror of the last
@@ -573,32 +591,39 @@ static int sweep2_prefetch() {
   return v;
 }
 
-template <int NIN, int MINB>
+template <int TYV, int NIN, int MINB>
 static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                     sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st) {
+  using G = geom<TYV>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sweep2<NIN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem_bytes(NIN));
+    cudaFuncSetAttribute(k_sweep2<TYV, NIN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         G::smem_bytes(NIN));
     attr = true;
   }
-  k_sweep2<NIN, MINB><<<nctas, dim3(TX, TY), smem_bytes(NIN), st>>>(
+  k_sweep2<TYV, NIN, MINB><<<nctas, dim3(G::TX, G::TY), G::smem_bytes(NIN), st>>>(
       vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas, static_cast<const maps2_t*>(maps),
       sweep2_prefetch(), fin, pins);
 }
 
-// SF_SWEEP2_VARIANT: 0 = 3 S0 stages, 2 CTAs/SM (default); 1 = 6 stages, 1 CTA/SM
-void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                   sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st) {
-  if (nctas <= 0) return;
+// SF_SWEEP2_VARIANT: 0 = 32x8 tile, 3 S0 stages, 2 CTAs/SM (default);
+// 1 = 32x8, 6 stages, 1 CTA/SM; 2 = 32x16, 3 stages, 1 CTA/SM
+static int sweep2_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SF_SWEEP2_VARIANT");
     v = e ? atoi(e) : 0;
   }
-  switch (v) {
-    case 1: launch2<6, 1>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st); break;
-    default: launch2<3, 2>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st); break;
+  return v;
+}
+
+void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                   sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st) {
+  if (nctas <= 0) return;
+  switch (sweep2_variant()) {
+    case 1: launch2<8, 6, 1>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st); break;
+    case 2: launch2<16, 3, 1>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st); break;
+    default: launch2<8, 3, 2>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st); break;
   }
 }
 
