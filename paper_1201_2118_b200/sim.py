@@ -141,8 +141,11 @@ def _cstrs(names: Iterable[str]):
 class Simulation:
     """Device-resident cfd::simulation.  ``workers`` grid components of
     grid::decompose() live on ``device``.  ``fused``: 1/True = fused half-sweep,
-    TMA-pipelined (default); 2 = fused half-sweep with plain loads; 0/False =
-    the reference's unfused dataflow (refresh, SWEEP, refresh, DIV, reduce)."""
+    TMA-pipelined, with the temporal pass (two half-sweeps per launch) wherever
+    every face is a wall, a symmetry plane or a processor face and, with
+    processor faces, ``ghost`` >= 2 (default); 3 = TMA half-sweeps only; 2 =
+    fused half-sweep with plain loads; 0/False = the reference's unfused
+    dataflow (refresh, SWEEP, refresh, DIV, reduce)."""
 
     def __init__(self, cfg: SolverConfig, par: FluidParams, workers: int = 1, mode: str = "plain",
                  tile: Sequence[int] = (0, 0, 0), ghost: int = 1, form: str = "rows",
