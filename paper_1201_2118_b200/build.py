@@ -15,8 +15,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libsfb200.so")
-SOURCES = ["sf_kernels.cu", "sf_sweep_tma.cu", "sf_sweep2.cu", "sf_driver.cu"]
-HEADERS = ["sf_device.cuh", "sf_kernels.cuh", "sf_plan.hpp", "sf_jit.hpp"]
+SOURCES = ["sf_kernels.cu", "sf_sweep_tma.cu", "sf_sweep2.cu", "sf_uv_tma.cu", "sf_driver.cu"]
+HEADERS = ["sf_uv.cuh", "sf_device.cuh", "sf_kernels.cuh", "sf_plan.hpp", "sf_jit.hpp"]
 
 NVCC_FLAGS = [
     "-std=c++17",

@@ -1203,8 +1203,13 @@ class simulation {
 
   void provisional_device() {
     refresh({SF_VX, SF_VY, SF_VZ, SF_P});
-    const work_set& ws = items_for(SF_REGION_ALL, {1, 1, 1, 1, 1, 1}, zc_uv_);
-    launch_update_velocity(tview(ws), ws.nctas, zc_uv_, consts_, dctl_, 0.0, st_);
+    if (uvmaps_ && uv_tma_env_) {
+      const work_set& ws = items_for(SF_REGION_ALL, {1, 1, 1, 1, 1, 1}, zc_fused_, kTX, kTY);
+      launch_update_velocity_tma(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, uvmaps_, st_);
+    } else {
+      const work_set& ws = items_for(SF_REGION_ALL, {1, 1, 1, 1, 1, 1}, zc_uv_);
+      launch_update_velocity(tview(ws), ws.nctas, zc_uv_, consts_, dctl_, 0.0, st_);
+    }
     ++launches_;
     check_launch();
     swap_front_back();
@@ -1496,6 +1501,8 @@ class simulation {
   mutable unsigned long long compute_epoch_ = 1;
   unsigned long long table_epoch_ = 0;
   void* maps2_ = nullptr;  // temporal-pass descriptors (null: pass unavailable)
+  void* uvmaps_ = nullptr;  // TMA UPDATE_VELOCITY descriptors (null: plain-load kernel)
+  const bool uv_tma_env_ = getenv("SF_NO_UV_TMA") == nullptr;
   const bool temporal_env_ = getenv("SF_NO_TEMPORAL") == nullptr;
   std::vector<void*> dev_allocs_;
   std::map<std::string, work_set> items_;
@@ -1667,6 +1674,27 @@ class simulation {
       if (ok) {
         maps_ = dalloc(hm.size());
         SF_CK(cudaMemcpy(maps_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
+      }
+    }
+    // descriptors of the TMA-staged UPDATE_VELOCITY
+    if (maps_) {
+      std::vector<unsigned char> hm(uv_maps_bytes(), 0);
+      bool ok = true;
+      const int uvf[4] = {SF_VX, SF_VY, SF_VZ, SF_P};
+      for (int b = 0; b < nloc_ && ok; ++b)
+        for (int k = 0; k < 4 && ok; ++k)
+          for (int s = 0; s < kSlots && ok; ++s) {
+            double* p = htab_->ptr[b][uvf[k]][s];
+            if (!p) continue;
+            const sf_layout& L = lay_[b];
+            int bw, bh;
+            uv_box(uvf[k], &bw, &bh);
+            ok = bw <= L.sx && bh <= L.sy &&
+                 encode_box_map(hm.data() + uv_map_offset(b, k, s), p, L.sx, L.sy, L.sz, bw, bh) == 0;
+          }
+      if (ok) {
+        uvmaps_ = dalloc(hm.size());
+        SF_CK(cudaMemcpy(uvmaps_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
       }
     }
     // descriptors of the temporal pass (halo'd boxes)

@@ -16,6 +16,7 @@
 #include <cstdio>
 
 #include "sf_kernels.cuh"
+#include "sf_uv.cuh"
 
 namespace sfb {
 
@@ -203,78 +204,25 @@ __global__ void __launch_bounds__(kTX* kTY) k_update_vel(View vw, int zc, sf_con
   if (t.act) {
     for (long long k = t.k0; k < t.k1; ++k) {
       const long long o = off(B, t.i, t.j, k);
-#define u(a, b, c) __ldg(U + o + (a) + (b) * sx + (c) * sxy)
-#define v(a, b, c) __ldg(V + o + (a) + (b) * sx + (c) * sxy)
-#define w(a, b, c) __ldg(W + o + (a) + (b) * sx + (c) * sxy)
-#define q(a, b, c) __ldg(Q + o + (a) + (b) * sx + (c) * sxy)
-      const double u0 = u(0, 0, 0), v0 = v(0, 0, 0), w0 = w(0, 0, 0);
-      {  // x momentum, at this cell's high x face
-        const double ue = u(1, 0, 0), uw = u(-1, 0, 0);
-        const double un = u(0, 1, 0), us = u(0, -1, 0);
-        const double ut = u(0, 0, 1), ub = u(0, 0, -1);
-        const double vn = v(0, 0, 0) + v(1, 0, 0), vs = v(0, -1, 0) + v(1, -1, 0);
-        const double wt = w(0, 0, 0) + w(1, 0, 0), wb = w(0, 0, -1) + w(1, 0, -1);
-        double fux = (u0 + ue) * (u0 + ue) - (uw + u0) * (uw + u0);
-        fux += s.alpha * (fabs(u0 + ue) * (u0 - ue) - fabs(uw + u0) * (uw - u0));
-        double fuy = vn * (u0 + un) - vs * (us + u0);
-        fuy += s.alpha * (fabs(vn) * (u0 - un) - fabs(vs) * (us - u0));
-        double fuz = wt * (u0 + ut) - wb * (ub + u0);
-        fuz += s.alpha * (fabs(wt) * (u0 - ut) - fabs(wb) * (ub - u0));
-        const double lapu = (ue - 2.0 * u0 + uw) * s.ix2 + (un - 2.0 * u0 + us) * s.iy2 +
-                            (ut - 2.0 * u0 + ub) * s.iz2;
-        const double rhsu = (q(0, 0, 0) - q(1, 0, 0)) * s.ix -
-                            0.25 * (fux * s.ix + fuy * s.iy + fuz * s.iz) + s.nu * lapu + s.fx;
-        const double r = u0 + dt * rhsu;
-        Uo[o] = r;
-        const unsigned long long bb = abs_bits(r);
-        mx[0] = bb > mx[0] ? bb : mx[0];
+      struct ldg_acc {
+        const double *U, *V, *W, *Q;
+        long long o, sx, sxy;
+        __device__ __forceinline__ double u(int a, int b, int c) const { return __ldg(U + o + a + b * sx + c * sxy); }
+        __device__ __forceinline__ double v(int a, int b, int c) const { return __ldg(V + o + a + b * sx + c * sxy); }
+        __device__ __forceinline__ double w(int a, int b, int c) const { return __ldg(W + o + a + b * sx + c * sxy); }
+        __device__ __forceinline__ double q(int a, int b, int c) const { return __ldg(Q + o + a + b * sx + c * sxy); }
+      };
+      const ldg_acc A{U, V, W, Q, o, sx, sxy};
+      double r[3];
+      uv_point(A, s, dt, r);
+      Uo[o] = r[0];
+      Vo[o] = r[1];
+      Wo[o] = r[2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const unsigned long long bb = abs_bits(r[a]);
+        mx[a] = bb > mx[a] ? bb : mx[a];
       }
-      {  // y momentum, at the high y face
-        const double ve = v(1, 0, 0), vw = v(-1, 0, 0);
-        const double vnn = v(0, 1, 0), vss = v(0, -1, 0);
-        const double vt = v(0, 0, 1), vb = v(0, 0, -1);
-        const double ue2 = u(0, 0, 0) + u(0, 1, 0), uw2 = u(-1, 0, 0) + u(-1, 1, 0);
-        const double wt2 = w(0, 0, 0) + w(0, 1, 0), wb2 = w(0, 0, -1) + w(0, 1, -1);
-        double fvx = ue2 * (v0 + ve) - uw2 * (vw + v0);
-        fvx += s.alpha * (fabs(ue2) * (v0 - ve) - fabs(uw2) * (vw - v0));
-        double fvy = (v0 + vnn) * (v0 + vnn) - (vss + v0) * (vss + v0);
-        fvy += s.alpha * (fabs(v0 + vnn) * (v0 - vnn) - fabs(vss + v0) * (vss - v0));
-        double fvz = wt2 * (v0 + vt) - wb2 * (vb + v0);
-        fvz += s.alpha * (fabs(wt2) * (v0 - vt) - fabs(wb2) * (vb - v0));
-        const double lapv = (ve - 2.0 * v0 + vw) * s.ix2 + (vnn - 2.0 * v0 + vss) * s.iy2 +
-                            (vt - 2.0 * v0 + vb) * s.iz2;
-        const double rhsv = (q(0, 0, 0) - q(0, 1, 0)) * s.iy -
-                            0.25 * (fvx * s.ix + fvy * s.iy + fvz * s.iz) + s.nu * lapv + s.fy;
-        const double r = v0 + dt * rhsv;
-        Vo[o] = r;
-        const unsigned long long bb = abs_bits(r);
-        mx[1] = bb > mx[1] ? bb : mx[1];
-      }
-      {  // z momentum, at the high z face
-        const double we = w(1, 0, 0), ww = w(-1, 0, 0);
-        const double wn = w(0, 1, 0), ws = w(0, -1, 0);
-        const double wtt = w(0, 0, 1), wbb = w(0, 0, -1);
-        const double ue3 = u(0, 0, 0) + u(0, 0, 1), uw3 = u(-1, 0, 0) + u(-1, 0, 1);
-        const double vn3 = v(0, 0, 0) + v(0, 0, 1), vs3 = v(0, -1, 0) + v(0, -1, 1);
-        double fwx = ue3 * (w0 + we) - uw3 * (ww + w0);
-        fwx += s.alpha * (fabs(ue3) * (w0 - we) - fabs(uw3) * (ww - w0));
-        double fwy = vn3 * (w0 + wn) - vs3 * (ws + w0);
-        fwy += s.alpha * (fabs(vn3) * (w0 - wn) - fabs(vs3) * (ws - w0));
-        double fwz = (w0 + wtt) * (w0 + wtt) - (wbb + w0) * (wbb + w0);
-        fwz += s.alpha * (fabs(w0 + wtt) * (w0 - wtt) - fabs(wbb + w0) * (wbb - w0));
-        const double lapw = (we - 2.0 * w0 + ww) * s.ix2 + (wn - 2.0 * w0 + ws) * s.iy2 +
-                            (wtt - 2.0 * w0 + wbb) * s.iz2;
-        const double rhsw = (q(0, 0, 0) - q(0, 0, 1)) * s.iz -
-                            0.25 * (fwx * s.ix + fwy * s.iy + fwz * s.iz) + s.nu * lapw + s.fz;
-        const double r = w0 + dt * rhsw;
-        Wo[o] = r;
-        const unsigned long long bb = abs_bits(r);
-        mx[2] = bb > mx[2] ? bb : mx[2];
-      }
-#undef u
-#undef v
-#undef w
-#undef q
     }
   }
   if (ctl) block_max_atomic<3>(mx, &ctl->acc[1]);

@@ -30,6 +30,13 @@ void launch_tasks(const View& vw, const sf_task* tasks, int ntasks, long long ma
 template <class View>
 void launch_update_velocity(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                             double dt, cudaStream_t st);
+// TMA-staged UPDATE_VELOCITY (sf_uv_tma.cu): table view, 32 x 8 tiles;
+// maps = device table of uv descriptors (uv_box shapes).
+void launch_update_velocity_tma(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                                const void* maps, cudaStream_t st);
+size_t uv_maps_bytes();
+size_t uv_map_offset(int b, int f, int s);  // f: 0 vx, 1 vy, 2 vz, 3 p
+void uv_box(int field, int* bw, int* bh);
 template <class View>
 void launch_divergence(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                        int acc_slot, int predicated, cudaStream_t st);

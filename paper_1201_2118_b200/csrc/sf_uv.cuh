@@ -1,0 +1,74 @@
+// sf_uv.cuh -- the UPDATE_VELOCITY point update (cfd.hpp:524-589), written
+// once against an accessor so the plain-load and the TMA-staged kernels
+// evaluate the identical IEEE operations in the identical order.
+//   A.u(a, b, c), A.v(..), A.w(..), A.q(..): vx, vy, vz, p at offset (a, b, c)
+// out[0..2]: the provisional vx, vy, vz of the cell.
+#pragma once
+
+#include "sf_device.cuh"
+
+namespace sfb {
+
+template <class Acc>
+__device__ __forceinline__ void uv_point(const Acc& A, const sf_consts& s, double dt, double out[3]) {
+  const double u0 = A.u(0, 0, 0), v0 = A.v(0, 0, 0), w0 = A.w(0, 0, 0);
+  {  // x momentum, at this cell's high x face
+    const double ue = A.u(1, 0, 0), uw = A.u(-1, 0, 0);
+    const double un = A.u(0, 1, 0), us = A.u(0, -1, 0);
+    const double ut = A.u(0, 0, 1), ub = A.u(0, 0, -1);
+    const double vn = A.v(0, 0, 0) + A.v(1, 0, 0), vs = A.v(0, -1, 0) + A.v(1, -1, 0);
+    const double wt = A.w(0, 0, 0) + A.w(1, 0, 0), wb = A.w(0, 0, -1) + A.w(1, 0, -1);
+    double fux = (u0 + ue) * (u0 + ue) - (uw + u0) * (uw + u0);
+    fux += s.alpha * (fabs(u0 + ue) * (u0 - ue) - fabs(uw + u0) * (uw - u0));
+    double fuy = vn * (u0 + un) - vs * (us + u0);
+    fuy += s.alpha * (fabs(vn) * (u0 - un) - fabs(vs) * (us - u0));
+    double fuz = wt * (u0 + ut) - wb * (ub + u0);
+    fuz += s.alpha * (fabs(wt) * (u0 - ut) - fabs(wb) * (ub - u0));
+    const double lapu = (ue - 2.0 * u0 + uw) * s.ix2 + (un - 2.0 * u0 + us) * s.iy2 +
+                        (ut - 2.0 * u0 + ub) * s.iz2;
+    const double rhsu = (A.q(0, 0, 0) - A.q(1, 0, 0)) * s.ix -
+                        0.25 * (fux * s.ix + fuy * s.iy + fuz * s.iz) + s.nu * lapu + s.fx;
+    const double r = u0 + dt * rhsu;
+    out[0] = r;
+  }
+  {  // y momentum, at the high y face
+    const double ve = A.v(1, 0, 0), vw = A.v(-1, 0, 0);
+    const double vnn = A.v(0, 1, 0), vss = A.v(0, -1, 0);
+    const double vt = A.v(0, 0, 1), vb = A.v(0, 0, -1);
+    const double ue2 = A.u(0, 0, 0) + A.u(0, 1, 0), uw2 = A.u(-1, 0, 0) + A.u(-1, 1, 0);
+    const double wt2 = A.w(0, 0, 0) + A.w(0, 1, 0), wb2 = A.w(0, 0, -1) + A.w(0, 1, -1);
+    double fvx = ue2 * (v0 + ve) - uw2 * (vw + v0);
+    fvx += s.alpha * (fabs(ue2) * (v0 - ve) - fabs(uw2) * (vw - v0));
+    double fvy = (v0 + vnn) * (v0 + vnn) - (vss + v0) * (vss + v0);
+    fvy += s.alpha * (fabs(v0 + vnn) * (v0 - vnn) - fabs(vss + v0) * (vss - v0));
+    double fvz = wt2 * (v0 + vt) - wb2 * (vb + v0);
+    fvz += s.alpha * (fabs(wt2) * (v0 - vt) - fabs(wb2) * (vb - v0));
+    const double lapv = (ve - 2.0 * v0 + vw) * s.ix2 + (vnn - 2.0 * v0 + vss) * s.iy2 +
+                        (vt - 2.0 * v0 + vb) * s.iz2;
+    const double rhsv = (A.q(0, 0, 0) - A.q(0, 1, 0)) * s.iy -
+                        0.25 * (fvx * s.ix + fvy * s.iy + fvz * s.iz) + s.nu * lapv + s.fy;
+    const double r = v0 + dt * rhsv;
+    out[1] = r;
+  }
+  {  // z momentum, at the high z face
+    const double we = A.w(1, 0, 0), ww = A.w(-1, 0, 0);
+    const double wn = A.w(0, 1, 0), ws = A.w(0, -1, 0);
+    const double wtt = A.w(0, 0, 1), wbb = A.w(0, 0, -1);
+    const double ue3 = A.u(0, 0, 0) + A.u(0, 0, 1), uw3 = A.u(-1, 0, 0) + A.u(-1, 0, 1);
+    const double vn3 = A.v(0, 0, 0) + A.v(0, 0, 1), vs3 = A.v(0, -1, 0) + A.v(0, -1, 1);
+    double fwx = ue3 * (w0 + we) - uw3 * (ww + w0);
+    fwx += s.alpha * (fabs(ue3) * (w0 - we) - fabs(uw3) * (ww - w0));
+    double fwy = vn3 * (w0 + wn) - vs3 * (ws + w0);
+    fwy += s.alpha * (fabs(vn3) * (w0 - wn) - fabs(vs3) * (ws - w0));
+    double fwz = (w0 + wtt) * (w0 + wtt) - (wbb + w0) * (wbb + w0);
+    fwz += s.alpha * (fabs(w0 + wtt) * (w0 - wtt) - fabs(wbb + w0) * (wbb - w0));
+    const double lapw = (we - 2.0 * w0 + ww) * s.ix2 + (wn - 2.0 * w0 + ws) * s.iy2 +
+                        (wtt - 2.0 * w0 + wbb) * s.iz2;
+    const double rhsw = (A.q(0, 0, 0) - A.q(0, 0, 1)) * s.iz -
+                        0.25 * (fwx * s.ix + fwy * s.iy + fwz * s.iz) + s.nu * lapw + s.fz;
+    const double r = w0 + dt * rhsw;
+    out[2] = r;
+  }
+}
+
+}  // namespace sfb
