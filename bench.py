@@ -51,6 +51,8 @@ def parse_args():
                          "applies (default); tma1: one TMA half-sweep per launch; ldg: fused with plain "
                          "loads; unfused: the reference's dataflow")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="take the multi-rank (NCCL) path even at one rank (a check of that path on one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--workload", default="cavity", choices=["cavity", "stencil"],
@@ -224,7 +226,7 @@ def run_ours(args):
     n, S = args.n, args.sweeps
     fused = {"tma": 1, "tma1": 3, "ldg": 2, "unfused": 0}[args.variant]
     dist = None
-    if world > 1:  # one rank per GPU over NCCL, weak scaling: n^3 per rank
+    if world > 1 or args.force_dist:  # one rank per GPU over NCCL, weak scaling: n^3 per rank
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         uid = [sfb.nccl_unique_id() if rank == 0 else None]
