@@ -14,6 +14,9 @@
 //   k_reduce_*     grid::reduce (reductions.hpp:28-90)
 //   k_ctl          compute_dt / beta / loop bookkeeping (cfd.hpp:264-305)
 #include <cstdio>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "sf_kernels.cuh"
 #include "sf_uv.cuh"
@@ -853,6 +856,16 @@ __global__ void k_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, i
       }
       break;
   }
+}
+
+void ensure_smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert({kernel, dev}).second)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 // Condition of the pressure loop's CUDA-graph while node: run another body

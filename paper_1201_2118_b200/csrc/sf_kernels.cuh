@@ -93,6 +93,8 @@ enum ctl_op {
   CTL_PUBLISH = 10,          // loop state -> host-mapped flag (after the graph-captured loop)
   CTL_FINISH_PASS = 11,      // temporal pass finalise after the cross-rank allreduce of acc[0..1]
 };
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+void ensure_smem_attr(const void* kernel, int bytes);
 // sets the pressure-loop graph's while condition to !ctl->done
 void launch_loop_cond(cudaGraphConditionalHandle h, const sf_dev_ctl* ctl, cudaStream_t st);
 void launch_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, int op, double arg,

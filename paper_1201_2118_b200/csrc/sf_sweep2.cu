@@ -595,12 +595,7 @@ template <int TYV, int NIN, int MINB>
 static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                     sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st) {
   using G = geom<TYV>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sweep2<TYV, NIN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         G::smem_bytes(NIN));
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_sweep2<TYV, NIN, MINB>, G::smem_bytes(NIN));
   k_sweep2<TYV, NIN, MINB><<<nctas, dim3(G::TX, G::TY), G::smem_bytes(NIN), st>>>(
       vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas, static_cast<const maps2_t*>(maps),
       sweep2_prefetch(), fin, pins);

@@ -554,12 +554,7 @@ static void launch_variant(const table_view& vw, int nctas, int zc, const sf_con
                            sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,
                            cudaStream_t st) {
   const size_t smem = (size_t)tile<TX, TY>::BYTES * STAGES;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sweep_div_tma<STAGES, MINB, WS, TX, TY>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_sweep_div_tma<STAGES, MINB, WS, TX, TY>, (int)smem);
   k_sweep_div_tma<STAGES, MINB, WS, TX, TY><<<nctas, dim3(TX, TY + (WS ? 1 : 0)), smem, st>>>(
       vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas,
       static_cast<const sweep_maps*>(maps), fin, sweep_hints());

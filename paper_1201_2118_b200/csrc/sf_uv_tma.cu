@@ -167,11 +167,7 @@ __global__ void __launch_bounds__(NT, 2)
 void launch_update_velocity_tma(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                                 const void* maps, cudaStream_t st) {
   if (nctas <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_update_vel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, NST * ST_BYTES);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_update_vel_tma, NST * ST_BYTES);
   k_update_vel_tma<<<nctas, dim3(TX, TY), NST * ST_BYTES, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl,
                                                                  static_cast<const uvmaps_t*>(maps));
 }
