@@ -51,6 +51,9 @@ def parse_args():
                          "applies (default); tma1: one TMA half-sweep per launch; ldg: fused with plain "
                          "loads; unfused: the reference's dataflow")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--strong", type=int, default=0, metavar="N",
+                    help="strong scaling (BASELINE.json configs[3]): a fixed N^3 global grid block-decomposed "
+                         "over the ranks (default: weak scaling, --n^3 per rank)")
     ap.add_argument("--force-dist", action="store_true",
                     help="take the multi-rank (NCCL) path even at one rank (a check of that path on one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -231,21 +234,30 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         uid = [sfb.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        ext = weak_extents(n, world)
+        ext = (args.strong,) * 3 if args.strong else weak_extents(n, world)
         # the temporal pass reads 2-deep halos across processor faces
         ghost = 2 if fused == 1 else 1
         d = sfb.decompose(ext, world, ghost)
-        assert all(d.size(w) == (n, n, n) for w in range(world)), d
+        if not args.strong:
+            assert all(d.size(w) == (n, n, n) for w in range(world)), d
         cfg = cavity_cfg(sfb, n, S)
         cfg.extents = ext
         sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), device=dev, fused=fused, rank=rank, world=world,
                              nccl_id=uid[0], ghost=ghost)
     else:
         ghost = 1
+        if args.strong:
+            n = args.strong
         cfg = cavity_cfg(sfb, n, S)
         sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=1, device=dev, fused=fused)
-    cells = n * n * n          # per rank
-    total_cells = cells * world
+    if args.strong:  # this rank's block of the fixed global grid
+        cells = 1
+        for a in sim.block_shape():
+            cells *= a
+        total_cells = args.strong ** 3
+    else:
+        cells = n * n * n          # per rank
+        total_cells = cells * world
     sim.init_cavity()
     stream = torch.cuda.ExternalStream(sim.stream, device=dev)
 
@@ -373,9 +385,11 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (lid-driven cavity from rest, init_cavity)",
-        "config": {"workload": (f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)"
+        "config": {"workload": (f"3D lid-driven cavity {args.strong}^3 fp64 global grid, strong scaling over {world} B200 (BASELINE.json configs[3]), {S} half-sweeps per step"
+                                if args.strong else
+                                f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)"
                                 if world == 1 else
                                 f"3D lid-driven cavity, {n}^3 per GPU weak scaling, global {list(cfg.extents)} block-decomposed over {world} B200 with NCCL ghost exchange (BASELINE.json configs[2]), {S} half-sweeps per step"),
                    "grid": list(cfg.extents), "ghost": ghost, "sweeps_per_step": S,
@@ -419,7 +433,7 @@ def run_reference(args):
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (lid-driven cavity from rest, init_cavity)",
         "config": {"workload": f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)",
                    "grid": [n, n, n], "ghost": 1, "sweeps_per_step": S, "parallelism": f"{th} CPU worker threads"},
