@@ -363,6 +363,12 @@ class simulation {
     cudaEventDestroy(t1_);
     for (auto e : timers_) cudaEventDestroy(e);
     drop_loop_graph();
+    if (xs_) {
+      cudaStreamSynchronize(xs_);
+      cudaStreamDestroy(xs_);
+      cudaEventDestroy(ev_fork_);
+      cudaEventDestroy(ev_join_);
+    }
     if (io_[0]) {
       for (int k = 0; k < 2; ++k) {
         cudaStreamSynchronize(io_[k]);
@@ -1502,6 +1508,11 @@ class simulation {
   unsigned long long table_epoch_ = 0;
   void* maps2_ = nullptr;  // temporal-pass descriptors (null: pass unavailable)
   void* uvmaps_ = nullptr;  // TMA UPDATE_VELOCITY descriptors (null: plain-load kernel)
+  cudaStream_t xs_ = nullptr;  // halo exchange overlapped with the temporal pass
+  const bool overlap_env_ = getenv("SF_NO_OVERLAP") == nullptr;
+  const bool force_overlap_ = getenv("SF_OVERLAP") != nullptr;  // also on one device (tests)
+  work_set empty_ws_{};
+  cudaEvent_t ev_fork_{}, ev_join_{};
   const bool uv_tma_env_ = getenv("SF_NO_UV_TMA") == nullptr;
   const bool temporal_env_ = getenv("SF_NO_TEMPORAL") == nullptr;
   std::vector<void*> dev_allocs_;
@@ -1972,24 +1983,95 @@ class simulation {
     return phases_.emplace(key, ph).first->second;
   }
 
-  void run_phase(const phase& ph, bool predicated) {
+  void run_phase(const phase& ph, bool predicated, cudaStream_t on = nullptr) {
     const sf_dev_ctl* pred = predicated ? dctl_ : nullptr;
+    cudaStream_t s = on ? on : st_;
     if (ph.first.n) {
-      launch_tasks(tview(), ph.first.d, ph.first.n, ph.first.max_count, pred, st_);
+      launch_tasks(tview(), ph.first.d, ph.first.n, ph.first.max_count, pred, s);
       ++launches_;
     }
     if (!ph.sends.empty() || !ph.recvs.empty()) {
       SF_NC(nccl()->GroupStart());
       for (const auto& m : ph.sends)
-        SF_NC(nccl()->Send(ph.sbuf + m.off, (size_t)m.count, kNcclFloat64, m.peer, comm_, st_));
+        SF_NC(nccl()->Send(ph.sbuf + m.off, (size_t)m.count, kNcclFloat64, m.peer, comm_, s));
       for (const auto& m : ph.recvs)
-        SF_NC(nccl()->Recv(ph.rbuf + m.off, (size_t)m.count, kNcclFloat64, m.peer, comm_, st_));
+        SF_NC(nccl()->Recv(ph.rbuf + m.off, (size_t)m.count, kNcclFloat64, m.peer, comm_, s));
       SF_NC(nccl()->GroupEnd());
     }
     if (ph.unpack.n) {
-      launch_tasks(tview(), ph.unpack.d, ph.unpack.n, ph.unpack.max_count, pred, st_);
+      launch_tasks(tview(), ph.unpack.d, ph.unpack.n, ph.unpack.max_count, pred, s);
       ++launches_;
     }
+  }
+
+  // The temporal pass with processor faces, split so the halo exchange
+  // overlaps compute. Interior tiles read no ghost cell: their S0 boxes
+  // (x in [i0-2, i0+33], y in [j0-2, j0+9], z in [k0-2, k1+1]) stay inside
+  // the owned block. Boundary tiles are the rest, covered by up to six slabs.
+  // All tile origins are even in x (the TMA start rule).
+  std::pair<const work_set*, const work_set*> pass_split() {
+    const int ty = sweep2_tile_y(), zc = zc_fused_;
+    char key[64];
+    std::snprintf(key, sizeof key, "split:%d:%d", zc, ty);
+    auto ii = items_.find(std::string(key) + ":i");
+    if (ii != items_.end()) return {&ii->second, &items_.find(std::string(key) + ":b")->second};
+    std::vector<sf_work> vi, vb;
+    int ci = 0, cb = 0;
+    auto add = [&](std::vector<sf_work>& v, int& cta, int b, const i64 lo[3], const i64 hi[3]) {
+      if (lo[0] >= hi[0] || lo[1] >= hi[1] || lo[2] >= hi[2]) return;
+      sf_work w{};
+      w.blk = b;
+      w.cta_begin = cta;
+      for (int a = 0; a < 3; ++a) {
+        w.lo[a] = lo[a];
+        w.hi[a] = hi[a];
+      }
+      w.tiles[0] = (int)((hi[0] - lo[0] + kTX - 1) / kTX);
+      w.tiles[1] = (int)((hi[1] - lo[1] + ty - 1) / ty);
+      w.tiles[2] = (int)((hi[2] - lo[2] + zc - 1) / zc);
+      cta += w.tiles[0] * w.tiles[1] * w.tiles[2];
+      v.push_back(w);
+    };
+    for (int b = 0; b < nloc_; ++b) {
+      const auto n = dec_.dims(gid_[b]);
+      // interior: x tiles from 32 with i0 + 33 <= n0 - 1, y tiles from ty
+      // with j0 + ty + 1 <= n1 - 1, z in [2, n2 - 2)
+      const i64 qx = n[0] >= 66 ? (n[0] - 66) / kTX + 1 : 0;
+      const i64 qy = n[1] >= 2 * ty + 2 ? (n[1] - 2 * ty - 2) / ty + 1 : 0;
+      const i64 ilo[3] = {kTX, ty, 2}, ihi[3] = {kTX + kTX * qx, ty + ty * qy, n[2] - 2};
+      const bool has_int = qx > 0 && qy > 0 && ihi[2] > ilo[2];
+      if (!has_int) {
+        const i64 lo[3] = {0, 0, 0}, hi[3] = {n[0], n[1], n[2]};
+        add(vb, cb, b, lo, hi);
+        continue;
+      }
+      add(vi, ci, b, ilo, ihi);
+      const i64 z0[3] = {0, 0, 0}, zl[3] = {n[0], n[1], ilo[2]};
+      const i64 z1[3] = {0, 0, ihi[2]}, zh[3] = {n[0], n[1], n[2]};
+      add(vb, cb, b, z0, zl);  // z slabs: whole x-y planes
+      add(vb, cb, b, z1, zh);
+      const i64 y0[3] = {0, 0, ilo[2]}, yl[3] = {n[0], ilo[1], ihi[2]};
+      const i64 y1[3] = {0, ihi[1], ilo[2]}, yh[3] = {n[0], n[1], ihi[2]};
+      add(vb, cb, b, y0, yl);  // y slabs: full x rows
+      add(vb, cb, b, y1, yh);
+      const i64 x0[3] = {0, ilo[1], ilo[2]}, xl[3] = {ilo[0], ihi[1], ihi[2]};
+      const i64 x1[3] = {ihi[0], ilo[1], ilo[2]}, xh[3] = {n[0], ihi[1], ihi[2]};
+      add(vb, cb, b, x0, xl);  // x slabs
+      add(vb, cb, b, x1, xh);
+    }
+    auto mk = [&](std::vector<sf_work>& v, int nctas) {
+      work_set ws;
+      ws.n = (int)v.size();
+      ws.nctas = nctas;
+      if (!v.empty()) {
+        ws.d = (sf_work*)dalloc(sizeof(sf_work) * v.size());
+        SF_CK(cudaMemcpy(ws.d, v.data(), sizeof(sf_work) * v.size(), cudaMemcpyHostToDevice));
+      }
+      return ws;
+    };
+    items_.emplace(std::string(key) + ":i", mk(vi, ci));
+    items_.emplace(std::string(key) + ":b", mk(vb, cb));
+    return {&items_.find(std::string(key) + ":i")->second, &items_.find(std::string(key) + ":b")->second};
   }
 
   // max over ranks of n accumulators (IEEE bit patterns of |x|): order-free,
@@ -2042,21 +2124,52 @@ class simulation {
       enqueue_half_sweep();
       return 1;
     }
-    const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, kTX, sweep2_tile_y());
-    if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
     const int fin = dist_ ? 0 : 1;
-    launch_sweep2(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_);
-    if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
+    if (!has_proc_faces()) {
+      const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, kTX, sweep2_tile_y());
+      if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
+      launch_sweep2(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_);
+      if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
+    } else {
+      // Processor faces: the pass reads 2-deep halos of vx, vy, vz, divu (p
+      // only on owned cells). The exchange of the state the previous unit
+      // left (redundant for the first unit, skipped once the loop is done)
+      // runs on the exchange stream while the interior tiles compute; the
+      // boundary tiles follow it. Both launches share one last-CTA count.
+      const unsigned mask = (1u << SF_VX) | (1u << SF_VY) | (1u << SF_VZ) | (1u << SF_DIVU);
+      if (!xs_) {
+        SF_CK(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
+        SF_CK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+        SF_CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+      }
+      // The split costs 2-5 % (boundary slabs run with little work per CTA):
+      // measured on one device, where the exchange is a few device copies,
+      // serialising is faster. Across ranks the exchange goes through NCCL and
+      // is hidden behind the interior (SF_NO_OVERLAP serialises there too).
+      const bool overlap = (dist_ || force_overlap_) && overlap_env_;
+      const auto split = pass_split();
+      const work_set& wi = overlap ? *split.first : empty_ws_;
+      const work_set& wb =
+          overlap ? *split.second : items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, kTX, sweep2_tile_y());
+      const unsigned total = (unsigned)(wi.nctas + wb.nctas);
+      SF_CK(cudaEventRecord(ev_fork_, st_));
+      SF_CK(cudaStreamWaitEvent(xs_, ev_fork_, 0));
+      for (int axis = 0; axis < 3; ++axis) run_phase(phase_for(mask, axis, SF_SCOPE_ALL, true), true, xs_);
+      SF_CK(cudaEventRecord(ev_join_, xs_));
+      if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
+      if (wi.nctas)
+        launch_sweep2(tview(wi), wi.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_,
+                      total);
+      SF_CK(cudaStreamWaitEvent(st_, ev_join_, 0));
+      launch_sweep2(tview(wb), wb.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_,
+                    total);
+      if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
+      ++launches_;
+    }
     ++iter_launch_;
     if (!fin) {
       allreduce_max(&dctl_->acc[0], 2);
       ctl(CTL_FINISH_PASS, 0.0, 0, 0, 0, 1);
-    }
-    // processor faces: the next pass reads 2-deep halos of the new state
-    // (vx, vy, vz, divu; p is read on owned cells only)
-    if (has_proc_faces()) {
-      const unsigned mask = (1u << SF_VX) | (1u << SF_VY) | (1u << SF_VZ) | (1u << SF_DIVU);
-      for (int axis = 0; axis < 3; ++axis) run_phase(phase_for(mask, axis, SF_SCOPE_ALL, true), true);
     }
     // predicated redo of the first sweep when the pass stopped after it
     int ftx, fty;

@@ -62,8 +62,11 @@ void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_cons
 struct sweep2_pins {
   double u, v, w, ul, vl, wl;
 };
+// total_ctas: CTAs of the whole pass when it is split over several launches
+// (the last one to finish finalises); 0 = this launch alone
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                   sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st);
+                   sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
+                   unsigned total_ctas = 0);
 size_t sweep2_maps_bytes();
 size_t sweep2_map_offset(int b, int f, int s);
 void sweep2_box(int field, int* bw, int* bh);

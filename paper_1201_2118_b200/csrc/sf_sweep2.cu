@@ -593,12 +593,13 @@ static int sweep2_prefetch() {
 
 template <int TYV, int NIN, int MINB>
 static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st) {
+                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
+                    unsigned total) {
   using G = geom<TYV>;
   ensure_smem_attr((const void*)k_sweep2<TYV, NIN, MINB>, G::smem_bytes(NIN));
   k_sweep2<TYV, NIN, MINB><<<nctas, dim3(G::TX, G::TY), G::smem_bytes(NIN), st>>>(
-      vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas, static_cast<const maps2_t*>(maps),
-      sweep2_prefetch(), fin, pins);
+      vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, total ? total : (unsigned)nctas,
+      static_cast<const maps2_t*>(maps), sweep2_prefetch(), fin, pins);
 }
 
 // SF_SWEEP2_VARIANT: 0 = 32x8 tile, 3 S0 stages, 2 CTAs/SM (default);
@@ -613,12 +614,13 @@ static int sweep2_variant() {
 }
 
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                   sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st) {
+                   sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
+                   unsigned total) {
   if (nctas <= 0) return;
   switch (sweep2_variant()) {
-    case 1: launch2<8, 6, 1>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st); break;
-    case 2: launch2<16, 3, 1>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st); break;
-    default: launch2<8, 3, 2>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st); break;
+    case 1: launch2<8, 6, 1>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total); break;
+    case 2: launch2<16, 3, 1>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total); break;
+    default: launch2<8, 3, 2>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total); break;
   }
 }
 

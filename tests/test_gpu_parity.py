@@ -570,3 +570,25 @@ def test_temporal_pass_cross_rank_finalize_on_one_rank(maxs):
     assert [[x.dt, x.sweeps, x.residual] for x in a] == [[x.dt, x.sweeps, x.residual] for x in b]
     assert d.kernel_timing("sweep2")[1] > 0
     assert d.checksum() == s.checksum() and d.pending_color == s.pending_color
+
+
+@pytest.mark.parametrize("ext,workers", [((136, 40, 24), 2), ((140, 84, 30), 4)])
+def test_temporal_pass_with_overlapped_halo_exchange_matches_the_reference(ref_available, ext, workers, monkeypatch):
+    # components large enough to have interior tiles: the pass runs as an
+    # interior launch overlapping the halo exchange on a second stream, then
+    # the boundary launch (one last-CTA count across both). Used across ranks;
+    # SF_OVERLAP forces it for grid components on one device.
+    monkeypatch.setenv("SF_OVERLAP", "1")
+    c = cavity_case(ext, symmetry_z=False, tolerance=1e-4, max_sweeps=41, ghost=2, workers=workers)
+    d = sfb.decompose(ext, workers, 2, (False, False, False))
+    assert any(d.size(w)[0] >= 66 and d.size(w)[1] >= 18 for w in range(workers))
+    o = Oracle(c, "ref")
+    o.init_cavity()
+    so = o.advance(2)
+    dv = dev_from_case(c, fused=1)
+    dv.init_cavity()
+    dv.set_kernel_timing(True)
+    dd = [dv.step() for _ in range(2)]
+    assert [[x.dt, x.sweeps, x.residual] for x in dd] == [[float(a), int(b), float(r)] for a, b, r in zip(*so)]
+    assert dv.kernel_timing("sweep2")[1] > 0
+    assert dv.checksum() == o.checksum()
