@@ -287,8 +287,8 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
     const int Di = st + IN_D / 8, Ui = st + IN_U / 8, Vi = st + IN_V / 8, Wi = st + IN_W / 8,
               Pi = st + IN_P / 8, Dz = stn + IN_D / 8;
     const int u1 = fo + U1 * EN, v1 = fo + V1 * EN, w1 = fo + W1 * EN, p1 = fo + P1 * EN;
-    const long long gk = B.lo[2] + z;
-    const int zpar = (int)(gk & 1);
+    const int gk = lo2 + z;
+    const int zpar = gk & 1;
     if (fast_xy && z >= zf_lo && z <= zf_hi) {
 #pragma unroll
       for (int r = 0; r < NE; ++r) {
@@ -309,8 +309,8 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
       }
       return;
     }
-    const bool zin = lo2 + z >= 0 && lo2 + z < N2;
-    const int bz = bin(s.per[2], gk, nm2), bzp = bnx(s.per[2], gk, nm2);
+    const bool zin = gk >= 0 && gk < N2;
+    const int bz = s.per[2] | ((gk > 0) & (gk < (int)nm2)), bzp = s.per[2] | (gk + 1 < (int)nm2);
     const bool pz = lo2 + z == N2 - 1, zlow = lo2 + z == -1;
 #pragma unroll
     for (int r = 0; r < NE; ++r) {
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   // ---- this thread's tile cell ----------------------------------------------
   const int i = i0 + tx, j = j0 + ty;
   const bool act = i < (int)wk.hi[0] && j < (int)wk.hi[1];
-  const long long gi = B.lo[0] + i, gj = B.lo[1] + j;
+  const int gi = lo0 + i, gj = lo1 + j;  // global indices fit in int
   const int bx = bin(s.per[0], gi, nm0), bxp = bnx(s.per[0], gi, nm0);
   const int by = bin(s.per[1], gj, nm1), byp = bnx(s.per[1], gj, nm1);
   const int bxm = bin(s.per[0], gi - 1, nm0), bxpm = bnx(s.per[0], gi - 1, nm0);
@@ -379,7 +379,8 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   const int ic = (bx << 2) | (by << 1), iex = (bxp << 2) | (by << 1), iey = (bx << 2) | (byp << 1);
   const int ixm = (bxm << 2) | (by << 1), ixpm = (bxpm << 2) | (by << 1);
   const int iym = (bx << 2) | (bym << 1), iypm = (bx << 2) | (bypm << 1);
-  const int par_col = (int)((gi + gj) & 1);
+  const int par_col = (gi + gj) & 1;
+  const int N2m1 = N2 - 1, nm2i = (int)nm2, per2 = s.per[2];
   const int q0 = (ty + 2) * EW + (tx + 2);
 
   double* __restrict__ Dn = tab->ptr[b][SF_DIVU][ALT];
@@ -467,8 +468,8 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         wm2 = wn;
       } else if (act) {
         const double dZp = d1p[q0];
-        const long long gk = B.lo[2] + z;
-        const int bz = bin(s.per[2], gk, nm2), bzp = bnx(s.per[2], gk, nm2);
+        const int gk = lo2 + z;
+        const int bz = per2 | ((gk > 0) & (gk < nm2i)), bzp = per2 | (gk + 1 < nm2i);
         const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
         const double dXm = d1[q0 - 1], dYm = d1[q0 - EW];
         const int par = par_col ^ (int)(gk & 1);
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         double wn = w1[q0] + cw * (d0 - ezv);
         if (gi == N0 - 1) un = pin_u;
         if (gj == N1 - 1) vn = pin_v;
-        if (gk == N2 - 1) wn = pin_w;
+        if (gk == N2m1) wn = pin_w;
         // swept -x / -y neighbours; at the low wall the pinned ghost (in S1)
         double umn, vmn;
         if (gi > 0) {
@@ -525,7 +526,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         }
         if (gi == N0 - 1) Dn[o + 1] = dd;
         if (gj == N1 - 1) Dn[o + sx] = dd;
-        if (gk == N2 - 1) Dn[o + sxy] = dd;
+        if (gk == N2m1) Dn[o + sxy] = dd;
         const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
         r1 = b1 > r1 ? b1 : r1;
         r2 = b2 > r2 ? b2 : r2;
