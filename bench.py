@@ -62,6 +62,7 @@ def parse_args():
                     help="cavity = configs[1] (headline); stencil = configs[4], a descriptor-declared "
                          "high-order Laplacian (radius 2 or 3) JIT-compiled from its point function")
     ap.add_argument("--radius", type=int, default=2)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"], help="field storage for --workload stencil")
     ap.add_argument("--tile", default="32,8,64", help="descriptor TILE for --workload stencil")
     return ap.parse_args()
 
@@ -473,7 +474,8 @@ def run_stencil(args):
     """configs[4]: a ghost-width-2/3 stencil declared as an execution plan +
     point-function body (the reference's user-kernel path, executor.hpp:484),
     JIT-compiled for sm_100a.  One step = exchange(u) + run_kernel over the grid.
-    Algorithmic bytes: read u, write lu = 16 B/cell (fp64)."""
+    Algorithmic bytes: read u, write lu = 16 B/cell in fp64, 8 in fp32
+    (--dtype f32: fields stored in fp32, point function computes in fp64)."""
     import numpy as np
     import torch
 
@@ -486,8 +488,9 @@ def run_stencil(args):
     tile = tuple(int(x) for x in args.tile.split(","))
     cfg = sfb.SolverConfig(extents=(n, n, n), periodic=(True, True, True))
     sim = sfb.Simulation(cfg, sfb.FluidParams(), workers=1, ghost=r, device=local)
-    sim.create_field("u")
-    sim.create_field("lu")
+    es = 4 if args.dtype == "f32" else 8
+    sim.create_field("u", dtype=args.dtype)
+    sim.create_field("lu", dtype=args.dtype)
     sim.scatter("u", np.random.default_rng(1).uniform(-1, 1, size=(n, n, n)))
     name = f"LAP{2 * r}"
     sim.register_kernel(sfb.ExecutionPlan(name, tile, (r,) * 6, [("u", "IN", True), ("lu", "OUT")]),
@@ -517,18 +520,18 @@ def run_stencil(args):
     ms = e0.elapsed_time(e1)
     cells = n ** 3
     peak, src = measured_peaks()
-    ach = 16.0 * cells / (kms / args.steps / 1e3) / 1e9
+    ach = 2.0 * es * cells / (kms / args.steps / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": round(cells * args.steps / (ms / 1e3) / 1e6, 2), "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic (uniform random field)",
-        "config": {"workload": f"configs[4]: radius-{r} Laplacian ({6 * r + 1}-point, order {2 * r}) at {n}^3 fp64, "
+        "config": {"workload": f"configs[4]: radius-{r} Laplacian ({6 * r + 1}-point, order {2 * r}) at {n}^3 {'fp32' if es == 4 else 'fp64'}, "
                                f"ghost width {r}, descriptor TILE {tile}, periodic, exchange + run_kernel per step",
                    "grid": [n, n, n], "ghost": r, "tile": list(tile)},
         "roofline": {"bound": "hbm", "kernel": f"sf_user_kernel ({name}, NVRTC)", "achieved": round(ach, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
-                     "algorithmic_bytes_per_launch": 16 * cells, "avg_launch_ms": round(kms / args.steps, 4),
+                     "algorithmic_bytes_per_launch": 2 * es * cells, "avg_launch_ms": round(kms / args.steps, 4),
                      "peak_source": src},
         "gpu_launches": sim.launch_count(), "clocks": clk,
     }

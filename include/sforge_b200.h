@@ -223,6 +223,11 @@ typedef struct sf_plan {
 } sf_plan;
 /* field_store::create (field.hpp:108-112); stagger -1 none, 0/1/2 = x/y/z. */
 int sf_sim_create_field(sf_sim* s, const char* name, int stagger);
+/* The same with fp32 storage (value_bytes 4) or fp64 (8). An fp32 field is
+ * exchanged, reduced and read by descriptor kernels like any field; its
+ * values cross this interface as fp64 (gather widens exactly, scatter rounds
+ * to nearest), and kernels compute on them in fp64 and store rounded. */
+int sf_sim_create_field_typed(sf_sim* s, const char* name, int stagger, int value_bytes);
 /* executor::register_kernel with the point function given as the CUDA C++
  * BODY of `void f(const point_ctx& c)` against the reference's accessors
  * (c.field(s)(di,dj,dk), .load(), .store(v), c.param(s), c.i/c.j/c.k;

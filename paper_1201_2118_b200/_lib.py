@@ -186,6 +186,7 @@ SIGNATURES = [
     ("sf_sim_run_kernel", [_vp, _cp, _cpp, _dp, _i, _i], _i),
     ("sf_sim_reduce", [_vp, _cp, _i, _dp], _i),
     ("sf_sim_create_field", [_vp, _cp, _i], _i),
+    ("sf_sim_create_field_typed", [_vp, _cp, _i, _i], _i),
     ("sf_sim_register_kernel", [_vp, C.POINTER(Plan), _cpp, _i, _cpp, _i, _cp], _i),
     ("sf_sim_set_face_bc", [_vp, _i, _i, _i, _dp], _i),
     ("sf_sim_physical_bc", [_vp, _cpp, _i], _i),

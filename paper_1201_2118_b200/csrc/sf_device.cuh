@@ -49,6 +49,9 @@ struct sf_dev_table {
   double* ptr[kMaxBlocks][kMaxFields][kSlots];
   // physical buffer (0..2) occupying each slot: selects the TMA descriptor
   unsigned char bidx[kMaxBlocks][kMaxFields][kSlots];
+  // bytes per value of each field: 8 (fp64; every CFD field) or 4 (fp32 user
+  // fields). An fp32 field uses the block's padded layout in elements.
+  unsigned char esize[kMaxFields];
 };
 
 // Device control block of the pressure loop.  acc[] are max accumulators on
@@ -95,6 +98,7 @@ struct table_view {
   __device__ __forceinline__ const sf_dev_block& blk(int b) const { return tab->blk[b]; }
   __device__ __forceinline__ double* ptr(int b, int f, int s) const { return tab->ptr[b][f][s]; }
   __device__ __forceinline__ const sf_work* work() const { return items; }
+  __device__ __forceinline__ int esize(int f) const { return tab->esize[f]; }
 };
 
 constexpr int kDirectItems = 8;
@@ -106,6 +110,7 @@ struct direct_view {
   __device__ __forceinline__ const sf_dev_block& blk(int) const { return b0; }
   __device__ __forceinline__ double* ptr(int, int f, int s) const { return p[f][s]; }
   __device__ __forceinline__ const sf_work* work() const { return it; }
+  __device__ __forceinline__ int esize(int) const { return 8; }
 };
 
 // Global (all-block) constants of the CFD kernels: step_constants

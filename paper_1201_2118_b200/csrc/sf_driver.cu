@@ -401,7 +401,8 @@ class simulation {
 
   // field_store::create (field.hpp:108-112): a zero-filled front buffer on
   // every local component; stagger -1 none, 0/1/2 = x/y/z (field.hpp:23)
-  int create_field(const std::string& name, int stagger) {
+  int create_field(const std::string& name, int stagger, int esize = 8) {
+    if (esize != 8 && esize != 4) throw error(SF_ERR_ARG, "fields hold fp64 (8) or fp32 (4) values");
     for (const auto& n : fname_)
       if (n == name) throw error(SF_ERR_GRID, "field '" + name + "' already exists");
     if ((int)fname_.size() >= kMaxFields)
@@ -411,6 +412,8 @@ class simulation {
     const int f = (int)fname_.size();
     fname_.push_back(name);
     fstag_.push_back(stagger);
+    fes_.push_back(esize);
+    htab_->esize[f] = (unsigned char)esize;
     for (int b = 0; b < nloc_; ++b) alloc_slot(b, f, FRONT);
     upload_table();
     return f;
@@ -496,7 +499,7 @@ class simulation {
       const auto& L = lay_[b];
       const i64 n[3] = {L.dims[0], L.dims[1], L.dims[2]};
       const i64 lo[3] = {L.lo[0], L.lo[1], L.lo[2]};
-      launch_gather_owned(htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, n, lo, N, dglobal, 0, st_);
+      launch_gather_owned(htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, n, lo, N, dglobal, 0, st_, fes_[f]);
       ++launches_;
     }
     check_launch();
@@ -509,7 +512,7 @@ class simulation {
       const i64 n[3] = {L.dims[0], L.dims[1], L.dims[2]};
       const i64 lo[3] = {L.lo[0], L.lo[1], L.lo[2]};
       launch_gather_owned(htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, n, lo, N,
-                          const_cast<double*>(dglobal), 1, st_);
+                          const_cast<double*>(dglobal), 1, st_, fes_[f]);
       ++launches_;
     }
     check_launch();
@@ -529,7 +532,7 @@ class simulation {
     const auto& L = lay_[0];
     const i64 n[3] = {L.dims[0], L.dims[1], L.dims[2]};
     const i64 z[3] = {0, 0, 0};
-    launch_copy_box(htab_->ptr[0][f][FRONT], L.base, L.sx, L.sy, snd, 0, n[0], n[1], z, n, z, st_);
+    launch_copy_box_es(htab_->ptr[0][f][FRONT], fes_[f], L.base, L.sx, L.sy, snd, 8, 0, n[0], n[1], z, n, z, st_);
     ++launches_;
     SF_NC(nccl()->AllGather(snd, all, (size_t)maxc, kNcclFloat64, comm_, st_));
     std::vector<double> h((size_t)(maxc * world_));
@@ -564,6 +567,25 @@ class simulation {
     const auto& L = lay_[b];
     const i64 d[3] = {L.dims[0], L.dims[1], L.dims[2]};
     if (n < d[0] * d[1] * d[2]) throw error(SF_ERR_ARG, "block buffer too small");
+    if (fes_[f] != 8) {  // fp32 field: host values are fp64, converted through the staging buffer
+      download_table();
+      double* sg = staging();
+      const i64 z[3] = {0, 0, 0};
+      const size_t bytes = sizeof(double) * (size_t)(d[0] * d[1] * d[2]);
+      if (to_device) {
+        SF_CK(cudaMemcpyAsync(sg, host, bytes, cudaMemcpyHostToDevice, st_));
+        launch_copy_box_es(sg, 8, 0, d[0], d[1], htab_->ptr[b][f][FRONT], fes_[f], L.base, L.sx, L.sy, z, d, z,
+                           st_);
+        ghosts_ok_[fname_[f]] = false;
+      } else {
+        launch_copy_box_es(htab_->ptr[b][f][FRONT], fes_[f], L.base, L.sx, L.sy, sg, 8, 0, d[0], d[1], z, d, z,
+                           st_);
+        SF_CK(cudaMemcpyAsync(host, sg, bytes, cudaMemcpyDeviceToHost, st_));
+      }
+      ++launches_;
+      sync();
+      return;
+    }
     download_table(false);
     if (!io_[0]) {
       for (int k = 0; k < 2; ++k) SF_CK(cudaStreamCreateWithFlags(&io_[k], cudaStreamNonBlocking));
@@ -638,8 +660,8 @@ class simulation {
     double* sg = (double*)dalloc_tmp(sizeof(double) * (size_t)(ld[0] * ld[1] * ld[2]));
     const i64 slo[3] = {-g, -g, -g};
     const i64 zero[3] = {0, 0, 0};
-    launch_copy_box(htab_->ptr[w][f][FRONT], L.base, L.sx, L.sy, sg, 0, ld[0], ld[1], slo, ld, zero,
-                    st_);
+    launch_copy_box_es(htab_->ptr[w][f][FRONT], fes_[f], L.base, L.sx, L.sy, sg, 8, 0, ld[0], ld[1], slo, ld,
+                       zero, st_);
     ++launches_;
     check_launch();
     SF_CK(cudaMemcpyAsync(host, sg, sizeof(double) * (size_t)(ld[0] * ld[1] * ld[2]),
@@ -787,9 +809,13 @@ class simulation {
     std::vector<int> cs;
     for (size_t i = 0; i < bfields.size(); ++i)
       if (i < cached.size() && cached[i] && uk.intent[i] != 1) cs.push_back((int)i);
-    if (!cs.empty() && uk.tx % 2 == 0 && !getenv("SF_JIT_NO_TMA")) {
-      const int xl = (halo[0] + 1) / 2 * 2;
-      const int bw = (xl + uk.tx + halo[1] + 1) / 2 * 2;
+    // TMA box x start and row bytes must be 16-byte multiples: 2 fp64 or 4 fp32
+    int xa = 2;
+    for (int c : cs)
+      if (fes_[uk.fid[c]] == 4) xa = 4;
+    if (!cs.empty() && uk.tx % xa == 0 && !getenv("SF_JIT_NO_TMA")) {
+      const int xl = (halo[0] + xa - 1) / xa * xa;
+      const int bw = (xl + uk.tx + halo[1] + xa - 1) / xa * xa;
       const int bh = halo[2] + uk.ty + halo[3];
       const int ring = halo[4] + halo[5] + 1 + 3;  // window + one round (2 planes) + 1 in flight
       const size_t smem = (size_t)cs.size() * ring * ((bw * bh + 15) / 16 * 16) * 8;
@@ -834,6 +860,9 @@ class simulation {
     src += "__device__ constexpr int SF_READABLE[] = {" + rdb + "};\n";
     src += "__device__ constexpr int SF_WRITABLE[] = {" + wrb + "};\n";
     src += "__device__ constexpr int SF_CENTER_ONLY[] = {" + cen + "};\n";
+    std::string f32;
+    for (size_t i = 0; i < uk.fid.size(); ++i) f32 += (i ? "," : "") + std::string(fes_[uk.fid[i]] == 4 ? "1" : "0");
+    src += "__device__ constexpr int SF_F32[] = {" + f32 + "};\n";
     src += "__device__ constexpr int SF_HALO[] = {";
     for (int a = 0; a < 6; ++a) src += (a ? "," : "") + std::to_string(uk.halo[a]);
     src += "};\n#define SF_DEBUG " + std::string(debug_bounds() ? "1" : "0") + "\n";
@@ -854,6 +883,9 @@ class simulation {
       src += "#define SF_NC " + std::to_string(uk.cslot.size()) + "\n__device__ constexpr int SF_CSLOT[] = {" + csl +
              "};\n#define SF_XL " + std::to_string(uk.xl) + "\n#define SF_BW " + std::to_string(uk.bw) +
              "\n#define SF_BH " + std::to_string(uk.bh) + "\n#define SF_R " + std::to_string(uk.ring) + "\n";
+      size_t txb = 0;  // bytes one plane of every cached binding brings in
+      for (int c : uk.cslot) txb += (size_t)uk.bw * uk.bh * fes_[uk.fid[c]];
+      src += "#define SF_TXB " + std::to_string(txb) + "\n";
     }
     std::string tmpl = uk.tma ? jit_template_tma() : jit_template();
     const size_t at = tmpl.find("SF_BODY");
@@ -1127,7 +1159,7 @@ class simulation {
           if (!p) continue;
           const sf_layout& L = lay_[b];
           if (encode_box_map(hm.data() + 128 * ((b * uk.cslot.size() + c) * kSlots + sl), p, L.sx, L.sy, L.sz,
-                             uk.bw, uk.bh))
+                             uk.bw, uk.bh, fes_[f]))
             throw error(SF_ERR_CUDA, "cuTensorMapEncodeTiled failed for kernel '" + uk.name + "'");
         }
       }
@@ -1478,6 +1510,7 @@ class simulation {
   void* geo_ = nullptr;  // per local block: n[3], lo[3], sx, sy, base (sf_jit.hpp sf_geo)
   std::vector<std::string> fname_ = {"vx", "vy", "vz", "p", "divu"};
   std::vector<int> fstag_ = {0, 1, 2, -1, -1};  // stagger per field (field.hpp:23)
+  std::vector<int> fes_ = {8, 8, 8, 8, 8};       // bytes per value per field (user fields: 8 or 4)
   int rank_ = 0, world_ = 1;
   bool dist_ = false;  // NCCL transport (one grid component per rank)
   decomposition dec_;
@@ -1624,6 +1657,7 @@ class simulation {
 
   void allocate() {
     htab_ = std::make_unique<sf_dev_table>();
+    for (int f = 0; f < kMaxFields; ++f) htab_->esize[f] = 8;
     std::memset(htab_.get(), 0, sizeof(sf_dev_table));
     htab_->nblocks = nloc_;
     lay_.resize(nloc_);
@@ -1766,10 +1800,12 @@ class simulation {
   void upload_table() {
     SF_CK(cudaMemcpy(dtab_->ptr, htab_->ptr, sizeof(htab_->ptr), cudaMemcpyHostToDevice));
     SF_CK(cudaMemcpy(dtab_->bidx, htab_->bidx, sizeof(htab_->bidx), cudaMemcpyHostToDevice));
+    SF_CK(cudaMemcpy(dtab_->esize, htab_->esize, sizeof(htab_->esize), cudaMemcpyHostToDevice));
   }
+  int field_esize(int f) const { return fes_[f]; }
   void alloc_slot(int b, int f, int s) {
     const sf_layout& L = lay_[b];
-    const size_t bytes = sizeof(double) * (size_t)(L.sx * L.sy * L.sz);
+    const size_t bytes = (size_t)fes_[f] * (size_t)(L.sx * L.sy * L.sz);
     double* p = (double*)dalloc(bytes);
     SF_CK(cudaMemsetAsync(p, 0, bytes, st_));
     htab_->ptr[b][f][s] = p;
@@ -2629,6 +2665,12 @@ int sf_sim_reduce(sf_sim* s, const char* field, int op, double* out) {
     need(out, "out");
     if (op < 0 || op > 3) throw sfb::error(SF_ERR_ARG, "bad reduce op");
     *out = SIM(s).reduce(SIM(s).field_id(field), op);
+  });
+}
+int sf_sim_create_field_typed(sf_sim* s, const char* name, int stagger, int value_bytes) {
+  return guarded([&] {
+    need(name, "name");
+    SIM(s).create_field(name, stagger, value_bytes);
   });
 }
 int sf_sim_create_field(sf_sim* s, const char* name, int stagger) {

@@ -95,14 +95,18 @@ struct cell_view {
     if (di < -SF_HALO[0] || di > SF_HALO[1] || dj < -SF_HALO[2] || dj > SF_HALO[3] || dk < -SF_HALO[4] ||
         dk > SF_HALO[5]) { sf_violation(3, slot, di, dj, dk); return 0.0; }
 #endif
-    return rd[o + di + dj * sx + dk * sxy];
+    const long long q = o + di + dj * sx + dk * sxy;
+    return SF_F32[slot] ? (double)reinterpret_cast<const float*>(rd)[q] : rd[q];  // fp32 fields widen
   }
   __device__ __forceinline__ double load() const { return (*this)(0, 0, 0); }
   __device__ __forceinline__ void store(double v) const {
 #if SF_DEBUG
     if (!SF_WRITABLE[slot]) { sf_violation(4, slot, 0, 0, 0); return; }
 #endif
-    __stwb(wr + o, v);
+    if (SF_F32[slot])
+      reinterpret_cast<float*>(wr)[o] = (float)v;  // fp32 fields round to nearest
+    else
+      __stwb(wr + o, v);
   }
 };
 
@@ -208,15 +212,29 @@ struct cell_view {
     // the column itself comes from the register queue: one shared-memory load
     // per plane instead of one per z offset (offsets fold to constants)
     if (SF_CACHED[slot] && di == 0 && dj == 0) return zq[dk + SF_HALO[4]];
-    if (SF_CACHED[slot]) return rb[zoff[dk + SF_HALO[4]] + dj * SF_BW + di];
-    return SF_CENTER_ONLY[slot] ? __ldcg(rd + o + di + dj * sx + dk * sxy) : __ldg(rd + o + di + dj * sx + dk * sxy);
+    if (SF_CACHED[slot]) return ring(zoff[dk + SF_HALO[4]], dj * SF_BW + di);
+    const long long q = o + di + dj * sx + dk * sxy;
+    if (SF_F32[slot]) {  // fp32 fields widen exactly
+      const float* f = reinterpret_cast<const float*>(rd);
+      return (double)(SF_CENTER_ONLY[slot] ? __ldcg(f + q) : __ldg(f + q));
+    }
+    return SF_CENTER_ONLY[slot] ? __ldcg(rd + q) : __ldg(rd + q);
+  }
+  // ring plane at offset zo (in fp64 slots; an fp32 plane uses the first half),
+  // element e of the box relative to this cell
+  __device__ __forceinline__ double ring(int zo, int e) const {
+    if (SF_F32[slot]) return (double)reinterpret_cast<const float*>(rb)[2 * zo + e];
+    return rb[zo + e];
   }
   __device__ __forceinline__ double load() const { return (*this)(0, 0, 0); }
   __device__ __forceinline__ void store(double v) const {
 #if SF_DEBUG
     if (!SF_WRITABLE[slot]) { sf_violation(4, slot, 0, 0, 0); return; }
 #endif
-    __stwb(wr + o, v);
+    if (SF_F32[slot])
+      reinterpret_cast<float*>(wr)[o] = (float)v;  // fp32 fields round to nearest
+    else
+      __stwb(wr + o, v);
   }
 };
 
@@ -271,7 +289,7 @@ sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
   auto issue = [&](int q) {  // load plane q (z = k0 - hzl + q) of every cached binding
     const int slot = q % SF_R;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bars[slot])),
-                 "r"((unsigned)(SF_NC * SF_BW * SF_BH * 8)) : "memory");
+                 "r"((unsigned)(SF_TXB)) : "memory");
     for (int c = 0; c < SF_NC; ++c) {
       const int b = SF_CSLOT[c];
       const int phys = bidx[(w.blk * SF_MAXF + SF_FID[b]) * SF_SLOTS + 0];
@@ -301,7 +319,11 @@ sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
     c.f_[s].sx = sx;
     c.f_[s].sxy = sxy;
     c.f_[s].slot = s;
-    c.f_[s].rb = sring + SF_CIDX[s] * SF_R * SF_PLANE + (ty + SF_HALO[2]) * SF_BW + tx + SF_XL;
+    {  // ring base of this binding + this cell's in-plane element (fp32 planes hold floats)
+      const double* base = sring + SF_CIDX[s] * SF_R * SF_PLANE;
+      const int e = (ty + SF_HALO[2]) * SF_BW + tx + SF_XL;
+      c.f_[s].rb = SF_F32[s] ? reinterpret_cast<const double*>(reinterpret_cast<const float*>(base) + e) : base + e;
+    }
   }
   c.i = G.lo[0] + i;
   c.j = G.lo[1] + j;
@@ -330,11 +352,11 @@ sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
           if (SF_CACHED[s]) {  // column queue: shift in the plane that entered the window
             if (kq == 0) {
 #pragma unroll
-              for (int t = 0; t < SF_ZW; ++t) c.f_[s].zq[t] = c.f_[s].rb[zr[t]];
+              for (int t = 0; t < SF_ZW; ++t) c.f_[s].zq[t] = c.f_[s].ring(zr[t], 0);
             } else {
 #pragma unroll
               for (int t = 0; t < SF_ZW - 1; ++t) c.f_[s].zq[t] = c.f_[s].zq[t + 1];
-              c.f_[s].zq[SF_ZW - 1] = c.f_[s].rb[zr[SF_ZW - 1]];
+              c.f_[s].zq[SF_ZW - 1] = c.f_[s].ring(zr[SF_ZW - 1], 0);
             }
           }
         }

@@ -58,42 +58,10 @@ __device__ __forceinline__ bool pred_done(const sf_dev_ctl* ctl) {
 // ---------------------------------------------------------------------------
 // ghost refresh tasks
 // ---------------------------------------------------------------------------
-template <class View>
-__global__ void k_tasks(View vw, const sf_task* __restrict__ tasks,
-                        const sf_dev_ctl* pred) {
-  if (pred && pred_done(pred)) return;
-  const sf_task& T = tasks[blockIdx.y];
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  if (T.type == 2 || T.type == 3) {  // message pack / unpack (exchange.hpp:165-224)
-    const sf_dev_block& Bk = vw.blk(T.dst_blk);
-    double* f = vw.ptr(T.dst_blk, T.field, FRONT);
-    const long long nx = T.dims[0], nxy = T.dims[0] * T.dims[1];
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < T.count; e += stride) {
-      const long long kk = e / nxy, rem = e - kk * nxy, jj = rem / nx, ii = rem - jj * nx;
-      const long long o = off(Bk, T.lo[0] + ii, T.lo[1] + jj, T.lo[2] + kk);
-      if (T.type == 2)
-        T.buf[e] = f[o];
-      else
-        f[o] = T.buf[e];
-    }
-    return;
-  }
-  if (T.type == 0) {
-    const sf_dev_block& S = vw.blk(T.src_blk);
-    const sf_dev_block& D = vw.blk(T.dst_blk);
-    const double* src = vw.ptr(T.src_blk, T.field, FRONT);
-    double* dst = vw.ptr(T.dst_blk, T.field, FRONT);
-    const long long nx = T.dims[0], nxy = T.dims[0] * T.dims[1];
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < T.count; e += stride) {
-      const long long kk = e / nxy, rem = e - kk * nxy, jj = rem / nx, ii = rem - jj * nx;
-      dst[off(D, T.dlo[0] + ii, T.dlo[1] + jj, T.dlo[2] + kk)] =
-          src[off(S, T.lo[0] + ii, T.lo[1] + jj, T.lo[2] + kk)];
-    }
-    return;
-  }
-  // bc_face (exchange.hpp:231-480): one thread per tangential line.
-  const sf_dev_block& B = vw.blk(T.dst_blk);
-  double* f = vw.ptr(T.dst_blk, T.field, FRONT);
+// bc_face (exchange.hpp:231-480) on element type E: one thread per
+// tangential line. For fp64 the arithmetic is the reference's (2.0 * v - src).
+template <class E>
+__device__ __forceinline__ void bc_task(const sf_task& T, const sf_dev_block& B, E* f, long long stride) {
   const int a = T.axis;
   const int t1 = a == 0 ? 1 : 0;
   const int t2 = a == 2 ? 1 : 2;
@@ -107,15 +75,15 @@ __global__ void k_tasks(View vw, const sf_task* __restrict__ tasks,
     c[a] = 0;
     const long long o0 = off(B, c[0], c[1], c[2]);  // position 0 along the axis
 #define LINE(pos) f[o0 + (long long)(pos) * astr]
-    const double v = T.v;
+    const E v = (E)T.v;
     if (T.normal) {
       if (T.kind == SF_BC_WALL || T.kind == SF_BC_SYMMETRY) {
         if (T.side == 0) {
           if (T.scope != SF_SCOPE_OWNED_ONLY) {
             LINE(-1) = v;
             for (long long m = 2; m <= g; ++m) {
-              const double src = LINE(m - 2);
-              LINE(-m) = 2.0 * v - src;
+              const E src = LINE(m - 2);
+              LINE(-m) = (E)2 * v - src;
             }
           }
         } else {
@@ -127,16 +95,16 @@ __global__ void k_tasks(View vw, const sf_task* __restrict__ tasks,
             LINE(b - 1) = v;
           if (T.scope != SF_SCOPE_OWNED_ONLY)
             for (long long m = 1; m <= g; ++m) {
-              const double src = LINE(b - 1 - m);
-              LINE(b - 1 + m) = 2.0 * v - src;
+              const E src = LINE(b - 1 - m);
+              LINE(b - 1 + m) = (E)2 * v - src;
             }
         }
       } else if (T.kind == SF_BC_OUTFLOW && T.scope != SF_SCOPE_OWNED_ONLY) {
         if (T.side == 0) {
-          const double v0 = LINE(0);
+          const E v0 = LINE(0);
           for (long long m = 1; m <= g; ++m) LINE(-m) = v0;
         } else {
-          const double v0 = LINE(b - 1);
+          const E v0 = LINE(b - 1);
           for (long long m = 1; m <= g; ++m) LINE(b - 1 + m) = v0;
         }
       }
@@ -144,13 +112,13 @@ __global__ void k_tasks(View vw, const sf_task* __restrict__ tasks,
       if (T.kind == SF_BC_WALL && T.velocity) {
         if (T.side == 0)
           for (long long m = 1; m <= g; ++m) {
-            const double src = LINE(m - 1);
-            LINE(-m) = 2.0 * v - src;
+            const E src = LINE(m - 1);
+            LINE(-m) = (E)2 * v - src;
           }
         else
           for (long long m = 1; m <= g; ++m) {
-            const double src = LINE(b - m);
-            LINE(b - 1 + m) = 2.0 * v - src;
+            const E src = LINE(b - m);
+            LINE(b - 1 + m) = (E)2 * v - src;
           }
       } else if (T.kind == SF_BC_WALL || T.kind == SF_BC_SYMMETRY) {
         if (T.side == 0)
@@ -159,16 +127,66 @@ __global__ void k_tasks(View vw, const sf_task* __restrict__ tasks,
           for (long long m = 1; m <= g; ++m) LINE(b - 1 + m) = LINE(b - m);
       } else if (T.kind == SF_BC_OUTFLOW) {
         if (T.side == 0) {
-          const double v0 = LINE(0);
+          const E v0 = LINE(0);
           for (long long m = 1; m <= g; ++m) LINE(-m) = v0;
         } else {
-          const double v0 = LINE(b - 1);
+          const E v0 = LINE(b - 1);
           for (long long m = 1; m <= g; ++m) LINE(b - 1 + m) = v0;
         }
       }
     }
 #undef LINE
   }
+}
+
+template <class View>
+__global__ void k_tasks(View vw, const sf_task* __restrict__ tasks,
+                        const sf_dev_ctl* pred) {
+  if (pred && pred_done(pred)) return;
+  const sf_task& T = tasks[blockIdx.y];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const bool f32 = vw.esize(T.field) == 4;
+  if (T.type == 2 || T.type == 3) {  // message pack / unpack (exchange.hpp:165-224)
+    // fp32 values travel as exact fp64 conversions (message sizes stay fp64)
+    const sf_dev_block& Bk = vw.blk(T.dst_blk);
+    double* f = vw.ptr(T.dst_blk, T.field, FRONT);
+    float* ff = reinterpret_cast<float*>(f);
+    const long long nx = T.dims[0], nxy = T.dims[0] * T.dims[1];
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < T.count; e += stride) {
+      const long long kk = e / nxy, rem = e - kk * nxy, jj = rem / nx, ii = rem - jj * nx;
+      const long long o = off(Bk, T.lo[0] + ii, T.lo[1] + jj, T.lo[2] + kk);
+      if (T.type == 2)
+        T.buf[e] = f32 ? (double)ff[o] : f[o];
+      else if (f32)
+        ff[o] = (float)T.buf[e];
+      else
+        f[o] = T.buf[e];
+    }
+    return;
+  }
+  if (T.type == 0) {
+    const sf_dev_block& S = vw.blk(T.src_blk);
+    const sf_dev_block& D = vw.blk(T.dst_blk);
+    const double* src = vw.ptr(T.src_blk, T.field, FRONT);
+    double* dst = vw.ptr(T.dst_blk, T.field, FRONT);
+    const long long nx = T.dims[0], nxy = T.dims[0] * T.dims[1];
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < T.count; e += stride) {
+      const long long kk = e / nxy, rem = e - kk * nxy, jj = rem / nx, ii = rem - jj * nx;
+      const long long od = off(D, T.dlo[0] + ii, T.dlo[1] + jj, T.dlo[2] + kk);
+      const long long os = off(S, T.lo[0] + ii, T.lo[1] + jj, T.lo[2] + kk);
+      if (f32)
+        reinterpret_cast<float*>(dst)[od] = reinterpret_cast<const float*>(src)[os];
+      else
+        dst[od] = src[os];
+    }
+    return;
+  }
+  const sf_dev_block& B = vw.blk(T.dst_blk);
+  double* f = vw.ptr(T.dst_blk, T.field, FRONT);
+  if (f32)
+    bc_task<float>(T, B, reinterpret_cast<float*>(f), stride);
+  else
+    bc_task<double>(T, B, f, stride);
 }
 
 template <class View>
@@ -607,9 +625,12 @@ __global__ void __launch_bounds__(kTX* kTY) k_reduce_max(View vw, int zc, int f0
       if (q >= nfields) break;
       const double* __restrict__ F = vw.ptr(t.blk, fl[q], FRONT);
       const double* __restrict__ Bk = vw.ptr(t.blk, fl[q], BACK);
+      const bool f32 = vw.esize(fl[q]) == 4;  // fp32 values widen exactly
       for (long long k = t.k0; k < t.k1; ++k) {
         const long long o = off(B, t.i, t.j, k);
-        const double a = diff ? fabs(__ldg(F + o) - __ldg(Bk + o)) : fabs(__ldg(F + o));
+        const double x = f32 ? (double)__ldg(reinterpret_cast<const float*>(F) + o) : __ldg(F + o);
+        const double a = diff ? fabs(x - (f32 ? (double)__ldg(reinterpret_cast<const float*>(Bk) + o) : __ldg(Bk + o)))
+                              : fabs(x);
         const unsigned long long bb = abs_bits(a);
         mx[q] = bb > mx[q] ? bb : mx[q];
       }
@@ -646,10 +667,12 @@ __global__ void __launch_bounds__(kTX* kTY) k_reduce_sum(View vw, int zc, int fi
   const tile_loc t = locate(vw.work(), vw.nitems, zc);
   const sf_dev_block& B = vw.blk(t.blk);
   const double* __restrict__ F = vw.ptr(t.blk, field, FRONT);
+  const bool f32 = vw.esize(field) == 4;
   double acc = 0.0;
   if (t.act)
     for (long long k = t.k0; k < t.k1; ++k) {
-      const double x = __ldg(F + off(B, t.i, t.j, k));
+      const long long o = off(B, t.i, t.j, k);
+      const double x = f32 ? (double)__ldg(reinterpret_cast<const float*>(F) + o) : __ldg(F + o);
       acc += square ? x * x : x;
     }
   __shared__ double red[kTX * kTY];
@@ -885,8 +908,11 @@ void launch_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, int op,
 // ---------------------------------------------------------------------------
 // raw box copies (level-2 ABI, gather / scatter)
 // ---------------------------------------------------------------------------
-__global__ void k_copy_box(const double* __restrict__ src, long long s_base, long long s_sx,
-                           long long s_sy, double* __restrict__ dst, long long d_base,
+// element types S -> D (fp32 <-> fp64 conversions are exact widenings, or
+// round-to-nearest narrowings on the way into an fp32 field)
+template <class TS, class TD>
+__global__ void k_copy_box(const TS* __restrict__ src, long long s_base, long long s_sx,
+                           long long s_sy, TD* __restrict__ dst, long long d_base,
                            long long d_sx, long long d_sy, long long l0, long long l1,
                            long long l2, long long n0, long long n1, long long n2, long long m0,
                            long long m1, long long m2) {
@@ -895,21 +921,37 @@ __global__ void k_copy_box(const double* __restrict__ src, long long s_base, lon
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
     const long long k = e / (n0 * n1), r = e - k * n0 * n1, j = r / n0, i = r - j * n0;
     dst[d_base + ((m2 + k) * d_sy + (m1 + j)) * d_sx + (m0 + i)] =
-        src[s_base + ((l2 + k) * s_sy + (l1 + j)) * s_sx + (l0 + i)];
+        (TD)src[s_base + ((l2 + k) * s_sy + (l1 + j)) * s_sx + (l0 + i)];
   }
+}
+
+void launch_copy_box_es(const void* src, int s_es, long long s_base, long long s_sx, long long s_sy, void* dst,
+                        int d_es, long long d_base, long long d_sx, long long d_sy, const long long lo[3],
+                        const long long dims[3], const long long dlo[3], cudaStream_t st) {
+  const long long total = dims[0] * dims[1] * dims[2];
+  if (total <= 0) return;
+  long long nb = (total + 255) / 256;
+  if (nb > 148 * 16) nb = 148 * 16;
+#define SF_COPY(TS, TD)                                                                                  \
+  k_copy_box<TS, TD><<<(unsigned)nb, 256, 0, st>>>(static_cast<const TS*>(src), s_base, s_sx, s_sy,    \
+                                                    static_cast<TD*>(dst), d_base, d_sx, d_sy, lo[0], lo[1], \
+                                                    lo[2], dims[0], dims[1], dims[2], dlo[0], dlo[1], dlo[2])
+  if (s_es == 4 && d_es == 4)
+    SF_COPY(float, float);
+  else if (s_es == 4)
+    SF_COPY(float, double);
+  else if (d_es == 4)
+    SF_COPY(double, float);
+  else
+    SF_COPY(double, double);
+#undef SF_COPY
 }
 
 void launch_copy_box(const double* src, long long s_base, long long s_sx, long long s_sy,
                      double* dst, long long d_base, long long d_sx, long long d_sy,
                      const long long lo[3], const long long dims[3], const long long dlo[3],
                      cudaStream_t st) {
-  const long long total = dims[0] * dims[1] * dims[2];
-  if (total <= 0) return;
-  long long nb = (total + 255) / 256;
-  if (nb > 148 * 16) nb = 148 * 16;
-  k_copy_box<<<(unsigned)nb, 256, 0, st>>>(src, s_base, s_sx, s_sy, dst, d_base, d_sx, d_sy,
-                                            lo[0], lo[1], lo[2], dims[0], dims[1], dims[2],
-                                            dlo[0], dlo[1], dlo[2]);
+  launch_copy_box_es(src, 8, s_base, s_sx, s_sy, dst, 8, d_base, d_sx, d_sy, lo, dims, dlo, st);
 }
 
 __global__ void k_fill_box(double* __restrict__ dst, long long base, long long sx, long long sy,
@@ -936,13 +978,13 @@ void launch_fill_box(double* dst, long long base, long long sx, long long sy, co
 // owned cells <-> a global x-fastest array (grid::gather / scatter, io.hpp:25-65)
 void launch_gather_owned(const double* src, long long base, long long sx, long long sy,
                          const long long n[3], const long long lo[3], const long long N[3],
-                         double* dst_global, int to_field, cudaStream_t st) {
+                         double* dst_global, int to_field, cudaStream_t st, int field_es) {
   const long long zero[3] = {0, 0, 0};
   if (!to_field)
-    launch_copy_box(src, base, sx, sy, dst_global, 0, N[0], N[1], zero, n, lo, st);
+    launch_copy_box_es(src, field_es, base, sx, sy, dst_global, 8, 0, N[0], N[1], zero, n, lo, st);
   else
-    launch_copy_box(dst_global, 0, N[0], N[1], const_cast<double*>(src), base, sx, sy, lo, n, zero,
-                    st);
+    launch_copy_box_es(dst_global, 8, 0, N[0], N[1], const_cast<double*>(src), field_es, base, sx, sy, lo, n,
+                       zero, st);
 }
 
 }  // namespace sfb

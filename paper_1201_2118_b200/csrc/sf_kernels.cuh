@@ -73,7 +73,8 @@ void sweep2_box(int field, int* bw, int* bh);
 int sweep2_tile_y();  // tile height of the selected temporal-pass variant (tile width 32)
 int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field);
 size_t sweep_maps_bytes();
-int encode_box_map(void* map_out, double* base, long long sx, long long sy, long long sz, int bw, int bh);
+int encode_box_map(void* map_out, double* base, long long sx, long long sy, long long sz, int bw, int bh,
+                   int es = 8);
 void sweep_tile_shape(int* tx, int* ty);  // tile of the selected TMA pipeline variant
 size_t sweep_map_offset(int b, int f, int s);
 template <class View>
@@ -108,8 +109,14 @@ void launch_copy_box(const double* src, long long s_base, long long s_sx, long l
                      cudaStream_t st);
 void launch_fill_box(double* dst, long long base, long long sx, long long sy, const long long lo[3],
                      const long long dims[3], double v, cudaStream_t st);
+// element sizes 8 (double) or 4 (float); values convert on the way
+void launch_copy_box_es(const void* src, int s_es, long long s_base, long long s_sx, long long s_sy, void* dst,
+                        int d_es, long long d_base, long long d_sx, long long d_sy, const long long lo[3],
+                        const long long dims[3], const long long dlo[3], cudaStream_t st);
+// field_es: bytes per value of the field (the global array is always fp64)
 void launch_gather_owned(const double* src, long long base, long long sx, long long sy,
                          const long long n[3], const long long lo[3], const long long N[3],
-                         double* dst_global, int to_field /* 1 = scatter */, cudaStream_t st);
+                         double* dst_global, int to_field /* 1 = scatter */, cudaStream_t st,
+                         int field_es = 8);
 
 }  // namespace sfb

@@ -530,15 +530,17 @@ int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, lo
   return r == CUDA_SUCCESS ? 0 : 2;
 }
 
-// a 3-D FLOAT64 tensor map over one padded array with a (bw, bh, 1) box
-int encode_box_map(void* map_out, double* base, long long sx, long long sy, long long sz, int bw, int bh) {
+// a 3-D tensor map over one padded array with a (bw, bh, 1) box; es = bytes
+// per value (8: FLOAT64, 4: FLOAT32 with the same layout in elements)
+int encode_box_map(void* map_out, double* base, long long sx, long long sy, long long sz, int bw, int bh, int es) {
   auto fn = encode_fn();
   if (!fn) return 1;
   cuuint64_t gdim[3] = {(cuuint64_t)sx, (cuuint64_t)sy, (cuuint64_t)sz};
-  cuuint64_t gstride[2] = {(cuuint64_t)(sx * 8), (cuuint64_t)(sx * sy * 8)};
+  cuuint64_t gstride[2] = {(cuuint64_t)(sx * es), (cuuint64_t)(sx * sy * es)};
   cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, gdim,
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(map_out),
+                  es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, gdim,
                   gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : 2;

@@ -358,10 +358,13 @@ class Simulation:
         L.check(self._lib.sf_sim_reduce(self._h, name.encode(), REDUCE_OPS[op], C.byref(v)))
         return v.value
 
-    def create_field(self, name: str, stagger: str | int = "none"):
-        """field_store::create (field.hpp:108-112)."""
+    def create_field(self, name: str, stagger: str | int = "none", dtype: str = "f64"):
+        """field_store::create (field.hpp:108-112). ``dtype`` "f32" stores the
+        field in fp32 (values still cross the API as fp64)."""
         st = STAGGER[stagger] if isinstance(stagger, str) else int(stagger)
-        L.check(self._lib.sf_sim_create_field(self._h, name.encode(), st))
+        if dtype not in ("f64", "f32"):
+            raise ValueError("dtype must be 'f64' or 'f32'")
+        L.check(self._lib.sf_sim_create_field_typed(self._h, name.encode(), st, 8 if dtype == "f64" else 4))
 
     def register_kernel(self, plan: ExecutionPlan, signature: tuple, body: str):
         """executor::register_kernel (executor.hpp:484-488, 650-692).  ``signature``

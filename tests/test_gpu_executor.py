@@ -415,3 +415,29 @@ def test_higher_order_stencils_match_numpy_bitwise(radius, ghost, workers, tile)
     s.exchange(["u"])
     s.run_kernel(f"LAP{2 * radius}")
     assert same(s.gather("lu"), lap_np(data, radius))
+
+
+@pytest.mark.parametrize("no_tma", [False, True])
+@pytest.mark.parametrize("radius,ghost,workers,tile", [(2, 2, 1, (32, 4, 16)), (2, 3, 2, (64, 4, 8)),
+                                                       (3, 3, 4, (32, 8, 4))])
+def test_fp32_fields_in_descriptor_stencils(radius, ghost, workers, tile, no_tma, monkeypatch):
+    # configs[4] in fp32: fields stored as fp32, read widened to fp64, the point
+    # function computes in fp64 and stores rounded to nearest; the exchange
+    # moves fp32 values between components. numpy does the same operations.
+    if no_tma:
+        monkeypatch.setenv("SF_JIT_NO_TMA", "1")
+    ext = (20, 18, 16)
+    data = random_global(ext, 21).astype(np.float32).astype(np.float64)
+    s = rig(ext, workers, ghost, (True, True, True))
+    s.create_field("u", dtype="f32")
+    s.create_field("lu", dtype="f32")
+    s.scatter("u", data)
+    assert same(s.gather("u"), data)
+    s.register_kernel(Plan(f"LAP{2 * radius}F", tile, (radius,) * 6, [("u", "IN", True), ("lu", "OUT")]),
+                      (["u", "lu"], []), LAP4 if radius == 2 else LAP6)
+    s.exchange(["u"])
+    s.run_kernel(f"LAP{2 * radius}F")
+    want = lap_np(data, radius).astype(np.float32).astype(np.float64)
+    assert same(s.gather("lu"), want)
+    assert s.reduce("lu", "max_abs") == float(np.max(np.abs(want)))
+    assert s.reduce("lu", "sum") == pytest.approx(float(np.sum(want)), rel=1e-12)
