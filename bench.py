@@ -447,25 +447,25 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-LAP_BODIES = {
+LAP_BODIES = {  # written against sf_real: fp64, or fp32 when both fields are fp32 (--dtype f32)
     2: """
   const auto& f = c.field(0);
-  const double c0 = -2.5, c1 = 4.0 / 3.0, c2 = -1.0 / 12.0;
-  double sx = c1 * (f(-1, 0, 0) + f(1, 0, 0)) + c2 * (f(-2, 0, 0) + f(2, 0, 0));
-  double sy = c1 * (f(0, -1, 0) + f(0, 1, 0)) + c2 * (f(0, -2, 0) + f(0, 2, 0));
-  double sz = c1 * (f(0, 0, -1) + f(0, 0, 1)) + c2 * (f(0, 0, -2) + f(0, 0, 2));
-  c.field(1).store((3.0 * c0) * f.load() + ((sx + sy) + sz));
+  const sf_real c0 = -2.5, c1 = (sf_real)(4.0 / 3.0), c2 = (sf_real)(-1.0 / 12.0);
+  sf_real sx = c1 * (f(-1, 0, 0) + f(1, 0, 0)) + c2 * (f(-2, 0, 0) + f(2, 0, 0));
+  sf_real sy = c1 * (f(0, -1, 0) + f(0, 1, 0)) + c2 * (f(0, -2, 0) + f(0, 2, 0));
+  sf_real sz = c1 * (f(0, 0, -1) + f(0, 0, 1)) + c2 * (f(0, 0, -2) + f(0, 0, 2));
+  c.field(1).store(((sf_real)3 * c0) * f.load() + ((sx + sy) + sz));
 """,
     3: """
   const auto& f = c.field(0);
-  const double c0 = -49.0 / 18.0, c1 = 1.5, c2 = -0.15, c3 = 1.0 / 90.0;
-  double s[3];
+  const sf_real c0 = (sf_real)(-49.0 / 18.0), c1 = 1.5, c2 = (sf_real)(-0.15), c3 = (sf_real)(1.0 / 90.0);
+  sf_real s[3];
   for (int a = 0; a < 3; ++a) {
     const int x = a == 0, y = a == 1, z = a == 2;
     s[a] = c1 * (f(-x, -y, -z) + f(x, y, z)) + c2 * (f(-2 * x, -2 * y, -2 * z) + f(2 * x, 2 * y, 2 * z))
          + c3 * (f(-3 * x, -3 * y, -3 * z) + f(3 * x, 3 * y, 3 * z));
   }
-  c.field(1).store((3.0 * c0) * f.load() + ((s[0] + s[1]) + s[2]));
+  c.field(1).store(((sf_real)3 * c0) * f.load() + ((s[0] + s[1]) + s[2]));
 """,
 }
 

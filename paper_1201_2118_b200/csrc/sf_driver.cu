@@ -863,6 +863,11 @@ class simulation {
     std::string f32;
     for (size_t i = 0; i < uk.fid.size(); ++i) f32 += (i ? "," : "") + std::string(fes_[uk.fid[i]] == 4 ? "1" : "0");
     src += "__device__ constexpr int SF_F32[] = {" + f32 + "};\n";
+    // a kernel whose bindings are all fp32 computes in fp32: accessors return
+    // sf_real = float (bodies written with sf_real run in either precision)
+    bool all32 = !uk.fid.empty();
+    for (int f : uk.fid) all32 = all32 && fes_[f] == 4;
+    src += std::string("typedef ") + (all32 ? "float" : "double") + " sf_real;\n";
     src += "__device__ constexpr int SF_HALO[] = {";
     for (int a = 0; a < 6; ++a) src += (a ? "," : "") + std::to_string(uk.halo[a]);
     src += "};\n#define SF_DEBUG " + std::string(debug_bounds() ? "1" : "0") + "\n";

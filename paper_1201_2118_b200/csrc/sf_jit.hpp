@@ -88,7 +88,7 @@ struct cell_view {
   double* wr;
   long long o, sx, sxy;
   int slot;
-  __device__ __forceinline__ double operator()(int di, int dj, int dk) const {
+  __device__ __forceinline__ sf_real operator()(int di, int dj, int dk) const {
 #if SF_DEBUG
     if (!SF_READABLE[slot]) { sf_violation(1, slot, di, dj, dk); return 0.0; }
     if (SF_CENTER_ONLY[slot] && (di != 0 || dj != 0 || dk != 0)) { sf_violation(2, slot, di, dj, dk); return 0.0; }
@@ -96,17 +96,18 @@ struct cell_view {
         dk > SF_HALO[5]) { sf_violation(3, slot, di, dj, dk); return 0.0; }
 #endif
     const long long q = o + di + dj * sx + dk * sxy;
-    return SF_F32[slot] ? (double)reinterpret_cast<const float*>(rd)[q] : rd[q];  // fp32 fields widen
+    // fp32 fields widen to fp64 unless the whole kernel runs in fp32 (sf_real)
+    return SF_F32[slot] ? (sf_real)reinterpret_cast<const float*>(rd)[q] : (sf_real)rd[q];
   }
-  __device__ __forceinline__ double load() const { return (*this)(0, 0, 0); }
-  __device__ __forceinline__ void store(double v) const {
+  __device__ __forceinline__ sf_real load() const { return (*this)(0, 0, 0); }
+  __device__ __forceinline__ void store(sf_real v) const {
 #if SF_DEBUG
     if (!SF_WRITABLE[slot]) { sf_violation(4, slot, 0, 0, 0); return; }
 #endif
     if (SF_F32[slot])
       reinterpret_cast<float*>(wr)[o] = (float)v;  // fp32 fields round to nearest
     else
-      __stwb(wr + o, v);
+      __stwb(wr + o, (double)v);
   }
 };
 
@@ -201,8 +202,8 @@ struct cell_view {
   int slot;
   const double* rb;  // cached: ring base + this cell's in-plane offset
   int zoff[SF_ZW];   // cached: ring-plane offset for dk = t - halo_lo_z (updated per plane)
-  double zq[SF_ZW];  // cached: this column's values for dk = t - halo_lo_z (register queue)
-  __device__ __forceinline__ double operator()(int di, int dj, int dk) const {
+  sf_real zq[SF_ZW];  // cached: this column's values for dk = t - halo_lo_z (register queue)
+  __device__ __forceinline__ sf_real operator()(int di, int dj, int dk) const {
 #if SF_DEBUG
     if (!SF_READABLE[slot]) { sf_violation(1, slot, di, dj, dk); return 0.0; }
     if (SF_CENTER_ONLY[slot] && (di != 0 || dj != 0 || dk != 0)) { sf_violation(2, slot, di, dj, dk); return 0.0; }
@@ -214,27 +215,27 @@ struct cell_view {
     if (SF_CACHED[slot] && di == 0 && dj == 0) return zq[dk + SF_HALO[4]];
     if (SF_CACHED[slot]) return ring(zoff[dk + SF_HALO[4]], dj * SF_BW + di);
     const long long q = o + di + dj * sx + dk * sxy;
-    if (SF_F32[slot]) {  // fp32 fields widen exactly
+    if (SF_F32[slot]) {  // fp32 fields widen exactly (to sf_real)
       const float* f = reinterpret_cast<const float*>(rd);
-      return (double)(SF_CENTER_ONLY[slot] ? __ldcg(f + q) : __ldg(f + q));
+      return (sf_real)(SF_CENTER_ONLY[slot] ? __ldcg(f + q) : __ldg(f + q));
     }
-    return SF_CENTER_ONLY[slot] ? __ldcg(rd + q) : __ldg(rd + q);
+    return (sf_real)(SF_CENTER_ONLY[slot] ? __ldcg(rd + q) : __ldg(rd + q));
   }
   // ring plane at offset zo (in fp64 slots; an fp32 plane uses the first half),
   // element e of the box relative to this cell
-  __device__ __forceinline__ double ring(int zo, int e) const {
-    if (SF_F32[slot]) return (double)reinterpret_cast<const float*>(rb)[2 * zo + e];
-    return rb[zo + e];
+  __device__ __forceinline__ sf_real ring(int zo, int e) const {
+    if (SF_F32[slot]) return (sf_real)reinterpret_cast<const float*>(rb)[2 * zo + e];
+    return (sf_real)rb[zo + e];
   }
-  __device__ __forceinline__ double load() const { return (*this)(0, 0, 0); }
-  __device__ __forceinline__ void store(double v) const {
+  __device__ __forceinline__ sf_real load() const { return (*this)(0, 0, 0); }
+  __device__ __forceinline__ void store(sf_real v) const {
 #if SF_DEBUG
     if (!SF_WRITABLE[slot]) { sf_violation(4, slot, 0, 0, 0); return; }
 #endif
     if (SF_F32[slot])
       reinterpret_cast<float*>(wr)[o] = (float)v;  // fp32 fields round to nearest
     else
-      __stwb(wr + o, v);
+      __stwb(wr + o, (double)v);
   }
 };
 

@@ -417,13 +417,51 @@ def test_higher_order_stencils_match_numpy_bitwise(radius, ghost, workers, tile)
     assert same(s.gather("lu"), lap_np(data, radius))
 
 
+# the same stencils written against sf_real: float in a kernel whose bindings
+# are all fp32, double otherwise (the fp64 results equal LAP4 / LAP6 bitwise)
+LAP4R = """
+  const auto& f = c.field(0);
+  const sf_real c0 = -2.5, c1 = (sf_real)(4.0 / 3.0), c2 = (sf_real)(-1.0 / 12.0);
+  sf_real sx = c1 * (f(-1, 0, 0) + f(1, 0, 0)) + c2 * (f(-2, 0, 0) + f(2, 0, 0));
+  sf_real sy = c1 * (f(0, -1, 0) + f(0, 1, 0)) + c2 * (f(0, -2, 0) + f(0, 2, 0));
+  sf_real sz = c1 * (f(0, 0, -1) + f(0, 0, 1)) + c2 * (f(0, 0, -2) + f(0, 0, 2));
+  c.field(1).store(((sf_real)3 * c0) * f.load() + ((sx + sy) + sz));
+"""
+LAP6R = """
+  const auto& f = c.field(0);
+  const sf_real c0 = (sf_real)(-49.0 / 18.0), c1 = 1.5, c2 = (sf_real)(-0.15), c3 = (sf_real)(1.0 / 90.0);
+  sf_real s[3];
+  for (int a = 0; a < 3; ++a) {
+    const int x = a == 0, y = a == 1, z = a == 2;
+    s[a] = c1 * (f(-x, -y, -z) + f(x, y, z)) + c2 * (f(-2 * x, -2 * y, -2 * z) + f(2 * x, 2 * y, 2 * z))
+         + c3 * (f(-3 * x, -3 * y, -3 * z) + f(3 * x, 3 * y, 3 * z));
+  }
+  c.field(1).store(((sf_real)3 * c0) * f.load() + ((s[0] + s[1]) + s[2]));
+"""
+
+
+def lap_np32(data32, radius):
+    """lap_np in IEEE single precision, operation for operation (sf_real = float)."""
+    f = np.float32
+    r = lambda di, dj, dk: np.roll(data32, shift=(-dk, -dj, -di), axis=(0, 1, 2))  # noqa: E731
+    ax = lambda a, m: [m * (a == q) for q in range(3)]  # noqa: E731
+    if radius == 2:
+        c0, c1, c2 = f(-2.5), f(4.0 / 3.0), f(-1.0 / 12.0)
+        s = [c1 * (r(*ax(a, -1)) + r(*ax(a, 1))) + c2 * (r(*ax(a, -2)) + r(*ax(a, 2))) for a in range(3)]
+    else:
+        c0, c1, c2, c3 = f(-49.0 / 18.0), f(1.5), f(-0.15), f(1.0 / 90.0)
+        s = [c1 * (r(*ax(a, -1)) + r(*ax(a, 1))) + c2 * (r(*ax(a, -2)) + r(*ax(a, 2)))
+             + c3 * (r(*ax(a, -3)) + r(*ax(a, 3))) for a in range(3)]
+    return (f(3) * c0) * data32 + ((s[0] + s[1]) + s[2])
+
+
 @pytest.mark.parametrize("no_tma", [False, True])
 @pytest.mark.parametrize("radius,ghost,workers,tile", [(2, 2, 1, (32, 4, 16)), (2, 3, 2, (64, 4, 8)),
                                                        (3, 3, 4, (32, 8, 4))])
 def test_fp32_fields_in_descriptor_stencils(radius, ghost, workers, tile, no_tma, monkeypatch):
-    # configs[4] in fp32: fields stored as fp32, read widened to fp64, the point
-    # function computes in fp64 and stores rounded to nearest; the exchange
-    # moves fp32 values between components. numpy does the same operations.
+    # configs[4] in fp32: both fields fp32, so the kernel computes in fp32
+    # (sf_real = float); the exchange moves fp32 values between components.
+    # numpy repeats every single-precision operation.
     if no_tma:
         monkeypatch.setenv("SF_JIT_NO_TMA", "1")
     ext = (20, 18, 16)
@@ -434,10 +472,36 @@ def test_fp32_fields_in_descriptor_stencils(radius, ghost, workers, tile, no_tma
     s.scatter("u", data)
     assert same(s.gather("u"), data)
     s.register_kernel(Plan(f"LAP{2 * radius}F", tile, (radius,) * 6, [("u", "IN", True), ("lu", "OUT")]),
-                      (["u", "lu"], []), LAP4 if radius == 2 else LAP6)
+                      (["u", "lu"], []), LAP4R if radius == 2 else LAP6R)
     s.exchange(["u"])
     s.run_kernel(f"LAP{2 * radius}F")
-    want = lap_np(data, radius).astype(np.float32).astype(np.float64)
+    want = lap_np32(data.astype(np.float32), radius).astype(np.float64)
     assert same(s.gather("lu"), want)
     assert s.reduce("lu", "max_abs") == float(np.max(np.abs(want)))
     assert s.reduce("lu", "sum") == pytest.approx(float(np.sum(want)), rel=1e-12)
+
+
+@pytest.mark.parametrize("radius", [2, 3])
+def test_mixed_precision_kernel_computes_in_fp64(radius):
+    # an fp32 input with an fp64 output: accessors widen, the body runs in fp64;
+    # with every binding fp64 the sf_real bodies equal LAP4 / LAP6 bitwise
+    ext = (20, 18, 16)
+    data = random_global(ext, 22).astype(np.float32).astype(np.float64)
+    s = rig(ext, 1, radius, (True, True, True))
+    s.create_field("u", dtype="f32")
+    s.create_field("lu")
+    s.create_field("u64")
+    s.create_field("lu64")
+    s.scatter("u", data)
+    s.scatter("u64", data)
+    body = LAP4R if radius == 2 else LAP6R
+    s.register_kernel(Plan("MIX", (32, 4, 16), (radius,) * 6, [("u", "IN", True), ("lu", "OUT")]), (["u", "lu"], []),
+                      body)
+    s.register_kernel(Plan("F64", (32, 4, 16), (radius,) * 6, [("u64", "IN", True), ("lu64", "OUT")]),
+                      (["u64", "lu64"], []), body)
+    s.exchange(["u", "u64"])
+    s.run_kernel("MIX")
+    s.run_kernel("F64")
+    want = lap_np(data, radius)
+    assert same(s.gather("lu"), want)
+    assert same(s.gather("lu64"), want)
