@@ -368,7 +368,7 @@ def run_ours(args):
         e2e = {"value": round(total_cells * args.steps / (e_ms / 1e3) / 1e6, 3), "unit": UNIT,
                "h2d_bytes_per_step": 4 * total_cells * 8, "d2h_bytes_per_step": 4 * total_cells * 8,
                "ms_per_step": round(e_ms / args.steps, 3),
-               "path": "sf_sim_scatter_block_async(vx,vy,vz,p) from pinned host -> sf_sim_step -> sf_sim_gather_block_async(vx,vy,vz,p) to pinned host, per rank; 3-D copy-engine transfers straight into the padded blocks"}
+               "path": "sf_sim_scatter_block_async(vx,vy,vz,p) from pinned host -> sf_sim_step -> sf_sim_gather_block_async(vx,vy,vz,p) to pinned host, per rank; uploads land in dense device buffers and are installed by a kernel, downloads are device snapshots drained while the next step computes"}
 
     # ---- CPU baseline (rank 0, N=1): the reference on this host, bounded sample --
     cpu = None

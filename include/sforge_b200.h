@@ -187,11 +187,14 @@ int sf_sim_world(const sf_sim* s);
  * grid::gather / grid::scatter (io.hpp:25-65). */
 int sf_sim_gather_block(sf_sim* s, const char* field, int worker, double* host, int64_t n);
 int sf_sim_scatter_block(sf_sim* s, const char* field, int worker, const double* host, int64_t n);
-/* Asynchronous forms: the transfer is queued on the library's upload or
- * download stream and the call returns at once. `host` must be page-locked
- * and left untouched until sf_sim_synchronize. Device-side ordering against
- * compute and against other transfers of the same field is kept by the
- * library, so an upload of one field overlaps the download of another. */
+/* Asynchronous forms; the call returns at once and `host` must be
+ * page-locked and left untouched until sf_sim_synchronize.
+ *  - gather_block_async snapshots the block on the device, in order with the
+ *    compute already enqueued, and downloads the snapshot in the background:
+ *    later compute overlaps the transfer.
+ *  - scatter_block_async queues the upload on the library's upload stream;
+ *    later compute waits for it.
+ * Uploads and downloads of different fields overlap (PCIe is full duplex). */
 int sf_sim_gather_block_async(sf_sim* s, const char* field, int worker, double* host, int64_t n);
 int sf_sim_scatter_block_async(sf_sim* s, const char* field, int worker, const double* host, int64_t n);
 /* The exchange plan of one refresh phase (axis 0..2, slabs widened as in

@@ -376,6 +376,9 @@ class simulation {
       }
       for (auto e : io_ev_) cudaEventDestroy(e);
       for (auto e : io_up_) cudaEventDestroy(e);
+      for (auto e : io_snap_) cudaEventDestroy(e);
+      for (auto e : io_snapdn_) cudaEventDestroy(e);
+      for (auto e : io_inst_) cudaEventDestroy(e);
     }
     if (comm_ && nccl() && nccl()->CommDestroy) nccl()->CommDestroy(comm_);
     cudaStreamDestroy(st_);
@@ -567,6 +570,53 @@ class simulation {
     const auto& L = lay_[b];
     const i64 d[3] = {L.dims[0], L.dims[1], L.dims[2]};
     if (n < d[0] * d[1] * d[2]) throw error(SF_ERR_ARG, "block buffer too small");
+    if (!io_[0]) {
+      for (int k = 0; k < 2; ++k) SF_CK(cudaStreamCreateWithFlags(&io_[k], cudaStreamNonBlocking));
+      for (int k = 0; k < kMaxFields; ++k) {
+        SF_CK(cudaEventCreateWithFlags(&io_ev_[k], cudaEventDisableTiming));
+        SF_CK(cudaEventCreateWithFlags(&io_up_[k], cudaEventDisableTiming));
+        SF_CK(cudaEventCreateWithFlags(&io_snap_[k], cudaEventDisableTiming));
+        SF_CK(cudaEventCreateWithFlags(&io_snapdn_[k], cudaEventDisableTiming));
+        SF_CK(cudaEventCreateWithFlags(&io_inst_[k], cudaEventDisableTiming));
+      }
+    }
+    if (!to_device && async) {
+      // Snapshot, then download in the background: a pack task on the compute
+      // stream copies the owned block into a dense device buffer (FRONT is
+      // resolved on the device, so no host synchronisation), and the copy
+      // engine moves that buffer while later compute proceeds.
+      const size_t cnt = (size_t)(d[0] * d[1] * d[2]);
+      if (!snap_[b][f]) snap_[b][f] = (double*)dalloc(sizeof(double) * cnt);
+      SF_CK(cudaStreamWaitEvent(st_, io_snapdn_[f], 0));  // the last download out of this buffer
+      flush_io();
+      launch_snapshot(dtab_, b, f, snap_[b][f], d[1] * d[2], st_);
+      ++launches_;
+      SF_CK(cudaEventRecord(io_snap_[f], st_));
+      SF_CK(cudaStreamWaitEvent(io_[1], io_snap_[f], 0));
+      SF_CK(cudaMemcpyAsync(host, snap_[b][f], sizeof(double) * cnt, cudaMemcpyDeviceToHost, io_[1]));
+      SF_CK(cudaEventRecord(io_snapdn_[f], io_[1]));
+      check_launch();
+      return;
+    }
+    if (to_device && async) {
+      // Upload into a dense device buffer on the upload stream, then install
+      // it into FRONT with a kernel on the compute stream (FRONT resolved on
+      // the device): no host synchronisation, and compute enqueued later sees
+      // the new values.
+      const size_t cnt = (size_t)(d[0] * d[1] * d[2]);
+      if (!upb_[b][f]) upb_[b][f] = (double*)dalloc(sizeof(double) * cnt);
+      SF_CK(cudaStreamWaitEvent(io_[0], io_inst_[f], 0));  // the last install out of this buffer
+      SF_CK(cudaMemcpyAsync(upb_[b][f], host, sizeof(double) * cnt, cudaMemcpyHostToDevice, io_[0]));
+      SF_CK(cudaEventRecord(io_up_[f], io_[0]));
+      flush_io();
+      SF_CK(cudaStreamWaitEvent(st_, io_up_[f], 0));
+      launch_install(dtab_, b, f, upb_[b][f], d[1] * d[2], st_);
+      ++launches_;
+      SF_CK(cudaEventRecord(io_inst_[f], st_));
+      ghosts_ok_[fname_[f]] = false;
+      check_launch();
+      return;
+    }
     if (fes_[f] != 8) {  // fp32 field: host values are fp64, converted through the staging buffer
       download_table();
       double* sg = staging();
@@ -587,13 +637,6 @@ class simulation {
       return;
     }
     download_table(false);
-    if (!io_[0]) {
-      for (int k = 0; k < 2; ++k) SF_CK(cudaStreamCreateWithFlags(&io_[k], cudaStreamNonBlocking));
-      for (int k = 0; k < kMaxFields; ++k) {
-        SF_CK(cudaEventCreateWithFlags(&io_ev_[k], cudaEventDisableTiming));
-        SF_CK(cudaEventCreateWithFlags(&io_up_[k], cudaEventDisableTiming));
-      }
-    }
     cudaMemcpy3DParms prm = {};
     double* dev = htab_->ptr[b][f][FRONT] + L.base;
     cudaPitchedPtr dp = make_cudaPitchedPtr(dev, (size_t)L.sx * sizeof(double), (size_t)d[0] * sizeof(double),
@@ -605,7 +648,8 @@ class simulation {
       prm.srcPtr = hp;
       prm.dstPtr = dp;
       prm.kind = cudaMemcpyHostToDevice;
-      SF_CK(cudaStreamWaitEvent(io_[0], io_ev_[f], 0));  // the last download of f
+      SF_CK(cudaStreamWaitEvent(io_[0], io_ev_[f], 0));    // the last direct download of f
+      SF_CK(cudaStreamWaitEvent(io_[0], io_snap_[f], 0));  // the last snapshot of f
       SF_CK(cudaMemcpy3DAsync(&prm, io_[0]));
       SF_CK(cudaEventRecord(io_up_[f], io_[0]));
       io_pending_.push_back(io_up_[f]);
@@ -1539,6 +1583,11 @@ class simulation {
   cudaStream_t io_[2]{};    // host transfers: 0 uploads, 1 downloads
   cudaEvent_t io_ev_[kMaxFields]{};  // last download of each field
   cudaEvent_t io_up_[kMaxFields]{};  // last upload of each field
+  cudaEvent_t io_snap_[kMaxFields]{};    // last snapshot (pack) of each field for a background download
+  cudaEvent_t io_snapdn_[kMaxFields]{};  // last background download out of each snapshot buffer
+  double* snap_[kMaxBlocks][kMaxFields]{};
+  double* upb_[kMaxBlocks][kMaxFields]{};   // dense upload buffers of the asynchronous scatter
+  cudaEvent_t io_inst_[kMaxFields]{};       // last install out of each upload buffer
   mutable std::vector<cudaEvent_t> io_pending_;  // not yet ordered before compute
   // compute enqueues so far / at the last table download: block_io skips the
   // download (a copy that would queue behind large transfers) when equal

@@ -900,6 +900,49 @@ void launch_loop_cond(cudaGraphConditionalHandle h, const sf_dev_ctl* ctl, cudaS
   k_loop_cond<<<1, 1, 0, st>>>(h, ctl);
 }
 
+// Owned block of (b, f) FRONT -> dense x-fastest fp64 buffer, FRONT resolved
+// on the device (a snapshot that needs no host synchronisation). One warp
+// group per row, rows strided over the grid; fp32 fields widen.
+__global__ void k_snapshot(const sf_dev_table* __restrict__ tab, int b, int f, double* __restrict__ buf) {
+  const sf_dev_block& B = tab->blk[b];
+  const double* src = tab->ptr[b][f][FRONT];
+  const bool f32 = tab->esize[f] == 4;
+  const long long n0 = B.n[0], n1 = B.n[1], rows = B.n[1] * B.n[2];
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const long long k = r / n1, j = r - k * n1;
+    const long long o = off(B, 0, j, k);
+    double* dst = buf + r * n0;
+    for (long long i = threadIdx.x; i < n0; i += blockDim.x)
+      dst[i] = f32 ? (double)reinterpret_cast<const float*>(src)[o + i] : src[o + i];
+  }
+}
+void launch_snapshot(const sf_dev_table* tab, int b, int f, double* buf, long long rows, cudaStream_t st) {
+  const long long nb = rows < 148 * 32 ? rows : 148 * 32;
+  if (nb > 0) k_snapshot<<<(unsigned)nb, 256, 0, st>>>(tab, b, f, buf);
+}
+// the reverse: dense fp64 buffer -> owned block of (b, f) FRONT (fp32 fields round)
+__global__ void k_install(const sf_dev_table* __restrict__ tab, int b, int f, const double* __restrict__ buf) {
+  const sf_dev_block& B = tab->blk[b];
+  double* dst = tab->ptr[b][f][FRONT];
+  const bool f32 = tab->esize[f] == 4;
+  const long long n0 = B.n[0], n1 = B.n[1], rows = B.n[1] * B.n[2];
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const long long k = r / n1, j = r - k * n1;
+    const long long o = off(B, 0, j, k);
+    const double* src = buf + r * n0;
+    for (long long i = threadIdx.x; i < n0; i += blockDim.x) {
+      if (f32)
+        reinterpret_cast<float*>(dst)[o + i] = (float)src[i];
+      else
+        dst[o + i] = src[i];
+    }
+  }
+}
+void launch_install(const sf_dev_table* tab, int b, int f, const double* buf, long long rows, cudaStream_t st) {
+  const long long nb = rows < 148 * 32 ? rows : 148 * 32;
+  if (nb > 0) k_install<<<(unsigned)nb, 256, 0, st>>>(tab, b, f, buf);
+}
+
 void launch_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, int op, double arg,
                 int f, int a, int b, const sf_consts& c, int predicated, cudaStream_t st) {
   k_ctl<<<1, 1, 0, st>>>(tab, ctl, hflag, op, arg, f, a, b, c, predicated);

@@ -99,6 +99,10 @@ enum ctl_op {
 };
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
 void ensure_smem_attr(const void* kernel, int bytes);
+// owned block of (b, f) FRONT -> dense fp64 buffer, FRONT read from the device table
+void launch_snapshot(const sf_dev_table* tab, int b, int f, double* buf, long long rows, cudaStream_t st);
+// dense fp64 buffer -> owned block of (b, f) FRONT, FRONT read from the device table
+void launch_install(const sf_dev_table* tab, int b, int f, const double* buf, long long rows, cudaStream_t st);
 // sets the pressure-loop graph's while condition to !ctl->done
 void launch_loop_cond(cudaGraphConditionalHandle h, const sf_dev_ctl* ctl, cudaStream_t st);
 void launch_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, int op, double arg,
