@@ -381,6 +381,13 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   const int iym = (bx << 2) | (bym << 1), iypm = (bx << 2) | (bypm << 1);
   const int par_col = (gi + gj) & 1;
   const int N2m1 = N2 - 1, nm2i = (int)nm2, per2 = s.per[2];
+  // Boundary tiles on interior planes (bz = bzp = 1): this cell's scale
+  // factors and wall flags are per-thread constants, so sweep B runs the fast
+  // path's operations with them instead of the general path's lookups and
+  // branches (bitwise the same values).
+  const double sc_ = smb[ic | 1], sex_ = smb[iex | 1], sey_ = smb[iey | 1];
+  const double sxm_ = smb[ixm | 1], sxpm_ = smb[ixpm | 1], sym_ = smb[iym | 1], sypm_ = smb[iypm | 1];
+  const bool xlo = gi == 0, ylo = gj == 0, xhi = gi == N0 - 1, yhi = gj == N1 - 1;
   const int q0 = (ty + 2) * EW + (tx + 2);
 
   double* __restrict__ Dn = tab->ptr[b][SF_DIVU][ALT];
@@ -462,6 +469,52 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         Vn[o] = vn;
         Wn[o] = wn;
         Dn[o] = dd;
+        const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
+        r1 = b1 > r1 ? b1 : r1;
+        r2 = b2 > r2 ? b2 : r2;
+        wm2 = wn;
+      } else if (act && z >= zf_lo && z <= zf_hi) {
+        // boundary tile, interior plane: the general path's arithmetic with
+        // per-thread scales, selects for the wall cases (see sc_ above)
+        const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
+        const double dXm = d1[q0 - 1], dYm = d1[q0 - EW], dZp = d1p[q0];
+        const double p0 = p1[q0], u0 = u1[q0], uml = u1[q0 - 1], v0 = v1[q0], vml = v1[q0 - EW], w0 = w1[q0];
+        const int par = par_col ^ ((lo2 + z) & 1);
+        const double a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
+        const double d0 = sc_ * dC * a0;
+        const double exv = sex_ * dXp * a1;
+        const double eyv = sey_ * dYp * a1;
+        const double ezv = sc_ * dZp * a1;
+        const double pn = p0 + d0;
+        double un = u0 + cu * (d0 - exv);
+        double vn = v0 + cv * (d0 - eyv);
+        const double wn = w0 + cw * (d0 - ezv);
+        un = xhi ? pin_u : un;
+        vn = yhi ? pin_v : vn;
+        // swept -x / -y neighbours (parity a1; 1 - a1 == a0 exactly); at a low
+        // wall the pinned ghost
+        const double a1m = 1.0 - a1;
+        const double umr = uml + cu * (sxm_ * dXm * a1 - sxpm_ * dC * a1m);
+        const double vmr = vml + cv * (sym_ * dYm * a1 - sypm_ * dC * a1m);
+        const double umn = xlo ? uml : umr, vmn = ylo ? vml : vmr;
+        double dd = (un - umn) * s.ix;
+        dd += (vn - vmn) * s.iy;
+        dd += (wn - wm2) * s.iz;
+        Pn[o] = pn;
+        Un[o] = un;
+        Vn[o] = vn;
+        Wn[o] = wn;
+        Dn[o] = dd;
+        if (xlo) {
+          Un[o - 1] = umn;
+          Dn[o - 1] = dd;
+        }
+        if (ylo) {
+          Vn[o - sx] = vmn;
+          Dn[o - sx] = dd;
+        }
+        if (xhi) Dn[o + 1] = dd;
+        if (yhi) Dn[o + sx] = dd;
         const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
         r1 = b1 > r1 ? b1 : r1;
         r2 = b2 > r2 ? b2 : r2;
