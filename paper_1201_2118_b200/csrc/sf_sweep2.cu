@@ -309,6 +309,32 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
       }
       return;
     }
+    if (z >= zf_lo && z <= zf_hi) {
+      // boundary tile, interior plane (bz = bzp = 1): every cell evaluates the
+      // update and selects apply the wall cases, so no warp runs both sides of
+      // a branch (owned cells: bitwise the general path below)
+#pragma unroll
+      for (int r = 0; r < NE; ++r) {
+        if (r > 0 && !has2f) break;
+        const int ia = f_ia[r], e = f_e[r], bt = f_bt[r];
+        const double dc = S[Di + ia], dx = S[Di + ia + 1], dy = S[Di + ia + IW], dz = S[Dz + ia];
+        const double uu = S[Ui + ia], vv = S[Vi + ia], ww = S[Wi + ia], pp = S[Pi + ia];
+        const int rc = (bt & 7) | 1, rx = ((bt >> 3) & 7) | 1, ry = ((bt >> 6) & 7) | 1;
+        const double a0 = ((((bt >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
+        const double d0 = smb[rc] * dc * a0;
+        const double exv = smb[rx] * dx * a1;
+        const double eyv = smb[ry] * dy * a1;
+        const double ezv = smb[rc] * dz * a1;
+        const bool own = (bt >> 10) & 1;
+        const double un = ((bt >> 11) & 1) ? pin_u : uu + cu * (d0 - exv);
+        const double vn = ((bt >> 12) & 1) ? pin_v : vv + cv * (d0 - eyv);
+        S[p1 + e] = own ? pp + d0 : pp;
+        S[u1 + e] = own ? un : (((bt >> 13) & 1) ? pins.ul : uu);
+        S[v1 + e] = own ? vn : (((bt >> 14) & 1) ? pins.vl : vv);
+        S[w1 + e] = own ? ww + cw * (d0 - ezv) : ww;
+      }
+      return;
+    }
     const bool zin = gk >= 0 && gk < N2;
     const int bz = s.per[2] | ((gk > 0) & (gk < (int)nm2)), bzp = s.per[2] | (gk + 1 < (int)nm2);
     const bool pz = lo2 + z == N2 - 1, zlow = lo2 + z == -1;
