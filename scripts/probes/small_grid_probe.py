@@ -6,7 +6,7 @@ from paper_1201_2118_b200.cavity import run_cavity
 cfg = sfb.SolverConfig(extents=(129, 129, 3), reynolds=100.0, sigma=0.9, omega=1.9525, tolerance=1e-6,
                        max_sweeps=3000, symmetry_z=True)
 par = sfb.FluidParams(viscosity=0.01, lid_speed=1.0)
-for fused in (1, 3):
+for fused in ([int(x) for x in sys.argv[1].split(',')] if len(sys.argv) > 1 else (1, 3)):
     sim = sfb.Simulation(cfg, par, fused=fused)
     sim.init_cavity()
     for _ in range(200): sim.step()
