@@ -68,6 +68,8 @@ struct sf_dev_ctl {
   int redo;          // temporal pass stopped after its first sweep: redo it single
   double dt, beta, tolerance, residual;
   double vmax[3];
+  unsigned long long racc[3];  // persistent loop: residual maxima, rotating per half-sweep
+  unsigned int bar;            // persistent loop: grid barrier arrivals
 };
 
 // Host-mapped mirror the finalising CTA writes for the polling host.

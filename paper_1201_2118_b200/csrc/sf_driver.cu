@@ -1377,6 +1377,16 @@ class simulation {
     check_launch();
     if (opt_.fused) refresh({SF_DIVU});
     ctl(CTL_BEGIN_ITERATION);
+    if (persistent()) {
+      const int zc = zc_persist();
+      const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc);
+      SF_CK(launch_pressure_loop(tview(ws), ws.nctas, zc, consts_, dctl_, st_));
+      ++launches_;
+      ctl(CTL_PUBLISH);
+      sync();
+      if (hflag_->sweeps > 0) est_sweeps_ = hflag_->sweeps;
+      return finish_pressure_iteration();
+    }
     const int maxs = std::max(1, cfg_.max_sweeps);
     const bool graph = graph_env_ && !dist_ && !timing_ && pressure_calls_++ > 0;
     if (graph) {
@@ -1602,6 +1612,17 @@ class simulation {
   cudaEvent_t ev_fork_{}, ev_join_{};
   const bool uv_tma_env_ = getenv("SF_NO_UV_TMA") == nullptr;
   const bool temporal_env_ = getenv("SF_NO_TEMPORAL") == nullptr;
+  const int persist_env_ = getenv("SF_PERSIST") ? atoi(getenv("SF_PERSIST")) : -1;
+  const double persist_cells_ = getenv("SF_PERSIST_CELLS") ? atof(getenv("SF_PERSIST_CELLS")) : 4.0e5;
+  const int zc_persist_env_ = getenv("SF_PZC") ? atoi(getenv("SF_PZC")) : 0;
+  // z chunk of the persistent loop: about one tile per co-resident CTA
+  int zc_persist() const {
+    if (zc_persist_env_ > 0) return zc_persist_env_;
+    const sf_dev_block& B = htab_->blk[0];
+    const i64 cols = ((B.n[0] + kTX - 1) / kTX) * ((B.n[1] + kTY - 1) / kTY);
+    const i64 ctas = pressure_loop_ctas();
+    return (int)std::max<i64>(1, (B.n[2] * cols + ctas - 1) / ctas);
+  }
   std::vector<void*> dev_allocs_;
   std::map<std::string, work_set> items_;
   std::map<std::string, task_set> tasks_;
@@ -1637,7 +1658,27 @@ class simulation {
   const int zc_fused_ = getenv("SF_ZC") ? atoi(getenv("SF_ZC")) : 64;
   // z chunk of the temporal pass: longer chunks amortise its 3 prologue planes
   // (512^3: 2.64 ms at 64, 2.59 ms at 128, 2.61 ms at 256)
-  const int zc_pass_ = getenv("SF_ZC2") ? atoi(getenv("SF_ZC2")) : 128;
+  const int zc_pass_env_ = getenv("SF_ZC2") ? atoi(getenv("SF_ZC2")) : 0;
+  int zc_pass_cache_ = 0;
+  int sms_ = 0;
+  // z chunk of the temporal pass: 128 planes (fewer pipeline prologues) unless
+  // that leaves fewer than about two waves of CTAs (2 per SM), then halved
+  // down to 16 (a 128^3 grid has only 64 column tiles)
+  int zc_pass() {
+    if (zc_pass_env_ > 0) return zc_pass_env_;
+    if (zc_pass_cache_) return zc_pass_cache_;
+    if (!sms_) SF_CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, opt_.device));
+    const int ty = sweep2_tile_y();
+    i64 cols = 0, nz = 1;
+    for (int b = 0; b < nloc_; ++b) {
+      const sf_dev_block& B = htab_->blk[b];
+      cols += ((B.n[0] + kTX - 1) / kTX) * ((B.n[1] + ty - 1) / ty);
+      nz = std::max<i64>(nz, B.n[2]);
+    }
+    int zc = 128;
+    while (zc > 16 && cols * ((nz + zc - 1) / zc) < (i64)4 * sms_) zc /= 2;
+    return zc_pass_cache_ = zc;
+  }
 
   void validate() {
     // solver_config::validate / fluid_params::validate (cfd.hpp:36-66)
@@ -2103,7 +2144,7 @@ class simulation {
   // the owned block. Boundary tiles are the rest, covered by up to six slabs.
   // All tile origins are even in x (the TMA start rule).
   std::pair<const work_set*, const work_set*> pass_split() {
-    const int ty = sweep2_tile_y(), zc = zc_pass_;
+    const int ty = sweep2_tile_y(), zc = zc_pass();
     char key[64];
     std::snprintf(key, sizeof key, "split:%d:%d", zc, ty);
     auto ii = items_.find(std::string(key) + ":i");
@@ -2209,6 +2250,18 @@ class simulation {
     if (bc_[4].kind == SF_BC_WALL) p.wl = bc_[4].velocity[2];
     return p;
   }
+  // The persistent pressure loop (k_pressure_loop) applies to a single grid
+  // component in a single process whose fused half-sweep writes every divu
+  // ghost itself, when the grid is small enough that launches dominate
+  // (SF_PERSIST=0 off, =1 whenever it applies).
+  bool persistent() {
+    if (persist_env_ == 0 || dist_ || timing_ || !opt_.fused || nloc_ != 1 || has_proc_faces()) return false;
+    const phase& ph = phase_for(1u << SF_DIVU, -1, SF_SCOPE_ALL, true);
+    if (ph.first.n || ph.unpack.n || !ph.sends.empty() || !ph.recvs.empty()) return false;
+    if (persist_env_ == 1) return true;
+    const sf_dev_block& B = htab_->blk[0];
+    return (double)B.n[0] * B.n[1] * B.n[2] <= persist_cells_;
+  }
   bool tma_sweep() const { return maps_ && (opt_.fused == 1 || opt_.fused == 3); }
 
   // Enqueues one unit of the pressure loop; returns the half-sweeps it covers.
@@ -2219,9 +2272,9 @@ class simulation {
     }
     const int fin = dist_ ? 0 : 1;
     if (!has_proc_faces()) {
-      const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass_, kTX, sweep2_tile_y());
+      const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass(), kTX, sweep2_tile_y());
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
-      launch_sweep2(tview(ws), ws.nctas, zc_pass_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_);
+      launch_sweep2(tview(ws), ws.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
     } else {
       // Processor faces: the pass reads 2-deep halos of vx, vy, vz, divu (p
@@ -2243,7 +2296,7 @@ class simulation {
       const auto split = pass_split();
       const work_set& wi = overlap ? *split.first : empty_ws_;
       const work_set& wb =
-          overlap ? *split.second : items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass_, kTX, sweep2_tile_y());
+          overlap ? *split.second : items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass(), kTX, sweep2_tile_y());
       const unsigned total = (unsigned)(wi.nctas + wb.nctas);
       SF_CK(cudaEventRecord(ev_fork_, st_));
       SF_CK(cudaStreamWaitEvent(xs_, ev_fork_, 0));
@@ -2251,10 +2304,10 @@ class simulation {
       SF_CK(cudaEventRecord(ev_join_, xs_));
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
       if (wi.nctas)
-        launch_sweep2(tview(wi), wi.nctas, zc_pass_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_,
+        launch_sweep2(tview(wi), wi.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_,
                       total);
       SF_CK(cudaStreamWaitEvent(st_, ev_join_, 0));
-      launch_sweep2(tview(wb), wb.nctas, zc_pass_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_,
+      launch_sweep2(tview(wb), wb.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_,
                     total);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
       ++launches_;

@@ -13,7 +13,9 @@
 //                  max|divu| + the loop test of pressure_iteration (cfd.hpp:295-303)
 //   k_reduce_*     grid::reduce (reductions.hpp:28-90)
 //   k_ctl          compute_dt / beta / loop bookkeeping (cfd.hpp:264-305)
+#include <algorithm>
 #include <cstdio>
+#include <map>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -33,9 +35,8 @@ struct tile_loc {
   bool act;
 };
 
-__device__ __forceinline__ tile_loc locate(const sf_work* __restrict__ items, int nitems, int zc) {
+__device__ __forceinline__ tile_loc locate_at(const sf_work* __restrict__ items, int nitems, int zc, int cta) {
   tile_loc t;
-  const int cta = blockIdx.x;
   t.item = nitems > 1 ? find_item(items, nitems, cta) : 0;
   const sf_work& w = items[t.item];
   t.blk = w.blk;
@@ -49,6 +50,9 @@ __device__ __forceinline__ tile_loc locate(const sf_work* __restrict__ items, in
   t.k1 = min(t.k0 + zc, w.hi[2]);
   t.act = t.i < w.hi[0] && t.j < w.hi[1];
   return t;
+}
+__device__ __forceinline__ tile_loc locate(const sf_work* __restrict__ items, int nitems, int zc) {
+  return locate_at(items, nitems, zc, blockIdx.x);
 }
 
 __device__ __forceinline__ bool pred_done(const sf_dev_ctl* ctl) {
@@ -380,6 +384,12 @@ struct sweep_ctx {
   int color;
   long long nm1[3];
   int per[3];
+  // selects instead of a dynamically indexed array (which lives in local memory)
+  __device__ __forceinline__ double m(int a, int b, int c) const {
+    const double x0 = c ? mb[0][0][1] : mb[0][0][0], x1 = c ? mb[0][1][1] : mb[0][1][0];
+    const double x2 = c ? mb[1][0][1] : mb[1][0][0], x3 = c ? mb[1][1][1] : mb[1][1][0];
+    return a ? (b ? x3 : x2) : (b ? x1 : x0);
+  }
 };
 
 __device__ __forceinline__ int bit_in(const sweep_ctx& x, int a, long long g) {
@@ -392,26 +402,50 @@ __device__ __forceinline__ double act0(const sweep_ctx& x, long long gsum) {
   return ((gsum & 1) == x.color) ? 1.0 : 0.0;
 }
 
-__global__ void __launch_bounds__(kTX* kTY) k_sweep_div(sf_dev_table* __restrict__ tab,
-                                                        const sf_work* __restrict__ items,
-                                                        int nitems, int zc, sf_consts s,
-                                                        sf_dev_ctl* ctl, sf_host_flag* hflag,
-                                                        unsigned int total_ctas, int finalize) {
-  if (pred_done(ctl)) return;
-  const tile_loc t = locate(items, nitems, zc);
-  const sf_dev_block& B = tab->blk[t.blk];
-  const double* __restrict__ D = tab->ptr[t.blk][SF_DIVU][FRONT];
-  double* __restrict__ Dn = tab->ptr[t.blk][SF_DIVU][ALT];
-  double* __restrict__ P = tab->ptr[t.blk][SF_P][FRONT];
-  const double* __restrict__ U = tab->ptr[t.blk][SF_VX][FRONT];
-  const double* __restrict__ V = tab->ptr[t.blk][SF_VY][FRONT];
-  const double* __restrict__ W = tab->ptr[t.blk][SF_VZ][FRONT];
-  double* __restrict__ Un = tab->ptr[t.blk][SF_VX][ALT];
-  double* __restrict__ Vn = tab->ptr[t.blk][SF_VY][ALT];
-  double* __restrict__ Wn = tab->ptr[t.blk][SF_VZ][ALT];
-  const double beta = ctl->beta, dt = ctl->dt;
+// One tile of the fused half-sweep; returns the tile's max |divu'| bits for
+// this thread. CG = the persistent loop (k_pressure_loop): the tile reads
+// state other SMs wrote since the kernel started, so data loads bypass L1
+// (ld.global.cg).
+template <bool CG>
+__device__ __forceinline__ double ldd(const double* p) {
+  if constexpr (CG) return __ldcg(p); else return *p;
+}
+
+// the buffers of one half-sweep: read divu, vx, vy, vz; write their next
+// versions; p in place
+struct sd_bufs {
+  double *D, *U, *V, *W;  // read
+  double *Dn, *Un, *Vn, *Wn, *P;
+  __device__ __forceinline__ void flip() {  // the next half-sweep reads what this one wrote
+    double* t;
+    t = D; D = Dn; Dn = t;
+    t = U; U = Un; Un = t;
+    t = V; V = Vn; Vn = t;
+    t = W; W = Wn; Wn = t;
+  }
+};
+__device__ __forceinline__ sd_bufs table_bufs(const sf_dev_table* __restrict__ tab, int b, int cur) {
+  const int nxt = cur == FRONT ? ALT : FRONT;
+  return {tab->ptr[b][SF_DIVU][cur], tab->ptr[b][SF_VX][cur], tab->ptr[b][SF_VY][cur], tab->ptr[b][SF_VZ][cur],
+          tab->ptr[b][SF_DIVU][nxt], tab->ptr[b][SF_VX][nxt], tab->ptr[b][SF_VY][nxt], tab->ptr[b][SF_VZ][nxt],
+          tab->ptr[b][SF_P][FRONT]};
+}
+
+template <bool CG>
+__device__ __forceinline__ unsigned long long sweep_div_tile(const sf_dev_block& B, const sd_bufs& bf,
+                                                             const tile_loc& t, const sf_consts& s, double beta,
+                                                             double dt, int color) {
+  const double* __restrict__ D = bf.D;
+  double* __restrict__ Dn = bf.Dn;
+  double* __restrict__ P = bf.P;
+  const double* __restrict__ U = bf.U;
+  const double* __restrict__ V = bf.V;
+  const double* __restrict__ W = bf.W;
+  double* __restrict__ Un = bf.Un;
+  double* __restrict__ Vn = bf.Vn;
+  double* __restrict__ Wn = bf.Wn;
   sweep_ctx x;
-  x.color = ctl->color;
+  x.color = color;
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -451,7 +485,7 @@ __global__ void __launch_bounds__(kTX* kTY) k_sweep_div(sf_dev_table* __restrict
 
     long long o = off(B, i, j, t.k0);
     double wm_new;  // swept w of the -z neighbour
-    double dC = D[o];
+    double dC = ldd<CG>(D + o);
     {
       const long long k = t.k0;
       const long long gk = B.lo[2] + k;
@@ -461,32 +495,32 @@ __global__ void __launch_bounds__(kTX* kTY) k_sweep_div(sf_dev_table* __restrict
         const long long gkm = gk - 1;
         const int bzm = bit_in(x, 2, gkm), bzpm = bit_next(x, 2, gkm);
         const double a0m = act0(x, gi + gj + gkm), a1m = 1.0 - a0m;
-        const double d0m = x.mb[bx][by][bzm] * D[o - sxy] * a0m;
-        const double ezm = x.mb[bx][by][bzpm] * dC * a1m;
-        wm_new = W[o - sxy] + cw * (d0m - ezm);
+        const double d0m = x.m(bx, by, bzm) * ldd<CG>(D + o - sxy) * a0m;
+        const double ezm = x.m(bx, by, bzpm) * dC * a1m;
+        wm_new = ldd<CG>(W + o - sxy) + cw * (d0m - ezm);
       } else if (fzl == FACE_PROC || fzl == FACE_SELF) {
         const long long gkm = B.nb_ghost_gidx[4];
         const int bzm = bit_in(x, 2, gkm), bzpm = bit_next(x, 2, gkm);
         const double a0m = act0(x, gi + gj + gkm), a1m = 1.0 - a0m;
-        const double d0m = x.mb[bx][by][bzm] * D[o - sxy] * a0m;
-        const double ezm = x.mb[bx][by][bzpm] * dC * a1m;
-        wm_new = W[o - sxy] + cw * (d0m - ezm);
+        const double d0m = x.m(bx, by, bzm) * ldd<CG>(D + o - sxy) * a0m;
+        const double ezm = x.m(bx, by, bzpm) * dC * a1m;
+        wm_new = ldd<CG>(W + o - sxy) + cw * (d0m - ezm);
       } else {
-        wm_new = W[o - sxy];  // wall / symmetry pin; outflow fixed up below
+        wm_new = ldd<CG>(W + o - sxy);  // wall / symmetry pin; outflow fixed up below
       }
     }
     for (long long k = t.k0; k < t.k1; ++k, o += sxy) {
       const long long gk = B.lo[2] + k;
       const int bz = bit_in(x, 2, gk), bzp = bit_next(x, 2, gk);
-      const double dXp = D[o + 1], dYp = D[o + sx], dZp = D[o + sxy];
-      const double dXm = D[o - 1], dYm = D[o - sx];
-      const double p0 = P[o], u0 = U[o], v0 = V[o], w0 = W[o];
+      const double dXp = ldd<CG>(D + o + 1), dYp = ldd<CG>(D + o + sx), dZp = ldd<CG>(D + o + sxy);
+      const double dXm = ldd<CG>(D + o - 1), dYm = ldd<CG>(D + o - sx);
+      const double p0 = ldd<CG>(P + o), u0 = ldd<CG>(U + o), v0 = ldd<CG>(V + o), w0 = ldd<CG>(W + o);
       const double a0 = act0(x, gi + gj + gk), a1 = 1.0 - a0;
       // this cell's sweep (cfd.hpp:712-719)
-      const double d0 = x.mb[bx][by][bz] * dC * a0;
-      const double ex = x.mb[bxp][by][bz] * dXp * a1;
-      const double ey = x.mb[bx][byp][bz] * dYp * a1;
-      const double ez = x.mb[bx][by][bzp] * dZp * a1;
+      const double d0 = x.m(bx, by, bz) * dC * a0;
+      const double ex = x.m(bxp, by, bz) * dXp * a1;
+      const double ey = x.m(bx, byp, bz) * dYp * a1;
+      const double ez = x.m(bx, by, bzp) * dZp * a1;
       P[o] = p0 + d0;
       double un = u0 + cu * (d0 - ex);
       double vn = v0 + cv * (d0 - ey);
@@ -499,26 +533,26 @@ __global__ void __launch_bounds__(kTX* kTY) k_sweep_div(sf_dev_table* __restrict
       if (i > 0 || fxl == FACE_PROC || fxl == FACE_SELF) {
         const double a0m = i > 0 ? a1 : act0(x, gim + gj + gk);
         const double a1m = 1.0 - a0m;
-        const double d0m = x.mb[bxm][by][bz] * dXm * a0m;
-        const double exm = x.mb[bxpm][by][bz] * dC * a1m;
-        umn = U[o - 1] + cu * (d0m - exm);
+        const double d0m = x.m(bxm, by, bz) * dXm * a0m;
+        const double exm = x.m(bxpm, by, bz) * dC * a1m;
+        umn = ldd<CG>(U + o - 1) + cu * (d0m - exm);
       } else if (fxl == FACE_OUT) {
         umn = un;
       } else {
-        umn = U[o - 1];
+        umn = ldd<CG>(U + o - 1);
       }
       // swept -y neighbour of v
       double vmn;
       if (j > 0 || fyl == FACE_PROC || fyl == FACE_SELF) {
         const double a0m = j > 0 ? a1 : act0(x, gi + gjm + gk);
         const double a1m = 1.0 - a0m;
-        const double d0m = x.mb[bx][bym][bz] * dYm * a0m;
-        const double eym = x.mb[bx][bypm][bz] * dC * a1m;
-        vmn = V[o - sx] + cv * (d0m - eym);
+        const double d0m = x.m(bx, bym, bz) * dYm * a0m;
+        const double eym = x.m(bx, bypm, bz) * dC * a1m;
+        vmn = ldd<CG>(V + o - sx) + cv * (d0m - eym);
       } else if (fyl == FACE_OUT) {
         vmn = vn;
       } else {
-        vmn = V[o - sx];
+        vmn = ldd<CG>(V + o - sx);
       }
       if (k == 0 && fzl == FACE_OUT) wm_new = wn;
       // DIVERGENCE on the refreshed velocities (cfd.hpp:605-608)
@@ -564,41 +598,58 @@ __global__ void __launch_bounds__(kTX* kTY) k_sweep_div(sf_dev_table* __restrict
       dC = dZp;
     }
   }
-  block_max_atomic<1>(rmax, &ctl->acc[0]);
-  if (!finalize) return;  // across ranks: allreduce, then CTL_FINISH_FUSED
-  if (last_cta(&ctl->ctas_done, total_ctas)) {
-    if (threadIdx.x == 0 && threadIdx.y == 0) {
-      __threadfence();
-      const unsigned long long rb = *reinterpret_cast<volatile unsigned long long*>(&ctl->acc[0]);
-      const double residual = bits_to_max(rb);
-      ctl->acc[0] = 0ull;
-      ctl->ctas_done = 0u;
-      ctl->residual = residual;
-      ctl->color ^= 1;
-      const int sweeps = ctl->sweeps + 1;
-      ctl->sweeps = sweeps;
-      const int more = (residual > ctl->tolerance) && (sweeps < ctl->max_sweeps);
-      ctl->done = more ? 0 : 1;
-      for (int b = 0; b < tab->nblocks; ++b) {
-        for (int f = 0; f < 5; ++f) {
-          if (f == SF_P) continue;
-          double* tmp = tab->ptr[b][f][FRONT];
-          tab->ptr[b][f][FRONT] = tab->ptr[b][f][ALT];
-          tab->ptr[b][f][ALT] = tmp;
-          const unsigned char ti = tab->bidx[b][f][FRONT];
-          tab->bidx[b][f][FRONT] = tab->bidx[b][f][ALT];
-          tab->bidx[b][f][ALT] = ti;
-        }
-      }
-      if (hflag) {
-        hflag->sweeps = sweeps;
-        hflag->residual = residual;
-        hflag->done = more ? 0 : 1;
-        hflag->color = ctl->color;
-        __threadfence_system();
-      }
+  return rmax[0];
+}
+
+// The last CTA's bookkeeping after a half-sweep (cfd.hpp:295-303): residual,
+// colour flip, sweep count, loop test, FRONT <-> ALT swap of the velocities
+// and divu of every block, and (hflag) the host-visible copy.
+__device__ __forceinline__ void finish_half_sweep(sf_dev_table* __restrict__ tab, sf_dev_ctl* ctl,
+                                                  sf_host_flag* hflag) {
+  __threadfence();
+  const unsigned long long rb = *reinterpret_cast<volatile unsigned long long*>(&ctl->acc[0]);
+  const double residual = bits_to_max(rb);
+  ctl->acc[0] = 0ull;
+  ctl->ctas_done = 0u;
+  ctl->residual = residual;
+  ctl->color ^= 1;
+  const int sweeps = ctl->sweeps + 1;
+  ctl->sweeps = sweeps;
+  const int more = (residual > ctl->tolerance) && (sweeps < ctl->max_sweeps);
+  ctl->done = more ? 0 : 1;
+  for (int b = 0; b < tab->nblocks; ++b) {
+    for (int f = 0; f < 5; ++f) {
+      if (f == SF_P) continue;
+      double* tmp = tab->ptr[b][f][FRONT];
+      tab->ptr[b][f][FRONT] = tab->ptr[b][f][ALT];
+      tab->ptr[b][f][ALT] = tmp;
+      const unsigned char ti = tab->bidx[b][f][FRONT];
+      tab->bidx[b][f][FRONT] = tab->bidx[b][f][ALT];
+      tab->bidx[b][f][ALT] = ti;
     }
   }
+  if (hflag) {
+    hflag->sweeps = sweeps;
+    hflag->residual = residual;
+    hflag->done = more ? 0 : 1;
+    hflag->color = ctl->color;
+    __threadfence_system();
+  }
+}
+
+__global__ void __launch_bounds__(kTX* kTY) k_sweep_div(sf_dev_table* __restrict__ tab,
+                                                        const sf_work* __restrict__ items,
+                                                        int nitems, int zc, sf_consts s,
+                                                        sf_dev_ctl* ctl, sf_host_flag* hflag,
+                                                        unsigned int total_ctas, int finalize) {
+  if (pred_done(ctl)) return;
+  const tile_loc t = locate(items, nitems, zc);
+  unsigned long long rmax[1] = {
+      sweep_div_tile<false>(tab->blk[t.blk], table_bufs(tab, t.blk, FRONT), t, s, ctl->beta, ctl->dt, ctl->color)};
+  block_max_atomic<1>(rmax, &ctl->acc[0]);
+  if (!finalize) return;  // across ranks: allreduce, then CTL_FINISH_FUSED
+  if (last_cta(&ctl->ctas_done, total_ctas))
+    if (threadIdx.x == 0 && threadIdx.y == 0) finish_half_sweep(tab, ctl, hflag);
 }
 
 void launch_sweep_div(const table_view& vw, int nctas, int zc, const sf_consts& c,
@@ -606,6 +657,111 @@ void launch_sweep_div(const table_view& vw, int nctas, int zc, const sf_consts& 
   if (nctas <= 0) return;
   k_sweep_div<<<nctas, dim3(kTX, kTY), 0, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
                                                  (unsigned)nctas, fin);
+}
+
+// Persistent pressure loop (cooperative launch) for grids smaller than about
+// one wave of CTAs, where a launch per half-sweep costs more than the sweep.
+// Every CTA strides over the tiles; one grid barrier per half-sweep replaces
+// the kernel boundary. After it every CTA reads the half-sweep's residual and
+// takes the loop decision itself (the same test as finish_half_sweep), so no
+// second barrier is needed: the residual maxima rotate over three slots
+// (half-sweep m accumulates into racc[m % 3]; CTA 0 clears racc[(m + 1) % 3],
+// whose readers all passed barrier m - 1), and the FRONT/ALT parity is kept
+// in registers. CTA 0 writes the loop state and the table swap once at the
+// end. The cells are the same sweep_div_tile as k_sweep_div: bitwise equal.
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kTX* kTY, 2) k_pressure_loop(sf_dev_table* __restrict__ tab,
+                                                            const sf_work* __restrict__ items, int nitems,
+                                                            int zc, sf_consts s, sf_dev_ctl* ctl, int ntiles) {
+  __shared__ unsigned long long s_res;
+  if (pred_done(ctl)) return;
+  const int tid = threadIdx.y * kTX + threadIdx.x;
+  const int b = items[0].blk;  // one grid component
+  const sf_dev_block& B = tab->blk[b];
+  sd_bufs bf = table_bufs(tab, b, FRONT);
+  const double beta = ctl->beta, dt = ctl->dt, tol = ctl->tolerance;
+  const int sweeps0 = ctl->sweeps, max_sweeps = ctl->max_sweeps, color0 = ctl->color;
+  const unsigned int nctas = gridDim.x;
+  int m = 0;
+  double residual = 0.0;
+  bool more = true;
+  while (more) {
+    if (blockIdx.x == 0 && tid == 0) ctl->racc[(m + 1) % 3] = 0ull;
+    unsigned long long rmax[1] = {0ull};
+    for (int c = blockIdx.x; c < ntiles; c += gridDim.x) {
+      const unsigned long long r = sweep_div_tile<true>(B, bf, locate_at(items, nitems, zc, c), s, beta, dt,
+                                                        color0 ^ (m & 1));
+      rmax[0] = r > rmax[0] ? r : rmax[0];
+    }
+    block_max_atomic<1>(rmax, &ctl->racc[m % 3]);  // ends with thread 0's atomic
+    __syncthreads();
+    if (tid == 0) {  // arrive (release: this CTA's stores and atomics), wait (acquire)
+      const unsigned int target = nctas * (unsigned)(m + 1);
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ctl->bar) : "memory");
+      while (ld_acquire(&ctl->bar) < target) {
+      }
+      s_res = ld_acquire64(&ctl->racc[m % 3]);
+    }
+    __syncthreads();
+    residual = bits_to_max(s_res);
+    const int sweeps = sweeps0 + m + 1;
+    more = (residual > tol) && (sweeps < max_sweeps);
+    bf.flip();
+    ++m;
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    ctl->residual = residual;
+    ctl->sweeps = sweeps0 + m;
+    ctl->color = color0 ^ (m & 1);
+    ctl->done = 1;
+    if (m & 1) {
+      for (int f = 0; f < 5; ++f) {
+        if (f == SF_P) continue;
+        double* tmp = tab->ptr[b][f][FRONT];
+        tab->ptr[b][f][FRONT] = tab->ptr[b][f][ALT];
+        tab->ptr[b][f][ALT] = tmp;
+        const unsigned char ti = tab->bidx[b][f][FRONT];
+        tab->bidx[b][f][FRONT] = tab->bidx[b][f][ALT];
+        tab->bidx[b][f][ALT] = ti;
+      }
+    }
+  }
+}
+
+int pressure_loop_ctas() {
+  static std::mutex mu;
+  static std::map<int, int> per_dev;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = per_dev.find(dev);
+  if (it != per_dev.end()) return it->second;
+  int per_sm = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pressure_loop, kTX * kTY, 0);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return per_dev[dev] = per_sm * sms;
+}
+
+cudaError_t launch_pressure_loop(const table_view& vw, int ntiles, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                                 cudaStream_t st) {
+  if (ntiles <= 0) return cudaSuccess;
+  const int grid = std::min(ntiles, pressure_loop_ctas());
+  sf_dev_table* tab = vw.tab;
+  const sf_work* items = vw.items;
+  int nitems = vw.nitems;
+  sf_consts cc = c;
+  void* args[] = {&tab, &items, &nitems, &zc, &cc, &ctl, &ntiles};
+  return cudaLaunchCooperativeKernel((const void*)k_pressure_loop, dim3(grid), dim3(kTX, kTY), args, 0, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -748,6 +904,8 @@ __global__ void k_ctl(sf_dev_table* tab, sf_dev_ctl* ctl, sf_host_flag* hflag, i
       ctl->acc[1] = 0ull;
       ctl->ctas_done = 0u;
       ctl->redo = 0;
+      ctl->racc[0] = ctl->racc[1] = ctl->racc[2] = 0ull;
+      ctl->bar = 0u;
       ctl->done = ctl->abort_field >= 0 ? 1 : 0;
       ctl->max_sweeps = s.max_sweeps;
       ctl->tolerance = s.tolerance;

@@ -49,6 +49,11 @@ void launch_pressure_sweep(const View& vw, int nctas, int zc, const sf_consts& c
 // redo of a temporal pass's first sweep (see launch_sweep2)
 void launch_sweep_div(const table_view& vw, int nctas, int zc, const sf_consts& c,
                       sf_dev_ctl* ctl, sf_host_flag* hflag, int fin, cudaStream_t st);
+// The whole pressure loop in one cooperative launch (single process, no
+// processor faces): min(ntiles, co-resident CTAs) CTAs stride over the tiles.
+cudaError_t launch_pressure_loop(const table_view& vw, int ntiles, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                                 cudaStream_t st);
+int pressure_loop_ctas();
 // TMA-pipelined fused half-sweep (sf_sweep_tma.cu); maps = device sweep_maps.
 void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_consts& c,
                           sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,

@@ -592,3 +592,41 @@ def test_temporal_pass_with_overlapped_halo_exchange_matches_the_reference(ref_a
     assert [[x.dt, x.sweeps, x.residual] for x in dd] == [[float(a), int(b), float(r)] for a, b, r in zip(*so)]
     assert dv.kernel_timing("sweep2")[1] > 0
     assert dv.checksum() == o.checksum()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_persistent_pressure_loop_matches_the_reference(ref_available, seed, monkeypatch):
+    # the cooperative whole-loop kernel (one launch per pressure loop, two grid
+    # barriers per half-sweep) against the oracle: random extents and
+    # periodicity, tolerance and capped stops, z chunks 1..8 (so CTAs stride
+    # over more tiles than are co-resident for the larger cases)
+    rng = np.random.default_rng(700 + seed)
+    ext = (int(rng.integers(5, 70)), int(rng.integers(4, 40)), int(rng.integers(3, 30)))
+    per = tuple(bool(rng.integers(0, 2)) for _ in range(3)) if seed % 2 else (False,) * 3
+    monkeypatch.setenv("SF_PERSIST", "1")
+    monkeypatch.setenv("SF_PZC", str(int(rng.choice([1, 2, 4, 8]))))
+    c = Case(extents=ext, periodic=per, tolerance=float(rng.choice([1e-3, 1e-12])), max_sweeps=int(rng.integers(1, 60)),
+             viscosity=0.05, lid_speed=0.0 if any(per) else 1.0, workers=1)
+    o, d = _random_case_pair(c, 31 + seed, int(rng.choice([1, 3, 2])))
+    d.launch_count(reset=True)
+    so = o.advance(3)
+    dd = [d.step() for _ in range(3)]
+    assert [[x.dt, x.sweeps, x.residual] for x in dd] == [[float(a), int(b), float(r)] for a, b, r in zip(*so)]
+    for f in FIELDS5:
+        assert same(d.gather(f), o.gather(f)), f
+    assert d.pending_color == o.pending_color
+    assert d.launch_count() < 3 * 40, "one pressure-loop launch per step"
+
+
+def test_persistent_pressure_loop_matches_the_launch_per_sweep_paths(monkeypatch):
+    # grids above one wave of CTAs (SF_PZC=1 -> 2400 tiles): the strided tile
+    # loop against the temporal pass and the single-sweep kernel
+    out = {}
+    for mode, fused in (("1", 3), ("0", 1), ("0", 3)):
+        monkeypatch.setenv("SF_PERSIST", mode)
+        monkeypatch.setenv("SF_PZC", "1")
+        s = dev_cavity((150, 80, 24), tolerance=1e-5, max_sweeps=90, symmetry_z=False, fused=fused)
+        s.init_cavity()
+        st = [s.step() for _ in range(3)]
+        out[(mode, fused)] = ([[x.dt, x.sweeps, x.residual] for x in st], s.checksum(), s.pending_color)
+    assert out[("1", 3)] == out[("0", 1)] == out[("0", 3)]
