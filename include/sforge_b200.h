@@ -197,6 +197,13 @@ int sf_sim_scatter_block(sf_sim* s, const char* field, int worker, const double*
  * Uploads and downloads of different fields overlap (PCIe is full duplex). */
 int sf_sim_gather_block_async(sf_sim* s, const char* field, int worker, double* host, int64_t n);
 int sf_sim_scatter_block_async(sf_sim* s, const char* field, int worker, const double* host, int64_t n);
+/* scatter_block_async in two halves, so the next step's inputs cross PCIe
+ * while the current step computes: stage queues the upload into the field's
+ * device buffer (after the last install out of it); install_staged queues the
+ * copy into the field, in order with compute enqueued before and after it.
+ * install_staged without a staged upload fails (SF_ERR_ARG). */
+int sf_sim_stage_block_async(sf_sim* s, const char* field, int worker, const double* host, int64_t n);
+int sf_sim_install_staged(sf_sim* s, const char* field, int worker);
 /* The exchange plan of one refresh phase (axis 0..2, slabs widened as in
  * exchange.hpp:165-206) or of the fused loop's face exchange (axis = -1) for
  * rank `rank` of a `world`-rank decomposition -- host logic, no device.  Rows

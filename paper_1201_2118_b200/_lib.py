@@ -204,6 +204,8 @@ SIGNATURES = [
     ("sf_sim_scatter_block", [_vp, _cp, _i, _vp, _i64], _i),
     ("sf_sim_gather_block_async", [_vp, _cp, _i, _vp, _i64], _i),
     ("sf_sim_scatter_block_async", [_vp, _cp, _i, _vp, _i64], _i),
+    ("sf_sim_stage_block_async", [_vp, _cp, _i, _vp, _i64], _i),
+    ("sf_sim_install_staged", [_vp, _cp, _i], _i),
     ("sf_exchange_plan", [_i64p, _i, _i, _ip, _i, C.c_uint, _i, _i, _i64p, _ip], _i),
     ("sf_sim_synchronize", [_vp], _i),
     ("sf_sim_stream", [_vp], _vp),

@@ -563,6 +563,56 @@ class simulation {
   // Async mode returns at once: host memory must be pinned and stay untouched
   // until sf_sim_synchronize. Uploads then overlap downloads of other fields
   // (PCIe is full duplex).
+  // The two halves of an asynchronous upload. stage: H2D into the field's
+  // dense upload buffer on the upload stream, once the last install out of
+  // that buffer ran; install: a kernel on the compute stream, after the
+  // upload, copies the buffer into FRONT. Staging the next step's inputs
+  // before stepping overlaps their transfer with the step.
+  void ensure_io() {
+    if (io_[0]) return;
+    for (int k = 0; k < 2; ++k) SF_CK(cudaStreamCreateWithFlags(&io_[k], cudaStreamNonBlocking));
+    for (int k = 0; k < kMaxFields; ++k) {
+      SF_CK(cudaEventCreateWithFlags(&io_ev_[k], cudaEventDisableTiming));
+      SF_CK(cudaEventCreateWithFlags(&io_up_[k], cudaEventDisableTiming));
+      SF_CK(cudaEventCreateWithFlags(&io_snap_[k], cudaEventDisableTiming));
+      SF_CK(cudaEventCreateWithFlags(&io_snapdn_[k], cudaEventDisableTiming));
+      SF_CK(cudaEventCreateWithFlags(&io_inst_[k], cudaEventDisableTiming));
+    }
+  }
+  int owned_block(int w, i64 n) const {
+    if (w < 0 || w >= dec_.workers || lid_[w] < 0)
+      throw error(SF_ERR_ARG, "worker " + std::to_string(w) + " is not owned by this process");
+    const auto& L = lay_[lid_[w]];
+    if (n >= 0 && n < L.dims[0] * L.dims[1] * L.dims[2]) throw error(SF_ERR_ARG, "block buffer too small");
+    return lid_[w];
+  }
+  void stage_upload(int f, int b, const double* host, size_t cnt) {
+    ensure_io();
+    if (!upb_[b][f]) upb_[b][f] = (double*)dalloc(sizeof(double) * cnt);
+    SF_CK(cudaStreamWaitEvent(io_[0], io_inst_[f], 0));  // the last install out of this buffer
+    SF_CK(cudaMemcpyAsync(upb_[b][f], host, sizeof(double) * cnt, cudaMemcpyHostToDevice, io_[0]));
+    SF_CK(cudaEventRecord(io_up_[f], io_[0]));
+    staged_[b][f] = true;
+  }
+  void install_staged(int f, int b) {
+    if (!staged_[b][f]) throw error(SF_ERR_ARG, "no staged upload of field '" + fname_[f] + "'");
+    const auto& L = lay_[b];
+    flush_io();
+    SF_CK(cudaStreamWaitEvent(st_, io_up_[f], 0));
+    launch_install(dtab_, b, f, upb_[b][f], L.dims[1] * L.dims[2], st_);
+    ++launches_;
+    SF_CK(cudaEventRecord(io_inst_[f], st_));
+    staged_[b][f] = false;
+    ghosts_ok_[fname_[f]] = false;
+    check_launch();
+  }
+  void stage_block(int f, int w, const double* host, i64 n) {
+    const int b = owned_block(w, n);
+    const auto& L = lay_[b];
+    stage_upload(f, b, host, (size_t)(L.dims[0] * L.dims[1] * L.dims[2]));
+  }
+  void install_block(int f, int w) { install_staged(f, owned_block(w, -1)); }
+
   void block_io(int f, int w, double* host, i64 n, bool to_device, bool async = false) {
     if (w < 0 || w >= dec_.workers || lid_[w] < 0)
       throw error(SF_ERR_ARG, "worker " + std::to_string(w) + " is not owned by this process");
@@ -570,16 +620,7 @@ class simulation {
     const auto& L = lay_[b];
     const i64 d[3] = {L.dims[0], L.dims[1], L.dims[2]};
     if (n < d[0] * d[1] * d[2]) throw error(SF_ERR_ARG, "block buffer too small");
-    if (!io_[0]) {
-      for (int k = 0; k < 2; ++k) SF_CK(cudaStreamCreateWithFlags(&io_[k], cudaStreamNonBlocking));
-      for (int k = 0; k < kMaxFields; ++k) {
-        SF_CK(cudaEventCreateWithFlags(&io_ev_[k], cudaEventDisableTiming));
-        SF_CK(cudaEventCreateWithFlags(&io_up_[k], cudaEventDisableTiming));
-        SF_CK(cudaEventCreateWithFlags(&io_snap_[k], cudaEventDisableTiming));
-        SF_CK(cudaEventCreateWithFlags(&io_snapdn_[k], cudaEventDisableTiming));
-        SF_CK(cudaEventCreateWithFlags(&io_inst_[k], cudaEventDisableTiming));
-      }
-    }
+    ensure_io();
     if (!to_device && async) {
       // Snapshot, then download in the background: a pack task on the compute
       // stream copies the owned block into a dense device buffer (FRONT is
@@ -603,18 +644,8 @@ class simulation {
       // it into FRONT with a kernel on the compute stream (FRONT resolved on
       // the device): no host synchronisation, and compute enqueued later sees
       // the new values.
-      const size_t cnt = (size_t)(d[0] * d[1] * d[2]);
-      if (!upb_[b][f]) upb_[b][f] = (double*)dalloc(sizeof(double) * cnt);
-      SF_CK(cudaStreamWaitEvent(io_[0], io_inst_[f], 0));  // the last install out of this buffer
-      SF_CK(cudaMemcpyAsync(upb_[b][f], host, sizeof(double) * cnt, cudaMemcpyHostToDevice, io_[0]));
-      SF_CK(cudaEventRecord(io_up_[f], io_[0]));
-      flush_io();
-      SF_CK(cudaStreamWaitEvent(st_, io_up_[f], 0));
-      launch_install(dtab_, b, f, upb_[b][f], d[1] * d[2], st_);
-      ++launches_;
-      SF_CK(cudaEventRecord(io_inst_[f], st_));
-      ghosts_ok_[fname_[f]] = false;
-      check_launch();
+      stage_upload(f, b, host, (size_t)(d[0] * d[1] * d[2]));
+      install_staged(f, b);
       return;
     }
     if (fes_[f] != 8) {  // fp32 field: host values are fp64, converted through the staging buffer
@@ -1597,7 +1628,8 @@ class simulation {
   cudaEvent_t io_snapdn_[kMaxFields]{};  // last background download out of each snapshot buffer
   double* snap_[kMaxBlocks][kMaxFields]{};
   double* upb_[kMaxBlocks][kMaxFields]{};   // dense upload buffers of the asynchronous scatter
-  cudaEvent_t io_inst_[kMaxFields]{};       // last install out of each upload buffer
+  cudaEvent_t io_inst_[kMaxFields]{};
+  bool staged_[kMaxBlocks][kMaxFields]{};  // an upload is staged, not yet installed       // last install out of each upload buffer
   mutable std::vector<cudaEvent_t> io_pending_;  // not yet ordered before compute
   // compute enqueues so far / at the last table download: block_io skips the
   // download (a copy that would queue behind large transfers) when equal
@@ -2608,6 +2640,18 @@ int sf_sim_scatter_block_async(sf_sim* s, const char* field, int worker, const d
   return guarded([&] {
     need(s, "sim");
     s->s->block_io(s->s->field_id(field), worker, const_cast<double*>(host), n, true, true);
+  });
+}
+int sf_sim_stage_block_async(sf_sim* s, const char* field, int worker, const double* host, int64_t n) {
+  return guarded([&] {
+    need(s, "sim");
+    s->s->stage_block(s->s->field_id(field), worker, host, n);
+  });
+}
+int sf_sim_install_staged(sf_sim* s, const char* field, int worker) {
+  return guarded([&] {
+    need(s, "sim");
+    s->s->install_block(s->s->field_id(field), worker);
   });
 }
 int sf_sim_world(const sf_sim* s) { return s ? s->s->world() : 0; }

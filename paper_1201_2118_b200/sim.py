@@ -322,6 +322,22 @@ class Simulation:
         fn = self._lib.sf_sim_scatter_block if wait else self._lib.sf_sim_scatter_block_async
         L.check(fn(self._h, name.encode(), int(w), C.c_void_p(ptr), n))
 
+    def stage_block(self, name: str, data, worker: int | None = None):
+        """First half of an asynchronous scatter: queue the upload of ``data``
+        (pinned, unchanged until ``synchronize()``) into the field's device
+        buffer. ``install_staged`` later copies it into the field in stream
+        order, so staging step k+1's inputs before ``step()`` overlaps the
+        transfer with step k."""
+        w = self.rank if worker is None else worker
+        if not hasattr(data, "data_ptr"):
+            raise ValueError("a staged upload needs a pinned tensor")
+        L.check(self._lib.sf_sim_stage_block_async(self._h, name.encode(), int(w), C.c_void_p(data.data_ptr()),
+                                                   data.numel()))
+
+    def install_staged(self, name: str, worker: int | None = None):
+        w = self.rank if worker is None else worker
+        L.check(self._lib.sf_sim_install_staged(self._h, name.encode(), int(w)))
+
     def checksum(self) -> str:
         v = C.c_uint64()
         L.check(self._lib.sf_sim_checksum(self._h, C.byref(v)))

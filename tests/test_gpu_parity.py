@@ -630,3 +630,31 @@ def test_persistent_pressure_loop_matches_the_launch_per_sweep_paths(monkeypatch
         st = [s.step() for _ in range(3)]
         out[(mode, fused)] = ([[x.dt, x.sweeps, x.residual] for x in st], s.checksum(), s.pending_color)
     assert out[("1", 3)] == out[("0", 1)] == out[("0", 3)]
+
+
+def test_staged_uploads_install_in_stream_order():
+    # sf_sim_stage_block_async + sf_sim_install_staged: the upload staged before
+    # a step is not visible to that step, only to compute after the install
+    import torch
+    names = ("vx", "vy", "vz", "p")
+    s = dev_cavity((40, 24, 20), symmetry_z=False)
+    t = dev_cavity((40, 24, 20), symmetry_z=False)
+    for x in (s, t):
+        x.init_cavity()
+    with pytest.raises(sfb.SfError, match="no staged upload"):
+        s.install_staged("vx")
+    rng = np.random.default_rng(5)
+    nxt = {f: rng.uniform(-0.1, 0.1, size=(20, 24, 40)) for f in names}
+    pinned = {f: torch.from_numpy(nxt[f].reshape(-1)).pin_memory() for f in names}
+    for f in names:
+        s.stage_block(f, pinned[f])
+    a, b = s.step(), t.step()  # staged data not installed yet
+    assert [a.dt, a.sweeps, a.residual] == [b.dt, b.sweeps, b.residual]
+    for f in names:
+        s.install_staged(f)
+        t.scatter_block(f, nxt[f])
+    a, b = s.step(), t.step()
+    s.synchronize()
+    assert [a.dt, a.sweeps, a.residual] == [b.dt, b.sweeps, b.residual]
+    for f in FIELDS5:
+        assert same(s.gather(f), t.gather(f)), f
