@@ -143,6 +143,9 @@ int sf_sim_pending_color(sf_sim* s);          /* cfd.hpp:470 */
 int sf_sim_max_divergence(sf_sim* s, double* out);  /* cfd.hpp:342-345 */
 int sf_sim_steady_delta(sf_sim* s, double* out);    /* cfd.hpp:350-355 */
 int sf_sim_kinetic_energy(sf_sim* s, double* out);  /* cfd.hpp:357-363 */
+/* RMS distance of vx, vy, vz to the decayed Taylor-Green vortex at time t,
+ * bitwise the reference's (host sin/cos/exp, reference summation order). */
+int sf_sim_taylor_green_error(sf_sim* s, double t, double* out); /* cfd.hpp:367-401 */
 
 /* grid::scatter / grid::gather on one field (io.hpp:25-65): global x-fastest
  * float64 arrays of extents[0]*extents[1]*extents[2] values in HOST memory. */

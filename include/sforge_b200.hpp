@@ -188,6 +188,11 @@ class simulation {
     check(sf_sim_kinetic_energy(h_.get(), &v));
     return v;
   }
+  double taylor_green_error(double t) {
+    double v = 0.0;
+    check(sf_sim_taylor_green_error(h_.get(), t, &v));
+    return v;
+  }
 
   double time() const { return sf_sim_time(h_.get()); }
   long step_count() const { return sf_sim_step_count(h_.get()); }

@@ -154,6 +154,7 @@ def _load(kind: str) -> C.CDLL:
         "run_kernel": ([vp, C.c_char_p, C.c_char_p, i], i),
         "invalidate_all_ghosts": ([vp], None),
         "diag": ([vp, dp, dp, dp], i),
+        "taylor_green_error": ([vp, d, dp], i),
         "time_phases": ([vp, dp, dp, ip], i),
         "time_half_sweeps": ([vp, i, d, dp], i),
         "time_provisional": ([vp, dp, dp], i),
@@ -319,6 +320,11 @@ class Oracle:
     def kinetic_energy(self) -> float:
         v = C.c_double()
         self._ck(self._f("diag")(self._h, None, None, C.byref(v)))
+        return v.value
+
+    def taylor_green_error(self, t: float) -> float:
+        v = C.c_double()
+        self._ck(self._f("taylor_green_error")(self._h, float(t), C.byref(v)))
         return v.value
 
     def time_half_sweeps(self, k: int, beta: float) -> float:

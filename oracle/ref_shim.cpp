@@ -235,6 +235,10 @@ int sfref_diag(void* h, double* max_div, double* steady_delta, double* kinetic) 
   } catch (const std::exception& e) { return fail(e); }
 }
 
+int sfref_taylor_green_error(void* h, double t, double* out) {
+  try { *out = S(h).taylor_green_error(t); return 0; } catch (const std::exception& e) { return fail(e); }
+}
+
 // Bounded-sample timing probe for the CPU baseline:
 // wall seconds of compute_dt+provisional and of one pressure_iteration with
 // the configured max_sweeps, on this simulation's worker team.

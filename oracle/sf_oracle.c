@@ -518,6 +518,29 @@ int sfo_init_taylor_green(sfo_sim* s) {
   return 0;
 }
 
+/* cfd.hpp:367-401: RMS distance to the decayed analytic vortex, x-fastest
+ * over the owned cells (one worker, so one partial). */
+int sfo_taylor_green_error(sfo_sim* s, double t, double* out) {
+  const double tau = 2.0 * 3.14159265358979323846;
+  const double decay = exp(-2.0 * s->P.viscosity * tau * tau * t);
+  const double dx = s->P.spacing[0], dy = s->P.spacing[1];
+  fld *U = &s->f[F_VX], *V = &s->f[F_VY], *W = &s->f[F_VZ];
+  double sum = 0.0;
+  for (int64_t k = 0; k < U->n[2]; ++k)
+    for (int64_t j = 0; j < U->n[1]; ++j)
+      for (int64_t i = 0; i < U->n[0]; ++i) {
+        const double xc = ((double)i + 0.5) * dx, yc = ((double)j + 0.5) * dy;
+        const double xf = (double)(i + 1) * dx, yf = (double)(j + 1) * dy;
+        const double eu = AT(U, i, j, k) - sin(tau * xf) * cos(tau * yc) * decay;
+        const double ev = AT(V, i, j, k) + cos(tau * xc) * sin(tau * yf) * decay;
+        const double ew = AT(W, i, j, k);
+        sum += eu * eu + ev * ev + ew * ew;
+      }
+  const double n = (double)(U->n[0] * U->n[1] * U->n[2]);
+  *out = sqrt(sum / (3.0 * n));
+  return 0;
+}
+
 /* ---- data movement (io.hpp:25-65) ---------------------------------------- */
 int sfo_scatter(sfo_sim* s, const char* name, const double* global, int64_t n) {
   const int id = field_id(name);

@@ -175,6 +175,7 @@ SIGNATURES = [
     ("sf_sim_max_divergence", [_vp, _dp], _i),
     ("sf_sim_steady_delta", [_vp, _dp], _i),
     ("sf_sim_kinetic_energy", [_vp, _dp], _i),
+    ("sf_sim_taylor_green_error", [_vp, _d, _dp], _i),
     ("sf_sim_scatter", [_vp, _cp, _vp, _i64], _i),
     ("sf_sim_gather", [_vp, _cp, _vp, _i64], _i),
     ("sf_sim_scatter_device", [_vp, _cp, _vp, _i64], _i),

@@ -1544,6 +1544,65 @@ class simulation {
     d = d < m[2] ? m[2] : d;
     return d;
   }
+  // RMS distance to the decayed analytic vortex (cfd.hpp:367-401). The
+  // analytic factors use the host's sin/cos/exp as the reference does; the
+  // device evaluates each cell's term with the reference's operations; the
+  // host sums them in the reference's order (x-fastest within a worker,
+  // workers in order), so the result is bitwise the reference's.
+  double taylor_green_error(double t) {
+    const double tau = 2.0 * 3.14159265358979323846;
+    const double decay = std::exp(-2.0 * par_.viscosity * tau * tau * t);
+    const double dx = cfg_.spacing[0], dy = cfg_.spacing[1];
+    download_table();
+    std::vector<std::pair<int, double>> part;  // (worker, partial)
+    for (int b = 0; b < nloc_; ++b) {
+      const auto& L = lay_[b];
+      const sf_dev_block& B = htab_->blk[b];
+      const i64 nx = L.dims[0], ny = L.dims[1], nz = L.dims[2];
+      std::vector<double> tab(2 * (size_t)(nx * ny));
+      for (i64 j = 0; j < ny; ++j)
+        for (i64 i = 0; i < nx; ++i) {
+          const double xc = (static_cast<double>(B.lo[0] + i) + 0.5) * dx;
+          const double yc = (static_cast<double>(B.lo[1] + j) + 0.5) * dy;
+          const double xf = static_cast<double>(B.lo[0] + i + 1) * dx;
+          const double yf = static_cast<double>(B.lo[1] + j + 1) * dy;
+          tab[j * nx + i] = std::sin(tau * xf) * std::cos(tau * yc);
+          tab[nx * ny + j * nx + i] = std::cos(tau * xc) * std::sin(tau * yf);
+        }
+      double* dtabv = (double*)dalloc_tmp(sizeof(double) * tab.size());
+      SF_CK(cudaMemcpyAsync(dtabv, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice, st_));
+      const i64 dims[3] = {nx, ny, nz};
+      double* out = staging();
+      launch_tg_cells(htab_->ptr[b][SF_VX][FRONT], htab_->ptr[b][SF_VY][FRONT], htab_->ptr[b][SF_VZ][FRONT],
+                      L.base, L.sx, L.sy, dims, dtabv, dtabv + nx * ny, decay, out, st_);
+      ++launches_;
+      check_launch();
+      std::vector<double> cellv((size_t)(nx * ny * nz));
+      SF_CK(cudaMemcpyAsync(cellv.data(), out, sizeof(double) * cellv.size(), cudaMemcpyDeviceToHost, st_));
+      sync();
+      SF_CK(cudaFree(dtabv));
+      double sum = 0.0;
+      for (double x : cellv) sum += x;
+      part.push_back({gid_[b], sum});
+    }
+    std::vector<double> all;
+    if (dist_) {  // one block per rank: gather the partials, combine in rank (= worker) order
+      double* d = (double*)dalloc_tmp(sizeof(double) * (size_t)(world_ + 1));
+      SF_CK(cudaMemcpyAsync(d, &part[0].second, sizeof(double), cudaMemcpyHostToDevice, st_));
+      SF_NC(nccl()->AllGather(d, d + 1, 1, kNcclFloat64, comm_, st_));
+      all.resize(world_);
+      SF_CK(cudaMemcpyAsync(all.data(), d + 1, sizeof(double) * world_, cudaMemcpyDeviceToHost, st_));
+      sync();
+      SF_CK(cudaFree(d));
+    } else {
+      std::sort(part.begin(), part.end());
+      for (const auto& p : part) all.push_back(p.second);
+    }
+    double total = 0.0;
+    for (double x : all) total += x;
+    const double n = static_cast<double>(cells());
+    return std::sqrt(total / (3.0 * n));
+  }
   double kinetic_energy() {
     const double s = reduce(SF_VX, SF_SUM_SQ) + reduce(SF_VY, SF_SUM_SQ) + reduce(SF_VZ, SF_SUM_SQ);
     const double cell = cfg_.spacing[0] * cfg_.spacing[1] * cfg_.spacing[2];
@@ -2730,6 +2789,9 @@ int sf_sim_max_divergence(sf_sim* s, double* out) {
 }
 int sf_sim_steady_delta(sf_sim* s, double* out) {
   return guarded([&] { *out = SIM(s).steady_delta(); });
+}
+int sf_sim_taylor_green_error(sf_sim* s, double t, double* out) {
+  return guarded([&] { *out = SIM(s).taylor_green_error(t); });
 }
 int sf_sim_kinetic_energy(sf_sim* s, double* out) {
   return guarded([&] { *out = SIM(s).kinetic_energy(); });

@@ -764,6 +764,34 @@ cudaError_t launch_pressure_loop(const table_view& vw, int ntiles, int zc, const
   return cudaLaunchCooperativeKernel((const void*)k_pressure_loop, dim3(grid), dim3(kTX, kTY), args, 0, st);
 }
 
+// taylor_green_error per cell (cfd.hpp:388-393): eu = u - (sin*cos)*decay,
+// ev = v + (cos*sin)*decay, ew = w; the host sums the terms in the
+// reference's order (x-fastest per worker, workers in order).
+__global__ void k_tg_cells(const double* __restrict__ U, const double* __restrict__ V,
+                           const double* __restrict__ W, long long base, long long sx, long long sy, int nx,
+                           int ny, int nz, const double* __restrict__ su, const double* __restrict__ sv,
+                           double decay, double* __restrict__ out) {
+  const long long n = (long long)nx * ny * nz;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % nx), j = (int)((e / nx) % ny), k = (int)(e / ((long long)nx * ny));
+    const long long o = base + ((long long)k * sy + j) * sx + i;
+    const double eu = U[o] - su[(long long)j * nx + i] * decay;
+    const double ev = V[o] + sv[(long long)j * nx + i] * decay;
+    const double ew = W[o];
+    out[e] = eu * eu + ev * ev + ew * ew;
+  }
+}
+
+void launch_tg_cells(const double* U, const double* V, const double* W, long long base, long long sx, long long sy,
+                     const long long dims[3], const double* su, const double* sv, double decay, double* out,
+                     cudaStream_t st) {
+  const long long n = dims[0] * dims[1] * dims[2];
+  if (n <= 0) return;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 16);
+  k_tg_cells<<<blocks, 256, 0, st>>>(U, V, W, base, sx, sy, (int)dims[0], (int)dims[1], (int)dims[2], su, sv, decay,
+                                     out);
+}
+
 // ---------------------------------------------------------------------------
 // reductions (reductions.hpp:28-90)
 // ---------------------------------------------------------------------------

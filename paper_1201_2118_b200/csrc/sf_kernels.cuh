@@ -118,6 +118,11 @@ void launch_copy_box(const double* src, long long s_base, long long s_sx, long l
                      cudaStream_t st);
 void launch_fill_box(double* dst, long long base, long long sx, long long sy, const long long lo[3],
                      const long long dims[3], double v, cudaStream_t st);
+// taylor_green_error's per-cell term (cfd.hpp:388-393) of one block into a
+// dense x-fastest buffer; su / sv: the analytic sin*cos factors per (i, j)
+void launch_tg_cells(const double* U, const double* V, const double* W, long long base, long long sx, long long sy,
+                     const long long dims[3], const double* su, const double* sv, double decay, double* out,
+                     cudaStream_t st);
 // element sizes 8 (double) or 4 (float); values convert on the way
 void launch_copy_box_es(const void* src, int s_es, long long s_base, long long s_sx, long long s_sy, void* dst,
                         int d_es, long long d_base, long long d_sx, long long d_sy, const long long lo[3],

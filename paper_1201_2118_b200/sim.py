@@ -252,6 +252,12 @@ class Simulation:
         L.check(self._lib.sf_sim_steady_delta(self._h, C.byref(v)))
         return v.value
 
+    def taylor_green_error(self, t: float) -> float:
+        """RMS distance to the decayed analytic vortex (cfd.hpp:367-401), bitwise the reference's."""
+        v = C.c_double()
+        L.check(self._lib.sf_sim_taylor_green_error(self._h, float(t), C.byref(v)))
+        return v.value
+
     def kinetic_energy(self) -> float:
         v = C.c_double()
         L.check(self._lib.sf_sim_kinetic_energy(self._h, C.byref(v)))

@@ -29,6 +29,36 @@ def cavity_run(n, steps_list, **kw):
     return out
 
 
+def taylor_green_order(n, workers=2):
+    """Acceptance check 6 (tests/acceptance/acceptance_main.cpp:416-446): the
+    periodic Taylor-Green vortex on unit_box(n, n, 2) to T = 0.5 with 2
+    workers; returns [error, steps, total sweeps]."""
+    from oracle.oracle import Case
+    c = Case(extents=(n, n, 2), periodic=(True, True, True), tolerance=1e-8, max_sweeps=20000, viscosity=0.01,
+             lid_speed=0.0, workers=workers)
+    o = Oracle(c, "ref")
+    o.init_taylor_green()
+    T, t, steps, sweeps = 0.5, 0.0, 0, 0
+    while t < T:
+        dt = min(o.compute_dt(), T - t)
+        o.provisional(dt)
+        sw, _ = o.pressure_iteration(dt)
+        o.refresh(["p"])
+        t += dt
+        steps += 1
+        sweeps += sw
+    return [o.taylor_green_error(T), steps, sweeps]
+
+
+def add_taylor_green():
+    path = os.path.join(os.path.dirname(__file__), "golden.json")
+    g = json.load(open(path))
+    g["taylor_green_order"] = {str(n): taylor_green_order(n) for n in (32, 64)}
+    with open(path, "w") as f:
+        json.dump(g, f, indent=1)
+    print(g["taylor_green_order"])
+
+
 def main():
     t0 = time.time()
     g = {"source": "oracle/_ref/libsfref.so (reference stencilforge compiled in place)"}
@@ -41,6 +71,7 @@ def main():
     g["quasi2d_33"] = cavity_run((33, 33, 3), [20], sigma=0.8)
     g["cavity24_g2"] = cavity_run(24, [3], symmetry_z=False, ghost=2)
     g["cavity24_g3_w1"] = cavity_run(24, [2], symmetry_z=False, ghost=3)
+    g["taylor_green_order"] = {str(n): taylor_green_order(n) for n in (32, 64)}
     g["elapsed_s"] = time.time() - t0
     # the reference's own recorded artifacts of runs/re100.cfg (acceptance 7/8),
     # copied verbatim as data fixtures: profiles.csv is byte-reproducible
@@ -57,4 +88,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--taylor-green"]:  # only the acceptance-6 entry, merged into the existing JSON
+        add_taylor_green()
+    else:
+        main()

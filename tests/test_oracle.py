@@ -89,3 +89,35 @@ def test_reference_golden_fixture_is_reproducible(ref_available):
     o.init_cavity()
     o.advance(2)
     assert o.checksum() == GOLDEN["cavity24_g3_w1"]["checksums"]["2"]
+
+
+def _taylor_green_run(backend, n, workers=1, T=0.5):
+    # acceptance check 6's loop (tests/acceptance/acceptance_main.cpp:416-440)
+    c = Case(extents=(n, n, 2), periodic=(True, True, True), tolerance=1e-8, max_sweeps=20000, viscosity=0.01,
+             lid_speed=0.0, workers=workers)
+    o = Oracle(c, backend)
+    o.init_taylor_green()
+    t, steps, sweeps = 0.0, 0, 0
+    while t < T:
+        dt = min(o.compute_dt(), T - t)
+        o.provisional(dt)
+        sw, _ = o.pressure_iteration(dt)
+        o.refresh(["p"])
+        t += dt
+        steps += 1
+        sweeps += sw
+    return o.taylor_green_error(T), steps, sweeps
+
+
+def test_port_taylor_green_error_matches_the_reference(ref_available):
+    # cfd.hpp:367-401 restated in C: bitwise on one worker, at the start and
+    # after the vortex decays to T = 0.5
+    for T in (0.0, 0.5):
+        assert _taylor_green_run("port", 16, T=T) == _taylor_green_run("ref", 16, T=T)
+
+
+def test_taylor_green_order_golden_is_the_reference_check_6(ref_available):
+    # the acceptance-6 fixture (2 workers, 32^2 and 64^2): error falls >= 3.6x
+    g = GOLDEN["taylor_green_order"]
+    assert list(_taylor_green_run("ref", 32, workers=2)) == g["32"]
+    assert g["32"][0] / g["64"][0] >= 3.6
