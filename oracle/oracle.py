@@ -178,6 +178,29 @@ def available(kind: str) -> bool:
         return False
 
 
+def ref_ccl(text: str, fields: Sequence[str] | None = None, directory: str | None = None) -> tuple[int, str]:
+    """The reference's descriptor front end (descriptor.hpp / codegen.hpp) on
+    `text`: without `fields`, parse + canonical render; with them, parse +
+    validate_all + the concatenated rendered headers, and write_generated into
+    `directory`. Returns (0, result) or (1 parse_error | 2 descriptor_error |
+    3 other, message)."""
+    lib = _load("ref")
+    buf = C.create_string_buffer(1 << 20)
+    if fields is None:
+        f = lib.sfref_ccl_render
+        f.argtypes, f.restype = [C.c_char_p, C.c_char_p, C.c_size_t], C.c_int
+        rc = f(text.encode(), buf, len(buf))
+    else:
+        f = lib.sfref_ccl_generate
+        f.argtypes, f.restype = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_size_t], C.c_int
+        rc = f(text.encode(), ",".join(fields).encode(), (directory or ".").encode(), buf, len(buf))
+    if rc == 0:
+        return 0, buf.value.decode()
+    err = lib.sfref_last_error
+    err.restype = C.c_char_p
+    return rc, err().decode()
+
+
 def _dp(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 

@@ -11,6 +11,8 @@
 //   cli::field_checksum        proj/include/stencilforge/bench.hpp:24-39
 //   exec::executor             proj/include/stencilforge/executor.hpp:477-862
 //   grid::reduce               proj/include/stencilforge/reductions.hpp:28-90
+//   ccl::parse_descriptors / render / validate_all   descriptor.hpp:148-381
+//   codegen::render_header / write_generated         codegen.hpp:86-163
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -22,6 +24,8 @@
 
 #include "stencilforge/bench.hpp"
 #include "stencilforge/cfd.hpp"
+#include "stencilforge/codegen.hpp"
+#include "stencilforge/descriptor.hpp"
 #include "stencilforge/io.hpp"
 
 using namespace sforge;
@@ -237,6 +241,34 @@ int sfref_diag(void* h, double* max_div, double* steady_delta, double* kinetic) 
 
 int sfref_taylor_green_error(void* h, double t, double* out) {
   try { *out = S(h).taylor_green_error(t); return 0; } catch (const std::exception& e) { return fail(e); }
+}
+
+// Descriptor front end. Results are text written to out (cap bytes); the
+// return code says which stage failed: 0 ok, 1 parse_error, 2
+// descriptor_error, 3 other, 4 buffer too small; g_err holds the message.
+static int put(const std::string& r, char* out, size_t cap) {
+  if (r.size() + 1 > cap) return 4;
+  std::memcpy(out, r.c_str(), r.size() + 1);
+  return 0;
+}
+int sfref_ccl_render(const char* text, char* out, size_t cap) {
+  try {
+    return put(ccl::render(ccl::parse_descriptors(text)), out, cap);
+  } catch (const ccl::parse_error& e) { g_err = e.what(); return 1;
+  } catch (const std::exception& e) { g_err = e.what(); return 3; }
+}
+// headers of every kernel (concatenated) followed by the plans.txt manifest
+int sfref_ccl_generate(const char* text, const char* fields_csv, const char* dir, char* out, size_t cap) {
+  try {
+    const auto v = split_csv(fields_csv);
+    const auto ks = ccl::validate_all(ccl::parse_descriptors(text), std::set<std::string>(v.begin(), v.end()));
+    std::string r;
+    for (const auto& k : ks) r += codegen::render_header(k, codegen::build_plan(k).tmpl).text;
+    codegen::write_generated(ks, dir);
+    return put(r, out, cap);
+  } catch (const ccl::parse_error& e) { g_err = e.what(); return 1;
+  } catch (const ccl::descriptor_error& e) { g_err = e.what(); return 2;
+  } catch (const std::exception& e) { g_err = e.what(); return 3; }
 }
 
 // Bounded-sample timing probe for the CPU baseline:

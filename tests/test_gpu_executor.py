@@ -505,3 +505,30 @@ def test_mixed_precision_kernel_computes_in_fp64(radius):
     want = lap_np(data, radius)
     assert same(s.gather("lu"), want)
     assert same(s.gather("lu64"), want)
+
+
+SMOOTH_CCL = """# a user kernel declared in the descriptor language
+CCTK_CUDA_KERNEL SMOOTH TYPE=3DBLOCK STENCIL="1,1,1,1,1,1" TILE="8,4,4"
+{
+  CCTK_CUDA_KERNEL_VARIABLE CACHED=YES INTENT=IN { src } "SOURCE"
+  CCTK_CUDA_KERNEL_VARIABLE INTENT=OUT { dst } "RESULT"
+}
+"""
+
+
+@pytest.mark.parametrize("workers", [1, 4])
+def test_descriptor_file_drives_a_device_kernel(workers):
+    # .ccl text -> parse -> validate against the store's fields -> plan ->
+    # register_kernel -> run: the plugin path from the descriptor front end on
+    from paper_1201_2118_b200.descriptor import load_plans
+    n = 12
+    data = random_global((n, n, n), 7)
+    s = rig((n, n, n), workers, 1, (True, True, True))
+    s.create_field("src")
+    s.create_field("dst")
+    s.scatter("src", data)
+    plan = load_plans(SMOOTH_CCL, sfb.FIELDS + ("src", "dst"))["SMOOTH"]
+    s.register_kernel(plan, (["src", "dst"], []), SMOOTH_BODY)
+    s.exchange(["src"])
+    s.run_kernel("SMOOTH")
+    assert same(s.gather("dst"), smooth_np(data))
