@@ -93,6 +93,64 @@ def write_residuals(rows) -> str:
     return out.getvalue()
 
 
+SFG1_MAGIC = b"SFG1"
+
+
+def write_sfg1(out, extents, data) -> None:
+    """grid::write_sfg1 (io.hpp:66-84): "SFG1", nx ny nz as little-endian
+    int64, then nx*ny*nz little-endian float64 values, x fastest. ``out`` is a
+    binary stream or a path."""
+    import numpy as np
+    from ._lib import GridError
+    a = np.ascontiguousarray(data, dtype="<f8").reshape(-1)
+    if a.size != int(extents[0]) * int(extents[1]) * int(extents[2]):
+        raise GridError(2, "SFG1 write: data size does not match extents")
+    blob = SFG1_MAGIC + np.asarray([int(e) for e in extents], dtype="<i8").tobytes() + a.tobytes()
+    if isinstance(out, (str, bytes)) or hasattr(out, "__fspath__"):
+        with open(out, "wb") as f:
+            f.write(blob)
+    else:
+        out.write(blob)
+
+
+def read_sfg1(src):
+    """grid::read_sfg1 (io.hpp:86-101): returns (extents, values as a
+    (nz, ny, nx) float64 array); the same error texts."""
+    import numpy as np
+    from ._lib import GridError
+    if isinstance(src, (str, bytes)) or hasattr(src, "__fspath__"):
+        with open(src, "rb") as f:
+            blob = f.read()
+    else:
+        blob = src.read()
+    if blob[:4] != SFG1_MAGIC:
+        raise GridError(2, "not an SFG1 stream")
+    ext = []
+    for a in range(3):
+        raw = blob[4 + 8 * a:12 + 8 * a]
+        v = int(np.frombuffer(raw, dtype="<i8")[0]) if len(raw) == 8 else 0
+        if v < 1:
+            raise GridError(2, "SFG1 read: bad extents")
+        ext.append(v)
+    n = ext[0] * ext[1] * ext[2]
+    payload = blob[28:28 + 8 * n]
+    if len(payload) != 8 * n:
+        raise GridError(2, "SFG1 read: truncated payload")
+    return tuple(ext), np.frombuffer(payload, dtype="<f8").reshape(ext[2], ext[1], ext[0]).astype(np.float64)
+
+
+def dump_fields(sim: Simulation, directory: str) -> list:
+    """sforge.cpp dump_fields (:176-185): vx, vy, vz, p gathered to <dir>/<name>.sfg1."""
+    import os
+    os.makedirs(directory, exist_ok=True)
+    written = []
+    for name in ("vx", "vy", "vz", "p"):
+        path = os.path.join(directory, name + ".sfg1")
+        write_sfg1(path, sim.extents, sim.gather(name))
+        written.append(path)
+    return written
+
+
 def run_cavity(nx=129, ny=129, nz=3, re=100.0, sigma=0.9, omega=1.9525, tolerance=1e-6, max_sweeps=3000,
                alpha=0.0, lid_speed=1.0, symmetry_z=True, steady_tol=1e-6, max_steps=200000, workers=1,
                device=0, fused=1, progress=None):

@@ -690,3 +690,43 @@ def test_taylor_green_convergence_order_matches_the_reference_check_6(fused):
     e1 = _device_taylor_green(32, 1, fused)
     assert e1[1:] == g["32"][1:] and e1[0] == pytest.approx(g["32"][0], rel=1e-13)
     assert g["32"][0] / g["64"][0] >= 3.6
+
+
+SMALL_CAVITY_CFG = """nx = 17
+ny = 17
+nz = 3
+re = 100
+sigma = 0.9
+omega = 1.9525
+tolerance = 1e-6
+max_sweeps = 3000
+alpha = 0
+steady_tol = 1e-5
+max_steps = 200000
+output_cadence = 2000
+profiles_out = profiles.csv
+residuals_out = residuals.csv
+fields_out = fields
+"""
+
+
+def test_cavity_harness_outputs_are_byte_identical_to_the_reference_cli(tmp_path):
+    # the reference's own `sforge cavity` (oracle/_ref/sforge, built from
+    # proj/tools/sforge.cpp) against this harness on a 17x17x3 cavity to
+    # steady state: profiles.csv, residuals.csv and the SFG1 field dumps
+    import subprocess
+    from paper_1201_2118_b200.cavity import dump_fields, run_cavity
+    cli = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref", "sforge")
+    if not os.path.exists(cli):
+        pytest.skip("oracle/_ref/sforge not built")
+    ref = tmp_path / "ref"
+    ref.mkdir()
+    (ref / "small.cfg").write_text(SMALL_CAVITY_CFG)
+    subprocess.run([cli, "cavity", "--config", "small.cfg"], cwd=ref, check=True, capture_output=True, timeout=300)
+    summary, profiles, residuals, sim = run_cavity(nx=17, ny=17, nz=3, steady_tol=1e-5)
+    assert summary.converged
+    assert profiles == (ref / "profiles.csv").read_text()
+    assert residuals == (ref / "residuals.csv").read_text()
+    for path in dump_fields(sim, str(tmp_path / "mine")):
+        name = os.path.basename(path)
+        assert open(path, "rb").read() == (ref / "fields" / name).read_bytes(), name

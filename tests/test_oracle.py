@@ -121,3 +121,33 @@ def test_taylor_green_order_golden_is_the_reference_check_6(ref_available):
     g = GOLDEN["taylor_green_order"]
     assert list(_taylor_green_run("ref", 32, workers=2)) == g["32"]
     assert g["32"][0] / g["64"][0] >= 3.6
+
+
+def test_sfg1_format_round_trips_the_reference_cli_dumps(tmp_path):
+    # grid::write_sfg1 / read_sfg1 (io.hpp:66-101): files written by the
+    # reference's `sforge cavity` read back and rewrite byte for byte
+    import io
+    import subprocess
+
+    from paper_1201_2118_b200 import GridError
+    from paper_1201_2118_b200.cavity import read_sfg1, write_sfg1
+    cli = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref", "sforge")
+    if not os.path.exists(cli):
+        pytest.skip("oracle/_ref/sforge not built")
+    (tmp_path / "c.cfg").write_text("nx = 9\nny = 7\nnz = 3\nmax_steps = 3\nsteady_tol = 1e-30\nfields_out = f\n"
+                                    "profiles_out = p.csv\nresiduals_out = r.csv\n")
+    # (exits 1: "not steady after 3 steps"; the dumps are written first)
+    subprocess.run([cli, "cavity", "--config", "c.cfg"], cwd=tmp_path, capture_output=True, timeout=300)
+    for name in ("vx", "vy", "vz", "p"):
+        blob = (tmp_path / "f" / (name + ".sfg1")).read_bytes()
+        ext, data = read_sfg1(io.BytesIO(blob))
+        assert ext == (9, 7, 3) and data.shape == (3, 7, 9)
+        out = io.BytesIO()
+        write_sfg1(out, ext, data)
+        assert out.getvalue() == blob
+    with pytest.raises(GridError, match="not an SFG1 stream"):
+        read_sfg1(io.BytesIO(b"XXXX"))
+    with pytest.raises(GridError, match="truncated payload"):
+        read_sfg1(io.BytesIO(blob[:-8]))
+    with pytest.raises(GridError, match="does not match extents"):
+        write_sfg1(io.BytesIO(), (2, 2, 2), np.zeros(7))
