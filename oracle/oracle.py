@@ -201,6 +201,21 @@ def ref_ccl(text: str, fields: Sequence[str] | None = None, directory: str | Non
     return rc, err().decode()
 
 
+def ref_parse_config(text: str) -> tuple[int, str]:
+    """The reference's cli::parse_run_config on `text`: (0, key=value lines) or
+    (1 config_error | 2 cfd_error | 3 other, message)."""
+    lib = _load("ref")
+    buf = C.create_string_buffer(1 << 16)
+    f = lib.sfref_parse_config
+    f.argtypes, f.restype = [C.c_char_p, C.c_char_p, C.c_size_t], C.c_int
+    rc = f(text.encode(), buf, len(buf))
+    if rc == 0:
+        return 0, buf.value.decode()
+    err = lib.sfref_last_error
+    err.restype = C.c_char_p
+    return rc, err().decode()
+
+
 def _dp(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 

@@ -25,6 +25,7 @@
 #include "stencilforge/bench.hpp"
 #include "stencilforge/cfd.hpp"
 #include "stencilforge/codegen.hpp"
+#include "stencilforge/config.hpp"
 #include "stencilforge/descriptor.hpp"
 #include "stencilforge/io.hpp"
 
@@ -268,6 +269,29 @@ int sfref_ccl_generate(const char* text, const char* fields_csv, const char* dir
     return put(r, out, cap);
   } catch (const ccl::parse_error& e) { g_err = e.what(); return 1;
   } catch (const ccl::descriptor_error& e) { g_err = e.what(); return 2;
+  } catch (const std::exception& e) { g_err = e.what(); return 3; }
+}
+
+// cli::parse_run_config on text: every field as key=value lines (%.17g for
+// reals); 1 config_error, 2 cfd_error (the cross-field validate), 3 other.
+int sfref_parse_config(const char* text, char* out, size_t cap) {
+  try {
+    std::istringstream in(text);
+    const cli::run_config rc = cli::parse_run_config(in);
+    char b[2048];
+    std::snprintf(b, sizeof b,
+                  "nx=%ld\nny=%ld\nnz=%ld\nre=%.17g\nsigma=%.17g\nomega=%.17g\ntolerance=%.17g\nmax_sweeps=%ld\n"
+                  "alpha=%.17g\ndensity=%.17g\nlid_speed=%.17g\nsymmetry_z=%d\nsteady_tol=%.17g\nmax_steps=%ld\n"
+                  "output_cadence=%ld\nworkers=%d\nmode=%s\ntile=%d,%d,%d\nghost=%d\n",
+                  rc.nx, rc.ny, rc.nz, rc.re, rc.sigma, rc.omega, rc.tolerance, rc.max_sweeps, rc.alpha, rc.density,
+                  rc.lid_speed, rc.symmetry_z ? 1 : 0, rc.steady_tol, rc.max_steps, rc.output_cadence, rc.workers,
+                  rc.mode == exec::run_mode::plain ? "plain" : "overlap", rc.tile[0], rc.tile[1], rc.tile[2],
+                  rc.ghost);
+    return put(std::string(b) + "profiles_out=" + rc.profiles_out + "\nresiduals_out=" + rc.residuals_out +
+                   "\nfields_out=" + rc.fields_out + "\n",
+               out, cap);
+  } catch (const cli::config_error& e) { g_err = e.what(); return 1;
+  } catch (const cfd::cfd_error& e) { g_err = e.what(); return 2;
   } catch (const std::exception& e) { g_err = e.what(); return 3; }
 }
 
