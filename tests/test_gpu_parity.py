@@ -730,3 +730,27 @@ def test_cavity_harness_outputs_are_byte_identical_to_the_reference_cli(tmp_path
     for path in dump_fields(sim, str(tmp_path / "mine")):
         name = os.path.basename(path)
         assert open(path, "rb").read() == (ref / "fields" / name).read_bytes(), name
+
+
+@pytest.mark.parametrize("workers", [1, 2])
+def test_cavity_cli_matches_the_reference_cli(tmp_path, workers):
+    # `python -m paper_1201_2118_b200 cavity --config` against `sforge cavity`:
+    # the same stdout, exit status, CSVs and SFG1 dumps
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cli = os.path.join(root, "oracle", "_ref", "sforge")
+    if not os.path.exists(cli):
+        pytest.skip("oracle/_ref/sforge not built")
+    cfg = SMALL_CAVITY_CFG.replace("output_cadence = 2000", "output_cadence = 50")
+    res = {}
+    for name, cmd in (("mine", [sys.executable, "-m", "paper_1201_2118_b200"]), ("ref", [cli])):
+        d = tmp_path / name
+        d.mkdir()
+        (d / "c.cfg").write_text(cfg)
+        p = subprocess.run(cmd + ["cavity", "--config", "c.cfg", "--workers", str(workers)], cwd=d,
+                           capture_output=True, text=True, timeout=600, env=dict(os.environ, PYTHONPATH=root))
+        res[name] = (p.returncode, p.stdout, p.stderr)
+    assert res["mine"] == res["ref"] and res["ref"][0] == 0
+    for f in ("profiles.csv", "residuals.csv", "fields/vx.sfg1", "fields/vy.sfg1", "fields/vz.sfg1", "fields/p.sfg1"):
+        assert (tmp_path / "mine" / f).read_bytes() == (tmp_path / "ref" / f).read_bytes(), f
