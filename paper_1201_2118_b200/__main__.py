@@ -6,6 +6,8 @@
                                      the lid-driven cavity to steady state on the GPU
   validate --profiles <csv> --reference <csv> --tol <t>
                                      centerline profiles against a reference table
+  bench --config <file> [--workers 1,2,4] [--modes plain,overlap] [--steps N] [--out bench.csv]
+                                     the fixed-step benchmark table and CSV
 
 Same output lines, files and exit status (0 ok, 1 run or validation failure,
 2 usage error) as the reference's CLI. ``--mode`` and ``--tile`` select the
@@ -29,6 +31,9 @@ commands:
       run the lid-driven cavity to steady state, write profile and residual CSVs
   validate --profiles <csv> --reference <csv> --tol <t>
       compare centerline profiles against a reference table
+  bench --config <file> [--workers 1,2,4] [--modes plain,overlap] [--steps N]
+        [--out bench.csv]
+      fixed-step strong-scaling benchmark
 
 exit status: 0 success, 1 run or validation failure, 2 usage error
 """
@@ -288,6 +293,93 @@ def cmd_validate(args):
     return EXIT_FAILURE
 
 
+def cmd_bench(args):
+    """sforge bench (sforge.cpp:296-349, bench.hpp:46-143) on the device:
+    `workers` grid components on one GPU, each (workers, mode) run timed over
+    advance(steps) after a device synchronisation on both sides. The
+    reference's `bytes_staged` column (its executor's tile-staging ledger) is
+    the device path's algorithmic HBM traffic, 56 + 32 + 80 * sweeps bytes per
+    cell and step."""
+    import time
+
+    from .config import load_run_config
+    from .sim import Simulation
+    config_path, out_path, steps = "", "bench.csv", 20
+    workers, modes = [1, 2, 4], ["plain", "overlap"]
+    i = 0
+    while i < len(args):
+        a = args[i]
+        if a == "--config":
+            config_path = _flag_value(args, i, a)
+        elif a == "--workers":
+            workers = []
+            for part in _flag_value(args, i, a).split(","):
+                w = _parse_long(part, "--workers")
+                if w < 1:
+                    raise UsageError("--workers entries must be at least 1")
+                workers.append(w)
+        elif a == "--modes":
+            modes = []
+            for part in _flag_value(args, i, a).split(","):
+                if part not in ("plain", "overlap"):
+                    raise UsageError("mode must be plain or overlap, got '%s'" % part)
+                modes.append(part)
+        elif a == "--steps":
+            steps = _parse_long(_flag_value(args, i, a), "--steps")
+            if steps < 1:
+                raise UsageError("--steps must be at least 1")
+        elif a == "--out":
+            out_path = _flag_value(args, i, a)
+        else:
+            raise UsageError("unknown option '%s'" % a)
+        i += 2
+    if not config_path:
+        raise UsageError("bench needs --config <file>")
+    rc = load_run_config(config_path)
+    rows = []
+    for w in workers:
+        for mode in modes:
+            sim = Simulation(rc.solver(), rc.fluid(), workers=w, mode=mode, ghost=rc.ghost)
+            sim.init_cavity()
+            sim.synchronize()
+            sweeps = 0
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                sweeps += sim.step().sweeps
+            sim.synchronize()
+            wall = time.perf_counter() - t0
+            cells = rc.nx * rc.ny * rc.nz
+            rows.append({"workers": w, "mode": mode, "ext": (rc.nx, rc.ny, rc.nz), "steps": steps, "wall": wall,
+                         "ups": cells * steps / wall if wall > 0 else 0.0,
+                         "bytes": cells * ((56 + 32) * steps + 80 * sweeps), "checksum": sim.checksum()})
+            sim.close()
+    for r in rows:
+        base = min((o for o in rows if o["mode"] == r["mode"]), key=lambda o: o["workers"])
+        r["speedup"] = 1.0 if base is r else (base["wall"] / r["wall"] if r["wall"] > 0 else 1.0)
+    print("%8s %8s %14s %7s %10s %14s %8s %14s  %s" % ("workers", "mode", "grid", "steps", "wall[s]", "updates/s",
+                                                       "speedup", "bytes staged", "checksum"))
+    for r in rows:
+        print("%8d %8s %14s %7d %10.3f %14.4g %8.2f %14d  %s" % (
+            r["workers"], r["mode"], "%dx%dx%d" % r["ext"], r["steps"], r["wall"], r["ups"], r["speedup"],
+            r["bytes"], r["checksum"]))
+    with open(out_path, "w", newline="") as f:
+        f.write("workers,mode,nx,ny,nz,steps,wall_seconds,updates_per_second,speedup,bytes_staged,checksum\n")
+        for r in rows:
+            f.write("%d,%s,%d,%d,%d,%d,%.6f,%.6g,%.4f,%d,%s\n" % (
+                r["workers"], r["mode"], r["ext"][0], r["ext"][1], r["ext"][2], r["steps"], r["wall"], r["ups"],
+                r["speedup"], r["bytes"], r["checksum"]))
+    print("wrote " + out_path)
+    sys.stdout.flush()
+    mismatch = False
+    for a in rows:
+        for b in rows:
+            if a["workers"] == b["workers"] and a["checksum"] != b["checksum"]:
+                sys.stderr.write("sforge: checksum mismatch at %d workers: %s=%s vs %s=%s\n" % (
+                    a["workers"], a["mode"], a["checksum"], b["mode"], b["checksum"]))
+                mismatch = True
+    return EXIT_FAILURE if mismatch else EXIT_OK
+
+
 def main(argv=None) -> int:
     argv = list(sys.argv[1:] if argv is None else argv)
     if not argv:
@@ -301,6 +393,8 @@ def main(argv=None) -> int:
             return cmd_cavity(args)
         if cmd == "validate":
             return cmd_validate(args)
+        if cmd == "bench":
+            return cmd_bench(args)
         if cmd in ("-h", "--help", "help"):
             sys.stdout.write(SYNOPSIS)
             return EXIT_OK

@@ -754,3 +754,29 @@ def test_cavity_cli_matches_the_reference_cli(tmp_path, workers):
     assert res["mine"] == res["ref"] and res["ref"][0] == 0
     for f in ("profiles.csv", "residuals.csv", "fields/vx.sfg1", "fields/vy.sfg1", "fields/vz.sfg1", "fields/p.sfg1"):
         assert (tmp_path / "mine" / f).read_bytes() == (tmp_path / "ref" / f).read_bytes(), f
+
+
+def test_bench_cli_checksums_match_the_reference_bench(tmp_path):
+    # `python -m paper_1201_2118_b200 bench` against `sforge bench` on a 16^3
+    # fixed-step cavity: the CSV schema, grid/steps columns and the final-field
+    # checksums per (workers, mode) agree (the timings differ, of course)
+    import csv
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cli = os.path.join(root, "oracle", "_ref", "sforge")
+    if not os.path.exists(cli):
+        pytest.skip("oracle/_ref/sforge not built")
+    cfg = "nx = 16\nny = 16\nnz = 16\nsymmetry_z = false\ntolerance = 1e-30\nmax_sweeps = 40\n"
+    out = {}
+    for name, cmd in (("mine", [sys.executable, "-m", "paper_1201_2118_b200"]), ("ref", [cli])):
+        d = tmp_path / name
+        d.mkdir()
+        (d / "b.cfg").write_text(cfg)
+        p = subprocess.run(cmd + ["bench", "--config", "b.cfg", "--workers", "1,2", "--steps", "3"], cwd=d,
+                           capture_output=True, text=True, timeout=600, env=dict(os.environ, PYTHONPATH=root))
+        assert p.returncode == 0, p.stderr
+        out[name] = list(csv.DictReader(open(d / "bench.csv")))
+    assert list(out["mine"][0].keys()) == list(out["ref"][0].keys())
+    key = ("workers", "mode", "nx", "ny", "nz", "steps", "checksum")
+    assert [[r[k] for k in key] for r in out["mine"]] == [[r[k] for k in key] for r in out["ref"]]
