@@ -48,13 +48,6 @@ __device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P1;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      " @!P1 bra W_%=;\n}\n" ::"r"(smem32(bar)),
-      "r"(parity)
-      : "memory");
-}
 __device__ __forceinline__ void prefetch3(const CUtensorMap* map, int x, int y, int z) {
   asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
