@@ -2347,6 +2347,7 @@ class simulation {
   // (SF_PERSIST=0 off, =1 whenever it applies).
   bool persistent() {
     if (persist_env_ == 0 || dist_ || timing_ || !opt_.fused || nloc_ != 1 || has_proc_faces()) return false;
+    if (pressure_loop_ctas() < 1) return false;  // no co-resident CTA (occupancy query failed)
     const phase& ph = phase_for(1u << SF_DIVU, -1, SF_SCOPE_ALL, true);
     if (ph.first.n || ph.unpack.n || !ph.sends.empty() || !ph.recvs.empty()) return false;
     if (persist_env_ == 1) return true;
