@@ -232,6 +232,9 @@ def run_ours(args):
     dist = None
     if world > 1 or args.force_dist:  # one rank per GPU over NCCL, weak scaling: n^3 per rank
         import torch.distributed as dist
+        if "RANK" not in os.environ:  # --force-dist without a launcher: a one-rank job
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         uid = [sfb.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
