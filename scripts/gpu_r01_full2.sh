@@ -12,3 +12,4 @@ for f in ("bench_default","bench_tma1","bench_ref"):
         print(f, d.get("value"), d.get("ms_per_step"), (d.get("e2e") or {}).get("value"), (d.get("roofline") or {}).get("frac"), (d.get("cpu_baseline") or {}).get("value"), d.get("clocks"))
     except Exception as e: print(f, "ERR", e)
 P
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
