@@ -963,6 +963,10 @@ class simulation {
       src += "#define SF_NC " + std::to_string(uk.cslot.size()) + "\n__device__ constexpr int SF_CSLOT[] = {" + csl +
              "};\n#define SF_XL " + std::to_string(uk.xl) + "\n#define SF_BW " + std::to_string(uk.bw) +
              "\n#define SF_BH " + std::to_string(uk.bh) + "\n#define SF_R " + std::to_string(uk.ring) + "\n";
+      // one unrolled two-plane body per z-queue phase (sf_jit.hpp)
+      src += "#define SF_PLANE_CASES";
+      for (int p = 0; p < uk.halo[4] + uk.halo[5] + 1; ++p) src += " SF_PLANES(" + std::to_string(p) + ")";
+      src += "\n";
       size_t txb = 0;  // bytes one plane of every cached binding brings in
       for (int c : uk.cslot) txb += (size_t)uk.bw * uk.bh * fes_[uk.fid[c]];
       src += "#define SF_TXB " + std::to_string(txb) + "\n";

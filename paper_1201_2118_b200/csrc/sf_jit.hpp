@@ -194,6 +194,7 @@ __device__ __forceinline__ unsigned sa(const void* p) { return (unsigned)__cvta_
 constexpr int SF_PLANE = (SF_BW * SF_BH + 15) / 16 * 16;  // 128-byte aligned ring planes
 
 constexpr int SF_ZW = SF_HALO[4] + SF_HALO[5] + 1;  // z window of the stencil
+template <int N> struct sf_ic { static constexpr int value = N; };
 
 struct cell_view {
   const double* rd;
@@ -202,7 +203,11 @@ struct cell_view {
   int slot;
   const double* rb;  // cached: ring base + this cell's in-plane offset
   int zoff[SF_ZW];   // cached: ring-plane offset for dk = t - halo_lo_z (updated per plane)
-  sf_real zq[SF_ZW];  // cached: this column's values for dk = t - halo_lo_z (register queue)
+  // cached: this column's values of the z window, plane z in slot z % SF_ZW
+  // (a circular register queue: nothing shifts; ph = this plane's slot is a
+  // compile-time constant in every unrolled plane body)
+  sf_real zq[SF_ZW];
+  int ph;
   __device__ __forceinline__ sf_real operator()(int di, int dj, int dk) const {
 #if SF_DEBUG
     if (!SF_READABLE[slot]) { sf_violation(1, slot, di, dj, dk); return 0.0; }
@@ -212,7 +217,7 @@ struct cell_view {
 #endif
     // the column itself comes from the register queue: one shared-memory load
     // per plane instead of one per z offset (offsets fold to constants)
-    if (SF_CACHED[slot] && di == 0 && dj == 0) return zq[dk + SF_HALO[4]];
+    if (SF_CACHED[slot] && di == 0 && dj == 0) return zq[(ph + dk + SF_ZW) % SF_ZW];
     if (SF_CACHED[slot]) return ring(zoff[dk + SF_HALO[4]], dj * SF_BW + di);
     const long long q = o + di + dj * sx + dk * sxy;
     if (SF_F32[slot]) {  // fp32 fields widen exactly (to sf_real)
@@ -341,23 +346,22 @@ sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
     if (qn < nload) wait(qn);
     if (two && qn + 1 < nload) wait(qn + 1);
     if (act) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h == 1 && !two) break;
-        const int kq = kk + h;
+      // plane kq's body with its queue slot PH = kq % SF_ZW known at compile time
+      auto plane = [&](auto phc, int kq) {
+        constexpr int PH = decltype(phc)::value;
 #pragma unroll
         for (int s = 0; s < SF_NB; ++s) {
           c.f_[s].o = o;
+          c.f_[s].ph = PH;
 #pragma unroll
           for (int t = 0; t < SF_ZW; ++t) c.f_[s].zoff[t] = zr[t];
-          if (SF_CACHED[s]) {  // column queue: shift in the plane that entered the window
+          if (SF_CACHED[s]) {  // column queue: load the plane that entered the window
             if (kq == 0) {
 #pragma unroll
-              for (int t = 0; t < SF_ZW; ++t) c.f_[s].zq[t] = c.f_[s].ring(zr[t], 0);
+              for (int t = 0; t < SF_ZW; ++t)
+                c.f_[s].zq[(PH + t - SF_HALO[4] + SF_ZW) % SF_ZW] = c.f_[s].ring(zr[t], 0);
             } else {
-#pragma unroll
-              for (int t = 0; t < SF_ZW - 1; ++t) c.f_[s].zq[t] = c.f_[s].zq[t + 1];
-              c.f_[s].zq[SF_ZW - 1] = c.f_[s].ring(zr[SF_ZW - 1], 0);
+              c.f_[s].zq[(PH + SF_HALO[5]) % SF_ZW] = c.f_[s].ring(zr[SF_ZW - 1], 0);
             }
           }
         }
@@ -367,7 +371,16 @@ sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
 #pragma unroll
         for (int t = 0; t < SF_ZW - 1; ++t) zr[t] = zr[t + 1];
         zr[SF_ZW - 1] = ((kq + SF_ZW) % SF_R) * SF_PLANE;
+      };
+#define SF_PLANES(P)                                              \
+  case P:                                                         \
+    plane(sf_ic<(P) % SF_ZW>{}, kk);                              \
+    if (two) plane(sf_ic<((P) + 1) % SF_ZW>{}, kk + 1);           \
+    break;
+      switch (kk % SF_ZW) {
+        SF_PLANE_CASES
       }
+#undef SF_PLANES
     }
     __syncthreads();  // planes kk, kk+1 (ring q = kk, kk+1) left every window
     if (tid == 0) {
