@@ -1,0 +1,116 @@
+"""Randomised parity stress run: the device (every pressure-loop path the
+configuration selects: persistent loop, temporal pass, fused half-sweeps,
+unfused dataflow) against the reference compiled in place, bitwise, on random
+cavities (extents, periodicity, ghost width, grid components, random initial
+velocities, tolerance- and cap-driven stops). Test infrastructure: uses
+oracle/ (the checker). Prints one line per case and a summary.
+
+  python scripts/probes/parity_stress.py [n_cases] [seed] [max_seconds]
+"""
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_1201_2118_b200 as sfb  # noqa: E402
+from oracle.oracle import Case, Oracle  # noqa: E402
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+def gen(rng):
+    """All random draws of one case (so a case can be replayed by index)."""
+    per = tuple(bool(rng.integers(0, 2)) for _ in range(3)) if rng.random() < 0.3 else (False,) * 3
+    workers = int(rng.choice([1, 1, 1, 2, 3, 4]))
+    ghost = int(rng.choice([1, 1, 2, 3]))
+    lo = 2 * ghost + 2
+    ext = tuple(int(rng.integers(max(lo, 5), 48)) for _ in range(2)) + (int(rng.integers(max(lo, 3), 40)),)
+    fused = int(rng.choice([1, 1, 3, 2, 0]))
+    tol = float(rng.choice([1e-2, 1e-3, 1e-5, 1e-30]))
+    maxs = int(rng.integers(1, 80))
+    kw = dict(viscosity=float(rng.uniform(0.005, 0.05)))
+    kw["lid"] = 0.0 if any(per) else float(rng.uniform(0.2, 1.5))  # drawn only for walled boxes
+    kw.update(omega=float(rng.uniform(1.0, 1.95)), sigma=float(rng.uniform(0.2, 0.9)), symz=bool(rng.integers(0, 2)))
+    fields = {f: rng.uniform(-0.5, 0.5, size=ext[::-1]) for f in ("vx", "vy", "vz")} if rng.random() < 0.7 else None
+    steps = int(rng.integers(1, 4))
+    return dict(per=per, workers=workers, ghost=ghost, ext=ext, fused=fused, tol=tol, maxs=maxs, fields=fields,
+                steps=steps, **kw)
+
+
+def run(p, fused=None, detail=False):
+    ext, per, workers, ghost = p["ext"], p["per"], p["workers"], p["ghost"]
+    fused = p["fused"] if fused is None else fused
+    lid = p["lid"]
+    c = Case(extents=ext, periodic=per, tolerance=p["tol"], max_sweeps=p["maxs"], viscosity=p["viscosity"],
+             lid_speed=lid, workers=workers, ghost=ghost, omega=p["omega"], sigma=p["sigma"], symmetry_z=p["symz"])
+    o = Oracle(c, "ref")
+    cfg = sfb.SolverConfig(extents=ext, periodic=per, tolerance=p["tol"], max_sweeps=p["maxs"], omega=p["omega"],
+                           sigma=p["sigma"], symmetry_z=p["symz"])
+    d = sfb.Simulation(cfg, sfb.FluidParams(viscosity=p["viscosity"], lid_speed=lid), workers=workers,
+                       ghost=ghost, fused=fused)
+    o.init_cavity()
+    d.init_cavity()
+    if p["fields"]:
+        for f, a in p["fields"].items():
+            o.scatter(f, a)
+            d.scatter(f, a)
+        o.invalidate_all_ghosts()
+        d.invalidate_all_ghosts()
+    so = o.advance(p["steps"])
+    dd = [d.step() for _ in range(p["steps"])]
+    st_d = [[x.dt, x.sweeps, x.residual] for x in dd]
+    st_o = [[float(a), int(b), float(r)] for a, b, r in zip(*so)]
+    ok = st_d == st_o
+    diff = {}
+    for f in ("vx", "vy", "vz", "p"):
+        a, b = d.gather(f), o.gather(f)
+        e = not np.array_equal(bits(a), bits(b))
+        ok = ok and not e
+        if e and detail:
+            w = np.argwhere(bits(a) != bits(b))
+            diff[f] = (len(w), w[:3].tolist(), float(np.nanmax(np.abs(a - b))))
+    ok = ok and d.pending_color == o.pending_color
+    desc = "ext=%s per=%s w=%d g=%d fused=%d tol=%g maxs=%d steps=%d sweeps=%s" % (
+        ext, "".join("1" if q else "0" for q in per), workers, ghost, fused, p["tol"], p["maxs"], p["steps"],
+        [x.sweeps for x in dd])
+    if detail:
+        desc += "\n   device %s\n   oracle %s\n   fields %s" % (st_d, st_o, diff)
+    d.close()
+    return ok, desc
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 2026
+    budget = float(sys.argv[3]) if len(sys.argv) > 3 else 900.0
+    only = int(sys.argv[4]) if len(sys.argv) > 4 else None  # replay one case with details
+    rng = np.random.default_rng(seed)
+    t0 = time.time()
+    good = bad = 0
+    for k in range(n):
+        if time.time() - t0 > budget:
+            break
+        p = gen(rng)
+        if only is not None and k != only:
+            continue
+        try:
+            if only is not None:
+                for fz in (p["fused"], 3, 2, 0):
+                    print("fused=%d" % fz, run(p, fz, True))
+            ok, desc = run(p)
+        except Exception as e:  # noqa: BLE001 -- e.g. blocks thinner than the ghost width: rejected at setup
+            print("%4d SKIP %s: %s" % (k, type(e).__name__, e), flush=True)
+            continue
+        good += ok
+        bad += not ok
+        print("%4d %s %s" % (k, "OK  " if ok else "DIFF", desc), flush=True)
+    print("summary: %d cases, %d bitwise equal, %d differ, %.0f s, seed %d" % (good + bad, good, bad,
+                                                                             time.time() - t0, seed))
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -780,3 +780,28 @@ def test_bench_cli_checksums_match_the_reference_bench(tmp_path):
     assert list(out["mine"][0].keys()) == list(out["ref"][0].keys())
     key = ("workers", "mode", "nx", "ny", "nz", "steps", "checksum")
     assert [[r[k] for k in key] for r in out["mine"]] == [[r[k] for k in key] for r in out["ref"]]
+
+
+@pytest.mark.parametrize("workers,ghost", [(2, 2), (3, 2), (2, 3)])
+def test_periodic_axis_split_over_components_matches_the_reference(ref_available, workers, ghost):
+    # a periodic axis decomposed over grid components wraps through processor
+    # faces (both y neighbours of a component are the other one at 2 workers);
+    # odd extents make the wrapped parity differ from the unwrapped one
+    # (regression: scripts/probes/parity_stress.py seed 2026 case 278)
+    rng = np.random.default_rng(278)
+    ext = (39, 43, 13)
+    c = Case(extents=ext, periodic=(False, True, False), tolerance=1e-5, max_sweeps=39, viscosity=0.02,
+             lid_speed=0.0, workers=workers, ghost=ghost, symmetry_z=False)
+    fields = {f: rng.uniform(-0.5, 0.5, size=ext[::-1]) for f in ("vx", "vy", "vz")}
+    o = Oracle(c, "ref")
+    d = dev_from_case(c, fused=1)
+    for x in (o, d):
+        x.init_cavity()
+        for f, a in fields.items():
+            x.scatter(f, a)
+        x.invalidate_all_ghosts()
+    so = o.advance(2)
+    dd = [d.step() for _ in range(2)]
+    assert [[x.dt, x.sweeps, x.residual] for x in dd] == [[float(a), int(b), float(r)] for a, b, r in zip(*so)]
+    for f in FIELDS5:
+        assert same(d.gather(f), o.gather(f)), f
