@@ -5,7 +5,10 @@ cavities (extents, periodicity, ghost width, grid components, random initial
 velocities, tolerance- and cap-driven stops). Test infrastructure: uses
 oracle/ (the checker). Prints one line per case and a summary.
 
-  python scripts/probes/parity_stress.py [n_cases] [seed] [max_seconds]
+  python scripts/probes/parity_stress.py [n_cases] [seed] [max_seconds] [case_index | bc]
+
+"bc": random face conditions (moving walls, symmetry, outflow), the fused
+paths against the unfused dataflow.
 """
 import sys
 import time
@@ -82,17 +85,61 @@ def run(p, fused=None, detail=False):
     return ok, desc
 
 
+def run_bc(rng):
+    """Random face conditions (moving walls, symmetry, outflow) on random
+    velocities: the fused, TMA and temporal paths against the unfused
+    reference dataflow (fused=0, itself bitwise with the reference), since the
+    reference's simulation fixes its own boundary spec."""
+    ext = tuple(int(rng.integers(6, 44)) for _ in range(3))
+    workers = int(rng.choice([1, 1, 2, 3]))
+    ghost = int(rng.choice([1, 2]))
+    kinds = ["wall", "symmetry", "outflow"]
+    faces = [(a, sd, kinds[int(rng.integers(0, 3))], tuple(rng.uniform(-0.3, 0.3, 3))) for a in range(3)
+             for sd in range(2)]
+    tol = float(rng.choice([1e-3, 1e-4, 1e-30]))
+    maxs = int(rng.integers(1, 40))
+    vel = {f: rng.uniform(-0.5, 0.5, size=ext[::-1]) for f in ("vx", "vy", "vz")}
+    out = {}
+    for fused in (0, 1, 3, 2):
+        cfg = sfb.SolverConfig(extents=ext, tolerance=tol, max_sweeps=maxs, symmetry_z=False)
+        d = sfb.Simulation(cfg, sfb.FluidParams(viscosity=0.02, lid_speed=0.0), workers=workers, ghost=ghost,
+                           fused=fused)
+        d.init_cavity()
+        for a, sd, k, v in faces:
+            d.set_face_bc(a, sd, k, v)
+        for f, arr in vel.items():
+            d.scatter(f, arr)
+        st = [d.step() for _ in range(2)]
+        out[fused] = ([[x.dt, x.sweeps, x.residual] for x in st], d.checksum(), d.pending_color)
+        d.close()
+    ok = out[1] == out[0] and out[3] == out[0] and out[2] == out[0]
+    desc = "bc ext=%s w=%d g=%d faces=%s tol=%g maxs=%d sweeps=%s" % (
+        ext, workers, ghost, "".join(k[0] for _, _, k, _ in faces), tol, maxs, [r[1] for r in out[0][0]])
+    return ok, desc
+
+
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 2026
     budget = float(sys.argv[3]) if len(sys.argv) > 3 else 900.0
-    only = int(sys.argv[4]) if len(sys.argv) > 4 else None  # replay one case with details
+    only = int(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4] != "bc" else None  # replay one case
+    mode = "bc" if "bc" in sys.argv[4:] else "ref"
     rng = np.random.default_rng(seed)
     t0 = time.time()
     good = bad = 0
     for k in range(n):
         if time.time() - t0 > budget:
             break
+        if mode == "bc":
+            try:
+                ok, desc = run_bc(rng)
+            except Exception as e:  # noqa: BLE001
+                print("%4d SKIP %s: %s" % (k, type(e).__name__, e), flush=True)
+                continue
+            good += ok
+            bad += not ok
+            print("%4d %s %s" % (k, "OK  " if ok else "DIFF", desc), flush=True)
+            continue
         p = gen(rng)
         if only is not None and k != only:
             continue
