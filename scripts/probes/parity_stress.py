@@ -10,6 +10,7 @@ oracle/ (the checker). Prints one line per case and a summary.
 "bc": random face conditions (moving walls, symmetry, outflow), the fused
 paths against the unfused dataflow.
 """
+import os
 import sys
 import time
 
@@ -30,7 +31,8 @@ def gen(rng):
     workers = int(rng.choice([1, 1, 1, 2, 3, 4]))
     ghost = int(rng.choice([1, 1, 2, 3]))
     lo = 2 * ghost + 2
-    ext = tuple(int(rng.integers(max(lo, 5), 48)) for _ in range(2)) + (int(rng.integers(max(lo, 3), 40)),)
+    top = int(os.environ.get("PS_MAXEXT", "48"))  # larger grids reach the interior/boundary split of the pass
+    ext = tuple(int(rng.integers(max(lo, 5), top)) for _ in range(2)) + (int(rng.integers(max(lo, 3), max(top * 5 // 6, 4))),)
     fused = int(rng.choice([1, 1, 3, 2, 0]))
     tol = float(rng.choice([1e-2, 1e-3, 1e-5, 1e-30]))
     maxs = int(rng.integers(1, 80))
