@@ -2317,15 +2317,12 @@ class simulation {
   // fused = 1 when every face of every local grid component is a wall, a
   // symmetry plane or a processor face, and the ghost shell is 2 deep where
   // there are processor faces (the pass reads 2-deep halos of the old state).
-  // A periodic axis split over grid components wraps through processor faces;
-  // the pass's ghost-cell rules index cells by their unwrapped global
-  // coordinate, so periodic configurations keep the single half-sweeps
-  // (found by scripts/probes/parity_stress.py: 39x43x13, periodic y, two
-  // components, ghost 2).
+  // A periodic axis split over grid components wraps through processor faces:
+  // the pass gives ghost cells across the wrap their wrapped parity
+  // (sf_sweep2.cu; scripts/probes/parity_stress.py found the unwrapped
+  // version wrong on 39x43x13, periodic y, two components, ghost 2).
   bool temporal() const {
     if (!maps2_ || !temporal_env_ || opt_.fused != 1) return false;
-    for (int a = 0; a < 3; ++a)
-      if (cfg_.periodic[a]) return false;
     bool proc = false;
     for (int b = 0; b < nloc_; ++b)
       for (int fi = 0; fi < 6; ++fi) {

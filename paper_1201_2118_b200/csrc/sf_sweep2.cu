@@ -148,6 +148,11 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   // (another block's, valid in the ghost shell, g >= 2) are computed like
   // owned ones; cells outside the domain are physical ghosts
   const int N0 = (int)s.N[0], N1 = (int)s.N[1], N2 = (int)s.N[2];
+  // periodic axes (split over components: processor faces through the
+  // wrap): cells beyond the domain are the wrapped cells, with the wrapped
+  // parity, owned, never pinned
+  const int per0 = s.per[0], per1 = s.per[1], per2 = s.per[2];
+  auto wrp = [](int g, int n, int per) { return per ? ((g % n) + n) % n : g; };
   const int lo0 = (int)B.lo[0], lo1 = (int)B.lo[1], lo2 = (int)B.lo[2];
   const long long sx = B.sx, sxy = B.sx * B.sy;
   const double beta = ctl->beta, dt = ctl->dt;
@@ -241,8 +246,10 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
       f_e[r] = e;
       f_ia[r] = ey * IW + ex;
       f_bt[r] = ((bx << 2) | (by << 1)) | (((bxp << 2) | (by << 1)) << 3) | (((bx << 2) | (byp << 1)) << 6) |
-                ((int)((gi + gj) & 1) << 9) | ((gi >= 0 && gi < N0 && gj >= 0 && gj < N1) << 10) |
-                ((gi == N0 - 1) << 11) | ((gj == N1 - 1) << 12) | ((gi == -1) << 13) | ((gj == -1) << 14);
+                ((int)((wrp((int)gi, N0, per0) + wrp((int)gj, N1, per1)) & 1) << 9) |
+                (((per0 || (gi >= 0 && gi < N0)) && (per1 || (gj >= 0 && gj < N1))) << 10) |
+                ((!per0 && gi == N0 - 1) << 11) | ((!per1 && gj == N1 - 1) << 12) | ((!per0 && gi == -1) << 13) |
+                ((!per1 && gj == -1) << 14);
     }
     {
       const int e = r == 0 ? EN - 1 - tid : (has2d ? NT - tid : EN - 1);
@@ -251,8 +258,8 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
       // the +x / +y ghost (x = n0, y = n1) takes the wall mirror of the last
       // owned cell (exchange.hpp:438-449), evaluated with that cell's operands
       int dx = ex, dy = ey;
-      if (lo0 + x >= N0) dx -= lo0 + x - (N0 - 1);
-      if (lo1 + y >= N1) dy -= lo1 + y - (N1 - 1);
+      if (!per0 && lo0 + x >= N0) dx -= lo0 + x - (N0 - 1);
+      if (!per1 && lo1 + y >= N1) dy -= lo1 + y - (N1 - 1);
       d_e[r] = e;
       d_q[r] = dy * EW + dx;
       if (ex >= 1 && ey >= 1 && (r == 0 || has2d)) d_ok |= 1 << r;
@@ -281,7 +288,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
               Pi = st + IN_P / 8, Dz = stn + IN_D / 8;
     const int u1 = fo + U1 * EN, v1 = fo + V1 * EN, w1 = fo + W1 * EN, p1 = fo + P1 * EN;
     const int gk = lo2 + z;
-    const int zpar = gk & 1;
+    const int zpar = wrp(gk, N2, per2) & 1;
     if (fast_xy && z >= zf_lo && z <= zf_hi) {
 #pragma unroll
       for (int r = 0; r < NE; ++r) {
@@ -328,9 +335,9 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
       }
       return;
     }
-    const bool zin = gk >= 0 && gk < N2;
+    const bool zin = per2 || (gk >= 0 && gk < N2);
     const int bz = s.per[2] | ((gk > 0) & (gk < (int)nm2)), bzp = s.per[2] | (gk + 1 < (int)nm2);
-    const bool pz = lo2 + z == N2 - 1, zlow = lo2 + z == -1;
+    const bool pz = !per2 && lo2 + z == N2 - 1, zlow = !per2 && lo2 + z == -1;
 #pragma unroll
     for (int r = 0; r < NE; ++r) {
       if (r > 0 && !has2f) break;
@@ -361,7 +368,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   // fom (z-1) into divu1 slot d1; the ghost plane above a top wall mirrors
   // plane N2-1 (dm).
   auto s1_div = [&](int z, int fo, int fom, int d1, int dm) {
-    if (lo2 + z >= N2) {
+    if (!per2 && lo2 + z >= N2) {
 #pragma unroll
       for (int r = 0; r < NE; ++r) {
         if (r > 0 && !has2d) break;
@@ -399,14 +406,17 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   const int ixm = (bxm << 2) | (by << 1), ixpm = (bxpm << 2) | (by << 1);
   const int iym = (bx << 2) | (bym << 1), iypm = (bx << 2) | (bypm << 1);
   const int par_col = (gi + gj) & 1;
-  const int N2m1 = N2 - 1, nm2i = (int)nm2, per2 = s.per[2];
+  const int N2m1 = per2 ? -1 : N2 - 1, nm2i = (int)nm2;  // no pinned top plane on a periodic z
   // Boundary tiles on interior planes (bz = bzp = 1): this cell's scale
   // factors and wall flags are per-thread constants, so sweep B runs the fast
   // path's operations with them instead of the general path's lookups and
   // branches (bitwise the same values).
   const double sc_ = smb[ic | 1], sex_ = smb[iex | 1], sey_ = smb[iey | 1];
   const double sxm_ = smb[ixm | 1], sxpm_ = smb[ixpm | 1], sym_ = smb[iym | 1], sypm_ = smb[iypm | 1];
-  const bool xlo = gi == 0, ylo = gj == 0, xhi = gi == N0 - 1, yhi = gj == N1 - 1;
+  const bool xlo = !per0 && gi == 0, ylo = !per1 && gj == 0, xhi = !per0 && gi == N0 - 1, yhi = !per1 && gj == N1 - 1;
+  // -x / -y neighbour parities (the complement of this cell's, except across
+  // an odd periodic wrap)
+  const bool xm_same = per0 && gi == 0 && (N0 & 1), ym_same = per1 && gj == 0 && (N1 & 1);
   const int q0 = (ty + 2) * EW + (tx + 2);
 
   double* __restrict__ Dn = tab->ptr[b][SF_DIVU][ALT];
@@ -442,10 +452,10 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
     if (u == 1 && act) {
       // swept w2 of the plane below the chunk: sweep B's -z neighbour at k0
       const double w1_below = S[F(1) + W1 * EN + q0];
-      if (lo2 + k0 > 0) {
+      if (lo2 + k0 > 0 || per2) {
         const long long gkm = B.lo[2] + k0 - 1;
         const int bzm = bin(s.per[2], gkm, nm2), bzpm = bnx(s.per[2], gkm, nm2);
-        const double a0m = (((gi + gj + gkm) & 1) == colB) ? 1.0 : 0.0, a1m = 1.0 - a0m;
+        const double a0m = (((gi + gj + wrp((int)gkm, N2, per2)) & 1) == colB) ? 1.0 : 0.0, a1m = 1.0 - a0m;
         const double d0m = smb[ic | bzm] * S[Dr(1) + q0] * a0m;
         const double ezm = smb[ic | bzpm] * S[Dr(2) + q0] * a1m;
         wm2 = w1_below + cw * (d0m - ezm);
@@ -492,7 +502,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         r1 = b1 > r1 ? b1 : r1;
         r2 = b2 > r2 ? b2 : r2;
         wm2 = wn;
-      } else if (act && z >= zf_lo && z <= zf_hi) {
+      } else if (act && z >= zf_lo && z <= zf_hi && !(per0 | per1)) {
         // boundary tile, interior plane: the general path's arithmetic with
         // per-thread scales, selects for the wall cases (see sc_ above)
         const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
@@ -554,21 +564,21 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         double un = u1[q0] + cu * (d0 - exv);
         double vn = v1[q0] + cv * (d0 - eyv);
         double wn = w1[q0] + cw * (d0 - ezv);
-        if (gi == N0 - 1) un = pin_u;
-        if (gj == N1 - 1) vn = pin_v;
+        if (xhi) un = pin_u;
+        if (yhi) vn = pin_v;
         if (gk == N2m1) wn = pin_w;
         // swept -x / -y neighbours; at the low wall the pinned ghost (in S1)
         double umn, vmn;
-        if (gi > 0) {
-          const double a0m = a1, a1m = 1.0 - a0m;
+        if (gi > 0 || per0) {
+          const double a0m = xm_same ? a0 : a1, a1m = 1.0 - a0m;
           const double d0m = smb[ixm | bz] * dXm * a0m;
           const double exm = smb[ixpm | bz] * dC * a1m;
           umn = u1[q0 - 1] + cu * (d0m - exm);
         } else {
           umn = u1[q0 - 1];
         }
-        if (gj > 0) {
-          const double a0m = a1, a1m = 1.0 - a0m;
+        if (gj > 0 || per1) {
+          const double a0m = ym_same ? a0 : a1, a1m = 1.0 - a0m;
           const double d0m = smb[iym | bz] * dYm * a0m;
           const double eym = smb[iypm | bz] * dC * a1m;
           vmn = v1[q0 - EW] + cv * (d0m - eym);
@@ -584,20 +594,20 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         Wn[o] = wn;
         Dn[o] = dd;
         // ghosts the next pass reads: pinned low-face velocities, mirrored divu
-        if (gi == 0) {
+        if (xlo) {
           Un[o - 1] = umn;
           Dn[o - 1] = dd;
         }
-        if (gj == 0) {
+        if (ylo) {
           Vn[o - sx] = vmn;
           Dn[o - sx] = dd;
         }
-        if (gk == 0) {
+        if (!per2 && gk == 0) {
           Wn[o - sxy] = wm2;
           Dn[o - sxy] = dd;
         }
-        if (gi == N0 - 1) Dn[o + 1] = dd;
-        if (gj == N1 - 1) Dn[o + sx] = dd;
+        if (xhi) Dn[o + 1] = dd;
+        if (yhi) Dn[o + sx] = dd;
         if (gk == N2m1) Dn[o + sxy] = dd;
         const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
         r1 = b1 > r1 ? b1 : r1;

@@ -782,15 +782,20 @@ def test_bench_cli_checksums_match_the_reference_bench(tmp_path):
     assert [[r[k] for k in key] for r in out["mine"]] == [[r[k] for k in key] for r in out["ref"]]
 
 
-@pytest.mark.parametrize("workers,ghost", [(2, 2), (3, 2), (2, 3)])
-def test_periodic_axis_split_over_components_matches_the_reference(ref_available, workers, ghost):
+@pytest.mark.parametrize("ext,workers,ghost,per", [((39, 43, 13), 2, 2, (False, True, False)),
+                                                   ((39, 43, 13), 3, 2, (False, True, False)),
+                                                   ((39, 43, 13), 2, 3, (False, True, False)),
+                                                   ((39, 43, 13), 8, 2, (True, True, False)),
+                                                   ((39, 43, 13), 4, 2, (True, False, False)),
+                                                   ((75, 77, 73), 8, 2, (True, True, True))])
+def test_periodic_axis_split_over_components_matches_the_reference(ref_available, ext, workers, ghost, per):
     # a periodic axis decomposed over grid components wraps through processor
     # faces (both y neighbours of a component are the other one at 2 workers);
-    # odd extents make the wrapped parity differ from the unwrapped one
-    # (regression: scripts/probes/parity_stress.py seed 2026 case 278)
+    # odd extents make the wrapped parity differ from the unwrapped one. Every
+    # periodic axis here is split, so the temporal pass runs (regression:
+    # scripts/probes/parity_stress.py seed 2026 case 278)
     rng = np.random.default_rng(278)
-    ext = (39, 43, 13)
-    c = Case(extents=ext, periodic=(False, True, False), tolerance=1e-5, max_sweeps=39, viscosity=0.02,
+    c = Case(extents=ext, periodic=per, tolerance=1e-5, max_sweeps=39, viscosity=0.02,
              lid_speed=0.0, workers=workers, ghost=ghost, symmetry_z=False)
     fields = {f: rng.uniform(-0.5, 0.5, size=ext[::-1]) for f in ("vx", "vy", "vz")}
     o = Oracle(c, "ref")
@@ -800,8 +805,10 @@ def test_periodic_axis_split_over_components_matches_the_reference(ref_available
         for f, a in fields.items():
             x.scatter(f, a)
         x.invalidate_all_ghosts()
+    d.set_kernel_timing(True)
     so = o.advance(2)
     dd = [d.step() for _ in range(2)]
     assert [[x.dt, x.sweeps, x.residual] for x in dd] == [[float(a), int(b), float(r)] for a, b, r in zip(*so)]
     for f in FIELDS5:
         assert same(d.gather(f), o.gather(f)), f
+    assert d.kernel_timing("sweep2")[1] > 0, "the temporal pass did not run"
