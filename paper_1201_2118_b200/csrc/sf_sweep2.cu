@@ -116,7 +116,7 @@ void sweep2_box(int field, int* bw, int* bh) {
 // every warp does three cell updates per phase. Rings: S0 planes in q % NIN
 // (NIN >= 3), S1 fields (u1 v1 w1 p1) in m % 4, divu1 in m % 3 -- the slot a
 // phase overwrites was last read before the previous barrier.
-template <int TYV, int NIN, int MINB>
+template <int TYV, int NIN, int MINB, bool PER>
 __global__ void __launch_bounds__(32 * TYV, MINB)
     k_sweep2(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc,
              sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag, unsigned int total_ctas,
@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   // periodic axes (split over components: processor faces through the
   // wrap): cells beyond the domain are the wrapped cells, with the wrapped
   // parity, owned, never pinned
-  const int per0 = s.per[0], per1 = s.per[1], per2 = s.per[2];
+  // (PER = false: no periodic axis; the wrap logic folds away at compile time)
+  const int per0 = PER ? s.per[0] : 0, per1 = PER ? s.per[1] : 0, per2 = PER ? s.per[2] : 0;
   auto wrp = [](int g, int n, int per) { return per ? ((g % n) + n) % n : g; };
   const int lo0 = (int)B.lo[0], lo1 = (int)B.lo[1], lo2 = (int)B.lo[2];
   const long long sx = B.sx, sxy = B.sx * B.sy;
@@ -679,8 +680,10 @@ static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c,
                     sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
                     unsigned total) {
   using G = geom<TYV>;
-  ensure_smem_attr((const void*)k_sweep2<TYV, NIN, MINB>, G::smem_bytes(NIN));
-  k_sweep2<TYV, NIN, MINB><<<nctas, dim3(G::TX, G::TY), G::smem_bytes(NIN), st>>>(
+  const bool per = c.per[0] || c.per[1] || c.per[2];
+  auto k = per ? k_sweep2<TYV, NIN, MINB, true> : k_sweep2<TYV, NIN, MINB, false>;
+  ensure_smem_attr((const void*)k, G::smem_bytes(NIN));
+  k<<<nctas, dim3(G::TX, G::TY), G::smem_bytes(NIN), st>>>(
       vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, total ? total : (unsigned)nctas,
       static_cast<const maps2_t*>(maps), sweep2_prefetch(), fin, pins);
 }
