@@ -236,6 +236,29 @@ class simulation {
     check(sf_sim_checksum(h_.get(), &h));
     return h;
   }
+  // one grid component's owned block as a dense x-fastest host array
+  // (sf_sim_*_block*): synchronous, asynchronous (pinned host memory, valid
+  // until synchronize()), and the staged upload (stage now, install in stream
+  // order before the step that consumes it)
+  void gather_block(const std::string& field, int worker, double* host, int64_t n) {
+    check(sf_sim_gather_block(h_.get(), field.c_str(), worker, host, n));
+  }
+  void scatter_block(const std::string& field, int worker, const double* host, int64_t n) {
+    check(sf_sim_scatter_block(h_.get(), field.c_str(), worker, host, n));
+  }
+  void gather_block_async(const std::string& field, int worker, double* host, int64_t n) {
+    check(sf_sim_gather_block_async(h_.get(), field.c_str(), worker, host, n));
+  }
+  void scatter_block_async(const std::string& field, int worker, const double* host, int64_t n) {
+    check(sf_sim_scatter_block_async(h_.get(), field.c_str(), worker, host, n));
+  }
+  void stage_block_async(const std::string& field, int worker, const double* host, int64_t n) {
+    check(sf_sim_stage_block_async(h_.get(), field.c_str(), worker, host, n));
+  }
+  void install_staged(const std::string& field, int worker) {
+    check(sf_sim_install_staged(h_.get(), field.c_str(), worker));
+  }
+  void synchronize() { check(sf_sim_synchronize(h_.get())); }
   sf_sim* handle() { return h_.get(); }
 
  private:
