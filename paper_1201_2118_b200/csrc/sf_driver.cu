@@ -291,6 +291,7 @@ class simulation {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t k = nullptr;
     int tx = 32, ty = 8, zc = 16;
+    int rpt = 1;  // rows per thread (TMA template): the CTA tile is tx x (ty * rpt) cells
     bool debug = false;
     // TMA-staged template (CACHED readable bindings)
     bool tma = false;
@@ -879,6 +880,19 @@ class simulation {
     uk.tx = std::min(tile[0], 1024);
     uk.ty = std::max(1, std::min(tile[1], 1024 / uk.tx));
     uk.zc = tile[2];
+    // Each thread sweeps SF_JIT_ROWS (1 or 2; default 2) adjacent rows of the
+    // tile with its stores deferred to the end of the pair, so the
+    // shared-memory reads that coincide between the rows fold into one load
+    // (768^3 fp64: radius 2 1.43 -> 1.34 ms, radius 3 1.84 -> 1.64 ms;
+    // DESIGN.md §9).  Needs an even tile height and no INOUT binding (a
+    // deferred INOUT store would be invisible to a later read of the same
+    // cell).  Four rows measured slower (register pressure; the compiler
+    // stops folding loads that far apart).
+    static const int rows_env = getenv("SF_JIT_ROWS") ? atoi(getenv("SF_JIT_ROWS")) : 2;
+    bool inout = false;
+    for (int in : uk.intent) inout = inout || in == 2;
+    const int trows = uk.ty;  // cell rows per CTA tile
+    const int rpt = rows_env == 2 && trows % 2 == 0 && !inout ? 2 : 1;
     // CACHED readable bindings -> TMA plane ring (needs an even TX for the
     // 16-byte aligned box start, boxes <= 256 per dimension, fitting smem)
     std::vector<int> cs;
@@ -891,7 +905,7 @@ class simulation {
     if (!cs.empty() && uk.tx % xa == 0 && !getenv("SF_JIT_NO_TMA")) {
       const int xl = (halo[0] + xa - 1) / xa * xa;
       const int bw = (xl + uk.tx + halo[1] + xa - 1) / xa * xa;
-      const int bh = halo[2] + uk.ty + halo[3];
+      const int bh = halo[2] + trows + halo[3];
       // window + the two planes of a round + look-ahead (SF_JIT_RING_EXTRA planes, default 3)
       static const int ring_extra = getenv("SF_JIT_RING_EXTRA") ? std::max(3, atoi(getenv("SF_JIT_RING_EXTRA"))) : 3;
       const int ring = halo[4] + halo[5] + 1 + ring_extra;
@@ -906,6 +920,8 @@ class simulation {
         uk.bh = bh;
         uk.ring = ring;
         uk.smem = smem;
+        uk.rpt = rpt;
+        uk.ty = trows / rpt;
       }
     }
     compile_user(uk, body);
@@ -919,6 +935,7 @@ class simulation {
     src += "#define SF_NB " + std::to_string(uk.fid.size()) + "\n";
     src += "#define SF_NP " + std::to_string(uk.params.size()) + "\n";
     src += "#define SF_TX " + std::to_string(uk.tx) + "\n#define SF_TY " + std::to_string(uk.ty) + "\n";
+    src += "#define SF_RPT " + std::to_string(uk.rpt) + "\n";
     src += "#define SF_MAXF " + std::to_string(kMaxFields) + "\n#define SF_SLOTS " + std::to_string(kSlots) + "\n";
     std::string fids, wsl;
     for (size_t i = 0; i < uk.fid.size(); ++i) {
@@ -1178,7 +1195,7 @@ class simulation {
     }
     if (reg < 0 || reg > 2) throw error(SF_ERR_ARG, "bad region");
     if (debug_bounds()) check_ghosts(uk, reg);
-    const work_set& ws = items_for(reg, uk.halo, uk.zc, uk.tx, uk.ty);
+    const work_set& ws = items_for(reg, uk.halo, uk.zc, uk.tx, uk.ty * uk.rpt);
     if (ws.nctas > 0) {
       flush_io();
       double* const* ptrs = &dtab_->ptr[0][0][0];

@@ -201,13 +201,16 @@ struct cell_view {
   double* wr;
   long long o, sx, sxy;
   int slot;
-  const double* rb;  // cached: ring base + this cell's in-plane offset
+  const double* rb;  // cached: ring base of this binding (fp32 planes hold floats)
+  int e0;            // cached: this cell's in-plane element (shared index arithmetic lets two rows' loads fold)
   int zoff[SF_ZW];   // cached: ring-plane offset for dk = t - halo_lo_z (updated per plane)
   // cached: this column's values of the z window, plane z in slot z % SF_ZW
   // (a circular register queue: nothing shifts; ph = this plane's slot is a
   // compile-time constant in every unrolled plane body)
   sf_real zq[SF_ZW];
   int ph;
+  mutable sf_real dv;  // SF_RPT > 1: the deferred store of this cell
+  mutable bool dw;
   __device__ __forceinline__ sf_real operator()(int di, int dj, int dk) const {
 #if SF_DEBUG
     if (!SF_READABLE[slot]) { sf_violation(1, slot, di, dj, dk); return 0.0; }
@@ -229,14 +232,22 @@ struct cell_view {
   // ring plane at offset zo (in fp64 slots; an fp32 plane uses the first half),
   // element e of the box relative to this cell
   __device__ __forceinline__ sf_real ring(int zo, int e) const {
-    if (SF_F32[slot]) return (sf_real)reinterpret_cast<const float*>(rb)[2 * zo + e];
-    return (sf_real)rb[zo + e];
+    if (SF_F32[slot]) return (sf_real)reinterpret_cast<const float*>(rb)[2 * zo + e0 + e];
+    return (sf_real)rb[zo + e0 + e];
   }
   __device__ __forceinline__ sf_real load() const { return (*this)(0, 0, 0); }
   __device__ __forceinline__ void store(sf_real v) const {
 #if SF_DEBUG
     if (!SF_WRITABLE[slot]) { sf_violation(4, slot, 0, 0, 0); return; }
 #endif
+#if SF_RPT > 1
+    dv = v;  // written after both rows' bodies (the last store of a body wins)
+    dw = true;
+#else
+    put(v);
+#endif
+  }
+  __device__ __forceinline__ void put(sf_real v) const {
     if (SF_F32[slot])
       reinterpret_cast<float*>(wr)[o] = (float)v;  // fp32 fields round to nearest
     else
@@ -256,6 +267,12 @@ __device__ __forceinline__ void sf_user_point(const point_ctx& c) {
 SF_BODY
 }
 
+// SF_ROWS(stmt): stmt once per row r = 0 .. SF_RPT - 1 of the thread, with r
+// a compile-time constant and crow that row's context (the locals c0 .. c3,
+// picked by name so they stay in registers)
+#define SF_ROW_DO(R, ...) if constexpr ((R) < SF_RPT) { constexpr int r = (R); point_ctx& crow = c##R; (void)r; (void)crow; __VA_ARGS__ }
+#define SF_ROWS(...) SF_ROW_DO(0, __VA_ARGS__) SF_ROW_DO(1, __VA_ARGS__) SF_ROW_DO(2, __VA_ARGS__) SF_ROW_DO(3, __VA_ARGS__)
+
 extern "C" __global__ void __launch_bounds__(SF_TX * SF_TY)
 sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
                const sf_work* __restrict__ items, int nitems, int zc, sf_params prm,
@@ -274,8 +291,8 @@ sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
   const int tiy = (local / w.tiles[0]) % w.tiles[1];
   const int tiz = local / (w.tiles[0] * w.tiles[1]);
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * SF_TX + tx;
-  const long long i0 = w.lo[0] + (long long)tix * SF_TX, j0 = w.lo[1] + (long long)tiy * SF_TY;
-  const long long i = i0 + tx, j = j0 + ty;
+  const long long i0 = w.lo[0] + (long long)tix * SF_TX, j0 = w.lo[1] + (long long)tiy * (SF_TY * SF_RPT);
+  const long long i = i0 + tx, j = j0 + SF_RPT * ty;  // rows j .. j + SF_RPT - 1
   const long long k0 = w.lo[2] + (long long)tiz * zc;
   const long long k1 = k0 + zc < w.hi[2] ? k0 + zc : w.hi[2];
   const int nplanes = (int)(k1 - k0);
@@ -316,23 +333,24 @@ sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
     for (int q = 0; q < SF_R && q < nload; ++q) issue(q);
 
   const bool act = i < w.hi[0] && j < w.hi[1];
-  point_ctx c;
-  c.p_ = prm.v;
+  point_ctx c0, c1, c2, c3;  // rows j .. j + SF_RPT - 1 of this thread (SF_ROWS)
+  const long long jleft = w.hi[1] - j;  // row r is active when act && r < jleft
+  SF_ROWS({
+    point_ctx& c = crow;
+    c.p_ = prm.v;
 #pragma unroll
-  for (int s = 0; s < SF_NB; ++s) {
-    c.f_[s].rd = ptrs[(w.blk * SF_MAXF + SF_FID[s]) * SF_SLOTS + 0];
-    c.f_[s].wr = ptrs[(w.blk * SF_MAXF + SF_FID[s]) * SF_SLOTS + SF_WSLOT[s]];
-    c.f_[s].sx = sx;
-    c.f_[s].sxy = sxy;
-    c.f_[s].slot = s;
-    {  // ring base of this binding + this cell's in-plane element (fp32 planes hold floats)
-      const double* base = sring + SF_CIDX[s] * SF_R * SF_PLANE;
-      const int e = (ty + SF_HALO[2]) * SF_BW + tx + SF_XL;
-      c.f_[s].rb = SF_F32[s] ? reinterpret_cast<const double*>(reinterpret_cast<const float*>(base) + e) : base + e;
+    for (int s = 0; s < SF_NB; ++s) {
+      c.f_[s].rd = ptrs[(w.blk * SF_MAXF + SF_FID[s]) * SF_SLOTS + 0];
+      c.f_[s].wr = ptrs[(w.blk * SF_MAXF + SF_FID[s]) * SF_SLOTS + SF_WSLOT[s]];
+      c.f_[s].sx = sx;
+      c.f_[s].sxy = sxy;
+      c.f_[s].slot = s;
+      c.f_[s].rb = sring + SF_CIDX[s] * SF_R * SF_PLANE;  // ring base of this binding
+      c.f_[s].e0 = ((int)(j - j0) + r + SF_HALO[2]) * SF_BW + tx + SF_XL;  // this cell's in-plane element
     }
-  }
-  c.i = G.lo[0] + i;
-  c.j = G.lo[1] + j;
+    c.i = G.lo[0] + i;
+    c.j = G.lo[1] + j + r;
+  })
   for (int q = 0; q < SF_HALO[4] + SF_HALO[5] && q < nload; ++q) wait(q);
   long long o = G.base + (k0 * G.sy + j) * sx + i;
   int zr[SF_ZW];  // rolling ring-plane offsets of the z window
@@ -349,24 +367,40 @@ sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
       // plane kq's body with its queue slot PH = kq % SF_ZW known at compile time
       auto plane = [&](auto phc, int kq) {
         constexpr int PH = decltype(phc)::value;
+        auto setup = [&](point_ctx& cc, long long oc) {
 #pragma unroll
-        for (int s = 0; s < SF_NB; ++s) {
-          c.f_[s].o = o;
-          c.f_[s].ph = PH;
+          for (int s = 0; s < SF_NB; ++s) {
+            cc.f_[s].o = oc;
+            cc.f_[s].ph = PH;
+            cc.f_[s].dw = false;
 #pragma unroll
-          for (int t = 0; t < SF_ZW; ++t) c.f_[s].zoff[t] = zr[t];
-          if (SF_CACHED[s]) {  // column queue: load the plane that entered the window
-            if (kq == 0) {
+            for (int t = 0; t < SF_ZW; ++t) cc.f_[s].zoff[t] = zr[t];
+            if (SF_CACHED[s]) {  // column queue: load the plane that entered the window
+              if (kq == 0) {
 #pragma unroll
-              for (int t = 0; t < SF_ZW; ++t)
-                c.f_[s].zq[(PH + t - SF_HALO[4] + SF_ZW) % SF_ZW] = c.f_[s].ring(zr[t], 0);
-            } else {
-              c.f_[s].zq[(PH + SF_HALO[5]) % SF_ZW] = c.f_[s].ring(zr[SF_ZW - 1], 0);
+                for (int t = 0; t < SF_ZW; ++t)
+                  cc.f_[s].zq[(PH + t - SF_HALO[4] + SF_ZW) % SF_ZW] = cc.f_[s].ring(zr[t], 0);
+              } else {
+                cc.f_[s].zq[(PH + SF_HALO[5]) % SF_ZW] = cc.f_[s].ring(zr[SF_ZW - 1], 0);
+              }
             }
           }
-        }
-        c.k = G.lo[2] + k0 + kq;
-        sf_user_point(c);
+          cc.k = G.lo[2] + k0 + kq;
+        };
+        SF_ROWS(setup(crow, o + r * sx);)
+#if SF_RPT > 1
+        SF_ROWS(if (r < jleft) sf_user_point(crow);)
+        SF_ROWS({  // the rows' deferred stores
+          const point_ctx& c = crow;
+          if (r < jleft) {
+#pragma unroll
+            for (int s = 0; s < SF_NB; ++s)
+              if (SF_WRITABLE[s] && c.f_[s].dw) c.f_[s].put(c.f_[s].dv);
+          }
+        })
+#else
+        sf_user_point(c0);
+#endif
         o += sxy;
 #pragma unroll
         for (int t = 0; t < SF_ZW - 1; ++t) zr[t] = zr[t + 1];
