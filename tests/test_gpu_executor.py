@@ -121,6 +121,35 @@ def test_tiling_and_worker_count_are_transparent_bitwise(tile, workers):
     assert same(s.gather("dst"), want)
 
 
+@pytest.mark.parametrize("shape,workers,tile", [((13, 11, 9), 1, (32, 8, 4)), ((17, 15, 7), 2, (16, 6, 5)),
+                                                ((9, 7, 13), 4, (8, 2, 3)), ((40, 9, 6), 1, (32, 16, 64))])
+def test_two_rows_per_thread_on_ragged_tiles_bitwise(shape, workers, tile):
+    """The TMA template sweeps two adjacent rows per thread with the stores
+    deferred to the end of the pair (sf_jit.hpp SF_RPT, the default for an even
+    tile height).  Odd block heights leave a lone last row, a body that stores
+    twice keeps the last value (executor.hpp:173-184 store semantics), and a
+    second output and an uncached input are written/read per row."""
+    data = random_global(shape, 3)
+    extra = random_global(shape, 4)
+    s = rig(shape, workers, 1, (True, True, True))
+    for f in ("src", "dst", "aux", "w"):
+        s.create_field(f)
+    s.scatter("src", data)
+    s.scatter("w", extra)
+    body = SMOOTH_BODY + """
+  c.field(2).store(-1.0);
+  c.field(2).store((c.field(0)(0, 1, 0) - c.field(0)(0, -1, 0)) * c.field(3)(0, 1, 0));
+"""
+    s.register_kernel(Plan("SMOOTH2", tile, (1,) * 6,
+                           [("src", "IN", True), ("dst", "OUT"), ("aux", "OUT"), ("w", "IN")]),
+                      (["src", "dst", "aux", "w"], []), body)
+    s.exchange(["src", "w"])
+    s.run_kernel("SMOOTH2")
+    r = lambda a, dj: np.roll(a, shift=-dj, axis=1)  # noqa: E731
+    assert same(s.gather("dst"), smooth_np(data))
+    assert same(s.gather("aux"), (r(data, 1) - r(data, -1)) * r(extra, 1))
+
+
 @pytest.mark.parametrize("tile", [(2, 2, 2), (8, 8, 8), (3, 1, 5)])
 def test_separate_inout_reads_the_pre_kernel_state(tile):
     s = rig((8, 4, 4), 2, 1, (True, False, False), bc="outflow")
