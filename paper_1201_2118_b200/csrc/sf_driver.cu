@@ -907,7 +907,7 @@ class simulation {
       const int bw = (xl + uk.tx + halo[1] + xa - 1) / xa * xa;
       const int bh = halo[2] + trows + halo[3];
       // window + the two planes of a round + look-ahead (SF_JIT_RING_EXTRA planes, default 3)
-      static const int ring_extra = getenv("SF_JIT_RING_EXTRA") ? std::max(3, atoi(getenv("SF_JIT_RING_EXTRA"))) : 3;
+      static const int ring_extra = getenv("SF_JIT_RING_EXTRA") ? std::max(2, atoi(getenv("SF_JIT_RING_EXTRA"))) : 3;
       const int ring = halo[4] + halo[5] + 1 + ring_extra;
       const size_t smem = (size_t)cs.size() * ring * ((bw * bh + 15) / 16 * 16) * 8;
       bool fits = true;  // a box larger than the padded array is pointless (and rejected)
