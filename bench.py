@@ -63,7 +63,7 @@ def parse_args():
                          "high-order Laplacian (radius 2 or 3) JIT-compiled from its point function")
     ap.add_argument("--radius", type=int, default=2)
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"], help="field storage for --workload stencil")
-    ap.add_argument("--tile", default="32,8,64", help="descriptor TILE for --workload stencil")
+    ap.add_argument("--tile", default="32,16,64", help="descriptor TILE for --workload stencil")
     return ap.parse_args()
 
 
