@@ -936,6 +936,12 @@ class simulation {
     src += "#define SF_NP " + std::to_string(uk.params.size()) + "\n";
     src += "#define SF_TX " + std::to_string(uk.tx) + "\n#define SF_TY " + std::to_string(uk.ty) + "\n";
     src += "#define SF_RPT " + std::to_string(uk.rpt) + "\n";
+    // SF_JIT_MINB: resident CTAs per SM the TMA template is compiled for
+    // (__launch_bounds__ second argument, caps registers); unset = no minimum.
+    // Measured per radius in DESIGN.md §10 (no single value wins).
+    static const int minb = getenv("SF_JIT_MINB") ? std::max(1, atoi(getenv("SF_JIT_MINB"))) : 0;
+    src += "#define SF_LAUNCH_BOUNDS __launch_bounds__(SF_TX * SF_TY" +
+           (minb ? ", " + std::to_string(minb) : std::string()) + ")\n";
     src += "#define SF_MAXF " + std::to_string(kMaxFields) + "\n#define SF_SLOTS " + std::to_string(kSlots) + "\n";
     std::string fids, wsl;
     for (size_t i = 0; i < uk.fid.size(); ++i) {

@@ -273,7 +273,7 @@ SF_BODY
 #define SF_ROW_DO(R, ...) if constexpr ((R) < SF_RPT) { constexpr int r = (R); point_ctx& crow = c##R; (void)r; (void)crow; __VA_ARGS__ }
 #define SF_ROWS(...) SF_ROW_DO(0, __VA_ARGS__) SF_ROW_DO(1, __VA_ARGS__) SF_ROW_DO(2, __VA_ARGS__) SF_ROW_DO(3, __VA_ARGS__)
 
-extern "C" __global__ void __launch_bounds__(SF_TX * SF_TY)
+extern "C" __global__ void SF_LAUNCH_BOUNDS
 sf_user_kernel(double* const* __restrict__ ptrs, const sf_geo* __restrict__ geo,
                const sf_work* __restrict__ items, int nitems, int zc, sf_params prm,
                const unsigned char* __restrict__ bidx, const sf_tmap* __restrict__ maps) {
