@@ -58,10 +58,16 @@ def parse_args():
                     help="take the multi-rank (NCCL) path even at one rank (a check of that path on one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--ref-budget", type=float, default=1200.0,
+                    help="--impl reference: wall seconds of timed reference steps (at least one step runs)")
     ap.add_argument("--workload", default="cavity", choices=["cavity", "stencil"],
                     help="cavity = configs[1] (headline); stencil = configs[4], a descriptor-declared "
                          "high-order Laplacian (radius 2 or 3) JIT-compiled from its point function")
     ap.add_argument("--radius", type=int, default=2)
+    ap.add_argument("--config", default="c1", choices=["c1", "c0"],
+                    help="c1: BASELINE.json configs[1] fixed-work cavity (default); c0: configs[0], the 64^3 "
+                         "reference oracle run with the default solver config (tolerance 1e-6, up to 500 "
+                         "half-sweeps per step), timed from rest over --steps steps")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"], help="field storage for --workload stencil")
     ap.add_argument("--tile", default="32,16,64", help="descriptor TILE for --workload stencil")
     return ap.parse_args()
@@ -142,9 +148,26 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def cavity_cfg(sfb, n, sweeps):
+def cavity_cfg(sfb, n, sweeps, c0=False):
+    if c0:  # configs[0]: the reference oracle run, cli::run_config defaults (config.hpp:51-94)
+        return sfb.SolverConfig(extents=(n, n, n), reynolds=100.0, symmetry_z=False)
     return sfb.SolverConfig(extents=(n, n, n), reynolds=100.0, sigma=0.5, omega=1.9525,
                             tolerance=1e-30, max_sweeps=sweeps, symmetry_z=False)
+
+
+def golden_checksums(n, sweeps, c0):
+    """FNV checksums (bench.hpp:24-39) the reference produced for this
+    configuration from rest, by step count (tests/golden/golden.json, made by
+    tests/golden/make_golden.py from oracle/_ref)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+            g = json.load(f)
+    except Exception:
+        return {}, None
+    key = "cavity64" if (c0 and n == 64) else ("cavity512_s200" if (n == 512 and sweeps == 200 and not c0) else None)
+    if key is None or key not in g:
+        return {}, None
+    return {int(k): v for k, v in g[key]["checksums"].items()}, key
 
 
 def dist_env():
@@ -155,41 +178,42 @@ def dist_env():
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference compiled in place, bounded sample
 # ---------------------------------------------------------------------------
-def reference_sample(n, sweeps, threads, samples=1, warmup=0, log=None):
-    """Times the reference's own implementation (oracle/_ref/libsfref.so) on a
-    bounded sample of the workload: per sample one compute_dt+provisional
-    (cfd.hpp:264-282) and one half-sweep of pressure_iteration's loop body
-    (refresh(divu), PRESSURE_SWEEP, refresh(v), DIVERGENCE, reduce; cfd.hpp:
-    295-303) through the reference executor.  A full step is projected as
-    t_prov + (sweeps + 1) * t_half (the +1 covers the initial
-    refresh_divergence and the final refresh(p))."""
+def reference_steps(n, sweeps, threads, steps, warmup=0, budget_s=None, log=None, c0=False):
+    """Times the reference's own implementation (oracle/_ref/libsfref.so, the
+    unmodified stencilforge compiled in place) on full steps of the workload:
+    each timed unit is one complete cfd::simulation::step (cfd.hpp:307-316;
+    compute_dt, provisional, the whole pressure loop of `sweeps` half-sweeps,
+    refresh(p)) through the reference executor with `threads` worker threads,
+    as the reference's own bench times sim.advance (bench.hpp:68-80).  Nothing
+    is projected.  `budget_s` caps the timed steps (at least one) so a slow
+    host still ends within the driver's step limit; the steps actually timed
+    are returned."""
     from oracle.oracle import Oracle, available, cavity_case
     kind = "reference" if available("ref") else "port"
     t0 = time.time()
-    o = Oracle(cavity_case(n, symmetry_z=False, omega=1.9525, tolerance=1e-30, max_sweeps=sweeps,
-                           workers=threads if kind == "reference" else 1),
-               "ref" if kind == "reference" else "port")
+    wk = threads if kind == "reference" else 1
+    case = (cavity_case(n, symmetry_z=False, workers=wk) if c0 else
+            cavity_case(n, symmetry_z=False, omega=1.9525, tolerance=1e-30, max_sweeps=sweeps, workers=wk))
+    o = Oracle(case, "ref" if kind == "reference" else "port")
     o.init_cavity()
     setup = time.time() - t0
-    ix2 = float(n * n)
-    per_step = []
-    for q in range(warmup + samples):
-        if kind == "reference":
-            tp, dt = o.time_provisional()
-            beta = 1.9525 / (2.0 * dt * (ix2 + ix2 + ix2))
-            th = o.time_half_sweeps(3, beta) / 3.0
-        else:
-            t1 = time.time()
-            dt = o.compute_dt()
-            o.provisional(dt)
-            tp = time.time() - t1
-            t1 = time.time()
-            o.run_kernel("DIVERGENCE")
-            th = (time.time() - t1) * 3.0  # crude: the port has no per-sweep probe
-        if q >= warmup:
-            per_step.append((tp, th, tp + (sweeps + 1) * th))
+    for q in range(warmup):
+        t1 = time.perf_counter()
+        o.step()
         if log:
-            log(f"reference sample {q}: provisional {tp:.3f}s half-sweep {th:.3f}s")
+            log(f"reference warm-up step {q}: {time.perf_counter() - t1:.2f}s")
+    per_step = []
+    t_start = time.perf_counter()
+    for q in range(steps):
+        t1 = time.perf_counter()
+        _, sw, _ = o.step()
+        per_step.append(time.perf_counter() - t1)
+        if log:
+            log(f"reference step {q}: {per_step[-1]:.2f}s, {sw} half-sweeps")
+        if budget_s and q + 1 < steps:
+            mean = (time.perf_counter() - t_start) / (q + 1)
+            if time.perf_counter() - t_start + mean > budget_s:
+                break
     o.close()
     return kind, per_step, setup
 
@@ -227,6 +251,9 @@ def run_ours(args):
     rank, world, local = dist_env()
     dev = local
     torch.cuda.set_device(dev)
+    c0 = args.config == "c0"
+    if c0:
+        args.n, args.sweeps = (64 if args.n == 512 else args.n), 500
     n, S = args.n, args.sweeps
     fused = {"tma": 1, "tma1": 3, "ldg": 2, "unfused": 0}[args.variant]
     dist = None
@@ -252,7 +279,7 @@ def run_ours(args):
         ghost = 1
         if args.strong:
             n = args.strong
-        cfg = cavity_cfg(sfb, n, S)
+        cfg = cavity_cfg(sfb, n, S, c0)
         sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=1, device=dev, fused=fused)
     if args.strong:  # this rank's block of the fixed global grid
         cells = 1
@@ -276,8 +303,25 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
 
-    for _ in range(args.warmup):
+    # ---- parity: the first steps from rest against the reference's checksums --
+    golden, gkey = golden_checksums(n, S, c0) if (world == 1 and not args.strong) else ({}, None)
+    parity = {"ok": None, "golden": gkey,
+              "note": "no reference checksum for this configuration (multi-rank and strong-scaling grids are "
+                      "pinned by tests/test_gpu_*: grid components, cross-process transport, path equivalence)"}
+    done = 0
+    if golden and not c0:  # warm-up steps 1 and 2 are checked (untimed)
+        got = {}
+        for k in sorted(golden):
+            while done < k:
+                sim.step()
+                done += 1
+            got[k] = sim.checksum()
+        parity = {"ok": all(got[k] == golden[k] for k in golden), "golden": gkey,
+                  "checked": {str(k): {"checksum": got[k], "reference": golden[k]} for k in sorted(golden)}}
+    for _ in range(max(0, args.warmup - done)):
         sim.step()
+    if c0:  # configs[0] is timed from rest: the warm-up ran on the same grid, start over
+        sim.init_cavity()
 
     # ---- device-timed region: K full steps, inputs resident in HBM -------------
     clocks = ClockSampler(dev)
@@ -305,7 +349,13 @@ def run_ours(args):
     ms_per_step = ms_total / args.steps
     value = total_cells * args.steps / (ms_total / 1e3) / 1e6
     sweeps_done = sum(s.sweeps for s in stats)
-    assert sweeps_done == S * args.steps, "fixed-work config must run exactly max_sweeps per step"
+    if c0:
+        if args.steps in golden:  # the timed steps themselves, from rest
+            got = sim.checksum()
+            parity = {"ok": got == golden[args.steps], "golden": gkey,
+                      "checked": {str(args.steps): {"checksum": got, "reference": golden[args.steps]}}}
+    else:
+        assert sweeps_done == S * args.steps, "fixed-work config must run exactly max_sweeps per step"
 
     peak, peak_src = measured_peaks()
     avg_launch_s = (k_ms / k_n) / 1e3 if k_n else None
@@ -381,25 +431,26 @@ def run_ours(args):
                "ms_per_step": round(e_ms / args.steps, 3),
                "path": "per rank and step: sf_sim_install_staged(vx,vy,vz,p) -> sf_sim_stage_block_async(next step's vx,vy,vz,p from pinned host) -> sf_sim_step -> sf_sim_gather_block_async(vx,vy,vz,p to pinned host); uploads cross PCIe during the previous step and are installed by a kernel, downloads are device snapshots drained while the next step computes"}
 
-    # ---- CPU baseline (rank 0, N=1): the reference on this host, bounded sample --
+    # ---- CPU baseline (rank 0, N=1): the reference on this host, one full step --
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         th = cpu_threads(args)
-        kind, per, setup = reference_sample(n, S, th, samples=1)
-        tp, thalf, tstep = per[0]
-        cpu = {"value": round(cells / tstep / 1e6, 4), "unit": UNIT, "cores": th,
+        kind, per, setup = reference_steps(n, S, th, steps=1, c0=c0)
+        cpu = {"value": round(cells / per[0] / 1e6, 4), "unit": UNIT, "cores": th,
                "kind": "reference" if kind == "reference" else "port",
-               "sample": (f"{n}^3 cavity, reference executor with {th} worker threads: one "
-                          f"compute_dt+provisional ({tp:.2f}s) + one pressure half-sweep ({thalf:.2f}s), "
-                          f"projected to a {S}-sweep step = {tstep:.1f}s"),
-               "ms_per_step_projected": round(tstep * 1e3, 1)}
+               "sample": (f"one full step of the same {n}^3 cavity ({S} half-sweeps) from rest through the "
+                          f"reference executor with {th} worker threads, measured: {per[0]:.1f}s"),
+               "ms_per_step": round(per[0] * 1e3, 1)}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
         "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (lid-driven cavity from rest, init_cavity)",
-        "config": {"workload": (f"3D lid-driven cavity {args.strong}^3 fp64 global grid, strong scaling over {world} B200 (BASELINE.json configs[3]), {S} half-sweeps per step"
+        "config": {"workload": (f"configs[0]: 3D lid-driven cavity {n}^3 fp64, ghost 1, the reference oracle run "
+                                f"(default solver config: tolerance 1e-6, up to 500 half-sweeps per step), "
+                                f"{args.steps} steps from rest" if c0 else
+                                f"3D lid-driven cavity {args.strong}^3 fp64 global grid, strong scaling over {world} B200 (BASELINE.json configs[3]), {S} half-sweeps per step"
                                 if args.strong else
                                 f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)"
                                 if world == 1 else
@@ -412,6 +463,7 @@ def run_ours(args):
                             "unfused": "unfused (reference dataflow)"}[args.variant],
                    "l2": "inputs larger than L2: 9 resident fp64 arrays of %.2f GB" % (cells * 8 / 1e9)},
         "half_sweep_rate": round(total_cells * sweeps_done / (ms_total / 1e3) / 1e6, 1),
+        "parity": parity,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -433,22 +485,36 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    c0 = args.config == "c0"
+    if c0:
+        args.n, args.sweeps = (64 if args.n == 512 else args.n), 500
     n, S = args.n, args.sweeps
     cells = n * n * n
     th = cpu_threads(args)
-    kind, per, setup = reference_sample(n, S, th, samples=args.steps, warmup=args.warmup)
-    tsteps = [x[2] for x in per]
+    # full steps, nothing projected; one warm-up step (a CPU has no clocks or
+    # caches to settle beyond first touch, which init_cavity already did) and a
+    # wall budget so K steps of ~35 s each end inside the driver's step limit
+    warm = min(args.warmup, 1)
+    log = (lambda m: print(m, file=sys.stderr, flush=True))
+    kind, tsteps, setup = reference_steps(n, S, th, steps=args.steps, warmup=warm, budget_s=args.ref_budget, log=log,
+                                         c0=c0)
     ms = 1e3 * sum(tsteps) / len(tsteps)
     value = cells * len(tsteps) / sum(tsteps) / 1e6
-    sample = (f"per step: one compute_dt+provisional and one pressure half-sweep of the {n}^3 cavity "
-              f"through the reference executor ({th} worker threads), projected to {S} half-sweeps")
+    sample = (f"{len(tsteps)} full steps (of {args.steps} requested) of the {n}^3 cavity, {S} half-sweeps each, "
+              f"through the reference executor ({th} worker threads), after {warm} warm-up step; each step "
+              f"timed whole (cfd::simulation::step), nothing projected")
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1),
+        "steps": len(tsteps), "warmup": warm, "ms_per_step": round(ms, 1),
         "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (lid-driven cavity from rest, init_cavity)",
-        "config": {"workload": f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)",
-                   "grid": [n, n, n], "ghost": 1, "sweeps_per_step": S, "parallelism": f"{th} CPU worker threads"},
+        "config": {"workload": (f"configs[0]: 3D lid-driven cavity {n}^3 fp64, ghost 1, the reference oracle run "
+                                f"(default solver config: tolerance 1e-6, up to 500 half-sweeps per step)" if c0 else
+                                f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)"),
+                   "grid": [n, n, n], "ghost": 1, "sweeps_per_step": S, "parallelism": f"{th} CPU worker threads",
+                   "build": "oracle/Makefile: g++ -std=c++20 -O3 -march=x86-64-v3 -ffp-contract=off -pthread (the "
+                            "reference CMake uses -march=native; x86-64-v3 so the library built here runs on the "
+                            "bench host)"},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": th,
                          "kind": "reference" if kind == "reference" else "port", "sample": sample},

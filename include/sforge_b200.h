@@ -357,8 +357,13 @@ int sf_launch_pack_box(const sf_layout* l, const double* src, const int64_t lo[3
                        const int64_t dims[3], double* buf, void* stream);
 int sf_launch_unpack_box(const sf_layout* l, double* dst, const int64_t lo[3],
                          const int64_t dims[3], const double* buf, void* stream);
-/* max_abs / max_abs_diff over owned cells into *dev_out (a device double,
- * NaN-sticky, reductions.hpp:39-71); the caller zeroes *dev_out first. */
+/* max_abs / max_abs_diff over owned cells (reductions.hpp:39-71), folded
+ * into *dev_out, a device double the caller initialises (0.0 to start a
+ * reduction; calls on further blocks or fields accumulate into it).  The
+ * kernel combines with an integer atomicMax on the IEEE bit pattern of |x|,
+ * which orders non-negative doubles exactly, so the result is bitwise the
+ * reference's max for any evaluation order; a NaN anywhere wins (its |x|
+ * pattern exceeds +inf's, 0x7ff0000000000000) and reads back as a NaN. */
 int sf_launch_reduce_max(const sf_layout* l, const double* front, const double* back, int op,
                          double* dev_out, void* stream);
 

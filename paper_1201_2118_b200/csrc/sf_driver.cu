@@ -498,6 +498,7 @@ class simulation {
   }
   void gather_to_device(int f, double* dglobal) {
     download_table();
+    flush_io();  // bumps the compute epoch: a later block_io must wait for this launch
     const i64 N[3] = {cfg_.extents[0], cfg_.extents[1], cfg_.extents[2]};
     for (int b = 0; b < nloc_; ++b) {
       const auto& L = lay_[b];
@@ -510,6 +511,7 @@ class simulation {
   }
   void scatter_from_device(int f, const double* dglobal) {
     download_table();
+    flush_io();  // bumps the compute epoch: a later block_io must wait for this launch
     const i64 N[3] = {cfg_.extents[0], cfg_.extents[1], cfg_.extents[2]};
     for (int b = 0; b < nloc_; ++b) {
       const auto& L = lay_[b];
@@ -906,9 +908,9 @@ class simulation {
       const int xl = (halo[0] + xa - 1) / xa * xa;
       const int bw = (xl + uk.tx + halo[1] + xa - 1) / xa * xa;
       const int bh = halo[2] + trows + halo[3];
-      // window + the two planes of a round + look-ahead (SF_JIT_RING_EXTRA planes, default 3)
-      static const int ring_extra = getenv("SF_JIT_RING_EXTRA") ? std::max(2, atoi(getenv("SF_JIT_RING_EXTRA"))) : 3;
-      const int ring = halo[4] + halo[5] + 1 + ring_extra;
+      // window + the two planes of a round + one plane of look-ahead (2 extra
+      // planes measured 20-50 % slower, 4 within noise)
+      const int ring = halo[4] + halo[5] + 1 + 3;
       const size_t smem = (size_t)cs.size() * ring * ((bw * bh + 15) / 16 * 16) * 8;
       bool fits = true;  // a box larger than the padded array is pointless (and rejected)
       for (const auto& L : lay_) fits = fits && bw <= L.sx && bh <= L.sy;
@@ -936,12 +938,9 @@ class simulation {
     src += "#define SF_NP " + std::to_string(uk.params.size()) + "\n";
     src += "#define SF_TX " + std::to_string(uk.tx) + "\n#define SF_TY " + std::to_string(uk.ty) + "\n";
     src += "#define SF_RPT " + std::to_string(uk.rpt) + "\n";
-    // SF_JIT_MINB: resident CTAs per SM the TMA template is compiled for
-    // (__launch_bounds__ second argument, caps registers); unset = no minimum.
-    // Measured per radius in DESIGN.md §10 (no single value wins).
-    static const int minb = getenv("SF_JIT_MINB") ? std::max(1, atoi(getenv("SF_JIT_MINB"))) : 0;
-    src += "#define SF_LAUNCH_BOUNDS __launch_bounds__(SF_TX * SF_TY" +
-           (minb ? ", " + std::to_string(minb) : std::string()) + ")\n";
+    // no minimum of resident CTAs per SM: every explicit minimum measured
+    // slower or equal
+    src += "#define SF_LAUNCH_BOUNDS __launch_bounds__(SF_TX * SF_TY)\n";
     src += "#define SF_MAXF " + std::to_string(kMaxFields) + "\n#define SF_SLOTS " + std::to_string(kSlots) + "\n";
     std::string fids, wsl;
     for (size_t i = 0; i < uk.fid.size(); ++i) {
@@ -3168,13 +3167,8 @@ int sf_launch_bc_face(const sf_layout* l, double* front, int stagger, int axis, 
       }
     }
     t.count = t.dims[0] * t.dims[1] * t.dims[2];
-    cudaStream_t st = as_stream(stream);
-    sfb::sf_task* d = nullptr;
-    SF_CK(cudaMallocAsync((void**)&d, sizeof t, st));
-    SF_CK(cudaMemcpyAsync(d, &t, sizeof t, cudaMemcpyHostToDevice, st));
-    sfb::launch_tasks(v, d, 1, t.count, nullptr, st);
+    sfb::launch_task_one(v, t, as_stream(stream));
     check_last();
-    SF_CK(cudaFreeAsync(d, st));
   });
 }
 

@@ -143,54 +143,89 @@ __device__ __forceinline__ void bc_task(const sf_task& T, const sf_dev_block& B,
   }
 }
 
+// One refresh task. Box copies of rows at least a warp wide go warp per
+// row (one 64-bit div/mod per row, not per element; each warp moves a
+// contiguous run); narrow boxes (the x faces, 1-3 cells wide) go element per
+// thread.
+template <class View, class F>
+__device__ __forceinline__ void for_box_elems(const sf_task& T, F&& body) {
+  const long long nx = T.dims[0], ny = T.dims[1], rows = T.dims[1] * T.dims[2];
+  if (nx >= 32) {
+    const int lane = threadIdx.x & 31;
+    const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long ws = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long r = w0; r < rows; r += ws) {
+      const long long kk = r / ny, jj = r - kk * ny;
+      for (long long ii = lane; ii < nx; ii += 32) body(r * nx + ii, ii, jj, kk);
+    }
+  } else {
+    const long long nxy = nx * ny, stride = (long long)gridDim.x * blockDim.x;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < T.count; e += stride) {
+      const long long kk = e / nxy, rem = e - kk * nxy, jj = rem / nx, ii = rem - jj * nx;
+      body(e, ii, jj, kk);
+    }
+  }
+}
+
 template <class View>
-__global__ void k_tasks(View vw, const sf_task* __restrict__ tasks,
-                        const sf_dev_ctl* pred) {
-  if (pred && pred_done(pred)) return;
-  const sf_task& T = tasks[blockIdx.y];
-  const long long stride = (long long)gridDim.x * blockDim.x;
+__device__ __forceinline__ void run_task(const View& vw, const sf_task& T) {
   const bool f32 = vw.esize(T.field) == 4;
   if (T.type == 2 || T.type == 3) {  // message pack / unpack (exchange.hpp:165-224)
     // fp32 values travel as exact fp64 conversions (message sizes stay fp64)
     const sf_dev_block& Bk = vw.blk(T.dst_blk);
     double* f = vw.ptr(T.dst_blk, T.field, FRONT);
     float* ff = reinterpret_cast<float*>(f);
-    const long long nx = T.dims[0], nxy = T.dims[0] * T.dims[1];
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < T.count; e += stride) {
-      const long long kk = e / nxy, rem = e - kk * nxy, jj = rem / nx, ii = rem - jj * nx;
+    double* buf = T.buf;
+    const bool pack = T.type == 2;
+    for_box_elems<View>(T, [&](long long e, long long ii, long long jj, long long kk) {
       const long long o = off(Bk, T.lo[0] + ii, T.lo[1] + jj, T.lo[2] + kk);
-      if (T.type == 2)
-        T.buf[e] = f32 ? (double)ff[o] : f[o];
+      if (pack)
+        buf[e] = f32 ? (double)ff[o] : f[o];
       else if (f32)
-        ff[o] = (float)T.buf[e];
+        ff[o] = (float)buf[e];
       else
-        f[o] = T.buf[e];
-    }
+        f[o] = buf[e];
+    });
     return;
   }
-  if (T.type == 0) {
+  if (T.type == 0) {  // box copy between blocks of this process
     const sf_dev_block& S = vw.blk(T.src_blk);
     const sf_dev_block& D = vw.blk(T.dst_blk);
     const double* src = vw.ptr(T.src_blk, T.field, FRONT);
     double* dst = vw.ptr(T.dst_blk, T.field, FRONT);
-    const long long nx = T.dims[0], nxy = T.dims[0] * T.dims[1];
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < T.count; e += stride) {
-      const long long kk = e / nxy, rem = e - kk * nxy, jj = rem / nx, ii = rem - jj * nx;
+    for_box_elems<View>(T, [&](long long, long long ii, long long jj, long long kk) {
       const long long od = off(D, T.dlo[0] + ii, T.dlo[1] + jj, T.dlo[2] + kk);
       const long long os = off(S, T.lo[0] + ii, T.lo[1] + jj, T.lo[2] + kk);
       if (f32)
         reinterpret_cast<float*>(dst)[od] = reinterpret_cast<const float*>(src)[os];
       else
         dst[od] = src[os];
-    }
+    });
     return;
   }
+  const long long stride = (long long)gridDim.x * blockDim.x;
   const sf_dev_block& B = vw.blk(T.dst_blk);
   double* f = vw.ptr(T.dst_blk, T.field, FRONT);
   if (f32)
     bc_task<float>(T, B, reinterpret_cast<float*>(f), stride);
   else
     bc_task<double>(T, B, f, stride);
+}
+
+template <class View>
+__global__ void k_tasks(View vw, const sf_task* __restrict__ tasks, const sf_dev_ctl* pred) {
+  if (pred && pred_done(pred)) return;
+  run_task(vw, tasks[blockIdx.y]);
+}
+// a single task passed by value (level-2 sf_launch_bc_face: no device allocation per call)
+template <class View>
+__global__ void k_task_one(View vw, sf_task task) {
+  run_task(vw, task);
+}
+
+// CTAs per task: one thread per element or tangential line, at most 1184 (8 per SM)
+static unsigned task_ctas(const sf_task& t) {
+  return (unsigned)std::max(1ll, std::min((t.count + 255) / 256, 1184ll));
 }
 
 template <class View>
@@ -202,6 +237,9 @@ void launch_tasks(const View& vw, const sf_task* tasks, int ntasks, long long ma
   if (bx < 1) bx = 1;
   dim3 grid((unsigned)bx, (unsigned)ntasks);
   k_tasks<View><<<grid, 256, 0, st>>>(vw, tasks, pred);
+}
+void launch_task_one(const direct_view& vw, const sf_task& t, cudaStream_t st) {
+  k_task_one<direct_view><<<task_ctas(t), 256, 0, st>>>(vw, t);
 }
 template void launch_tasks<table_view>(const table_view&, const sf_task*, int, long long,
                                        const sf_dev_ctl*, cudaStream_t);

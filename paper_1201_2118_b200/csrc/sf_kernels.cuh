@@ -27,6 +27,8 @@ constexpr int kTY = 8;
 template <class View>
 void launch_tasks(const View& vw, const sf_task* tasks, int ntasks, long long max_count,
                   const sf_dev_ctl* pred, cudaStream_t st);
+// one task passed by value (no device task list)
+void launch_task_one(const direct_view& vw, const sf_task& t, cudaStream_t st);
 template <class View>
 void launch_update_velocity(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                             double dt, cudaStream_t st);

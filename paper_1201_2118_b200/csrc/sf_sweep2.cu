@@ -48,12 +48,6 @@ __device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void prefetch3(const CUtensorMap* map, int x, int y, int z) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(x), "r"(y), "r"(z)
-               : "memory");
-}
 __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
@@ -97,9 +91,11 @@ size_t sweep2_maps_bytes() { return sizeof(maps2_t); }
 size_t sweep2_map_offset(int b, int f, int s) {
   return sizeof(CUtensorMap) * (((size_t)b * SF_NFIELDS + f) * kSlots + s);
 }
-static int sweep2_variant();
-// tile height of the selected variant (SF_SWEEP2_VARIANT 2: 32 x 16)
-int sweep2_tile_y() { return sweep2_variant() == 2 ? 16 : 8; }
+// 32 x 8 tiles, 3 S0 stages, 2 CTAs per SM. (Measured alternatives: 32 x 16
+// tiles, 6 stages at 1 CTA/SM, L2 prefetch of later planes -- all slower;
+// DESIGN.md §10.)
+constexpr int kPassTY = 8, kPassStages = 3, kPassMinB = 2;
+int sweep2_tile_y() { return kPassTY; }
 void sweep2_box(int field, int* bw, int* bh) {
   const int ty = sweep2_tile_y();
   *bw = 32 + 4;
@@ -120,7 +116,7 @@ template <int TYV, int NIN, int MINB, bool PER>
 __global__ void __launch_bounds__(32 * TYV, MINB)
     k_sweep2(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc,
              sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag, unsigned int total_ctas,
-             const maps2_t* __restrict__ maps, int pf, int finalize, sweep2_pins pins) {
+             const maps2_t* __restrict__ maps, int finalize, sweep2_pins pins) {
   static_assert(NIN >= 3, "three S0 planes are read or in flight per phase");
   using G = geom<TYV>;
   constexpr int TX = G::TX, TY = G::TY, NT = G::NT, EW = G::EW, EN = G::EN, NE = G::NE, R2 = G::R2;
@@ -196,15 +192,6 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
     tma3(st + IN_V, mV, bar, xs, ys, zs + q);
     tma3(st + IN_W, mW, bar, xs, ys, zs + q);
     tma3(st + IN_P, mP, bar, xs, ys, zs + q);
-    // L2 prefetch pf planes further: more bytes in flight than the stages hold
-    if (pf > 0 && q + pf < nin) {
-      const int zp = zs + q + pf;
-      prefetch3(mD, xs, ys, zp);
-      prefetch3(mU, xs, ys, zp);
-      prefetch3(mV, xs, ys, zp);
-      prefetch3(mW, xs, ys, zp);
-      prefetch3(mP, xs, ys, zp);
-    }
   };
   const uint32_t bar0 = smem32(&bars[0]);
   auto wait_in = [&](int q) {
@@ -665,49 +652,18 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   }
 }
 
-// SF_S2_PF: L2 prefetch distance in planes (default 0 = off: measured no gain)
-static int sweep2_prefetch() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SF_S2_PF");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
-template <int TYV, int NIN, int MINB>
-static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
-                    unsigned total) {
-  using G = geom<TYV>;
-  const bool per = c.per[0] || c.per[1] || c.per[2];
-  auto k = per ? k_sweep2<TYV, NIN, MINB, true> : k_sweep2<TYV, NIN, MINB, false>;
-  ensure_smem_attr((const void*)k, G::smem_bytes(NIN));
-  k<<<nctas, dim3(G::TX, G::TY), G::smem_bytes(NIN), st>>>(
-      vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, total ? total : (unsigned)nctas,
-      static_cast<const maps2_t*>(maps), sweep2_prefetch(), fin, pins);
-}
-
-// SF_SWEEP2_VARIANT: 0 = 32x8 tile, 3 S0 stages, 2 CTAs/SM (default);
-// 1 = 32x8, 6 stages, 1 CTA/SM; 2 = 32x16, 3 stages, 1 CTA/SM
-static int sweep2_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SF_SWEEP2_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
                    unsigned total) {
   if (nctas <= 0) return;
-  switch (sweep2_variant()) {
-    case 1: launch2<8, 6, 1>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total); break;
-    case 2: launch2<16, 3, 1>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total); break;
-    default: launch2<8, 3, 2>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total); break;
-  }
+  constexpr int TYV = kPassTY, NIN = kPassStages, MINB = kPassMinB;
+  using G = geom<TYV>;
+  const bool per = c.per[0] || c.per[1] || c.per[2];
+  auto k = per ? k_sweep2<TYV, NIN, MINB, true> : k_sweep2<TYV, NIN, MINB, false>;
+  ensure_smem_attr((const void*)k, G::smem_bytes(NIN));
+  k<<<nctas, dim3(G::TX, G::TY), G::smem_bytes(NIN), st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
+                                                           total ? total : (unsigned)nctas,
+                                                           static_cast<const maps2_t*>(maps), fin, pins);
 }
 
 }  // namespace sfb

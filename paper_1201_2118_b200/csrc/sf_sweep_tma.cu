@@ -49,20 +49,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// with an L2 cache-policy operand (createpolicy), for read-once streams
-__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
-                                                 int y, int z, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
                                             int y, int z) {
   asm volatile(
@@ -102,15 +88,15 @@ struct sweep_maps {  // per block: [field][physical buffer]
   CUtensorMap m[kMaxBlocks][SF_NFIELDS][kSlots];
 };
 
-// STAGES: ring depth.  MINB: CTAs per SM the register budget targets.  WS:
-// warp-specialised -- a ninth warp produces (TMA) and consumer warps release
-// stages through "empty" mbarriers instead of a per-plane CTA barrier.
-template <int STAGES, int MINB, bool WS, int TX, int TY>
-__global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
+// STAGES: ring depth.  MINB: CTAs per SM the register budget targets.
+// (Measured alternatives -- a warp-specialised TMA producer, 2-8 stages,
+// 64x4 / 128x2 tiles, streaming stores, evict-first loads -- were all slower;
+// DESIGN.md §4.)
+template <int STAGES, int MINB, int TX, int TY>
+__global__ void __launch_bounds__(TX* TY, MINB)
     k_sweep_div_tma(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems,
                     int zc, sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag,
-                    unsigned int total_ctas, const sweep_maps* __restrict__ maps, int finalize,
-                    int hints) {
+                    unsigned int total_ctas, const sweep_maps* __restrict__ maps, int finalize) {
   constexpr int kStages = STAGES;
   using TL = tile<TX, TY>;
   // finalize 2: redo of a temporal pass's first sweep (sf_sweep2.cu), runs
@@ -123,12 +109,10 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto sptr = [&](int st, int off) { return reinterpret_cast<double*>(smem_raw + st * TL::BYTES + off); };
   __shared__ __align__(8) uint64_t bars[kStages];
-  __shared__ __align__(8) uint64_t empty_bars[kStages];
   __shared__ double smb[8];
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * TX + tx;
-  const bool producer_warp = WS && ty == TY;
   // tile location
   const int cta = blockIdx.x;
   const int it = nitems > 1 ? find_item(items, nitems, cta) : 0;
@@ -151,7 +135,6 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
 #pragma unroll
     for (int q = 0; q < kStages; ++q) {
       mbar_init(&bars[q], 1);
-      if (WS) mbar_init(&empty_bars[q], TY);  // one arrive per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -174,33 +157,17 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
   const CUtensorMap* mW = &maps->m[b][SF_VZ][tab->bidx[b][SF_VZ][FRONT]];
   const CUtensorMap* mP = &maps->m[b][SF_P][tab->bidx[b][SF_P][FRONT]];
   const int xc = (int)(xo + i0), yc = (int)(g + j0), zc0 = (int)(g + k0);
-  const uint64_t pol = (hints & 2) ? policy_evict_first() : 0ull;
   auto issue = [&](int stage, int plane) {
     mbar_expect_tx(&bars[stage], TL::TXB);
     tma_load_3d(sptr(stage, TL::OFF_D), mD, &bars[stage], xc - kXL, yc - 1, zc0 + plane);
-    if (hints & 2) {  // p and vz are read by this CTA only: evict first
-      tma_load_3d(sptr(stage, TL::OFF_U), mU, &bars[stage], xc - kXL, yc, zc0 + plane);
-      tma_load_3d(sptr(stage, TL::OFF_V), mV, &bars[stage], xc, yc - 1, zc0 + plane);
-      tma_load_3d_hint(sptr(stage, TL::OFF_P), mP, &bars[stage], xc, yc, zc0 + plane, pol);
-      tma_load_3d_hint(sptr(stage, TL::OFF_W), mW, &bars[stage], xc, yc, zc0 + plane, pol);
-    } else {
-      tma_load_3d(sptr(stage, TL::OFF_U), mU, &bars[stage], xc - kXL, yc, zc0 + plane);
-      tma_load_3d(sptr(stage, TL::OFF_V), mV, &bars[stage], xc, yc - 1, zc0 + plane);
-      tma_load_3d(sptr(stage, TL::OFF_P), mP, &bars[stage], xc, yc, zc0 + plane);
-      tma_load_3d(sptr(stage, TL::OFF_W), mW, &bars[stage], xc, yc, zc0 + plane);
-    }
+    tma_load_3d(sptr(stage, TL::OFF_U), mU, &bars[stage], xc - kXL, yc, zc0 + plane);
+    tma_load_3d(sptr(stage, TL::OFF_V), mV, &bars[stage], xc, yc - 1, zc0 + plane);
+    tma_load_3d(sptr(stage, TL::OFF_P), mP, &bars[stage], xc, yc, zc0 + plane);
+    tma_load_3d(sptr(stage, TL::OFF_W), mW, &bars[stage], xc, yc, zc0 + plane);
   };
-  if (!WS && tid == 0) {
+  if (tid == 0) {
     const int npro = nplanes < kStages ? nplanes : kStages;
     for (int q = 0; q < npro; ++q) issue(q, q);
-  }
-  if (WS && producer_warp) {
-    if (tx == 0)
-      for (int kk = 0; kk < nplanes; ++kk) {
-        const int st = kk % kStages;
-        if (kk >= kStages) mbar_wait(&empty_bars[st], (uint32_t)(((kk / kStages) - 1) & 1));
-        issue(st, kk);
-      }
   }
 
   double* __restrict__ Dn = tab->ptr[b][SF_DIVU][ALT];
@@ -213,7 +180,7 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
   const double cu = dt * s.ix, cv = dt * s.iy, cw = dt * s.iz;
 
   const long long i = i0 + tx, j = j0 + ty;
-  const bool act = !producer_warp && i < wk.hi[0] && j < wk.hi[1];
+  const bool act = i < wk.hi[0] && j < wk.hi[1];
   const long long n0 = B.n[0], n1 = B.n[1], n2 = B.n[2];
   const long long sx = B.sx, sxy = B.sx * B.sy;
   const long long gi = B.lo[0] + i, gj = B.lo[1] + j;
@@ -271,7 +238,7 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
     }
   }
 
-  for (int kk = 0; kk < nplanes && !producer_warp; ++kk, o += sxy) {
+  for (int kk = 0; kk < nplanes; ++kk, o += sxy) {
     const int st = kk % kStages;
     mbar_wait(&bars[st], (uint32_t)((kk / kStages) & 1));
     const bool has_next = kk + 1 < nplanes;
@@ -306,19 +273,11 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
       double dd = (un - umn) * s.ix;
       dd += (vn - vmn) * s.iy;
       dd += (wn - wm_new) * s.iz;
-      if (hints & 1) {  // streaming stores (evict-first): nothing here is re-read this sweep
-        __stcs(P + o, pn);
-        __stcs(Un + o, un);
-        __stcs(Vn + o, vn);
-        __stcs(Wn + o, wn);
-        __stcs(Dn + o, dd);
-      } else {
-        P[o] = pn;
-        Un[o] = un;
-        Vn[o] = vn;
-        Wn[o] = wn;
-        Dn[o] = dd;
-      }
+      P[o] = pn;
+      Un[o] = un;
+      Vn[o] = vn;
+      Wn[o] = wn;
+      Dn[o] = dd;
       const unsigned long long bb = abs_bits(dd);
       rmax = bb > rmax ? bb : rmax;
       wm_new = wn;
@@ -410,13 +369,8 @@ __global__ void __launch_bounds__(TX* TY + (WS ? 32 : 0), MINB)
       rmax = bb > rmax ? bb : rmax;
       wm_new = wn;
     }
-    if (WS) {
-      __syncwarp();
-      if (tx == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty_bars[st])) : "memory");
-    } else {
-      __syncthreads();  // every thread is done with stage st
-      if (tid == 0 && kk + kStages < nplanes) issue(st, kk + kStages);
-    }
+    __syncthreads();  // every thread is done with stage st
+    if (tid == 0 && kk + kStages < nplanes) issue(st, kk + kStages);
   }
 
   if (finalize == 2) {  // counters and residual were set by the temporal pass
@@ -490,15 +444,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static int sweep_variant();
-static int sweep_hints();
-// tile shape of the selected pipeline variant
+constexpr int kSweepTX = 32, kSweepTY = 8, kSweepStages = 4, kSweepMinB = 2;
+// tile shape of the single half-sweep kernel
 void sweep_tile_shape(int* tx, int* ty) {
-  switch (sweep_variant()) {
-    case 9: case 11: *tx = 64; *ty = 4; break;
-    case 10: *tx = 128; *ty = 2; break;
-    default: *tx = 32; *ty = 8; break;
-  }
+  *tx = kSweepTX;
+  *ty = kSweepTY;
 }
 
 // Box shape per field role (see tile<>).
@@ -524,8 +474,7 @@ int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, lo
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, gdim,
                   gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  getenv("SF_L2_PROMO") ? (CUtensorMapL2promotion)atoi(getenv("SF_L2_PROMO"))
-                                        : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : 2;
 }
@@ -551,55 +500,16 @@ size_t sweep_map_offset(int b, int f, int s) {
   return offsetof(sweep_maps, m) + sizeof(CUtensorMap) * ((size_t)(b * SF_NFIELDS + f) * kSlots + s);
 }
 
-template <int STAGES, int MINB, bool WS, int TX = 32, int TY = 8>
-static void launch_variant(const table_view& vw, int nctas, int zc, const sf_consts& c,
-                           sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,
-                           cudaStream_t st) {
-  const size_t smem = (size_t)tile<TX, TY>::BYTES * STAGES;
-  ensure_smem_attr((const void*)k_sweep_div_tma<STAGES, MINB, WS, TX, TY>, (int)smem);
-  k_sweep_div_tma<STAGES, MINB, WS, TX, TY><<<nctas, dim3(TX, TY + (WS ? 1 : 0)), smem, st>>>(
-      vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas,
-      static_cast<const sweep_maps*>(maps), fin, sweep_hints());
-}
-
-// SF_SWEEP_HINTS: bit 0 streaming stores, bit 1 evict-first TMA loads of p / vz
-static int sweep_hints() {
-  static int h = -1;
-  if (h < 0) {
-    const char* e = getenv("SF_SWEEP_HINTS");
-    h = e ? atoi(e) : 0;
-  }
-  return h;
-}
-
-// SF_SWEEP_VARIANT selects the pipeline shape for A/B runs (default 0).
-static int sweep_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SF_SWEEP_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
 void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_consts& c,
                           sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,
                           cudaStream_t st) {
   if (nctas <= 0) return;
-  switch (sweep_variant()) {
-    case 1: launch_variant<3, 3, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-    case 2: launch_variant<4, 2, true>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-    case 3: launch_variant<3, 3, true>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-    case 4: launch_variant<6, 2, true>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-    case 5: launch_variant<2, 4, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-    case 6: launch_variant<6, 2, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-    case 7: launch_variant<8, 2, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-    case 8: launch_variant<6, 1, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-    case 9: launch_variant<4, 2, false, 64, 4>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-    case 10: launch_variant<4, 2, false, 128, 2>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-    case 11: launch_variant<3, 2, false, 64, 4>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-    default: launch_variant<4, 2, false>(vw, nctas, zc, c, ctl, hflag, maps, fin, st); break;
-  }
+  constexpr int S = kSweepStages, M = kSweepMinB, TX = kSweepTX, TY = kSweepTY;
+  const size_t smem = (size_t)tile<TX, TY>::BYTES * S;
+  ensure_smem_attr((const void*)k_sweep_div_tma<S, M, TX, TY>, (int)smem);
+  k_sweep_div_tma<S, M, TX, TY><<<nctas, dim3(TX, TY), smem, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
+                                                                  (unsigned)nctas,
+                                                                  static_cast<const sweep_maps*>(maps), fin);
 }
 
 }  // namespace sfb

@@ -132,6 +132,34 @@ class StepStats:
     residual: float
 
 
+def _host_f64(buf, what: str, pinned: bool = False):
+    """(pointer, element count) of a contiguous float64 host buffer (numpy
+    array or CPU torch tensor); the C side reads or writes 8 bytes per
+    element, so any other dtype or a strided view is rejected."""
+    if hasattr(buf, "data_ptr"):  # torch tensor
+        import torch
+        if buf.is_cuda:
+            raise ValueError(f"{what}: expected a host buffer, got a CUDA tensor")
+        if buf.dtype != torch.float64 or not buf.is_contiguous():
+            raise ValueError(f"{what}: expected a contiguous float64 tensor, got {buf.dtype}"
+                             f"{'' if buf.is_contiguous() else ' (non-contiguous)'}")
+        if pinned and not buf.is_pinned():
+            raise ValueError(f"{what}: an asynchronous transfer needs a pinned tensor")
+        return buf.data_ptr(), buf.numel()
+    if pinned:
+        raise ValueError(f"{what}: an asynchronous transfer needs a pinned tensor")
+    if not isinstance(buf, np.ndarray) or buf.dtype != np.float64 or not buf.flags.c_contiguous:
+        raise ValueError(f"{what}: expected a C-contiguous float64 array")
+    return buf.ctypes.data, buf.size
+
+
+def _device_f64(t, what: str):
+    import torch
+    if t.dtype != torch.float64 or not t.is_contiguous():
+        raise ValueError(f"{what}: expected a contiguous float64 CUDA tensor, got {t.dtype}")
+    return t
+
+
 def _cstrs(names: Iterable[str]):
     ns = [n.encode() for n in names]
     arr = (C.c_char_p * max(1, len(ns)))(*ns)
@@ -172,6 +200,7 @@ class Simulation:
         else:
             L.check(self._lib.sf_sim_create(C.byref(self._ccfg), C.byref(self._cpar), C.byref(opt), C.byref(h)))
         self._h = h
+        self._async_keep = []  # host buffers of queued transfers, held until synchronize()
         self.rank = int(rank or 0)
         self.world = int(world or 1)
         self.extents = tuple(int(x) for x in cfg.extents)
@@ -271,23 +300,35 @@ class Simulation:
 
     def scatter(self, name: str, data) -> None:
         if hasattr(data, "is_cuda") and data.is_cuda:
-            t = data.contiguous()
+            import torch
+            t = data.to(torch.float64).contiguous()
+            cur, ext = self._torch_order()
+            ext.wait_stream(cur)  # the data was produced on torch's stream
             L.check(self._lib.sf_sim_scatter_device(self._h, name.encode(), C.c_void_p(t.data_ptr()), t.numel()))
+            t.record_stream(ext)  # a temporary stays allocated until the copy ran
+            cur.wait_stream(ext)
             return
-        a = np.ascontiguousarray(data, dtype=np.float64).reshape(-1)
-        if hasattr(data, "data_ptr") and hasattr(data, "is_pinned") and data.is_contiguous() and data.dtype.itemsize == 8:
+        if hasattr(data, "data_ptr"):
+            import torch
+            data = data.to(torch.float64).contiguous()
             ptr, n = data.data_ptr(), data.numel()
         else:
-            ptr, n = a.ctypes.data, a.size
+            data = np.ascontiguousarray(data, dtype=np.float64).reshape(-1)
+            ptr, n = data.ctypes.data, data.size
         L.check(self._lib.sf_sim_scatter(self._h, name.encode(), C.c_void_p(ptr), n))
 
     def gather(self, name: str, out=None) -> np.ndarray:
         nx, ny, nz = self.extents
         if out is not None and hasattr(out, "is_cuda") and out.is_cuda:
+            _device_f64(out, "gather(out=)")
+            cur, ext = self._torch_order()
+            ext.wait_stream(cur)  # torch may still use `out`
             L.check(self._lib.sf_sim_gather_device(self._h, name.encode(), C.c_void_p(out.data_ptr()), out.numel()))
+            cur.wait_stream(ext)  # later torch work sees the gathered values
             return out
-        if out is not None and hasattr(out, "data_ptr"):
-            L.check(self._lib.sf_sim_gather(self._h, name.encode(), C.c_void_p(out.data_ptr()), out.numel()))
+        if out is not None:
+            ptr, n = _host_f64(out, "gather(out=)")
+            L.check(self._lib.sf_sim_gather(self._h, name.encode(), C.c_void_p(ptr), n))
             return out
         a = np.empty((nz, ny, nx), dtype=np.float64)
         L.check(self._lib.sf_sim_gather(self._h, name.encode(), C.c_void_p(a.ctypes.data), a.size))
@@ -308,25 +349,24 @@ class Simulation:
                 raise ValueError("an asynchronous gather needs a pinned `out` buffer")
             nx, ny, nz = self.block_shape(w)
             out = np.empty((nz, ny, nx), dtype=np.float64)
-        ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
-        n = out.numel() if hasattr(out, "numel") else out.size
+        ptr, n = _host_f64(out, "gather_block(out=)", pinned=not wait)
         fn = self._lib.sf_sim_gather_block if wait else self._lib.sf_sim_gather_block_async
         L.check(fn(self._h, name.encode(), int(w), C.c_void_p(ptr), n))
+        if not wait:
+            self._async_keep.append(out)
         return out
 
     def scatter_block(self, name: str, data, worker: int | None = None, wait: bool = True):
         """Dense host array -> owned block. ``wait=False`` queues the upload
         (``data`` must be pinned and unchanged until ``synchronize()``)."""
         w = self.rank if worker is None else worker
-        if hasattr(data, "data_ptr"):
-            ptr, n = data.data_ptr(), data.numel()
-        else:
-            if not wait:
-                raise ValueError("an asynchronous scatter needs a pinned tensor")
+        if wait and not hasattr(data, "data_ptr"):
             data = np.ascontiguousarray(data, dtype=np.float64)
-            ptr, n = data.ctypes.data, data.size
+        ptr, n = _host_f64(data, "scatter_block", pinned=not wait)
         fn = self._lib.sf_sim_scatter_block if wait else self._lib.sf_sim_scatter_block_async
         L.check(fn(self._h, name.encode(), int(w), C.c_void_p(ptr), n))
+        if not wait:
+            self._async_keep.append(data)
 
     def stage_block(self, name: str, data, worker: int | None = None):
         """First half of an asynchronous scatter: queue the upload of ``data``
@@ -335,10 +375,9 @@ class Simulation:
         order, so staging step k+1's inputs before ``step()`` overlaps the
         transfer with step k."""
         w = self.rank if worker is None else worker
-        if not hasattr(data, "data_ptr"):
-            raise ValueError("a staged upload needs a pinned tensor")
-        L.check(self._lib.sf_sim_stage_block_async(self._h, name.encode(), int(w), C.c_void_p(data.data_ptr()),
-                                                   data.numel()))
+        ptr, n = _host_f64(data, "stage_block", pinned=True)
+        L.check(self._lib.sf_sim_stage_block_async(self._h, name.encode(), int(w), C.c_void_p(ptr), n))
+        self._async_keep.append(data)
 
     def install_staged(self, name: str, worker: int | None = None):
         w = self.rank if worker is None else worker
@@ -475,6 +514,14 @@ class Simulation:
     # -- device plumbing -----------------------------------------------------
     def synchronize(self):
         L.check(self._lib.sf_sim_synchronize(self._h))
+        self._async_keep.clear()
+
+    def _torch_order(self):
+        """(torch's current stream, the simulation's stream as a torch stream):
+        device-pointer transfers are ordered against torch's work in both
+        directions."""
+        import torch
+        return torch.cuda.current_stream(), torch.cuda.ExternalStream(self.stream)
 
     @property
     def stream(self) -> int:

@@ -87,8 +87,30 @@ def main():
     print(json.dumps({k: v.get("checksums") if isinstance(v, dict) else v for k, v in g.items()}, indent=1))
 
 
+def add_cavity512(steps=1, workers=8):
+    """The headline bench configuration (bench.py: BASELINE.json configs[1]):
+    512^3 cavity, re 100, symmetry_z false, omega 1.9525, tolerance 1e-30,
+    max_sweeps 200, ghost 1 -- checksum and (dt, sweeps, residual) after
+    `steps` steps, from the reference with `workers` threads (results are
+    worker-count invariant, tests/test_cfd.cpp:231-273).  About 6 min per step
+    on 8 cores; merged into the existing JSON."""
+    path = os.path.join(os.path.dirname(__file__), "golden.json")
+    g = json.load(open(path))
+    t0 = time.time()
+    entry = cavity_run(512, list(range(1, steps + 1)), symmetry_z=False, omega=1.9525, tolerance=1e-30,
+                       max_sweeps=200, workers=workers)
+    entry["elapsed_s"] = time.time() - t0
+    entry["workers"] = workers
+    g["cavity512_s200"] = entry
+    with open(path, "w") as f:
+        json.dump(g, f, indent=1)
+    print(json.dumps(entry, indent=1))
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["--taylor-green"]:  # only the acceptance-6 entry, merged into the existing JSON
         add_taylor_green()
+    elif sys.argv[1:2] == ["--cavity512"]:
+        add_cavity512(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
     else:
         main()
