@@ -305,7 +305,10 @@ class Simulation:
             cur, ext = self._torch_order()
             ext.wait_stream(cur)  # the data was produced on torch's stream
             L.check(self._lib.sf_sim_scatter_device(self._h, name.encode(), C.c_void_p(t.data_ptr()), t.numel()))
-            t.record_stream(ext)  # a temporary stays allocated until the copy ran
+            # torch's stream waits for the copy: a temporary from .to()/.contiguous()
+            # goes back to the caching allocator on that stream, so no later torch
+            # work can reuse it before the copy ran (no record_stream on the
+            # library's stream, which may be destroyed before the tensor)
             cur.wait_stream(ext)
             return
         if hasattr(data, "data_ptr"):
