@@ -183,6 +183,37 @@ int sf_nccl_unique_id(void* out128);
 int sf_sim_create_distributed(const sf_solver_config* cfg, const sf_fluid_params* par,
                               const sf_sim_options* opt, int rank, int world, const void* nccl_id,
                               sf_sim** out);
+/* The same decomposition with the CUDA-IPC transport instead of NCCL: every
+ * rank maps its peers' device buffers into its own address space
+ * (cudaIpcGetMemHandle / cudaIpcOpenMemHandle) and moves ghost messages with
+ * device-to-device copies or direct stores; the host callbacks below carry
+ * only the 64-byte handles, residual maxima and barriers.  All ranks call
+ * every function of a simulation in the same order (as with NCCL).  The ranks
+ * may share one device (separate processes; the host orders them, no kernel
+ * waits on another rank) or sit on peer-accessible devices of one node.
+ * Callbacks return 0 on success. */
+typedef struct sf_host_transport {
+  void* ctx;
+  /* recv (world * bytes) = every rank's `bytes` of send, in rank order */
+  int (*allgather)(void* ctx, const void* send, void* recv, int64_t bytes);
+  int (*barrier)(void* ctx);
+} sf_host_transport;
+/* Host-only: the direct-store plan of the temporal pass's exchange for one
+ * rank (no device needed): up to 26 rows of 14 int64 each -- peer, direction
+ * d[3], source box lo[3] and dims[3] (this rank's local coordinates),
+ * destination dlo[3] (the peer's local coordinates), count. */
+int sf_direct_plan(const int64_t extents[3], int world, int ghost, const int periodic[3], int rank, int max_boxes,
+                   int64_t* out, int* n_out);
+int sf_sim_create_ipc(const sf_solver_config* cfg, const sf_fluid_params* par, const sf_sim_options* opt,
+                      int rank, int world, const sf_host_transport* transport, sf_sim** out);
+/* Exchange of the temporal pass across ranks (exchange.hpp:165-224): 1
+ * (default) = one launch of direct stores into the peers' ghost shells (26
+ * neighbours) after each pass, where every peer's buffers map into this
+ * process; 0 = pack, send/recv, unpack in three axis phases, overlapped with
+ * the interior tiles.  sf_sim_direct_exchange reports whether the direct
+ * stores are in use (a collective call the first time). */
+int sf_sim_set_direct_exchange(sf_sim* s, int on);
+int sf_sim_direct_exchange(sf_sim* s);
 int sf_sim_rank(const sf_sim* s);
 int sf_sim_world(const sf_sim* s);
 /* Owned cells of one grid component (global worker id) as a dense x-fastest

@@ -136,6 +136,15 @@ class ScheduleStep(C.Structure):
     ]
 
 
+# sf_host_transport (include/sforge_b200.h): host callbacks of the CUDA-IPC transport
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64)
+BARRIER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p)
+
+
+class HostTransport(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allgather", ALLGATHER_FN), ("barrier", BARRIER_FN)]
+
+
 class CfdConsts(C.Structure):
     _fields_ = [
         ("dt", C.c_double), ("nu", C.c_double), ("alpha", C.c_double),
@@ -199,6 +208,11 @@ SIGNATURES = [
     ("sf_nccl_unique_id", [_vp], _i),
     ("sf_sim_create_distributed", [C.POINTER(SolverConfig), C.POINTER(FluidParams), C.POINTER(SimOptions),
                                    _i, _i, _vp, C.POINTER(_vp)], _i),
+    ("sf_direct_plan", [_i64p, _i, _i, C.POINTER(_i), _i, _i, _i64p, C.POINTER(_i)], _i),
+    ("sf_sim_create_ipc", [C.POINTER(SolverConfig), C.POINTER(FluidParams), C.POINTER(SimOptions), _i, _i,
+                           C.POINTER(HostTransport), C.POINTER(_vp)], _i),
+    ("sf_sim_set_direct_exchange", [_vp, _i], _i),
+    ("sf_sim_direct_exchange", [_vp], _i),
     ("sf_sim_rank", [_vp], _i),
     ("sf_sim_world", [_vp], _i),
     ("sf_sim_gather_block", [_vp, _cp, _i, _vp, _i64], _i),

@@ -101,6 +101,7 @@ struct table_view {
   __device__ __forceinline__ double* ptr(int b, int f, int s) const { return tab->ptr[b][f][s]; }
   __device__ __forceinline__ const sf_work* work() const { return items; }
   __device__ __forceinline__ int esize(int f) const { return tab->esize[f]; }
+  __device__ __forceinline__ int phys(int b, int f, int s) const { return tab->bidx[b][f][s]; }
 };
 
 constexpr int kDirectItems = 8;
@@ -113,6 +114,7 @@ struct direct_view {
   __device__ __forceinline__ double* ptr(int, int f, int s) const { return p[f][s]; }
   __device__ __forceinline__ const sf_work* work() const { return it; }
   __device__ __forceinline__ int esize(int) const { return 8; }
+  __device__ __forceinline__ int phys(int, int, int s) const { return s; }
 };
 
 // Global (all-block) constants of the CFD kernels: step_constants

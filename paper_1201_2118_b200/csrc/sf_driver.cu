@@ -26,6 +26,7 @@
 #include <vector>
 
 #include <dlfcn.h>
+#include <unistd.h>
 
 #include "sf_kernels.cuh"
 #include "sf_plan.hpp"
@@ -304,13 +305,21 @@ class simulation {
   // world > 1: one process per GPU; this rank owns grid component `rank` of
   // grid::decompose(dom, world, ghost, periodic) and talks to the others over
   // NCCL (communicator from `uid`, created collectively here).
+  // htr != nullptr: the same, with the CUDA-IPC transport (peers' device
+  // buffers mapped into this process; host callbacks for handles, scalars
+  // and barriers) instead of NCCL.
   simulation(const sf_solver_config& cfg, const sf_fluid_params& par, const sf_sim_options& opt,
-             int rank = 0, int world = 1, const void* uid = nullptr)
+             int rank = 0, int world = 1, const void* uid = nullptr, const sf_host_transport* htr = nullptr)
       : cfg_(cfg), par_(par), opt_(opt), rank_(rank), world_(world) {
     validate();
     const bool per[3] = {cfg.periodic[0] != 0, cfg.periodic[1] != 0, cfg.periodic[2] != 0};
     const i64 ext[3] = {cfg.extents[0], cfg.extents[1], cfg.extents[2]};
-    dist_ = uid != nullptr;
+    dist_ = uid != nullptr || htr != nullptr;
+    tr_ = htr ? TR_IPC : (uid ? TR_NCCL : TR_NONE);
+    if (htr) {
+      if (!htr->allgather || !htr->barrier) throw error(SF_ERR_ARG, "host transport needs allgather and barrier");
+      htr_ = *htr;
+    }
     if (dist_) {
       if (opt.workers != 1)
         throw error(SF_ERR_ARG, "distributed mode owns one grid component per rank (workers must be 1)");
@@ -333,9 +342,8 @@ class simulation {
     make_consts();
     SF_CK(cudaSetDevice(opt.device));
     SF_CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
-    if (dist_) {
+    if (tr_ == TR_NCCL) {
       if (!nccl()) throw error(SF_ERR_CUDA, "NCCL library not found (set SF_NCCL_LIB)");
-      if (!uid) throw error(SF_ERR_ARG, "distributed mode needs the NCCL unique id of rank 0");
       nccl_uid id;
       std::memcpy(&id, uid, sizeof id);
       SF_NC(nccl()->CommInitRank(&comm_, world_, id, rank_));
@@ -381,6 +389,7 @@ class simulation {
       for (auto e : io_snapdn_) cudaEventDestroy(e);
       for (auto e : io_inst_) cudaEventDestroy(e);
     }
+    for (auto& kv : ipc_open_) cudaIpcCloseMemHandle(kv.second);
     if (comm_ && nccl() && nccl()->CommDestroy) nccl()->CommDestroy(comm_);
     cudaStreamDestroy(st_);
   }
@@ -540,7 +549,7 @@ class simulation {
     const i64 z[3] = {0, 0, 0};
     launch_copy_box_es(htab_->ptr[0][f][FRONT], fes_[f], L.base, L.sx, L.sy, snd, 8, 0, n[0], n[1], z, n, z, st_);
     ++launches_;
-    SF_NC(nccl()->AllGather(snd, all, (size_t)maxc, kNcclFloat64, comm_, st_));
+    dev_allgather(snd, all, (size_t)maxc);
     std::vector<double> h((size_t)(maxc * world_));
     SF_CK(cudaMemcpyAsync(h.data(), all, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st_));
     sync();
@@ -1319,7 +1328,7 @@ class simulation {
     if (dist_) {  // partials combined in rank order, as reductions.hpp:75-88 does
       double* d = (double*)dalloc_tmp(sizeof(double) * (size_t)(world_ + 1));
       SF_CK(cudaMemcpyAsync(d, &acc, sizeof(double), cudaMemcpyHostToDevice, st_));
-      SF_NC(nccl()->AllGather(d, d + 1, 1, kNcclFloat64, comm_, st_));
+      dev_allgather(d, d + 1, 1);
       std::vector<double> all(world_);
       SF_CK(cudaMemcpyAsync(all.data(), d + 1, sizeof(double) * world_, cudaMemcpyDeviceToHost, st_));
       sync();
@@ -1617,7 +1626,7 @@ class simulation {
     if (dist_) {  // one block per rank: gather the partials, combine in rank (= worker) order
       double* d = (double*)dalloc_tmp(sizeof(double) * (size_t)(world_ + 1));
       SF_CK(cudaMemcpyAsync(d, &part[0].second, sizeof(double), cudaMemcpyHostToDevice, st_));
-      SF_NC(nccl()->AllGather(d, d + 1, 1, kNcclFloat64, comm_, st_));
+      dev_allgather(d, d + 1, 1);
       all.resize(world_);
       SF_CK(cudaMemcpyAsync(all.data(), d + 1, sizeof(double) * world_, cudaMemcpyDeviceToHost, st_));
       sync();
@@ -1696,6 +1705,18 @@ class simulation {
   std::vector<int> lid_;    // global worker id -> local block, or -1
   std::vector<int> owner_;  // global worker id -> rank
   nccl_comm_t comm_ = nullptr;
+  enum { TR_NONE = 0, TR_NCCL = 1, TR_IPC = 2 };
+  int tr_ = TR_NONE;         // how ranks talk: NCCL, or CUDA IPC + host callbacks
+  sf_host_transport htr_{};
+  std::map<std::string, void*> ipc_open_;  // peer allocations mapped here, by handle
+  // the temporal pass's exchange as direct stores into the peers' arrays
+  bool direct_on_ = true;   // sf_sim_set_direct_exchange
+  int direct_state_ = 0;    // 0 not set up, 1 active, -1 unavailable (a peer is not mappable)
+  struct task_set_ref {
+    sf_task* d = nullptr;
+    int n = 0;
+    i64 max_count = 0;
+  } direct_tasks_;
   sf_face_bc bc_[6]{};
   sf_consts consts_{};
   std::vector<sf_layout> lay_;
@@ -2140,6 +2161,10 @@ class simulation {
     std::vector<msg> sends, recvs;
     double* sbuf = nullptr;
     double* rbuf = nullptr;
+    // CUDA-IPC transport: the peer's send buffer (mapped) at the offset of the
+    // message for this rank, per receive; set up collectively on first use
+    mutable bool x_ready = false, x_any = false;
+    mutable std::vector<const double*> x_src;
   };
   std::map<std::string, phase> phases_;
 
@@ -2243,14 +2268,7 @@ class simulation {
       launch_tasks(tview(), ph.first.d, ph.first.n, ph.first.max_count, pred, s);
       ++launches_;
     }
-    if (!ph.sends.empty() || !ph.recvs.empty()) {
-      SF_NC(nccl()->GroupStart());
-      for (const auto& m : ph.sends)
-        SF_NC(nccl()->Send(ph.sbuf + m.off, (size_t)m.count, kNcclFloat64, m.peer, comm_, s));
-      for (const auto& m : ph.recvs)
-        SF_NC(nccl()->Recv(ph.rbuf + m.off, (size_t)m.count, kNcclFloat64, m.peer, comm_, s));
-      SF_NC(nccl()->GroupEnd());
-    }
+    sendrecv(ph, s);
     if (ph.unpack.n) {
       launch_tasks(tview(), ph.unpack.d, ph.unpack.n, ph.unpack.max_count, pred, s);
       ++launches_;
@@ -2332,8 +2350,245 @@ class simulation {
   // (reductions.hpp:75-88)
   void allreduce_max(unsigned long long* dev, int n) {
     if (!dist_) return;
-    SF_NC(nccl()->AllReduce(dev, dev, (size_t)n, kNcclUint64, kNcclMax, comm_, st_));
+    if (tr_ == TR_NCCL) {
+      SF_NC(nccl()->AllReduce(dev, dev, (size_t)n, kNcclUint64, kNcclMax, comm_, st_));
+      return;
+    }
+    unsigned long long mine[8];
+    std::vector<unsigned long long> all((size_t)(8 * world_));
+    SF_CK(cudaMemcpyAsync(mine, dev, sizeof(mine[0]) * (size_t)n, cudaMemcpyDeviceToHost, st_));
+    SF_CK(cudaStreamSynchronize(st_));
+    host_allgather(mine, all.data(), sizeof(mine[0]) * (size_t)n);
+    for (int r = 0; r < world_; ++r)
+      for (int q = 0; q < n; ++q) mine[q] = std::max(mine[q], all[(size_t)(r * n + q)]);
+    SF_CK(cudaMemcpyAsync(dev, mine, sizeof(mine[0]) * (size_t)n, cudaMemcpyHostToDevice, st_));
+    SF_CK(cudaStreamSynchronize(st_));
   }
+
+  // ---- transports -------------------------------------------------------------
+  // NCCL (one rank per GPU; the production path) or CUDA IPC: every rank maps
+  // its peers' device buffers (cudaIpcOpenMemHandle) and moves messages with
+  // device copies or direct stores; the caller's host callbacks carry the
+  // 64-byte handles, the residual maxima and barriers. The IPC transport also
+  // runs several ranks on ONE device (each a separate process), which is how
+  // the cross-process data plane is tested on a one-GPU box: no kernel ever
+  // waits on another rank's kernel, the host orders them.
+  void host_allgather(const void* send, void* recv, size_t bytes) {
+    if (tr_ == TR_IPC) {
+      if (htr_.allgather(htr_.ctx, send, recv, (int64_t)bytes) != 0)
+        throw error(SF_ERR_CUDA, "host transport: allgather failed");
+      return;
+    }
+    const size_t w = (bytes + 7) / 8;  // NCCL: through device memory
+    double* d = (double*)dalloc_tmp(8 * w * (size_t)(world_ + 1));
+    std::vector<double> h(w * (size_t)(world_ + 1), 0.0);
+    std::memcpy(h.data(), send, bytes);
+    SF_CK(cudaMemcpyAsync(d, h.data(), 8 * w, cudaMemcpyHostToDevice, st_));
+    SF_NC(nccl()->AllGather(d, d + w, w, kNcclFloat64, comm_, st_));
+    SF_CK(cudaMemcpyAsync(h.data() + w, d + w, 8 * w * (size_t)world_, cudaMemcpyDeviceToHost, st_));
+    SF_CK(cudaStreamSynchronize(st_));
+    SF_CK(cudaFree(d));
+    for (int r = 0; r < world_; ++r) std::memcpy((char*)recv + r * bytes, h.data() + w * (size_t)(r + 1), bytes);
+  }
+  void host_barrier() {
+    if (tr_ == TR_IPC) {
+      if (htr_.barrier(htr_.ctx) != 0) throw error(SF_ERR_CUDA, "host transport: barrier failed");
+      return;
+    }
+    int x = 0;
+    std::vector<int> all((size_t)world_);
+    host_allgather(&x, all.data(), sizeof x);
+  }
+  // count doubles per rank from device buffer snd into all (rank order), on st_
+  void dev_allgather(const double* snd, double* all, size_t count) {
+    if (tr_ == TR_NCCL) {
+      SF_NC(nccl()->AllGather(snd, all, count, kNcclFloat64, comm_, st_));
+      return;
+    }
+    std::vector<double> mine(count), h(count * (size_t)world_);
+    SF_CK(cudaMemcpyAsync(mine.data(), snd, 8 * count, cudaMemcpyDeviceToHost, st_));
+    SF_CK(cudaStreamSynchronize(st_));
+    host_allgather(mine.data(), h.data(), 8 * count);
+    SF_CK(cudaMemcpyAsync(all, h.data(), 8 * h.size(), cudaMemcpyHostToDevice, st_));
+    SF_CK(cudaStreamSynchronize(st_));
+  }
+  void* open_ipc(const cudaIpcMemHandle_t& h) {
+    const std::string key(reinterpret_cast<const char*>(&h), sizeof h);
+    auto it = ipc_open_.find(key);
+    if (it != ipc_open_.end()) return it->second;
+    void* p = nullptr;
+    SF_CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ipc_open_[key] = p;
+    return p;
+  }
+  // One phase's messages. NCCL: one group of per-peer send/recv. IPC: every
+  // rank pulls its messages out of the senders' buffers with device copies,
+  // between two host barriers (all packed / all pulled).
+  void sendrecv(const phase& ph, cudaStream_t s) {
+    if (tr_ == TR_NCCL) {
+      if (ph.sends.empty() && ph.recvs.empty()) return;
+      SF_NC(nccl()->GroupStart());
+      for (const auto& m : ph.sends)
+        SF_NC(nccl()->Send(ph.sbuf + m.off, (size_t)m.count, kNcclFloat64, m.peer, comm_, s));
+      for (const auto& m : ph.recvs)
+        SF_NC(nccl()->Recv(ph.rbuf + m.off, (size_t)m.count, kNcclFloat64, m.peer, comm_, s));
+      SF_NC(nccl()->GroupEnd());
+      return;
+    }
+    if (tr_ != TR_IPC) return;
+    if (!ph.x_ready) setup_phase_ipc(ph);
+    if (!ph.x_any) return;
+    SF_CK(cudaStreamSynchronize(s));  // this rank's packs are in its send buffer
+    host_barrier();
+    for (size_t q = 0; q < ph.recvs.size(); ++q)
+      SF_CK(cudaMemcpyAsync(ph.rbuf + ph.recvs[q].off, ph.x_src[q], sizeof(double) * (size_t)ph.recvs[q].count,
+                            cudaMemcpyDeviceToDevice, s));
+    SF_CK(cudaStreamSynchronize(s));
+    host_barrier();  // every rank pulled: the send buffers may be refilled
+  }
+  static constexpr int kMaxMsgs = 32;
+  struct ipc_phase_rec {
+    cudaIpcMemHandle_t h;
+    int has, n;
+    int peer[kMaxMsgs];
+    long long off[kMaxMsgs], cnt[kMaxMsgs];
+  };
+  // Collective (every rank runs the same phases in the same order): publish
+  // this rank's send buffer and the offset of each peer's message in it.
+  void setup_phase_ipc(const phase& ph) {
+    ipc_phase_rec me;
+    std::memset(&me, 0, sizeof me);
+    if ((int)ph.sends.size() > kMaxMsgs) throw error(SF_ERR_ARG, "too many messages in one exchange phase");
+    me.has = ph.sbuf != nullptr;
+    if (me.has) SF_CK(cudaIpcGetMemHandle(&me.h, ph.sbuf));
+    me.n = (int)ph.sends.size();
+    for (int q = 0; q < me.n; ++q) {
+      me.peer[q] = ph.sends[q].peer;
+      me.off[q] = ph.sends[q].off;
+      me.cnt[q] = ph.sends[q].count;
+    }
+    std::vector<ipc_phase_rec> all((size_t)world_);
+    host_allgather(&me, all.data(), sizeof me);
+    ph.x_src.clear();
+    for (const auto& m : ph.recvs) {
+      const ipc_phase_rec& r = all[(size_t)m.peer];
+      int at = -1;
+      for (int q = 0; q < r.n; ++q)
+        if (r.peer[q] == rank_) at = q;
+      if (at < 0 || r.cnt[at] != m.count || !r.has)
+        throw error(SF_ERR_CUDA, "IPC transport: send and receive plans disagree with rank " + std::to_string(m.peer));
+      ph.x_src.push_back(static_cast<const double*>(open_ipc(r.h)) + r.off[at]);
+    }
+    ph.x_any = false;
+    for (const auto& r : all) ph.x_any = ph.x_any || r.n > 0;
+    ph.x_ready = true;
+  }
+
+  // ---- direct exchange of the temporal pass ------------------------------------
+  // After each pass, the pass's outputs in the g owned layers next to every
+  // processor face, edge and corner are stored straight into the ghost shell
+  // of the neighbour across it (26 directions, diagonal neighbours included):
+  // pack + send + unpack of exchange.hpp:165-224 become one launch of direct
+  // peer stores. It runs before the pass's max-allreduce, which every rank
+  // waits for before its next pass, so the stores have landed when they are
+  // read (and the ghosts they overwrite are in the buffer the peers' current
+  // pass does not read: outputs ping-pong). Ghost cells beside a physical face
+  // are left as the 3-phase exchange-only refresh leaves them: the pass never
+  // reads their values (sf_sweep2.cu takes pins there).
+  struct ipc_field_rec {
+    unsigned long long host;
+    char pci[32];
+    int has[4][kSlots];
+    cudaIpcMemHandle_t h[4][kSlots];
+    long long sx, sy, base, n[3];
+  };
+  bool direct_active() {
+    if (!dist_ || !direct_on_) return false;
+    if (direct_state_ == 0) setup_direct();
+    return direct_state_ > 0;
+  }
+  void setup_direct() {
+    static const int F4[4] = {SF_VX, SF_VY, SF_VZ, SF_DIVU};
+    download_table();
+    ipc_field_rec me;
+    std::memset(&me, 0, sizeof me);
+    char hn[256] = {0};
+    gethostname(hn, sizeof hn - 1);
+    me.host = std::hash<std::string>()(std::string(hn));
+    SF_CK(cudaDeviceGetPCIBusId(me.pci, (int)sizeof me.pci, opt_.device));
+    const sf_layout& L = lay_[0];
+    me.sx = L.sx;
+    me.sy = L.sy;
+    me.base = L.base;
+    for (int a = 0; a < 3; ++a) me.n[a] = L.dims[a];
+    for (int k = 0; k < 4; ++k)
+      for (int q = 0; q < kSlots; ++q) {
+        double* p = htab_->ptr[0][F4[k]][q];
+        if (!p) continue;
+        const int phys = htab_->bidx[0][F4[k]][q];
+        me.has[k][phys] = 1;
+        SF_CK(cudaIpcGetMemHandle(&me.h[k][phys], p));
+      }
+    std::vector<ipc_field_rec> all((size_t)world_);
+    host_allgather(&me, all.data(), sizeof me);
+    const auto dirs = build_direct_plan(dec_, rank_);
+    // every peer must be mappable here (same node, device visible and
+    // peer-accessible, or the same device); the decision is collective
+    int ok = 1;
+    for (const auto& dr : dirs) {
+      const ipc_field_rec& r = all[(size_t)dr.peer];
+      int dev = -1;
+      if (r.host != me.host || cudaDeviceGetByPCIBusId(&dev, r.pci) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+        continue;
+      }
+      int can = dev == opt_.device;
+      if (!can) cudaDeviceCanAccessPeer(&can, opt_.device, dev);
+      for (int k = 0; k < 4; ++k)
+        for (int q = 0; q < kSlots; ++q)
+          if (me.has[k][q] != r.has[k][q]) can = 0;
+      ok = ok && can;
+    }
+    std::vector<int> oks((size_t)world_);
+    host_allgather(&ok, oks.data(), sizeof ok);
+    for (int v : oks) ok = ok && v;
+    if (!ok) {
+      direct_state_ = -1;
+      return;
+    }
+    std::vector<sf_task> tasks;
+    for (const auto& dr : dirs) {
+      const ipc_field_rec& r = all[(size_t)dr.peer];
+      sf_task t{};
+      t.type = 4;
+      t.src_blk = 0;
+      t.slot = ALT;
+      t.rsx = r.sx;
+      t.rsy = r.sy;
+      t.rbase = r.base;
+      for (int a = 0; a < 3; ++a) {
+        t.lo[a] = dr.lo[a];
+        t.dims[a] = dr.dims[a];
+        t.dlo[a] = dr.dlo[a];
+      }
+      t.count = dr.count;
+      for (int k = 0; k < 4; ++k) {
+        t.field = F4[k];
+        for (int q = 0; q < kSlots; ++q) t.rptr[q] = r.has[k][q] ? static_cast<double*>(open_ipc(r.h[k][q])) : nullptr;
+        tasks.push_back(t);
+      }
+    }
+    task_set ts = upload_tasks(tasks);
+    direct_tasks_.d = ts.d;
+    direct_tasks_.n = ts.n;
+    direct_tasks_.max_count = ts.max_count;
+    direct_state_ = 1;
+  }
+ public:
+  void set_direct(bool on) { direct_on_ = on; }
+  bool direct_enabled() { return direct_active(); }
+ private:
 
   // The temporal pass (two half-sweeps per launch, sf_sweep2.cu) applies with
   // fused = 1 when every face of every local grid component is a wall, a
@@ -2416,6 +2671,26 @@ class simulation {
       // measured on one device, where the exchange is a few device copies,
       // serialising is faster. Across ranks the exchange goes through NCCL and
       // is hidden behind the interior (SF_NO_OVERLAP serialises there too).
+      if (direct_active()) {
+        // one launch over all tiles, then the direct stores into the peers
+        // (predicated like the pass), then the max-allreduce below
+        const work_set& wa = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass(), kTX, sweep2_tile_y());
+        if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
+        launch_sweep2(tview(wa), wa.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_);
+        if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
+        launch_tasks(tview(), direct_tasks_.d, direct_tasks_.n, direct_tasks_.max_count, dctl_, st_, 296);
+        launches_ += 2;
+        ++iter_launch_;
+        allreduce_max(&dctl_->acc[0], 2);
+        ctl(CTL_FINISH_PASS, 0.0, 0, 0, 0, 1);
+        int ftx, fty;
+        sweep_tile_shape(&ftx, &fty);
+        const work_set& wr = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, ftx, fty);
+        launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, 2, st_);
+        launches_ += 2;
+        check_launch();
+        return 2;
+      }
       const bool overlap = (dist_ || force_overlap_) && overlap_env_;
       const auto split = pass_split();
       const work_set& wi = overlap ? *split.first : empty_ws_;
@@ -2709,6 +2984,59 @@ int sf_sim_create_distributed(const sf_solver_config* cfg, const sf_fluid_params
   });
 }
 
+int sf_direct_plan(const int64_t extents[3], int world, int ghost, const int periodic[3], int rank, int max_boxes,
+                   int64_t* out, int* n_out) {
+  return guarded([&] {
+    need(extents, "extents");
+    need(n_out, "n_out");
+    const long long ext[3] = {extents[0], extents[1], extents[2]};
+    const double sp[3] = {1.0, 1.0, 1.0};
+    const bool per[3] = {periodic && periodic[0] != 0, periodic && periodic[1] != 0,
+                         periodic && periodic[2] != 0};
+    const auto d = sfb::decompose(ext, sp, world, ghost, per);
+    if (rank < 0 || rank >= world) throw sfb::error(SF_ERR_ARG, "rank out of range");
+    const auto P = sfb::build_direct_plan(d, rank);
+    // rows: peer, d[3], lo[3], dims[3], dlo[3], count
+    int n = 0;
+    for (const auto& b : P) {
+      if (out && n < max_boxes) {
+        int64_t* r = out + 14 * n;
+        r[0] = b.peer;
+        for (int a = 0; a < 3; ++a) {
+          r[1 + a] = b.d[a];
+          r[4 + a] = b.lo[a];
+          r[7 + a] = b.dims[a];
+          r[10 + a] = b.dlo[a];
+        }
+        r[13] = b.count;
+      }
+      ++n;
+    }
+    *n_out = n;
+  });
+}
+int sf_sim_create_ipc(const sf_solver_config* cfg, const sf_fluid_params* par, const sf_sim_options* opt,
+                      int rank, int world, const sf_host_transport* tr, sf_sim** out) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(par, "par");
+    need(tr, "transport");
+    need(out, "out");
+    *out = nullptr;
+    sf_sim_options o;
+    if (opt) o = *opt; else sf_sim_options_default(&o);
+    auto h = std::make_unique<sf_sim>();
+    h->s = std::make_unique<sfb::simulation>(*cfg, *par, o, rank, world, nullptr, tr);
+    *out = h.release();
+  });
+}
+int sf_sim_set_direct_exchange(sf_sim* s, int on) {
+  return guarded([&] {
+    need(s, "sim");
+    s->s->set_direct(on != 0);
+  });
+}
+int sf_sim_direct_exchange(sf_sim* s) { return s ? (s->s->direct_enabled() ? 1 : 0) : 0; }
 int sf_sim_rank(const sf_sim* s) { return s ? s->s->rank() : -1; }
 int sf_sim_gather_block(sf_sim* s, const char* field, int worker, double* host, int64_t n) {
   return guarded([&] {

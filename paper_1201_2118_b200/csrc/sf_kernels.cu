@@ -188,6 +188,20 @@ __device__ __forceinline__ void run_task(const View& vw, const sf_task& T) {
     });
     return;
   }
+  if (T.type == 4) {  // direct store into a peer's ghost region (fp64 CFD fields)
+    const sf_dev_block& S = vw.blk(T.src_blk);
+    const double* src = vw.ptr(T.src_blk, T.field, T.slot);
+    double* dst = T.rptr[vw.phys(T.src_blk, T.field, T.slot)];
+    for_box_elems<View>(T, [&](long long, long long ii, long long jj, long long kk) {
+      dst[T.rbase + ((T.dlo[2] + kk) * T.rsy + T.dlo[1] + jj) * T.rsx + T.dlo[0] + ii] =
+          src[off(S, T.lo[0] + ii, T.lo[1] + jj, T.lo[2] + kk)];
+    });
+    // the stores cross to another device or process: make them visible
+    // system-wide before this kernel completes (the max-allreduce that
+    // follows on this stream is what the peer waits for)
+    __threadfence_system();
+    return;
+  }
   if (T.type == 0) {  // box copy between blocks of this process
     const sf_dev_block& S = vw.blk(T.src_blk);
     const sf_dev_block& D = vw.blk(T.dst_blk);
@@ -230,10 +244,10 @@ static unsigned task_ctas(const sf_task& t) {
 
 template <class View>
 void launch_tasks(const View& vw, const sf_task* tasks, int ntasks, long long max_count,
-                  const sf_dev_ctl* pred, cudaStream_t st) {
+                  const sf_dev_ctl* pred, cudaStream_t st, int max_ctas) {
   if (ntasks <= 0) return;
   long long bx = (max_count + 255) / 256;
-  if (bx > 1184) bx = 1184;
+  if (bx > max_ctas) bx = max_ctas;
   if (bx < 1) bx = 1;
   dim3 grid((unsigned)bx, (unsigned)ntasks);
   k_tasks<View><<<grid, 256, 0, st>>>(vw, tasks, pred);
@@ -242,9 +256,9 @@ void launch_task_one(const direct_view& vw, const sf_task& t, cudaStream_t st) {
   k_task_one<direct_view><<<task_ctas(t), 256, 0, st>>>(vw, t);
 }
 template void launch_tasks<table_view>(const table_view&, const sf_task*, int, long long,
-                                       const sf_dev_ctl*, cudaStream_t);
+                                       const sf_dev_ctl*, cudaStream_t, int);
 template void launch_tasks<direct_view>(const direct_view&, const sf_task*, int, long long,
-                                        const sf_dev_ctl*, cudaStream_t);
+                                        const sf_dev_ctl*, cudaStream_t, int);
 
 // ---------------------------------------------------------------------------
 // UPDATE_VELOCITY (cfd.hpp:524-589): reads front, writes back (SEPARATEINOUT)

@@ -8,7 +8,8 @@ namespace sfb {
 // One ghost-refresh task: a copy between blocks (one message of
 // exchange.hpp:165-224) or one physical face fill (bc_face, :231-480).
 struct sf_task {
-  int type;  // 0 copy, 1 bc, 2 pack (box -> buf), 3 unpack (buf -> box)
+  int type;  // 0 copy, 1 bc, 2 pack (box -> buf), 3 unpack (buf -> box),
+             // 4 direct store into a peer process's array (pack + send + unpack in one)
   int field;
   int src_blk, dst_blk;
   long long lo[3];    // copy: source box (src-local); bc: tangential box (axis entry unused)
@@ -18,15 +19,23 @@ struct sf_task {
   int axis, side, normal, velocity, kind, scope;
   double v;           // wall velocity component (normal pin / tangential reflection)
   double* buf;        // pack / unpack: contiguous x-fastest message buffer
+  // direct store (type 4): the source is slot `slot` of (src_blk, field); the
+  // destination is the peer's array of the same physical buffer index (every
+  // rank swaps identically), mapped into this process (CUDA IPC), with the
+  // peer's padded layout; dlo is in the peer's local coordinates
+  int slot;
+  double* rptr[kSlots];
+  long long rsx, rsy, rbase;
 };
 
 // Tile shapes (threads = TX x TY; each thread marches z over a chunk).
 constexpr int kTX = 32;
 constexpr int kTY = 8;
 
+// max_ctas: CTAs per task (grid x); 1184 = 8 per SM
 template <class View>
 void launch_tasks(const View& vw, const sf_task* tasks, int ntasks, long long max_count,
-                  const sf_dev_ctl* pred, cudaStream_t st);
+                  const sf_dev_ctl* pred, cudaStream_t st, int max_ctas = 1184);
 // one task passed by value (no device task list)
 void launch_task_one(const direct_view& vw, const sf_task& t, cudaStream_t st);
 template <class View>

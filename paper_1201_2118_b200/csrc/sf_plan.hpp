@@ -123,4 +123,71 @@ phase_plan build_phase_plan(const Dec& dec, const std::vector<int>& gid, const s
   return P;
 }
 
+// The temporal pass's exchange as direct stores (no phases): for each of the
+// 26 directions d in {-1,0,1}^3 \ 0 whose neighbour exists (every non-zero
+// axis leads through a processor face, periodic wraps included, and the
+// neighbour is another component), the g owned layers along each non-zero
+// axis of d (all owned cells along the zero axes) go straight into that
+// neighbour's ghost shell: d = -1 -> its high ghosts [m, m+g), d = +1 -> its
+// low ghosts [-g, 0), d = 0 -> the same local index (the neighbour shares the
+// coordinate). For every ghost cell whose out-of-range axes all lead through
+// processor faces this is the value the three exchange-only axis phases
+// (exchange.hpp:107-119, slabs widened over earlier axes) deliver, since that
+// chain ends at the same diagonal neighbour's owned cell.
+struct direct_box {
+  int peer = -1;
+  int d[3]{};
+  long long lo[3]{}, dims[3]{}, dlo[3]{};
+  long long count = 0;
+};
+
+template <class Dec>
+std::vector<direct_box> build_direct_plan(const Dec& dec, int w) {
+  std::vector<direct_box> out;
+  const long long g = dec.ghost;
+  const auto c = dec.coords_of(w);
+  const auto n = dec.dims(w);
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int d[3] = {dx, dy, dz};
+        if (!dx && !dy && !dz) continue;
+        std::array<int, 3> cp = c;
+        bool ok = true;
+        for (int a = 0; a < 3 && ok; ++a) {
+          if (!d[a]) continue;
+          cp[a] += d[a];
+          if (cp[a] < 0 || cp[a] >= dec.pg[a]) {
+            if (!dec.periodic[a]) ok = false;
+            cp[a] = (cp[a] + dec.pg[a]) % dec.pg[a];
+          }
+        }
+        if (!ok || g == 0) continue;
+        const int peer = dec.id_of(cp);
+        if (peer == w) continue;
+        const auto m = dec.dims(peer);
+        direct_box b;
+        b.peer = peer;
+        for (int a = 0; a < 3; ++a) {
+          b.d[a] = d[a];
+          if (d[a] < 0) {
+            b.lo[a] = 0;
+            b.dims[a] = g;
+            b.dlo[a] = m[a];
+          } else if (d[a] > 0) {
+            b.lo[a] = n[a] - g;
+            b.dims[a] = g;
+            b.dlo[a] = -g;
+          } else {
+            b.lo[a] = 0;
+            b.dims[a] = n[a];
+            b.dlo[a] = 0;
+          }
+        }
+        b.count = b.dims[0] * b.dims[1] * b.dims[2];
+        out.push_back(b);
+      }
+  return out;
+}
+
 }  // namespace sfb

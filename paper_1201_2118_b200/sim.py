@@ -178,10 +178,16 @@ class Simulation:
     def __init__(self, cfg: SolverConfig, par: FluidParams, workers: int = 1, mode: str = "plain",
                  tile: Sequence[int] = (0, 0, 0), ghost: int = 1, form: str = "rows",
                  device: int = 0, fused: int | bool = True, rank: int | None = None,
-                 world: int | None = None, nccl_id: bytes | None = None):
+                 world: int | None = None, nccl_id: bytes | None = None, transport: str | None = None,
+                 group=None):
         """With ``nccl_id`` (from :func:`nccl_unique_id` on rank 0, broadcast to all
         ranks) the simulation is the rank-``rank`` component of a ``world``-rank
-        decomposition and exchanges ghosts over NCCL."""
+        decomposition and exchanges ghosts over NCCL.
+        With ``transport="ipc"`` it exchanges them through CUDA IPC instead
+        (peers' device buffers mapped into this process); the host side of that
+        transport (handles, residual maxima, barriers) runs over the
+        ``torch.distributed`` process group ``group`` (default: the world
+        group, e.g. gloo). Ranks may then share one device."""
         self._h = None
         self.cfg, self.par = cfg, par
         self._lib = L.lib()
@@ -193,7 +199,14 @@ class Simulation:
         opt.ghost, opt.form, opt.device, opt.fused = int(ghost), (1 if form == "points" else 0), int(device), int(fused)
         self._ccfg, self._cpar, self._opt = cfg.to_c(), par.to_c(), opt
         h = C.c_void_p()
-        if nccl_id is not None:
+        if transport == "ipc":
+            self._transport = _TorchHostTransport(group)
+            L.check(self._lib.sf_sim_create_ipc(C.byref(self._ccfg), C.byref(self._cpar), C.byref(opt),
+                                                int(rank or 0), int(world or 1), C.byref(self._transport.c),
+                                                C.byref(h)))
+        elif transport not in (None, "nccl"):
+            raise ValueError("transport must be 'nccl' or 'ipc'")
+        elif nccl_id is not None:
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
             L.check(self._lib.sf_sim_create_distributed(C.byref(self._ccfg), C.byref(self._cpar), C.byref(opt),
                                                         int(rank or 0), int(world or 1), idbuf, C.byref(h)))
@@ -515,6 +528,17 @@ class Simulation:
         return bool(self._lib.sf_sim_ghosts_valid(self._h, name.encode()))
 
     # -- device plumbing -----------------------------------------------------
+    def set_direct_exchange(self, on: bool):
+        """Temporal-pass exchange across ranks: direct stores into the peers'
+        ghost shells (True, default, where the peers' buffers map) or pack /
+        send / unpack phases overlapped with the interior (False)."""
+        L.check(self._lib.sf_sim_set_direct_exchange(self._h, 1 if on else 0))
+
+    @property
+    def direct_exchange(self) -> bool:
+        """Whether the direct peer stores are in use (collective on first use)."""
+        return bool(self._lib.sf_sim_direct_exchange(self._h))
+
     def synchronize(self):
         L.check(self._lib.sf_sim_synchronize(self._h))
         self._async_keep.clear()
@@ -540,6 +564,43 @@ class Simulation:
         ms, n = C.c_double(), C.c_int64()
         L.check(self._lib.sf_sim_kernel_timing(self._h, kernel.encode(), C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+
+class _TorchHostTransport:
+    """sf_host_transport over a torch.distributed process group: the
+    allgather and barrier callbacks the CUDA-IPC transport calls (from the
+    thread that drives the simulation)."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self._torch, self._dist, self._group = torch, dist, group
+        self.world = dist.get_world_size(group)
+        self.error = None
+        self._ag = L.ALLGATHER_FN(self._allgather)  # referenced for the simulation's lifetime
+        self._bar = L.BARRIER_FN(self._barrier)
+        self.c = L.HostTransport(None, self._ag, self._bar)
+
+    def _allgather(self, ctx, send, recv, nbytes):
+        try:
+            torch = self._torch
+            mine = torch.frombuffer(bytearray(C.string_at(send, nbytes)), dtype=torch.uint8) if nbytes else \
+                torch.empty(0, dtype=torch.uint8)
+            out = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(self.world)]
+            self._dist.all_gather(out, mine, group=self._group)
+            C.memmove(recv, b"".join(bytes(t.numpy()) for t in out), nbytes * self.world)
+            return 0
+        except Exception as e:  # pragma: no cover - reported through the C status
+            self.error = e
+            return 1
+
+    def _barrier(self, ctx):
+        try:
+            self._dist.barrier(group=self._group)
+            return 0
+        except Exception as e:  # pragma: no cover
+            self.error = e
+            return 1
 
 
 def nccl_unique_id() -> bytes:

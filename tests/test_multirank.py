@@ -202,3 +202,155 @@ def test_plan_counts_match_between_peers():
             assert sent.keys() == recv.keys()
             for k in sent:
                 assert sent[k] == recv[k], (world, axis, k)
+
+
+# ---- the temporal pass's direct-store exchange (sf_direct_plan) -------------------
+def direct_plan(ext, world, ghost, periodic, rank):
+    lib = sfb.lib()
+    e = (C.c_int64 * 3)(*ext)
+    per = (C.c_int * 3)(*[1 if p else 0 for p in periodic])
+    n = C.c_int()
+    out = (C.c_int64 * (14 * 26))()
+    _lib.check(lib.sf_direct_plan(e, world, ghost, per, rank, 26, out, C.byref(n)))
+    rows = [list(out[14 * i: 14 * i + 14]) for i in range(n.value)]
+    return [dict(peer=r[0], d=r[1:4], lo=r[4:7], dims=r[7:10], dlo=r[10:13], count=r[13]) for r in rows]
+
+
+def direct_exchange_on_rank(rank, world, ext, ghost, periodic):
+    """The driver's direct stores (k_tasks type 4) restated: every box of this
+    rank's plan goes straight into the peer's ghost shell; here the boxes of
+    one peer travel as one gloo message in plan order, and the receiver places
+    them with the sender's plan (the device stores need no message at all)."""
+    d = sfb.decompose(ext, world, ghost, periodic)
+    lo, dims = d.lo[rank], d.size(rank)
+    g = ghost
+    a = np.full((dims[2] + 2 * g, dims[1] + 2 * g, dims[0] + 2 * g), np.nan)
+    kk, jj, ii = np.meshgrid(np.arange(dims[2]), np.arange(dims[1]), np.arange(dims[0]), indexing="ij")
+    a[g:-g, g:-g, g:-g] = cell_tag(ii + lo[0], jj + lo[1], kk + lo[2])
+    mine = direct_plan(ext, world, ghost, periodic, rank)
+    sends = {}
+    for b in mine:
+        sends.setdefault(b["peer"], []).append(box_view(a, g, b["lo"], b["dims"]).reshape(-1).copy())
+    incoming = {}
+    for p in range(world):
+        if p == rank:
+            continue
+        boxes = [b for b in direct_plan(ext, world, ghost, periodic, p) if b["peer"] == rank]
+        if boxes:
+            incoming[p] = boxes
+    reqs, bufs = [], {}
+    for p, parts in sends.items():
+        reqs.append(dist.isend(torch.from_numpy(np.concatenate(parts)), dst=p))
+    for p, boxes in incoming.items():
+        bufs[p] = torch.empty(sum(b["count"] for b in boxes), dtype=torch.float64)
+        reqs.append(dist.irecv(bufs[p], src=p))
+    for r in reqs:
+        r.wait()
+    for p, boxes in incoming.items():
+        flat, at = bufs[p].numpy(), 0
+        for b in boxes:
+            box_view(a, g, b["dlo"], b["dims"])[...] = flat[at:at + b["count"]].reshape(b["dims"][::-1])
+            at += b["count"]
+    return a, lo, dims
+
+
+def _worker_direct(rank, world, port, cases, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        results = []
+        for ext, ghost, periodic in cases:
+            d = sfb.decompose(ext, world, ghost, periodic)
+            a, lo, dims = direct_exchange_on_rank(rank, world, ext, ghost, periodic)
+            # the same ghosts as the three exchange-only axis phases deliver
+            results.append(check_ghosts(a, lo, dims, ext, ghost, periodic, d, rank, False))
+        q.put((rank, results))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_world_direct(world, cases):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_direct, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+# every periodic axis split over >= 2 ranks (the temporal pass's precondition:
+# no self-wrap); 2-deep and 3-deep shells, uneven blocks
+DIRECT_CASES = [
+    ((14, 12, 10), 2, (False, False, False)),
+    ((15, 11, 9), 2, (True, False, False)),
+    ((13, 12, 11), 3, (False, False, False)),
+]
+
+
+def test_direct_store_plan_fills_the_ghosts_of_the_exchange_phases_two_ranks():
+    out = run_world_direct(2, DIRECT_CASES)
+    for rank, res in out.items():
+        assert res == [0] * len(DIRECT_CASES), (rank, res)
+
+
+def test_direct_store_plan_with_edges_and_corners_four_ranks():
+    # (2,2,1): edge neighbours (diagonals), and with periodic x and y both x
+    # (and y) faces of a rank face the same peer
+    out = run_world_direct(4, DIRECT_CASES[:1] + [((14, 12, 10), 2, (True, True, False))])
+    for rank, res in out.items():
+        assert res == [0, 0], (rank, res)
+
+
+def test_direct_store_plan_is_symmetric_between_peers():
+    # what rank r stores into peer p is exactly what p's ghost boxes expect:
+    # same count per direction, and opposite directions pair up
+    for world, ext, per in [(2, (14, 12, 10), (True, False, False)), (4, (14, 12, 10), (False, False, False)),
+                            (8, (12, 12, 12), (True, True, True))]:
+        plans = {r: direct_plan(ext, world, 2, per, r) for r in range(world)}
+        for r, P in plans.items():
+            for b in P:
+                back = [c for c in plans[b["peer"]] if c["peer"] == r and c["d"] == [-x for x in b["d"]]]
+                assert back and back[0]["count"] == b["count"], (world, r, b)
+
+
+def _worker_transport(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1201_2118_b200.sim import _TorchHostTransport
+        t = _TorchHostTransport()
+        # call through the C function pointers the library receives
+        ag = C.cast(C.cast(t.c.allgather, C.c_void_p), _lib.ALLGATHER_FN)
+        bar = C.cast(C.cast(t.c.barrier, C.c_void_p), _lib.BARRIER_FN)
+        send = (C.c_uint64 * 3)(rank, 100 + rank, 2 ** 63 + rank)
+        recv = (C.c_uint64 * (3 * world))()
+        rc1 = ag(None, C.cast(send, C.c_void_p), C.cast(recv, C.c_void_p), 24)
+        rc2 = bar(None)
+        want = [v for r in range(world) for v in (r, 100 + r, 2 ** 63 + r)]
+        q.put((rank, [rc1, rc2, list(recv) == want]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_transport_callbacks_over_gloo():
+    # the allgather / barrier callbacks of the CUDA-IPC transport
+    # (sf_host_transport) as the library calls them: rank-ordered bytes
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_transport, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in range(3))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, res in out.items():
+        assert res == [0, 0, True], (rank, res)
