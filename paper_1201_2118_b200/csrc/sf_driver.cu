@@ -2600,6 +2600,8 @@ class simulation {
   // version wrong on 39x43x13, periodic y, two components, ghost 2).
   bool temporal() const {
     if (!maps2_ || !temporal_env_ || opt_.fused != 1) return false;
+    for (int b = 0; b < nloc_; ++b)  // the pass addresses its arrays with 32-bit element offsets
+      if ((unsigned long long)(lay_[b].sx * lay_[b].sy * lay_[b].sz) >= (1ull << 32)) return false;
     bool proc = false;
     for (int b = 0; b < nloc_; ++b)
       for (int fi = 0; fi < 6; ++fi) {

@@ -151,7 +151,9 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   const int per0 = PER ? s.per[0] : 0, per1 = PER ? s.per[1] : 0, per2 = PER ? s.per[2] : 0;
   auto wrp = [](int g, int n, int per) { return per ? ((g % n) + n) % n : g; };
   const int lo0 = (int)B.lo[0], lo1 = (int)B.lo[1], lo2 = (int)B.lo[2];
-  const long long sx = B.sx, sxy = B.sx * B.sy;
+  // element offsets fit 32 bits (the driver checks sx * sy * sz < 2^32):
+  // one IMAD.WIDE per store address instead of a 64-bit add pair
+  const unsigned sx = (unsigned)B.sx, sxy = (unsigned)(B.sx * B.sy);
   const double beta = ctl->beta, dt = ctl->dt;
   const int colA = ctl->color, colB = colA ^ 1;
   const double cu = dt * s.ix, cv = dt * s.iy, cw = dt * s.iz;
@@ -414,7 +416,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   double* __restrict__ Wn = tab->ptr[b][SF_VZ][ALT];
   unsigned long long r1 = 0ull, r2 = 0ull;
   double wm2 = 0.0;  // swept w2 of the -z neighbour (marching register)
-  long long o = B.base + ((long long)k0 * B.sy + j) * sx + i;
+  unsigned o = (unsigned)(B.base + ((long long)k0 * B.sy + j) * B.sx + i);
 
   // pre-phase: S1 fields of planes 0 and 1 (S0 planes 0..2)
   wait_in(0);
@@ -428,15 +430,28 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
     issue(NIN + 1);
   }
 
-  // S1 plane m: fields in slot m & 3, divu1 in slot m % 3 (dsu = u % 3)
-  int dsu = 0;
+  // S1 plane m: fields in slot m & 3, divu1 in slot m % 3 (dsu = u % 3).
+  // S0 planes u+2 and u+3 sit in stages st2 and st3 (carried, not divided:
+  // the ring indices are uniform per CTA and cost nothing per cell)
+  int dsu = 0, st2 = 2 % NIN, st3 = 3 % NIN;
+  uint32_t ph3 = (uint32_t)((3 / NIN) & 1);
   for (int u = 0; u <= nplanes + 1; ++u) {
     const int dsu1 = dsu == 2 ? 0 : dsu + 1;
-    wait_in(u + 3);
-    if (u <= nplanes) s1_fields(k0 + u, so(u + 2), so(u + 3), F((u + 2) & 3));
+    if (u + 3 < nin) {
+      const uint32_t a = bar0 + 8u * (uint32_t)st3;
+      asm volatile(
+          "{\n .reg .pred P1;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+          " @!P1 bra W_%=;\n}\n" ::"r"(a),
+          "r"(ph3)
+          : "memory");
+    }
+    if (u <= nplanes) s1_fields(k0 + u, st2 * (IN_BYTES / 8), st3 * (IN_BYTES / 8), F((u + 2) & 3));
     s1_div(k0 + u - 1, F((u + 1) & 3), F(u & 3), Dr(dsu1), Dr(dsu));
     __syncthreads();
     if (tid == 0) issue(u + 2 + NIN);  // S0 plane u+2 is consumed
+    st2 = st3;
+    st3 = st3 + 1 == NIN ? 0 : st3 + 1;
+    ph3 ^= st3 == 0 ? 1u : 0u;
     if (u == 1 && act) {
       // swept w2 of the plane below the chunk: sweep B's -z neighbour at k0
       const double w1_below = S[F(1) + W1 * EN + q0];
@@ -481,11 +496,11 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         double dd = (un - umn) * s.ix;
         dd += (vn - vmn) * s.iy;
         dd += (wn - wm2) * s.iz;
-        Pn[o] = pn;
-        Un[o] = un;
-        Vn[o] = vn;
-        Wn[o] = wn;
-        Dn[o] = dd;
+        __stwb(Pn + o, pn);
+        __stwb(Un + o, un);
+        __stwb(Vn + o, vn);
+        __stwb(Wn + o, wn);
+        __stwb(Dn + o, dd);
         const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
         r1 = b1 > r1 ? b1 : r1;
         r2 = b2 > r2 ? b2 : r2;
@@ -517,11 +532,11 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         double dd = (un - umn) * s.ix;
         dd += (vn - vmn) * s.iy;
         dd += (wn - wm2) * s.iz;
-        Pn[o] = pn;
-        Un[o] = un;
-        Vn[o] = vn;
-        Wn[o] = wn;
-        Dn[o] = dd;
+        __stwb(Pn + o, pn);
+        __stwb(Un + o, un);
+        __stwb(Vn + o, vn);
+        __stwb(Wn + o, wn);
+        __stwb(Dn + o, dd);
         if (xlo) {
           Un[o - 1] = umn;
           Dn[o - 1] = dd;
@@ -576,11 +591,11 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         double dd = (un - umn) * s.ix;
         dd += (vn - vmn) * s.iy;
         dd += (wn - wm2) * s.iz;
-        Pn[o] = pn;
-        Un[o] = un;
-        Vn[o] = vn;
-        Wn[o] = wn;
-        Dn[o] = dd;
+        __stwb(Pn + o, pn);
+        __stwb(Un + o, un);
+        __stwb(Vn + o, vn);
+        __stwb(Wn + o, wn);
+        __stwb(Dn + o, dd);
         // ghosts the next pass reads: pinned low-face velocities, mirrored divu
         if (xlo) {
           Un[o - 1] = umn;
