@@ -39,7 +39,55 @@ struct domain {  // grid.hpp:25-31
   index_t cells() const { return extents[0] * extents[1] * extents[2]; }
 };
 enum class reduce_op { max_abs = SF_MAX_ABS, sum = SF_SUM, sum_sq = SF_SUM_SQ, max_abs_diff = SF_MAX_ABS_DIFF };
+enum class stagger : int { none = -1, x = 0, y = 1, z = 2 };  // field.hpp:23
+
+struct face_bc {  // exchange.hpp:18-26
+  enum class kind { unset = SF_BC_UNSET, wall = SF_BC_WALL, symmetry = SF_BC_SYMMETRY, outflow = SF_BC_OUTFLOW };
+  kind k = kind::unset;
+  std::array<double, 3> velocity{};
+  static face_bc wall(std::array<double, 3> v = {0, 0, 0}) { return {kind::wall, v}; }
+  static face_bc symmetry() { return {kind::symmetry, {}}; }
+  static face_bc outflow() { return {kind::outflow, {}}; }
+};
+struct boundary_spec {  // exchange.hpp:30-42
+  std::array<face_bc, 6> faces{};
+  face_bc& at(int axis, int side) { return faces[static_cast<std::size_t>(2 * axis + side)]; }
+  const face_bc& at(int axis, int side) const { return faces[static_cast<std::size_t>(2 * axis + side)]; }
+  static boundary_spec uniform(face_bc fb) {
+    boundary_spec b;
+    b.faces.fill(fb);
+    return b;
+  }
+};
 }  // namespace grid
+
+namespace ccl {
+enum class intent { in = 0, out = 1, inout = 2, separate_inout = 3 };  // descriptor.hpp:216
+}  // namespace ccl
+
+namespace codegen {  // codegen.hpp:30-57
+enum class template_id { threedblock };
+struct binding {
+  std::string field;
+  ccl::intent io = ccl::intent::in;
+  bool cached = false;
+};
+struct execution_plan {
+  std::string kernel;
+  template_id tmpl = template_id::threedblock;
+  std::array<int, 3> tile{};
+  std::array<int, 6> halo{};
+  std::vector<binding> bindings;
+  std::vector<std::string> parameters;
+  int halo_lo(int axis) const { return halo[static_cast<std::size_t>(2 * axis)]; }
+  int halo_hi(int axis) const { return halo[static_cast<std::size_t>(2 * axis + 1)]; }
+  int max_halo() const {
+    int m = 0;
+    for (int h : halo) m = m < h ? h : m;
+    return m;
+  }
+};
+}  // namespace codegen
 
 namespace exec {
 struct exec_error : std::runtime_error {
@@ -47,7 +95,33 @@ struct exec_error : std::runtime_error {
 };
 enum class region { all = SF_REGION_ALL, interior = SF_REGION_INTERIOR, boundary = SF_REGION_BOUNDARY };
 enum class run_mode { plain = 0, overlap = 1 };
+struct kernel_signature {  // executor.hpp:46-49
+  std::vector<std::string> fields;
+  std::vector<std::string> params;
+};
+// A point function for the device, given as the CUDA C++ text of the body of
+// the reference's F(const point_ctx& c) (executor.hpp:130-184): c.field(s)(di,
+// dj, dk), c.field(s).load(), c.field(s).store(v), c.param(s), c.i / c.j /
+// c.k.  register_kernel JIT-compiles it for sm_100a (--fmad=false).
+struct device_function {
+  std::string body;
+};
 }  // namespace exec
+
+// A point function usable by BOTH executors: SF_POINT_FUNCTION(NAME, body)
+// defines a functor type whose templated operator() is the body (the
+// reference's executor::register_kernel calls it with its point_ctx) and
+// whose source() is the body's text (this executor::register_kernel compiles
+// it for the device).  The body must be plain C++ over `c` without
+// preprocessor directives or line comments.
+#define SF_POINT_FUNCTION(NAME, ...)                                \
+  struct NAME {                                                     \
+    template <class Ctx>                                            \
+    void operator()(const Ctx& c) const {                           \
+      __VA_ARGS__                                                   \
+    }                                                               \
+    static const char* source() { return #__VA_ARGS__; }            \
+  }
 
 namespace cfd {
 struct cfd_error : std::runtime_error {
@@ -271,4 +345,217 @@ class simulation {
 };
 
 }  // namespace cfd
+
+namespace exec {
+struct schedule_step {  // executor.hpp:422-466
+  enum class kind { run = 0, exchange = 1, physical_bc = 2, refresh = 3, reduce = 4 };
+  kind what = kind::run;
+  std::string kernel;
+  region reg = region::all;
+  std::vector<std::string> fields;
+  grid::reduce_op op = grid::reduce_op::max_abs;
+  std::string source;
+  std::string target;
+  static schedule_step run(std::string kernel, region r = region::all) {
+    schedule_step s;
+    s.what = kind::run;
+    s.kernel = std::move(kernel);
+    s.reg = r;
+    return s;
+  }
+  static schedule_step exchange(std::vector<std::string> fields) {
+    schedule_step s;
+    s.what = kind::exchange;
+    s.fields = std::move(fields);
+    return s;
+  }
+  static schedule_step physical_bc(std::vector<std::string> fields) {
+    schedule_step s;
+    s.what = kind::physical_bc;
+    s.fields = std::move(fields);
+    return s;
+  }
+  static schedule_step refresh(std::vector<std::string> fields) {
+    schedule_step s;
+    s.what = kind::refresh;
+    s.fields = std::move(fields);
+    return s;
+  }
+  static schedule_step reduce(std::string source, grid::reduce_op op, std::string target) {
+    schedule_step s;
+    s.what = kind::reduce;
+    s.source = std::move(source);
+    s.op = op;
+    s.target = std::move(target);
+    return s;
+  }
+};
+struct schedule {
+  std::vector<schedule_step> steps;
+};
+
+// exec::executor (executor.hpp:477-862) over device-resident distributed
+// fields: the grid components of grid::decompose(dom, workers, ghost,
+// periodic) live on one device; fields, exchanges, physical boundary
+// conditions, kernels, reductions, schedules and ghost validity keep the
+// reference's semantics and error texts.  The reference builds the executor
+// over its worker_group and field_store; here the constructor takes the
+// decomposition's inputs and owns the store.
+class executor {
+ public:
+  executor(const grid::domain& dom, int workers, int ghost, std::array<bool, 3> periodic,
+           grid::boundary_spec bc = {}, int device = 0) {
+    sf_solver_config c{};
+    for (int a = 0; a < 3; ++a) {
+      c.extents[a] = dom.extents[a];
+      c.spacing[a] = dom.spacing[a];
+      c.origin[a] = dom.origin[a];
+      c.periodic[a] = periodic[a] ? 1 : 0;
+    }
+    c.reynolds = 100.0;
+    c.sigma = 0.5;
+    c.tolerance = 1e-6;
+    c.omega = 1.7;
+    c.max_sweeps = 1;
+    c.symmetry_z = 0;
+    sf_fluid_params p{};
+    p.viscosity = 0.01;
+    p.density = 1.0;
+    sf_sim_options o;
+    sf_sim_options_default(&o);
+    o.workers = workers;
+    o.ghost = ghost < 1 ? 1 : ghost;  // the device store always carries the CFD kernels' one layer
+    o.device = device;
+    sf_sim* h = nullptr;
+    cfd::check(sf_sim_create(&c, &p, &o, &h));
+    h_.reset(h);
+    set_boundary(bc);
+  }
+
+  // executor::boundary() (executor.hpp:482): replace the face conditions
+  void set_boundary(const grid::boundary_spec& bc) {
+    bc_ = bc;
+    for (int axis = 0; axis < 3; ++axis)
+      for (int side = 0; side < 2; ++side) {
+        const grid::face_bc& f = bc.at(axis, side);
+        cfd::check(sf_sim_set_face_bc(h_.get(), axis, side, (int)f.k, f.velocity.data()));
+      }
+  }
+  const grid::boundary_spec& boundary() const { return bc_; }
+
+  // field_store::create (field.hpp:108-112); fp32 = false keeps fp64 storage
+  void create_field(const std::string& name, grid::stagger st, bool fp32 = false) {
+    cfd::check(sf_sim_create_field_typed(h_.get(), name.c_str(), (int)st, fp32 ? 4 : 8));
+  }
+
+  // executor::register_kernel (executor.hpp:484-488) with a device function
+  void register_kernel(const codegen::execution_plan& plan, const kernel_signature& sig, const device_function& fn) {
+    std::vector<sf_binding> b;
+    for (const auto& x : plan.bindings) b.push_back({x.field.c_str(), (int)x.io, x.cached ? 1 : 0});
+    std::vector<const char*> pn, sf, sp;
+    for (const auto& x : plan.parameters) pn.push_back(x.c_str());
+    for (const auto& x : sig.fields) sf.push_back(x.c_str());
+    for (const auto& x : sig.params) sp.push_back(x.c_str());
+    sf_plan cp{};
+    cp.kernel = plan.kernel.c_str();
+    for (int a = 0; a < 3; ++a) cp.tile[a] = plan.tile[a];
+    for (int a = 0; a < 6; ++a) cp.halo[a] = plan.halo[a];
+    cp.bindings = b.data();
+    cp.n_bindings = (int)b.size();
+    cp.params = pn.data();
+    cp.n_params = (int)pn.size();
+    cfd::check(sf_sim_register_kernel(h_.get(), &cp, sf.data(), (int)sf.size(), sp.data(), (int)sp.size(),
+                                      fn.body.c_str()));
+  }
+  // ... or with an SF_POINT_FUNCTION functor (the reference's F: void(const point_ctx&))
+  template <class F, class = decltype(F::source())>
+  void register_kernel(const codegen::execution_plan& plan, const kernel_signature& sig, F) {
+    register_kernel(plan, sig, device_function{F::source()});
+  }
+
+  void run_kernel(const std::string& name, const std::map<std::string, double>& params, region reg = region::all) {
+    std::vector<const char*> n;
+    std::vector<double> v;
+    for (auto& kv : params) {
+      n.push_back(kv.first.c_str());
+      v.push_back(kv.second);
+    }
+    cfd::check(sf_sim_run_kernel(h_.get(), name.c_str(), n.data(), v.data(), (int)n.size(), (int)reg));
+  }
+  void exchange(const std::vector<std::string>& fields) { fields_call(sf_sim_exchange, fields); }
+  void physical_bc(const std::vector<std::string>& fields) { fields_call(sf_sim_physical_bc, fields); }
+  void refresh(const std::vector<std::string>& fields) { fields_call(sf_sim_refresh, fields); }
+  double reduce(const std::string& field, grid::reduce_op op) {
+    double v = 0.0;
+    cfd::check(sf_sim_reduce(h_.get(), field.c_str(), (int)op, &v));
+    return v;
+  }
+
+  // executor::run_schedule (executor.hpp:533-553): dry run, then `steps` passes
+  void run_schedule(const schedule& s, const std::map<std::string, double>& params, int steps,
+                    run_mode mode = run_mode::plain, std::map<std::string, double>* results = nullptr) {
+    std::vector<sf_schedule_step> cs;
+    std::vector<std::vector<const char*>> keep;
+    keep.reserve(s.steps.size());
+    for (const auto& st : s.steps) {
+      keep.emplace_back();
+      for (const auto& f : st.fields) keep.back().push_back(f.c_str());
+      sf_schedule_step c{};
+      c.kind = (int)st.what;
+      c.kernel = st.kernel.c_str();
+      c.region = (int)st.reg;
+      c.fields = keep.back().data();
+      c.n_fields = (int)keep.back().size();
+      c.source = st.source.c_str();
+      c.op = (int)st.op;
+      c.target = st.target.c_str();
+      cs.push_back(c);
+    }
+    std::vector<const char*> n;
+    std::vector<double> v;
+    for (auto& kv : params) {
+      n.push_back(kv.first.c_str());
+      v.push_back(kv.second);
+    }
+    cfd::check(sf_sim_run_schedule(h_.get(), cs.data(), (int)cs.size(), n.data(), v.data(), (int)n.size(), steps,
+                                   (int)mode));
+    if (results)
+      for (const auto& st : s.steps)
+        if (st.what == schedule_step::kind::reduce) {
+          double r = 0.0;
+          cfd::check(sf_sim_result(h_.get(), st.target.c_str(), &r));
+          (*results)[st.target] = r;
+        }
+  }
+
+  // ghost validity (executor.hpp:610-613)
+  bool ghosts_valid(const std::string& field) const { return sf_sim_ghosts_valid(h_.get(), field.c_str()) == 1; }
+  void invalidate_ghosts(const std::string& field) { cfd::check(sf_sim_invalidate_ghosts(h_.get(), field.c_str())); }
+  void invalidate_all_ghosts() { cfd::check(sf_sim_invalidate_all_ghosts(h_.get())); }
+
+  // grid::gather / grid::scatter (io.hpp:25-65) of a field of this store
+  std::vector<double> gather(const std::string& field, grid::index_t cells) {
+    std::vector<double> g((size_t)cells);
+    cfd::check(sf_sim_gather(h_.get(), field.c_str(), g.data(), (int64_t)g.size()));
+    return g;
+  }
+  void scatter(const std::string& field, const std::vector<double>& g) {
+    cfd::check(sf_sim_scatter(h_.get(), field.c_str(), g.data(), (int64_t)g.size()));
+  }
+  sf_sim* handle() { return h_.get(); }
+
+ private:
+  template <class Fn>
+  void fields_call(Fn fn, const std::vector<std::string>& fields) {
+    std::vector<const char*> f;
+    for (auto& x : fields) f.push_back(x.c_str());
+    cfd::check(fn(h_.get(), f.data(), (int)f.size()));
+  }
+  struct del {
+    void operator()(sf_sim* s) const { sf_sim_destroy(s); }
+  };
+  grid::boundary_spec bc_;
+  std::unique_ptr<sf_sim, del> h_;
+};
+}  // namespace exec
 }  // namespace sforge_b200

@@ -263,7 +263,7 @@ template void launch_tasks<direct_view>(const direct_view&, const sf_task*, int,
 // ---------------------------------------------------------------------------
 // UPDATE_VELOCITY (cfd.hpp:524-589): reads front, writes back (SEPARATEINOUT)
 // ---------------------------------------------------------------------------
-template <class View>
+template <class View, bool BLEND>
 __global__ void __launch_bounds__(kTX* kTY) k_update_vel(View vw, int zc, sf_consts s,
                                                          sf_dev_ctl* ctl, double dt_arg) {
   const tile_loc t = locate(vw.work(), vw.nitems, zc);
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kTX* kTY) k_update_vel(View vw, int zc, sf_con
       };
       const ldg_acc A{U, V, W, Q, o, sx, sxy};
       double r[3];
-      uv_point(A, s, dt, r);
+      uv_point<ldg_acc, BLEND>(A, s, dt, r);
       Uo[o] = r[0];
       Vo[o] = r[1];
       Wo[o] = r[2];
@@ -309,7 +309,11 @@ template <class View>
 void launch_update_velocity(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                             double dt, cudaStream_t st) {
   if (nctas <= 0) return;
-  k_update_vel<View><<<nctas, dim3(kTX, kTY), 0, st>>>(vw, zc, c, ctl, dt);
+  // alpha == 0 (either sign): the blend terms are only evaluated on zero fluxes (sf_uv.cuh)
+  if (c.alpha == 0.0)
+    k_update_vel<View, false><<<nctas, dim3(kTX, kTY), 0, st>>>(vw, zc, c, ctl, dt);
+  else
+    k_update_vel<View, true><<<nctas, dim3(kTX, kTY), 0, st>>>(vw, zc, c, ctl, dt);
 }
 template void launch_update_velocity<table_view>(const table_view&, int, int, const sf_consts&,
                                                  sf_dev_ctl*, double, cudaStream_t);

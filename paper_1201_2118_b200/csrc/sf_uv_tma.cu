@@ -48,6 +48,7 @@ void uv_box(int field, int* bw, int* bh) {
   *bh = field == SF_P ? PH : VH;
 }
 
+template <bool BLEND>
 __global__ void __launch_bounds__(NT, 2)
     k_update_vel_tma(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc,
                      sf_consts s, sf_dev_ctl* ctl, const uvmaps_t* __restrict__ maps) {
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(NT, 2)
         if (c > 0) A.pr[c - 1] = reinterpret_cast<const double*>(st + ST_P);
       }
       double r[3];
-      uv_point(A, s, dt, r);
+      uv_point<acc, BLEND>(A, s, dt, r);
       Uo[o] = r[0];
       Vo[o] = r[1];
       Wo[o] = r[2];
@@ -167,9 +168,11 @@ __global__ void __launch_bounds__(NT, 2)
 void launch_update_velocity_tma(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                                 const void* maps, cudaStream_t st) {
   if (nctas <= 0) return;
-  ensure_smem_attr((const void*)k_update_vel_tma, NST * ST_BYTES);
-  k_update_vel_tma<<<nctas, dim3(TX, TY), NST * ST_BYTES, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl,
-                                                                 static_cast<const uvmaps_t*>(maps));
+  // alpha == 0 (either sign): the blend terms are only evaluated on zero fluxes (sf_uv.cuh)
+  auto k = c.alpha == 0.0 ? k_update_vel_tma<false> : k_update_vel_tma<true>;
+  ensure_smem_attr((const void*)k, NST * ST_BYTES);
+  k<<<nctas, dim3(TX, TY), NST * ST_BYTES, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl,
+                                                 static_cast<const uvmaps_t*>(maps));
 }
 
 }  // namespace sfb
