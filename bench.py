@@ -68,7 +68,9 @@ def parse_args():
                     help="c1: BASELINE.json configs[1] fixed-work cavity (default); c0: configs[0], the 64^3 "
                          "reference oracle run with the default solver config (tolerance 1e-6, up to 500 "
                          "half-sweeps per step), timed from rest over --steps steps")
-    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"], help="field storage for --workload stencil")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
+                    help="field storage: --workload stencil fields; --workload cavity: f32 = the fp32 variant of the "
+                         "CFD fields (fused TMA half-sweep in fp32; tolerance-checked, not bitwise)")
     ap.add_argument("--tile", default="32,16,64", help="descriptor TILE for --workload stencil")
     return ap.parse_args()
 
@@ -280,7 +282,9 @@ def run_ours(args):
         if args.strong:
             n = args.strong
         cfg = cavity_cfg(sfb, n, S, c0)
-        sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=1, device=dev, fused=fused)
+        if args.dtype == "f32" and fused == 1:
+            fused = 3  # the temporal pass is fp64-only; fp32 runs the fused TMA half-sweep
+        sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=1, device=dev, fused=fused, precision=args.dtype)
     if args.strong:  # this rank's block of the fixed global grid
         cells = 1
         for a in sim.block_shape():
@@ -304,10 +308,13 @@ def run_ours(args):
             dist.barrier()
 
     # ---- parity: the first steps from rest against the reference's checksums --
-    golden, gkey = golden_checksums(n, S, c0) if (world == 1 and not args.strong) else ({}, None)
+    golden, gkey = (golden_checksums(n, S, c0) if (world == 1 and not args.strong and args.dtype == "f64")
+                    else ({}, None))
     parity = {"ok": None, "golden": gkey,
-              "note": "no reference checksum for this configuration (multi-rank and strong-scaling grids are "
-                      "pinned by tests/test_gpu_*: grid components, cross-process transport, path equivalence)"}
+              "note": ("fp32 variant: compared with the fp64 reference under stated per-field tolerances "
+                       "(tests/test_gpu_fp32.py), not by checksum" if args.dtype == "f32" else
+                       "no reference checksum for this configuration (multi-rank and strong-scaling grids are "
+                       "pinned by tests/test_gpu_*: grid components, cross-process transport, path equivalence)")}
     done = 0
     if golden and not c0:  # warm-up steps 1 and 2 are checked (untimed)
         got = {}
@@ -363,10 +370,11 @@ def run_ours(args):
     # pass processes two half-sweeps per launch (its DRAM traffic is half of
     # that: the first sweep's state never leaves the SM, see dram_* below)
     units = 2 if kname == "sweep2" else 1
-    algo_launch = BYTES_PER_HALF_SWEEP * units * cells
+    es = 4 if args.dtype == "f32" else 8
+    algo_launch = BYTES_PER_HALF_SWEEP * es // 8 * units * cells
     achieved = (algo_launch / avg_launch_s / 1e9) if avg_launch_s else None
-    traffic, _ = ncu_traffic(kname)
-    step_bytes = (BYTES_UV + BYTES_DIV + BYTES_PER_HALF_SWEEP * S) * cells
+    traffic, _ = ncu_traffic(kname) if es == 8 else (None, None)
+    step_bytes = (BYTES_UV + BYTES_DIV + BYTES_PER_HALF_SWEEP * S) * es // 8 * cells
     roofline = {
         "bound": "hbm",
         "kernel": ("k_sweep2 (temporal pass: two fused half-sweeps per launch)" if kname == "sweep2"
@@ -445,7 +453,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
-        "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+        "dtype": args.dtype if args.workload == "cavity" else "f64",
         "data": "synthetic (lid-driven cavity from rest, init_cavity)",
         "config": {"workload": (f"configs[0]: 3D lid-driven cavity {n}^3 fp64, ghost 1, the reference oracle run "
                                 f"(default solver config: tolerance 1e-6, up to 500 half-sweeps per step), "

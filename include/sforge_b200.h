@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SF_ABI_VERSION 1
+#define SF_ABI_VERSION 2
 
 enum sf_status {
   SF_OK = 0,
@@ -108,6 +108,10 @@ typedef struct sf_sim_options {
                   one grid component per device, wall / symmetry faces;
                   3 = TMA half-sweep only; 2 = fused, plain loads (A/B
                   baseline); 0 = the reference's unfused dataflow */
+  int precision; /* bytes per value of the CFD fields: 8 = fp64 (default; bitwise
+                    the reference), 4 = fp32 storage and arithmetic on the fused
+                    TMA half-sweep (fused 1 or 3; compared with the reference
+                    under stated per-field tolerances) */
 } sf_sim_options;
 
 /* cfd::step_stats (cfd.hpp:86-90) */

@@ -80,6 +80,7 @@ class SimOptions(C.Structure):
         ("form", C.c_int),
         ("device", C.c_int),
         ("fused", C.c_int),
+        ("precision", C.c_int),
     ]
 
 

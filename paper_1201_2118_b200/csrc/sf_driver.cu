@@ -316,6 +316,17 @@ class simulation {
     const i64 ext[3] = {cfg.extents[0], cfg.extents[1], cfg.extents[2]};
     dist_ = uid != nullptr || htr != nullptr;
     tr_ = htr ? TR_IPC : (uid ? TR_NCCL : TR_NONE);
+    // the fp32 variant of the CFD fields: storage and arithmetic in fp32 on the
+    // fused TMA path (the temporal pass, the plain-load kernels and the
+    // single CFD kernels stay fp64)
+    if (opt.precision != 0 && opt.precision != 8 && opt.precision != 4)
+      throw error(SF_ERR_ARG, "precision must be 8 (fp64) or 4 (fp32) bytes per value");
+    cfd_es_ = opt.precision == 4 ? 4 : 8;
+    if (cfd_es_ == 4) {
+      if (opt.fused != 1 && opt.fused != 3)
+        throw error(SF_ERR_ARG, "fp32 CFD fields run the fused TMA half-sweep (fused = 1 or 3)");
+      for (int f = 0; f < SF_NFIELDS; ++f) fes_[f] = 4;
+    }
     if (htr) {
       if (!htr->allgather || !htr->barrier) throw error(SF_ERR_ARG, "host transport needs allgather and barrier");
       htr_ = *htr;
@@ -349,6 +360,8 @@ class simulation {
       SF_NC(nccl()->CommInitRank(&comm_, world_, id, rank_));
     }
     allocate();
+    if (cfd_es_ == 4 && (!maps_ || !uvmaps_))
+      throw error(SF_ERR_CUDA, "fp32 CFD fields need the TMA kernels (cuTensorMapEncodeTiled unavailable)");
     SF_CK(cudaEventCreateWithFlags(&ev_[0], cudaEventDisableTiming));
     SF_CK(cudaEventCreateWithFlags(&ev_[1], cudaEventDisableTiming));
     SF_CK(cudaEventCreate(&t0_));
@@ -457,7 +470,7 @@ class simulation {
       const auto& L = lay_[b];
       const i64 lo[3] = {0, 0, 0};
       const i64 dims[3] = {L.dims[0], L.dims[1], L.dims[2]};
-      launch_fill_box(htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, lo, dims, v, st_);
+      launch_fill_box(htab_->ptr[b][f][FRONT], L.base, L.sx, L.sy, lo, dims, v, st_, fes_[f]);
       ++launches_;
     }
     check_launch();
@@ -802,6 +815,9 @@ class simulation {
     for (const auto& p : cfd_plans())
       if (p.name == name) kp = &p;
     if (!kp) throw error(SF_ERR_EXEC, "unknown kernel '" + name + "'");
+    if (cfd_es_ != 8)
+      throw error(SF_ERR_ARG, "kernel '" + name + "': the single CFD kernels are fp64; an fp32 simulation runs them "
+                              "fused inside step() / provisional() / pressure_iteration()");
     std::vector<double> pv;
     for (const auto& pn : kp->params) {
       auto it = params.find(pn);
@@ -1358,9 +1374,10 @@ class simulation {
 
   void provisional_device() {
     refresh({SF_VX, SF_VY, SF_VZ, SF_P});
+    if (cfd_es_ != 8 && !(uvmaps_ && uv_tma_env_)) throw error(SF_ERR_ARG, "fp32 CFD fields need the TMA UPDATE_VELOCITY");
     if (uvmaps_ && uv_tma_env_) {
       const work_set& ws = items_for(SF_REGION_ALL, {1, 1, 1, 1, 1, 1}, zc_fused_, kTX, kTY);
-      launch_update_velocity_tma(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, uvmaps_, st_);
+      launch_update_velocity_tma(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, uvmaps_, st_, cfd_es_);
     } else {
       const work_set& ws = items_for(SF_REGION_ALL, {1, 1, 1, 1, 1, 1}, zc_uv_);
       launch_update_velocity(tview(ws), ws.nctas, zc_uv_, consts_, dctl_, 0.0, st_);
@@ -1440,7 +1457,7 @@ class simulation {
   std::pair<int, double> pressure_iteration_device() {
     refresh({SF_VX, SF_VY, SF_VZ});
     const work_set& wd = items_for(SF_REGION_ALL, {1, 0, 1, 0, 1, 0}, zc_plain_);
-    launch_divergence(tview(wd), wd.nctas, zc_plain_, consts_, dctl_, -1, 0, st_);
+    launch_divergence(tview(wd), wd.nctas, zc_plain_, consts_, dctl_, -1, 0, st_, cfd_es_);
     ++launches_;
     check_launch();
     if (opt_.fused) refresh({SF_DIVU});
@@ -1553,7 +1570,7 @@ class simulation {
     refresh({SF_VX, SF_VY, SF_VZ});
     ctl(CTL_CLEAR_ACC);
     const work_set& wd = items_for(SF_REGION_ALL, {1, 0, 1, 0, 1, 0}, zc_plain_);
-    launch_divergence(tview(wd), wd.nctas, zc_plain_, consts_, dctl_, 7, 0, st_);
+    launch_divergence(tview(wd), wd.nctas, zc_plain_, consts_, dctl_, 7, 0, st_, cfd_es_);
     ++launches_;
     check_launch();
     allreduce_max(&dctl_->acc[7], 1);
@@ -1587,6 +1604,7 @@ class simulation {
   // host sums them in the reference's order (x-fastest within a worker,
   // workers in order), so the result is bitwise the reference's.
   double taylor_green_error(double t) {
+    if (cfd_es_ != 8) throw error(SF_ERR_ARG, "taylor_green_error needs fp64 CFD fields");
     const double tau = 2.0 * 3.14159265358979323846;
     const double decay = std::exp(-2.0 * par_.viscosity * tau * tau * t);
     const double dx = cfg_.spacing[0], dy = cfg_.spacing[1];
@@ -1698,6 +1716,7 @@ class simulation {
   std::vector<int> fstag_ = {0, 1, 2, -1, -1};  // stagger per field (field.hpp:23)
   std::vector<int> fes_ = {8, 8, 8, 8, 8};       // bytes per value per field (user fields: 8 or 4)
   int rank_ = 0, world_ = 1;
+  int cfd_es_ = 8;     // bytes per value of the five CFD fields (4: the fp32 variant)
   bool dist_ = false;  // NCCL transport (one grid component per rank)
   decomposition dec_;
   int nloc_ = 0;
@@ -1898,6 +1917,7 @@ class simulation {
     for (int f = 0; f < kMaxFields; ++f) htab_->esize[f] = 8;
     std::memset(htab_.get(), 0, sizeof(sf_dev_table));
     htab_->nblocks = nloc_;
+    for (int f = 0; f < SF_NFIELDS; ++f) htab_->esize[f] = (unsigned char)cfd_es_;
     lay_.resize(nloc_);
     for (int b = 0; b < nloc_; ++b) {
       const int gw = gid_[b];
@@ -1952,7 +1972,7 @@ class simulation {
             double* p = htab_->ptr[b][f][s];
             if (!p) continue;
             const sf_layout& L = lay_[b];
-            ok = encode_sweep_map(hm.data() + sweep_map_offset(b, f, s), p, L.sx, L.sy, L.sz, f) == 0;
+            ok = encode_sweep_map(hm.data() + sweep_map_offset(b, f, s), p, L.sx, L.sy, L.sz, f, fes_[f]) == 0;
           }
       if (ok) {
         maps_ = dalloc(hm.size());
@@ -1971,17 +1991,17 @@ class simulation {
             if (!p) continue;
             const sf_layout& L = lay_[b];
             int bw, bh;
-            uv_box(uvf[k], &bw, &bh);
+            uv_box(uvf[k], &bw, &bh, fes_[uvf[k]]);
             ok = bw <= L.sx && bh <= L.sy &&
-                 encode_box_map(hm.data() + uv_map_offset(b, k, s), p, L.sx, L.sy, L.sz, bw, bh) == 0;
+                 encode_box_map(hm.data() + uv_map_offset(b, k, s), p, L.sx, L.sy, L.sz, bw, bh, fes_[uvf[k]]) == 0;
           }
       if (ok) {
         uvmaps_ = dalloc(hm.size());
         SF_CK(cudaMemcpy(uvmaps_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
       }
     }
-    // descriptors of the temporal pass (halo'd boxes)
-    if (maps_) {
+    // descriptors of the temporal pass (halo'd boxes; fp64 only)
+    if (maps_ && cfd_es_ == 8) {
       std::vector<unsigned char> hm(sweep2_maps_bytes(), 0);
       bool ok = true;
       for (int b = 0; b < nloc_ && ok; ++b)
@@ -2599,7 +2619,7 @@ class simulation {
   // (sf_sweep2.cu; scripts/probes/parity_stress.py found the unwrapped
   // version wrong on 39x43x13, periodic y, two components, ghost 2).
   bool temporal() const {
-    if (!maps2_ || !temporal_env_ || opt_.fused != 1) return false;
+    if (!maps2_ || !temporal_env_ || opt_.fused != 1 || cfd_es_ != 8) return false;
     for (int b = 0; b < nloc_; ++b)  // the pass addresses its arrays with 32-bit element offsets
       if ((unsigned long long)(lay_[b].sx * lay_[b].sy * lay_[b].sz) >= (1ull << 32)) return false;
     bool proc = false;
@@ -2635,7 +2655,8 @@ class simulation {
   // ghost itself, when the grid is small enough that launches dominate
   // (SF_PERSIST=0 off, =1 whenever it applies).
   bool persistent() {
-    if (persist_env_ == 0 || dist_ || timing_ || !opt_.fused || nloc_ != 1 || has_proc_faces()) return false;
+    if (persist_env_ == 0 || dist_ || timing_ || !opt_.fused || nloc_ != 1 || has_proc_faces() || cfd_es_ != 8)
+      return false;
     if (pressure_loop_ctas() < 1) return false;  // no co-resident CTA (occupancy query failed)
     const phase& ph = phase_for(1u << SF_DIVU, -1, SF_SCOPE_ALL, true);
     if (ph.first.n || ph.unpack.n || !ph.sends.empty() || !ph.recvs.empty()) return false;
@@ -2738,7 +2759,7 @@ class simulation {
       // ranks the residual first needs the max over ranks
       const int fin = dist_ ? 0 : 1;
       if (tma_sweep())
-        launch_sweep_div_tma(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, fin, st_);
+        launch_sweep_div_tma(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, fin, st_, cfd_es_);
       else
         launch_sweep_div(tview(ws), ws.nctas, zc_fused_, consts_, dctl_, loop_flag(), fin, st_);
       ++launches_;
@@ -3087,6 +3108,7 @@ void sf_sim_options_default(sf_sim_options* o) {
   o->form = 0;
   o->device = 0;
   o->fused = 1;
+  o->precision = 8;
 }
 
 int sf_sim_create(const sf_solver_config* cfg, const sf_fluid_params* par,

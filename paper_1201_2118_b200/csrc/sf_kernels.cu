@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kTX* kTY) k_update_vel(View vw, int zc, sf_con
       };
       const ldg_acc A{U, V, W, Q, o, sx, sxy};
       double r[3];
-      uv_point<ldg_acc, BLEND>(A, s, dt, r);
+      uv_point<ldg_acc, BLEND>(A, uv_consts<double>(s), dt, r);
       Uo[o] = r[0];
       Vo[o] = r[1];
       Wo[o] = r[2];
@@ -323,27 +323,29 @@ template void launch_update_velocity<direct_view>(const direct_view&, int, int, 
 // ---------------------------------------------------------------------------
 // DIVERGENCE (cfd.hpp:595-618) with max|divu| into acc[acc_slot]
 // ---------------------------------------------------------------------------
-template <class View>
+// T = float: the fp32 variant of the CFD fields
+template <class View, class T>
 __global__ void __launch_bounds__(kTX* kTY) k_divergence(View vw, int zc, sf_consts s,
                                                          sf_dev_ctl* ctl, int acc_slot,
                                                          int predicated) {
   if (predicated && pred_done(ctl)) return;
   const tile_loc t = locate(vw.work(), vw.nitems, zc);
   const sf_dev_block& B = vw.blk(t.blk);
-  const double* __restrict__ U = vw.ptr(t.blk, SF_VX, FRONT);
-  const double* __restrict__ V = vw.ptr(t.blk, SF_VY, FRONT);
-  const double* __restrict__ W = vw.ptr(t.blk, SF_VZ, FRONT);
-  double* __restrict__ D = vw.ptr(t.blk, SF_DIVU, FRONT);
+  const T* __restrict__ U = reinterpret_cast<const T*>(vw.ptr(t.blk, SF_VX, FRONT));
+  const T* __restrict__ V = reinterpret_cast<const T*>(vw.ptr(t.blk, SF_VY, FRONT));
+  const T* __restrict__ W = reinterpret_cast<const T*>(vw.ptr(t.blk, SF_VZ, FRONT));
+  T* __restrict__ D = reinterpret_cast<T*>(vw.ptr(t.blk, SF_DIVU, FRONT));
+  const T ix = (T)s.ix, iy = (T)s.iy, iz = (T)s.iz;
   const long long sx = B.sx, sxy = B.sx * B.sy;
   unsigned long long mx[1] = {0ull};
   if (t.act) {
     for (long long k = t.k0; k < t.k1; ++k) {
       const long long o = off(B, t.i, t.j, k);
-      double d = (__ldg(U + o) - __ldg(U + o - 1)) * s.ix;
-      d += (__ldg(V + o) - __ldg(V + o - sx)) * s.iy;
-      d += (__ldg(W + o) - __ldg(W + o - sxy)) * s.iz;
+      T d = (__ldg(U + o) - __ldg(U + o - 1)) * ix;
+      d += (__ldg(V + o) - __ldg(V + o - sx)) * iy;
+      d += (__ldg(W + o) - __ldg(W + o - sxy)) * iz;
       D[o] = d;
-      const unsigned long long bb = abs_bits(d);
+      const unsigned long long bb = abs_bits((double)d);
       mx[0] = bb > mx[0] ? bb : mx[0];
     }
   }
@@ -352,14 +354,17 @@ __global__ void __launch_bounds__(kTX* kTY) k_divergence(View vw, int zc, sf_con
 
 template <class View>
 void launch_divergence(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                       int acc_slot, int predicated, cudaStream_t st) {
+                       int acc_slot, int predicated, cudaStream_t st, int es) {
   if (nctas <= 0) return;
-  k_divergence<View><<<nctas, dim3(kTX, kTY), 0, st>>>(vw, zc, c, ctl, acc_slot, predicated);
+  if (es == 4)
+    k_divergence<View, float><<<nctas, dim3(kTX, kTY), 0, st>>>(vw, zc, c, ctl, acc_slot, predicated);
+  else
+    k_divergence<View, double><<<nctas, dim3(kTX, kTY), 0, st>>>(vw, zc, c, ctl, acc_slot, predicated);
 }
 template void launch_divergence<table_view>(const table_view&, int, int, const sf_consts&,
-                                            sf_dev_ctl*, int, int, cudaStream_t);
+                                            sf_dev_ctl*, int, int, cudaStream_t, int);
 template void launch_divergence<direct_view>(const direct_view&, int, int, const sf_consts&,
-                                             sf_dev_ctl*, int, int, cudaStream_t);
+                                             sf_dev_ctl*, int, int, cudaStream_t, int);
 
 // ---------------------------------------------------------------------------
 // PRESSURE_SWEEP (cfd.hpp:699-720), in place on p, vx, vy, vz
@@ -1239,9 +1244,10 @@ void launch_copy_box(const double* src, long long s_base, long long s_sx, long l
   launch_copy_box_es(src, 8, s_base, s_sx, s_sy, dst, 8, d_base, d_sx, d_sy, lo, dims, dlo, st);
 }
 
-__global__ void k_fill_box(double* __restrict__ dst, long long base, long long sx, long long sy,
+template <class T>
+__global__ void k_fill_box(T* __restrict__ dst, long long base, long long sx, long long sy,
                            long long l0, long long l1, long long l2, long long n0, long long n1,
-                           long long n2, double v) {
+                           long long n2, T v) {
   const long long total = n0 * n1 * n2;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
@@ -1250,14 +1256,18 @@ __global__ void k_fill_box(double* __restrict__ dst, long long base, long long s
   }
 }
 
-void launch_fill_box(double* dst, long long base, long long sx, long long sy, const long long lo[3],
-                     const long long dims[3], double v, cudaStream_t st) {
+void launch_fill_box(void* dst, long long base, long long sx, long long sy, const long long lo[3],
+                     const long long dims[3], double v, cudaStream_t st, int es) {
   const long long total = dims[0] * dims[1] * dims[2];
   if (total <= 0) return;
   long long nb = (total + 255) / 256;
   if (nb > 148 * 16) nb = 148 * 16;
-  k_fill_box<<<(unsigned)nb, 256, 0, st>>>(dst, base, sx, sy, lo[0], lo[1], lo[2], dims[0],
-                                            dims[1], dims[2], v);
+  if (es == 4)
+    k_fill_box<float><<<(unsigned)nb, 256, 0, st>>>(static_cast<float*>(dst), base, sx, sy, lo[0], lo[1], lo[2],
+                                                    dims[0], dims[1], dims[2], (float)v);
+  else
+    k_fill_box<double><<<(unsigned)nb, 256, 0, st>>>(static_cast<double*>(dst), base, sx, sy, lo[0], lo[1], lo[2],
+                                                     dims[0], dims[1], dims[2], v);
 }
 
 // owned cells <-> a global x-fastest array (grid::gather / scatter, io.hpp:25-65)

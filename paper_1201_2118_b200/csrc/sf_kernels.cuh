@@ -44,13 +44,13 @@ void launch_update_velocity(const View& vw, int nctas, int zc, const sf_consts& 
 // TMA-staged UPDATE_VELOCITY (sf_uv_tma.cu): table view, 32 x 8 tiles;
 // maps = device table of uv descriptors (uv_box shapes).
 void launch_update_velocity_tma(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                                const void* maps, cudaStream_t st);
+                                const void* maps, cudaStream_t st, int es = 8);
 size_t uv_maps_bytes();
 size_t uv_map_offset(int b, int f, int s);  // f: 0 vx, 1 vy, 2 vz, 3 p
-void uv_box(int field, int* bw, int* bh);
+void uv_box(int field, int* bw, int* bh, int es = 8);
 template <class View>
 void launch_divergence(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                       int acc_slot, int predicated, cudaStream_t st);
+                       int acc_slot, int predicated, cudaStream_t st, int es = 8);
 // beta_color_dt: null = beta, colour and dt from ctl; else {beta, colour, dt}
 template <class View>
 void launch_pressure_sweep(const View& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
@@ -66,9 +66,10 @@ cudaError_t launch_pressure_loop(const table_view& vw, int ntiles, int zc, const
                                  cudaStream_t st);
 int pressure_loop_ctas();
 // TMA-pipelined fused half-sweep (sf_sweep_tma.cu); maps = device sweep_maps.
+// es = 4: the fp32 variant of the CFD fields (storage and arithmetic in fp32).
 void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_consts& c,
                           sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,
-                          cudaStream_t st);
+                          cudaStream_t st, int es = 8);
 // Temporal pass: two half-sweeps per launch (sf_sweep2.cu). Blocks whose
 // faces are walls, symmetry planes or processor faces (ghost width >= 2 when
 // there are processor faces); maps = device table of sweep2 descriptors.
@@ -87,7 +88,7 @@ size_t sweep2_maps_bytes();
 size_t sweep2_map_offset(int b, int f, int s);
 void sweep2_box(int field, int* bw, int* bh);
 int sweep2_tile_y();  // tile height of the selected temporal-pass variant (tile width 32)
-int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field);
+int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field, int es = 8);
 size_t sweep_maps_bytes();
 int encode_box_map(void* map_out, double* base, long long sx, long long sy, long long sz, int bw, int bh,
                    int es = 8);
@@ -127,8 +128,8 @@ void launch_copy_box(const double* src, long long s_base, long long s_sx, long l
                      double* dst, long long d_base, long long d_sx, long long d_sy,
                      const long long lo[3], const long long dims[3], const long long dlo[3],
                      cudaStream_t st);
-void launch_fill_box(double* dst, long long base, long long sx, long long sy, const long long lo[3],
-                     const long long dims[3], double v, cudaStream_t st);
+void launch_fill_box(void* dst, long long base, long long sx, long long sy, const long long lo[3],
+                     const long long dims[3], double v, cudaStream_t st, int es = 8);
 // taylor_green_error's per-cell term (cfd.hpp:388-393) of one block into a
 // dense x-fastest buffer; su / sv: the analytic sin*cos factors per (i, j)
 void launch_tg_cells(const double* U, const double* V, const double* W, long long base, long long sx, long long sy,

@@ -61,27 +61,30 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 // ---------------------------------------------------------------------------
 // stage layout (every TMA destination 128-byte aligned)
 // ---------------------------------------------------------------------------
-// On B200 a TMA tile load of 8-byte elements must START on a 16-byte aligned
-// inner coordinate (an odd x start raises "illegal instruction"; measured with
-// scripts/probes/tma_probe2.cu), so the x halo boxes begin two cells left of
-// the tile: divu covers x in [i0-2, i0+34), vx covers [i0-2, i0+32).
-constexpr int kXL = 2;  // cells left of the tile in the x-halo boxes
-
+// On B200 a TMA tile load must START on a 16-byte aligned inner coordinate
+// (an odd fp64 x start raises "illegal instruction"; measured with
+// scripts/probes/tma_probe2.cu), so the x halo boxes begin kXL = 16 / sizeof(T)
+// cells left of the tile (2 fp64, 4 fp32): for fp64 divu covers x in
+// [i0-2, i0+34), vx covers [i0-2, i0+32).
+//
 // Shared-memory stage of one z plane for a TX x TY tile (every TMA
-// destination 128-byte aligned):
-//   divu (TX+4) x (TY+2), vx (TX+2) x TY, vy TX x (TY+1), p and vz TX x TY
-template <int TX, int TY>
+// destination 128-byte aligned), element type T (fp64, or fp32 for the fp32
+// variant of the CFD fields):
+//   divu (TX+2kXL) x (TY+2), vx (TX+kXL) x TY, vy TX x (TY+1), p and vz TX x TY
+template <int TX, int TY, class T = double>
 struct tile {
-  static constexpr int DW = TX + 4, DH = TY + 2, UW = TX + 2, VH = TY + 1;
+  static constexpr int ES = (int)sizeof(T), kXL = 16 / ES;
+  static constexpr int DW = TX + 2 * kXL, DH = TY + 2, UW = TX + kXL, VH = TY + 1;
   static constexpr int r128(int b) { return (b + 127) / 128 * 128; }
   static constexpr int OFF_D = 0;
-  static constexpr int OFF_U = r128(8 * DH * DW);
-  static constexpr int OFF_V = OFF_U + r128(8 * TY * UW);
-  static constexpr int OFF_P = OFF_V + r128(8 * VH * TX);
-  static constexpr int OFF_W = OFF_P + r128(8 * TY * TX);
-  static constexpr int BYTES = OFF_W + r128(8 * TY * TX);
-  static constexpr uint32_t TXB = 8u * (DH * DW + TY * UW + VH * TX + 2 * TY * TX);
-  static_assert((UW * 8) % 16 == 0 && (DW * 8) % 16 == 0, "TMA rows must be 16-byte multiples");
+  static constexpr int OFF_U = r128(ES * DH * DW);
+  static constexpr int OFF_V = OFF_U + r128(ES * TY * UW);
+  static constexpr int OFF_P = OFF_V + r128(ES * VH * TX);
+  static constexpr int OFF_W = OFF_P + r128(ES * TY * TX);
+  static constexpr int BYTES = OFF_W + r128(ES * TY * TX);
+  static constexpr uint32_t TXB = (uint32_t)ES * (DH * DW + TY * UW + VH * TX + 2 * TY * TX);
+  static_assert((UW * ES) % 16 == 0 && (DW * ES) % 16 == 0 && (TX * ES) % 16 == 0,
+                "TMA rows must be 16-byte multiples");
 };
 
 struct sweep_maps {  // per block: [field][physical buffer]
@@ -92,13 +95,14 @@ struct sweep_maps {  // per block: [field][physical buffer]
 // (Measured alternatives -- a warp-specialised TMA producer, 2-8 stages,
 // 64x4 / 128x2 tiles, streaming stores, evict-first loads -- were all slower;
 // DESIGN.md §4.)
-template <int STAGES, int MINB, int TX, int TY>
+template <int STAGES, int MINB, int TX, int TY, class T>
 __global__ void __launch_bounds__(TX* TY, MINB)
     k_sweep_div_tma(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems,
                     int zc, sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag,
                     unsigned int total_ctas, const sweep_maps* __restrict__ maps, int finalize) {
   constexpr int kStages = STAGES;
-  using TL = tile<TX, TY>;
+  using TL = tile<TX, TY, T>;
+  constexpr int kXL = TL::kXL;
   // finalize 2: redo of a temporal pass's first sweep (sf_sweep2.cu), runs
   // only when that pass flagged it
   if (finalize == 2) {
@@ -107,9 +111,9 @@ __global__ void __launch_bounds__(TX* TY, MINB)
     return;
   }
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  auto sptr = [&](int st, int off) { return reinterpret_cast<double*>(smem_raw + st * TL::BYTES + off); };
+  auto sptr = [&](int st, int off) { return reinterpret_cast<T*>(smem_raw + st * TL::BYTES + off); };
   __shared__ __align__(8) uint64_t bars[kStages];
-  __shared__ double smb[8];
+  __shared__ T smb[8];
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * TX + tx;
@@ -130,6 +134,7 @@ __global__ void __launch_bounds__(TX* TY, MINB)
   const sf_dev_block& B = tab->blk[b];
 
   const double beta = ctl->beta, dt = ctl->dt;
+  const T Tix = (T)s.ix, Tiy = (T)s.iy, Tiz = (T)s.iz;
   const int color = finalize == 2 ? (ctl->color ^ 1) : ctl->color;
   if (tid == 0) {
 #pragma unroll
@@ -144,7 +149,7 @@ __global__ void __launch_bounds__(TX* TY, MINB)
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       if (q == tid) sc = s.bscale[q >> 2][(q >> 1) & 1][q & 1];
-    smb[tid] = -(beta * sc);
+    smb[tid] = (T)(-(beta * sc));
   }
   __syncthreads();
 
@@ -170,14 +175,14 @@ __global__ void __launch_bounds__(TX* TY, MINB)
     for (int q = 0; q < npro; ++q) issue(q, q);
   }
 
-  double* __restrict__ Dn = tab->ptr[b][SF_DIVU][ALT];
-  double* __restrict__ P = tab->ptr[b][SF_P][FRONT];
-  double* __restrict__ Un = tab->ptr[b][SF_VX][ALT];
-  double* __restrict__ Vn = tab->ptr[b][SF_VY][ALT];
-  double* __restrict__ Wn = tab->ptr[b][SF_VZ][ALT];
-  const double* __restrict__ D = tab->ptr[b][SF_DIVU][FRONT];
-  const double* __restrict__ W = tab->ptr[b][SF_VZ][FRONT];
-  const double cu = dt * s.ix, cv = dt * s.iy, cw = dt * s.iz;
+  T* __restrict__ Dn = reinterpret_cast<T*>(tab->ptr[b][SF_DIVU][ALT]);
+  T* __restrict__ P = reinterpret_cast<T*>(tab->ptr[b][SF_P][FRONT]);
+  T* __restrict__ Un = reinterpret_cast<T*>(tab->ptr[b][SF_VX][ALT]);
+  T* __restrict__ Vn = reinterpret_cast<T*>(tab->ptr[b][SF_VY][ALT]);
+  T* __restrict__ Wn = reinterpret_cast<T*>(tab->ptr[b][SF_VZ][ALT]);
+  const T* __restrict__ D = reinterpret_cast<T*>(tab->ptr[b][SF_DIVU][FRONT]);
+  const T* __restrict__ W = reinterpret_cast<T*>(tab->ptr[b][SF_VZ][FRONT]);
+  const T cu = (T)(dt * Tix), cv = (T)(dt * Tiy), cw = (T)(dt * Tiz);
 
   const long long i = i0 + tx, j = j0 + ty;
   const bool act = i < wk.hi[0] && j < wk.hi[1];
@@ -202,9 +207,9 @@ __global__ void __launch_bounds__(TX* TY, MINB)
   const bool pin_u = (fxh == FACE_WALL || fxh == FACE_SYM) && i == n0 - 1;
   const bool pin_v = (fyh == FACE_WALL || fyh == FACE_SYM) && j == n1 - 1;
   const bool pin_w = (fzh == FACE_WALL || fzh == FACE_SYM);
-  const double pv_u = fxh == FACE_WALL ? B.fvel[1][0] : 0.0;
-  const double pv_v = fyh == FACE_WALL ? B.fvel[3][1] : 0.0;
-  const double pv_w = fzh == FACE_WALL ? B.fvel[5][2] : 0.0;
+  const T pv_u = fxh == FACE_WALL ? B.fvel[1][0] : 0.0;
+  const T pv_v = fyh == FACE_WALL ? B.fvel[3][1] : 0.0;
+  const T pv_w = fzh == FACE_WALL ? B.fvel[5][2] : 0.0;
   const bool xm_swept = i > 0 || fxl == FACE_PROC || fxl == FACE_SELF;
   const bool ym_swept = j > 0 || fyl == FACE_PROC || fyl == FACE_SELF;
   // Interior column: every x/y scale bit of the cell and of its -x/-y
@@ -215,23 +220,23 @@ __global__ void __launch_bounds__(TX* TY, MINB)
   // general path restricted to such cells.
   const bool col_fast = i >= 1 && i <= n0 - 2 && j >= 1 && j <= n1 - 2 && bx && bxp && bxm &&
                         bxpm && by && byp && bym && bypm;
-  const double mbI = smb[7];  // -(beta * bscale[1][1][1])
+  const T mbI = smb[7];  // -(beta * bscale[1][1][1])
   const int zlo_fast = (int)max(1ll, (per2 ? 0ll : 1ll) - B.lo[2]);  // local k range of the fast path
   const int zhi_fast = (int)min(n2 - 2, (per2 ? n2 - 2 : s.nm1[2] - 2 - B.lo[2]));
   const int par_col = (int)((gi + gj) & 1);
 
   long long o = off(B, i, j, k0);
   unsigned long long rmax = 0ull;
-  double wm_new = 0.0;
+  T wm_new = 0.0;
   if (act) {  // swept w of the cell below the chunk (carried while marching)
     const long long gk = B.lo[2] + k0;
-    const double dC0 = D[o];
+    const T dC0 = D[o];
     if (k0 > 0 || fzl == FACE_PROC || fzl == FACE_SELF) {
       const long long gkm = k0 > 0 ? gk - 1 : B.nb_ghost_gidx[4];
       const int bzm = bin(per2, gkm, s.nm1[2]), bzpm = bnx(per2, gkm, s.nm1[2]);
-      const double a0m = (((gi + gj + gkm) & 1) == color) ? 1.0 : 0.0, a1m = 1.0 - a0m;
-      const double d0m = smb[ic | bzm] * D[o - sxy] * a0m;
-      const double ezm = smb[ic | bzpm] * dC0 * a1m;
+      const T a0m = (((gi + gj + gkm) & 1) == color) ? 1.0 : 0.0, a1m = 1.0 - a0m;
+      const T d0m = smb[ic | bzm] * D[o - sxy] * a0m;
+      const T ezm = smb[ic | bzpm] * dC0 * a1m;
       wm_new = W[o - sxy] + cw * (d0m - ezm);
     } else {
       wm_new = W[o - sxy];
@@ -246,94 +251,94 @@ __global__ void __launch_bounds__(TX* TY, MINB)
     if (has_next) mbar_wait(&bars[st1], (uint32_t)(((kk + 1) / kStages) & 1));
     const int kl = (int)(k0 + kk);
     if (act && col_fast && kl >= zlo_fast && kl <= zhi_fast) {
-      const double* Td = sptr(st, TL::OFF_D);
-      const double* Tu = sptr(st, TL::OFF_U);
-      const double* Tv = sptr(st, TL::OFF_V);
-      const double* Tp = sptr(st, TL::OFF_P);
-      const double* Tw = sptr(st, TL::OFF_W);
-      const double dC = Td[(ty + 1) * TL::DW + (tx + kXL)];
-      const double dXp = Td[(ty + 1) * TL::DW + (tx + kXL + 1)], dXm = Td[(ty + 1) * TL::DW + (tx + kXL - 1)];
-      const double dYp = Td[(ty + 2) * TL::DW + (tx + kXL)], dYm = Td[(ty) * TL::DW + (tx + kXL)];
-      const double dZp = has_next ? sptr(st1, TL::OFF_D)[(ty + 1) * TL::DW + (tx + kXL)] : D[o + sxy];
-      const double p0 = Tp[(ty) * TX + (tx)], u0 = Tu[(ty) * TL::UW + (tx + kXL)], uml = Tu[(ty) * TL::UW + (tx + kXL - 1)];
-      const double v0 = Tv[(ty + 1) * TX + (tx)], vml = Tv[(ty) * TX + (tx)], w0 = Tw[(ty) * TX + (tx)];
+      const T* Td = sptr(st, TL::OFF_D);
+      const T* Tu = sptr(st, TL::OFF_U);
+      const T* Tv = sptr(st, TL::OFF_V);
+      const T* Tp = sptr(st, TL::OFF_P);
+      const T* Tw = sptr(st, TL::OFF_W);
+      const T dC = Td[(ty + 1) * TL::DW + (tx + kXL)];
+      const T dXp = Td[(ty + 1) * TL::DW + (tx + kXL + 1)], dXm = Td[(ty + 1) * TL::DW + (tx + kXL - 1)];
+      const T dYp = Td[(ty + 2) * TL::DW + (tx + kXL)], dYm = Td[(ty) * TL::DW + (tx + kXL)];
+      const T dZp = has_next ? sptr(st1, TL::OFF_D)[(ty + 1) * TL::DW + (tx + kXL)] : D[o + sxy];
+      const T p0 = Tp[(ty) * TX + (tx)], u0 = Tu[(ty) * TL::UW + (tx + kXL)], uml = Tu[(ty) * TL::UW + (tx + kXL - 1)];
+      const T v0 = Tv[(ty + 1) * TX + (tx)], vml = Tv[(ty) * TX + (tx)], w0 = Tw[(ty) * TX + (tx)];
       const int par = par_col ^ ((int)(B.lo[2] + kl) & 1);
-      const double a0 = (par == color) ? 1.0 : 0.0, a1 = 1.0 - a0;
-      const double d0 = mbI * dC * a0;
-      const double ex = mbI * dXp * a1;
-      const double ey = mbI * dYp * a1;
-      const double ez = mbI * dZp * a1;
-      const double pn = p0 + d0;
-      const double un = u0 + cu * (d0 - ex);
-      const double vn = v0 + cv * (d0 - ey);
-      const double wn = w0 + cw * (d0 - ez);
+      const T a0 = (par == color) ? 1.0 : 0.0, a1 = 1.0 - a0;
+      const T d0 = mbI * dC * a0;
+      const T ex = mbI * dXp * a1;
+      const T ey = mbI * dYp * a1;
+      const T ez = mbI * dZp * a1;
+      const T pn = p0 + d0;
+      const T un = u0 + cu * (d0 - ex);
+      const T vn = v0 + cv * (d0 - ey);
+      const T wn = w0 + cw * (d0 - ez);
       // -x / -y neighbours: parity a1, their +x/+y term is mbI*dC*a0 == d0
-      const double umn = uml + cu * (mbI * dXm * a1 - d0);
-      const double vmn = vml + cv * (mbI * dYm * a1 - d0);
-      double dd = (un - umn) * s.ix;
-      dd += (vn - vmn) * s.iy;
-      dd += (wn - wm_new) * s.iz;
+      const T umn = uml + cu * (mbI * dXm * a1 - d0);
+      const T vmn = vml + cv * (mbI * dYm * a1 - d0);
+      T dd = (un - umn) * Tix;
+      dd += (vn - vmn) * Tiy;
+      dd += (wn - wm_new) * Tiz;
       P[o] = pn;
       Un[o] = un;
       Vn[o] = vn;
       Wn[o] = wn;
       Dn[o] = dd;
-      const unsigned long long bb = abs_bits(dd);
+      const unsigned long long bb = abs_bits((double)dd);
       rmax = bb > rmax ? bb : rmax;
       wm_new = wn;
     } else if (act) {
-      const double* Td = sptr(st, TL::OFF_D);
-      const double* Tu = sptr(st, TL::OFF_U);
-      const double* Tv = sptr(st, TL::OFF_V);
-      const double* Tp = sptr(st, TL::OFF_P);
-      const double* Tw = sptr(st, TL::OFF_W);
+      const T* Td = sptr(st, TL::OFF_D);
+      const T* Tu = sptr(st, TL::OFF_U);
+      const T* Tv = sptr(st, TL::OFF_V);
+      const T* Tp = sptr(st, TL::OFF_P);
+      const T* Tw = sptr(st, TL::OFF_W);
       const long long k = k0 + kk;
       const long long gk = B.lo[2] + k;
       const int bz = bin(per2, gk, s.nm1[2]), bzp = bnx(per2, gk, s.nm1[2]);
-      const double dC = Td[(ty + 1) * TL::DW + (tx + kXL)];
-      const double dXp = Td[(ty + 1) * TL::DW + (tx + kXL + 1)], dXm = Td[(ty + 1) * TL::DW + (tx + kXL - 1)];
-      const double dYp = Td[(ty + 2) * TL::DW + (tx + kXL)], dYm = Td[(ty) * TL::DW + (tx + kXL)];
-      const double dZp = has_next ? sptr(st1, TL::OFF_D)[(ty + 1) * TL::DW + (tx + kXL)] : D[o + sxy];
-      const double p0 = Tp[(ty) * TX + (tx)], u0 = Tu[(ty) * TL::UW + (tx + kXL)], uml = Tu[(ty) * TL::UW + (tx + kXL - 1)];
-      const double v0 = Tv[(ty + 1) * TX + (tx)], vml = Tv[(ty) * TX + (tx)], w0 = Tw[(ty) * TX + (tx)];
-      const double a0 = (((gi + gj + gk) & 1) == color) ? 1.0 : 0.0, a1 = 1.0 - a0;
+      const T dC = Td[(ty + 1) * TL::DW + (tx + kXL)];
+      const T dXp = Td[(ty + 1) * TL::DW + (tx + kXL + 1)], dXm = Td[(ty + 1) * TL::DW + (tx + kXL - 1)];
+      const T dYp = Td[(ty + 2) * TL::DW + (tx + kXL)], dYm = Td[(ty) * TL::DW + (tx + kXL)];
+      const T dZp = has_next ? sptr(st1, TL::OFF_D)[(ty + 1) * TL::DW + (tx + kXL)] : D[o + sxy];
+      const T p0 = Tp[(ty) * TX + (tx)], u0 = Tu[(ty) * TL::UW + (tx + kXL)], uml = Tu[(ty) * TL::UW + (tx + kXL - 1)];
+      const T v0 = Tv[(ty + 1) * TX + (tx)], vml = Tv[(ty) * TX + (tx)], w0 = Tw[(ty) * TX + (tx)];
+      const T a0 = (((gi + gj + gk) & 1) == color) ? 1.0 : 0.0, a1 = 1.0 - a0;
       // this cell's sweep (cfd.hpp:712-719)
-      const double d0 = smb[ic | bz] * dC * a0;
-      const double ex = smb[iex | bz] * dXp * a1;
-      const double ey = smb[iey | bz] * dYp * a1;
-      const double ez = smb[ic | bzp] * dZp * a1;
+      const T d0 = smb[ic | bz] * dC * a0;
+      const T ex = smb[iex | bz] * dXp * a1;
+      const T ey = smb[iey | bz] * dYp * a1;
+      const T ez = smb[ic | bzp] * dZp * a1;
       P[o] = p0 + d0;
-      double un = u0 + cu * (d0 - ex);
-      double vn = v0 + cv * (d0 - ey);
-      double wn = w0 + cw * (d0 - ez);
+      T un = u0 + cu * (d0 - ex);
+      T vn = v0 + cv * (d0 - ey);
+      T wn = w0 + cw * (d0 - ez);
       if (pin_u) un = pv_u;
       if (pin_v) vn = pv_v;
       if (pin_w && k == n2 - 1) wn = pv_w;
       // swept -x / -y neighbours (the refreshed values DIVERGENCE reads)
-      double umn, vmn;
+      T umn, vmn;
       if (xm_swept) {
-        const double a0m = i > 0 ? a1 : ((((gim + gj + gk) & 1) == color) ? 1.0 : 0.0);
-        const double a1m = 1.0 - a0m;
-        const double d0m = smb[ixm | bz] * dXm * a0m;
-        const double exm = smb[ixpm | bz] * dC * a1m;
+        const T a0m = i > 0 ? a1 : ((((gim + gj + gk) & 1) == color) ? 1.0 : 0.0);
+        const T a1m = 1.0 - a0m;
+        const T d0m = smb[ixm | bz] * dXm * a0m;
+        const T exm = smb[ixpm | bz] * dC * a1m;
         umn = uml + cu * (d0m - exm);
       } else {
         umn = fxl == FACE_OUT ? un : uml;
       }
       if (ym_swept) {
-        const double a0m = j > 0 ? a1 : ((((gi + gjm + gk) & 1) == color) ? 1.0 : 0.0);
-        const double a1m = 1.0 - a0m;
-        const double d0m = smb[iym | bz] * dYm * a0m;
-        const double eym = smb[iypm | bz] * dC * a1m;
+        const T a0m = j > 0 ? a1 : ((((gi + gjm + gk) & 1) == color) ? 1.0 : 0.0);
+        const T a1m = 1.0 - a0m;
+        const T d0m = smb[iym | bz] * dYm * a0m;
+        const T eym = smb[iypm | bz] * dC * a1m;
         vmn = vml + cv * (d0m - eym);
       } else {
         vmn = fyl == FACE_OUT ? vn : vml;
       }
       if (k == 0 && fzl == FACE_OUT) wm_new = wn;
       // DIVERGENCE (cfd.hpp:605-608)
-      double dd = (un - umn) * s.ix;
-      dd += (vn - vmn) * s.iy;
-      dd += (wn - wm_new) * s.iz;
+      T dd = (un - umn) * Tix;
+      dd += (vn - vmn) * Tiy;
+      dd += (wn - wm_new) * Tiz;
       Un[o] = un;
       Vn[o] = vn;
       Wn[o] = wn;
@@ -365,7 +370,7 @@ __global__ void __launch_bounds__(TX* TY, MINB)
         if (fzh == FACE_WALL || fzh == FACE_SYM || fzh == FACE_OUT) Dn[o + sxy] = dd;
         if (fzl == FACE_SELF) Dn[o - n2 * sxy] = dd;
       }
-      const unsigned long long bb = abs_bits(dd);
+      const unsigned long long bb = abs_bits((double)dd);
       rmax = bb > rmax ? bb : rmax;
       wm_new = wn;
     }
@@ -451,28 +456,28 @@ void sweep_tile_shape(int* tx, int* ty) {
   *ty = kSweepTY;
 }
 
-// Box shape per field role (see tile<>).
-static void box_for(int field, cuuint32_t box[3]) {
-  int tx, ty;
-  sweep_tile_shape(&tx, &ty);
+// Box shape per field role (see tile<>); es = bytes per value.
+static void box_for(int field, cuuint32_t box[3], int es) {
+  const int tx = kSweepTX, ty = kSweepTY, xl = 16 / es;
   box[2] = 1;
   switch (field) {
-    case SF_DIVU: box[0] = tx + 4; box[1] = ty + 2; break;
-    case SF_VX: box[0] = tx + 2; box[1] = ty; break;
+    case SF_DIVU: box[0] = tx + 2 * xl; box[1] = ty + 2; break;
+    case SF_VX: box[0] = tx + xl; box[1] = ty; break;
     case SF_VY: box[0] = tx; box[1] = ty + 1; break;
     default: box[0] = tx; box[1] = ty; break;
   }
 }
 
-int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field) {
+int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field, int es) {
   auto fn = encode_fn();
   if (!fn) return 1;
   cuuint64_t gdim[3] = {(cuuint64_t)sx, (cuuint64_t)sy, (cuuint64_t)sz};
-  cuuint64_t gstride[2] = {(cuuint64_t)(sx * 8), (cuuint64_t)(sx * sy * 8)};
+  cuuint64_t gstride[2] = {(cuuint64_t)(sx * es), (cuuint64_t)(sx * sy * es)};
   cuuint32_t box[3];
-  box_for(field, box);
+  box_for(field, box, es);
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, gdim,
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(map_out),
+                  es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, gdim,
                   gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -500,16 +505,24 @@ size_t sweep_map_offset(int b, int f, int s) {
   return offsetof(sweep_maps, m) + sizeof(CUtensorMap) * ((size_t)(b * SF_NFIELDS + f) * kSlots + s);
 }
 
+template <class T>
+static void launch_sweep_tma_t(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                               sf_host_flag* hflag, const void* maps, int fin, cudaStream_t st) {
+  constexpr int S = kSweepStages, M = kSweepMinB, TX = kSweepTX, TY = kSweepTY;
+  const size_t smem = (size_t)tile<TX, TY, T>::BYTES * S;
+  auto k = k_sweep_div_tma<S, M, TX, TY, T>;
+  ensure_smem_attr((const void*)k, (int)smem);
+  k<<<nctas, dim3(TX, TY), smem, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag, (unsigned)nctas,
+                                       static_cast<const sweep_maps*>(maps), fin);
+}
 void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_consts& c,
                           sf_dev_ctl* ctl, sf_host_flag* hflag, const void* maps, int fin,
-                          cudaStream_t st) {
+                          cudaStream_t st, int es) {
   if (nctas <= 0) return;
-  constexpr int S = kSweepStages, M = kSweepMinB, TX = kSweepTX, TY = kSweepTY;
-  const size_t smem = (size_t)tile<TX, TY>::BYTES * S;
-  ensure_smem_attr((const void*)k_sweep_div_tma<S, M, TX, TY>, (int)smem);
-  k_sweep_div_tma<S, M, TX, TY><<<nctas, dim3(TX, TY), smem, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
-                                                                  (unsigned)nctas,
-                                                                  static_cast<const sweep_maps*>(maps), fin);
+  if (es == 4)
+    launch_sweep_tma_t<float>(vw, nctas, zc, c, ctl, hflag, maps, fin, st);
+  else
+    launch_sweep_tma_t<double>(vw, nctas, zc, c, ctl, hflag, maps, fin, st);
 }
 
 }  // namespace sfb

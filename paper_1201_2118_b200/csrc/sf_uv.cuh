@@ -19,70 +19,81 @@
 
 namespace sfb {
 
+// T = float is the fp32 variant of the CFD fields (storage and arithmetic in
+// fp32; constants rounded from the host's fp64 step constants).  For T =
+// double every expression is the reference's, operation for operation.
+template <class T>
+struct uv_consts {
+  T alpha, ix, iy, iz, ix2, iy2, iz2, nu, fx, fy, fz;
+  __device__ __forceinline__ explicit uv_consts(const sf_consts& c)
+      : alpha((T)c.alpha), ix((T)c.ix), iy((T)c.iy), iz((T)c.iz), ix2((T)c.ix2), iy2((T)c.iy2), iz2((T)c.iz2),
+        nu((T)c.nu), fx((T)c.fx), fy((T)c.fy), fz((T)c.fz) {}
+};
+
 // flux + alpha * X, X evaluated lazily (see above)
-#define SF_BLEND(f, X)                       \
-  do {                                       \
-    if (BLEND || f == 0.0) f += s.alpha * (X); \
+#define SF_BLEND(f, X)                            \
+  do {                                            \
+    if (BLEND || f == (T)0) f += s.alpha * (X);   \
   } while (0)
 
-template <class Acc, bool BLEND = true>
-__device__ __forceinline__ void uv_point(const Acc& A, const sf_consts& s, double dt, double out[3]) {
-  const double u0 = A.u(0, 0, 0), v0 = A.v(0, 0, 0), w0 = A.w(0, 0, 0);
+template <class Acc, bool BLEND = true, class T = double>
+__device__ __forceinline__ void uv_point(const Acc& A, const uv_consts<T>& s, T dt, T out[3]) {
+  const T u0 = A.u(0, 0, 0), v0 = A.v(0, 0, 0), w0 = A.w(0, 0, 0);
   {  // x momentum, at this cell's high x face
-    const double ue = A.u(1, 0, 0), uw = A.u(-1, 0, 0);
-    const double un = A.u(0, 1, 0), us = A.u(0, -1, 0);
-    const double ut = A.u(0, 0, 1), ub = A.u(0, 0, -1);
-    const double vn = A.v(0, 0, 0) + A.v(1, 0, 0), vs = A.v(0, -1, 0) + A.v(1, -1, 0);
-    const double wt = A.w(0, 0, 0) + A.w(1, 0, 0), wb = A.w(0, 0, -1) + A.w(1, 0, -1);
-    double fux = (u0 + ue) * (u0 + ue) - (uw + u0) * (uw + u0);
+    const T ue = A.u(1, 0, 0), uw = A.u(-1, 0, 0);
+    const T un = A.u(0, 1, 0), us = A.u(0, -1, 0);
+    const T ut = A.u(0, 0, 1), ub = A.u(0, 0, -1);
+    const T vn = A.v(0, 0, 0) + A.v(1, 0, 0), vs = A.v(0, -1, 0) + A.v(1, -1, 0);
+    const T wt = A.w(0, 0, 0) + A.w(1, 0, 0), wb = A.w(0, 0, -1) + A.w(1, 0, -1);
+    T fux = (u0 + ue) * (u0 + ue) - (uw + u0) * (uw + u0);
     SF_BLEND(fux, (fabs(u0 + ue) * (u0 - ue) - fabs(uw + u0) * (uw - u0)));
-    double fuy = vn * (u0 + un) - vs * (us + u0);
+    T fuy = vn * (u0 + un) - vs * (us + u0);
     SF_BLEND(fuy, (fabs(vn) * (u0 - un) - fabs(vs) * (us - u0)));
-    double fuz = wt * (u0 + ut) - wb * (ub + u0);
+    T fuz = wt * (u0 + ut) - wb * (ub + u0);
     SF_BLEND(fuz, (fabs(wt) * (u0 - ut) - fabs(wb) * (ub - u0)));
-    const double lapu = (ue - 2.0 * u0 + uw) * s.ix2 + (un - 2.0 * u0 + us) * s.iy2 +
-                        (ut - 2.0 * u0 + ub) * s.iz2;
-    const double rhsu = (A.q(0, 0, 0) - A.q(1, 0, 0)) * s.ix -
-                        0.25 * (fux * s.ix + fuy * s.iy + fuz * s.iz) + s.nu * lapu + s.fx;
-    const double r = u0 + dt * rhsu;
+    const T lapu = (ue - (T)2 * u0 + uw) * s.ix2 + (un - (T)2 * u0 + us) * s.iy2 +
+                        (ut - (T)2 * u0 + ub) * s.iz2;
+    const T rhsu = (A.q(0, 0, 0) - A.q(1, 0, 0)) * s.ix -
+                        (T)0.25 * (fux * s.ix + fuy * s.iy + fuz * s.iz) + s.nu * lapu + s.fx;
+    const T r = u0 + dt * rhsu;
     out[0] = r;
   }
   {  // y momentum, at the high y face
-    const double ve = A.v(1, 0, 0), vw = A.v(-1, 0, 0);
-    const double vnn = A.v(0, 1, 0), vss = A.v(0, -1, 0);
-    const double vt = A.v(0, 0, 1), vb = A.v(0, 0, -1);
-    const double ue2 = A.u(0, 0, 0) + A.u(0, 1, 0), uw2 = A.u(-1, 0, 0) + A.u(-1, 1, 0);
-    const double wt2 = A.w(0, 0, 0) + A.w(0, 1, 0), wb2 = A.w(0, 0, -1) + A.w(0, 1, -1);
-    double fvx = ue2 * (v0 + ve) - uw2 * (vw + v0);
+    const T ve = A.v(1, 0, 0), vw = A.v(-1, 0, 0);
+    const T vnn = A.v(0, 1, 0), vss = A.v(0, -1, 0);
+    const T vt = A.v(0, 0, 1), vb = A.v(0, 0, -1);
+    const T ue2 = A.u(0, 0, 0) + A.u(0, 1, 0), uw2 = A.u(-1, 0, 0) + A.u(-1, 1, 0);
+    const T wt2 = A.w(0, 0, 0) + A.w(0, 1, 0), wb2 = A.w(0, 0, -1) + A.w(0, 1, -1);
+    T fvx = ue2 * (v0 + ve) - uw2 * (vw + v0);
     SF_BLEND(fvx, (fabs(ue2) * (v0 - ve) - fabs(uw2) * (vw - v0)));
-    double fvy = (v0 + vnn) * (v0 + vnn) - (vss + v0) * (vss + v0);
+    T fvy = (v0 + vnn) * (v0 + vnn) - (vss + v0) * (vss + v0);
     SF_BLEND(fvy, (fabs(v0 + vnn) * (v0 - vnn) - fabs(vss + v0) * (vss - v0)));
-    double fvz = wt2 * (v0 + vt) - wb2 * (vb + v0);
+    T fvz = wt2 * (v0 + vt) - wb2 * (vb + v0);
     SF_BLEND(fvz, (fabs(wt2) * (v0 - vt) - fabs(wb2) * (vb - v0)));
-    const double lapv = (ve - 2.0 * v0 + vw) * s.ix2 + (vnn - 2.0 * v0 + vss) * s.iy2 +
-                        (vt - 2.0 * v0 + vb) * s.iz2;
-    const double rhsv = (A.q(0, 0, 0) - A.q(0, 1, 0)) * s.iy -
-                        0.25 * (fvx * s.ix + fvy * s.iy + fvz * s.iz) + s.nu * lapv + s.fy;
-    const double r = v0 + dt * rhsv;
+    const T lapv = (ve - (T)2 * v0 + vw) * s.ix2 + (vnn - (T)2 * v0 + vss) * s.iy2 +
+                        (vt - (T)2 * v0 + vb) * s.iz2;
+    const T rhsv = (A.q(0, 0, 0) - A.q(0, 1, 0)) * s.iy -
+                        (T)0.25 * (fvx * s.ix + fvy * s.iy + fvz * s.iz) + s.nu * lapv + s.fy;
+    const T r = v0 + dt * rhsv;
     out[1] = r;
   }
   {  // z momentum, at the high z face
-    const double we = A.w(1, 0, 0), ww = A.w(-1, 0, 0);
-    const double wn = A.w(0, 1, 0), ws = A.w(0, -1, 0);
-    const double wtt = A.w(0, 0, 1), wbb = A.w(0, 0, -1);
-    const double ue3 = A.u(0, 0, 0) + A.u(0, 0, 1), uw3 = A.u(-1, 0, 0) + A.u(-1, 0, 1);
-    const double vn3 = A.v(0, 0, 0) + A.v(0, 0, 1), vs3 = A.v(0, -1, 0) + A.v(0, -1, 1);
-    double fwx = ue3 * (w0 + we) - uw3 * (ww + w0);
+    const T we = A.w(1, 0, 0), ww = A.w(-1, 0, 0);
+    const T wn = A.w(0, 1, 0), ws = A.w(0, -1, 0);
+    const T wtt = A.w(0, 0, 1), wbb = A.w(0, 0, -1);
+    const T ue3 = A.u(0, 0, 0) + A.u(0, 0, 1), uw3 = A.u(-1, 0, 0) + A.u(-1, 0, 1);
+    const T vn3 = A.v(0, 0, 0) + A.v(0, 0, 1), vs3 = A.v(0, -1, 0) + A.v(0, -1, 1);
+    T fwx = ue3 * (w0 + we) - uw3 * (ww + w0);
     SF_BLEND(fwx, (fabs(ue3) * (w0 - we) - fabs(uw3) * (ww - w0)));
-    double fwy = vn3 * (w0 + wn) - vs3 * (ws + w0);
+    T fwy = vn3 * (w0 + wn) - vs3 * (ws + w0);
     SF_BLEND(fwy, (fabs(vn3) * (w0 - wn) - fabs(vs3) * (ws - w0)));
-    double fwz = (w0 + wtt) * (w0 + wtt) - (wbb + w0) * (wbb + w0);
+    T fwz = (w0 + wtt) * (w0 + wtt) - (wbb + w0) * (wbb + w0);
     SF_BLEND(fwz, (fabs(w0 + wtt) * (w0 - wtt) - fabs(wbb + w0) * (wbb - w0)));
-    const double lapw = (we - 2.0 * w0 + ww) * s.ix2 + (wn - 2.0 * w0 + ws) * s.iy2 +
-                        (wtt - 2.0 * w0 + wbb) * s.iz2;
-    const double rhsw = (A.q(0, 0, 0) - A.q(0, 0, 1)) * s.iz -
-                        0.25 * (fwx * s.ix + fwy * s.iy + fwz * s.iz) + s.nu * lapw + s.fz;
-    const double r = w0 + dt * rhsw;
+    const T lapw = (we - (T)2 * w0 + ww) * s.ix2 + (wn - (T)2 * w0 + ws) * s.iy2 +
+                        (wtt - (T)2 * w0 + wbb) * s.iz2;
+    const T rhsw = (A.q(0, 0, 0) - A.q(0, 0, 1)) * s.iz -
+                        (T)0.25 * (fwx * s.ix + fwy * s.iy + fwz * s.iz) + s.nu * lapw + s.fz;
+    const T r = w0 + dt * rhsw;
     out[2] = r;
   }
 }

@@ -179,7 +179,7 @@ class Simulation:
                  tile: Sequence[int] = (0, 0, 0), ghost: int = 1, form: str = "rows",
                  device: int = 0, fused: int | bool = True, rank: int | None = None,
                  world: int | None = None, nccl_id: bytes | None = None, transport: str | None = None,
-                 group=None):
+                 group=None, precision: str = "f64"):
         """With ``nccl_id`` (from :func:`nccl_unique_id` on rank 0, broadcast to all
         ranks) the simulation is the rank-``rank`` component of a ``world``-rank
         decomposition and exchanges ghosts over NCCL.
@@ -187,7 +187,11 @@ class Simulation:
         (peers' device buffers mapped into this process); the host side of that
         transport (handles, residual maxima, barriers) runs over the
         ``torch.distributed`` process group ``group`` (default: the world
-        group, e.g. gloo). Ranks may then share one device."""
+        group, e.g. gloo). Ranks may then share one device.
+        ``precision="f32"`` stores the five CFD fields in fp32 and runs the
+        fused TMA half-sweep and UPDATE_VELOCITY in fp32 arithmetic (the fp32
+        variant; compared with the fp64 reference under per-field tolerances,
+        tests/test_gpu_fp32.py)."""
         self._h = None
         self.cfg, self.par = cfg, par
         self._lib = L.lib()
@@ -197,6 +201,9 @@ class Simulation:
         for a in range(3):
             opt.tile[a] = int(tile[a])
         opt.ghost, opt.form, opt.device, opt.fused = int(ghost), (1 if form == "points" else 0), int(device), int(fused)
+        if precision not in ("f64", "f32"):
+            raise ValueError("precision must be 'f64' or 'f32'")
+        opt.precision = 8 if precision == "f64" else 4  # f32: the fp32 variant of the CFD fields
         self._ccfg, self._cpar, self._opt = cfg.to_c(), par.to_c(), opt
         h = C.c_void_p()
         if transport == "ipc":

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, n), n
     bound = {s[0] for s in _lib.SIGNATURES}
     assert set(names) == bound
-    assert lib.sf_abi_version() == 1
+    assert lib.sf_abi_version() == 2
 
 
 def test_library_is_the_in_tree_build():
