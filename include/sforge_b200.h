@@ -210,12 +210,14 @@ int sf_direct_plan(const int64_t extents[3], int world, int ghost, const int per
                    int64_t* out, int* n_out);
 int sf_sim_create_ipc(const sf_solver_config* cfg, const sf_fluid_params* par, const sf_sim_options* opt,
                       int rank, int world, const sf_host_transport* transport, sf_sim** out);
-/* Exchange of the temporal pass across ranks (exchange.hpp:165-224): 1
- * (default) = one launch of direct stores into the peers' ghost shells (26
- * neighbours) after each pass, where every peer's buffers map into this
- * process; 0 = pack, send/recv, unpack in three axis phases, overlapped with
- * the interior tiles.  sf_sim_direct_exchange reports whether the direct
- * stores are in use (a collective call the first time). */
+/* Exchange of the temporal pass across ranks (exchange.hpp:165-224), where
+ * every peer's buffers map into this process: 1 (default) = fused into the
+ * pass -- its cells within g of a processor face also store their outputs
+ * straight into the neighbours' ghost shells (26 directions: faces, edges,
+ * corners); 2 = one separate launch of the same direct stores after each
+ * pass; 0 = pack, send/recv, unpack in three axis phases, overlapped with the
+ * interior tiles.  sf_sim_direct_exchange returns the mode in use (0 when the
+ * peers do not map; a collective call the first time). */
 int sf_sim_set_direct_exchange(sf_sim* s, int on);
 int sf_sim_direct_exchange(sf_sim* s);
 int sf_sim_rank(const sf_sim* s);

@@ -1729,7 +1729,10 @@ class simulation {
   sf_host_transport htr_{};
   std::map<std::string, void*> ipc_open_;  // peer allocations mapped here, by handle
   // the temporal pass's exchange as direct stores into the peers' arrays
-  bool direct_on_ = true;   // sf_sim_set_direct_exchange
+  // sf_sim_set_direct_exchange: 1 = fused into the pass (default), 2 = one
+  // separate launch of direct stores after it, 0 = exchange phases
+  int direct_mode_ = 1;
+  sweep2_remote* remote_ = nullptr;  // device table of the fused exchange
   int direct_state_ = 0;    // 0 not set up, 1 active, -1 unavailable (a peer is not mappable)
   struct task_set_ref {
     sf_task* d = nullptr;
@@ -2522,8 +2525,77 @@ class simulation {
     cudaIpcMemHandle_t h[4][kSlots];
     long long sx, sy, base, n[3];
   };
+  // blocks of at least 2g cells per axis: a cell lies in at most one layer
+  // band per axis (the fused epilogue's assumption)
+  bool thick_blocks() const {
+    for (const auto& L : lay_)
+      for (int a = 0; a < 3; ++a)
+        if (L.dims[a] < 2 * dec_.ghost) return false;
+    return true;
+  }
+  // The fused-exchange table of local block b: one entry per direction of
+  // the direct-store plan; ptr_of(peer, field k, physical buffer) and
+  // layout_of(peer, {sx, sy, base}) resolve the neighbour's arrays.
+  template <class P, class Lay>
+  sweep2_remote build_remote(int b, P ptr_of, Lay layout_of) {
+    static const int F4[4] = {SF_VX, SF_VY, SF_VZ, SF_DIVU};
+    (void)F4;
+    sweep2_remote h{};
+    h.g = dec_.ghost;
+    for (int q = 0; q < 27; ++q) h.idx[q] = -1;
+    int np = 0;
+    for (const auto& dr : build_direct_plan(dec_, gid_[b])) {
+      sweep2_peer& Pe = h.peer[np];
+      for (int k = 0; k < 4; ++k)
+        for (int q = 0; q < kSlots; ++q) Pe.ptr[k][q] = ptr_of(dr.peer, k, q);
+      long long l[3];
+      layout_of(dr.peer, l);
+      Pe.rsx = l[0];
+      Pe.rsy = l[1];
+      Pe.rbase = l[2];
+      for (int a = 0; a < 3; ++a) Pe.shift[a] = dr.dlo[a] - dr.lo[a];
+      h.idx[(dr.d[0] + 1) + 3 * (dr.d[1] + 1) + 9 * (dr.d[2] + 1)] = np++;
+    }
+    return h;
+  }
+  sweep2_remote* upload_remote(const std::vector<sweep2_remote>& v) {
+    auto* d = (sweep2_remote*)dalloc(sizeof(sweep2_remote) * v.size());
+    SF_CK(cudaMemcpy(d, v.data(), sizeof(sweep2_remote) * v.size(), cudaMemcpyHostToDevice));
+    return d;
+  }
+  // One process, several grid components on the device: the temporal pass
+  // stores its boundary outputs straight into the neighbouring components'
+  // ghost shells (pointers by physical buffer; every component swaps alike),
+  // so no exchange runs between passes. SF_OVERLAP (tests) keeps the phases.
+  int local_fused_ = 0;  // 0 not set up, 1 active, -1 unavailable
+  bool local_fused() {
+    if (dist_ || force_overlap_ || !direct_mode_) return false;
+    if (local_fused_ == 0) {
+      local_fused_ = -1;
+      if (thick_blocks()) {
+        static const int F4[4] = {SF_VX, SF_VY, SF_VZ, SF_DIVU};
+        download_table();
+        std::vector<sweep2_remote> v;
+        for (int b = 0; b < nloc_; ++b)
+          v.push_back(build_remote(b, [&](int peer, int k, int phys) -> double* {
+            const int lb = lid_[peer];
+            for (int q = 0; q < kSlots; ++q)
+              if (htab_->ptr[lb][F4[k]][q] && htab_->bidx[lb][F4[k]][q] == phys) return htab_->ptr[lb][F4[k]][q];
+            return nullptr;
+          }, [&](int peer, long long* l) {
+            const sf_layout& L = lay_[lid_[peer]];
+            l[0] = L.sx;
+            l[1] = L.sy;
+            l[2] = L.base;
+          }));
+        remote_ = upload_remote(v);
+        local_fused_ = 1;
+      }
+    }
+    return local_fused_ > 0;
+  }
   bool direct_active() {
-    if (!dist_ || !direct_on_) return false;
+    if (!dist_ || !direct_mode_) return false;
     if (direct_state_ == 0) setup_direct();
     return direct_state_ > 0;
   }
@@ -2603,11 +2675,25 @@ class simulation {
     direct_tasks_.d = ts.d;
     direct_tasks_.n = ts.n;
     direct_tasks_.max_count = ts.max_count;
+    // the same plan as the pass's fused epilogue table
+    if (thick_blocks())
+      remote_ = upload_remote({build_remote(0, [&](int peer, int k, int phys) {
+                                 const ipc_field_rec& r = all[(size_t)peer];
+                                 return r.has[k][phys] ? static_cast<double*>(open_ipc(r.h[k][phys])) : nullptr;
+                               }, [&](int peer, long long* sxsybase) {
+                                 const ipc_field_rec& r = all[(size_t)peer];
+                                 sxsybase[0] = r.sx;
+                                 sxsybase[1] = r.sy;
+                                 sxsybase[2] = r.base;
+                               })});
     direct_state_ = 1;
   }
  public:
-  void set_direct(bool on) { direct_on_ = on; }
-  bool direct_enabled() { return direct_active(); }
+  void set_direct(int mode) {
+    if (mode < 0 || mode > 2) throw error(SF_ERR_ARG, "direct exchange mode must be 0, 1 or 2");
+    direct_mode_ = mode;
+  }
+  int direct_enabled() { return direct_active() ? (direct_mode_ == 1 && remote_ ? 1 : 2) : 0; }
  private:
 
   // The temporal pass (two half-sweeps per launch, sf_sweep2.cu) applies with
@@ -2694,15 +2780,37 @@ class simulation {
       // measured on one device, where the exchange is a few device copies,
       // serialising is faster. Across ranks the exchange goes through NCCL and
       // is hidden behind the interior (SF_NO_OVERLAP serialises there too).
+      if (local_fused()) {
+        // components on this device: one launch, the exchange fused into it
+        const work_set& wa = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass(), kTX, sweep2_tile_y());
+        if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
+        launch_sweep2(tview(wa), wa.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_, 0,
+                      remote_);
+        if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
+        ++launches_;
+        ++iter_launch_;
+        int ftx, fty;
+        sweep_tile_shape(&ftx, &fty);
+        const work_set& wr = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, ftx, fty);
+        launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, 2, st_);
+        launches_ += 2;
+        check_launch();
+        return 2;
+      }
       if (direct_active()) {
         // one launch over all tiles, then the direct stores into the peers
         // (predicated like the pass), then the max-allreduce below
         const work_set& wa = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass(), kTX, sweep2_tile_y());
+        const bool fused_x = direct_mode_ == 1 && remote_;
         if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
-        launch_sweep2(tview(wa), wa.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_);
+        launch_sweep2(tview(wa), wa.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_, 0,
+                      fused_x ? remote_ : nullptr);
         if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
-        launch_tasks(tview(), direct_tasks_.d, direct_tasks_.n, direct_tasks_.max_count, dctl_, st_, 296);
-        launches_ += 2;
+        if (!fused_x) {
+          launch_tasks(tview(), direct_tasks_.d, direct_tasks_.n, direct_tasks_.max_count, dctl_, st_, 296);
+          ++launches_;
+        }
+        ++launches_;
         ++iter_launch_;
         allreduce_max(&dctl_->acc[0], 2);
         ctl(CTL_FINISH_PASS, 0.0, 0, 0, 0, 1);
@@ -3056,10 +3164,10 @@ int sf_sim_create_ipc(const sf_solver_config* cfg, const sf_fluid_params* par, c
 int sf_sim_set_direct_exchange(sf_sim* s, int on) {
   return guarded([&] {
     need(s, "sim");
-    s->s->set_direct(on != 0);
+    s->s->set_direct(on);
   });
 }
-int sf_sim_direct_exchange(sf_sim* s) { return s ? (s->s->direct_enabled() ? 1 : 0) : 0; }
+int sf_sim_direct_exchange(sf_sim* s) { return s ? s->s->direct_enabled() : 0; }
 int sf_sim_rank(const sf_sim* s) { return s ? s->s->rank() : -1; }
 int sf_sim_gather_block(sf_sim* s, const char* field, int worker, double* host, int64_t n) {
   return guarded([&] {

@@ -79,11 +79,28 @@ void launch_sweep_div_tma(const table_view& vw, int nctas, int zc, const sf_cons
 struct sweep2_pins {
   double u, v, w, ul, vl, wl;
 };
+// Across ranks, the pass can store its outputs in the g owned layers next to
+// every processor face, edge and corner straight into the neighbour's ghost
+// shell (the ghost exchange fused into the update): one entry per direction
+// of the direct-store plan (sf_plan.hpp build_direct_plan), the peer's arrays
+// mapped into this process.
+struct sweep2_peer {
+  double* ptr[4][kSlots];  // vx, vy, vz, divu of the peer, by physical buffer index
+  long long rsx, rsy, rbase;
+  long long shift[3];      // peer-local index = this block's local index + shift
+};
+struct sweep2_remote {
+  int g;
+  int idx[27];  // direction (dx+1) + 3 (dy+1) + 9 (dz+1) -> peer entry, or -1
+  sweep2_peer peer[26];
+};
 // total_ctas: CTAs of the whole pass when it is split over several launches
-// (the last one to finish finalises); 0 = this launch alone
+// (the last one to finish finalises); 0 = this launch alone.
+// remote: device array of sweep2_remote (one per local block) for the fused
+// exchange, or null
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
-                   unsigned total_ctas = 0);
+                   unsigned total_ctas = 0, const sweep2_remote* remote = nullptr);
 size_t sweep2_maps_bytes();
 size_t sweep2_map_offset(int b, int f, int s);
 void sweep2_box(int field, int* bw, int* bh);

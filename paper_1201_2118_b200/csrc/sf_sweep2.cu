@@ -112,11 +112,16 @@ void sweep2_box(int field, int* bw, int* bh) {
 // every warp does three cell updates per phase. Rings: S0 planes in q % NIN
 // (NIN >= 3), S1 fields (u1 v1 w1 p1) in m % 4, divu1 in m % 3 -- the slot a
 // phase overwrites was last read before the previous barrier.
-template <int TYV, int NIN, int MINB, bool PER>
+// REMOTE: the outputs of cells within g of a processor face also go straight
+// into the neighbours' ghost shells (sweep2_remote), up to 7 directions per
+// cell (face, edges, corner): the ghost exchange of the next pass fused into
+// this one.
+template <int TYV, int NIN, int MINB, bool PER, bool REMOTE>
 __global__ void __launch_bounds__(32 * TYV, MINB)
     k_sweep2(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc,
              sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag, unsigned int total_ctas,
-             const maps2_t* __restrict__ maps, int finalize, sweep2_pins pins) {
+             const maps2_t* __restrict__ maps, int finalize, sweep2_pins pins,
+             const sweep2_remote* __restrict__ rem) {
   static_assert(NIN >= 3, "three S0 planes are read or in flight per phase");
   using G = geom<TYV>;
   constexpr int TX = G::TX, TY = G::TY, NT = G::NT, EW = G::EW, EN = G::EN, NE = G::NE, R2 = G::R2;
@@ -414,6 +419,36 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   double* __restrict__ Un = tab->ptr[b][SF_VX][ALT];
   double* __restrict__ Vn = tab->ptr[b][SF_VY][ALT];
   double* __restrict__ Wn = tab->ptr[b][SF_VZ][ALT];
+  // fused exchange: this cell's class along x / y (-1 low layers, +1 high
+  // layers, 0 neither) and the physical buffers the outputs land in
+  int rcx = 0, rcy = 0, rg = 0, rphys = 0;
+  const sweep2_remote* __restrict__ R = REMOTE ? rem + b : nullptr;  // this component's table
+  if (REMOTE) {
+    rg = R->g;
+    rcx = i < rg ? -1 : (i >= n0 - rg ? 1 : 0);
+    rcy = j < rg ? -1 : (j >= n1 - rg ? 1 : 0);
+    rphys = tab->bidx[b][SF_VX][ALT] | (tab->bidx[b][SF_VY][ALT] << 2) | (tab->bidx[b][SF_VZ][ALT] << 4) |
+            (tab->bidx[b][SF_DIVU][ALT] << 6);
+  }
+  auto remote_store = [&](int z, double un, double vn, double wn, double dd) {
+    const int rcz = z < rg ? -1 : (z >= n2 - rg ? 1 : 0);
+    if (!(rcx | rcy | rcz)) return;
+    for (int ez = 0; ez < 2; ++ez)
+      for (int ey = 0; ey < 2; ++ey)
+        for (int ex = 0; ex < 2; ++ex) {
+          const int dx = ex ? rcx : 0, dy = ey ? rcy : 0, dz = ez ? rcz : 0;
+          if ((ex && !rcx) || (ey && !rcy) || (ez && !rcz) || !(dx | dy | dz)) continue;
+          const int q = R->idx[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)];
+          if (q < 0) continue;
+          const sweep2_peer& P = R->peer[q];
+          const long long ro =
+              P.rbase + ((z + P.shift[2]) * P.rsy + (j + P.shift[1])) * P.rsx + (i + P.shift[0]);
+          __stwb(P.ptr[0][rphys & 3] + ro, un);
+          __stwb(P.ptr[1][(rphys >> 2) & 3] + ro, vn);
+          __stwb(P.ptr[2][(rphys >> 4) & 3] + ro, wn);
+          __stwb(P.ptr[3][(rphys >> 6) & 3] + ro, dd);
+        }
+  };
   unsigned long long r1 = 0ull, r2 = 0ull;
   double wm2 = 0.0;  // swept w2 of the -z neighbour (marching register)
   unsigned o = (unsigned)(B.base + ((long long)k0 * B.sy + j) * B.sx + i);
@@ -501,6 +536,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         __stwb(Vn + o, vn);
         __stwb(Wn + o, wn);
         __stwb(Dn + o, dd);
+        if (REMOTE) remote_store(z, un, vn, wn, dd);
         const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
         r1 = b1 > r1 ? b1 : r1;
         r2 = b2 > r2 ? b2 : r2;
@@ -537,6 +573,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         __stwb(Vn + o, vn);
         __stwb(Wn + o, wn);
         __stwb(Dn + o, dd);
+        if (REMOTE) remote_store(z, un, vn, wn, dd);
         if (xlo) {
           Un[o - 1] = umn;
           Dn[o - 1] = dd;
@@ -596,6 +633,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         __stwb(Vn + o, vn);
         __stwb(Wn + o, wn);
         __stwb(Dn + o, dd);
+        if (REMOTE) remote_store(z, un, vn, wn, dd);
         // ghosts the next pass reads: pinned low-face velocities, mirrored divu
         if (xlo) {
           Un[o - 1] = umn;
@@ -622,6 +660,10 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
     dsu = dsu1;
   }
 
+  // stores into peers (other devices or processes) are visible system-wide
+  // before this kernel completes; the max-allreduce after it is what the
+  // peers wait for
+  if (REMOTE) __threadfence_system();
   unsigned long long rr[2] = {r1, r2};
   block_max_atomic<2>(rr, &ctl->acc[0]);
   if (!finalize) return;  // across ranks: allreduce acc[0..1], then CTL_FINISH_PASS
@@ -669,16 +711,17 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
 
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
-                   unsigned total) {
+                   unsigned total, const sweep2_remote* remote) {
   if (nctas <= 0) return;
   constexpr int TYV = kPassTY, NIN = kPassStages, MINB = kPassMinB;
   using G = geom<TYV>;
   const bool per = c.per[0] || c.per[1] || c.per[2];
-  auto k = per ? k_sweep2<TYV, NIN, MINB, true> : k_sweep2<TYV, NIN, MINB, false>;
+  auto k = remote ? (per ? k_sweep2<TYV, NIN, MINB, true, true> : k_sweep2<TYV, NIN, MINB, false, true>)
+                  : (per ? k_sweep2<TYV, NIN, MINB, true, false> : k_sweep2<TYV, NIN, MINB, false, false>);
   ensure_smem_attr((const void*)k, G::smem_bytes(NIN));
   k<<<nctas, dim3(G::TX, G::TY), G::smem_bytes(NIN), st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
                                                            total ? total : (unsigned)nctas,
-                                                           static_cast<const maps2_t*>(maps), fin, pins);
+                                                           static_cast<const maps2_t*>(maps), fin, pins, remote);
 }
 
 }  // namespace sfb

@@ -535,16 +535,18 @@ class Simulation:
         return bool(self._lib.sf_sim_ghosts_valid(self._h, name.encode()))
 
     # -- device plumbing -----------------------------------------------------
-    def set_direct_exchange(self, on: bool):
-        """Temporal-pass exchange across ranks: direct stores into the peers'
-        ghost shells (True, default, where the peers' buffers map) or pack /
-        send / unpack phases overlapped with the interior (False)."""
-        L.check(self._lib.sf_sim_set_direct_exchange(self._h, 1 if on else 0))
+    def set_direct_exchange(self, mode: int | bool):
+        """Temporal-pass exchange across ranks, where the peers' buffers map:
+        1/True (default) = fused into the pass (boundary cells store straight
+        into the neighbours' ghost shells), 2 = one separate launch of the
+        same direct stores after each pass, 0/False = pack / send / unpack
+        phases overlapped with the interior."""
+        L.check(self._lib.sf_sim_set_direct_exchange(self._h, int(mode)))
 
     @property
-    def direct_exchange(self) -> bool:
-        """Whether the direct peer stores are in use (collective on first use)."""
-        return bool(self._lib.sf_sim_direct_exchange(self._h))
+    def direct_exchange(self) -> int:
+        """The direct-exchange mode in use (0 = phases; collective on first use)."""
+        return int(self._lib.sf_sim_direct_exchange(self._h))
 
     def synchronize(self):
         L.check(self._lib.sf_sim_synchronize(self._h))

@@ -27,11 +27,12 @@ import torch.distributed as dist  # noqa: E402
 
 import paper_1201_2118_b200 as sfb  # noqa: E402
 
-VARIANTS = {  # name: (fused, direct exchange)
-    "temporal-direct": (1, True),
-    "temporal-phases-overlapped": (1, False),
-    "single-half-sweep": (3, True),
-    "unfused": (0, True),
+VARIANTS = {  # name: (fused, direct exchange mode)
+    "temporal-direct-fused": (1, 1),     # boundary cells of the pass store into the peers' ghosts
+    "temporal-direct-launch": (1, 2),    # one launch of direct stores after each pass
+    "temporal-phases-overlapped": (1, 0),  # pack / pull / unpack phases beside the interior tiles
+    "single-half-sweep": (3, 1),
+    "unfused": (0, 1),
 }
 
 
@@ -65,7 +66,7 @@ def main():
         sim.set_kernel_timing(True)
         stats = [sim.step() for _ in range(a.steps)]
         csum = sim.checksum()  # collective: grid::gather over the ranks
-        used_direct = sim.direct_exchange if fused == 1 else False
+        used_direct = sim.direct_exchange if fused == 1 else 0
         results[name] = {"stats": [[s.dt, s.sweeps, s.residual] for s in stats], "checksum": csum,
                          "passes": sim.kernel_timing("sweep2")[1], "half_sweeps": sim.kernel_timing("sweep_div")[1],
                          "direct": used_direct, "block": list(sim.block_shape())}

@@ -7,7 +7,8 @@ message through them -- pack tasks (k_tasks type 2), the per-peer posting
 order, device copies out of the peers' send buffers, unpack tasks (type 3),
 the residual max-allreduce and the cross-rank loop decisions
 (CTL_FINISH_FUSED / CTL_FINISH_PASS), and for the temporal pass the direct
-stores into the peers' ghost shells (type 4) or the overlapped three-phase
+stores into the peers' ghost shells -- fused into the pass's epilogue, or
+as one separate launch (k_tasks type 4) -- or the overlapped three-phase
 exchange.  No kernel waits on another rank's kernel (the host orders them
 with gloo barriers), so co-scheduling the ranks on one GPU is safe.
 
@@ -51,8 +52,9 @@ def test_ranks_in_separate_processes_match_the_reference(ref_available, world, e
     for name, v in res["variants"].items():
         assert v["ok"], (name, v, res["reference"])
     v = res["variants"]
-    assert v["temporal-direct"]["direct"] and v["temporal-direct"]["passes"] > 0
-    assert not v["temporal-phases-overlapped"]["direct"] and v["temporal-phases-overlapped"]["passes"] > 0
+    assert v["temporal-direct-fused"]["direct"] == 1 and v["temporal-direct-fused"]["passes"] > 0
+    assert v["temporal-direct-launch"]["direct"] == 2 and v["temporal-direct-launch"]["passes"] > 0
+    assert v["temporal-phases-overlapped"]["direct"] == 0 and v["temporal-phases-overlapped"]["passes"] > 0
     assert v["single-half-sweep"]["passes"] == 0 and v["single-half-sweep"]["half_sweeps"] > 0
     # blocks large enough that the overlapped variant has interior tiles
     assert v["temporal-phases-overlapped"]["block"][0] >= 66
