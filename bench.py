@@ -85,13 +85,31 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
+def kernel_source_sha() -> str:
+    """sha256 (16 hex) over the library's CUDA sources (scripts/ncu_summary.py
+    records the same hash with each capture)."""
+    import hashlib
+    h = hashlib.sha256()
+    src = os.path.join(ROOT, "paper_1201_2118_b200", "csrc")
+    for n in sorted(os.listdir(src)):
+        if n.endswith((".cu", ".cuh", ".hpp")):
+            with open(os.path.join(src, n), "rb") as f:
+                h.update(n.encode() + f.read())
+    return h.hexdigest()[:16]
+
+
 def ncu_traffic(kernel="sweep_div"):
-    """DRAM bytes per launch of the dominant kernel from its committed ncu capture."""
+    """DRAM bytes per launch of the dominant kernel from its committed ncu
+    capture (profiles/ncu_<kernel>.json), with the capture's provenance: the
+    traffic is marked stale when the kernel sources changed since."""
     p = os.path.join(ROOT, "profiles", f"ncu_{kernel}.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("grid")
+        sha = d.get("kernel_source_sha")
+        src = {"file": os.path.relpath(p, ROOT), "captured_from": d.get("captured_from"),
+               "kernel_source_sha": sha, "stale": sha != kernel_source_sha()}
+        return d.get("dram_bytes_per_launch"), src
     except Exception:
         return None, None
 
@@ -332,7 +350,11 @@ def run_ours(args):
 
     # ---- device-timed region: K full steps, inputs resident in HBM -------------
     clocks = ClockSampler(dev)
-    sim.set_kernel_timing(True)
+    # per-launch CUDA events around the dominant kernel, except on small grids:
+    # there the persistent pressure loop (one launch per loop)
+    # is what runs, and per-launch timing would swap in the launch-per-sweep path
+    small = cells <= 4.0e5
+    sim.set_kernel_timing(not small)
     sim.launch_count(reset=True)
     barrier()
     torch.cuda.synchronize()
@@ -349,8 +371,8 @@ def run_ours(args):
     launches = sim.launch_count()
     # the dominant kernel: the temporal pass where it ran, else the half-sweep;
     # both move 80 algorithmic bytes per cell per launch (read S0, write S2)
-    kname = "sweep2" if sim.kernel_timing("sweep2")[1] > 0 else "sweep_div"
-    k_ms, k_n = sim.kernel_timing(kname)
+    kname = "sweep2" if sim.kernel_timing("sweep2")[1] > 0 else ("loop" if small else "sweep_div")
+    k_ms, k_n = sim.kernel_timing(kname) if not small else (0.0, 0)
     k_ms = max_over_ranks(k_ms)
     sim.set_kernel_timing(False)
     ms_per_step = ms_total / args.steps
@@ -373,15 +395,20 @@ def run_ours(args):
     es = 4 if args.dtype == "f32" else 8
     algo_launch = BYTES_PER_HALF_SWEEP * es // 8 * units * cells
     achieved = (algo_launch / avg_launch_s / 1e9) if avg_launch_s else None
-    traffic, _ = ncu_traffic(kname) if es == 8 else (None, None)
-    step_bytes = (BYTES_UV + BYTES_DIV + BYTES_PER_HALF_SWEEP * S) * es // 8 * cells
+    traffic, traffic_src = ncu_traffic(kname) if es == 8 else (None, None)
+    step_bytes = (BYTES_UV + BYTES_DIV + BYTES_PER_HALF_SWEEP * sweeps_done / args.steps) * es / 8 * cells
+    if small:  # the whole step stands in for the kernel (L2-resident, launch/latency-bound regime)
+        achieved = step_bytes / (ms_per_step / 1e3) / 1e9
     roofline = {
         "bound": "hbm",
         "kernel": ("k_sweep2 (temporal pass: two fused half-sweeps per launch)" if kname == "sweep2"
+                   else "whole step: persistent pressure loop k_pressure_loop (grid L2-resident; achieved = "
+                        "step algorithmic bytes / step time)" if small
                    else "k_sweep_div (fused half-sweep)"),
         "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4) if achieved else None,
         "traffic": traffic,
+        "traffic_source": traffic_src,
         "half_sweeps_per_launch": units,
         "algorithmic_bytes_per_launch": algo_launch,
         "avg_launch_ms": round(k_ms / k_n, 4) if k_n else None, "launches_timed": k_n,

@@ -43,6 +43,18 @@ KEYS = [
 ]
 
 
+def kernel_source_sha() -> str:
+    """sha256 (16 hex) over the CUDA sources of the library (same as bench.py)."""
+    import hashlib
+    h = hashlib.sha256()
+    src = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1201_2118_b200", "csrc")
+    for n in sorted(os.listdir(src)):
+        if n.endswith((".cu", ".cuh", ".hpp")):
+            with open(os.path.join(src, n), "rb") as f:
+                h.update(n.encode() + f.read())
+    return h.hexdigest()[:16]
+
+
 def raw(rep: str):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -139,6 +151,9 @@ def main():
         first = js["launches"][0] if js["launches"] else {}
         js["dram_bytes_per_launch"] = first.get("dram_bytes_per_launch")
         js["algo_bytes_per_launch"] = a.algo_bytes
+        # provenance: bench.py flags the traffic as stale once the kernel source changes
+        js["kernel_source_sha"] = kernel_source_sha()
+        js["captured_from"] = os.path.basename(a.rep)
         with open(a.json, "w") as f:
             json.dump(js, f, indent=1)
     print("\n".join(md))
