@@ -285,22 +285,36 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
     const int gk = lo2 + z;
     const int zpar = wrp(gk, N2, per2) & 1;
     if (fast_xy && z >= zf_lo && z <= zf_hi) {
-#pragma unroll
-      for (int r = 0; r < NE; ++r) {
-        if (r > 0 && !has2f) break;
-        const int ia = f_ia[r], e = f_e[r];
-        // all loads first: the stores below may alias them as far as the compiler knows
-        const double dc = S[Di + ia], dx = S[Di + ia + 1], dy = S[Di + ia + IW], dz = S[Dz + ia];
-        const double uu = S[Ui + ia], vv = S[Vi + ia], ww = S[Wi + ia], pp = S[Pi + ia];
+      // both rounds' loads are issued before either round's stores (the
+      // compiler cannot reorder them itself: one shared array), doubling the
+      // independent work in flight for the warps that own two cells (warps
+      // 0-3; the branch is warp-uniform)
+      struct ld8 {
+        double dc, dx, dy, dz, uu, vv, ww, pp;
+      };
+      auto load = [&](int r) {
+        const int ia = f_ia[r];
+        return ld8{S[Di + ia], S[Di + ia + 1], S[Di + ia + IW], S[Dz + ia],
+                   S[Ui + ia], S[Vi + ia],     S[Wi + ia],      S[Pi + ia]};
+      };
+      auto update = [&](int r, const ld8& L) {
+        const int e = f_e[r];
         const double a0 = ((((f_bt[r] >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
-        const double d0 = mbI * dc * a0;
-        const double exv = mbI * dx * a1;
-        const double eyv = mbI * dy * a1;
-        const double ezv = mbI * dz * a1;
-        S[p1 + e] = pp + d0;
-        S[u1 + e] = uu + cu * (d0 - exv);
-        S[v1 + e] = vv + cv * (d0 - eyv);
-        S[w1 + e] = ww + cw * (d0 - ezv);
+        const double d0 = mbI * L.dc * a0;
+        const double exv = mbI * L.dx * a1;
+        const double eyv = mbI * L.dy * a1;
+        const double ezv = mbI * L.dz * a1;
+        S[p1 + e] = L.pp + d0;
+        S[u1 + e] = L.uu + cu * (d0 - exv);
+        S[v1 + e] = L.vv + cv * (d0 - eyv);
+        S[w1 + e] = L.ww + cw * (d0 - ezv);
+      };
+      if (has2f) {
+        const ld8 L0 = load(0), L1 = load(1);
+        update(0, L0);
+        update(1, L1);
+      } else {
+        update(0, load(0));
       }
       return;
     }
@@ -372,18 +386,30 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
       return;
     }
     const int u1 = fo + U1 * EN, v1 = fo + V1 * EN, w1 = fo + W1 * EN, w1m = fom + W1 * EN;
-#pragma unroll
-    for (int r = 0; r < NE; ++r) {
-      if (r > 0 && !has2d) break;
-      // non-source cells compute on in-bounds operands and skip the store
+    // non-source cells compute on in-bounds operands and skip the store; both
+    // rounds' loads precede the stores (see s1_fields)
+    struct ld6 {
+      double u, um, v, vm, w, wm;
+    };
+    auto load = [&](int r) {
       const int q = d_q[r];
-      const double du = S[u1 + q] - S[u1 + q - 1];
-      const double dv = S[v1 + q] - S[v1 + q - EW];
-      const double dw = S[w1 + q] - S[w1m + q];
+      return ld6{S[u1 + q], S[u1 + q - 1], S[v1 + q], S[v1 + q - EW], S[w1 + q], S[w1m + q]};
+    };
+    auto div = [&](int r, const ld6& L) {
+      const double du = L.u - L.um;
+      const double dv = L.v - L.vm;
+      const double dw = L.w - L.wm;
       double dd = du * s.ix;
       dd += dv * s.iy;
       dd += dw * s.iz;
       if ((d_ok >> r) & 1) S[d1 + d_e[r]] = dd;
+    };
+    if (has2d) {
+      const ld6 L0 = load(0), L1 = load(1);
+      div(0, L0);
+      div(1, L1);
+    } else {
+      div(0, load(0));
     }
   };
   auto F = [&](int slot) { return FRING + slot * 4 * EN; };  // field slot offset
