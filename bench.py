@@ -300,8 +300,6 @@ def run_ours(args):
         if args.strong:
             n = args.strong
         cfg = cavity_cfg(sfb, n, S, c0)
-        if args.dtype == "f32" and fused == 1:
-            fused = 3  # the temporal pass is fp64-only; fp32 runs the fused TMA half-sweep
         sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=1, device=dev, fused=fused, precision=args.dtype)
     if args.strong:  # this rank's block of the fixed global grid
         cells = 1

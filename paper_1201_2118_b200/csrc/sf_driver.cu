@@ -2003,8 +2003,8 @@ class simulation {
         SF_CK(cudaMemcpy(uvmaps_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
       }
     }
-    // descriptors of the temporal pass (halo'd boxes; fp64 only)
-    if (maps_ && cfd_es_ == 8) {
+    // descriptors of the temporal pass (halo'd boxes)
+    if (maps_) {
       std::vector<unsigned char> hm(sweep2_maps_bytes(), 0);
       bool ok = true;
       for (int b = 0; b < nloc_ && ok; ++b)
@@ -2014,9 +2014,9 @@ class simulation {
             if (!p) continue;
             const sf_layout& L = lay_[b];
             int bw, bh;
-            sweep2_box(f, &bw, &bh);
+            sweep2_box(f, &bw, &bh, fes_[f]);
             ok = bw <= L.sx && bh <= L.sy &&
-                 encode_box_map(hm.data() + sweep2_map_offset(b, f, s), p, L.sx, L.sy, L.sz, bw, bh) == 0;
+                 encode_box_map(hm.data() + sweep2_map_offset(b, f, s), p, L.sx, L.sy, L.sz, bw, bh, fes_[f]) == 0;
           }
       if (ok) {
         maps2_ = dalloc(hm.size());
@@ -2595,7 +2595,9 @@ class simulation {
     return local_fused_ > 0;
   }
   bool direct_active() {
-    if (!dist_ || !direct_mode_) return false;
+    // the separate direct-store launch (mode 2) moves fp64 values; an fp32
+    // simulation uses the fused stores or the phases
+    if (!dist_ || !direct_mode_ || (direct_mode_ == 2 && cfd_es_ != 8)) return false;
     if (direct_state_ == 0) setup_direct();
     return direct_state_ > 0;
   }
@@ -2705,7 +2707,7 @@ class simulation {
   // (sf_sweep2.cu; scripts/probes/parity_stress.py found the unwrapped
   // version wrong on 39x43x13, periodic y, two components, ghost 2).
   bool temporal() const {
-    if (!maps2_ || !temporal_env_ || opt_.fused != 1 || cfd_es_ != 8) return false;
+    if (!maps2_ || !temporal_env_ || opt_.fused != 1) return false;
     for (int b = 0; b < nloc_; ++b)  // the pass addresses its arrays with 32-bit element offsets
       if ((unsigned long long)(lay_[b].sx * lay_[b].sy * lay_[b].sz) >= (1ull << 32)) return false;
     bool proc = false;
@@ -2762,7 +2764,8 @@ class simulation {
     if (!has_proc_faces()) {
       const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass(), kTX, sweep2_tile_y());
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
-      launch_sweep2(tview(ws), ws.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_);
+      launch_sweep2(tview(ws), ws.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_, 0,
+                    nullptr, cfd_es_);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
     } else {
       // Processor faces: the pass reads 2-deep halos of vx, vy, vz, divu (p
@@ -2785,14 +2788,14 @@ class simulation {
         const work_set& wa = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass(), kTX, sweep2_tile_y());
         if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
         launch_sweep2(tview(wa), wa.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_, 0,
-                      remote_);
+                      remote_, cfd_es_);
         if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
         ++launches_;
         ++iter_launch_;
         int ftx, fty;
         sweep_tile_shape(&ftx, &fty);
         const work_set& wr = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, ftx, fty);
-        launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, 2, st_);
+        launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, 2, st_, cfd_es_);
         launches_ += 2;
         check_launch();
         return 2;
@@ -2804,7 +2807,7 @@ class simulation {
         const bool fused_x = direct_mode_ == 1 && remote_;
         if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
         launch_sweep2(tview(wa), wa.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_, 0,
-                      fused_x ? remote_ : nullptr);
+                      fused_x ? remote_ : nullptr, cfd_es_);
         if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
         if (!fused_x) {
           launch_tasks(tview(), direct_tasks_.d, direct_tasks_.n, direct_tasks_.max_count, dctl_, st_, 296);
@@ -2817,7 +2820,7 @@ class simulation {
         int ftx, fty;
         sweep_tile_shape(&ftx, &fty);
         const work_set& wr = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, ftx, fty);
-        launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, 2, st_);
+        launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, 2, st_, cfd_es_);
         launches_ += 2;
         check_launch();
         return 2;
@@ -2835,10 +2838,10 @@ class simulation {
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
       if (wi.nctas)
         launch_sweep2(tview(wi), wi.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_,
-                      total);
+                      total, nullptr, cfd_es_);
       SF_CK(cudaStreamWaitEvent(st_, ev_join_, 0));
       launch_sweep2(tview(wb), wb.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_,
-                    total);
+                    total, nullptr, cfd_es_);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
       ++launches_;
     }
@@ -2851,7 +2854,7 @@ class simulation {
     int ftx, fty;
     sweep_tile_shape(&ftx, &fty);
     const work_set& wr = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, ftx, fty);
-    launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, 2, st_);
+    launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, 2, st_, cfd_es_);
     launches_ += 2;
     check_launch();
     return 2;

@@ -100,10 +100,10 @@ struct sweep2_remote {
 // exchange, or null
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
-                   unsigned total_ctas = 0, const sweep2_remote* remote = nullptr);
+                   unsigned total_ctas = 0, const sweep2_remote* remote = nullptr, int es = 8);
 size_t sweep2_maps_bytes();
 size_t sweep2_map_offset(int b, int f, int s);
-void sweep2_box(int field, int* bw, int* bh);
+void sweep2_box(int field, int* bw, int* bh, int es = 8);
 int sweep2_tile_y();  // tile height of the selected temporal-pass variant (tile width 32)
 int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field, int es = 8);
 size_t sweep_maps_bytes();

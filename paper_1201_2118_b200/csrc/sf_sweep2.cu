@@ -59,24 +59,30 @@ __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, uint64_t
 constexpr int r128(int b) { return (b + 127) / 128 * 128; }
 
 // Tile geometry: TX x TY cells per CTA (one thread each), the S1 tile widened
-// to EW x EH, and the S0 stage layout (every TMA destination 128-byte aligned).
-template <int TYV>
+// to EW x EH, and the S0 stage layout (every TMA destination 128-byte aligned)
+// for element type T (fp64; fp32 for the fp32 variant of the CFD fields). A
+// TMA box starts on a 16-byte aligned x: XA = 16 / sizeof(T) cells left of the
+// tile (2 fp64, 4 fp32), so the widened S1 region (from i0-2) sits XSH = XA-2
+// cells into each S0 row.
+template <int TYV, class T = double>
 struct geom {
+  static constexpr int ES = (int)sizeof(T), XA = 16 / ES, XSH = XA - 2;
   static constexpr int TX = 32, TY = TYV, NT = TX * TY;
   static constexpr int EW = TX + 3, EH = TY + 3, EN = EW * EH;  // widened S1 tile
   static constexpr int NE = (EN + NT - 1) / NT;                  // widened cells per thread
   static constexpr int R2 = EN - 1 - NT;                         // second-round cells
-  static constexpr int IW = TX + 4;                              // S0 box width (x from i0-2)
+  static constexpr int IW = (TX + 2 + XA + XA - 1) / XA * XA;    // S0 box width (x from i0-XA): 36 / 40
   static constexpr int IDH = TY + 4, IFH = TY + 3;               // divu / other S0 box heights
   static constexpr int IN_D = 0;
-  static constexpr int IN_U = r128(8 * IW * IDH);
-  static constexpr int IN_V = IN_U + r128(8 * IW * IFH);
-  static constexpr int IN_W = IN_V + r128(8 * IW * IFH);
-  static constexpr int IN_P = IN_W + r128(8 * IW * IFH);
-  static constexpr int IN_BYTES = IN_P + r128(8 * IW * IFH);
-  static constexpr uint32_t IN_TX = 8u * (IW * IDH + 4 * IW * IFH);
-  static constexpr int smem_bytes(int nin) { return nin * IN_BYTES + (4 * 4 + 3) * EN * 8; }
+  static constexpr int IN_U = r128(ES * IW * IDH);
+  static constexpr int IN_V = IN_U + r128(ES * IW * IFH);
+  static constexpr int IN_W = IN_V + r128(ES * IW * IFH);
+  static constexpr int IN_P = IN_W + r128(ES * IW * IFH);
+  static constexpr int IN_BYTES = IN_P + r128(ES * IW * IFH);
+  static constexpr uint32_t IN_TX = (uint32_t)ES * (IW * IDH + 4 * IW * IFH);
+  static constexpr int smem_bytes(int nin) { return nin * IN_BYTES + (4 * 4 + 3) * EN * ES; }
   static_assert(NE == 2 && R2 > 0 && R2 <= NT, "two rounds of widened cells per thread");
+  static_assert(IN_BYTES % ES == 0 && (IW * ES) % 16 == 0, "TMA rows");
 };
 
 enum { U1 = 0, V1 = 1, W1 = 2, P1 = 3, D1 = 4 };
@@ -94,12 +100,11 @@ size_t sweep2_map_offset(int b, int f, int s) {
 // 32 x 8 tiles, 3 S0 stages, 2 CTAs per SM. (Measured alternatives: 32 x 16
 // tiles, 6 stages at 1 CTA/SM, L2 prefetch of later planes -- all slower;
 // DESIGN.md §10.)
-constexpr int kPassTY = 8, kPassStages = 3, kPassMinB = 2;
+constexpr int kPassTY = 8, kPassStages = 3, kPassMinB = 2, kPassMinB32 = 3;
 int sweep2_tile_y() { return kPassTY; }
-void sweep2_box(int field, int* bw, int* bh) {
-  const int ty = sweep2_tile_y();
-  *bw = 32 + 4;
-  *bh = field == SF_DIVU ? ty + 4 : ty + 3;
+void sweep2_box(int field, int* bw, int* bh, int es) {
+  *bw = es == 4 ? geom<kPassTY, float>::IW : geom<kPassTY, double>::IW;
+  *bh = field == SF_DIVU ? kPassTY + 4 : kPassTY + 3;
 }
 
 // Schedule (S0 plane q and S1 plane m both mean z = k0 - 2 + q / m). One CTA
@@ -116,14 +121,15 @@ void sweep2_box(int field, int* bw, int* bh) {
 // into the neighbours' ghost shells (sweep2_remote), up to 7 directions per
 // cell (face, edges, corner): the ghost exchange of the next pass fused into
 // this one.
-template <int TYV, int NIN, int MINB, bool PER, bool REMOTE>
+template <int TYV, int NIN, int MINB, bool PER, bool REMOTE, class T>
 __global__ void __launch_bounds__(32 * TYV, MINB)
     k_sweep2(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc,
              sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag, unsigned int total_ctas,
              const maps2_t* __restrict__ maps, int finalize, sweep2_pins pins,
              const sweep2_remote* __restrict__ rem) {
   static_assert(NIN >= 3, "three S0 planes are read or in flight per phase");
-  using G = geom<TYV>;
+  using G = geom<TYV, T>;
+  constexpr int ES = G::ES, XSH = G::XSH;
   constexpr int TX = G::TX, TY = G::TY, NT = G::NT, EW = G::EW, EN = G::EN, NE = G::NE, R2 = G::R2;
   constexpr int IW = G::IW, IN_D = G::IN_D, IN_U = G::IN_U, IN_V = G::IN_V, IN_W = G::IN_W, IN_P = G::IN_P;
   constexpr int IN_BYTES = G::IN_BYTES;
@@ -131,7 +137,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t bars[NIN];
-  __shared__ double smb[8];
+  __shared__ T smb[8];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
   const int cta = blockIdx.x;
   const sf_work& wk = items[nitems > 1 ? find_item(items, nitems, cta) : 0];
@@ -160,9 +166,10 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   // one IMAD.WIDE per store address instead of a 64-bit add pair
   const unsigned sx = (unsigned)B.sx, sxy = (unsigned)(B.sx * B.sy);
   const double beta = ctl->beta, dt = ctl->dt;
+  const T Tix = (T)s.ix, Tiy = (T)s.iy, Tiz = (T)s.iz;
   const int colA = ctl->color, colB = colA ^ 1;
-  const double cu = dt * s.ix, cv = dt * s.iy, cw = dt * s.iz;
-  const double pin_u = pins.u, pin_v = pins.v, pin_w = pins.w;  // global high-wall normals
+  const T cu = (T)(dt * s.ix), cv = (T)(dt * s.iy), cw = (T)(dt * s.iz);
+  const T pin_u = (T)pins.u, pin_v = (T)pins.v, pin_w = (T)pins.w;  // global high-wall normals
   const long long nm0 = s.nm1[0], nm1 = s.nm1[1], nm2 = s.nm1[2];
   auto bin = [](int per, long long gg, long long nm) { return per | ((gg > 0) & (gg < nm)); };
   auto bnx = [](int per, long long gg, long long nm) { return per | (gg + 1 < nm); };
@@ -176,13 +183,13 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       if (q == tid) sc = s.bscale[q >> 2][(q >> 1) & 1][q & 1];
-    smb[tid] = -(beta * sc);  // -(beta * bscale[..]) as cfd.hpp:712-715 forms it
+    smb[tid] = (T)(-(beta * sc));  // -(beta * bscale[..]) as cfd.hpp:712-715 forms it
   }
   __syncthreads();
 
   // ---- S0 input ring ---------------------------------------------------------
   const int xo = (int)(B.base % B.sx), g = B.g;
-  const int xs = xo + i0 - 2, ys = g + j0 - 2, zs = g + k0 - 2;
+  const int xs = xo + i0 - 2 - XSH, ys = g + j0 - 2, zs = g + k0 - 2;
   const CUtensorMap* mD = &maps->m[b][SF_DIVU][tab->bidx[b][SF_DIVU][FRONT]];
   const CUtensorMap* mU = &maps->m[b][SF_VX][tab->bidx[b][SF_VX][FRONT]];
   const CUtensorMap* mV = &maps->m[b][SF_VY][tab->bidx[b][SF_VY][FRONT]];
@@ -215,9 +222,9 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
     for (int q = 0; q < NIN; ++q) issue(q);
 
   // All shared-memory accesses below index one array with 32-bit offsets.
-  double* const S = reinterpret_cast<double*>(sm);
-  constexpr int FRING = NIN * IN_BYTES / 8, DRING = FRING + 4 * 4 * EN;
-  auto so = [&](int q) { return (q % NIN) * (IN_BYTES / 8); };  // S0 stage offset
+  T* const S = reinterpret_cast<T*>(sm);
+  constexpr int FRING = NIN * IN_BYTES / ES, DRING = FRING + 4 * 4 * EN;
+  auto so = [&](int q) { return (q % NIN) * (IN_BYTES / ES); };  // S0 stage offset
 
   // ---- per-thread widened cells ---------------------------------------------
   // s1_fields: thread t owns e = t + 1 and, for t < R2, e = t + 1 + NT.
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
       const int bx = bin(s.per[0], gi, nm0), bxp = bnx(s.per[0], gi, nm0);
       const int by = bin(s.per[1], gj, nm1), byp = bnx(s.per[1], gj, nm1);
       f_e[r] = e;
-      f_ia[r] = ey * IW + ex;
+      f_ia[r] = ey * IW + ex + XSH;
       f_bt[r] = ((bx << 2) | (by << 1)) | (((bxp << 2) | (by << 1)) << 3) | (((bx << 2) | (byp << 1)) << 6) |
                 ((int)((wrp((int)gi, N0, per0) + wrp((int)gj, N1, per1)) & 1) << 9) |
                 (((per0 || (gi >= 0 && gi < N0)) && (per1 || (gj >= 0 && gj < N1))) << 10) |
@@ -272,15 +279,15 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
                        j0 + TY <= (int)wk.hi[1];
   const int zf_lo = s.per[2] ? 1 << 30 : (int)max(1ll, 1ll - B.lo[2]);
   const int zf_hi = (int)(nm2 - 2 - B.lo[2]);
-  const double mbI = smb[7];
+  const T mbI = smb[7];
 
   // S1 fields of plane z from its S0 stage (st) and divu0 of plane z+1 (stn):
   // sweep A's cell update (cfd.hpp:699-719) with the wall pins, into field
   // slot fo. Cells outside the domain carry S0; their wall-normal values are
   // the constant pins.
   auto s1_fields = [&](int z, int st, int stn, int fo) {
-    const int Di = st + IN_D / 8, Ui = st + IN_U / 8, Vi = st + IN_V / 8, Wi = st + IN_W / 8,
-              Pi = st + IN_P / 8, Dz = stn + IN_D / 8;
+    const int Di = st + IN_D / ES, Ui = st + IN_U / ES, Vi = st + IN_V / ES, Wi = st + IN_W / ES,
+              Pi = st + IN_P / ES, Dz = stn + IN_D / ES;
     const int u1 = fo + U1 * EN, v1 = fo + V1 * EN, w1 = fo + W1 * EN, p1 = fo + P1 * EN;
     const int gk = lo2 + z;
     const int zpar = wrp(gk, N2, per2) & 1;
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
       // independent work in flight for the warps that own two cells (warps
       // 0-3; the branch is warp-uniform)
       struct ld8 {
-        double dc, dx, dy, dz, uu, vv, ww, pp;
+        T dc, dx, dy, dz, uu, vv, ww, pp;
       };
       auto load = [&](int r) {
         const int ia = f_ia[r];
@@ -299,11 +306,11 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
       };
       auto update = [&](int r, const ld8& L) {
         const int e = f_e[r];
-        const double a0 = ((((f_bt[r] >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
-        const double d0 = mbI * L.dc * a0;
-        const double exv = mbI * L.dx * a1;
-        const double eyv = mbI * L.dy * a1;
-        const double ezv = mbI * L.dz * a1;
+        const T a0 = ((((f_bt[r] >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
+        const T d0 = mbI * L.dc * a0;
+        const T exv = mbI * L.dx * a1;
+        const T eyv = mbI * L.dy * a1;
+        const T ezv = mbI * L.dz * a1;
         S[p1 + e] = L.pp + d0;
         S[u1 + e] = L.uu + cu * (d0 - exv);
         S[v1 + e] = L.vv + cv * (d0 - eyv);
@@ -326,17 +333,17 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
       for (int r = 0; r < NE; ++r) {
         if (r > 0 && !has2f) break;
         const int ia = f_ia[r], e = f_e[r], bt = f_bt[r];
-        const double dc = S[Di + ia], dx = S[Di + ia + 1], dy = S[Di + ia + IW], dz = S[Dz + ia];
-        const double uu = S[Ui + ia], vv = S[Vi + ia], ww = S[Wi + ia], pp = S[Pi + ia];
+        const T dc = S[Di + ia], dx = S[Di + ia + 1], dy = S[Di + ia + IW], dz = S[Dz + ia];
+        const T uu = S[Ui + ia], vv = S[Vi + ia], ww = S[Wi + ia], pp = S[Pi + ia];
         const int rc = (bt & 7) | 1, rx = ((bt >> 3) & 7) | 1, ry = ((bt >> 6) & 7) | 1;
-        const double a0 = ((((bt >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
-        const double d0 = smb[rc] * dc * a0;
-        const double exv = smb[rx] * dx * a1;
-        const double eyv = smb[ry] * dy * a1;
-        const double ezv = smb[rc] * dz * a1;
+        const T a0 = ((((bt >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
+        const T d0 = smb[rc] * dc * a0;
+        const T exv = smb[rx] * dx * a1;
+        const T eyv = smb[ry] * dy * a1;
+        const T ezv = smb[rc] * dz * a1;
         const bool own = (bt >> 10) & 1;
-        const double un = ((bt >> 11) & 1) ? pin_u : uu + cu * (d0 - exv);
-        const double vn = ((bt >> 12) & 1) ? pin_v : vv + cv * (d0 - eyv);
+        const T un = ((bt >> 11) & 1) ? pin_u : uu + cu * (d0 - exv);
+        const T vn = ((bt >> 12) & 1) ? pin_v : vv + cv * (d0 - eyv);
         S[p1 + e] = own ? pp + d0 : pp;
         S[u1 + e] = own ? un : (((bt >> 13) & 1) ? pins.ul : uu);
         S[v1 + e] = own ? vn : (((bt >> 14) & 1) ? pins.vl : vv);
@@ -362,11 +369,11 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         continue;
       }
       const int rc = bt & 7, rx = (bt >> 3) & 7, ry = (bt >> 6) & 7;
-      const double a0 = ((((bt >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
-      const double d0 = smb[rc | bz] * S[Di + ia] * a0;
-      const double exv = smb[rx | bz] * S[Di + ia + 1] * a1;
-      const double eyv = smb[ry | bz] * S[Di + ia + IW] * a1;
-      const double ezv = smb[rc | bzp] * S[Dz + ia] * a1;
+      const T a0 = ((((bt >> 9) & 1) ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
+      const T d0 = smb[rc | bz] * S[Di + ia] * a0;
+      const T exv = smb[rx | bz] * S[Di + ia + 1] * a1;
+      const T eyv = smb[ry | bz] * S[Di + ia + IW] * a1;
+      const T ezv = smb[rc | bzp] * S[Dz + ia] * a1;
       S[p1 + e] = S[Pi + ia] + d0;
       S[u1 + e] = ((bt >> 11) & 1) ? pin_u : S[Ui + ia] + cu * (d0 - exv);
       S[v1 + e] = ((bt >> 12) & 1) ? pin_v : S[Vi + ia] + cv * (d0 - eyv);
@@ -389,19 +396,19 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
     // non-source cells compute on in-bounds operands and skip the store; both
     // rounds' loads precede the stores (see s1_fields)
     struct ld6 {
-      double u, um, v, vm, w, wm;
+      T u, um, v, vm, w, wm;
     };
     auto load = [&](int r) {
       const int q = d_q[r];
       return ld6{S[u1 + q], S[u1 + q - 1], S[v1 + q], S[v1 + q - EW], S[w1 + q], S[w1m + q]};
     };
     auto div = [&](int r, const ld6& L) {
-      const double du = L.u - L.um;
-      const double dv = L.v - L.vm;
-      const double dw = L.w - L.wm;
-      double dd = du * s.ix;
-      dd += dv * s.iy;
-      dd += dw * s.iz;
+      const T du = L.u - L.um;
+      const T dv = L.v - L.vm;
+      const T dw = L.w - L.wm;
+      T dd = du * Tix;
+      dd += dv * Tiy;
+      dd += dw * Tiz;
       if ((d_ok >> r) & 1) S[d1 + d_e[r]] = dd;
     };
     if (has2d) {
@@ -432,19 +439,19 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   // factors and wall flags are per-thread constants, so sweep B runs the fast
   // path's operations with them instead of the general path's lookups and
   // branches (bitwise the same values).
-  const double sc_ = smb[ic | 1], sex_ = smb[iex | 1], sey_ = smb[iey | 1];
-  const double sxm_ = smb[ixm | 1], sxpm_ = smb[ixpm | 1], sym_ = smb[iym | 1], sypm_ = smb[iypm | 1];
+  const T sc_ = smb[ic | 1], sex_ = smb[iex | 1], sey_ = smb[iey | 1];
+  const T sxm_ = smb[ixm | 1], sxpm_ = smb[ixpm | 1], sym_ = smb[iym | 1], sypm_ = smb[iypm | 1];
   const bool xlo = !per0 && gi == 0, ylo = !per1 && gj == 0, xhi = !per0 && gi == N0 - 1, yhi = !per1 && gj == N1 - 1;
   // -x / -y neighbour parities (the complement of this cell's, except across
   // an odd periodic wrap)
   const bool xm_same = per0 && gi == 0 && (N0 & 1), ym_same = per1 && gj == 0 && (N1 & 1);
   const int q0 = (ty + 2) * EW + (tx + 2);
 
-  double* __restrict__ Dn = tab->ptr[b][SF_DIVU][ALT];
-  double* __restrict__ Pn = tab->ptr[b][SF_P][ALT];
-  double* __restrict__ Un = tab->ptr[b][SF_VX][ALT];
-  double* __restrict__ Vn = tab->ptr[b][SF_VY][ALT];
-  double* __restrict__ Wn = tab->ptr[b][SF_VZ][ALT];
+  T* __restrict__ Dn = reinterpret_cast<T*>(tab->ptr[b][SF_DIVU][ALT]);
+  T* __restrict__ Pn = reinterpret_cast<T*>(tab->ptr[b][SF_P][ALT]);
+  T* __restrict__ Un = reinterpret_cast<T*>(tab->ptr[b][SF_VX][ALT]);
+  T* __restrict__ Vn = reinterpret_cast<T*>(tab->ptr[b][SF_VY][ALT]);
+  T* __restrict__ Wn = reinterpret_cast<T*>(tab->ptr[b][SF_VZ][ALT]);
   // fused exchange: this cell's class along x / y (-1 low layers, +1 high
   // layers, 0 neither) and the physical buffers the outputs land in
   int rcx = 0, rcy = 0, rg = 0, rphys = 0;
@@ -456,7 +463,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
     rphys = tab->bidx[b][SF_VX][ALT] | (tab->bidx[b][SF_VY][ALT] << 2) | (tab->bidx[b][SF_VZ][ALT] << 4) |
             (tab->bidx[b][SF_DIVU][ALT] << 6);
   }
-  auto remote_store = [&](int z, double un, double vn, double wn, double dd) {
+  auto remote_store = [&](int z, T un, T vn, T wn, T dd) {
     const int rcz = z < rg ? -1 : (z >= n2 - rg ? 1 : 0);
     if (!(rcx | rcy | rcz)) return;
     for (int ez = 0; ez < 2; ++ez)
@@ -469,14 +476,14 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
           const sweep2_peer& P = R->peer[q];
           const long long ro =
               P.rbase + ((z + P.shift[2]) * P.rsy + (j + P.shift[1])) * P.rsx + (i + P.shift[0]);
-          __stwb(P.ptr[0][rphys & 3] + ro, un);
-          __stwb(P.ptr[1][(rphys >> 2) & 3] + ro, vn);
-          __stwb(P.ptr[2][(rphys >> 4) & 3] + ro, wn);
-          __stwb(P.ptr[3][(rphys >> 6) & 3] + ro, dd);
+          __stwb(reinterpret_cast<T*>(P.ptr[0][rphys & 3]) + ro, un);
+          __stwb(reinterpret_cast<T*>(P.ptr[1][(rphys >> 2) & 3]) + ro, vn);
+          __stwb(reinterpret_cast<T*>(P.ptr[2][(rphys >> 4) & 3]) + ro, wn);
+          __stwb(reinterpret_cast<T*>(P.ptr[3][(rphys >> 6) & 3]) + ro, dd);
         }
   };
   unsigned long long r1 = 0ull, r2 = 0ull;
-  double wm2 = 0.0;  // swept w2 of the -z neighbour (marching register)
+  T wm2 = 0.0;  // swept w2 of the -z neighbour (marching register)
   unsigned o = (unsigned)(B.base + ((long long)k0 * B.sy + j) * B.sx + i);
 
   // pre-phase: S1 fields of planes 0 and 1 (S0 planes 0..2)
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
           "r"(ph3)
           : "memory");
     }
-    if (u <= nplanes) s1_fields(k0 + u, st2 * (IN_BYTES / 8), st3 * (IN_BYTES / 8), F((u + 2) & 3));
+    if (u <= nplanes) s1_fields(k0 + u, st2 * (IN_BYTES / ES), st3 * (IN_BYTES / ES), F((u + 2) & 3));
     s1_div(k0 + u - 1, F((u + 1) & 3), F(u & 3), Dr(dsu1), Dr(dsu));
     __syncthreads();
     if (tid == 0) issue(u + 2 + NIN);  // S0 plane u+2 is consumed
@@ -515,13 +522,13 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
     ph3 ^= st3 == 0 ? 1u : 0u;
     if (u == 1 && act) {
       // swept w2 of the plane below the chunk: sweep B's -z neighbour at k0
-      const double w1_below = S[F(1) + W1 * EN + q0];
+      const T w1_below = S[F(1) + W1 * EN + q0];
       if (lo2 + k0 > 0 || per2) {
         const long long gkm = B.lo[2] + k0 - 1;
         const int bzm = bin(s.per[2], gkm, nm2), bzpm = bnx(s.per[2], gkm, nm2);
-        const double a0m = (((gi + gj + wrp((int)gkm, N2, per2)) & 1) == colB) ? 1.0 : 0.0, a1m = 1.0 - a0m;
-        const double d0m = smb[ic | bzm] * S[Dr(1) + q0] * a0m;
-        const double ezm = smb[ic | bzpm] * S[Dr(2) + q0] * a1m;
+        const T a0m = (((gi + gj + wrp((int)gkm, N2, per2)) & 1) == colB) ? 1.0 : 0.0, a1m = 1.0 - a0m;
+        const T d0m = smb[ic | bzm] * S[Dr(1) + q0] * a0m;
+        const T ezm = smb[ic | bzpm] * S[Dr(2) + q0] * a1m;
         wm2 = w1_below + cw * (d0m - ezm);
       } else {
         wm2 = w1_below;  // pinned ghost plane
@@ -530,70 +537,70 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
     if (u >= 2) {
       // sweep B on plane m = u, z = k0 + u - 2
       const int z = k0 + u - 2;
-      const double* u1 = S + F(u & 3) + U1 * EN;
-      const double* v1 = S + F(u & 3) + V1 * EN;
-      const double* w1 = S + F(u & 3) + W1 * EN;
-      const double* p1 = S + F(u & 3) + P1 * EN;
-      const double* d1 = S + Dr(dsu);
-      const double* d1p = S + Dr(dsu1);
+      const T* u1 = S + F(u & 3) + U1 * EN;
+      const T* v1 = S + F(u & 3) + V1 * EN;
+      const T* w1 = S + F(u & 3) + W1 * EN;
+      const T* p1 = S + F(u & 3) + P1 * EN;
+      const T* d1 = S + Dr(dsu);
+      const T* d1p = S + Dr(dsu1);
       if (fast_xy && z >= zf_lo && z <= zf_hi) {
         // interior plane (see fast_xy): bitwise the general path below
-        const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
-        const double dXm = d1[q0 - 1], dYm = d1[q0 - EW], dZp = d1p[q0];
-        const double p0 = p1[q0], u0 = u1[q0], uml = u1[q0 - 1], v0 = v1[q0], vml = v1[q0 - EW], w0 = w1[q0];
+        const T dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
+        const T dXm = d1[q0 - 1], dYm = d1[q0 - EW], dZp = d1p[q0];
+        const T p0 = p1[q0], u0 = u1[q0], uml = u1[q0 - 1], v0 = v1[q0], vml = v1[q0 - EW], w0 = w1[q0];
         const int par = par_col ^ (int)((B.lo[2] + z) & 1);
-        const double a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
-        const double d0 = mbI * dC * a0;
-        const double exv = mbI * dXp * a1;
-        const double eyv = mbI * dYp * a1;
-        const double ezv = mbI * dZp * a1;
-        const double pn = p0 + d0;
-        const double un = u0 + cu * (d0 - exv);
-        const double vn = v0 + cv * (d0 - eyv);
-        const double wn = w0 + cw * (d0 - ezv);
+        const T a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
+        const T d0 = mbI * dC * a0;
+        const T exv = mbI * dXp * a1;
+        const T eyv = mbI * dYp * a1;
+        const T ezv = mbI * dZp * a1;
+        const T pn = p0 + d0;
+        const T un = u0 + cu * (d0 - exv);
+        const T vn = v0 + cv * (d0 - eyv);
+        const T wn = w0 + cw * (d0 - ezv);
         // -x / -y neighbours: parity a1, their +x / +y term is mbI*dC*a0 == d0
-        const double umn = uml + cu * (mbI * dXm * a1 - d0);
-        const double vmn = vml + cv * (mbI * dYm * a1 - d0);
-        double dd = (un - umn) * s.ix;
-        dd += (vn - vmn) * s.iy;
-        dd += (wn - wm2) * s.iz;
+        const T umn = uml + cu * (mbI * dXm * a1 - d0);
+        const T vmn = vml + cv * (mbI * dYm * a1 - d0);
+        T dd = (un - umn) * Tix;
+        dd += (vn - vmn) * Tiy;
+        dd += (wn - wm2) * Tiz;
         __stwb(Pn + o, pn);
         __stwb(Un + o, un);
         __stwb(Vn + o, vn);
         __stwb(Wn + o, wn);
         __stwb(Dn + o, dd);
         if (REMOTE) remote_store(z, un, vn, wn, dd);
-        const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
+        const unsigned long long b1 = abs_bits((double)dC), b2 = abs_bits((double)dd);
         r1 = b1 > r1 ? b1 : r1;
         r2 = b2 > r2 ? b2 : r2;
         wm2 = wn;
       } else if (act && z >= zf_lo && z <= zf_hi && !(per0 | per1)) {
         // boundary tile, interior plane: the general path's arithmetic with
         // per-thread scales, selects for the wall cases (see sc_ above)
-        const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
-        const double dXm = d1[q0 - 1], dYm = d1[q0 - EW], dZp = d1p[q0];
-        const double p0 = p1[q0], u0 = u1[q0], uml = u1[q0 - 1], v0 = v1[q0], vml = v1[q0 - EW], w0 = w1[q0];
+        const T dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
+        const T dXm = d1[q0 - 1], dYm = d1[q0 - EW], dZp = d1p[q0];
+        const T p0 = p1[q0], u0 = u1[q0], uml = u1[q0 - 1], v0 = v1[q0], vml = v1[q0 - EW], w0 = w1[q0];
         const int par = par_col ^ ((lo2 + z) & 1);
-        const double a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
-        const double d0 = sc_ * dC * a0;
-        const double exv = sex_ * dXp * a1;
-        const double eyv = sey_ * dYp * a1;
-        const double ezv = sc_ * dZp * a1;
-        const double pn = p0 + d0;
-        double un = u0 + cu * (d0 - exv);
-        double vn = v0 + cv * (d0 - eyv);
-        const double wn = w0 + cw * (d0 - ezv);
+        const T a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
+        const T d0 = sc_ * dC * a0;
+        const T exv = sex_ * dXp * a1;
+        const T eyv = sey_ * dYp * a1;
+        const T ezv = sc_ * dZp * a1;
+        const T pn = p0 + d0;
+        T un = u0 + cu * (d0 - exv);
+        T vn = v0 + cv * (d0 - eyv);
+        const T wn = w0 + cw * (d0 - ezv);
         un = xhi ? pin_u : un;
         vn = yhi ? pin_v : vn;
         // swept -x / -y neighbours (parity a1; 1 - a1 == a0 exactly); at a low
         // wall the pinned ghost
-        const double a1m = 1.0 - a1;
-        const double umr = uml + cu * (sxm_ * dXm * a1 - sxpm_ * dC * a1m);
-        const double vmr = vml + cv * (sym_ * dYm * a1 - sypm_ * dC * a1m);
-        const double umn = xlo ? uml : umr, vmn = ylo ? vml : vmr;
-        double dd = (un - umn) * s.ix;
-        dd += (vn - vmn) * s.iy;
-        dd += (wn - wm2) * s.iz;
+        const T a1m = 1.0 - a1;
+        const T umr = uml + cu * (sxm_ * dXm * a1 - sxpm_ * dC * a1m);
+        const T vmr = vml + cv * (sym_ * dYm * a1 - sypm_ * dC * a1m);
+        const T umn = xlo ? uml : umr, vmn = ylo ? vml : vmr;
+        T dd = (un - umn) * Tix;
+        dd += (vn - vmn) * Tiy;
+        dd += (wn - wm2) * Tiz;
         __stwb(Pn + o, pn);
         __stwb(Un + o, un);
         __stwb(Vn + o, vn);
@@ -610,50 +617,50 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         }
         if (xhi) Dn[o + 1] = dd;
         if (yhi) Dn[o + sx] = dd;
-        const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
+        const unsigned long long b1 = abs_bits((double)dC), b2 = abs_bits((double)dd);
         r1 = b1 > r1 ? b1 : r1;
         r2 = b2 > r2 ? b2 : r2;
         wm2 = wn;
       } else if (act) {
-        const double dZp = d1p[q0];
+        const T dZp = d1p[q0];
         const int gk = lo2 + z;
         const int bz = per2 | ((gk > 0) & (gk < nm2i)), bzp = per2 | (gk + 1 < nm2i);
-        const double dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
-        const double dXm = d1[q0 - 1], dYm = d1[q0 - EW];
+        const T dC = d1[q0], dXp = d1[q0 + 1], dYp = d1[q0 + EW];
+        const T dXm = d1[q0 - 1], dYm = d1[q0 - EW];
         const int par = par_col ^ (int)(gk & 1);
-        const double a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
-        const double d0 = smb[ic | bz] * dC * a0;
-        const double exv = smb[iex | bz] * dXp * a1;
-        const double eyv = smb[iey | bz] * dYp * a1;
-        const double ezv = smb[ic | bzp] * dZp * a1;
-        const double pn = p1[q0] + d0;
-        double un = u1[q0] + cu * (d0 - exv);
-        double vn = v1[q0] + cv * (d0 - eyv);
-        double wn = w1[q0] + cw * (d0 - ezv);
+        const T a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
+        const T d0 = smb[ic | bz] * dC * a0;
+        const T exv = smb[iex | bz] * dXp * a1;
+        const T eyv = smb[iey | bz] * dYp * a1;
+        const T ezv = smb[ic | bzp] * dZp * a1;
+        const T pn = p1[q0] + d0;
+        T un = u1[q0] + cu * (d0 - exv);
+        T vn = v1[q0] + cv * (d0 - eyv);
+        T wn = w1[q0] + cw * (d0 - ezv);
         if (xhi) un = pin_u;
         if (yhi) vn = pin_v;
         if (gk == N2m1) wn = pin_w;
         // swept -x / -y neighbours; at the low wall the pinned ghost (in S1)
-        double umn, vmn;
+        T umn, vmn;
         if (gi > 0 || per0) {
-          const double a0m = xm_same ? a0 : a1, a1m = 1.0 - a0m;
-          const double d0m = smb[ixm | bz] * dXm * a0m;
-          const double exm = smb[ixpm | bz] * dC * a1m;
+          const T a0m = xm_same ? a0 : a1, a1m = 1.0 - a0m;
+          const T d0m = smb[ixm | bz] * dXm * a0m;
+          const T exm = smb[ixpm | bz] * dC * a1m;
           umn = u1[q0 - 1] + cu * (d0m - exm);
         } else {
           umn = u1[q0 - 1];
         }
         if (gj > 0 || per1) {
-          const double a0m = ym_same ? a0 : a1, a1m = 1.0 - a0m;
-          const double d0m = smb[iym | bz] * dYm * a0m;
-          const double eym = smb[iypm | bz] * dC * a1m;
+          const T a0m = ym_same ? a0 : a1, a1m = 1.0 - a0m;
+          const T d0m = smb[iym | bz] * dYm * a0m;
+          const T eym = smb[iypm | bz] * dC * a1m;
           vmn = v1[q0 - EW] + cv * (d0m - eym);
         } else {
           vmn = v1[q0 - EW];
         }
-        double dd = (un - umn) * s.ix;
-        dd += (vn - vmn) * s.iy;
-        dd += (wn - wm2) * s.iz;
+        T dd = (un - umn) * Tix;
+        dd += (vn - vmn) * Tiy;
+        dd += (wn - wm2) * Tiz;
         __stwb(Pn + o, pn);
         __stwb(Un + o, un);
         __stwb(Vn + o, vn);
@@ -676,7 +683,7 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
         if (xhi) Dn[o + 1] = dd;
         if (yhi) Dn[o + sx] = dd;
         if (gk == N2m1) Dn[o + sxy] = dd;
-        const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
+        const unsigned long long b1 = abs_bits((double)dC), b2 = abs_bits((double)dd);
         r1 = b1 > r1 ? b1 : r1;
         r2 = b2 > r2 ? b2 : r2;
         wm2 = wn;
@@ -735,19 +742,29 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   }
 }
 
-void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                   sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
-                   unsigned total, const sweep2_remote* remote) {
-  if (nctas <= 0) return;
-  constexpr int TYV = kPassTY, NIN = kPassStages, MINB = kPassMinB;
-  using G = geom<TYV>;
+template <class T, int MINB>
+static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
+                    unsigned total, const sweep2_remote* remote) {
+  constexpr int TYV = kPassTY, NIN = kPassStages;
+  using G = geom<TYV, T>;
   const bool per = c.per[0] || c.per[1] || c.per[2];
-  auto k = remote ? (per ? k_sweep2<TYV, NIN, MINB, true, true> : k_sweep2<TYV, NIN, MINB, false, true>)
-                  : (per ? k_sweep2<TYV, NIN, MINB, true, false> : k_sweep2<TYV, NIN, MINB, false, false>);
+  auto k = remote ? (per ? k_sweep2<TYV, NIN, MINB, true, true, T> : k_sweep2<TYV, NIN, MINB, false, true, T>)
+                  : (per ? k_sweep2<TYV, NIN, MINB, true, false, T> : k_sweep2<TYV, NIN, MINB, false, false, T>);
   ensure_smem_attr((const void*)k, G::smem_bytes(NIN));
   k<<<nctas, dim3(G::TX, G::TY), G::smem_bytes(NIN), st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
                                                            total ? total : (unsigned)nctas,
                                                            static_cast<const maps2_t*>(maps), fin, pins, remote);
+}
+
+void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                   sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
+                   unsigned total, const sweep2_remote* remote, int es) {
+  if (nctas <= 0) return;
+  if (es == 4)  // fp32: half the shared memory per CTA (56 KB), up to 3 CTAs per SM
+    launch2<float, kPassMinB32>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total, remote);
+  else
+    launch2<double, kPassMinB>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total, remote);
 }
 
 }  // namespace sfb

@@ -1,5 +1,6 @@
 """The fp32 variant of the CFD fields (precision="f32": storage and arithmetic
-in fp32 on the fused TMA path) against the fp64 reference after N steps.
+in fp32 on the fused TMA path -- the temporal pass with fused = 1, the single
+half-sweep with fused = 3) against the fp64 reference after N steps.
 
 fp32 cannot reach the default pressure tolerance (max|div| 1e-6: roundoff x
 1/dx is ~6e-6 at 64^3; SURVEY.md §7 hard part 6), so the comparison uses the
@@ -72,31 +73,35 @@ def test_fp32_cavity64_fixed_work_within_stated_tolerance(ref_available, fused):
         assert e <= TOL[f], (f, e, TOL[f])
 
 
-def test_fp32_cavity64_ten_steps_within_stated_tolerance(ref_available):
+@pytest.mark.parametrize("fused", [1, 3])
+def test_fp32_cavity64_ten_steps_within_stated_tolerance(ref_available, fused):
     # a longer horizon: fp32 roundoff must not grow past the tolerance
-    errs = _compare(64, 200, 10)
+    errs = _compare(64, 200, 10, fused=fused)
     print("fp32 64^3 x 10 steps:", json.dumps(errs))
     for f, e in errs.items():
         assert e <= TOL[f], (f, e, TOL[f])
 
 
-def test_fp32_bench128_config_within_stated_tolerance(ref_available):
+@pytest.mark.parametrize("fused", [1, 3])
+def test_fp32_bench128_config_within_stated_tolerance(ref_available, fused):
     # runs/bench128.cfg: 128^3, omega 1.9525, 200 half-sweeps per step, 2 steps
-    errs = _compare(128, 200, 2)
+    errs = _compare(128, 200, 2, fused=fused)
     print("fp32 128^3 x 2 steps:", json.dumps(errs))
     for f, e in errs.items():
         assert e <= TOL[f], (f, e, TOL[f])
 
 
 def test_fp32_odd_extents_and_refresh_paths(ref_available):
-    # uneven tiles, quasi-2D symmetry faces, two grid components on the device
+    # uneven tiles, symmetry faces, two grid components on the device (the
+    # temporal pass with the fused exchange between them), an odd sweep cap
+    # (the redo of a pass's first sweep)
     n = (45, 37, 11)
-    c = cavity_case(n, workers=2, symmetry_z=True, omega=1.7, tolerance=1e-30, max_sweeps=60)
+    c = cavity_case(n, workers=2, symmetry_z=True, omega=1.7, tolerance=1e-30, max_sweeps=61)
     o = Oracle(c, "ref")
     o.init_cavity()
     o.advance(4)
-    cfg = sfb.SolverConfig(extents=n, reynolds=100.0, symmetry_z=True, omega=1.7, tolerance=1e-30, max_sweeps=60)
-    d = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=2, fused=3, precision="f32")
+    cfg = sfb.SolverConfig(extents=n, reynolds=100.0, symmetry_z=True, omega=1.7, tolerance=1e-30, max_sweeps=61)
+    d = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), workers=2, ghost=2, fused=1, precision="f32")
     d.init_cavity()
     d.advance(4)
     for f, e in field_errors(d, o).items():
