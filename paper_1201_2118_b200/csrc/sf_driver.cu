@@ -2435,6 +2435,18 @@ class simulation {
     SF_CK(cudaMemcpyAsync(all, h.data(), 8 * h.size(), cudaMemcpyHostToDevice, st_));
     SF_CK(cudaStreamSynchronize(st_));
   }
+  // open_ipc without throwing: false (and the CUDA error cleared) on failure
+  bool try_open_ipc(const cudaIpcMemHandle_t& h) {
+    const std::string key(reinterpret_cast<const char*>(&h), sizeof h);
+    if (ipc_open_.count(key)) return true;
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    ipc_open_[key] = p;
+    return true;
+  }
   void* open_ipc(const cudaIpcMemHandle_t& h) {
     const std::string key(reinterpret_cast<const char*>(&h), sizeof h);
     auto it = ipc_open_.find(key);
@@ -2606,6 +2618,7 @@ class simulation {
     download_table();
     ipc_field_rec me;
     std::memset(&me, 0, sizeof me);
+    int me_ok = 1;
     char hn[256] = {0};
     gethostname(hn, sizeof hn - 1);
     me.host = std::hash<std::string>()(std::string(hn));
@@ -2620,15 +2633,19 @@ class simulation {
         double* p = htab_->ptr[0][F4[k]][q];
         if (!p) continue;
         const int phys = htab_->bidx[0][F4[k]][q];
-        me.has[k][phys] = 1;
-        SF_CK(cudaIpcGetMemHandle(&me.h[k][phys], p));
+        if (cudaIpcGetMemHandle(&me.h[k][phys], p) == cudaSuccess) {
+          me.has[k][phys] = 1;
+        } else {  // not exportable: the collective decision falls back to the phases
+          cudaGetLastError();
+          me_ok = 0;
+        }
       }
     std::vector<ipc_field_rec> all((size_t)world_);
     host_allgather(&me, all.data(), sizeof me);
     const auto dirs = build_direct_plan(dec_, rank_);
     // every peer must be mappable here (same node, device visible and
     // peer-accessible, or the same device); the decision is collective
-    int ok = 1;
+    int ok = me_ok;
     for (const auto& dr : dirs) {
       const ipc_field_rec& r = all[(size_t)dr.peer];
       int dev = -1;
@@ -2642,6 +2659,11 @@ class simulation {
       for (int k = 0; k < 4; ++k)
         for (int q = 0; q < kSlots; ++q)
           if (me.has[k][q] != r.has[k][q]) can = 0;
+      // map every buffer now: a failure (driver, permissions) turns the
+      // collective decision below into the exchange phases on every rank
+      for (int k = 0; k < 4 && can; ++k)
+        for (int q = 0; q < kSlots && can; ++q)
+          if (r.has[k][q] && !try_open_ipc(r.h[k][q])) can = 0;
       ok = ok && can;
     }
     std::vector<int> oks((size_t)world_);
