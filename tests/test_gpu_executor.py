@@ -510,6 +510,30 @@ def test_fp32_fields_in_descriptor_stencils(radius, ghost, workers, tile, no_tma
     assert s.reduce("lu", "sum") == pytest.approx(float(np.sum(want)), rel=1e-12)
 
 
+# configs[4] in fp32 against the fp64 result (the stated tolerance of the fp32
+# variant): inputs rounded to fp32, every operation in fp32; the error is a few
+# fp32 ulps of the result's scale
+FP32_STENCIL_TOL = 1e-6  # max |lu_fp32 - lu_fp64| / max |lu_fp64|
+
+
+@pytest.mark.parametrize("radius", [2, 3])
+def test_fp32_stencil_within_the_stated_tolerance_of_fp64(radius):
+    ext = (48, 40, 36)
+    data = random_global(ext, 31)  # fp64 data: the fp32 run also rounds its inputs
+    s = rig(ext, 2, radius, (True, True, True))
+    s.create_field("u", dtype="f32")
+    s.create_field("lu", dtype="f32")
+    s.scatter("u", data)
+    s.register_kernel(Plan(f"LAP{2 * radius}T", (32, 16, 64), (radius,) * 6, [("u", "IN", True), ("lu", "OUT")]),
+                      (["u", "lu"], []), LAP4R if radius == 2 else LAP6R)
+    s.exchange(["u"])
+    s.run_kernel(f"LAP{2 * radius}T")
+    want = lap_np(data, radius)
+    err = float(np.max(np.abs(s.gather("lu") - want)) / np.max(np.abs(want)))
+    print(f"fp32 radius {radius} stencil: relative error {err:.3g}")
+    assert err <= FP32_STENCIL_TOL, err
+
+
 @pytest.mark.parametrize("radius", [2, 3])
 def test_mixed_precision_kernel_computes_in_fp64(radius):
     # an fp32 input with an fp64 output: accessors widen, the body runs in fp64;
