@@ -399,7 +399,8 @@ def run_ours(args):
         achieved = step_bytes / (ms_per_step / 1e3) / 1e9
     roofline = {
         "bound": "hbm",
-        "kernel": ("k_sweep2 (temporal pass: two fused half-sweeps per launch)" if kname == "sweep2"
+        "kernel": ("temporal pass, two fused half-sweeps per pass (one walled fp64 component: k_sweep2i over the "
+                   "interior tiles beside k_sweep2 over the boundary slabs, concurrent; else k_sweep2)" if kname == "sweep2"
                    else "whole step: persistent pressure loop k_pressure_loop (grid L2-resident; achieved = "
                         "step algorithmic bytes / step time)" if small
                    else "k_sweep_div (fused half-sweep)"),

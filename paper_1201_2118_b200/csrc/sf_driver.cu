@@ -1766,6 +1766,9 @@ class simulation {
   mutable unsigned long long compute_epoch_ = 1;
   unsigned long long table_epoch_ = 0;
   void* maps2_ = nullptr;  // temporal-pass descriptors (null: pass unavailable)
+  void* maps3_ = nullptr;  // descriptors of the interior form of the pass (sweep2i_box shapes)
+  int ibzc_ = 32;          // z chunk of the boundary slabs beside the interior form
+  const bool interior_env_ = getenv("SF_NO_INTERIOR_PASS") == nullptr;
   void* uvmaps_ = nullptr;  // TMA UPDATE_VELOCITY descriptors (null: plain-load kernel)
   cudaStream_t xs_ = nullptr;  // halo exchange overlapped with the temporal pass
   const bool overlap_env_ = getenv("SF_NO_OVERLAP") == nullptr;
@@ -2021,6 +2024,25 @@ class simulation {
       if (ok) {
         maps2_ = dalloc(hm.size());
         SF_CK(cudaMemcpy(maps2_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
+      }
+    }
+    // descriptors of the interior form of the pass (fp64, one component)
+    if (maps2_ && cfd_es_ == 8 && nloc_ == 1) {
+      std::vector<unsigned char> hm(sweep2_maps_bytes(), 0);
+      bool ok = true;
+      for (int f : {SF_VX, SF_VY, SF_VZ, SF_P, SF_DIVU})
+        for (int s = 0; s < kSlots && ok; ++s) {
+          double* p = htab_->ptr[0][f][s];
+          if (!p) continue;
+          const sf_layout& L = lay_[0];
+          int bw, bh;
+          sweep2i_box(f, &bw, &bh);
+          ok = bw <= L.sx && bh <= L.sy &&
+               encode_box_map(hm.data() + sweep2_map_offset(0, f, s), p, L.sx, L.sy, L.sz, bw, bh) == 0;
+        }
+      if (ok) {
+        maps3_ = dalloc(hm.size());
+        SF_CK(cudaMemcpy(maps3_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
       }
     }
     {
@@ -2366,6 +2388,87 @@ class simulation {
     items_.emplace(std::string(key) + ":i", mk(vi, ci));
     items_.emplace(std::string(key) + ":b", mk(vb, cb));
     return {&items_.find(std::string(key) + ":i")->second, &items_.find(std::string(key) + ":b")->second};
+  }
+
+  // The temporal pass over one walled component as two work sets: the interior
+  // tiles, where k_sweep2 takes its fast path everywhere (every widened cell
+  // inside [1, N-3] on x and y: i0 in [3, N-35], j0 in [3, N-11]; S0 planes
+  // k0-2 .. k1+1 inside [1, N-2] on z: planes [3, N-3)), for k_sweep2i, and
+  // the six boundary slabs around them for k_sweep2. {null, null} when it
+  // does not apply (fp32, several components, periodic axes, small grids).
+  std::pair<const work_set*, const work_set*> interior_split() {
+    if (!maps3_ || !interior_env_ || cfd_es_ != 8 || nloc_ != 1 || dist_ || !temporal() || has_proc_faces())
+      return {nullptr, nullptr};
+    if (cfg_.periodic[0] || cfg_.periodic[1] || cfg_.periodic[2]) return {nullptr, nullptr};
+    if (!xs_) {
+      SF_CK(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
+      SF_CK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+      SF_CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    }
+    const int ty = sweep2_tile_y(), zc = zc_pass();
+    // the slabs: 32-plane chunks, more CTAs to fill in beside the interior
+    // (measured per pass: 128 2.43 ms, 64 2.40, 32 2.40, 16 2.44, 8 2.54)
+    const int bzc = std::min(zc, 32);
+    ibzc_ = bzc;
+    char key[64];
+    std::snprintf(key, sizeof key, "isplit:%d:%d:%d", zc, ty, bzc);
+    auto ii = items_.find(std::string(key) + ":i");
+    if (ii != items_.end())
+      return ii->second.nctas ? std::make_pair(&ii->second, &items_.find(std::string(key) + ":b")->second)
+                              : std::make_pair((const work_set*)nullptr, (const work_set*)nullptr);
+    const auto n = dec_.dims(gid_[0]);
+    // interior tiles: i0 = ox + 32 a <= N - 35, j0 = oy + 8 b <= N - 11
+    // (tile origins 32 / 8: the tiles' rows stay 128-byte aligned; starting
+    // them at 4 / 4 shrinks the slabs but measured 4 % slower)
+    const i64 ox = kTX, oy = ty;
+    const i64 qx = n[0] >= ox + kTX + 3 ? (n[0] - 3 - kTX - ox) / kTX + 1 : 0;
+    const i64 qy = n[1] >= oy + ty + 3 ? (n[1] - 3 - ty - oy) / ty + 1 : 0;
+    const i64 ilo[3] = {ox, oy, 3}, ihi[3] = {ox + kTX * qx, oy + ty * qy, n[2] - 3};
+    std::vector<sf_work> vi, vb;
+    int ci = 0, cb = 0;
+    auto add = [&](std::vector<sf_work>& v, int& cta, const i64 lo[3], const i64 hi[3], int zcb) {
+      if (lo[0] >= hi[0] || lo[1] >= hi[1] || lo[2] >= hi[2]) return;
+      sf_work w{};
+      w.blk = 0;
+      w.cta_begin = cta;
+      for (int a = 0; a < 3; ++a) {
+        w.lo[a] = lo[a];
+        w.hi[a] = hi[a];
+      }
+      w.tiles[0] = (int)((hi[0] - lo[0] + kTX - 1) / kTX);
+      w.tiles[1] = (int)((hi[1] - lo[1] + ty - 1) / ty);
+      w.tiles[2] = (int)((hi[2] - lo[2] + zcb - 1) / zcb);
+      cta += w.tiles[0] * w.tiles[1] * w.tiles[2];
+      v.push_back(w);
+    };
+    if (qx > 0 && qy > 0 && ihi[2] > ilo[2]) {
+      add(vi, ci, ilo, ihi, zc);
+      const i64 z0[3] = {0, 0, 0}, zl[3] = {n[0], n[1], ilo[2]};
+      const i64 z1[3] = {0, 0, ihi[2]}, zh[3] = {n[0], n[1], n[2]};
+      add(vb, cb, z0, zl, bzc);
+      add(vb, cb, z1, zh, bzc);
+      const i64 y0[3] = {0, 0, ilo[2]}, yl[3] = {n[0], ilo[1], ihi[2]};
+      const i64 y1[3] = {0, ihi[1], ilo[2]}, yh[3] = {n[0], n[1], ihi[2]};
+      add(vb, cb, y0, yl, bzc);
+      add(vb, cb, y1, yh, bzc);
+      const i64 x0[3] = {0, ilo[1], ilo[2]}, xl[3] = {ilo[0], ihi[1], ihi[2]};
+      const i64 x1[3] = {ihi[0], ilo[1], ilo[2]}, xh[3] = {n[0], ihi[1], ihi[2]};
+      add(vb, cb, x0, xl, bzc);
+      add(vb, cb, x1, xh, bzc);
+    }
+    auto mk = [&](std::vector<sf_work>& v, int nctas) {
+      work_set ws;
+      ws.n = (int)v.size();
+      ws.nctas = nctas;
+      if (!v.empty()) {
+        ws.d = (sf_work*)dalloc(sizeof(sf_work) * v.size());
+        SF_CK(cudaMemcpy(ws.d, v.data(), sizeof(sf_work) * v.size(), cudaMemcpyHostToDevice));
+      }
+      return ws;
+    };
+    items_.emplace(std::string(key) + ":i", mk(vi, ci));
+    items_.emplace(std::string(key) + ":b", mk(vb, cb));
+    return interior_split();
   }
 
   // max over ranks of n accumulators (IEEE bit patterns of |x|): order-free,
@@ -2783,7 +2886,27 @@ class simulation {
       return 1;
     }
     const int fin = dist_ ? 0 : 1;
-    if (!has_proc_faces()) {
+    const auto split = interior_split();
+    if (!has_proc_faces() && split.first) {
+      // the interior tiles on the interior form (3 CTAs per SM), the boundary
+      // slabs on k_sweep2 on the second stream at the same time; one
+      // last-CTA count spans both launches
+      const work_set& wi = *split.first;
+      const work_set& wb = *split.second;
+      const unsigned total = (unsigned)(wi.nctas + wb.nctas);
+      if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
+      // boundary slabs first on the second stream, the interior beside them
+      // (measured: concurrent 2.40 ms, either order on one stream 2.58 ms)
+      SF_CK(cudaEventRecord(ev_fork_, st_));
+      SF_CK(cudaStreamWaitEvent(xs_, ev_fork_, 0));
+      launch_sweep2(tview(wb), wb.nctas, ibzc_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), xs_, total,
+                    nullptr, cfd_es_);
+      launch_sweep2i(tview(wi), wi.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps3_, fin, st_, total);
+      SF_CK(cudaEventRecord(ev_join_, xs_));
+      SF_CK(cudaStreamWaitEvent(st_, ev_join_, 0));
+      if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
+      launches_ += 2;
+    } else if (!has_proc_faces()) {
       const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass(), kTX, sweep2_tile_y());
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
       launch_sweep2(tview(ws), ws.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_, 0,

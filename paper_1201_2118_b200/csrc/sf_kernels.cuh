@@ -101,6 +101,13 @@ struct sweep2_remote {
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
                    unsigned total_ctas = 0, const sweep2_remote* remote = nullptr, int es = 8);
+// The interior form of the temporal pass (fp64; tiles where k_sweep2 takes its
+// fast path everywhere): no S1 field ring, 3 CTAs per SM. maps: a maps table
+// with sweep2i_box shapes; total: CTAs of the whole pass (with the k_sweep2
+// launch over the boundary slabs).
+void launch_sweep2i(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                    sf_host_flag* hflag, const void* maps, int fin, cudaStream_t st, unsigned total);
+void sweep2i_box(int field, int* bw, int* bh);
 size_t sweep2_maps_bytes();
 size_t sweep2_map_offset(int b, int f, int s);
 void sweep2_box(int field, int* bw, int* bh, int es = 8);

@@ -117,6 +117,56 @@ void sweep2_box(int field, int* bw, int* bh, int es) {
 // every warp does three cell updates per phase. Rings: S0 planes in q % NIN
 // (NIN >= 3), S1 fields (u1 v1 w1 p1) in m % 4, divu1 in m % 3 -- the slot a
 // phase overwrites was last read before the previous barrier.
+// The end of a temporal pass (every CTA of every launch of the pass): fold
+// both sweeps' residual maxima; with finalize, the last CTA evaluates both loop
+// tests (cfd.hpp:295-303): stop after sweep A (S0 intact: the single kernel
+// redoes it, ctl->redo), or count both sweeps and swap FRONT/ALT. Across ranks
+// (finalize 0) the caller allreduces acc[0..1] and runs CTL_FINISH_PASS.
+__device__ __forceinline__ void pass_finalize(unsigned long long (&rr)[2], sf_dev_table* tab, sf_dev_ctl* ctl,
+                                              sf_host_flag* hflag, unsigned total_ctas, int finalize) {
+  block_max_atomic<2>(rr, &ctl->acc[0]);
+  if (!finalize) return;
+  if (last_cta(&ctl->ctas_done, total_ctas)) {
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      __threadfence();
+      const double res1 = bits_to_max(*reinterpret_cast<volatile unsigned long long*>(&ctl->acc[0]));
+      const double res2 = bits_to_max(*reinterpret_cast<volatile unsigned long long*>(&ctl->acc[1]));
+      ctl->acc[0] = 0ull;
+      ctl->acc[1] = 0ull;
+      ctl->ctas_done = 0u;
+      const int sw = ctl->sweeps;
+      if (!((res1 > ctl->tolerance) && (sw + 1 < ctl->max_sweeps))) {
+        ctl->sweeps = sw + 1;
+        ctl->residual = res1;
+        ctl->color ^= 1;
+        ctl->done = 1;
+        ctl->redo = 1;
+      } else {
+        ctl->sweeps = sw + 2;
+        ctl->residual = res2;
+        const int more = (res2 > ctl->tolerance) && (sw + 2 < ctl->max_sweeps);
+        ctl->done = more ? 0 : 1;
+        for (int q = 0; q < tab->nblocks; ++q)
+          for (int f = 0; f < 5; ++f) {
+            double* tmp = tab->ptr[q][f][FRONT];
+            tab->ptr[q][f][FRONT] = tab->ptr[q][f][ALT];
+            tab->ptr[q][f][ALT] = tmp;
+            const unsigned char ti = tab->bidx[q][f][FRONT];
+            tab->bidx[q][f][FRONT] = tab->bidx[q][f][ALT];
+            tab->bidx[q][f][ALT] = ti;
+          }
+      }
+      if (hflag) {
+        hflag->sweeps = ctl->sweeps;
+        hflag->residual = ctl->residual;
+        hflag->done = ctl->done;
+        hflag->color = ctl->color;
+        __threadfence_system();
+      }
+    }
+  }
+}
+
 // REMOTE: the outputs of cells within g of a processor face also go straight
 // into the neighbours' ghost shells (sweep2_remote), up to 7 directions per
 // cell (face, edges, corner): the ghost exchange of the next pass fused into
@@ -698,48 +748,262 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
   // peers wait for
   if (REMOTE) __threadfence_system();
   unsigned long long rr[2] = {r1, r2};
-  block_max_atomic<2>(rr, &ctl->acc[0]);
-  if (!finalize) return;  // across ranks: allreduce acc[0..1], then CTL_FINISH_PASS
-  if (last_cta(&ctl->ctas_done, total_ctas)) {
-    if (tid == 0) {
-      __threadfence();
-      const double res1 = bits_to_max(*reinterpret_cast<volatile unsigned long long*>(&ctl->acc[0]));
-      const double res2 = bits_to_max(*reinterpret_cast<volatile unsigned long long*>(&ctl->acc[1]));
-      ctl->acc[0] = 0ull;
-      ctl->acc[1] = 0ull;
-      ctl->ctas_done = 0u;
-      const int sw = ctl->sweeps;
-      if (!((res1 > ctl->tolerance) && (sw + 1 < ctl->max_sweeps))) {
-        // the loop stops after sweep A: S0 is intact, the single kernel redoes A
-        ctl->sweeps = sw + 1;
-        ctl->residual = res1;
-        ctl->color ^= 1;
-        ctl->done = 1;
-        ctl->redo = 1;
-      } else {
-        ctl->sweeps = sw + 2;
-        ctl->residual = res2;
-        const int more = (res2 > ctl->tolerance) && (sw + 2 < ctl->max_sweeps);
-        ctl->done = more ? 0 : 1;
-        for (int q = 0; q < tab->nblocks; ++q)
-          for (int f = 0; f < 5; ++f) {
-            double* tmp = tab->ptr[q][f][FRONT];
-            tab->ptr[q][f][FRONT] = tab->ptr[q][f][ALT];
-            tab->ptr[q][f][ALT] = tmp;
-            const unsigned char ti = tab->bidx[q][f][FRONT];
-            tab->bidx[q][f][FRONT] = tab->bidx[q][f][ALT];
-            tab->bidx[q][f][ALT] = ti;
-          }
-      }
-      if (hflag) {
-        hflag->sweeps = ctl->sweeps;
-        hflag->residual = ctl->residual;
-        hflag->done = ctl->done;
-        hflag->color = ctl->color;
-        __threadfence_system();
-      }
+  pass_finalize(rr, tab, ctl, hflag, total_ctas, finalize);
+}
+
+// ---------------------------------------------------------------------------
+// The interior form of the temporal pass (fp64). Tiles whose widened region
+// lies inside the domain on x and y and whose S0 planes k0-2 .. k1+1 are
+// interior in z take k_sweep2's fast path everywhere; for them this kernel
+// drops the S1 field ring. Each thread keeps its own tile cell's sweep-A
+// values (p1, u1, v1, w1 and the -x / -y neighbours' u1, v1) in registers from
+// the plane it computes them to the plane sweep B consumes them, and computes
+// the neighbours' values it needs from S0 with the same IEEE operations as the
+// fast path (the -x neighbour's +x term IS this cell's d0). Shared memory holds
+// a 4-stage S0 ring (p only over the tile, u and w one row shorter) and a
+// 3-slot divu1 ring over the tile and its 1-cell ring: 65 KB, so 3 CTAs (24
+// warps) per SM instead of 2 (16). Bitwise the fast path of k_sweep2.
+namespace ig {
+constexpr int TX = 32, TY = 8, NT = TX * TY;
+constexpr int RW = TX + 2, RH = TY + 2, RN = RW * RH;  // divu1 region: x from i0-1, y from j0-1
+constexpr int R2N = RN - NT;                            // its ring cells (84), one more per thread 0..83
+constexpr int BW = TX + 4;                              // S0 box width, x from i0-2
+constexpr int DH = TY + 4, UH = TY + 2, VH = TY + 3, WH = TY + 2;  // divu, vx, vy, vz box heights
+constexpr int O_D = 0, O_U = r128(8 * BW * DH), O_V = O_U + r128(8 * BW * UH), O_W = O_V + r128(8 * BW * VH);
+constexpr int O_P = O_W + r128(8 * BW * WH);
+constexpr int ST_BYTES = O_P + r128(8 * TX * TY);
+constexpr uint32_t ST_TX = 8u * (BW * DH + BW * UH + BW * VH + BW * WH + TX * TY);
+constexpr int D1_BYTES = r128(8 * RN);
+constexpr int NIN = 4;
+constexpr int SMEM = NIN * ST_BYTES + 3 * D1_BYTES;
+}  // namespace ig
+
+__global__ void __launch_bounds__(ig::NT, 3)
+    k_sweep2i(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc, sf_consts s,
+              sf_dev_ctl* ctl, sf_host_flag* hflag, unsigned int total_ctas, const maps2_t* __restrict__ maps,
+              int finalize) {
+  using namespace ig;
+  if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) uint64_t bars[NIN];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+  const sf_work& wk = items[nitems > 1 ? find_item(items, nitems, blockIdx.x) : 0];
+  const int local = blockIdx.x - wk.cta_begin;
+  const int tix = local % wk.tiles[0], tiy = (local / wk.tiles[0]) % wk.tiles[1];
+  const int tiz = local / (wk.tiles[0] * wk.tiles[1]);
+  const int i0 = (int)wk.lo[0] + tix * TX, j0 = (int)wk.lo[1] + tiy * TY;
+  const int k0 = (int)wk.lo[2] + tiz * zc;
+  const int k1 = (int)min((long long)k0 + zc, wk.hi[2]);
+  const int nplanes = k1 - k0;
+  const int b = wk.blk;
+  const sf_dev_block& B = tab->blk[b];
+  const double beta = ctl->beta, dt = ctl->dt;
+  const int colA = ctl->color, colB = colA ^ 1;
+  const double cu = dt * s.ix, cv = dt * s.iy, cw = dt * s.iz;
+  const double mbI = -(beta * s.bscale[1][1][1]);  // every scale of an interior cell (cfd.hpp:712-715)
+  if (tid == 0) {
+    for (int q = 0; q < NIN; ++q) bar_init(&bars[q]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // S0 plane q holds z = k0 - 2 + q (q = 0 .. nplanes + 3)
+  const int xo = (int)(B.base % B.sx), g = B.g;
+  const int xs = xo + i0 - 2, ys = g + j0 - 2, zs = g + k0 - 2;
+  const CUtensorMap* mD = &maps->m[b][SF_DIVU][tab->bidx[b][SF_DIVU][FRONT]];
+  const CUtensorMap* mU = &maps->m[b][SF_VX][tab->bidx[b][SF_VX][FRONT]];
+  const CUtensorMap* mV = &maps->m[b][SF_VY][tab->bidx[b][SF_VY][FRONT]];
+  const CUtensorMap* mW = &maps->m[b][SF_VZ][tab->bidx[b][SF_VZ][FRONT]];
+  const CUtensorMap* mP = &maps->m[b][SF_P][tab->bidx[b][SF_P][FRONT]];
+  const int nin = nplanes + 4;
+  auto issue = [&](int q) {
+    if (q >= nin) return;
+    unsigned char* st = sm + (q % NIN) * ST_BYTES;
+    uint64_t* bar = &bars[q % NIN];
+    bar_expect(bar, ST_TX);
+    tma3(st + O_D, mD, bar, xs, ys, zs + q);
+    tma3(st + O_U, mU, bar, xs, ys + 1, zs + q);
+    tma3(st + O_V, mV, bar, xs, ys, zs + q);
+    tma3(st + O_W, mW, bar, xs, ys + 1, zs + q);
+    tma3(st + O_P, mP, bar, xs + 2, ys + 2, zs + q);
+  };
+  const uint32_t bar0 = smem32(&bars[0]);
+  auto wait_in = [&](int q) {
+    if (q < nin) {
+      const uint32_t a = bar0 + 8u * (uint32_t)(q % NIN), par = (uint32_t)((q / NIN) & 1);
+      asm volatile(
+          "{\n .reg .pred P1;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+          " @!P1 bra W_%=;\n}\n" ::"r"(a),
+          "r"(par)
+          : "memory");
+    }
+  };
+  if (tid == 0)
+    for (int q = 0; q < NIN; ++q) issue(q);
+
+  const double* const S = reinterpret_cast<const double*>(sm);
+  double* const D1 = reinterpret_cast<double*>(sm + NIN * ST_BYTES);
+  constexpr int SST = ST_BYTES / 8, SD1 = D1_BYTES / 8;
+
+  // the two divu1-region cells of this thread: its tile cell (A) and, for
+  // tid < 84, one cell of the region's 1-cell ring (R)
+  const int rA = (ty + 1) * RW + (tx + 1);
+  const int rR = tid < RW ? tid
+                 : tid < 2 * RW ? (RH - 1) * RW + (tid - RW)
+                 : tid < 2 * RW + (RH - 2) ? (tid - 2 * RW + 1) * RW
+                 : (tid - 2 * RW - (RH - 2) + 1) * RW + (RW - 1);
+  const bool hasR = tid < R2N;
+  auto dv = [](int r) { return (r / RW + 1) * BW + (r % RW) + 1; };  // divu / vy box element (rows from j0-2)
+  auto uw = [](int r) { return (r / RW) * BW + (r % RW) + 1; };      // vx / vz box element (rows from j0-1)
+  const int dA = dv(rA), uA = uw(rA), pA = ty * TX + tx;
+  const int dR = dv(rR), uR = uw(rR);
+  const int gi = (int)B.lo[0] + i0 + tx, gj = (int)B.lo[1] + j0 + ty;
+  const int parA = (gi + gj) & 1;
+  const int parR = ((int)B.lo[0] + i0 - 1 + rR % RW + (int)B.lo[1] + j0 - 1 + rR / RW) & 1;
+  const int gk0 = (int)B.lo[2] + k0;  // global z of local plane k0
+
+  // sweep A (colour colA, cfd.hpp:699-719) at a region cell on S0 stage st
+  // (plane z) with stn (plane z+1): its u1, v1, w1 and the swept -x / -y
+  // neighbours' u1, v1 (their parity is the complement; their +x / +y term is
+  // this cell's d0, the identical product)
+  auto sweepA = [&](int st, int stn, int d, int uo, int par, int zpar, double& u, double& v, double& w,
+                    double& um, double& vm, double& d0) {
+    const double dc = S[st + O_D / 8 + d], dxp = S[st + O_D / 8 + d + 1], dyp = S[st + O_D / 8 + d + BW];
+    const double dzp = S[stn + O_D / 8 + d], dxm = S[st + O_D / 8 + d - 1], dym = S[st + O_D / 8 + d - BW];
+    const double uu = S[st + O_U / 8 + uo], uum = S[st + O_U / 8 + uo - 1];
+    const double vv = S[st + O_V / 8 + d], vvm = S[st + O_V / 8 + d - BW], ww = S[st + O_W / 8 + uo];
+    const double a0 = ((par ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
+    d0 = mbI * dc * a0;
+    const double exv = mbI * dxp * a1;
+    const double eyv = mbI * dyp * a1;
+    const double ezv = mbI * dzp * a1;
+    u = uu + cu * (d0 - exv);
+    v = vv + cv * (d0 - eyv);
+    w = ww + cw * (d0 - ezv);
+    um = uum + cu * (mbI * dxm * a1 - d0);
+    vm = vvm + cv * (mbI * dym * a1 - d0);
+  };
+  // DIVERGENCE of S1 (cfd.hpp:605-608)
+  auto div1 = [&](double u, double um, double v, double vm, double w, double wbelow) {
+    double dd = (u - um) * s.ix;
+    dd += (v - vm) * s.iy;
+    dd += (w - wbelow) * s.iz;
+    return dd;
+  };
+
+  // prologue: w1 of plane k0-2 (for the divergence at k0-1), then plane k0-1
+  wait_in(0);
+  wait_in(1);
+  wait_in(2);
+  double cp, cu1, cv1, cw1, cum, cvm;  // this cell's S1 at the plane sweep B handles next
+  double wA, wR = 0.0;                 // w1 one plane below (tile cell, ring cell)
+  {
+    double u, v, um, vm, d0;
+    sweepA(0, SST, dA, uA, parA, (gk0 - 2) & 1, u, v, wA, um, vm, d0);
+    if (hasR) sweepA(0, SST, dR, uR, parR, (gk0 - 2) & 1, u, v, wR, um, vm, d0);
+    double d0A;
+    sweepA(SST, 2 * SST, dA, uA, parA, (gk0 - 1) & 1, cu1, cv1, cw1, cum, cvm, d0A);
+    cp = S[SST + O_P / 8 + pA] + d0A;
+    D1[rA] = div1(cu1, cum, cv1, cvm, cw1, wA);
+    wA = cw1;
+    if (hasR) {
+      double w;
+      sweepA(SST, 2 * SST, dR, uR, parR, (gk0 - 1) & 1, u, v, w, um, vm, d0);
+      D1[rR] = div1(u, um, v, vm, w, wR);
+      wR = w;
     }
   }
+  __syncthreads();
+  if (tid == 0) {  // S0 planes 0 and 1 are consumed
+    issue(NIN);
+    issue(NIN + 1);
+  }
+
+  const int i = i0 + tx, j = j0 + ty;
+  double* __restrict__ Dn = tab->ptr[b][SF_DIVU][ALT];
+  double* __restrict__ Pn = tab->ptr[b][SF_P][ALT];
+  double* __restrict__ Un = tab->ptr[b][SF_VX][ALT];
+  double* __restrict__ Vn = tab->ptr[b][SF_VY][ALT];
+  double* __restrict__ Wn = tab->ptr[b][SF_VZ][ALT];
+  const unsigned sxy = (unsigned)(B.sx * B.sy);
+  unsigned o = (unsigned)(B.base + ((long long)k0 * B.sy + j) * B.sx + i);
+  unsigned long long r1 = 0ull, r2 = 0ull;
+  double wm2 = 0.0;  // swept w2 of the -z neighbour
+  // iteration t: sweep A on plane m+1 = k0+t (S0 planes t+2, t+3) and its
+  // divergence into divu1 slot (t+1) % 3; barrier; sweep B on plane m = k0-1+t
+  // (divu1 slots t % 3, (t+1) % 3), or at t = 0 the -z neighbour's swept w
+  int s0 = 2 % NIN, s1 = 3 % NIN;  // stages of S0 planes t+2, t+3
+  int dcur = 0, dnxt = 1;          // divu1 slots of planes m, m+1
+  for (int t = 0; t <= nplanes; ++t) {
+    wait_in(t + 3);
+    const int zp = (gk0 + t) & 1;
+    double np, nu1, nv1, nw1, num, nvm;
+    {
+      double d0A;
+      sweepA(s0 * SST, s1 * SST, dA, uA, parA, zp, nu1, nv1, nw1, num, nvm, d0A);
+      np = S[s0 * SST + O_P / 8 + pA] + d0A;
+      D1[dnxt * SD1 + rA] = div1(nu1, num, nv1, nvm, nw1, wA);
+      wA = nw1;
+      if (hasR) {
+        double u, v, w, um, vm, d0;
+        sweepA(s0 * SST, s1 * SST, dR, uR, parR, zp, u, v, w, um, vm, d0);
+        D1[dnxt * SD1 + rR] = div1(u, um, v, vm, w, wR);
+        wR = w;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) issue(t + 2 + NIN);  // S0 plane t+2 is consumed
+    const double* d1 = D1 + dcur * SD1;
+    const double* d1p = D1 + dnxt * SD1;
+    if (t == 0) {
+      // swept w2 of the plane below the chunk: sweep B's -z neighbour at k0
+      const double a0m = (((gi + gj + gk0 - 1) & 1) == colB) ? 1.0 : 0.0, a1m = 1.0 - a0m;
+      const double d0m = mbI * d1[rA] * a0m;
+      const double ezm = mbI * d1p[rA] * a1m;
+      wm2 = cw1 + cw * (d0m - ezm);
+    } else {
+      // sweep B on plane m = k0 + t - 1 (k_sweep2's interior fast path)
+      const double dC = d1[rA], dXp = d1[rA + 1], dYp = d1[rA + RW];
+      const double dXm = d1[rA - 1], dYm = d1[rA - RW], dZp = d1p[rA];
+      const int par = (parA ^ ((gk0 + t - 1) & 1));
+      const double a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
+      const double d0 = mbI * dC * a0;
+      const double exv = mbI * dXp * a1;
+      const double eyv = mbI * dYp * a1;
+      const double ezv = mbI * dZp * a1;
+      const double pn = cp + d0;
+      const double un = cu1 + cu * (d0 - exv);
+      const double vn = cv1 + cv * (d0 - eyv);
+      const double wn = cw1 + cw * (d0 - ezv);
+      const double umn = cum + cu * (mbI * dXm * a1 - d0);
+      const double vmn = cvm + cv * (mbI * dYm * a1 - d0);
+      double dd = (un - umn) * s.ix;
+      dd += (vn - vmn) * s.iy;
+      dd += (wn - wm2) * s.iz;
+      __stwb(Pn + o, pn);
+      __stwb(Un + o, un);
+      __stwb(Vn + o, vn);
+      __stwb(Wn + o, wn);
+      __stwb(Dn + o, dd);
+      const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
+      r1 = b1 > r1 ? b1 : r1;
+      r2 = b2 > r2 ? b2 : r2;
+      wm2 = wn;
+      o += sxy;
+    }
+    cp = np;
+    cu1 = nu1;
+    cv1 = nv1;
+    cw1 = nw1;
+    cum = num;
+    cvm = nvm;
+    s0 = s1;
+    s1 = s1 + 1 == NIN ? 0 : s1 + 1;
+    dcur = dnxt;
+    dnxt = dnxt == 2 ? 0 : dnxt + 1;
+  }
+  unsigned long long rr[2] = {r1, r2};
+  pass_finalize(rr, tab, ctl, hflag, total_ctas, finalize);
 }
 
 template <class T, int MINB>
@@ -755,6 +1019,26 @@ static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c,
   k<<<nctas, dim3(G::TX, G::TY), G::smem_bytes(NIN), st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
                                                            total ? total : (unsigned)nctas,
                                                            static_cast<const maps2_t*>(maps), fin, pins, remote);
+}
+
+void sweep2i_box(int field, int* bw, int* bh) {
+  using namespace ig;
+  switch (field) {
+    case SF_DIVU: *bw = BW; *bh = DH; break;
+    case SF_VX: *bw = BW; *bh = UH; break;
+    case SF_VY: *bw = BW; *bh = VH; break;
+    case SF_VZ: *bw = BW; *bh = WH; break;
+    default: *bw = TX; *bh = TY; break;
+  }
+}
+
+void launch_sweep2i(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                    sf_host_flag* hflag, const void* maps, int fin, cudaStream_t st, unsigned total) {
+  if (nctas <= 0) return;
+  ensure_smem_attr((const void*)k_sweep2i, ig::SMEM);
+  k_sweep2i<<<nctas, dim3(ig::TX, ig::TY), ig::SMEM, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
+                                                           total ? total : (unsigned)nctas,
+                                                           static_cast<const maps2_t*>(maps), fin);
 }
 
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
