@@ -2026,8 +2026,8 @@ class simulation {
         SF_CK(cudaMemcpy(maps2_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
       }
     }
-    // descriptors of the interior form of the pass (fp64, one component)
-    if (maps2_ && cfd_es_ == 8 && nloc_ == 1) {
+    // descriptors of the interior form of the pass (one component)
+    if (maps2_ && nloc_ == 1) {
       std::vector<unsigned char> hm(sweep2_maps_bytes(), 0);
       bool ok = true;
       for (int f : {SF_VX, SF_VY, SF_VZ, SF_P, SF_DIVU})
@@ -2036,9 +2036,9 @@ class simulation {
           if (!p) continue;
           const sf_layout& L = lay_[0];
           int bw, bh;
-          sweep2i_box(f, &bw, &bh);
+          sweep2i_box(f, &bw, &bh, cfd_es_);
           ok = bw <= L.sx && bh <= L.sy &&
-               encode_box_map(hm.data() + sweep2_map_offset(0, f, s), p, L.sx, L.sy, L.sz, bw, bh) == 0;
+               encode_box_map(hm.data() + sweep2_map_offset(0, f, s), p, L.sx, L.sy, L.sz, bw, bh, cfd_es_) == 0;
         }
       if (ok) {
         maps3_ = dalloc(hm.size());
@@ -2397,7 +2397,7 @@ class simulation {
   // the six boundary slabs around them for k_sweep2. {null, null} when it
   // does not apply (fp32, several components, periodic axes, small grids).
   std::pair<const work_set*, const work_set*> interior_split() {
-    if (!maps3_ || !interior_env_ || cfd_es_ != 8 || nloc_ != 1 || dist_ || !temporal() || has_proc_faces())
+    if (!maps3_ || !interior_env_ || nloc_ != 1 || dist_ || !temporal() || has_proc_faces())
       return {nullptr, nullptr};
     if (cfg_.periodic[0] || cfg_.periodic[1] || cfg_.periodic[2]) return {nullptr, nullptr};
     if (!xs_) {
@@ -2901,7 +2901,7 @@ class simulation {
       SF_CK(cudaStreamWaitEvent(xs_, ev_fork_, 0));
       launch_sweep2(tview(wb), wb.nctas, ibzc_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), xs_, total,
                     nullptr, cfd_es_);
-      launch_sweep2i(tview(wi), wi.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps3_, fin, st_, total);
+      launch_sweep2i(tview(wi), wi.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps3_, fin, st_, total, cfd_es_);
       SF_CK(cudaEventRecord(ev_join_, xs_));
       SF_CK(cudaStreamWaitEvent(st_, ev_join_, 0));
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));

@@ -106,8 +106,8 @@ void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, 
 // with sweep2i_box shapes; total: CTAs of the whole pass (with the k_sweep2
 // launch over the boundary slabs).
 void launch_sweep2i(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                    sf_host_flag* hflag, const void* maps, int fin, cudaStream_t st, unsigned total);
-void sweep2i_box(int field, int* bw, int* bh);
+                    sf_host_flag* hflag, const void* maps, int fin, cudaStream_t st, unsigned total, int es = 8);
+void sweep2i_box(int field, int* bw, int* bh, int es = 8);
 size_t sweep2_maps_bytes();
 size_t sweep2_map_offset(int b, int f, int s);
 void sweep2_box(int field, int* bw, int* bh, int es = 8);

@@ -763,26 +763,37 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
 // a 4-stage S0 ring (p only over the tile, u and w one row shorter) and a
 // 3-slot divu1 ring over the tile and its 1-cell ring: 65 KB, so 3 CTAs (24
 // warps) per SM instead of 2 (16). Bitwise the fast path of k_sweep2.
-namespace ig {
-constexpr int TX = 32, TY = 8, NT = TX * TY;
-constexpr int RW = TX + 2, RH = TY + 2, RN = RW * RH;  // divu1 region: x from i0-1, y from j0-1
-constexpr int R2N = RN - NT;                            // its ring cells (84), one more per thread 0..83
-constexpr int BW = TX + 4;                              // S0 box width, x from i0-2
-constexpr int DH = TY + 4, UH = TY + 2, VH = TY + 3, WH = TY + 2;  // divu, vx, vy, vz box heights
-constexpr int O_D = 0, O_U = r128(8 * BW * DH), O_V = O_U + r128(8 * BW * UH), O_W = O_V + r128(8 * BW * VH);
-constexpr int O_P = O_W + r128(8 * BW * WH);
-constexpr int ST_BYTES = O_P + r128(8 * TX * TY);
-constexpr uint32_t ST_TX = 8u * (BW * DH + BW * UH + BW * VH + BW * WH + TX * TY);
-constexpr int D1_BYTES = r128(8 * RN);
-constexpr int NIN = 4;
-constexpr int SMEM = NIN * ST_BYTES + 3 * D1_BYTES;
-}  // namespace ig
+// Geometry for element type T: the boxes start XA = 16 / sizeof(T) cells
+// left of the tile's x (a 16-byte aligned TMA start; 2 fp64, 4 fp32), i.e. the
+// cells of a row sit XSH = XA - 2 further in than for fp64.
+template <class T>
+struct ig {
+  static constexpr int ES = (int)sizeof(T), XA = 16 / ES, XSH = XA - 2;
+  static constexpr int TX = 32, TY = 8, NT = TX * TY;
+  static constexpr int RW = TX + 2, RH = TY + 2, RN = RW * RH;  // divu1 region: x from i0-1, y from j0-1
+  static constexpr int R2N = RN - NT;                            // its ring cells (84), one more per thread 0..83
+  static constexpr int BW = (TX + 4 + XSH + XA - 1) / XA * XA;   // S0 box width, x from i0-2-XSH: 36 / 40
+  static constexpr int DH = TY + 4, UH = TY + 2, VH = TY + 3, WH = TY + 2;  // divu, vx, vy, vz box heights
+  static constexpr int O_D = 0, O_U = r128(ES * BW * DH), O_V = O_U + r128(ES * BW * UH);
+  static constexpr int O_W = O_V + r128(ES * BW * VH), O_P = O_W + r128(ES * BW * WH);
+  static constexpr int ST_BYTES = O_P + r128(ES * TX * TY);
+  static constexpr uint32_t ST_TX = (uint32_t)ES * (BW * DH + BW * UH + BW * VH + BW * WH + TX * TY);
+  static constexpr int D1_BYTES = r128(ES * RN);
+  static constexpr int NIN = 4;
+  static constexpr int SMEM = NIN * ST_BYTES + 3 * D1_BYTES;
+  static constexpr int MINB = ES == 8 ? 3 : 4;  // CTAs per SM the registers are budgeted for
+};
 
-__global__ void __launch_bounds__(ig::NT, 3)
+template <class T>
+__global__ void __launch_bounds__(ig<T>::NT, ig<T>::MINB)
     k_sweep2i(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc, sf_consts s,
               sf_dev_ctl* ctl, sf_host_flag* hflag, unsigned int total_ctas, const maps2_t* __restrict__ maps,
               int finalize) {
-  using namespace ig;
+  using G = ig<T>;
+  constexpr int TX = G::TX, TY = G::TY, RW = G::RW, RH = G::RH, R2N = G::R2N, BW = G::BW, XSH = G::XSH;
+  constexpr int O_D = G::O_D, O_U = G::O_U, O_V = G::O_V, O_W = G::O_W, O_P = G::O_P, ES = G::ES;
+  constexpr int ST_BYTES = G::ST_BYTES, D1_BYTES = G::D1_BYTES, NIN = G::NIN;
+  constexpr uint32_t ST_TX = G::ST_TX;
   if (*reinterpret_cast<const volatile int*>(&ctl->done)) return;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t bars[NIN];
@@ -798,9 +809,10 @@ __global__ void __launch_bounds__(ig::NT, 3)
   const int b = wk.blk;
   const sf_dev_block& B = tab->blk[b];
   const double beta = ctl->beta, dt = ctl->dt;
+  const T Tix = (T)s.ix, Tiy = (T)s.iy, Tiz = (T)s.iz;
   const int colA = ctl->color, colB = colA ^ 1;
-  const double cu = dt * s.ix, cv = dt * s.iy, cw = dt * s.iz;
-  const double mbI = -(beta * s.bscale[1][1][1]);  // every scale of an interior cell (cfd.hpp:712-715)
+  const T cu = (T)(dt * s.ix), cv = (T)(dt * s.iy), cw = (T)(dt * s.iz);
+  const T mbI = (T)(-(beta * s.bscale[1][1][1]));  // every scale of an interior cell (cfd.hpp:712-715)
   if (tid == 0) {
     for (int q = 0; q < NIN; ++q) bar_init(&bars[q]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -809,7 +821,7 @@ __global__ void __launch_bounds__(ig::NT, 3)
 
   // S0 plane q holds z = k0 - 2 + q (q = 0 .. nplanes + 3)
   const int xo = (int)(B.base % B.sx), g = B.g;
-  const int xs = xo + i0 - 2, ys = g + j0 - 2, zs = g + k0 - 2;
+  const int xs = xo + i0 - 2 - XSH, ys = g + j0 - 2, zs = g + k0 - 2;
   const CUtensorMap* mD = &maps->m[b][SF_DIVU][tab->bidx[b][SF_DIVU][FRONT]];
   const CUtensorMap* mU = &maps->m[b][SF_VX][tab->bidx[b][SF_VX][FRONT]];
   const CUtensorMap* mV = &maps->m[b][SF_VY][tab->bidx[b][SF_VY][FRONT]];
@@ -825,7 +837,7 @@ __global__ void __launch_bounds__(ig::NT, 3)
     tma3(st + O_U, mU, bar, xs, ys + 1, zs + q);
     tma3(st + O_V, mV, bar, xs, ys, zs + q);
     tma3(st + O_W, mW, bar, xs, ys + 1, zs + q);
-    tma3(st + O_P, mP, bar, xs + 2, ys + 2, zs + q);
+    tma3(st + O_P, mP, bar, xs + 2 + XSH, ys + 2, zs + q);
   };
   const uint32_t bar0 = smem32(&bars[0]);
   auto wait_in = [&](int q) {
@@ -841,9 +853,9 @@ __global__ void __launch_bounds__(ig::NT, 3)
   if (tid == 0)
     for (int q = 0; q < NIN; ++q) issue(q);
 
-  const double* const S = reinterpret_cast<const double*>(sm);
-  double* const D1 = reinterpret_cast<double*>(sm + NIN * ST_BYTES);
-  constexpr int SST = ST_BYTES / 8, SD1 = D1_BYTES / 8;
+  const T* const S = reinterpret_cast<const T*>(sm);
+  T* const D1 = reinterpret_cast<T*>(sm + NIN * ST_BYTES);
+  constexpr int SST = ST_BYTES / ES, SD1 = D1_BYTES / ES;
 
   // the two divu1-region cells of this thread: its tile cell (A) and, for
   // tid < 84, one cell of the region's 1-cell ring (R)
@@ -853,8 +865,8 @@ __global__ void __launch_bounds__(ig::NT, 3)
                  : tid < 2 * RW + (RH - 2) ? (tid - 2 * RW + 1) * RW
                  : (tid - 2 * RW - (RH - 2) + 1) * RW + (RW - 1);
   const bool hasR = tid < R2N;
-  auto dv = [](int r) { return (r / RW + 1) * BW + (r % RW) + 1; };  // divu / vy box element (rows from j0-2)
-  auto uw = [](int r) { return (r / RW) * BW + (r % RW) + 1; };      // vx / vz box element (rows from j0-1)
+  auto dv = [](int r) { return (r / RW + 1) * BW + (r % RW) + 1 + XSH; };  // divu / vy box element (rows from j0-2)
+  auto uw = [](int r) { return (r / RW) * BW + (r % RW) + 1 + XSH; };      // vx / vz box element (rows from j0-1)
   const int dA = dv(rA), uA = uw(rA), pA = ty * TX + tx;
   const int dR = dv(rR), uR = uw(rR);
   const int gi = (int)B.lo[0] + i0 + tx, gj = (int)B.lo[1] + j0 + ty;
@@ -866,17 +878,17 @@ __global__ void __launch_bounds__(ig::NT, 3)
   // (plane z) with stn (plane z+1): its u1, v1, w1 and the swept -x / -y
   // neighbours' u1, v1 (their parity is the complement; their +x / +y term is
   // this cell's d0, the identical product)
-  auto sweepA = [&](int st, int stn, int d, int uo, int par, int zpar, double& u, double& v, double& w,
-                    double& um, double& vm, double& d0) {
-    const double dc = S[st + O_D / 8 + d], dxp = S[st + O_D / 8 + d + 1], dyp = S[st + O_D / 8 + d + BW];
-    const double dzp = S[stn + O_D / 8 + d], dxm = S[st + O_D / 8 + d - 1], dym = S[st + O_D / 8 + d - BW];
-    const double uu = S[st + O_U / 8 + uo], uum = S[st + O_U / 8 + uo - 1];
-    const double vv = S[st + O_V / 8 + d], vvm = S[st + O_V / 8 + d - BW], ww = S[st + O_W / 8 + uo];
-    const double a0 = ((par ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
+  auto sweepA = [&](int st, int stn, int d, int uo, int par, int zpar, T& u, T& v, T& w,
+                    T& um, T& vm, T& d0) {
+    const T dc = S[st + O_D / ES + d], dxp = S[st + O_D / ES + d + 1], dyp = S[st + O_D / ES + d + BW];
+    const T dzp = S[stn + O_D / ES + d], dxm = S[st + O_D / ES + d - 1], dym = S[st + O_D / ES + d - BW];
+    const T uu = S[st + O_U / ES + uo], uum = S[st + O_U / ES + uo - 1];
+    const T vv = S[st + O_V / ES + d], vvm = S[st + O_V / ES + d - BW], ww = S[st + O_W / ES + uo];
+    const T a0 = ((par ^ zpar) == colA) ? 1.0 : 0.0, a1 = 1.0 - a0;
     d0 = mbI * dc * a0;
-    const double exv = mbI * dxp * a1;
-    const double eyv = mbI * dyp * a1;
-    const double ezv = mbI * dzp * a1;
+    const T exv = mbI * dxp * a1;
+    const T eyv = mbI * dyp * a1;
+    const T ezv = mbI * dzp * a1;
     u = uu + cu * (d0 - exv);
     v = vv + cv * (d0 - eyv);
     w = ww + cw * (d0 - ezv);
@@ -884,10 +896,10 @@ __global__ void __launch_bounds__(ig::NT, 3)
     vm = vvm + cv * (mbI * dym * a1 - d0);
   };
   // DIVERGENCE of S1 (cfd.hpp:605-608)
-  auto div1 = [&](double u, double um, double v, double vm, double w, double wbelow) {
-    double dd = (u - um) * s.ix;
-    dd += (v - vm) * s.iy;
-    dd += (w - wbelow) * s.iz;
+  auto div1 = [&](T u, T um, T v, T vm, T w, T wbelow) {
+    T dd = (u - um) * Tix;
+    dd += (v - vm) * Tiy;
+    dd += (w - wbelow) * Tiz;
     return dd;
   };
 
@@ -895,19 +907,19 @@ __global__ void __launch_bounds__(ig::NT, 3)
   wait_in(0);
   wait_in(1);
   wait_in(2);
-  double cp, cu1, cv1, cw1, cum, cvm;  // this cell's S1 at the plane sweep B handles next
-  double wA, wR = 0.0;                 // w1 one plane below (tile cell, ring cell)
+  T cp, cu1, cv1, cw1, cum, cvm;  // this cell's S1 at the plane sweep B handles next
+  T wA, wR = 0.0;                 // w1 one plane below (tile cell, ring cell)
   {
-    double u, v, um, vm, d0;
+    T u, v, um, vm, d0;
     sweepA(0, SST, dA, uA, parA, (gk0 - 2) & 1, u, v, wA, um, vm, d0);
     if (hasR) sweepA(0, SST, dR, uR, parR, (gk0 - 2) & 1, u, v, wR, um, vm, d0);
-    double d0A;
+    T d0A;
     sweepA(SST, 2 * SST, dA, uA, parA, (gk0 - 1) & 1, cu1, cv1, cw1, cum, cvm, d0A);
-    cp = S[SST + O_P / 8 + pA] + d0A;
+    cp = S[SST + O_P / ES + pA] + d0A;
     D1[rA] = div1(cu1, cum, cv1, cvm, cw1, wA);
     wA = cw1;
     if (hasR) {
-      double w;
+      T w;
       sweepA(SST, 2 * SST, dR, uR, parR, (gk0 - 1) & 1, u, v, w, um, vm, d0);
       D1[rR] = div1(u, um, v, vm, w, wR);
       wR = w;
@@ -920,15 +932,15 @@ __global__ void __launch_bounds__(ig::NT, 3)
   }
 
   const int i = i0 + tx, j = j0 + ty;
-  double* __restrict__ Dn = tab->ptr[b][SF_DIVU][ALT];
-  double* __restrict__ Pn = tab->ptr[b][SF_P][ALT];
-  double* __restrict__ Un = tab->ptr[b][SF_VX][ALT];
-  double* __restrict__ Vn = tab->ptr[b][SF_VY][ALT];
-  double* __restrict__ Wn = tab->ptr[b][SF_VZ][ALT];
+  T* __restrict__ Dn = reinterpret_cast<T*>(tab->ptr[b][SF_DIVU][ALT]);
+  T* __restrict__ Pn = reinterpret_cast<T*>(tab->ptr[b][SF_P][ALT]);
+  T* __restrict__ Un = reinterpret_cast<T*>(tab->ptr[b][SF_VX][ALT]);
+  T* __restrict__ Vn = reinterpret_cast<T*>(tab->ptr[b][SF_VY][ALT]);
+  T* __restrict__ Wn = reinterpret_cast<T*>(tab->ptr[b][SF_VZ][ALT]);
   const unsigned sxy = (unsigned)(B.sx * B.sy);
   unsigned o = (unsigned)(B.base + ((long long)k0 * B.sy + j) * B.sx + i);
   unsigned long long r1 = 0ull, r2 = 0ull;
-  double wm2 = 0.0;  // swept w2 of the -z neighbour
+  T wm2 = 0.0;  // swept w2 of the -z neighbour
   // iteration t: sweep A on plane m+1 = k0+t (S0 planes t+2, t+3) and its
   // divergence into divu1 slot (t+1) % 3; barrier; sweep B on plane m = k0-1+t
   // (divu1 slots t % 3, (t+1) % 3), or at t = 0 the -z neighbour's swept w
@@ -937,15 +949,15 @@ __global__ void __launch_bounds__(ig::NT, 3)
   for (int t = 0; t <= nplanes; ++t) {
     wait_in(t + 3);
     const int zp = (gk0 + t) & 1;
-    double np, nu1, nv1, nw1, num, nvm;
+    T np, nu1, nv1, nw1, num, nvm;
     {
-      double d0A;
+      T d0A;
       sweepA(s0 * SST, s1 * SST, dA, uA, parA, zp, nu1, nv1, nw1, num, nvm, d0A);
-      np = S[s0 * SST + O_P / 8 + pA] + d0A;
+      np = S[s0 * SST + O_P / ES + pA] + d0A;
       D1[dnxt * SD1 + rA] = div1(nu1, num, nv1, nvm, nw1, wA);
       wA = nw1;
       if (hasR) {
-        double u, v, w, um, vm, d0;
+        T u, v, w, um, vm, d0;
         sweepA(s0 * SST, s1 * SST, dR, uR, parR, zp, u, v, w, um, vm, d0);
         D1[dnxt * SD1 + rR] = div1(u, um, v, vm, w, wR);
         wR = w;
@@ -953,39 +965,39 @@ __global__ void __launch_bounds__(ig::NT, 3)
     }
     __syncthreads();
     if (tid == 0) issue(t + 2 + NIN);  // S0 plane t+2 is consumed
-    const double* d1 = D1 + dcur * SD1;
-    const double* d1p = D1 + dnxt * SD1;
+    const T* d1 = D1 + dcur * SD1;
+    const T* d1p = D1 + dnxt * SD1;
     if (t == 0) {
       // swept w2 of the plane below the chunk: sweep B's -z neighbour at k0
-      const double a0m = (((gi + gj + gk0 - 1) & 1) == colB) ? 1.0 : 0.0, a1m = 1.0 - a0m;
-      const double d0m = mbI * d1[rA] * a0m;
-      const double ezm = mbI * d1p[rA] * a1m;
+      const T a0m = (((gi + gj + gk0 - 1) & 1) == colB) ? 1.0 : 0.0, a1m = 1.0 - a0m;
+      const T d0m = mbI * d1[rA] * a0m;
+      const T ezm = mbI * d1p[rA] * a1m;
       wm2 = cw1 + cw * (d0m - ezm);
     } else {
       // sweep B on plane m = k0 + t - 1 (k_sweep2's interior fast path)
-      const double dC = d1[rA], dXp = d1[rA + 1], dYp = d1[rA + RW];
-      const double dXm = d1[rA - 1], dYm = d1[rA - RW], dZp = d1p[rA];
+      const T dC = d1[rA], dXp = d1[rA + 1], dYp = d1[rA + RW];
+      const T dXm = d1[rA - 1], dYm = d1[rA - RW], dZp = d1p[rA];
       const int par = (parA ^ ((gk0 + t - 1) & 1));
-      const double a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
-      const double d0 = mbI * dC * a0;
-      const double exv = mbI * dXp * a1;
-      const double eyv = mbI * dYp * a1;
-      const double ezv = mbI * dZp * a1;
-      const double pn = cp + d0;
-      const double un = cu1 + cu * (d0 - exv);
-      const double vn = cv1 + cv * (d0 - eyv);
-      const double wn = cw1 + cw * (d0 - ezv);
-      const double umn = cum + cu * (mbI * dXm * a1 - d0);
-      const double vmn = cvm + cv * (mbI * dYm * a1 - d0);
-      double dd = (un - umn) * s.ix;
-      dd += (vn - vmn) * s.iy;
-      dd += (wn - wm2) * s.iz;
+      const T a0 = (par == colB) ? 1.0 : 0.0, a1 = 1.0 - a0;
+      const T d0 = mbI * dC * a0;
+      const T exv = mbI * dXp * a1;
+      const T eyv = mbI * dYp * a1;
+      const T ezv = mbI * dZp * a1;
+      const T pn = cp + d0;
+      const T un = cu1 + cu * (d0 - exv);
+      const T vn = cv1 + cv * (d0 - eyv);
+      const T wn = cw1 + cw * (d0 - ezv);
+      const T umn = cum + cu * (mbI * dXm * a1 - d0);
+      const T vmn = cvm + cv * (mbI * dYm * a1 - d0);
+      T dd = (un - umn) * Tix;
+      dd += (vn - vmn) * Tiy;
+      dd += (wn - wm2) * Tiz;
       __stwb(Pn + o, pn);
       __stwb(Un + o, un);
       __stwb(Vn + o, vn);
       __stwb(Wn + o, wn);
       __stwb(Dn + o, dd);
-      const unsigned long long b1 = abs_bits(dC), b2 = abs_bits(dd);
+      const unsigned long long b1 = abs_bits((double)dC), b2 = abs_bits((double)dd);
       r1 = b1 > r1 ? b1 : r1;
       r2 = b2 > r2 ? b2 : r2;
       wm2 = wn;
@@ -1021,8 +1033,10 @@ static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c,
                                                            static_cast<const maps2_t*>(maps), fin, pins, remote);
 }
 
-void sweep2i_box(int field, int* bw, int* bh) {
-  using namespace ig;
+void sweep2i_box(int field, int* bw, int* bh, int es) {
+  const int BW = es == 4 ? ig<float>::BW : ig<double>::BW;
+  constexpr int TX = ig<double>::TX, TY = ig<double>::TY, DH = ig<double>::DH, UH = ig<double>::UH;
+  constexpr int VH = ig<double>::VH, WH = ig<double>::WH;
   switch (field) {
     case SF_DIVU: *bw = BW; *bh = DH; break;
     case SF_VX: *bw = BW; *bh = UH; break;
@@ -1032,13 +1046,22 @@ void sweep2i_box(int field, int* bw, int* bh) {
   }
 }
 
-void launch_sweep2i(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
-                    sf_host_flag* hflag, const void* maps, int fin, cudaStream_t st, unsigned total) {
-  if (nctas <= 0) return;
-  ensure_smem_attr((const void*)k_sweep2i, ig::SMEM);
-  k_sweep2i<<<nctas, dim3(ig::TX, ig::TY), ig::SMEM, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
+template <class T>
+static void launch2i(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                     sf_host_flag* hflag, const void* maps, int fin, cudaStream_t st, unsigned total) {
+  using G = ig<T>;
+  ensure_smem_attr((const void*)k_sweep2i<T>, G::SMEM);
+  k_sweep2i<T><<<nctas, dim3(G::TX, G::TY), G::SMEM, st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
                                                            total ? total : (unsigned)nctas,
                                                            static_cast<const maps2_t*>(maps), fin);
+}
+void launch_sweep2i(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
+                    sf_host_flag* hflag, const void* maps, int fin, cudaStream_t st, unsigned total, int es) {
+  if (nctas <= 0) return;
+  if (es == 4)
+    launch2i<float>(vw, nctas, zc, c, ctl, hflag, maps, fin, st, total);
+  else
+    launch2i<double>(vw, nctas, zc, c, ctl, hflag, maps, fin, st, total);
 }
 
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
