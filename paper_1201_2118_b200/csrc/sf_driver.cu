@@ -2405,28 +2405,28 @@ class simulation {
       SF_CK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
       SF_CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     }
-    const int ty = sweep2_tile_y(), zc = zc_pass();
+    const int ty = sweep2_tile_y(), tyi = sweep2i_tile_y(cfd_es_), zc = zc_pass();
     // the slabs: 32-plane chunks, more CTAs to fill in beside the interior
     // (measured per pass: 128 2.43 ms, 64 2.40, 32 2.40, 16 2.44, 8 2.54)
     const int bzc = std::min(zc, 32);
     ibzc_ = bzc;
     char key[64];
-    std::snprintf(key, sizeof key, "isplit:%d:%d:%d", zc, ty, bzc);
+    std::snprintf(key, sizeof key, "isplit:%d:%d:%d:%d", zc, ty, tyi, bzc);
     auto ii = items_.find(std::string(key) + ":i");
     if (ii != items_.end())
       return ii->second.nctas ? std::make_pair(&ii->second, &items_.find(std::string(key) + ":b")->second)
                               : std::make_pair((const work_set*)nullptr, (const work_set*)nullptr);
     const auto n = dec_.dims(gid_[0]);
-    // interior tiles: i0 = ox + 32 a <= N - 35, j0 = oy + 8 b <= N - 11
+    // interior tiles: i0 = ox + 32 a <= N - 35, j0 = oy + tyi b <= N - tyi - 3
     // (tile origins 32 / 8: the tiles' rows stay 128-byte aligned; starting
     // them at 4 / 4 shrinks the slabs but measured 4 % slower)
     const i64 ox = kTX, oy = ty;
     const i64 qx = n[0] >= ox + kTX + 3 ? (n[0] - 3 - kTX - ox) / kTX + 1 : 0;
-    const i64 qy = n[1] >= oy + ty + 3 ? (n[1] - 3 - ty - oy) / ty + 1 : 0;
-    const i64 ilo[3] = {ox, oy, 3}, ihi[3] = {ox + kTX * qx, oy + ty * qy, n[2] - 3};
+    const i64 qy = n[1] >= oy + tyi + 3 ? (n[1] - 3 - tyi - oy) / tyi + 1 : 0;
+    const i64 ilo[3] = {ox, oy, 3}, ihi[3] = {ox + kTX * qx, oy + tyi * qy, n[2] - 3};
     std::vector<sf_work> vi, vb;
     int ci = 0, cb = 0;
-    auto add = [&](std::vector<sf_work>& v, int& cta, const i64 lo[3], const i64 hi[3], int zcb) {
+    auto add = [&](std::vector<sf_work>& v, int& cta, const i64 lo[3], const i64 hi[3], int zcb, int tyb) {
       if (lo[0] >= hi[0] || lo[1] >= hi[1] || lo[2] >= hi[2]) return;
       sf_work w{};
       w.blk = 0;
@@ -2436,25 +2436,25 @@ class simulation {
         w.hi[a] = hi[a];
       }
       w.tiles[0] = (int)((hi[0] - lo[0] + kTX - 1) / kTX);
-      w.tiles[1] = (int)((hi[1] - lo[1] + ty - 1) / ty);
+      w.tiles[1] = (int)((hi[1] - lo[1] + tyb - 1) / tyb);
       w.tiles[2] = (int)((hi[2] - lo[2] + zcb - 1) / zcb);
       cta += w.tiles[0] * w.tiles[1] * w.tiles[2];
       v.push_back(w);
     };
     if (qx > 0 && qy > 0 && ihi[2] > ilo[2]) {
-      add(vi, ci, ilo, ihi, zc);
+      add(vi, ci, ilo, ihi, zc, tyi);
       const i64 z0[3] = {0, 0, 0}, zl[3] = {n[0], n[1], ilo[2]};
       const i64 z1[3] = {0, 0, ihi[2]}, zh[3] = {n[0], n[1], n[2]};
-      add(vb, cb, z0, zl, bzc);
-      add(vb, cb, z1, zh, bzc);
+      add(vb, cb, z0, zl, bzc, ty);
+      add(vb, cb, z1, zh, bzc, ty);
       const i64 y0[3] = {0, 0, ilo[2]}, yl[3] = {n[0], ilo[1], ihi[2]};
       const i64 y1[3] = {0, ihi[1], ilo[2]}, yh[3] = {n[0], n[1], ihi[2]};
-      add(vb, cb, y0, yl, bzc);
-      add(vb, cb, y1, yh, bzc);
+      add(vb, cb, y0, yl, bzc, ty);
+      add(vb, cb, y1, yh, bzc, ty);
       const i64 x0[3] = {0, ilo[1], ilo[2]}, xl[3] = {ilo[0], ihi[1], ihi[2]};
       const i64 x1[3] = {ihi[0], ilo[1], ilo[2]}, xh[3] = {n[0], ihi[1], ihi[2]};
-      add(vb, cb, x0, xl, bzc);
-      add(vb, cb, x1, xh, bzc);
+      add(vb, cb, x0, xl, bzc, ty);
+      add(vb, cb, x1, xh, bzc, ty);
     }
     auto mk = [&](std::vector<sf_work>& v, int nctas) {
       work_set ws;
@@ -2888,7 +2888,7 @@ class simulation {
     const int fin = dist_ ? 0 : 1;
     const auto split = interior_split();
     if (!has_proc_faces() && split.first) {
-      // the interior tiles on the interior form (3 CTAs per SM), the boundary
+      // the interior tiles on the interior form (sweep2i_tile_y rows), the boundary
       // slabs on k_sweep2 on the second stream at the same time; one
       // last-CTA count spans both launches
       const work_set& wi = *split.first;
@@ -2896,7 +2896,9 @@ class simulation {
       const unsigned total = (unsigned)(wi.nctas + wb.nctas);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
       // boundary slabs first on the second stream, the interior beside them
-      // (measured: concurrent 2.40 ms, either order on one stream 2.58 ms)
+      // (measured with 32x20 interior tiles: concurrent 2.27 ms, interior
+      // launched first 2.27, either order on one stream 2.33; slab chunks of
+      // 16 / 32 / 64 planes 2.31 / 2.27 / 2.27)
       SF_CK(cudaEventRecord(ev_fork_, st_));
       SF_CK(cudaStreamWaitEvent(xs_, ev_fork_, 0));
       launch_sweep2(tview(wb), wb.nctas, ibzc_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), xs_, total,

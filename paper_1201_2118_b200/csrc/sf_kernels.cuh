@@ -112,6 +112,7 @@ size_t sweep2_maps_bytes();
 size_t sweep2_map_offset(int b, int f, int s);
 void sweep2_box(int field, int* bw, int* bh, int es = 8);
 int sweep2_tile_y();  // tile height of the selected temporal-pass variant (tile width 32)
+int sweep2i_tile_y(int es = 8);  // tile height of the interior form (k_sweep2i; width 32)
 int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field, int es = 8);
 size_t sweep_maps_bytes();
 int encode_box_map(void* map_out, double* base, long long sx, long long sy, long long sz, int bw, int bh,

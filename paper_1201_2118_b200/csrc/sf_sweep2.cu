@@ -766,10 +766,33 @@ __global__ void __launch_bounds__(32 * TYV, MINB)
 // Geometry for element type T: the boxes start XA = 16 / sizeof(T) cells
 // left of the tile's x (a 16-byte aligned TMA start; 2 fp64, 4 fp32), i.e. the
 // cells of a row sit XSH = XA - 2 further in than for fp64.
+#ifndef SF_ITY
+#define SF_ITY 20
+#endif
+#ifndef SF_ITY32
+#define SF_ITY32 16
+#endif
+#ifndef SF_ININ
+#define SF_ININ 4
+#endif
+#ifndef SF_ININ32
+#define SF_ININ32 6
+#endif
+// tile height and S0 stages of the interior form per element type. Measured
+// at 512^3 (ms per pass, same box): fp64 32x8 (3 CTAs/SM) 2.48, 32x12 (2)
+// 2.41, 32x16 (1) 2.31, 32x20 (1) 2.28, 32x24 2.32 (a 24-row slab), 32x32
+// (3 stages, spills) 2.49; 32x20 with 3 / 5 stages 2.46 / 2.28. fp32 32x8
+// 1.398, 32x12 1.411, 32x16 1.389, 32x8 6 stages 1.378, 32x16 6 stages 1.371.
+// Taller tiles re-read fewer halo rows: DRAM reads per interior cell 53.7 B
+// at 32x8, 45.5 B at 32x20 (40 B without halos).
 template <class T>
+constexpr int kInteriorTY = sizeof(T) == 8 ? SF_ITY : SF_ITY32;
+int sweep2i_tile_y(int es) { return es == 4 ? kInteriorTY<float> : kInteriorTY<double>; }
+
+template <class T, int TYV = kInteriorTY<T>>
 struct ig {
   static constexpr int ES = (int)sizeof(T), XA = 16 / ES, XSH = XA - 2;
-  static constexpr int TX = 32, TY = 8, NT = TX * TY;
+  static constexpr int TX = 32, TY = TYV, NT = TX * TY;
   static constexpr int RW = TX + 2, RH = TY + 2, RN = RW * RH;  // divu1 region: x from i0-1, y from j0-1
   static constexpr int R2N = RN - NT;                            // its ring cells (84), one more per thread 0..83
   static constexpr int BW = (TX + 4 + XSH + XA - 1) / XA * XA;   // S0 box width, x from i0-2-XSH: 36 / 40
@@ -779,9 +802,11 @@ struct ig {
   static constexpr int ST_BYTES = O_P + r128(ES * TX * TY);
   static constexpr uint32_t ST_TX = (uint32_t)ES * (BW * DH + BW * UH + BW * VH + BW * WH + TX * TY);
   static constexpr int D1_BYTES = r128(ES * RN);
-  static constexpr int NIN = 4;
+  static constexpr int NIN = ES == 8 ? SF_ININ : SF_ININ32;
   static constexpr int SMEM = NIN * ST_BYTES + 3 * D1_BYTES;
-  static constexpr int MINB = ES == 8 ? 3 : 4;  // CTAs per SM the registers are budgeted for
+  // CTAs per SM the registers are budgeted for: 768 fp64 threads (<= 85
+  // registers each), 1024 fp32 threads (<= 64)
+  static constexpr int MINB = (ES == 8 ? 768 : 1024) / NT > 0 ? (ES == 8 ? 768 : 1024) / NT : 1;
 };
 
 template <class T>
@@ -1033,17 +1058,21 @@ static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c,
                                                            static_cast<const maps2_t*>(maps), fin, pins, remote);
 }
 
-void sweep2i_box(int field, int* bw, int* bh, int es) {
-  const int BW = es == 4 ? ig<float>::BW : ig<double>::BW;
-  constexpr int TX = ig<double>::TX, TY = ig<double>::TY, DH = ig<double>::DH, UH = ig<double>::UH;
-  constexpr int VH = ig<double>::VH, WH = ig<double>::WH;
+template <class G>
+static void box2i(int field, int* bw, int* bh) {
   switch (field) {
-    case SF_DIVU: *bw = BW; *bh = DH; break;
-    case SF_VX: *bw = BW; *bh = UH; break;
-    case SF_VY: *bw = BW; *bh = VH; break;
-    case SF_VZ: *bw = BW; *bh = WH; break;
-    default: *bw = TX; *bh = TY; break;
+    case SF_DIVU: *bw = G::BW; *bh = G::DH; break;
+    case SF_VX: *bw = G::BW; *bh = G::UH; break;
+    case SF_VY: *bw = G::BW; *bh = G::VH; break;
+    case SF_VZ: *bw = G::BW; *bh = G::WH; break;
+    default: *bw = G::TX; *bh = G::TY; break;
   }
+}
+void sweep2i_box(int field, int* bw, int* bh, int es) {
+  if (es == 4)
+    box2i<ig<float>>(field, bw, bh);
+  else
+    box2i<ig<double>>(field, bw, bh);
 }
 
 template <class T>
