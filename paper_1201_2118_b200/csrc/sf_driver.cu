@@ -1767,6 +1767,7 @@ class simulation {
   unsigned long long table_epoch_ = 0;
   void* maps2_ = nullptr;  // temporal-pass descriptors (null: pass unavailable)
   void* maps3_ = nullptr;  // descriptors of the interior form of the pass (sweep2i_box shapes)
+  void* maps4_ = nullptr;  // descriptors of the pass's x-slab form (sweep2_box shape 1)
   int ibzc_ = 32;          // z chunk of the boundary slabs beside the interior form
   const bool interior_env_ = getenv("SF_NO_INTERIOR_PASS") == nullptr;
   void* uvmaps_ = nullptr;  // TMA UPDATE_VELOCITY descriptors (null: plain-load kernel)
@@ -2043,6 +2044,21 @@ class simulation {
       if (ok) {
         maps3_ = dalloc(hm.size());
         SF_CK(cudaMemcpy(maps3_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
+      }
+      hm.assign(sweep2_maps_bytes(), 0);
+      for (int f : {SF_VX, SF_VY, SF_VZ, SF_P, SF_DIVU})
+        for (int s = 0; s < kSlots && ok; ++s) {
+          double* p = htab_->ptr[0][f][s];
+          if (!p) continue;
+          const sf_layout& L = lay_[0];
+          int bw, bh;
+          sweep2_box(f, &bw, &bh, cfd_es_, 1);
+          ok = bw <= L.sx && bh <= L.sy &&
+               encode_box_map(hm.data() + sweep2_map_offset(0, f, s), p, L.sx, L.sy, L.sz, bw, bh, cfd_es_) == 0;
+        }
+      if (ok) {
+        maps4_ = dalloc(hm.size());
+        SF_CK(cudaMemcpy(maps4_, hm.data(), hm.size(), cudaMemcpyHostToDevice));
       }
     }
     {
@@ -2396,37 +2412,46 @@ class simulation {
   // k0-2 .. k1+1 inside [1, N-2] on z: planes [3, N-3)), for k_sweep2i, and
   // the six boundary slabs around them for k_sweep2. {null, null} when it
   // does not apply (fp32, several components, periodic axes, small grids).
-  std::pair<const work_set*, const work_set*> interior_split() {
-    if (!maps3_ || !interior_env_ || nloc_ != 1 || dist_ || !temporal() || has_proc_faces())
-      return {nullptr, nullptr};
-    if (cfg_.periodic[0] || cfg_.periodic[1] || cfg_.periodic[2]) return {nullptr, nullptr};
+  struct isplit {
+    const work_set* in = nullptr;    // interior tiles (k_sweep2i)
+    const work_set* slab = nullptr;  // z and y slabs (k_sweep2, 32 x sweep2_tile_y tiles)
+    const work_set* xs = nullptr;    // x slabs (k_sweep2, x-slab form)
+  };
+  isplit interior_split() {
+    if (!maps3_ || !maps4_ || !interior_env_ || nloc_ != 1 || dist_ || !temporal() || has_proc_faces()) return {};
+    if (cfg_.periodic[0] || cfg_.periodic[1] || cfg_.periodic[2]) return {};
     if (!xs_) {
       SF_CK(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
       SF_CK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
       SF_CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     }
+    int stx, sty;
+    sweep2_tile(1, &stx, &sty);
     const int ty = sweep2_tile_y(), tyi = sweep2i_tile_y(cfd_es_), zc = zc_pass();
     // the slabs: 32-plane chunks, more CTAs to fill in beside the interior
-    // (measured per pass: 128 2.43 ms, 64 2.40, 32 2.40, 16 2.44, 8 2.54)
+    // (measured per pass with 32x20 interior tiles: 16 / 32 / 64 planes
+    // 2.31 / 2.27 / 2.27 ms)
     const int bzc = std::min(zc, 32);
     ibzc_ = bzc;
     char key[64];
     std::snprintf(key, sizeof key, "isplit:%d:%d:%d:%d", zc, ty, tyi, bzc);
     auto ii = items_.find(std::string(key) + ":i");
-    if (ii != items_.end())
-      return ii->second.nctas ? std::make_pair(&ii->second, &items_.find(std::string(key) + ":b")->second)
-                              : std::make_pair((const work_set*)nullptr, (const work_set*)nullptr);
+    if (ii != items_.end()) {
+      if (!ii->second.nctas) return {};
+      return {&ii->second, &items_.find(std::string(key) + ":b")->second,
+              &items_.find(std::string(key) + ":x")->second};
+    }
     const auto n = dec_.dims(gid_[0]);
-    // interior tiles: i0 = ox + 32 a <= N - 35, j0 = oy + tyi b <= N - tyi - 3
-    // (tile origins 32 / 8: the tiles' rows stay 128-byte aligned; starting
-    // them at 4 / 4 shrinks the slabs but measured 4 % slower)
-    const i64 ox = kTX, oy = ty;
+    // interior tiles: i0 = ox + 32 a <= N - 35, j0 = oy + tyi b <= N - tyi - 3.
+    // ox = 16 keeps the tiles' rows 128-byte aligned and leaves x slabs one
+    // 16-wide tile column each side (x-slab form); oy = 8: one 32 x 8 tile row
+    const i64 ox = stx, oy = ty;
     const i64 qx = n[0] >= ox + kTX + 3 ? (n[0] - 3 - kTX - ox) / kTX + 1 : 0;
     const i64 qy = n[1] >= oy + tyi + 3 ? (n[1] - 3 - tyi - oy) / tyi + 1 : 0;
     const i64 ilo[3] = {ox, oy, 3}, ihi[3] = {ox + kTX * qx, oy + tyi * qy, n[2] - 3};
-    std::vector<sf_work> vi, vb;
-    int ci = 0, cb = 0;
-    auto add = [&](std::vector<sf_work>& v, int& cta, const i64 lo[3], const i64 hi[3], int zcb, int tyb) {
+    std::vector<sf_work> vi, vb, vx;
+    int ci = 0, cb = 0, cx = 0;
+    auto add = [&](std::vector<sf_work>& v, int& cta, const i64 lo[3], const i64 hi[3], int zcb, int txb, int tyb) {
       if (lo[0] >= hi[0] || lo[1] >= hi[1] || lo[2] >= hi[2]) return;
       sf_work w{};
       w.blk = 0;
@@ -2435,26 +2460,26 @@ class simulation {
         w.lo[a] = lo[a];
         w.hi[a] = hi[a];
       }
-      w.tiles[0] = (int)((hi[0] - lo[0] + kTX - 1) / kTX);
+      w.tiles[0] = (int)((hi[0] - lo[0] + txb - 1) / txb);
       w.tiles[1] = (int)((hi[1] - lo[1] + tyb - 1) / tyb);
       w.tiles[2] = (int)((hi[2] - lo[2] + zcb - 1) / zcb);
       cta += w.tiles[0] * w.tiles[1] * w.tiles[2];
       v.push_back(w);
     };
     if (qx > 0 && qy > 0 && ihi[2] > ilo[2]) {
-      add(vi, ci, ilo, ihi, zc, tyi);
+      add(vi, ci, ilo, ihi, zc, kTX, tyi);
       const i64 z0[3] = {0, 0, 0}, zl[3] = {n[0], n[1], ilo[2]};
       const i64 z1[3] = {0, 0, ihi[2]}, zh[3] = {n[0], n[1], n[2]};
-      add(vb, cb, z0, zl, bzc, ty);
-      add(vb, cb, z1, zh, bzc, ty);
+      add(vb, cb, z0, zl, bzc, kTX, ty);
+      add(vb, cb, z1, zh, bzc, kTX, ty);
       const i64 y0[3] = {0, 0, ilo[2]}, yl[3] = {n[0], ilo[1], ihi[2]};
       const i64 y1[3] = {0, ihi[1], ilo[2]}, yh[3] = {n[0], n[1], ihi[2]};
-      add(vb, cb, y0, yl, bzc, ty);
-      add(vb, cb, y1, yh, bzc, ty);
+      add(vb, cb, y0, yl, bzc, kTX, ty);
+      add(vb, cb, y1, yh, bzc, kTX, ty);
       const i64 x0[3] = {0, ilo[1], ilo[2]}, xl[3] = {ilo[0], ihi[1], ihi[2]};
       const i64 x1[3] = {ihi[0], ilo[1], ilo[2]}, xh[3] = {n[0], ihi[1], ihi[2]};
-      add(vb, cb, x0, xl, bzc, ty);
-      add(vb, cb, x1, xh, bzc, ty);
+      add(vx, cx, x0, xl, bzc, stx, sty);
+      add(vx, cx, x1, xh, bzc, stx, sty);
     }
     auto mk = [&](std::vector<sf_work>& v, int nctas) {
       work_set ws;
@@ -2468,6 +2493,7 @@ class simulation {
     };
     items_.emplace(std::string(key) + ":i", mk(vi, ci));
     items_.emplace(std::string(key) + ":b", mk(vb, cb));
+    items_.emplace(std::string(key) + ":x", mk(vx, cx));
     return interior_split();
   }
 
@@ -2887,13 +2913,14 @@ class simulation {
     }
     const int fin = dist_ ? 0 : 1;
     const auto split = interior_split();
-    if (!has_proc_faces() && split.first) {
-      // the interior tiles on the interior form (sweep2i_tile_y rows), the boundary
-      // slabs on k_sweep2 on the second stream at the same time; one
-      // last-CTA count spans both launches
-      const work_set& wi = *split.first;
-      const work_set& wb = *split.second;
-      const unsigned total = (unsigned)(wi.nctas + wb.nctas);
+    if (!has_proc_faces() && split.in) {
+      // the interior tiles on the interior form (sweep2i_tile_y rows), the
+      // slabs on k_sweep2 (x slabs on its x-slab form) on the second stream
+      // at the same time; one last-CTA count spans the launches
+      const work_set& wi = *split.in;
+      const work_set& wb = *split.slab;
+      const work_set& wx = *split.xs;
+      const unsigned total = (unsigned)(wi.nctas + wb.nctas + wx.nctas);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
       // boundary slabs first on the second stream, the interior beside them
       // (measured with 32x20 interior tiles: concurrent 2.27 ms, interior
@@ -2903,11 +2930,13 @@ class simulation {
       SF_CK(cudaStreamWaitEvent(xs_, ev_fork_, 0));
       launch_sweep2(tview(wb), wb.nctas, ibzc_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), xs_, total,
                     nullptr, cfd_es_);
+      launch_sweep2(tview(wx), wx.nctas, ibzc_, consts_, dctl_, loop_flag(), maps4_, fin, wall_pins(), xs_, total,
+                    nullptr, cfd_es_, 1);
       launch_sweep2i(tview(wi), wi.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps3_, fin, st_, total, cfd_es_);
       SF_CK(cudaEventRecord(ev_join_, xs_));
       SF_CK(cudaStreamWaitEvent(st_, ev_join_, 0));
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
-      launches_ += 2;
+      launches_ += (wi.nctas > 0) + (wb.nctas > 0) + (wx.nctas > 0);
     } else if (!has_proc_faces()) {
       const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass(), kTX, sweep2_tile_y());
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));

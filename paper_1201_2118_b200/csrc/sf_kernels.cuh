@@ -100,7 +100,7 @@ struct sweep2_remote {
 // exchange, or null
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
-                   unsigned total_ctas = 0, const sweep2_remote* remote = nullptr, int es = 8);
+                   unsigned total_ctas = 0, const sweep2_remote* remote = nullptr, int es = 8, int shape = 0);
 // The interior form of the temporal pass (fp64; tiles where k_sweep2 takes its
 // fast path everywhere): no S1 field ring, 3 CTAs per SM. maps: a maps table
 // with sweep2i_box shapes; total: CTAs of the whole pass (with the k_sweep2
@@ -110,7 +110,9 @@ void launch_sweep2i(const table_view& vw, int nctas, int zc, const sf_consts& c,
 void sweep2i_box(int field, int* bw, int* bh, int es = 8);
 size_t sweep2_maps_bytes();
 size_t sweep2_map_offset(int b, int f, int s);
-void sweep2_box(int field, int* bw, int* bh, int es = 8);
+// shape 0: the pass's tiles (32 x sweep2_tile_y()); 1: the x-slab form
+void sweep2_box(int field, int* bw, int* bh, int es = 8, int shape = 0);
+void sweep2_tile(int shape, int* tx, int* ty);
 int sweep2_tile_y();  // tile height of the selected temporal-pass variant (tile width 32)
 int sweep2i_tile_y(int es = 8);  // tile height of the interior form (k_sweep2i; width 32)
 int encode_sweep_map(void* map_out, double* base, long long sx, long long sy, long long sz, int field, int es = 8);

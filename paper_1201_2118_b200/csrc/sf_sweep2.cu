@@ -64,10 +64,10 @@ constexpr int r128(int b) { return (b + 127) / 128 * 128; }
 // TMA box starts on a 16-byte aligned x: XA = 16 / sizeof(T) cells left of the
 // tile (2 fp64, 4 fp32), so the widened S1 region (from i0-2) sits XSH = XA-2
 // cells into each S0 row.
-template <int TYV, class T = double>
+template <int TXV, int TYV, class T = double>
 struct geom {
   static constexpr int ES = (int)sizeof(T), XA = 16 / ES, XSH = XA - 2;
-  static constexpr int TX = 32, TY = TYV, NT = TX * TY;
+  static constexpr int TX = TXV, TY = TYV, NT = TX * TY;
   static constexpr int EW = TX + 3, EH = TY + 3, EN = EW * EH;  // widened S1 tile
   static constexpr int NE = (EN + NT - 1) / NT;                  // widened cells per thread
   static constexpr int R2 = EN - 1 - NT;                         // second-round cells
@@ -101,9 +101,22 @@ size_t sweep2_map_offset(int b, int f, int s) {
 // tiles, 6 stages at 1 CTA/SM, L2 prefetch of later planes -- all slower;
 // DESIGN.md §10.)
 constexpr int kPassTY = 8, kPassStages = 3, kPassMinB = 2, kPassMinB32 = 3;
+// the x-slab form: 16 x 16 tiles for the slabs beside the interior tiles
+// along x (16 cells wide: one tile column where 32-wide tiles would take two
+// half-empty ones)
+constexpr int kSlabTX = 16, kSlabTY = 16;
 int sweep2_tile_y() { return kPassTY; }
-void sweep2_box(int field, int* bw, int* bh, int es) {
-  *bw = es == 4 ? geom<kPassTY, float>::IW : geom<kPassTY, double>::IW;
+void sweep2_tile(int shape, int* tx, int* ty) {
+  *tx = shape ? kSlabTX : kTX;
+  *ty = shape ? kSlabTY : kPassTY;
+}
+void sweep2_box(int field, int* bw, int* bh, int es, int shape) {
+  if (shape) {
+    *bw = es == 4 ? geom<kSlabTX, kSlabTY, float>::IW : geom<kSlabTX, kSlabTY, double>::IW;
+    *bh = field == SF_DIVU ? kSlabTY + 4 : kSlabTY + 3;
+    return;
+  }
+  *bw = es == 4 ? geom<kTX, kPassTY, float>::IW : geom<kTX, kPassTY, double>::IW;
   *bh = field == SF_DIVU ? kPassTY + 4 : kPassTY + 3;
 }
 
@@ -171,14 +184,14 @@ __device__ __forceinline__ void pass_finalize(unsigned long long (&rr)[2], sf_de
 // into the neighbours' ghost shells (sweep2_remote), up to 7 directions per
 // cell (face, edges, corner): the ghost exchange of the next pass fused into
 // this one.
-template <int TYV, int NIN, int MINB, bool PER, bool REMOTE, class T>
-__global__ void __launch_bounds__(32 * TYV, MINB)
+template <int TXV, int TYV, int NIN, int MINB, bool PER, bool REMOTE, class T>
+__global__ void __launch_bounds__(TXV * TYV, MINB)
     k_sweep2(sf_dev_table* __restrict__ tab, const sf_work* __restrict__ items, int nitems, int zc,
              sf_consts s, sf_dev_ctl* ctl, sf_host_flag* hflag, unsigned int total_ctas,
              const maps2_t* __restrict__ maps, int finalize, sweep2_pins pins,
              const sweep2_remote* __restrict__ rem) {
   static_assert(NIN >= 3, "three S0 planes are read or in flight per phase");
-  using G = geom<TYV, T>;
+  using G = geom<TXV, TYV, T>;
   constexpr int ES = G::ES, XSH = G::XSH;
   constexpr int TX = G::TX, TY = G::TY, NT = G::NT, EW = G::EW, EN = G::EN, NE = G::NE, R2 = G::R2;
   constexpr int IW = G::IW, IN_D = G::IN_D, IN_U = G::IN_U, IN_V = G::IN_V, IN_W = G::IN_W, IN_P = G::IN_P;
@@ -1043,15 +1056,16 @@ __global__ void __launch_bounds__(ig<T>::NT, ig<T>::MINB)
   pass_finalize(rr, tab, ctl, hflag, total_ctas, finalize);
 }
 
-template <class T, int MINB>
+template <class T, int MINB, int TXV = kTX, int TYV = kPassTY>
 static void launch2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                     sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
                     unsigned total, const sweep2_remote* remote) {
-  constexpr int TYV = kPassTY, NIN = kPassStages;
-  using G = geom<TYV, T>;
+  constexpr int NIN = kPassStages;
+  using G = geom<TXV, TYV, T>;
   const bool per = c.per[0] || c.per[1] || c.per[2];
-  auto k = remote ? (per ? k_sweep2<TYV, NIN, MINB, true, true, T> : k_sweep2<TYV, NIN, MINB, false, true, T>)
-                  : (per ? k_sweep2<TYV, NIN, MINB, true, false, T> : k_sweep2<TYV, NIN, MINB, false, false, T>);
+  auto k = remote ? (per ? k_sweep2<TXV, TYV, NIN, MINB, true, true, T> : k_sweep2<TXV, TYV, NIN, MINB, false, true, T>)
+                  : (per ? k_sweep2<TXV, TYV, NIN, MINB, true, false, T>
+                         : k_sweep2<TXV, TYV, NIN, MINB, false, false, T>);
   ensure_smem_attr((const void*)k, G::smem_bytes(NIN));
   k<<<nctas, dim3(G::TX, G::TY), G::smem_bytes(NIN), st>>>(vw.tab, vw.items, vw.nitems, zc, c, ctl, hflag,
                                                            total ? total : (unsigned)nctas,
@@ -1095,8 +1109,15 @@ void launch_sweep2i(const table_view& vw, int nctas, int zc, const sf_consts& c,
 
 void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, sf_dev_ctl* ctl,
                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
-                   unsigned total, const sweep2_remote* remote, int es) {
+                   unsigned total, const sweep2_remote* remote, int es, int shape) {
   if (nctas <= 0) return;
+  if (shape) {  // the x-slab form (no periodic axis, no fused exchange: the interior split)
+    if (es == 4)
+      launch2<float, kPassMinB32, kSlabTX, kSlabTY>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total, nullptr);
+    else
+      launch2<double, kPassMinB, kSlabTX, kSlabTY>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total, nullptr);
+    return;
+  }
   if (es == 4)  // fp32: half the shared memory per CTA (56 KB), up to 3 CTAs per SM
     launch2<float, kPassMinB32>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total, remote);
   else
