@@ -1478,6 +1478,7 @@ class simulation {
       const int mode = opt_.fused | (temporal() ? 16 : 0);
       if (!loop_exec_ || loop_mode_ != mode) build_loop_graph(mode);
       SF_CK(cudaGraphLaunch(loop_exec_, st_));
+      enqueue_redo_after_loop();
       ctl(CTL_PUBLISH);
       sync();
       const int sweeps = hflag_->sweeps;
@@ -1512,6 +1513,7 @@ class simulation {
       if (!more) break;
       cur ^= 1;
     }
+    enqueue_redo_after_loop();
     sync();
     const int sweeps = hflag_->sweeps;
     const double residual = hflag_->residual;
@@ -2943,6 +2945,7 @@ class simulation {
       launch_sweep2(tview(ws), ws.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_, 0,
                     nullptr, cfd_es_);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
+      ++launches_;
     } else {
       // Processor faces: the pass reads 2-deep halos of vx, vy, vz, divu (p
       // only on owned cells). The exchange of the state the previous unit
@@ -3025,15 +3028,25 @@ class simulation {
     if (!fin) {
       allreduce_max(&dctl_->acc[0], 2);
       ctl(CTL_FINISH_PASS, 0.0, 0, 0, 0, 1);
+      enqueue_redo();
     }
-    // predicated redo of the first sweep when the pass stopped after it
+    // (one process: the redo, if any, runs once after the loop -- a pass that
+    // stops after its first sweep also ends the loop, and every later unit is
+    // predicated off without touching the fields or ctl->redo)
+    check_launch();
+    return 2;
+  }
+  // predicated redo of a temporal pass's first sweep when the pass stopped
+  // after it (ctl->redo): k_sweep_div_tma on the pass's input
+  void enqueue_redo() {
     int ftx, fty;
     sweep_tile_shape(&ftx, &fty);
     const work_set& wr = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_fused_, ftx, fty);
     launch_sweep_div_tma(tview(wr), wr.nctas, zc_fused_, consts_, dctl_, loop_flag(), maps_, 2, st_, cfd_es_);
-    launches_ += 2;
-    check_launch();
-    return 2;
+    ++launches_;
+  }
+  void enqueue_redo_after_loop() {
+    if (temporal() && !dist_) enqueue_redo();
   }
 
   void enqueue_half_sweep() {

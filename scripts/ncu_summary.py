@@ -103,6 +103,9 @@ def main():
     ap.add_argument("--json")
     ap.add_argument("--algo-bytes", type=float, default=None)
     ap.add_argument("--note", default="")
+    ap.add_argument("--sum-launches", action="store_true",
+                    help="the captured launches together form one unit (e.g. the launches of one pass): "
+                         "the JSON traffic is their sum")
     a = ap.parse_args()
     L = raw(a.rep)
     md = [f"# ncu summary: {a.name}", "", f"source: `{os.path.basename(a.rep)}` (`ncu --set full --clock-control none`), {len(L)} profiled launch(es)", ""]
@@ -149,7 +152,11 @@ def main():
         f.write("\n".join(md))
     if a.json:
         first = js["launches"][0] if js["launches"] else {}
-        js["dram_bytes_per_launch"] = first.get("dram_bytes_per_launch")
+        if a.sum_launches:
+            js["dram_bytes_per_launch"] = sum(r.get("dram_bytes_per_launch") or 0.0 for r in js["launches"])
+            js["note"] = a.note or "traffic = the sum over the captured launches (one unit)"
+        else:
+            js["dram_bytes_per_launch"] = first.get("dram_bytes_per_launch")
         js["algo_bytes_per_launch"] = a.algo_bytes
         # provenance: bench.py flags the traffic as stale once the kernel source changes
         js["kernel_source_sha"] = kernel_source_sha()
