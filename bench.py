@@ -98,10 +98,12 @@ def kernel_source_sha() -> str:
     return h.hexdigest()[:16]
 
 
-def ncu_traffic(kernel="sweep_div"):
+def ncu_traffic(kernel="sweep_div", algo_bytes=None):
     """DRAM bytes per launch of the dominant kernel from its committed ncu
     capture (profiles/ncu_<kernel>.json), with the capture's provenance: the
-    traffic is marked stale when the kernel sources changed since."""
+    traffic is marked stale when the kernel sources changed since, and is not
+    reported for another workload (the capture's algorithmic bytes per launch
+    differ from this run's)."""
     p = os.path.join(ROOT, "profiles", f"ncu_{kernel}.json")
     try:
         with open(p) as f:
@@ -109,6 +111,11 @@ def ncu_traffic(kernel="sweep_div"):
         sha = d.get("kernel_source_sha")
         src = {"file": os.path.relpath(p, ROOT), "captured_from": d.get("captured_from"),
                "kernel_source_sha": sha, "stale": sha != kernel_source_sha()}
+        cap = d.get("algo_bytes_per_launch")
+        if algo_bytes is not None and cap is not None and int(cap) != int(algo_bytes):
+            src["not_applicable"] = "captured on a workload of %d algorithmic bytes per launch, this run has %d" % (
+                int(cap), int(algo_bytes))
+            return None, src
         return d.get("dram_bytes_per_launch"), src
     except Exception:
         return None, None
@@ -393,14 +400,15 @@ def run_ours(args):
     es = 4 if args.dtype == "f32" else 8
     algo_launch = BYTES_PER_HALF_SWEEP * es // 8 * units * cells
     achieved = (algo_launch / avg_launch_s / 1e9) if avg_launch_s else None
-    traffic, traffic_src = ncu_traffic(kname) if es == 8 else (None, None)
+    traffic, traffic_src = ncu_traffic(kname, algo_launch)
     step_bytes = (BYTES_UV + BYTES_DIV + BYTES_PER_HALF_SWEEP * sweeps_done / args.steps) * es / 8 * cells
     if small:  # the whole step stands in for the kernel (L2-resident, launch/latency-bound regime)
         achieved = step_bytes / (ms_per_step / 1e3) / 1e9
     roofline = {
         "bound": "hbm",
-        "kernel": ("temporal pass, two fused half-sweeps per pass (one walled fp64 component: k_sweep2i over the "
-                   "interior tiles beside k_sweep2 over the boundary slabs, concurrent; else k_sweep2)" if kname == "sweep2"
+        "kernel": ("temporal pass, two fused half-sweeps per pass (one walled component in one process: k_sweep2i "
+                   "over the interior tiles beside k_sweep2 over the z / y slabs and its x-slab form over the x "
+                   "slabs, concurrent; else k_sweep2)" if kname == "sweep2"
                    else "whole step: persistent pressure loop k_pressure_loop (grid L2-resident; achieved = "
                         "step algorithmic bytes / step time)" if small
                    else "k_sweep_div (fused half-sweep)"),
@@ -487,7 +495,7 @@ def run_ours(args):
                                 f"{args.steps} steps from rest" if c0 else
                                 f"3D lid-driven cavity {args.strong}^3 fp64 global grid, strong scaling over {world} B200 (BASELINE.json configs[3]), {S} half-sweeps per step"
                                 if args.strong else
-                                f"3D lid-driven cavity {n}^3 fp64, {S} pressure half-sweeps per step (BASELINE.json configs[1]; runs/bench128.cfg fixed-work pattern)"
+                                f"3D lid-driven cavity {n}^3 {'fp64' if es == 8 else 'fp32'}, {S} pressure half-sweeps per step (BASELINE.json configs[1]{'' if es == 8 else '-shaped'}; runs/bench128.cfg fixed-work pattern)"
                                 if world == 1 else
                                 f"3D lid-driven cavity, {n}^3 per GPU weak scaling, global {list(cfg.extents)} block-decomposed over {world} B200 with NCCL ghost exchange (BASELINE.json configs[2]), {S} half-sweeps per step"),
                    "grid": list(cfg.extents), "ghost": ghost, "sweeps_per_step": S,
@@ -496,7 +504,7 @@ def run_ours(args):
                             else "fused half-sweep, TMA pipeline",
                             "tma1": "fused half-sweep, TMA pipeline", "ldg": "fused half-sweep, plain loads",
                             "unfused": "unfused (reference dataflow)"}[args.variant],
-                   "l2": "inputs larger than L2: 9 resident fp64 arrays of %.2f GB" % (cells * 8 / 1e9)},
+                   "l2": "inputs larger than L2: 9 resident %s arrays of %.2f GB" % (args.dtype, cells * es / 1e9)},
         "half_sweep_rate": round(total_cells * sweeps_done / (ms_total / 1e3) / 1e6, 1),
         "parity": parity,
         "roofline": roofline,
