@@ -321,7 +321,9 @@ int64_t sf_sim_launch_count(sf_sim* s, int reset);
 /* Per-kernel CUDA-event timing of the pressure loop: when enabled, the driver
  * records events around every executed launch of the fused half-sweep
  * (kernel "sweep_div") or of the temporal pass (kernel "sweep2", two
- * half-sweeps per launch); read back the summed milliseconds and launches. */
+ * half-sweeps per launch); read back the summed milliseconds and launches.
+ * "sweep2i" counts the passes among them that ran on the interior form
+ * (k_sweep2i beside the slab launches; milliseconds 0). */
 int sf_sim_set_kernel_timing(sf_sim* s, int enable);
 int sf_sim_kernel_timing(sf_sim* s, const char* kernel, double* total_ms, int64_t* launches);
 

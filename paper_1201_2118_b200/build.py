@@ -6,15 +6,20 @@ every fp64 expression unfused so results are bitwise those of the reference.
 """
 from __future__ import annotations
 
+import fcntl
+import hashlib
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libsfb200.so")
+STAMP = LIB + ".sha"  # hash of the sources the library was built from
 SOURCES = ["sf_kernels.cu", "sf_sweep_tma.cu", "sf_sweep2.cu", "sf_uv_tma.cu", "sf_driver.cu"]
 HEADERS = ["sf_uv.cuh", "sf_device.cuh", "sf_kernels.cuh", "sf_plan.hpp", "sf_jit.hpp"]
 
@@ -36,41 +41,67 @@ def _nvcc() -> str:
     return "nvcc"
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
+def source_hash() -> str:
+    """Hash of everything the library is built from (sources, headers, the C
+    ABI header, this recipe). Content, not modification times: a snapshot of
+    the tree copied to another machine keeps its prebuilt library valid."""
+    h = hashlib.sha256()
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
-    deps.append(os.path.join(ROOT, "include", "sforge_b200.h"))
-    deps.append(os.path.abspath(__file__))
-    return any(os.path.getmtime(d) > t for d in deps)
+    deps += [os.path.join(ROOT, "include", "sforge_b200.h"), os.path.abspath(__file__)]
+    for d in deps:
+        with open(d, "rb") as f:
+            h.update(os.path.basename(d).encode() + b"\0" + f.read())
+    return h.hexdigest()
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+        return True
+    with open(STAMP) as f:
+        return f.read().strip() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Build under an exclusive file lock (several processes -- e.g. the ranks
+    of a torchrun job -- may find the library stale at once): objects go to a
+    private directory, the library and its stamp are replaced atomically."""
     if not force and not _stale():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
-    objs = []
-    log = []
-    for s in SOURCES:
-        obj = os.path.join(OUT_DIR, s.replace(".cu", ".o"))
-        cmd = [_nvcc(), *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), "-c",
-               os.path.join(CSRC, s), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError("nvcc failed for %s:\n%s" % (s, r.stdout + r.stderr))
-        objs.append(obj)
-    tmp = LIB + ".tmp"
-    cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xlinker", "--no-undefined", "-o", tmp, *objs, "-ldl"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError("nvcc link failed:\n%s" % (r.stdout + r.stderr))
-    os.replace(tmp, LIB)
-    with open(os.path.join(OUT_DIR, "ptxas.log"), "w") as f:
-        f.write("\n".join(log))
-    if verbose:
-        print("\n".join(log))
+    with open(os.path.join(OUT_DIR, ".build.lock"), "w") as lockf:
+        fcntl.flock(lockf, fcntl.LOCK_EX)
+        if not force and not _stale():  # another process built it meanwhile
+            return LIB
+        want = source_hash()
+        work = tempfile.mkdtemp(prefix=".build-", dir=OUT_DIR)
+        try:
+            objs = []
+            log = []
+            for s in SOURCES:
+                obj = os.path.join(work, s.replace(".cu", ".o"))
+                cmd = [_nvcc(), *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), "-c",
+                       os.path.join(CSRC, s), "-o", obj]
+                r = subprocess.run(cmd, capture_output=True, text=True)
+                log.append(r.stdout + r.stderr)
+                if r.returncode != 0:
+                    raise RuntimeError("nvcc failed for %s:\n%s" % (s, r.stdout + r.stderr))
+                objs.append(obj)
+            tmp = os.path.join(work, "libsfb200.so")
+            cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xlinker", "--no-undefined",
+                   "-o", tmp, *objs, "-ldl"]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError("nvcc link failed:\n%s" % (r.stdout + r.stderr))
+            os.replace(tmp, LIB)
+            with open(os.path.join(work, "stamp"), "w") as f:
+                f.write(want + "\n")
+            os.replace(os.path.join(work, "stamp"), STAMP)
+            with open(os.path.join(OUT_DIR, "ptxas.log"), "w") as f:
+                f.write("\n".join(log))
+            if verbose:
+                print("\n".join(log))
+        finally:
+            shutil.rmtree(work, ignore_errors=True)
     return LIB
 
 

@@ -1527,6 +1527,7 @@ class simulation {
         SF_CK(cudaEventElapsedTime(&ms, timer(q, 0), timer(q, 1)));
         (two ? pass_ms_ : sweep_ms_) += ms;
         ++(two ? pass_launches_ : sweep_launches_);
+        if (two && q < (int)unit_form_.size() && unit_form_[q]) ++interior_passes_;
       }
     }
     (void)residual;
@@ -1687,12 +1688,14 @@ class simulation {
   void set_timing(bool on) {
     timing_ = on;
     sweep_ms_ = pass_ms_ = 0.0;
-    sweep_launches_ = pass_launches_ = 0;
+    sweep_launches_ = pass_launches_ = interior_passes_ = 0;
   }
   // which = 0: single half-sweep kernel; 1: temporal pass (two half-sweeps)
+  // which: 0 single half-sweeps, 1 temporal passes, 2 the passes among them
+  // that ran on the interior form (k_sweep2i beside the slabs; count only)
   void timing(int which, double* ms, i64* n) const {
-    *ms = which ? pass_ms_ : sweep_ms_;
-    *n = which ? pass_launches_ : sweep_launches_;
+    *ms = which == 1 ? pass_ms_ : which == 0 ? sweep_ms_ : 0.0;
+    *n = which == 1 ? pass_launches_ : which == 0 ? sweep_launches_ : interior_passes_;
   }
 
  private:
@@ -1810,7 +1813,13 @@ class simulation {
   i64 launches_ = 0;
   bool timing_ = false;
   double sweep_ms_ = 0.0, pass_ms_ = 0.0;
-  i64 sweep_launches_ = 0, pass_launches_ = 0;
+  i64 sweep_launches_ = 0, pass_launches_ = 0, interior_passes_ = 0;
+  std::vector<char> unit_form_;  // (timing) per timed unit: 1 = the interior form ran
+  void mark_form(int q, char f) {
+    if (!timing_) return;
+    if ((int)unit_form_.size() <= q) unit_form_.resize((size_t)q + 1, 0);
+    unit_form_[(size_t)q] = f;
+  }
   std::vector<cudaEvent_t> timers_;
   int iter_launch_ = 0;
   cudaEvent_t timer(int q, int which) {
@@ -2419,8 +2428,11 @@ class simulation {
     const work_set* slab = nullptr;  // z and y slabs (k_sweep2, 32 x sweep2_tile_y tiles)
     const work_set* xs = nullptr;    // x slabs (k_sweep2, x-slab form)
   };
-  isplit interior_split() {
-    if (!maps3_ || !maps4_ || !interior_env_ || nloc_ != 1 || dist_ || !temporal() || has_proc_faces()) return {};
+  // proc: the caller stores the slabs' processor-face layers into the peers
+  // (the fused exchange, k_sweep2's REMOTE instantiation)
+  isplit interior_split(bool proc = false) {
+    if (!maps3_ || !maps4_ || !interior_env_ || nloc_ != 1 || !temporal()) return {};
+    if ((dist_ || has_proc_faces()) && !proc) return {};
     if (cfg_.periodic[0] || cfg_.periodic[1] || cfg_.periodic[2]) return {};
     if (!xs_) {
       SF_CK(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
@@ -2496,7 +2508,7 @@ class simulation {
     items_.emplace(std::string(key) + ":i", mk(vi, ci));
     items_.emplace(std::string(key) + ":b", mk(vb, cb));
     items_.emplace(std::string(key) + ":x", mk(vx, cx));
-    return interior_split();
+    return interior_split(proc);
   }
 
   // max over ranks of n accumulators (IEEE bit patterns of |x|): order-free,
@@ -2923,6 +2935,7 @@ class simulation {
       const work_set& wb = *split.slab;
       const work_set& wx = *split.xs;
       const unsigned total = (unsigned)(wi.nctas + wb.nctas + wx.nctas);
+      mark_form(iter_launch_, 1);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
       // boundary slabs first on the second stream, the interior beside them
       // (measured with 32x20 interior tiles: concurrent 2.27 ms, interior
@@ -2941,6 +2954,7 @@ class simulation {
       launches_ += (wi.nctas > 0) + (wb.nctas > 0) + (wx.nctas > 0);
     } else if (!has_proc_faces()) {
       const work_set& ws = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass(), kTX, sweep2_tile_y());
+      mark_form(iter_launch_, 0);
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
       launch_sweep2(tview(ws), ws.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_, 0,
                     nullptr, cfd_es_);
@@ -2984,9 +2998,32 @@ class simulation {
         // (predicated like the pass), then the max-allreduce below
         const work_set& wa = items_for(SF_REGION_ALL, {0, 0, 0, 0, 0, 0}, zc_pass(), kTX, sweep2_tile_y());
         const bool fused_x = direct_mode_ == 1 && remote_;
+        const auto ps = fused_x ? interior_split(true) : isplit{};
+        mark_form(iter_launch_, ps.in ? 1 : 0);
         if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 0), st_));
-        launch_sweep2(tview(wa), wa.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_, 0,
-                      fused_x ? remote_ : nullptr, cfd_es_);
+        if (ps.in) {
+          // the interior tiles on the interior form; the slabs (which hold
+          // every layer next to a processor face) on k_sweep2's REMOTE
+          // instantiation on the second stream, storing into the peers
+          const work_set& wi = *ps.in;
+          const work_set& wb = *ps.slab;
+          const work_set& wx = *ps.xs;
+          const unsigned total = (unsigned)(wi.nctas + wb.nctas + wx.nctas);
+          SF_CK(cudaEventRecord(ev_fork_, st_));
+          SF_CK(cudaStreamWaitEvent(xs_, ev_fork_, 0));
+          launch_sweep2(tview(wb), wb.nctas, ibzc_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), xs_, total,
+                        remote_, cfd_es_);
+          launch_sweep2(tview(wx), wx.nctas, ibzc_, consts_, dctl_, loop_flag(), maps4_, fin, wall_pins(), xs_, total,
+                        remote_, cfd_es_, 1);
+          launch_sweep2i(tview(wi), wi.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps3_, fin, st_, total,
+                         cfd_es_);
+          SF_CK(cudaEventRecord(ev_join_, xs_));
+          SF_CK(cudaStreamWaitEvent(st_, ev_join_, 0));
+          launches_ += (wi.nctas > 0) + (wb.nctas > 0) + (wx.nctas > 0) - 1;
+        } else {
+          launch_sweep2(tview(wa), wa.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_, 0,
+                        fused_x ? remote_ : nullptr, cfd_es_);
+        }
         if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
         if (!fused_x) {
           launch_tasks(tview(), direct_tasks_.d, direct_tasks_.n, direct_tasks_.max_count, dctl_, st_, 296);
@@ -3668,11 +3705,11 @@ int sf_sim_set_kernel_timing(sf_sim* s, int enable) {
 int sf_sim_kernel_timing(sf_sim* s, const char* kernel, double* total_ms, int64_t* launches) {
   return guarded([&] {
     const std::string k = kernel ? kernel : "";
-    if (k != "sweep_div" && k != "sweep2")
-      throw sfb::error(SF_ERR_ARG, "timed kernels: sweep_div, sweep2");
+    if (k != "sweep_div" && k != "sweep2" && k != "sweep2i")
+      throw sfb::error(SF_ERR_ARG, "timed kernels: sweep_div, sweep2, sweep2i");
     double ms = 0.0;
     long long n = 0;
-    SIM(s).timing(k == "sweep2" ? 1 : 0, &ms, &n);
+    SIM(s).timing(k == "sweep2" ? 1 : k == "sweep2i" ? 2 : 0, &ms, &n);
     *total_ms = ms;
     *launches = n;
   });

@@ -1111,11 +1111,11 @@ void launch_sweep2(const table_view& vw, int nctas, int zc, const sf_consts& c, 
                    sf_host_flag* hflag, const void* maps, int fin, const sweep2_pins& pins, cudaStream_t st,
                    unsigned total, const sweep2_remote* remote, int es, int shape) {
   if (nctas <= 0) return;
-  if (shape) {  // the x-slab form (no periodic axis, no fused exchange: the interior split)
+  if (shape) {  // the x-slab form (the interior split: no periodic axis)
     if (es == 4)
-      launch2<float, kPassMinB32, kSlabTX, kSlabTY>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total, nullptr);
+      launch2<float, kPassMinB32, kSlabTX, kSlabTY>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total, remote);
     else
-      launch2<double, kPassMinB, kSlabTX, kSlabTY>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total, nullptr);
+      launch2<double, kPassMinB, kSlabTX, kSlabTY>(vw, nctas, zc, c, ctl, hflag, maps, fin, pins, st, total, remote);
     return;
   }
   if (es == 4)  // fp32: half the shared memory per CTA (56 KB), up to 3 CTAs per SM

@@ -62,6 +62,7 @@ def main():
         sim = sfb.Simulation(cfg, sfb.cavity_fluid(cfg), ghost=a.ghost, device=dev, fused=fused, rank=rank,
                              world=world, transport="ipc")
         sim.set_direct_exchange(direct)
+        print(f"rank {rank}: variant {name}", flush=True)
         sim.init_cavity()
         sim.set_kernel_timing(True)
         stats = [sim.step() for _ in range(a.steps)]
@@ -69,6 +70,7 @@ def main():
         used_direct = sim.direct_exchange if fused == 1 else 0
         results[name] = {"stats": [[s.dt, s.sweeps, s.residual] for s in stats], "checksum": csum,
                          "passes": sim.kernel_timing("sweep2")[1], "half_sweeps": sim.kernel_timing("sweep_div")[1],
+                         "interior": sim.kernel_timing("sweep2i")[1],
                          "direct": used_direct, "block": list(sim.block_shape())}
         dist.barrier()
         sim.close()

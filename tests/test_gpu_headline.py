@@ -88,6 +88,7 @@ def test_temporal_pass_z_chunks_match_the_reference(ref_available, zc, ext, max_
     want = [[float(a), int(b), float(r)] for a, b, r in zip(*so)]
     assert [[x.dt, x.sweeps, x.residual] for x in dd] == want
     assert d.kernel_timing("sweep2")[1] == 2 * ((max_sweeps + 1) // 2)
+    assert d.kernel_timing("sweep2i")[1] == d.kernel_timing("sweep2")[1]  # every pass on the interior form
     assert d.checksum() == o.checksum()
     # divu too: the interior form recomputes it instead of storing it, and
     # the driver restores the field after the loop (and before a redo)

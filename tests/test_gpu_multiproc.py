@@ -53,6 +53,10 @@ def test_ranks_in_separate_processes_match_the_reference(ref_available, world, e
         assert v["ok"], (name, v, res["reference"])
     v = res["variants"]
     assert v["temporal-direct-fused"]["direct"] == 1 and v["temporal-direct-fused"]["passes"] > 0
+    # with the exchange fused into the slabs' stores, every pass runs the
+    # interior form (k_sweep2i) beside the REMOTE slab launches
+    assert v["temporal-direct-fused"]["interior"] == v["temporal-direct-fused"]["passes"]
+    assert v["temporal-phases-overlapped"]["interior"] == 0
     assert v["temporal-direct-launch"]["direct"] == 2 and v["temporal-direct-launch"]["passes"] > 0
     assert v["temporal-phases-overlapped"]["direct"] == 0 and v["temporal-phases-overlapped"]["passes"] > 0
     assert v["single-half-sweep"]["passes"] == 0 and v["single-half-sweep"]["half_sweeps"] > 0
