@@ -92,7 +92,8 @@ def run_bc(rng):
     velocities: the fused, TMA and temporal paths against the unfused
     reference dataflow (fused=0, itself bitwise with the reference), since the
     reference's simulation fixes its own boundary spec."""
-    ext = tuple(int(rng.integers(6, 44)) for _ in range(3))
+    top = int(os.environ.get("PS_BCMAX", "44"))  # larger grids reach the interior form of the pass
+    ext = tuple(int(rng.integers(6, top)) for _ in range(3))
     workers = int(rng.choice([1, 1, 2, 3]))
     ghost = int(rng.choice([1, 2]))
     kinds = ["wall", "symmetry", "outflow"]
