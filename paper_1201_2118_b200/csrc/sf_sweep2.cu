@@ -251,8 +251,19 @@ __global__ void __launch_bounds__(TXV * TYV, MINB)
   __syncthreads();
 
   // ---- S0 input ring ---------------------------------------------------------
+  // The x-slab form next to a physical x face: the S0 boxes start (end) on
+  // the face's cache line instead of XA cells beyond it. The ghost columns
+  // there never reach a result: the -x ghost's normal u is the pin and its
+  // divergence only feeds the -x term a low-wall cell discards; the +x ghost's
+  // divergence is the mirror of N-1 and the high-wall cell's u the pin. So
+  // their box elements are clamped into the row (any value), and a 16-wide
+  // slab row touches 2 lines of 128 B instead of 3 (fp32: 1 instead of 2).
+  const int xsh = (TXV != kSlabTX || PER) ? 0
+                  : (i0 == 0 && B.face[0] != FACE_PROC) ? G::XA
+                  : (i0 + TX >= n0 && B.face[1] != FACE_PROC) ? -G::XA
+                  : 0;
   const int xo = (int)(B.base % B.sx), g = B.g;
-  const int xs = xo + i0 - 2 - XSH, ys = g + j0 - 2, zs = g + k0 - 2;
+  const int xs = xo + i0 - 2 - XSH + xsh, ys = g + j0 - 2, zs = g + k0 - 2;
   const CUtensorMap* mD = &maps->m[b][SF_DIVU][tab->bidx[b][SF_DIVU][FRONT]];
   const CUtensorMap* mU = &maps->m[b][SF_VX][tab->bidx[b][SF_VX][FRONT]];
   const CUtensorMap* mV = &maps->m[b][SF_VY][tab->bidx[b][SF_VY][FRONT]];
@@ -309,7 +320,8 @@ __global__ void __launch_bounds__(TXV * TYV, MINB)
       const int bx = bin(s.per[0], gi, nm0), bxp = bnx(s.per[0], gi, nm0);
       const int by = bin(s.per[1], gj, nm1), byp = bnx(s.per[1], gj, nm1);
       f_e[r] = e;
-      f_ia[r] = ey * IW + ex + XSH;
+      const int ix = ex + XSH - xsh;
+      f_ia[r] = ey * IW + (ix < 0 ? 0 : ix > IW - 1 ? IW - 1 : ix);
       f_bt[r] = ((bx << 2) | (by << 1)) | (((bxp << 2) | (by << 1)) << 3) | (((bx << 2) | (byp << 1)) << 6) |
                 ((int)((wrp((int)gi, N0, per0) + wrp((int)gj, N1, per1)) & 1) << 9) |
                 (((per0 || (gi >= 0 && gi < N0)) && (per1 || (gj >= 0 && gj < N1))) << 10) |
