@@ -388,11 +388,6 @@ class simulation {
     if (xs_) {
       cudaStreamSynchronize(xs_);
       cudaStreamDestroy(xs_);
-      if (xs2_) {
-        cudaStreamSynchronize(xs2_);
-        cudaStreamDestroy(xs2_);
-      }
-      if (ev_join2_) cudaEventDestroy(ev_join2_);
       cudaEventDestroy(ev_fork_);
       cudaEventDestroy(ev_join_);
     }
@@ -1779,12 +1774,9 @@ class simulation {
   void* maps3_ = nullptr;  // descriptors of the interior form of the pass (sweep2i_box shapes)
   void* maps4_ = nullptr;  // descriptors of the pass's x-slab form (sweep2_box shape 1)
   int ibzc_ = 32;          // z chunk of the boundary slabs beside the interior form
-  int izc_ = 128;          // z chunk of the interior form
   const bool interior_env_ = getenv("SF_NO_INTERIOR_PASS") == nullptr;
   void* uvmaps_ = nullptr;  // TMA UPDATE_VELOCITY descriptors (null: plain-load kernel)
   cudaStream_t xs_ = nullptr;  // halo exchange overlapped with the temporal pass
-  cudaStream_t xs2_ = nullptr;  // (interior split) the x slabs beside the z / y slabs
-  cudaEvent_t ev_join2_ = nullptr;
   const bool overlap_env_ = getenv("SF_NO_OVERLAP") == nullptr;
   const bool force_overlap_ = getenv("SF_OVERLAP") != nullptr;  // also on one device (tests)
   work_set empty_ws_{};
@@ -2447,10 +2439,6 @@ class simulation {
       SF_CK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
       SF_CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     }
-    if (!xs2_) {
-      SF_CK(cudaStreamCreateWithFlags(&xs2_, cudaStreamNonBlocking));
-      SF_CK(cudaEventCreateWithFlags(&ev_join2_, cudaEventDisableTiming));
-    }
     int stx, sty;
     sweep2_tile(1, &stx, &sty);
     const int ty = sweep2_tile_y(), tyi = sweep2i_tile_y(cfd_es_), zc = zc_pass();
@@ -2459,6 +2447,14 @@ class simulation {
     // 2.31 / 2.27 / 2.27 ms)
     const int bzc = std::min(zc, 32);
     ibzc_ = bzc;
+    char key[64];
+    std::snprintf(key, sizeof key, "isplit:%d:%d:%d:%d", zc, ty, tyi, bzc);
+    auto ii = items_.find(std::string(key) + ":i");
+    if (ii != items_.end()) {
+      if (!ii->second.nctas) return {};
+      return {&ii->second, &items_.find(std::string(key) + ":b")->second,
+              &items_.find(std::string(key) + ":x")->second};
+    }
     const auto n = dec_.dims(gid_[0]);
     // interior tiles: i0 = ox + 32 a <= N - 35, j0 = oy + tyi b <= N - tyi - 3.
     // ox = 16 keeps the tiles' rows 128-byte aligned and leaves x slabs one
@@ -2467,21 +2463,6 @@ class simulation {
     const i64 qx = n[0] >= ox + kTX + 3 ? (n[0] - 3 - kTX - ox) / kTX + 1 : 0;
     const i64 qy = n[1] >= oy + tyi + 3 ? (n[1] - 3 - tyi - oy) / tyi + 1 : 0;
     const i64 ilo[3] = {ox, oy, 3}, ihi[3] = {ox + kTX * qx, oy + tyi * qy, n[2] - 3};
-    // the interior's z chunk: whole columns when they make 2-4 waves of one
-    // CTA per SM (512^3: 375 columns; neighbouring tiles then march their
-    // columns in step, sharing halo rows in L2), else the pass's chunk.
-    // Measured per pass at 512^3: 128 planes 2.220 ms, 171 2.210, 256 2.188,
-    // 506 2.175; at 1024^3 (1550 columns): 128 16.26, 256 16.60, 512 16.77.
-    const i64 cols = qx * qy;
-    izc_ = (cols >= 2 * (i64)sms_ && cols <= 4 * (i64)sms_ && ihi[2] > ilo[2]) ? (int)(ihi[2] - ilo[2]) : zc;
-    char key[64];
-    std::snprintf(key, sizeof key, "isplit:%d:%d:%d:%d:%d", zc, ty, tyi, bzc, izc_);
-    auto ii = items_.find(std::string(key) + ":i");
-    if (ii != items_.end()) {
-      if (!ii->second.nctas) return {};
-      return {&ii->second, &items_.find(std::string(key) + ":b")->second,
-              &items_.find(std::string(key) + ":x")->second};
-    }
     std::vector<sf_work> vi, vb, vx;
     int ci = 0, cb = 0, cx = 0;
     auto add = [&](std::vector<sf_work>& v, int& cta, const i64 lo[3], const i64 hi[3], int zcb, int txb, int tyb) {
@@ -2500,7 +2481,7 @@ class simulation {
       v.push_back(w);
     };
     if (qx > 0 && qy > 0 && ihi[2] > ilo[2]) {
-      add(vi, ci, ilo, ihi, izc_, kTX, tyi);
+      add(vi, ci, ilo, ihi, zc, kTX, tyi);
       const i64 z0[3] = {0, 0, 0}, zl[3] = {n[0], n[1], ilo[2]};
       const i64 z1[3] = {0, 0, ihi[2]}, zh[3] = {n[0], n[1], n[2]};
       add(vb, cb, z0, zl, bzc, kTX, ty);
@@ -2962,18 +2943,13 @@ class simulation {
       // 16 / 32 / 64 planes 2.31 / 2.27 / 2.27)
       SF_CK(cudaEventRecord(ev_fork_, st_));
       SF_CK(cudaStreamWaitEvent(xs_, ev_fork_, 0));
-      // the x slabs on a third stream beside the z / y slabs (2.243 vs 2.229 ms
-      // per pass against one slab stream)
-      SF_CK(cudaStreamWaitEvent(xs2_, ev_fork_, 0));
       launch_sweep2(tview(wb), wb.nctas, ibzc_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), xs_, total,
                     nullptr, cfd_es_);
-      launch_sweep2(tview(wx), wx.nctas, ibzc_, consts_, dctl_, loop_flag(), maps4_, fin, wall_pins(), xs2_, total,
+      launch_sweep2(tview(wx), wx.nctas, ibzc_, consts_, dctl_, loop_flag(), maps4_, fin, wall_pins(), xs_, total,
                     nullptr, cfd_es_, 1);
-      launch_sweep2i(tview(wi), wi.nctas, izc_, consts_, dctl_, loop_flag(), maps3_, fin, st_, total, cfd_es_);
+      launch_sweep2i(tview(wi), wi.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps3_, fin, st_, total, cfd_es_);
       SF_CK(cudaEventRecord(ev_join_, xs_));
       SF_CK(cudaStreamWaitEvent(st_, ev_join_, 0));
-      SF_CK(cudaEventRecord(ev_join2_, xs2_));
-      SF_CK(cudaStreamWaitEvent(st_, ev_join2_, 0));
       if (timing_) SF_CK(cudaEventRecord(timer(iter_launch_, 1), st_));
       launches_ += (wi.nctas > 0) + (wb.nctas > 0) + (wx.nctas > 0);
     } else if (!has_proc_faces()) {
@@ -3035,17 +3011,14 @@ class simulation {
           const unsigned total = (unsigned)(wi.nctas + wb.nctas + wx.nctas);
           SF_CK(cudaEventRecord(ev_fork_, st_));
           SF_CK(cudaStreamWaitEvent(xs_, ev_fork_, 0));
-          SF_CK(cudaStreamWaitEvent(xs2_, ev_fork_, 0));
           launch_sweep2(tview(wb), wb.nctas, ibzc_, consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), xs_, total,
                         remote_, cfd_es_);
-          launch_sweep2(tview(wx), wx.nctas, ibzc_, consts_, dctl_, loop_flag(), maps4_, fin, wall_pins(), xs2_,
-                        total, remote_, cfd_es_, 1);
-          launch_sweep2i(tview(wi), wi.nctas, izc_, consts_, dctl_, loop_flag(), maps3_, fin, st_, total,
+          launch_sweep2(tview(wx), wx.nctas, ibzc_, consts_, dctl_, loop_flag(), maps4_, fin, wall_pins(), xs_, total,
+                        remote_, cfd_es_, 1);
+          launch_sweep2i(tview(wi), wi.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps3_, fin, st_, total,
                          cfd_es_);
           SF_CK(cudaEventRecord(ev_join_, xs_));
           SF_CK(cudaStreamWaitEvent(st_, ev_join_, 0));
-          SF_CK(cudaEventRecord(ev_join2_, xs2_));
-          SF_CK(cudaStreamWaitEvent(st_, ev_join2_, 0));
           launches_ += (wi.nctas > 0) + (wb.nctas > 0) + (wx.nctas > 0) - 1;
         } else {
           launch_sweep2(tview(wa), wa.nctas, zc_pass(), consts_, dctl_, loop_flag(), maps2_, fin, wall_pins(), st_, 0,
