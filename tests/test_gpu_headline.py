@@ -51,6 +51,7 @@ def test_bench_config_512_matches_the_reference_checksums(fused):
         # the temporal pass ran at the headline chunk: 4096 CTAs = 16 x 64 columns x 4 chunks
         if fused == 1:
             assert s.kernel_timing("sweep2")[1] == 200
+            assert s.kernel_timing("sweep2i")[1] == 200  # the interior form beside the slab launches
         else:
             assert s.kernel_timing("sweep_div")[1] == 400
     finally:
