@@ -172,3 +172,26 @@ def test_cpp_header_compiles_against_the_library(tmp_path):
     if sfb.lib().sf_device_count() == 0:
         out = subprocess.run([str(exe), "8", "1"], capture_output=True, text=True)
         assert out.returncode == 1 and "error:" in out.stdout
+
+
+def test_library_stamp_is_the_hash_of_its_sources():
+    # freshness by content, not file times: a copied tree keeps its prebuilt
+    # library, and concurrent importers see one consistent answer
+    from paper_1201_2118_b200 import build
+    assert os.path.exists(build.STAMP)
+    assert open(build.STAMP).read().strip() == build.source_hash()
+    assert not build._stale()
+
+
+def test_bench_reports_ncu_traffic_only_for_its_workload():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    import json
+    cap = json.load(open(os.path.join(ROOT, "profiles", "ncu_sweep2.json")))
+    t, src = bench.ncu_traffic("sweep2", cap["algo_bytes_per_launch"])
+    assert t == cap["dram_bytes_per_launch"] and src["captured_from"] == cap["captured_from"]
+    assert "not_applicable" not in src
+    t, src = bench.ncu_traffic("sweep2", 8 * cap["algo_bytes_per_launch"])  # e.g. the 1024^3 pass
+    assert t is None and "not_applicable" in src
