@@ -178,6 +178,7 @@ def test_library_stamp_is_the_hash_of_its_sources():
     # freshness by content, not file times: a copied tree keeps its prebuilt
     # library, and concurrent importers see one consistent answer
     from paper_1201_2118_b200 import build
+    sfb.lib()  # builds (and stamps) the library if it is missing or stale
     assert os.path.exists(build.STAMP)
     assert open(build.STAMP).read().strip() == build.source_hash()
     assert not build._stale()
